@@ -1,0 +1,180 @@
+/*
+ * oracle/api.c -- flat C entry points of liborc.so for the Python test
+ * harness (oracle/oracle.py, via ctypes).  TEST INFRASTRUCTURE ONLY.
+ */
+#include "orc.h"
+#include <stdlib.h>
+#include <string.h>
+
+orc_params *orc_params_new(int, int, const int *, int, const int *, int, const int *);
+void orc_params_free(orc_params *);
+orc_keys *orc_keygen(const orc_params *, u64, int, const int *, int, int);
+void orc_keys_free(orc_keys *);
+orc_ct *orc_encrypt_pk(const orc_params *, const orc_keys *, const u64 *, int, u64, u64);
+orc_ct *orc_encrypt_sk(const orc_params *, const orc_keys *, const u64 *, int, u64, u64);
+void orc_decrypt(const orc_params *, const orc_keys *, const orc_ct *, u64 *);
+double orc_encode_naive_coeff(const orc_params *, const double *, const double *, double, int);
+
+typedef orc_ct *(*orc_bts_fn)(const orc_params *, const orc_keys *, const orc_ct *, void *);
+typedef struct {
+    int n, m, k, variant;
+    const orc_cheb *exp_poly;
+    const orc_cheb *inv_poly;
+    orc_bts_fn bts;
+    void *bts_ctx;
+} orc_softmax_desc;
+int orc_softmax(const orc_params *, const orc_keys *, const orc_softmax_desc *, orc_ct *const *, orc_ct **);
+
+orc_params *orc_api_params(int log_n, int n_q, const int *q_bits, int n_p, const int *p_bits, int alpha,
+                           const int *log2_anchor)
+{
+    return orc_params_new(log_n, n_q, q_bits, n_p, p_bits, alpha, log2_anchor);
+}
+void orc_api_params_free(orc_params *P) { orc_params_free(P); }
+void orc_api_primes(const orc_params *P, u64 *out) { memcpy(out, P->prime, sizeof(u64) * (P->n_q + P->n_p)); }
+u64 orc_api_psi(const orc_params *P, int i) { return P->psi[i]; }
+double orc_api_scale(const orc_params *P, int l) { return P->scale[l]; }
+
+void orc_api_ntt(const orc_params *P, int pi, u64 *a, int inverse)
+{
+    if (inverse) orc_ntt_inv(P, pi, a);
+    else orc_ntt_fwd(P, pi, a);
+}
+void orc_api_ntt_naive(const orc_params *P, int pi, u64 *a) { orc_ntt_naive(P, pi, a); }
+void orc_api_galois_perm(const orc_params *P, int k, unsigned *perm) { orc_galois_perm(P, k, perm); }
+void orc_api_chacha20(const uint32_t *key, uint32_t counter, const uint32_t *nonce, uint32_t *out)
+{
+    orc_chacha20_block(key, counter, nonce, out);
+}
+u64 orc_api_stream(u64 seed, uint32_t tag, u64 sub, u64 idx) { return orc_stream(seed, tag, sub, idx); }
+u64 orc_api_residue(double x, u64 q) { return orc_residue_of_double(x, q); }
+int orc_api_galois_of_rot(const orc_params *P, int r) { return orc_galois_of_rot(P, r); }
+
+orc_keys *orc_api_keygen(const orc_params *P, u64 seed, int h, const int *galois, int n, int relin)
+{
+    return orc_keygen(P, seed, h, galois, n, relin);
+}
+void orc_api_keys_free(orc_keys *K) { orc_keys_free(K); }
+void orc_api_secret(const orc_params *P, const orc_keys *K, int64_t *out) { memcpy(out, K->s_coeff, sizeof(int64_t) * P->n); }
+void orc_api_pk(const orc_params *P, const orc_keys *K, u64 *out)
+{
+    memcpy(out, K->pk, sizeof(u64) * 2 * (size_t)P->n_q * P->n);
+}
+/* [dnum][2][n_q+n_p][N] */
+int orc_api_swk(const orc_params *P, const orc_keys *K, int galois, u64 *out)
+{
+    const orc_swk *k = orc_find_key(K, galois);
+    if (!k) return -1;
+    memcpy(out, k->k, sizeof(u64) * (size_t)P->dnum * 2 * (P->n_q + P->n_p) * P->n);
+    return 0;
+}
+
+void orc_api_encode(const orc_params *P, const double *re, const double *im, double scale, int level, u64 *out)
+{
+    orc_encode_coeffs(P, re, im, scale, level, out);
+}
+double orc_api_encode_naive(const orc_params *P, const double *re, const double *im, double scale, int t)
+{
+    return orc_encode_naive_coeff(P, re, im, scale, t);
+}
+
+/* decrypt and decode with the canonical scale of the ciphertext's level,
+ * from the q_0 residue (centred). */
+void orc_api_decrypt_decode(const orc_params *P, const orc_keys *K, const orc_ct *c, double *re, double *im)
+{
+    int N = P->n;
+    u64 *m = malloc(sizeof(u64) * (size_t)(c->level + 1) * N);
+    orc_decrypt(P, K, c, m);
+    i128 *co = malloc(sizeof(i128) * N);
+    u64 q0 = P->prime[0];
+    for (int t = 0; t < N; t++) co[t] = m[t] > q0 / 2 ? (i128)m[t] - (i128)q0 : (i128)m[t];
+    orc_decode_coeffs(P, co, P->scale[c->level], re, im);
+    free(co);
+    free(m);
+}
+void orc_api_decrypt(const orc_params *P, const orc_keys *K, const orc_ct *c, u64 *out) { orc_decrypt(P, K, c, out); }
+
+orc_ct *orc_api_encrypt(const orc_params *P, const orc_keys *K, const u64 *pt, int level, u64 seed, u64 idx, int use_sk)
+{
+    return use_sk ? orc_encrypt_sk(P, K, pt, level, seed, idx) : orc_encrypt_pk(P, K, pt, level, seed, idx);
+}
+
+orc_ct *orc_api_ct_import(const orc_params *P, int level, int ncomp, const u64 *w)
+{
+    orc_ct *c = orc_ct_alloc(P, level, ncomp);
+    memcpy(c->a, w, sizeof(u64) * (size_t)ncomp * (level + 1) * P->n);
+    return c;
+}
+void orc_api_ct_export(const orc_params *P, const orc_ct *c, u64 *w)
+{
+    memcpy(w, c->a, sizeof(u64) * (size_t)c->ncomp * (c->level + 1) * P->n);
+}
+int orc_api_ct_level(const orc_ct *c) { return c->level; }
+int orc_api_ct_ncomp(const orc_ct *c) { return c->ncomp; }
+void orc_api_ct_free(orc_ct *c) { orc_ct_release(c); }
+
+enum { OP_ADD, OP_SUB, OP_MULT, OP_TENSOR, OP_RELIN, OP_RESCALE, OP_LEVEL_DOWN, OP_MULT_CONST,
+       OP_ADD_CONST, OP_MULT_INT, OP_ROTATE, OP_CONJ, OP_GALOIS };
+
+orc_ct *orc_api_op(const orc_params *P, const orc_keys *K, int op, const orc_ct *a, const orc_ct *b, double c, int i)
+{
+    switch (op) {
+    case OP_ADD: return orc_op_add(P, a, b);
+    case OP_SUB: return orc_op_sub(P, a, b);
+    case OP_MULT: return orc_op_mult(P, K, a, b);
+    case OP_TENSOR: return orc_op_tensor(P, a, b);
+    case OP_RELIN: return orc_op_relin(P, K, a);
+    case OP_RESCALE: return orc_op_rescale(P, a);
+    case OP_LEVEL_DOWN: return orc_op_level_down(P, a, i);
+    case OP_MULT_CONST: return orc_op_mult_const(P, a, c, i);
+    case OP_ADD_CONST: return orc_op_add_const(P, a, c);
+    case OP_MULT_INT: return orc_op_mult_int(P, a, (int64_t)i);
+    case OP_ROTATE: return orc_op_rotate(P, K, a, i);
+    case OP_CONJ: return orc_op_conjugate(P, K, a);
+    case OP_GALOIS: return orc_op_galois(P, K, a, i);
+    }
+    return NULL;
+}
+
+orc_ct *orc_api_mult_pt(const orc_params *P, const orc_ct *a, const double *re, const double *im, int target)
+{
+    return orc_op_mult_pt(P, a, re, im, target);
+}
+
+int orc_api_keyswitch(const orc_params *P, const orc_keys *K, int galois, int level, const u64 *d, u64 *o0, u64 *o1)
+{
+    const orc_swk *k = orc_find_key(K, galois);
+    if (!k) return -1;
+    orc_keyswitch(P, k, level, d, o0, o1);
+    return 0;
+}
+
+orc_ct *orc_api_cheb(const orc_params *P, const orc_keys *K, const orc_ct *x, int deg, double a, double b, const double *c)
+{
+    orc_cheb p = {deg, a, b, c};
+    return orc_eval_cheb(P, K, x, &p);
+}
+int orc_api_cheb_depth(int deg) { return orc_cheb_depth(deg); }
+
+/* polys: n_poly = 1 + k entries (exp first), degs/as/bs arrays, coeffs concatenated */
+int orc_api_softmax(const orc_params *P, const orc_keys *K, int n, int m, int k, int variant,
+                    const int *degs, const double *as, const double *bs, const double *coeffs,
+                    orc_ct *const *in, orc_ct **out)
+{
+    orc_cheb *polys = malloc(sizeof(orc_cheb) * (k + 1));
+    const double *cp = coeffs;
+    for (int i = 0; i <= k; i++) {
+        polys[i].deg = degs[i];
+        polys[i].a = as[i];
+        polys[i].b = bs[i];
+        polys[i].c = cp;
+        cp += degs[i] + 1;
+    }
+    orc_softmax_desc d = {n, m, k, variant, &polys[0], &polys[1], NULL, NULL};
+    int rc = orc_softmax(P, K, &d, in, out);
+    free(polys);
+    return rc;
+}
+
+void orc_api_ledger(long *out) { memcpy(out, orc_ledger, sizeof(orc_ledger)); }
+void orc_api_ledger_reset(void) { memset(orc_ledger, 0, sizeof(orc_ledger)); }

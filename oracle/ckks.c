@@ -1,0 +1,613 @@
+/*
+ * oracle/ckks.c -- RNS-CKKS scheme operations of the oracle.
+ * TEST INFRASTRUCTURE ONLY (see orc.h).
+ *
+ * PAPER.md section 2.2.1 (lines 262-271) lists the functionalities: KeyGen,
+ * Enc, Dec, Add, Mult, Rot.  The paper delegates all of them to HEaaN
+ * (line 386), so each convention below is a DESIGN.md reading:
+ *   C5 randomness, C6 pk/Enc, C7 hybrid key switching, C8 HMult,
+ *   C9 rescale, C10 rotation, C11 operand levels, C12 canonical scales.
+ * Ciphertexts are kept in the NTT domain, limb-major.
+ */
+#include "orc.h"
+#include <stdlib.h>
+#include <string.h>
+#include <math.h>
+
+enum { TAG_SK = 1, TAG_PK_A = 2, TAG_PK_E = 3, TAG_KSK_A = 4, TAG_KSK_E = 5,
+       TAG_ENC_V = 6, TAG_ENC_E0 = 7, TAG_ENC_E1 = 8, TAG_ENC_A = 9 };
+#define ETA_ERR 21
+#define ETA_V 1
+
+orc_ct *orc_ct_alloc(const orc_params *P, int level, int ncomp)
+{
+    orc_ct *c = malloc(sizeof(*c));
+    c->level = level;
+    c->ncomp = ncomp;
+    c->a = calloc((size_t)ncomp * (level + 1) * P->n, sizeof(u64));
+    return c;
+}
+
+orc_ct *orc_ct_copy(const orc_params *P, const orc_ct *s)
+{
+    orc_ct *c = orc_ct_alloc(P, s->level, s->ncomp);
+    memcpy(c->a, s->a, sizeof(u64) * (size_t)s->ncomp * (s->level + 1) * P->n);
+    return c;
+}
+
+void orc_ct_release(orc_ct *c)
+{
+    if (!c) return;
+    free(c->a);
+    free(c);
+}
+
+/* keep limbs 0..level (exact: the value mod Q_level is unchanged) */
+static orc_ct *drop_limbs(const orc_params *P, const orc_ct *s, int level)
+{
+    orc_ct *c = orc_ct_alloc(P, level, s->ncomp);
+    for (int k = 0; k < s->ncomp; k++)
+        for (int i = 0; i <= level; i++)
+            memcpy(LIMB(P, c, k, i), LIMB(P, s, k, i), sizeof(u64) * P->n);
+    return c;
+}
+
+/* ---------------------------------------------------------------- keys (C5, C6, C7) */
+
+/* integer coefficient vector -> NTT-domain residues for prime index pi */
+static void int_to_ntt(const orc_params *P, const int64_t *v, int pi, u64 *out)
+{
+    u64 q = P->prime[pi];
+    for (int t = 0; t < P->n; t++) {
+        int64_t x = v[t] % (int64_t)q;
+        out[t] = (u64)(x < 0 ? x + (int64_t)q : x);
+    }
+    orc_ntt_fwd(P, pi, out);
+}
+
+static void sample_cbd_vec(const orc_params *P, u64 seed, uint32_t tag, u64 sub, int eta, int64_t *out)
+{
+    for (int t = 0; t < P->n; t++) out[t] = orc_cbd(orc_stream(seed, tag, sub, (u64)t), eta);
+}
+
+/* sparse ternary secret with exactly h non-zeros: partial Fisher-Yates over
+ * positions, word 2i picks j = i + w mod (N-i), bit 0 of word 2i+1 the sign. */
+static void sample_secret(const orc_params *P, u64 seed, int h, int64_t *s)
+{
+    int N = P->n;
+    int *perm = malloc(sizeof(int) * N);
+    for (int i = 0; i < N; i++) perm[i] = i;
+    memset(s, 0, sizeof(int64_t) * N);
+    for (int i = 0; i < h; i++) {
+        u64 w = orc_stream(seed, TAG_SK, 0, 2 * (u64)i);
+        int j = i + (int)(w % (u64)(N - i));
+        int t = perm[i]; perm[i] = perm[j]; perm[j] = t;
+        u64 sg = orc_stream(seed, TAG_SK, 0, 2 * (u64)i + 1);
+        s[perm[i]] = (sg & 1) ? -1 : 1;
+    }
+    free(perm);
+}
+
+/* C7: evk_j = (-a_j s + e_j + [i in D_j] (P mod q_i) s', a_j) over Q_L u P. */
+static void make_swk(const orc_params *P, const orc_keys *K, u64 seed, int key_id, const u64 *sprime, orc_swk *out)
+{
+    int N = P->n, nt = P->n_q + P->n_p;
+    out->galois = key_id;
+    out->dnum = P->dnum;
+    out->k = malloc(sizeof(u64) * (size_t)P->dnum * 2 * nt * N);
+    int64_t *e = malloc(sizeof(int64_t) * N);
+    for (int j = 0; j < P->dnum; j++) {
+        u64 sub = (u64)key_id * 256 + (u64)j;
+        sample_cbd_vec(P, seed, TAG_KSK_E, sub, ETA_ERR, e);
+        #pragma omp parallel for
+        for (int i = 0; i < nt; i++) {
+            u64 q = P->prime[i];
+            u64 *k0 = out->k + (((size_t)j * 2 + 0) * nt + i) * N;
+            u64 *k1 = out->k + (((size_t)j * 2 + 1) * nt + i) * N;
+            int_to_ntt(P, e, i, k0);  /* k0 = e_j (NTT) */
+            const u64 *s = K->s_ntt + (size_t)i * N;
+            int in_digit = (i < P->n_q) && (i / P->alpha == j);
+            for (int t = 0; t < N; t++) {
+                u64 a = orc_uniform_mod(seed, TAG_KSK_A, sub, (u64)i * N + t, q);
+                k1[t] = a;
+                u64 v = orc_sub(k0[t], orc_mul(a, s[t], q), q);
+                if (in_digit) v = orc_add(v, orc_mul(P->p_mod_q[i], sprime[(size_t)i * N + t], q), q);
+                k0[t] = v;
+            }
+        }
+    }
+    free(e);
+}
+
+int orc_galois_of_rot(const orc_params *P, int r)
+{
+    int N0 = P->n / 2;
+    r %= N0;
+    if (r < 0) r += N0;
+    return (int)orc_pow(5, (u64)r, 2ull * P->n);
+}
+
+orc_keys *orc_keygen(const orc_params *P, u64 seed, int h, const int *galois, int n_galois, int relin)
+{
+    int N = P->n, nt = P->n_q + P->n_p;
+    orc_keys *K = calloc(1, sizeof(*K));
+    K->s_coeff = malloc(sizeof(int64_t) * N);
+    sample_secret(P, seed, h, K->s_coeff);
+    K->s_ntt = malloc(sizeof(u64) * (size_t)nt * N);
+    #pragma omp parallel for
+    for (int i = 0; i < nt; i++) int_to_ntt(P, K->s_coeff, i, K->s_ntt + (size_t)i * N);
+    /* pk over Q_L */
+    K->pk = malloc(sizeof(u64) * 2 * (size_t)P->n_q * N);
+    int64_t *e = malloc(sizeof(int64_t) * N);
+    sample_cbd_vec(P, seed, TAG_PK_E, 0, ETA_ERR, e);
+    #pragma omp parallel for
+    for (int i = 0; i < P->n_q; i++) {
+        u64 q = P->prime[i];
+        u64 *b = K->pk + (size_t)i * N, *a = K->pk + ((size_t)P->n_q + i) * N;
+        int_to_ntt(P, e, i, b);
+        for (int t = 0; t < N; t++) {
+            a[t] = orc_uniform_mod(seed, TAG_PK_A, 0, (u64)i * N + t, q);
+            b[t] = orc_sub(b[t], orc_mul(a[t], K->s_ntt[(size_t)i * N + t], q), q);
+        }
+    }
+    free(e);
+    K->n_swk = n_galois + (relin ? 1 : 0);
+    K->swk = calloc(K->n_swk, sizeof(orc_swk));
+    u64 *sp = malloc(sizeof(u64) * (size_t)nt * N);
+    unsigned *perm = malloc(sizeof(unsigned) * N);
+    int w = 0;
+    if (relin) {
+        for (size_t x = 0; x < (size_t)nt * N; x++) {
+            u64 q = P->prime[x / N];
+            sp[x] = orc_mul(K->s_ntt[x], K->s_ntt[x], q);
+        }
+        make_swk(P, K, seed, 0, sp, &K->swk[w++]);
+    }
+    for (int g = 0; g < n_galois; g++) {
+        orc_galois_perm(P, galois[g], perm);
+        for (int i = 0; i < nt; i++)
+            for (int t = 0; t < N; t++) sp[(size_t)i * N + t] = K->s_ntt[(size_t)i * N + perm[t]];
+        make_swk(P, K, seed, galois[g], sp, &K->swk[w++]);
+    }
+    free(sp);
+    free(perm);
+    return K;
+}
+
+void orc_keys_free(orc_keys *K)
+{
+    if (!K) return;
+    for (int i = 0; i < K->n_swk; i++) free(K->swk[i].k);
+    free(K->swk);
+    free(K->s_coeff);
+    free(K->s_ntt);
+    free(K->pk);
+    free(K);
+}
+
+const orc_swk *orc_find_key(const orc_keys *K, int galois)
+{
+    for (int i = 0; i < K->n_swk; i++)
+        if (K->swk[i].galois == galois) return &K->swk[i];
+    return NULL;
+}
+
+/* ---------------------------------------------------------------- Enc / Dec (C6) */
+
+/* pt: (level+1) limbs of coefficient-domain residues. */
+orc_ct *orc_encrypt_pk(const orc_params *P, const orc_keys *K, const u64 *pt, int level, u64 seed, u64 ct_index)
+{
+    int N = P->n;
+    orc_ct *c = orc_ct_alloc(P, level, 2);
+    int64_t *v = malloc(sizeof(int64_t) * N), *e0 = malloc(sizeof(int64_t) * N), *e1 = malloc(sizeof(int64_t) * N);
+    sample_cbd_vec(P, seed, TAG_ENC_V, ct_index, ETA_V, v);
+    sample_cbd_vec(P, seed, TAG_ENC_E0, ct_index, ETA_ERR, e0);
+    sample_cbd_vec(P, seed, TAG_ENC_E1, ct_index, ETA_ERR, e1);
+    #pragma omp parallel for
+    for (int i = 0; i <= level; i++) {
+        u64 q = P->prime[i];
+        u64 *vn = malloc(sizeof(u64) * N), *m = malloc(sizeof(u64) * N);
+        int_to_ntt(P, v, i, vn);
+        memcpy(m, pt + (size_t)i * N, sizeof(u64) * N);
+        orc_ntt_fwd(P, i, m);
+        u64 *c0 = LIMB(P, c, 0, i), *c1 = LIMB(P, c, 1, i);
+        int_to_ntt(P, e0, i, c0);
+        int_to_ntt(P, e1, i, c1);
+        const u64 *b = K->pk + (size_t)i * N, *a = K->pk + ((size_t)P->n_q + i) * N;
+        for (int t = 0; t < N; t++) {
+            c0[t] = orc_add(orc_add(c0[t], orc_mul(vn[t], b[t], q), q), m[t], q);
+            c1[t] = orc_add(c1[t], orc_mul(vn[t], a[t], q), q);
+        }
+        free(vn);
+        free(m);
+    }
+    free(v); free(e0); free(e1);
+    return c;
+}
+
+orc_ct *orc_encrypt_sk(const orc_params *P, const orc_keys *K, const u64 *pt, int level, u64 seed, u64 ct_index)
+{
+    int N = P->n;
+    orc_ct *c = orc_ct_alloc(P, level, 2);
+    int64_t *e = malloc(sizeof(int64_t) * N);
+    sample_cbd_vec(P, seed, TAG_ENC_E0, ct_index, ETA_ERR, e);
+    #pragma omp parallel for
+    for (int i = 0; i <= level; i++) {
+        u64 q = P->prime[i];
+        u64 *m = malloc(sizeof(u64) * N);
+        memcpy(m, pt + (size_t)i * N, sizeof(u64) * N);
+        orc_ntt_fwd(P, i, m);
+        u64 *c0 = LIMB(P, c, 0, i), *c1 = LIMB(P, c, 1, i);
+        int_to_ntt(P, e, i, c0);
+        for (int t = 0; t < N; t++) {
+            u64 a = orc_uniform_mod(seed, TAG_ENC_A, ct_index, (u64)i * N + t, q);
+            c1[t] = a;
+            c0[t] = orc_add(orc_sub(c0[t], orc_mul(a, K->s_ntt[(size_t)i * N + t], q), q), m[t], q);
+        }
+        free(m);
+    }
+    free(e);
+    return c;
+}
+
+/* m = c0 + c1 s mod Q_l, returned as coefficient-domain residues (l+1 limbs). */
+void orc_decrypt(const orc_params *P, const orc_keys *K, const orc_ct *c, u64 *out)
+{
+    int N = P->n;
+    #pragma omp parallel for
+    for (int i = 0; i <= c->level; i++) {
+        u64 q = P->prime[i];
+        const u64 *c0 = LIMB(P, c, 0, i), *c1 = LIMB(P, c, 1, i);
+        u64 *o = out + (size_t)i * N;
+        for (int t = 0; t < N; t++) o[t] = orc_add(c0[t], orc_mul(c1[t], K->s_ntt[(size_t)i * N + t], q), q);
+        orc_ntt_inv(P, i, o);
+    }
+}
+
+/* ---------------------------------------------------------------- arithmetic */
+
+orc_ct *orc_op_level_down(const orc_params *P, const orc_ct *a, int target)
+{
+    if (a->level == target) return orc_ct_copy(P, a);
+    orc_ledger[LG_LEVELDOWN]++;
+    return orc_op_mult_const(P, a, 1.0, target);
+}
+
+static void match_levels(const orc_params *P, const orc_ct *a, const orc_ct *b, orc_ct **a2, orc_ct **b2)
+{
+    int l = a->level < b->level ? a->level : b->level;
+    *a2 = orc_op_level_down(P, a, l);
+    *b2 = orc_op_level_down(P, b, l);
+}
+
+static orc_ct *addsub(const orc_params *P, const orc_ct *a0, const orc_ct *b0, int sub)
+{
+    orc_ct *a, *b;
+    match_levels(P, a0, b0, &a, &b);
+    int nc = a->ncomp > b->ncomp ? a->ncomp : b->ncomp;
+    orc_ct *c = orc_ct_alloc(P, a->level, nc);
+    for (int k = 0; k < nc; k++)
+        for (int i = 0; i <= a->level; i++) {
+            u64 q = P->prime[i];
+            u64 *o = LIMB(P, c, k, i);
+            for (int t = 0; t < P->n; t++) {
+                u64 x = k < a->ncomp ? LIMB(P, a, k, i)[t] : 0;
+                u64 y = k < b->ncomp ? LIMB(P, b, k, i)[t] : 0;
+                o[t] = sub ? orc_sub(x, y, q) : orc_add(x, y, q);
+            }
+        }
+    orc_ct_release(a);
+    orc_ct_release(b);
+    return c;
+}
+
+orc_ct *orc_op_add(const orc_params *P, const orc_ct *a, const orc_ct *b) { return addsub(P, a, b, 0); }
+orc_ct *orc_op_sub(const orc_params *P, const orc_ct *a, const orc_ct *b) { return addsub(P, a, b, 1); }
+
+orc_ct *orc_op_mult_int(const orc_params *P, const orc_ct *a, int64_t c)
+{
+    orc_ct *r = orc_ct_copy(P, a);
+    for (int k = 0; k < a->ncomp; k++)
+        for (int i = 0; i <= a->level; i++) {
+            u64 q = P->prime[i];
+            int64_t cm = c % (int64_t)q;
+            u64 cu = (u64)(cm < 0 ? cm + (int64_t)q : cm);
+            u64 *o = LIMB(P, r, k, i);
+            for (int t = 0; t < P->n; t++) o[t] = orc_mul(o[t], cu, q);
+        }
+    return r;
+}
+
+/* c0 += rint(c * Delta_l) (a constant polynomial is constant in the NTT domain) */
+orc_ct *orc_op_add_const(const orc_params *P, const orc_ct *a, double c)
+{
+    orc_ct *r = orc_ct_copy(P, a);
+    double v = c * P->scale[a->level];
+    for (int i = 0; i <= a->level; i++) {
+        u64 q = P->prime[i], C = orc_residue_of_double(v, q);
+        u64 *o = LIMB(P, r, 0, i);
+        for (int t = 0; t < P->n; t++) o[t] = orc_add(o[t], C, q);
+    }
+    return r;
+}
+
+/* C9: a'_i = (a_i - [a_l]_centred) * q_l^{-1} mod q_i */
+orc_ct *orc_op_rescale(const orc_params *P, const orc_ct *a)
+{
+    int l = a->level, N = P->n;
+    orc_ct *r = orc_ct_alloc(P, l - 1, a->ncomp);
+    u64 ql = P->prime[l];
+    u64 *last = malloc(sizeof(u64) * N);
+    for (int k = 0; k < a->ncomp; k++) {
+        memcpy(last, LIMB(P, a, k, l), sizeof(u64) * N);
+        orc_ntt_inv(P, l, last);
+        #pragma omp parallel for
+        for (int i = 0; i < l; i++) {
+            u64 q = P->prime[i], qinv = orc_inv(ql % q, q);
+            u64 *v = malloc(sizeof(u64) * N);
+            for (int t = 0; t < N; t++) {
+                u64 x = last[t];
+                if (x <= (ql - 1) / 2) v[t] = x % q;             /* centred rep >= 0 */
+                else v[t] = orc_sub(0, (ql - x) % q, q);         /* centred rep < 0  */
+            }
+            orc_ntt_fwd(P, i, v);
+            const u64 *ai = LIMB(P, a, k, i);
+            u64 *o = LIMB(P, r, k, i);
+            for (int t = 0; t < N; t++) o[t] = orc_mul(orc_sub(ai[t], v[t], q), qinv, q);
+            free(v);
+        }
+    }
+    free(last);
+    orc_ledger[LG_RESCALE]++;
+    return r;
+}
+
+/* C12: multiply by a real constant and land at level `target` < level with the
+ * canonical scale: drop to target+1, multiply by rint(c*sc) with
+ * sc = (Delta_target * q_{target+1}) / Delta_level, rescale by q_{target+1}. */
+orc_ct *orc_op_mult_const(const orc_params *P, const orc_ct *a, double c, int target)
+{
+    orc_ct *d = drop_limbs(P, a, target + 1);
+    double sc = (P->scale[target] * (double)P->prime[target + 1]) / P->scale[a->level];
+    double v = c * sc;
+    for (int i = 0; i <= target + 1; i++) {
+        u64 q = P->prime[i], C = orc_residue_of_double(v, q);
+        for (int k = 0; k < d->ncomp; k++) {
+            u64 *o = LIMB(P, d, k, i);
+            for (int t = 0; t < P->n; t++) o[t] = orc_mul(o[t], C, q);
+        }
+    }
+    orc_ct *r = orc_op_rescale(P, d);
+    orc_ct_release(d);
+    orc_ledger[LG_CMULT]++;
+    return r;
+}
+
+/* Plaintext (slot vector) multiply, landing like mult_const (same sc). */
+orc_ct *orc_op_mult_pt(const orc_params *P, const orc_ct *a, const double *re, const double *im, int target)
+{
+    int N = P->n;
+    orc_ct *d = drop_limbs(P, a, target + 1);
+    double sc = (P->scale[target] * (double)P->prime[target + 1]) / P->scale[a->level];
+    u64 *pt = malloc(sizeof(u64) * (size_t)(target + 2) * N);
+    orc_encode_coeffs(P, re, im, sc, target + 1, pt);
+    #pragma omp parallel for
+    for (int i = 0; i <= target + 1; i++) {
+        u64 q = P->prime[i];
+        u64 *m = pt + (size_t)i * N;
+        orc_ntt_fwd(P, i, m);
+        for (int k = 0; k < d->ncomp; k++) {
+            u64 *o = LIMB(P, d, k, i);
+            for (int t = 0; t < N; t++) o[t] = orc_mul(o[t], m[t], q);
+        }
+    }
+    free(pt);
+    orc_ct *r = orc_op_rescale(P, d);
+    orc_ct_release(d);
+    orc_ledger[LG_PMULT]++;
+    return r;
+}
+
+/* tensor: (a0 b0, a0 b1 + a1 b0, a1 b1) at the common level (C8) */
+orc_ct *orc_op_tensor(const orc_params *P, const orc_ct *a0, const orc_ct *b0)
+{
+    orc_ct *a, *b;
+    match_levels(P, a0, b0, &a, &b);
+    orc_ct *c = orc_ct_alloc(P, a->level, 3);
+    for (int i = 0; i <= a->level; i++) {
+        u64 q = P->prime[i];
+        const u64 *x0 = LIMB(P, a, 0, i), *x1 = LIMB(P, a, 1, i), *y0 = LIMB(P, b, 0, i), *y1 = LIMB(P, b, 1, i);
+        u64 *d0 = LIMB(P, c, 0, i), *d1 = LIMB(P, c, 1, i), *d2 = LIMB(P, c, 2, i);
+        for (int t = 0; t < P->n; t++) {
+            d0[t] = orc_mul(x0[t], y0[t], q);
+            d1[t] = orc_add(orc_mul(x0[t], y1[t], q), orc_mul(x1[t], y0[t], q), q);
+            d2[t] = orc_mul(x1[t], y1[t], q);
+        }
+    }
+    orc_ct_release(a);
+    orc_ct_release(b);
+    orc_ledger[LG_TENSOR]++;
+    return c;
+}
+
+/* ---------------------------------------------------------------- key switching (C7) */
+
+/* d: (level+1) limbs NTT domain.  out0/out1: (level+1) limbs NTT domain. */
+void orc_keyswitch(const orc_params *P, const orc_swk *key, int level, const u64 *d, u64 *out0, u64 *out1)
+{
+    int N = P->n, nq = P->n_q, np = P->n_p, nt = nq + np, alpha = P->alpha;
+    int nl = level + 1;                       /* live Q limbs */
+    int beta = (nl + alpha - 1) / alpha;
+    /* target prime list: q_0..q_level, p_0..p_{np-1} (global indices) */
+    int ntg = nl + np;
+    int *gidx = malloc(sizeof(int) * ntg);
+    for (int i = 0; i < nl; i++) gidx[i] = i;
+    for (int k = 0; k < np; k++) gidx[nl + k] = nq + k;
+    u64 *acc = calloc((size_t)2 * ntg * N, sizeof(u64));
+    u64 *x = malloc(sizeof(u64) * (size_t)nl * N);
+    /* coefficient form of d */
+    memcpy(x, d, sizeof(u64) * (size_t)nl * N);
+    #pragma omp parallel for
+    for (int i = 0; i < nl; i++) orc_ntt_inv(P, i, x + (size_t)i * N);
+    for (int j = 0; j < beta; j++) {
+        int lo = j * alpha, hi = (j + 1) * alpha < nl ? (j + 1) * alpha : nl; /* digit primes [lo,hi) */
+        /* y_i = x_i * qhat_i^{-1} mod q_i */
+        int dn = hi - lo;
+        u64 *y = malloc(sizeof(u64) * (size_t)dn * N);
+        for (int a = 0; a < dn; a++) {
+            int i = lo + a;
+            u64 q = P->prime[i], qh = 1;
+            for (int b = lo; b < hi; b++) if (b != i) qh = orc_mul(qh, P->prime[b] % q, q);
+            u64 qhi = orc_inv(qh, q);
+            for (int t = 0; t < N; t++) y[(size_t)a * N + t] = orc_mul(x[(size_t)i * N + t], qhi, q);
+        }
+        #pragma omp parallel for
+        for (int g = 0; g < ntg; g++) {
+            int pi = gidx[g];
+            u64 p = P->prime[pi];
+            u64 *ext = malloc(sizeof(u64) * N);
+            if (pi >= lo && pi < hi) {
+                memcpy(ext, d + (size_t)pi * N, sizeof(u64) * N);   /* own limb: unchanged */
+            } else {
+                u64 *qhp = malloc(sizeof(u64) * dn);
+                for (int a = 0; a < dn; a++) {
+                    u64 v = 1;
+                    for (int b = lo; b < hi; b++) if (b != lo + a) v = orc_mul(v, P->prime[b] % p, p);
+                    qhp[a] = v;
+                }
+                for (int t = 0; t < N; t++) {
+                    u64 s = 0;
+                    for (int a = 0; a < dn; a++) s = orc_add(s, orc_mul(y[(size_t)a * N + t] % p, qhp[a], p), p);
+                    ext[t] = s;
+                }
+                free(qhp);
+                orc_ntt_fwd(P, pi, ext);
+            }
+            const u64 *k0 = key->k + (((size_t)j * 2 + 0) * nt + pi) * N;
+            const u64 *k1 = key->k + (((size_t)j * 2 + 1) * nt + pi) * N;
+            u64 *a0 = acc + (size_t)g * N, *a1 = acc + ((size_t)ntg + g) * N;
+            for (int t = 0; t < N; t++) {
+                a0[t] = orc_add(a0[t], orc_mul(ext[t], k0[t], p), p);
+                a1[t] = orc_add(a1[t], orc_mul(ext[t], k1[t], p), p);
+            }
+            free(ext);
+        }
+        free(y);
+    }
+    /* ModDown: (acc_Q - BConv_{P->Q}(acc_P)) * P^{-1} */
+    for (int c = 0; c < 2; c++) {
+        u64 *A = acc + (size_t)c * ntg * N;
+        u64 *out = c == 0 ? out0 : out1;
+        u64 *z = malloc(sizeof(u64) * (size_t)np * N);
+        for (int k = 0; k < np; k++) {
+            int pi = nq + k;
+            u64 p = P->prime[pi], ph = 1;
+            for (int b = 0; b < np; b++) if (b != k) ph = orc_mul(ph, P->prime[nq + b] % p, p);
+            u64 phi = orc_inv(ph, p);
+            memcpy(z + (size_t)k * N, A + (size_t)(nl + k) * N, sizeof(u64) * N);
+            orc_ntt_inv(P, pi, z + (size_t)k * N);
+            for (int t = 0; t < N; t++) z[(size_t)k * N + t] = orc_mul(z[(size_t)k * N + t], phi, p);
+        }
+        #pragma omp parallel for
+        for (int i = 0; i < nl; i++) {
+            u64 q = P->prime[i];
+            u64 *php = malloc(sizeof(u64) * np);
+            for (int k = 0; k < np; k++) {
+                u64 v = 1;
+                for (int b = 0; b < np; b++) if (b != k) v = orc_mul(v, P->prime[nq + b] % q, q);
+                php[k] = v;
+            }
+            u64 *conv = malloc(sizeof(u64) * N);
+            for (int t = 0; t < N; t++) {
+                u64 s = 0;
+                for (int k = 0; k < np; k++) s = orc_add(s, orc_mul(z[(size_t)k * N + t] % q, php[k], q), q);
+                conv[t] = s;
+            }
+            orc_ntt_fwd(P, i, conv);
+            for (int t = 0; t < N; t++)
+                out[(size_t)i * N + t] = orc_mul(orc_sub(A[(size_t)i * N + t], conv[t], q), P->p_inv_mod_q[i], q);
+            free(conv);
+            free(php);
+        }
+        free(z);
+    }
+    free(acc);
+    free(x);
+    free(gidx);
+    orc_ledger[LG_KS]++;
+}
+
+/* relinearise a degree-2 ciphertext (no rescale) */
+orc_ct *orc_op_relin(const orc_params *P, const orc_keys *K, const orc_ct *d)
+{
+    const orc_swk *rk = orc_find_key(K, 0);
+    int l = d->level;
+    size_t sz = (size_t)(l + 1) * P->n;
+    u64 *k0 = malloc(sizeof(u64) * sz), *k1 = malloc(sizeof(u64) * sz);
+    orc_keyswitch(P, rk, l, LIMB(P, d, 2, 0), k0, k1);
+    orc_ct *c = orc_ct_alloc(P, l, 2);
+    for (int i = 0; i <= l; i++) {
+        u64 q = P->prime[i];
+        for (int t = 0; t < P->n; t++) {
+            LIMB(P, c, 0, i)[t] = orc_add(LIMB(P, d, 0, i)[t], k0[(size_t)i * P->n + t], q);
+            LIMB(P, c, 1, i)[t] = orc_add(LIMB(P, d, 1, i)[t], k1[(size_t)i * P->n + t], q);
+        }
+    }
+    free(k0);
+    free(k1);
+    return c;
+}
+
+/* C8: HMult = tensor -> relin (KS of d2 under s^2) -> rescale */
+orc_ct *orc_op_mult(const orc_params *P, const orc_keys *K, const orc_ct *a, const orc_ct *b)
+{
+    orc_ct *d = orc_op_tensor(P, a, b);
+    orc_ct *c = orc_op_relin(P, K, d);
+    orc_ct *r = orc_op_rescale(P, c);
+    orc_ct_release(d);
+    orc_ct_release(c);
+    orc_ledger[LG_HMULT]++;
+    return r;
+}
+
+/* C10: sigma_k on both components then KS(sigma_k(c1)) from sigma_k(s) to s */
+orc_ct *orc_op_galois(const orc_params *P, const orc_keys *K, const orc_ct *a, int k)
+{
+    int N = P->n, l = a->level;
+    const orc_swk *key = orc_find_key(K, k);
+    if (!key) return NULL;
+    unsigned *perm = malloc(sizeof(unsigned) * N);
+    orc_galois_perm(P, k, perm);
+    orc_ct *s = orc_ct_alloc(P, l, 2);
+    for (int c = 0; c < 2; c++)
+        for (int i = 0; i <= l; i++)
+            for (int t = 0; t < N; t++) LIMB(P, s, c, i)[t] = LIMB(P, a, c, i)[perm[t]];
+    size_t sz = (size_t)(l + 1) * N;
+    u64 *k0 = malloc(sizeof(u64) * sz), *k1 = malloc(sizeof(u64) * sz);
+    orc_keyswitch(P, key, l, LIMB(P, s, 1, 0), k0, k1);
+    orc_ct *r = orc_ct_alloc(P, l, 2);
+    for (int i = 0; i <= l; i++) {
+        u64 q = P->prime[i];
+        for (int t = 0; t < N; t++) {
+            LIMB(P, r, 0, i)[t] = orc_add(LIMB(P, s, 0, i)[t], k0[(size_t)i * N + t], q);
+            LIMB(P, r, 1, i)[t] = k1[(size_t)i * N + t];
+        }
+    }
+    free(k0);
+    free(k1);
+    free(perm);
+    orc_ct_release(s);
+    orc_ledger[LG_ROT]++;
+    return r;
+}
+
+/* left rotation by r (G1): out_j = in_{j+r} */
+orc_ct *orc_op_rotate(const orc_params *P, const orc_keys *K, const orc_ct *a, int r)
+{
+    return orc_op_galois(P, K, a, orc_galois_of_rot(P, r));
+}
+
+orc_ct *orc_op_conjugate(const orc_params *P, const orc_keys *K, const orc_ct *a)
+{
+    return orc_op_galois(P, K, a, 2 * P->n - 1);
+}

@@ -1,0 +1,342 @@
+"""ctypes wrapper of the CPU oracle (oracle/liborc.so).
+
+TEST INFRASTRUCTURE ONLY: only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference legs may import this module.  The product
+package (paper_2410_11184_b200) never imports it, and the oracle shares no
+code with the product.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = os.path.join(_HERE, "liborc.so")
+
+u64p = np.ctypeslib.ndpointer(dtype=np.uint64, flags="C_CONTIGUOUS")
+i64p = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
+f64p = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+i32p = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")
+u32p = np.ctypeslib.ndpointer(dtype=np.uint32, flags="C_CONTIGUOUS")
+
+OP = dict(add=0, sub=1, mult=2, tensor=3, relin=4, rescale=5, level_down=6, mult_const=7,
+          add_const=8, mult_int=9, rotate=10, conj=11, galois=12)
+LEDGER = ["hmult", "tensor", "ks", "rot", "rescale", "cmult", "pmult", "leveldown", "bts", "ntt"]
+
+
+def build() -> str:
+    subprocess.run(["make", "-s", "-C", _HERE], check=True)
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB):
+            build()
+        L = C.CDLL(_LIB)
+        vp = C.c_void_p
+        L.orc_api_params.restype = vp
+        L.orc_api_params.argtypes = [C.c_int, C.c_int, i32p, C.c_int, i32p, C.c_int, i32p]
+        L.orc_api_params_free.argtypes = [vp]
+        L.orc_api_primes.argtypes = [vp, u64p]
+        L.orc_api_psi.restype = C.c_uint64
+        L.orc_api_psi.argtypes = [vp, C.c_int]
+        L.orc_api_scale.restype = C.c_double
+        L.orc_api_scale.argtypes = [vp, C.c_int]
+        L.orc_api_ntt.argtypes = [vp, C.c_int, u64p, C.c_int]
+        L.orc_api_ntt_naive.argtypes = [vp, C.c_int, u64p]
+        L.orc_api_galois_perm.argtypes = [vp, C.c_int, u32p]
+        L.orc_api_chacha20.argtypes = [u32p, C.c_uint32, u32p, u32p]
+        L.orc_api_stream.restype = C.c_uint64
+        L.orc_api_stream.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64]
+        L.orc_api_residue.restype = C.c_uint64
+        L.orc_api_residue.argtypes = [C.c_double, C.c_uint64]
+        L.orc_api_galois_of_rot.restype = C.c_int
+        L.orc_api_galois_of_rot.argtypes = [vp, C.c_int]
+        L.orc_api_keygen.restype = vp
+        L.orc_api_keygen.argtypes = [vp, C.c_uint64, C.c_int, i32p, C.c_int, C.c_int]
+        L.orc_api_keys_free.argtypes = [vp]
+        L.orc_api_secret.argtypes = [vp, vp, i64p]
+        L.orc_api_pk.argtypes = [vp, vp, u64p]
+        L.orc_api_swk.restype = C.c_int
+        L.orc_api_swk.argtypes = [vp, vp, C.c_int, u64p]
+        L.orc_api_encode.argtypes = [vp, f64p, f64p, C.c_double, C.c_int, u64p]
+        L.orc_api_encode_naive.restype = C.c_double
+        L.orc_api_encode_naive.argtypes = [vp, f64p, f64p, C.c_double, C.c_int]
+        L.orc_api_decrypt_decode.argtypes = [vp, vp, vp, f64p, f64p]
+        L.orc_api_decrypt.argtypes = [vp, vp, vp, u64p]
+        L.orc_api_encrypt.restype = vp
+        L.orc_api_encrypt.argtypes = [vp, vp, u64p, C.c_int, C.c_uint64, C.c_uint64, C.c_int]
+        L.orc_api_ct_import.restype = vp
+        L.orc_api_ct_import.argtypes = [vp, C.c_int, C.c_int, u64p]
+        L.orc_api_ct_export.argtypes = [vp, vp, u64p]
+        L.orc_api_ct_level.restype = C.c_int
+        L.orc_api_ct_level.argtypes = [vp]
+        L.orc_api_ct_ncomp.restype = C.c_int
+        L.orc_api_ct_ncomp.argtypes = [vp]
+        L.orc_api_ct_free.argtypes = [vp]
+        L.orc_api_op.restype = vp
+        L.orc_api_op.argtypes = [vp, vp, C.c_int, vp, vp, C.c_double, C.c_int]
+        L.orc_api_mult_pt.restype = vp
+        L.orc_api_mult_pt.argtypes = [vp, vp, f64p, f64p, C.c_int]
+        L.orc_api_keyswitch.restype = C.c_int
+        L.orc_api_keyswitch.argtypes = [vp, vp, C.c_int, C.c_int, u64p, u64p, u64p]
+        L.orc_api_cheb.restype = vp
+        L.orc_api_cheb.argtypes = [vp, vp, vp, C.c_int, C.c_double, C.c_double, f64p]
+        L.orc_api_cheb_depth.restype = C.c_int
+        L.orc_api_cheb_depth.argtypes = [C.c_int]
+        L.orc_api_softmax.restype = C.c_int
+        L.orc_api_softmax.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, i32p, f64p, f64p, f64p,
+                                      C.POINTER(vp), C.POINTER(vp)]
+        L.orc_api_ledger.argtypes = [C.POINTER(C.c_long)]
+        _lib = L
+    return _lib
+
+
+class Params:
+    """An oracle parameter set (C1, C2, C12)."""
+
+    def __init__(self, log_n, q_bits, p_bits, alpha, log2_anchor):
+        L = lib()
+        self.log_n, self.n = log_n, 1 << log_n
+        self.q_bits, self.p_bits = list(q_bits), list(p_bits)
+        self.n_q, self.n_p, self.alpha = len(q_bits), len(p_bits), alpha
+        self.ptr = L.orc_api_params(log_n, self.n_q, np.array(q_bits, np.int32), self.n_p,
+                                    np.array(p_bits, np.int32), alpha, np.array(log2_anchor, np.int32))
+        assert self.ptr
+        pr = np.zeros(self.n_q + self.n_p, np.uint64)
+        L.orc_api_primes(self.ptr, pr)
+        self.primes = [int(x) for x in pr]
+        self.dnum = (self.n_q + alpha - 1) // alpha
+
+    @classmethod
+    def from_preset(cls, pre: dict):
+        return cls(pre["log_n"], pre["q_bits"], pre["p_bits"], pre["alpha"], pre["log2_anchor"])
+
+    def __del__(self):
+        if getattr(self, "ptr", None) and _lib is not None:
+            _lib.orc_api_params_free(self.ptr)
+            self.ptr = None
+
+    def psi(self, i):
+        return int(lib().orc_api_psi(self.ptr, i))
+
+    def scale(self, level):
+        return float(lib().orc_api_scale(self.ptr, level))
+
+    def ntt(self, pi, a, inverse=False):
+        a = np.ascontiguousarray(a, dtype=np.uint64).copy()
+        lib().orc_api_ntt(self.ptr, pi, a, 1 if inverse else 0)
+        return a
+
+    def ntt_naive(self, pi, a):
+        a = np.ascontiguousarray(a, dtype=np.uint64).copy()
+        lib().orc_api_ntt_naive(self.ptr, pi, a)
+        return a
+
+    def galois_perm(self, k):
+        p = np.zeros(self.n, np.uint32)
+        lib().orc_api_galois_perm(self.ptr, k, p)
+        return p
+
+    def galois_of_rot(self, r):
+        return int(lib().orc_api_galois_of_rot(self.ptr, r))
+
+    def encode(self, re, im=None, scale=None, level=0):
+        re = np.ascontiguousarray(re, np.float64)
+        im = np.zeros_like(re) if im is None else np.ascontiguousarray(im, np.float64)
+        out = np.zeros((level + 1) * self.n, np.uint64)
+        lib().orc_api_encode(self.ptr, re, im, scale, level, out)
+        return out.reshape(level + 1, self.n)
+
+
+class Keys:
+    def __init__(self, params: Params, seed: int, h: int, galois=(), relin=True):
+        self.P = params
+        g = np.array(list(galois), np.int32) if len(galois) else np.zeros(1, np.int32)
+        self.galois = list(galois)
+        self.ptr = lib().orc_api_keygen(params.ptr, seed, h, g, len(galois), 1 if relin else 0)
+
+    def __del__(self):
+        if getattr(self, "ptr", None) and _lib is not None:
+            _lib.orc_api_keys_free(self.ptr)
+            self.ptr = None
+
+    def secret(self):
+        s = np.zeros(self.P.n, np.int64)
+        lib().orc_api_secret(self.P.ptr, self.ptr, s)
+        return s
+
+    def pk(self):
+        o = np.zeros(2 * self.P.n_q * self.P.n, np.uint64)
+        lib().orc_api_pk(self.P.ptr, self.ptr, o)
+        return o.reshape(2, self.P.n_q, self.P.n)
+
+    def swk(self, galois):
+        P = self.P
+        o = np.zeros(P.dnum * 2 * (P.n_q + P.n_p) * P.n, np.uint64)
+        assert lib().orc_api_swk(P.ptr, self.ptr, galois, o) == 0
+        return o.reshape(P.dnum, 2, P.n_q + P.n_p, P.n)
+
+
+class Ct:
+    def __init__(self, params: Params, ptr):
+        assert ptr, "oracle op failed"
+        self.P, self.ptr = params, ptr
+
+    def __del__(self):
+        if getattr(self, "ptr", None) and _lib is not None:
+            _lib.orc_api_ct_free(self.ptr)
+            self.ptr = None
+
+    @property
+    def level(self):
+        return lib().orc_api_ct_level(self.ptr)
+
+    @property
+    def ncomp(self):
+        return lib().orc_api_ct_ncomp(self.ptr)
+
+    def words(self):
+        w = np.zeros(self.ncomp * (self.level + 1) * self.P.n, np.uint64)
+        lib().orc_api_ct_export(self.P.ptr, self.ptr, w)
+        return w.reshape(self.ncomp, self.level + 1, self.P.n)
+
+    @classmethod
+    def from_words(cls, params, words):
+        words = np.ascontiguousarray(words, np.uint64)
+        nc, l1, _ = words.shape
+        return cls(params, lib().orc_api_ct_import(params.ptr, l1 - 1, nc, words.ravel()))
+
+
+def encrypt(P: Params, K: Keys, pt, level, seed, idx, use_sk=False) -> Ct:
+    pt = np.ascontiguousarray(pt, np.uint64).reshape(-1)
+    return Ct(P, lib().orc_api_encrypt(P.ptr, K.ptr, pt, level, seed, idx, 1 if use_sk else 0))
+
+
+def decrypt_decode(P: Params, K: Keys, ct: Ct):
+    re = np.zeros(P.n // 2)
+    im = np.zeros(P.n // 2)
+    lib().orc_api_decrypt_decode(P.ptr, K.ptr, ct.ptr, re, im)
+    return re + 1j * im
+
+
+def decrypt(P: Params, K: Keys, ct: Ct):
+    o = np.zeros((ct.level + 1) * P.n, np.uint64)
+    lib().orc_api_decrypt(P.ptr, K.ptr, ct.ptr, o)
+    return o.reshape(ct.level + 1, P.n)
+
+
+def op(P: Params, K, name, a: Ct, b: Ct = None, c: float = 0.0, i: int = 0) -> Ct:
+    return Ct(P, lib().orc_api_op(P.ptr, K.ptr if K is not None else None, OP[name], a.ptr,
+                                  b.ptr if b is not None else None, c, i))
+
+
+def mult_pt(P: Params, a: Ct, re, im=None, target=None) -> Ct:
+    re = np.ascontiguousarray(re, np.float64)
+    im = np.zeros_like(re) if im is None else np.ascontiguousarray(im, np.float64)
+    return Ct(P, lib().orc_api_mult_pt(P.ptr, a.ptr, re, im, a.level - 1 if target is None else target))
+
+
+def keyswitch(P: Params, K: Keys, galois, level, d):
+    d = np.ascontiguousarray(d, np.uint64).reshape(-1)
+    o0 = np.zeros((level + 1) * P.n, np.uint64)
+    o1 = np.zeros_like(o0)
+    assert lib().orc_api_keyswitch(P.ptr, K.ptr, galois, level, d, o0, o1) == 0
+    return o0.reshape(level + 1, P.n), o1.reshape(level + 1, P.n)
+
+
+def cheb(P: Params, K: Keys, x: Ct, poly: dict) -> Ct:
+    c = np.ascontiguousarray(poly["coeffs"], np.float64)
+    return Ct(P, lib().orc_api_cheb(P.ptr, K.ptr, x.ptr, len(c) - 1, poly["a"], poly["b"], c))
+
+
+def cheb_depth(deg):
+    return lib().orc_api_cheb_depth(deg)
+
+
+def softmax(P: Params, K: Keys, cts, n, k, variant, exp_poly, inv_polys):
+    polys = [exp_poly] + list(inv_polys)
+    assert len(inv_polys) == k
+    degs = np.array([len(p["coeffs"]) - 1 for p in polys], np.int32)
+    a_s = np.array([p["a"] for p in polys], np.float64)
+    b_s = np.array([p["b"] for p in polys], np.float64)
+    co = np.concatenate([np.asarray(p["coeffs"], np.float64) for p in polys])
+    m = len(cts)
+    ins = (C.c_void_p * m)(*[c.ptr for c in cts])
+    outs = (C.c_void_p * m)()
+    rc = lib().orc_api_softmax(P.ptr, K.ptr, n, m, k, variant, degs, a_s, b_s, co, ins, outs)
+    if rc != 0:
+        raise RuntimeError(f"oracle softmax failed rc={rc}")
+    return [Ct(P, outs[i]) for i in range(m)]
+
+
+def ledger():
+    a = (C.c_long * len(LEDGER))()
+    lib().orc_api_ledger(a)
+    return dict(zip(LEDGER, list(a)))
+
+
+def ledger_reset():
+    lib().orc_api_ledger_reset()
+
+
+def chacha20_block(key, counter, nonce):
+    out = np.zeros(16, np.uint32)
+    lib().orc_api_chacha20(np.array(key, np.uint32), counter, np.array(nonce, np.uint32), out)
+    return out
+
+
+def stream(seed, tag, sub, idx):
+    return int(lib().orc_api_stream(seed, tag, sub, idx))
+
+
+def residue(x, q):
+    return int(lib().orc_api_residue(x, q))
+
+
+# ---------------------------------------------------------------- packing (a13)
+def pack(x, n0, m):
+    """PAPER.md 94-131: x[L, n] -> m slot vectors of N0.
+
+    nb = n/m coordinate blocks per ciphertext, stride = N0/nb; instance o's
+    coordinate i goes to ciphertext i // nb, slot (i % nb) * stride + o.
+    Unused lanes (o >= L) carry the input x = 0 (G9)."""
+    L, n = x.shape
+    nb = n // m
+    stride = n0 // nb
+    assert n % m == 0 and L <= stride
+    out = np.zeros((m, n0))
+    for i in range(n):
+        out[i // nb, (i % nb) * stride: (i % nb) * stride + L] = x[:, i]
+    return out
+
+
+def unpack(slots, L, n):
+    m, n0 = slots.shape
+    nb = n // m
+    stride = n0 // nb
+    y = np.zeros((L, n))
+    for i in range(n):
+        y[:, i] = slots[i // nb, (i % nb) * stride: (i % nb) * stride + L]
+    return y
+
+
+def softmax_rotation_galois(P, n, m):
+    """Galois elements the aux thread needs: rotations by -+stride*2^i (Alg 2)."""
+    nb = n // m
+    stride = (P.n // 2) // nb
+    out = set()
+    i = 0
+    while (1 << i) < nb:
+        out.add(P.galois_of_rot(stride << i))
+        out.add(P.galois_of_rot(-(stride << i)))
+        i += 1
+    return sorted(out)

@@ -1,0 +1,164 @@
+"""Offline weighted-minimax (Remez) generator for the Softmax polynomial tables.
+
+PAPER.md 423-427 [sec 5.1.2]: the paper computed its approximants with Sollya:
+minimax for exp, and for x^(-1/2) the *weighted* minimax that minimises
+||P(x) sqrt(x) - 1||_inf; degrees of the form 2^t - 1.  The coefficients were
+not printed (G15), so this tool recomputes them.  It is host tooling
+that writes DATA (data/poly_tables.json); the tables are method parameters that
+both the CUDA path and the oracle receive as inputs, like the paper's Sollya
+output.  Neither side imports this module.
+
+Representation: Chebyshev series on [a, b]: P(x) = sum_i c_i T_i(u),
+u = (2x - a - b) / (b - a).
+
+Usage:  python tools/remez.py            (rewrites data/poly_tables.json)
+"""
+from __future__ import annotations
+
+import json
+import math
+import os
+import sys
+
+import numpy as np
+from numpy.polynomial import chebyshev as Ch
+
+
+def _cheb_vander(u, d):
+    return Ch.chebvander(u, d)
+
+
+def remez(f, w, a, b, d, iters=60, grid=None, tol=1e-3):
+    """Weighted minimax: minimise max_x |w(x) (f(x) - P(x))| over [a, b].
+
+    Returns (coeffs, max_weighted_error).  Classical multiple-exchange Remez in
+    the Chebyshev basis, float64 (well conditioned up to degree ~255).
+    """
+    n_grid = grid or max(4000, 40 * (d + 2))
+    # dense grid clustered at the end points (Chebyshev-Lobatto in u)
+    ug = -np.cos(np.pi * np.arange(n_grid) / (n_grid - 1))
+    xg = 0.5 * (b - a) * ug + 0.5 * (a + b)
+    fg, wg = f(xg), w(xg)
+    Vg = _cheb_vander(ug, d)
+    # initial reference: Chebyshev extrema of T_{d+1}
+    ref = np.sort(-np.cos(np.pi * np.arange(d + 2) / (d + 1)))
+    best = None
+    for _ in range(iters):
+        xr = 0.5 * (b - a) * ref + 0.5 * (a + b)
+        A = np.zeros((d + 2, d + 2))
+        A[:, : d + 1] = _cheb_vander(ref, d)
+        A[:, d + 1] = [(-1) ** i / w(np.array([x]))[0] for i, x in enumerate(xr)]
+        sol = np.linalg.solve(A, f(xr))
+        c = sol[: d + 1]
+        err = wg * (fg - Vg @ c)
+        emax = np.max(np.abs(err))
+        if best is None or emax < best[1]:
+            best = (c.copy(), emax)
+        # new reference: extremum of each sign-constant run
+        s = np.sign(err)
+        s[s == 0] = 1
+        runs, start = [], 0
+        for i in range(1, n_grid + 1):
+            if i == n_grid or s[i] != s[start]:
+                j = start + int(np.argmax(np.abs(err[start:i])))
+                runs.append(j)
+                start = i
+        # keep d+2 alternating points with the largest |err| (drop smallest
+        # interior/end runs while too many)
+        while len(runs) > d + 2:
+            vals = [abs(err[j]) for j in runs]
+            # remove the smaller of the two end points or the smallest pair
+            if vals[0] < vals[-1]:
+                runs.pop(0)
+            else:
+                runs.pop()
+        if len(runs) < d + 2:
+            break
+        new_ref = ug[runs]
+        levelled = (np.max(np.abs(err[runs])) - np.min(np.abs(err[runs]))) / emax
+        ref = np.sort(new_ref)
+        if levelled < tol:
+            break
+    return best
+
+
+def cheb_eval(coeffs, a, b, x):
+    u = (2 * np.asarray(x, dtype=np.float64) - a - b) / (b - a)
+    return Ch.chebval(u, coeffs)
+
+
+def make_exp(M, k, deg):
+    f = lambda x: np.exp(x / 2.0 ** k)
+    c, e = remez(f, lambda x: np.ones_like(x), -float(M), 0.0, deg)
+    return dict(func=f"exp(x/2^{k})", a=-float(M), b=0.0, coeffs=[float(v) for v in c], weight="abs",
+                max_err=float(e), log2_err=float(math.log2(e)))
+
+
+def make_invpow(p, a, b, deg):
+    """Weighted minimax of x^(-p): minimise |P(x) x^p - 1| (PAPER.md 424)."""
+    f = lambda x: x ** (-p)
+    w = lambda x: x ** p
+    c, e = remez(f, w, float(a), float(b), deg)
+    return dict(func=f"x^(-{p})", a=float(a), b=float(b), coeffs=[float(v) for v in c], weight="rel",
+                max_err=float(e), log2_err=float(math.log2(e)))
+
+
+def softmax_tables(n, M, k, variant, deg_exp, deg_first, deg_mid, deg_last, guard=0.02, alpha=None):
+    """Per-iteration polynomial list for one (n, M, k, variant) configuration.
+
+    First interval  [n e^{-M/2^(k-1)} (1-guard), n (1+guard)]   (PAPER.md 1001-1002)
+    Later intervals [(1-alpha)^2/n, (1+alpha)^2]                  (PAPER.md 427)
+    alpha = 2 * (weighted error of the previous step), i.e. |x P^2 - 1|.
+    """
+    polys = {"exp": make_exp(M, k, deg_exp)}
+    lo = n * math.exp(-M / 2.0 ** (k - 1)) * (1 - guard)
+    hi = n * (1 + guard)
+    inv = []
+    prev_alpha = None
+    for j in range(1, k + 1):
+        p = 0.5 if variant == "A" else 0.5 ** j
+        if j == 1:
+            a, b = lo, hi
+            deg = deg_first if k > 1 else deg_last
+        else:
+            al = prev_alpha * (1 + guard) + guard / 4
+            a, b = (1 - al) ** 2 / n, (1 + al) ** 2
+            deg = deg_last if j == k else deg_mid
+        pol = make_invpow(p, a, b, deg)
+        # |x P(x)^(1/p) - 1|: P ~ x^-p within relative e  ->  x P^(1/p) within ~ e/p
+        prev_alpha = pol["max_err"] / p
+        pol["alpha_out"] = prev_alpha
+        inv.append(pol)
+    polys["inv"] = inv
+    return polys
+
+
+CONFIGS = {
+    # config 1 (TOY12): n = 16, M = 2, k = 1 (forced), Alg 1
+    "toy_n16_M2_k1_A": dict(n=16, M=2, k=1, variant="A", deg_exp=7, deg_first=15, deg_mid=15, deg_last=15),
+    # toy with two iterations (exercises first/last split) -- parity only
+    "toy_n16_M4_k2_A": dict(n=16, M=4, k=2, variant="A", deg_exp=7, deg_first=7, deg_mid=7, deg_last=31),
+    "toy_n16_M4_k2_B": dict(n=16, M=4, k=2, variant="B", deg_exp=7, deg_first=7, deg_mid=7, deg_last=31),
+    # P16 configs 2-4 (n=256/128, M=128, k=5)
+    "p16_n256_M128_k5_A": dict(n=256, M=128, k=5, variant="A", deg_exp=15, deg_first=63, deg_mid=31, deg_last=127),
+    "p16_n256_M128_k5_B": dict(n=256, M=128, k=5, variant="B", deg_exp=15, deg_first=63, deg_mid=31, deg_last=127),
+    "p16_n128_M128_k5_B": dict(n=128, M=128, k=5, variant="B", deg_exp=15, deg_first=63, deg_mid=31, deg_last=127),
+}
+
+
+def main(out_path=None):
+    out_path = out_path or os.path.join(os.path.dirname(__file__), "..", "data", "poly_tables.json")
+    tables = {}
+    for name, cfg in CONFIGS.items():
+        t = softmax_tables(**cfg)
+        t["config"] = cfg
+        tables[name] = t
+        print(name, "exp", round(t["exp"]["log2_err"], 1),
+              "inv", [round(p["log2_err"], 1) for p in t["inv"]], file=sys.stderr)
+    with open(out_path, "w") as fh:
+        json.dump(tables, fh, indent=1)
+    return tables
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,96 @@
+"""Seeded synthetic inputs and parameter presets shared by the tests, the
+oracle harness and bench.py.
+
+This module holds NO arithmetic of the method: only parameter *data*
+(prime bit sizes, anchors), the synthetic input distribution of the paper's
+experiments (PAPER.md 466-475: x ~ N(-M/2, (M/6)^2) tail-cut to [-M, 0] by
+resampling, G17) and the seed derivation.  Both the CUDA path and
+the oracle consume what it produces; neither imports the other.
+"""
+from __future__ import annotations
+
+import json
+import os
+
+import numpy as np
+
+BASE_SEED = 0x241011184
+_DATA = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "data")
+
+
+def _anchors(n_q, pairs):
+    a = [0] * n_q
+    for lvl, v in pairs:
+        a[lvl] = v
+    return a
+
+
+# Parameter presets.  q_bits[l] is the bit size of
+# q_l (level l), p_bits the special primes; log2_anchor[l] != 0 pins the
+# canonical scale of level l to 2^anchor (C12), 0 = derived by Delta^2/q.
+PRESETS = {
+    # tiny ring for big-integer pins of the oracle (N = 32, insecure)
+    "TINY": dict(log_n=5, q_bits=[60, 40, 40, 40], p_bits=[61], alpha=1,
+                 log2_anchor=_anchors(4, [(3, 40)]), h=8),
+    # config 1: N = 2^12, 16 Q limbs, 2 special primes (alpha = 2), no BTS (insecure toy)
+    "TOY12": dict(log_n=12, q_bits=[60] + [40] * 15, p_bits=[61, 61], alpha=2,
+                  log2_anchor=_anchors(16, [(15, 40)]), h=192),
+    # N = 2^12 with a deep chain (28 Q limbs): toy Softmax with k = 2 (parity only)
+    "TOY12D": dict(log_n=12, q_bits=[60] + [40] * 27, p_bits=[61, 61, 61], alpha=3,
+                   log2_anchor=_anchors(28, [(27, 40)]), h=192),
+    # configs 2-5: N = 2^16, FGb-shaped.  Levels: 0 (60b), 1-12 user (40b, Delta=2^40),
+    # 13-15 SlotToCoeff (48b), 16-25 EvalMod (58b), 26-28 CoeffToSlot (58b);
+    # 5 special primes of 61 bits (alpha = 5, dnum = 6).
+    "P16": dict(log_n=16, q_bits=[60] + [40] * 12 + [48] * 3 + [58] * 10 + [58] * 3, p_bits=[61] * 5, alpha=5,
+                log2_anchor=_anchors(29, [(28, 58), (27, 58), (26, 58), (25, 58), (14, 48), (13, 48), (12, 40)]),
+                h=192),
+    # N = 2^16 with only the user chain (levels 0-12): primitive parity and
+    # key-switch measurements at the user levels without BTS-sized keys.
+    "P16U": dict(log_n=16, q_bits=[60] + [40] * 12, p_bits=[61] * 5, alpha=5,
+                 log2_anchor=_anchors(13, [(12, 40)]), h=192),
+}
+
+
+def preset(name: str) -> dict:
+    return dict(PRESETS[name])
+
+
+def derive_seed(*parts) -> int:
+    """Deterministic 64-bit seed from the base seed and a tag path (SplitMix64)."""
+    x = BASE_SEED
+    for p in parts:
+        v = p if isinstance(p, int) else int.from_bytes(str(p).encode()[:8].ljust(8, b"\0"), "little")
+        x = (x ^ v) & 0xFFFFFFFFFFFFFFFF
+        x = (x + 0x9E3779B97F4A7C15) & 0xFFFFFFFFFFFFFFFF
+        z = x
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & 0xFFFFFFFFFFFFFFFF
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & 0xFFFFFFFFFFFFFFFF
+        x = z ^ (z >> 31)
+    return x
+
+
+def softmax_inputs(L: int, n: int, M: float, seed: int, dist: str = "normal") -> np.ndarray:
+    """L Softmax inputs of dimension n in [-M, 0] (PAPER.md 466-475)."""
+    rng = np.random.default_rng(seed)
+    if dist == "uniform":
+        return rng.uniform(-M, 0.0, size=(L, n))
+    x = rng.normal(-M / 2, M / 6, size=(L, n))
+    bad = (x < -M) | (x > 0)
+    while bad.any():
+        x[bad] = rng.normal(-M / 2, M / 6, size=int(bad.sum()))
+        bad = (x < -M) | (x > 0)
+    return x
+
+
+def poly_tables() -> dict:
+    with open(os.path.join(_DATA, "poly_tables.json")) as fh:
+        return json.load(fh)
+
+
+# Softmax workloads of BASELINE.json's configs
+WORKLOADS = {
+    "config1": dict(preset="TOY12", n=16, L=128, m=1, M=2.0, k=1, variant="A", table="toy_n16_M2_k1_A"),
+    "config2": dict(preset="P16", n=256, L=128, m=1, M=128.0, k=5, variant="A", table="p16_n256_M128_k5_A"),
+    "config3": dict(preset="P16", n=256, L=8192, m=64, M=128.0, k=5, variant="B", table="p16_n256_M128_k5_B"),
+    "config4": dict(preset="P16", n=128, L=4096, m=16, M=128.0, k=5, variant="B", table="p16_n128_M128_k5_B"),
+}

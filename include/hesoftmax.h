@@ -1,0 +1,216 @@
+/*
+ * hesoftmax.h -- C ABI of the B200-native RNS-CKKS Softmax library
+ * (libhesoftmax.so, built from paper_2410_11184_b200/csrc).
+ *
+ * The calls follow the paper's problem statement (arXiv 2410.11184,
+ * PAPER.md):
+ *   - CKKS functionalities KeyGen / Enc / Dec / Add / Mult / Rot
+ *     (PAPER.md 262-271, sec 2.2.1);
+ *   - Softmax of x in [-M, 0]^n with parameter k (PAPER.md 688-691, 776-787);
+ *   - L Softmax packed in one ciphertext (PAPER.md 94-111, sec 4.1) or in m
+ *     ciphertexts with one shared auxiliary ciphertext (PAPER.md 113-131,
+ *     sec 4.2), Alg 1 or version B (PAPER.md 168-181).
+ * Every convention the paper leaves open (primes, NTT order, randomness,
+ * key switching, rescale rounding, scales, polynomial evaluation tree,
+ * schedule) is fixed in DESIGN.md (C1-C15, G1-G23); results are
+ * word-for-word identical to the CPU oracle under those conventions.
+ *
+ * Conventions of this header:
+ *   - No C++ exception crosses the ABI; every call returns hs_status.
+ *     On failure hs_last_error() (thread-local) describes the cause and
+ *     *out parameters are left untouched.
+ *   - Handles are opaque and freed by the matching *_destroy (NULL is a no-op).
+ *   - "stream" is a cudaStream_t passed as void* (NULL = legacy default
+ *     stream).  Device work is enqueued on it; calls that return host data
+ *     synchronise that stream.
+ *   - Ciphertext words are uint64 residues in [0, q_i), limb-major
+ *     [component][limb][N], NTT (evaluation) domain: limb i of a level-l
+ *     ciphertext is reduced mod q_i, i = 0..l.
+ *   - Plaintext words (encode output, decrypt output) are coefficient-domain
+ *     residues [limb][N].
+ *   - The scale of a ciphertext is implicit: the canonical scale of its
+ *     level (C12, hs_params_scale).
+ */
+#ifndef HESOFTMAX_H
+#define HESOFTMAX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    HS_OK = 0,
+    HS_EINVAL = 1,     /* bad argument, inconsistent sizes, packing not divisible */
+    HS_ELEVEL = 2,     /* the planned schedule does not fit the modulus chain     */
+    HS_EKEY = 3,       /* a required rotation / relinearisation key is missing    */
+    HS_ESCALE = 4,     /* scale mismatch                                          */
+    HS_EOVERFLOW = 5,  /* |round(Delta v)| too large for the modulus              */
+    HS_EDOMAIN = 6,    /* debug: decrypted intermediate outside its interval       */
+    HS_ENOMEM = 7,
+    HS_ECUDA = 8,
+    HS_ENCCL = 9       /* collective (exchange callback) failure                  */
+} hs_status;
+
+typedef struct hs_params hs_params;   /* host tables (primes, twiddles, BConv)  */
+typedef struct hs_ctx hs_ctx;         /* one GPU: device tables, pools, ledger  */
+typedef struct hs_keys hs_keys;       /* secret, public and evaluation keys     */
+typedef struct hs_ct hs_ct;           /* a device ciphertext                    */
+
+/* Last error message of the calling thread ("" if none). */
+const char *hs_last_error(void);
+
+/* ------------------------------------------------------------ parameters */
+/* q_bits[l]: bit size of q_l (sized primes) or the target size (derived
+ * primes); p_bits[k]: special primes; alpha: primes per key-switching digit;
+ * log2_anchor[l] != 0 pins Delta_l = 2^anchor (top level must be anchored).
+ * Prime selection is DESIGN.md C1, psi C2, canonical scales C12.
+ * HS_EINVAL if sizes are inconsistent or no prime can be found. */
+typedef struct {
+    int log_n;
+    int n_q;
+    const int *q_bits;
+    int n_p;
+    const int *p_bits;
+    int alpha;
+    const int *log2_anchor;
+} hs_params_desc;
+
+hs_status hs_ckks_params(const hs_params_desc *d, hs_params **out);
+void hs_params_destroy(hs_params *p);
+int hs_params_log_n(const hs_params *p);
+int hs_params_n_q(const hs_params *p);
+int hs_params_n_p(const hs_params *p);
+/* out: n_q + n_p primes, Q primes first. */
+hs_status hs_params_primes(const hs_params *p, uint64_t *out);
+uint64_t hs_params_psi(const hs_params *p, int prime_index);
+double hs_params_scale(const hs_params *p, int level);
+/* Galois element 5^r mod 2N of a left rotation by r slots (G1). */
+int hs_galois_of_rot(const hs_params *p, int r);
+
+/* ------------------------------------------------------------ context */
+hs_status hs_context_create(const hs_params *p, int device, hs_ctx **out);
+void hs_context_destroy(hs_ctx *c);
+
+/* ------------------------------------------------------------ keys (C5-C7) */
+/* Keys are generated on the device from the counter-based ChaCha20 stream of
+ * DESIGN.md C5 keyed by `seed`: secret with Hamming weight h, public key,
+ * relinearisation key (if relin != 0) and one switching key per Galois
+ * element in galois[0..n_galois).  Immutable after creation. */
+hs_status hs_ckks_keygen(hs_ctx *c, uint64_t seed, int h, const int32_t *galois, size_t n_galois,
+                         int relin, void *stream, hs_keys **out);
+void hs_keys_destroy(hs_keys *k);
+/* Test hooks: copy a switching key ([dnum][2][n_q+n_p][N], galois 0 = relin)
+ * or the secret (N int64 coefficients) to host memory.  HS_EKEY if absent. */
+hs_status hs_keys_export_swk(hs_ctx *c, const hs_keys *k, int galois, uint64_t *host_out);
+hs_status hs_keys_export_secret(hs_ctx *c, const hs_keys *k, int64_t *host_out);
+
+/* ------------------------------------------------------------ encode / decode (C4) */
+/* Canonical-embedding encode of n_slots = N/2 complex slots (im may be NULL)
+ * at `scale`, coefficients rounded half-even from a quad-precision
+ * evaluation; out = (level+1) x N coefficient residues (host). */
+hs_status hs_ckks_encode(const hs_params *p, const double *re, const double *im, size_t n_slots,
+                         int level, double scale, uint64_t *out);
+/* Decode the q_0 residues (N coefficients, centred) at `scale`. */
+hs_status hs_ckks_decode(const hs_params *p, const uint64_t *q0_coeffs, double scale, double *re,
+                         double *im, size_t n_slots);
+/* Packing (PAPER.md 94-131): x[L][n] (row-major) into m
+ * slot vectors of N0 = N/2 (row-major [m][N0]); padding lanes hold x = 0 (G9).
+ * HS_EINVAL unless n % m == 0, n/m a power of two <= N0 and L <= N0 m / n. */
+hs_status hs_pack(const double *x, size_t L, size_t n, size_t m, size_t n0, double *slots);
+hs_status hs_unpack(const double *slots, size_t L, size_t n, size_t m, size_t n0, double *x);
+
+/* ------------------------------------------------------------ encrypt / decrypt (C6) */
+/* pt: (level+1) x N coefficient residues in host memory.  use_sk != 0 selects
+ * secret-key encryption (tests).  Randomness: C5 stream keyed by (seed,
+ * ct_index). */
+hs_status hs_ckks_encrypt(hs_ctx *c, const hs_keys *k, const uint64_t *pt, int level, uint64_t seed,
+                          uint64_t ct_index, int use_sk, void *stream, hs_ct **out);
+/* m = c0 + c1 s (coefficient residues, (level+1) x N, host). */
+hs_status hs_ckks_decrypt(hs_ctx *c, const hs_keys *k, const hs_ct *ct, uint64_t *host_out, void *stream);
+
+/* ------------------------------------------------------------ ciphertexts */
+/* words: ncomp x (level+1) x N uint64, on the device if on_device else host. */
+hs_status hs_ct_import(hs_ctx *c, int level, int ncomp, const uint64_t *words, int on_device, void *stream,
+                       hs_ct **out);
+hs_status hs_ct_export(hs_ctx *c, const hs_ct *ct, uint64_t *words, int on_device, void *stream);
+int hs_ct_level(const hs_ct *ct);
+int hs_ct_ncomp(const hs_ct *ct);
+void hs_ct_destroy(hs_ct *ct);
+
+/* ------------------------------------------------------------ scheme operations */
+typedef enum {
+    HS_OP_ADD = 0, HS_OP_SUB = 1,
+    HS_OP_MULT = 2,        /* tensor -> relin -> rescale (C8)                    */
+    HS_OP_TENSOR = 3, HS_OP_RELIN = 4, HS_OP_RESCALE = 5,
+    HS_OP_LEVEL_DOWN = 6,  /* i = target level (C12 landing)                      */
+    HS_OP_MULT_CONST = 7,  /* c = real constant, i = target level                 */
+    HS_OP_ADD_CONST = 8,   /* c = real constant                                   */
+    HS_OP_MULT_INT = 9,    /* i = integer                                         */
+    HS_OP_ROTATE = 10,     /* i = left rotation (G1)                              */
+    HS_OP_CONJ = 11,
+    HS_OP_GALOIS = 12      /* i = Galois element                                  */
+} hs_op_code;
+
+hs_status hs_op(hs_ctx *c, const hs_keys *k, int op, const hs_ct *a, const hs_ct *b, double cst, int i,
+                void *stream, hs_ct **out);
+/* slot-vector multiply landing at level `target` (C12). */
+hs_status hs_mult_pt(hs_ctx *c, const hs_ct *a, const double *re, const double *im, int target, void *stream,
+                     hs_ct **out);
+/* Hybrid key switch of one (level+1)-limb polynomial (device pointers). */
+hs_status hs_keyswitch(hs_ctx *c, const hs_keys *k, int galois, int level, const uint64_t *d,
+                       uint64_t *out0, uint64_t *out1, void *stream);
+/* Forward / inverse negacyclic NTT (C3) of n_limbs consecutive device limbs,
+ * limb j reduced mod prime (prime_index + j). */
+hs_status hs_ntt(hs_ctx *c, int prime_index, int n_limbs, uint64_t *data, int inverse, void *stream);
+
+/* ------------------------------------------------------------ polynomials (C13) */
+typedef struct {
+    int deg;
+    double a, b;            /* interval; Chebyshev variable u = (2x-a-b)/(b-a) */
+    const double *coeffs;   /* deg+1 Chebyshev coefficients                     */
+} hs_poly;
+
+hs_status hs_cheb(hs_ctx *c, const hs_keys *k, const hs_ct *x, const hs_poly *p, void *stream, hs_ct **out);
+int hs_cheb_depth(int deg);
+
+/* ------------------------------------------------------------ Softmax */
+/* Exchange callback for the sharded many-ciphertext case:
+ * called with the device buffer of this rank's partial aux sum (`words`
+ * uint64 per rank) and must leave in `gathered` (world * words uint64,
+ * device) the partial sums of all ranks in rank order, e.g. an NCCL
+ * all-gather issued by the caller on `stream`.  Return 0 on success. */
+typedef int (*hs_exchange_fn)(void *user, const uint64_t *partial, uint64_t *gathered, size_t words,
+                              void *stream);
+
+typedef struct {
+    int n;                    /* Softmax dimension                                  */
+    int m;                    /* GLOBAL number of main-thread ciphertexts (1: one-ctxt) */
+    int k;                    /* iterations (PAPER.md 821)                          */
+    int variant;              /* 0 = Alg 1, 1 = version B                           */
+    const hs_poly *exp_poly;  /* exp(x/2^k) on [-M, 0]                              */
+    const hs_poly *inv_poly;  /* k polynomials (x^-1/2, or x^-1/2^j for version B)  */
+    int world, rank;          /* sharding of the m ciphertexts (1, 0 = one GPU)     */
+    hs_exchange_fn exchange;  /* required when world > 1                            */
+    void *exchange_user;
+} hs_softmax_desc;
+
+/* One ciphertext (m = 1). */
+hs_status hs_softmax_one_ctxt(hs_ctx *c, const hs_keys *k, const hs_softmax_desc *d, const hs_ct *in,
+                              void *stream, hs_ct **out);
+/* m_local = m / world ciphertexts of this rank (contiguous shard). */
+hs_status hs_softmax_many_ctxt(hs_ctx *c, const hs_keys *k, const hs_softmax_desc *d, const hs_ct *const *in,
+                               size_t m_local, void *stream, hs_ct **out);
+
+/* ------------------------------------------------------------ ledger (D8) */
+enum { HS_LG_HMULT, HS_LG_TENSOR, HS_LG_KS, HS_LG_ROT, HS_LG_RESCALE, HS_LG_CMULT, HS_LG_PMULT,
+       HS_LG_LEVELDOWN, HS_LG_BTS, HS_LG_NTT, HS_LG_KERNELS, HS_LG_COUNT };
+hs_status hs_ledger_get(hs_ctx *c, int64_t *out, int n);
+hs_status hs_ledger_reset(hs_ctx *c);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,274 @@
+"""B200-native RNS-CKKS Softmax (arXiv 2410.11184) -- Python binding.
+
+Same names as the C ABI in include/hesoftmax.h; this layer only marshals
+arguments.  PyTorch supplies streams (``torch.cuda.current_stream()``) and,
+for the sharded many-ciphertext case, the process group that performs the
+all-gather of partial aux sums.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib as L
+from ._lib import HsError, check
+
+__all__ = ["Params", "Context", "Keys", "Ciphertext", "HsError", "softmax_one_ctxt", "softmax_many_ctxt"]
+
+
+def _stream(stream):
+    if stream is None:
+        try:
+            import torch
+            if torch.cuda.is_available():
+                return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        except ImportError:
+            pass
+        return None
+    if isinstance(stream, int):
+        return C.c_void_p(stream)
+    return C.c_void_p(stream.cuda_stream)
+
+
+def _ints(v):
+    a = (C.c_int * len(v))(*v)
+    return a
+
+
+class Params:
+    """hs_ckks_params: primes (C1), psi (C2), canonical scales (C12)."""
+
+    def __init__(self, log_n, q_bits, p_bits, alpha, log2_anchor, **_):
+        self._keep = [_ints(q_bits), _ints(p_bits), _ints(log2_anchor)]
+        d = L.ParamsDesc(log_n, len(q_bits), self._keep[0], len(p_bits), self._keep[1], alpha, self._keep[2])
+        out = C.c_void_p()
+        check(L.hs_ckks_params(C.byref(d), C.byref(out)))
+        self.ptr = out
+        self.log_n, self.n = log_n, 1 << log_n
+        self.n_q, self.n_p, self.alpha = len(q_bits), len(p_bits), alpha
+        self.dnum = (self.n_q + alpha - 1) // alpha
+        pr = np.zeros(self.n_q + self.n_p, np.uint64)
+        check(L.hs_params_primes(self.ptr, pr))
+        self.primes = [int(x) for x in pr]
+
+    @classmethod
+    def from_preset(cls, pre):
+        return cls(**pre)
+
+    def __del__(self):
+        if getattr(self, "ptr", None):
+            L.hs_params_destroy(self.ptr)
+            self.ptr = None
+
+    def psi(self, i):
+        return int(L.hs_params_psi(self.ptr, i))
+
+    def scale(self, level):
+        return float(L.hs_params_scale(self.ptr, level))
+
+    def galois_of_rot(self, r):
+        return int(L.hs_galois_of_rot(self.ptr, r))
+
+    def encode(self, re, im=None, scale=None, level=0):
+        re = np.ascontiguousarray(re, np.float64)
+        imp = None if im is None else np.ascontiguousarray(im, np.float64)
+        out = np.zeros((level + 1) * self.n, np.uint64)
+        check(L.hs_ckks_encode(self.ptr, re, None if imp is None else imp.ctypes.data_as(C.c_void_p),
+                               len(re), level, scale, out))
+        return out.reshape(level + 1, self.n)
+
+    def decode(self, q0_coeffs, scale):
+        re, im = np.zeros(self.n // 2), np.zeros(self.n // 2)
+        check(L.hs_ckks_decode(self.ptr, np.ascontiguousarray(q0_coeffs, np.uint64), scale, re, im, self.n // 2))
+        return re + 1j * im
+
+    def pack(self, x, m):
+        x = np.ascontiguousarray(x, np.float64)
+        Lx, n = x.shape
+        out = np.zeros(m * self.n // 2)
+        check(L.hs_pack(x.ravel(), Lx, n, m, self.n // 2, out))
+        return out.reshape(m, self.n // 2)
+
+    def unpack(self, slots, Lx, n):
+        slots = np.ascontiguousarray(slots, np.float64)
+        m = slots.shape[0]
+        out = np.zeros(Lx * n)
+        check(L.hs_unpack(slots.ravel(), Lx, n, m, self.n // 2, out))
+        return out.reshape(Lx, n)
+
+
+class Context:
+    def __init__(self, params: Params, device: int = 0):
+        self.params = params
+        out = C.c_void_p()
+        check(L.hs_context_create(params.ptr, device, C.byref(out)))
+        self.ptr = out
+
+    def __del__(self):
+        if getattr(self, "ptr", None):
+            L.hs_context_destroy(self.ptr)
+            self.ptr = None
+
+    def ledger(self):
+        a = (C.c_int64 * len(L.LEDGER))()
+        check(L.hs_ledger_get(self.ptr, a, len(L.LEDGER)))
+        return dict(zip(L.LEDGER, list(a)))
+
+    def ledger_reset(self):
+        check(L.hs_ledger_reset(self.ptr))
+
+    def ntt(self, data_ptr, prime_index, n_limbs, inverse=False, stream=None):
+        check(L.hs_ntt(self.ptr, prime_index, n_limbs, C.c_void_p(data_ptr), 1 if inverse else 0, _stream(stream)))
+
+
+class Keys:
+    def __init__(self, ctx: Context, seed: int, h: int, galois=(), relin=True, stream=None):
+        self.ctx = ctx
+        g = np.array(list(galois) or [0], np.int32)
+        out = C.c_void_p()
+        check(L.hs_ckks_keygen(ctx.ptr, seed, h, g, len(galois), 1 if relin else 0, _stream(stream), C.byref(out)))
+        self.ptr = out
+
+    def __del__(self):
+        if getattr(self, "ptr", None):
+            L.hs_keys_destroy(self.ptr)
+            self.ptr = None
+
+    def swk(self, galois):
+        P = self.ctx.params
+        o = np.zeros(P.dnum * 2 * (P.n_q + P.n_p) * P.n, np.uint64)
+        check(L.hs_keys_export_swk(self.ctx.ptr, self.ptr, galois, o))
+        return o.reshape(P.dnum, 2, P.n_q + P.n_p, P.n)
+
+    def secret(self):
+        s = np.zeros(self.ctx.params.n, np.int64)
+        check(L.hs_keys_export_secret(self.ctx.ptr, self.ptr, s))
+        return s
+
+
+class Ciphertext:
+    def __init__(self, ctx: Context, ptr):
+        self.ctx, self.ptr = ctx, ptr
+
+    def __del__(self):
+        if getattr(self, "ptr", None):
+            L.hs_ct_destroy(self.ptr)
+            self.ptr = None
+
+    @property
+    def level(self):
+        return L.hs_ct_level(self.ptr)
+
+    @property
+    def ncomp(self):
+        return L.hs_ct_ncomp(self.ptr)
+
+    def words(self, stream=None):
+        P = self.ctx.params
+        w = np.zeros(self.ncomp * (self.level + 1) * P.n, np.uint64)
+        check(L.hs_ct_export(self.ctx.ptr, self.ptr, w.ctypes.data_as(C.c_void_p), 0, _stream(stream)))
+        return w.reshape(self.ncomp, self.level + 1, P.n)
+
+    @classmethod
+    def from_words(cls, ctx, words, stream=None):
+        words = np.ascontiguousarray(words, np.uint64)
+        nc, l1, _ = words.shape
+        out = C.c_void_p()
+        check(L.hs_ct_import(ctx.ptr, l1 - 1, nc, words.ctypes.data_as(C.c_void_p), 0, _stream(stream),
+                             C.byref(out)))
+        return cls(ctx, out)
+
+
+def encrypt(keys: Keys, pt, level, seed, idx, use_sk=False, stream=None) -> Ciphertext:
+    out = C.c_void_p()
+    check(L.hs_ckks_encrypt(keys.ctx.ptr, keys.ptr, np.ascontiguousarray(pt, np.uint64).ravel(), level, seed, idx,
+                            1 if use_sk else 0, _stream(stream), C.byref(out)))
+    return Ciphertext(keys.ctx, out)
+
+
+def decrypt(keys: Keys, ct: Ciphertext, stream=None):
+    P = keys.ctx.params
+    o = np.zeros((ct.level + 1) * P.n, np.uint64)
+    check(L.hs_ckks_decrypt(keys.ctx.ptr, keys.ptr, ct.ptr, o, _stream(stream)))
+    return o.reshape(ct.level + 1, P.n)
+
+
+def decrypt_decode(keys: Keys, ct: Ciphertext, stream=None):
+    P = keys.ctx.params
+    m = decrypt(keys, ct, stream)
+    return P.decode(m[0], P.scale(ct.level))
+
+
+def op(keys, name, a: Ciphertext, b: Ciphertext = None, c=0.0, i=0, stream=None) -> Ciphertext:
+    ctx = a.ctx
+    out = C.c_void_p()
+    check(L.hs_op(ctx.ptr, keys.ptr if keys is not None else None, L.OPS[name], a.ptr,
+                  b.ptr if b is not None else None, float(c), int(i), _stream(stream), C.byref(out)))
+    return Ciphertext(ctx, out)
+
+
+def mult_pt(a: Ciphertext, re, im=None, target=None, stream=None) -> Ciphertext:
+    re = np.ascontiguousarray(re, np.float64)
+    imp = None if im is None else np.ascontiguousarray(im, np.float64)
+    out = C.c_void_p()
+    check(L.hs_mult_pt(a.ctx.ptr, a.ptr, re, None if imp is None else imp.ctypes.data_as(C.c_void_p),
+                       a.level - 1 if target is None else target, _stream(stream), C.byref(out)))
+    return Ciphertext(a.ctx, out)
+
+
+def keyswitch(keys: Keys, galois, level, d_ptr, out0_ptr, out1_ptr, stream=None):
+    check(L.hs_keyswitch(keys.ctx.ptr, keys.ptr, galois, level, C.c_void_p(d_ptr), C.c_void_p(out0_ptr),
+                         C.c_void_p(out1_ptr), _stream(stream)))
+
+
+def _poly(p):
+    c = np.ascontiguousarray(p["coeffs"], np.float64)
+    return L.Poly(len(c) - 1, float(p["a"]), float(p["b"]), c.ctypes.data_as(C.POINTER(C.c_double))), c
+
+
+def cheb(keys: Keys, x: Ciphertext, poly, stream=None) -> Ciphertext:
+    pp, keep = _poly(poly)
+    out = C.c_void_p()
+    check(L.hs_cheb(keys.ctx.ptr, keys.ptr, x.ptr, C.byref(pp), _stream(stream), C.byref(out)))
+    return Ciphertext(x.ctx, out)
+
+
+def cheb_depth(deg):
+    return int(L.hs_cheb_depth(deg))
+
+
+def _softmax_desc(n, m, k, variant, exp_poly, inv_polys, world=1, rank=0, exchange=None):
+    keep = []
+    e, c = _poly(exp_poly)
+    keep.append(c)
+    arr = (L.Poly * len(inv_polys))()
+    for i, p in enumerate(inv_polys):
+        pp, c = _poly(p)
+        keep.append(c)
+        arr[i] = pp
+    ep = (L.Poly * 1)(e)
+    keep += [arr, ep]
+    fn = L.EXCHANGE_FN(0) if exchange is None else exchange
+    keep.append(fn)
+    d = L.SoftmaxDesc(n, m, k, 0 if variant in (0, "A") else 1, ep, arr, world, rank, fn, None)
+    return d, keep
+
+
+def softmax_one_ctxt(keys: Keys, ct: Ciphertext, n, k, variant, exp_poly, inv_polys, stream=None) -> Ciphertext:
+    d, keep = _softmax_desc(n, 1, k, variant, exp_poly, inv_polys)
+    out = C.c_void_p()
+    check(L.hs_softmax_one_ctxt(keys.ctx.ptr, keys.ptr, C.byref(d), ct.ptr, _stream(stream), C.byref(out)))
+    return Ciphertext(keys.ctx, out)
+
+
+def softmax_many_ctxt(keys: Keys, cts, n, m, k, variant, exp_poly, inv_polys, world=1, rank=0, exchange=None,
+                      stream=None):
+    """cts: this rank's m/world ciphertexts.  exchange: an EXCHANGE_FN (see
+    paper_2410_11184_b200.dist) when world > 1."""
+    d, keep = _softmax_desc(n, m, k, variant, exp_poly, inv_polys, world, rank, exchange)
+    ml = len(cts)
+    ins = (C.c_void_p * ml)(*[c.ptr.value if isinstance(c.ptr, C.c_void_p) else c.ptr for c in cts])
+    outs = (C.c_void_p * ml)()
+    check(L.hs_softmax_many_ctxt(keys.ctx.ptr, keys.ptr, C.byref(d), ins, ml, _stream(stream), outs))
+    return [Ciphertext(keys.ctx, C.c_void_p(outs[i])) for i in range(ml)]

@@ -1,0 +1,114 @@
+"""Thin ctypes binding of libhesoftmax.so (include/hesoftmax.h).
+
+Argument marshalling only: every step of the hot path runs in the library's
+CUDA kernels.  If the shared library is missing this module raises at import
+time -- there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhesoftmax.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} not built: run `make -C {_HERE}` or __graft_entry__.build()")
+
+_L = C.CDLL(LIB_PATH)
+
+vp = C.c_void_p
+u64p = np.ctypeslib.ndpointer(dtype=np.uint64, flags="C_CONTIGUOUS")
+i64p = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
+f64p = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+i32p = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")
+
+STATUS = ["HS_OK", "HS_EINVAL", "HS_ELEVEL", "HS_EKEY", "HS_ESCALE", "HS_EOVERFLOW", "HS_EDOMAIN",
+          "HS_ENOMEM", "HS_ECUDA", "HS_ENCCL"]
+OPS = dict(add=0, sub=1, mult=2, tensor=3, relin=4, rescale=5, level_down=6, mult_const=7, add_const=8,
+           mult_int=9, rotate=10, conj=11, galois=12)
+LEDGER = ["hmult", "tensor", "ks", "rot", "rescale", "cmult", "pmult", "leveldown", "bts", "ntt", "kernels"]
+
+
+class HsError(RuntimeError):
+    def __init__(self, code, msg):
+        self.code = code
+        super().__init__(f"{STATUS[code] if 0 <= code < len(STATUS) else code}: {msg}")
+
+
+class ParamsDesc(C.Structure):
+    _fields_ = [("log_n", C.c_int), ("n_q", C.c_int), ("q_bits", C.POINTER(C.c_int)), ("n_p", C.c_int),
+                ("p_bits", C.POINTER(C.c_int)), ("alpha", C.c_int), ("log2_anchor", C.POINTER(C.c_int))]
+
+
+class Poly(C.Structure):
+    _fields_ = [("deg", C.c_int), ("a", C.c_double), ("b", C.c_double), ("coeffs", C.POINTER(C.c_double))]
+
+
+EXCHANGE_FN = C.CFUNCTYPE(C.c_int, vp, vp, vp, C.c_size_t, vp)
+
+
+class SoftmaxDesc(C.Structure):
+    _fields_ = [("n", C.c_int), ("m", C.c_int), ("k", C.c_int), ("variant", C.c_int),
+                ("exp_poly", C.POINTER(Poly)), ("inv_poly", C.POINTER(Poly)), ("world", C.c_int),
+                ("rank", C.c_int), ("exchange", EXCHANGE_FN), ("exchange_user", vp)]
+
+
+def _sig(name, res, args):
+    f = getattr(_L, name)
+    f.restype = res
+    f.argtypes = args
+    return f
+
+
+hs_last_error = _sig("hs_last_error", C.c_char_p, [])
+hs_ckks_params = _sig("hs_ckks_params", C.c_int, [C.POINTER(ParamsDesc), C.POINTER(vp)])
+hs_params_destroy = _sig("hs_params_destroy", None, [vp])
+hs_params_log_n = _sig("hs_params_log_n", C.c_int, [vp])
+hs_params_n_q = _sig("hs_params_n_q", C.c_int, [vp])
+hs_params_n_p = _sig("hs_params_n_p", C.c_int, [vp])
+hs_params_primes = _sig("hs_params_primes", C.c_int, [vp, u64p])
+hs_params_psi = _sig("hs_params_psi", C.c_uint64, [vp, C.c_int])
+hs_params_scale = _sig("hs_params_scale", C.c_double, [vp, C.c_int])
+hs_galois_of_rot = _sig("hs_galois_of_rot", C.c_int, [vp, C.c_int])
+hs_context_create = _sig("hs_context_create", C.c_int, [vp, C.c_int, C.POINTER(vp)])
+hs_context_destroy = _sig("hs_context_destroy", None, [vp])
+hs_ckks_keygen = _sig("hs_ckks_keygen", C.c_int,
+                      [vp, C.c_uint64, C.c_int, i32p, C.c_size_t, C.c_int, vp, C.POINTER(vp)])
+hs_keys_destroy = _sig("hs_keys_destroy", None, [vp])
+hs_keys_export_swk = _sig("hs_keys_export_swk", C.c_int, [vp, vp, C.c_int, u64p])
+hs_keys_export_secret = _sig("hs_keys_export_secret", C.c_int, [vp, vp, i64p])
+hs_ckks_encode = _sig("hs_ckks_encode", C.c_int, [vp, f64p, vp, C.c_size_t, C.c_int, C.c_double, u64p])
+hs_ckks_decode = _sig("hs_ckks_decode", C.c_int, [vp, u64p, C.c_double, f64p, f64p, C.c_size_t])
+hs_pack = _sig("hs_pack", C.c_int, [f64p, C.c_size_t, C.c_size_t, C.c_size_t, C.c_size_t, f64p])
+hs_unpack = _sig("hs_unpack", C.c_int, [f64p, C.c_size_t, C.c_size_t, C.c_size_t, C.c_size_t, f64p])
+hs_ckks_encrypt = _sig("hs_ckks_encrypt", C.c_int,
+                       [vp, vp, u64p, C.c_int, C.c_uint64, C.c_uint64, C.c_int, vp, C.POINTER(vp)])
+hs_ckks_decrypt = _sig("hs_ckks_decrypt", C.c_int, [vp, vp, vp, u64p, vp])
+hs_ct_import = _sig("hs_ct_import", C.c_int, [vp, C.c_int, C.c_int, vp, C.c_int, vp, C.POINTER(vp)])
+hs_ct_export = _sig("hs_ct_export", C.c_int, [vp, vp, vp, C.c_int, vp])
+hs_ct_level = _sig("hs_ct_level", C.c_int, [vp])
+hs_ct_ncomp = _sig("hs_ct_ncomp", C.c_int, [vp])
+hs_ct_destroy = _sig("hs_ct_destroy", None, [vp])
+hs_op = _sig("hs_op", C.c_int, [vp, vp, C.c_int, vp, vp, C.c_double, C.c_int, vp, C.POINTER(vp)])
+hs_mult_pt = _sig("hs_mult_pt", C.c_int, [vp, vp, f64p, vp, C.c_int, vp, C.POINTER(vp)])
+hs_keyswitch = _sig("hs_keyswitch", C.c_int, [vp, vp, C.c_int, C.c_int, vp, vp, vp, vp])
+hs_ntt = _sig("hs_ntt", C.c_int, [vp, C.c_int, C.c_int, vp, C.c_int, vp])
+hs_cheb = _sig("hs_cheb", C.c_int, [vp, vp, vp, C.POINTER(Poly), vp, C.POINTER(vp)])
+hs_cheb_depth = _sig("hs_cheb_depth", C.c_int, [C.c_int])
+hs_softmax_one_ctxt = _sig("hs_softmax_one_ctxt", C.c_int,
+                           [vp, vp, C.POINTER(SoftmaxDesc), vp, vp, C.POINTER(vp)])
+hs_softmax_many_ctxt = _sig("hs_softmax_many_ctxt", C.c_int,
+                            [vp, vp, C.POINTER(SoftmaxDesc), C.POINTER(vp), C.c_size_t, vp, C.POINTER(vp)])
+hs_ledger_get = _sig("hs_ledger_get", C.c_int, [vp, C.POINTER(C.c_int64), C.c_int])
+hs_ledger_reset = _sig("hs_ledger_reset", C.c_int, [vp])
+
+# every symbol include/hesoftmax.h declares (checked by tests/test_abi.py)
+EXPORTED = [n for n in list(globals()) if n.startswith("hs_")]
+
+
+def check(rc):
+    if rc != 0:
+        raise HsError(rc, hs_last_error().decode())

@@ -1,0 +1,375 @@
+// capi.cpp -- the extern "C" boundary (include/hesoftmax.h).  No exception
+// crosses it: every entry point converts HsError / std::exception into an
+// hs_status and a thread-local message.
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "hs_internal.h"
+
+static thread_local std::string g_err;
+static std::mutex g_active_mu;
+static const hs_params *g_active = nullptr;
+
+#define HS_TRY try {
+#define HS_CATCH                                              \
+    }                                                         \
+    catch (const HsError &e) {                                \
+        g_err = e.what();                                     \
+        return e.code;                                        \
+    }                                                         \
+    catch (const std::bad_alloc &) {                          \
+        g_err = "host allocation failed";                     \
+        return HS_ENOMEM;                                     \
+    }                                                         \
+    catch (const std::exception &e) {                         \
+        g_err = e.what();                                     \
+        return HS_EINVAL;                                     \
+    }
+
+static cudaStream_t S(void *s) { return (cudaStream_t)s; }
+
+// The prime constants live in __constant__ memory of the module; make sure they
+// hold this context's parameter set before enqueueing work.
+static void activate(hs_ctx *c)
+{
+    std::lock_guard<std::mutex> g(g_active_mu);
+    HS_CUDA(cudaSetDevice(c->device));
+    if (g_active != c->P) {
+        HS_CUDA(cudaDeviceSynchronize());
+        upload_prime_constants(c->P);
+        g_active = c->P;
+    }
+}
+
+extern "C" {
+
+const char *hs_last_error(void) { return g_err.c_str(); }
+
+hs_status hs_ckks_params(const hs_params_desc *d, hs_params **out)
+{
+    HS_TRY
+    if (!out) throw HsError(HS_EINVAL, "out is NULL");
+    std::unique_ptr<hs_params> P(new hs_params);
+    hs_build_params(d, P.get());
+    *out = P.release();
+    return HS_OK;
+    HS_CATCH
+}
+
+void hs_params_destroy(hs_params *p)
+{
+    std::lock_guard<std::mutex> g(g_active_mu);
+    if (g_active == p) g_active = nullptr;
+    delete p;
+}
+int hs_params_log_n(const hs_params *p) { return p->log_n; }
+int hs_params_n_q(const hs_params *p) { return p->n_q; }
+int hs_params_n_p(const hs_params *p) { return p->n_p; }
+hs_status hs_params_primes(const hs_params *p, uint64_t *out)
+{
+    if (!p || !out) return HS_EINVAL;
+    memcpy(out, p->prime.data(), p->prime.size() * 8);
+    return HS_OK;
+}
+uint64_t hs_params_psi(const hs_params *p, int i) { return p->psi.at(i); }
+double hs_params_scale(const hs_params *p, int level) { return p->scale.at(level); }
+int hs_galois_of_rot(const hs_params *p, int r) { return hs_galois_elt(p, r); }
+
+hs_status hs_context_create(const hs_params *p, int device, hs_ctx **out)
+{
+    HS_TRY
+    if (!p || !out) throw HsError(HS_EINVAL, "NULL argument");
+    int ndev = 0;
+    HS_CUDA(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) throw HsError(HS_EINVAL, "no such CUDA device");
+    HS_CUDA(cudaSetDevice(device));
+    std::unique_ptr<hs_ctx> c(new hs_ctx);
+    c->P = p;
+    c->device = device;
+    const int np = p->n_q + p->n_p;
+    const size_t N = p->n;
+    std::vector<u64> h((size_t)np * 4 * N + 2 * np);
+    for (int i = 0; i < np; i++) memcpy(&h[(size_t)i * 4 * N], p->tw[i].data(), 4 * N * 8);
+    for (int i = 0; i < np; i++) {
+        h[(size_t)np * 4 * N + 2 * i] = p->n_inv[i];
+        h[(size_t)np * 4 * N + 2 * i + 1] = p->n_inv_sh[i];
+    }
+    HS_CUDA(cudaMalloc(&c->T.tw, h.size() * 8));
+    HS_CUDA(cudaMemcpy(c->T.tw, h.data(), h.size() * 8, cudaMemcpyHostToDevice));
+    // keep freed stream-ordered memory in the pool (no release back to the OS)
+    cudaMemPool_t pool;
+    HS_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = UINT64_MAX;
+    HS_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    activate(c.get());
+    *out = c.release();
+    return HS_OK;
+    HS_CATCH
+}
+
+void hs_context_destroy(hs_ctx *c) { delete c; }
+
+hs_status hs_ckks_keygen(hs_ctx *c, uint64_t seed, int h, const int32_t *galois, size_t n_galois, int relin,
+                         void *stream, hs_keys **out)
+{
+    HS_TRY
+    if (!c || !out || (n_galois && !galois)) throw HsError(HS_EINVAL, "NULL argument");
+    activate(c);
+    *out = keys_generate(c, seed, h, galois, n_galois, relin, S(stream));
+    return HS_OK;
+    HS_CATCH
+}
+
+void hs_keys_destroy(hs_keys *k) { delete k; }
+
+hs_status hs_keys_export_swk(hs_ctx *c, const hs_keys *k, int galois, uint64_t *host_out)
+{
+    HS_TRY
+    const SwKey *key = k->find(galois);
+    if (!key) throw HsError(HS_EKEY, "no such switching key");
+    const hs_params *P = c->P;
+    HS_CUDA(cudaDeviceSynchronize());
+    HS_CUDA(cudaMemcpy(host_out, key->k, (size_t)P->dnum * 2 * (P->n_q + P->n_p) * P->n * 8, cudaMemcpyDeviceToHost));
+    return HS_OK;
+    HS_CATCH
+}
+
+hs_status hs_keys_export_secret(hs_ctx *c, const hs_keys *k, int64_t *host_out)
+{
+    HS_TRY
+    memcpy(host_out, k->s_coeff.data(), k->s_coeff.size() * 8);
+    (void)c;
+    return HS_OK;
+    HS_CATCH
+}
+
+hs_status hs_ckks_encode(const hs_params *p, const double *re, const double *im, size_t n_slots, int level,
+                         double scale, uint64_t *out)
+{
+    HS_TRY
+    if (!p || !re || !out || n_slots != (size_t)p->n / 2 || level < 0 || level > p->L || !(scale > 0))
+        throw HsError(HS_EINVAL, "encode: bad arguments (n_slots must be N/2)");
+    double mx = 0;
+    for (size_t i = 0; i < n_slots; i++) {
+        mx = std::max(mx, std::fabs(re[i]));
+        if (im) mx = std::max(mx, std::fabs(im[i]));
+    }
+    double logq = 0;
+    for (int i = 0; i <= level; i++) logq += std::log2((double)p->prime[i]);
+    if (mx > 0 && (std::log2(mx * scale) + 1 >= logq || mx * scale >= 0x1p100))
+        throw HsError(HS_EOVERFLOW, "encode: |Delta v| too large for Q_level");
+    hs_encode_impl(p, re, im, scale, level, out);
+    return HS_OK;
+    HS_CATCH
+}
+
+hs_status hs_ckks_decode(const hs_params *p, const uint64_t *q0c, double scale, double *re, double *im, size_t n_slots)
+{
+    HS_TRY
+    if (!p || !q0c || !re || n_slots != (size_t)p->n / 2) throw HsError(HS_EINVAL, "decode: bad arguments");
+    hs_decode_impl(p, q0c, scale, re, im);
+    return HS_OK;
+    HS_CATCH
+}
+
+// PAPER.md 94-131 packing, unified: nb = n/m blocks per
+// ciphertext, stride = N0/nb; instance o, coordinate i -> ciphertext i / nb,
+// slot (i % nb) stride + o.
+static void check_pack(size_t L, size_t n, size_t m, size_t n0)
+{
+    if (!m || !n || n % m) throw HsError(HS_EINVAL, "pack: n must be a multiple of m");
+    size_t nb = n / m;
+    if ((nb & (nb - 1)) || nb > n0 || L > n0 / nb || L == 0) throw HsError(HS_EINVAL, "pack: sizes not divisible");
+}
+
+hs_status hs_pack(const double *x, size_t L, size_t n, size_t m, size_t n0, double *slots)
+{
+    HS_TRY
+    check_pack(L, n, m, n0);
+    size_t nb = n / m, stride = n0 / nb;
+    memset(slots, 0, m * n0 * 8);
+    for (size_t i = 0; i < n; i++)
+        for (size_t o = 0; o < L; o++) slots[(i / nb) * n0 + (i % nb) * stride + o] = x[o * n + i];
+    return HS_OK;
+    HS_CATCH
+}
+
+hs_status hs_unpack(const double *slots, size_t L, size_t n, size_t m, size_t n0, double *x)
+{
+    HS_TRY
+    check_pack(L, n, m, n0);
+    size_t nb = n / m, stride = n0 / nb;
+    for (size_t i = 0; i < n; i++)
+        for (size_t o = 0; o < L; o++) x[o * n + i] = slots[(i / nb) * n0 + (i % nb) * stride + o];
+    return HS_OK;
+    HS_CATCH
+}
+
+hs_status hs_ckks_encrypt(hs_ctx *c, const hs_keys *k, const uint64_t *pt, int level, uint64_t seed,
+                          uint64_t ct_index, int use_sk, void *stream, hs_ct **out)
+{
+    HS_TRY
+    if (!c || !k || !pt || !out) throw HsError(HS_EINVAL, "NULL argument");
+    activate(c);
+    *out = ev_encrypt(k, pt, level, seed, ct_index, use_sk != 0, S(stream)).release();
+    return HS_OK;
+    HS_CATCH
+}
+
+hs_status hs_ckks_decrypt(hs_ctx *c, const hs_keys *k, const hs_ct *ct, uint64_t *host_out, void *stream)
+{
+    HS_TRY
+    if (!c || !k || !ct || !host_out) throw HsError(HS_EINVAL, "NULL argument");
+    activate(c);
+    ev_decrypt(k, ct, host_out, S(stream));
+    return HS_OK;
+    HS_CATCH
+}
+
+hs_status hs_ct_import(hs_ctx *c, int level, int ncomp, const uint64_t *words, int on_device, void *stream,
+                       hs_ct **out)
+{
+    HS_TRY
+    if (!c || !words || !out || level < 0 || level > c->P->L || ncomp < 1 || ncomp > 3)
+        throw HsError(HS_EINVAL, "ct_import: bad arguments");
+    activate(c);
+    CtP r = ct_new(c, level, ncomp, S(stream));
+    HS_CUDA(cudaMemcpyAsync(r->d, words, r->limbs() * c->P->n * 8,
+                            on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, S(stream)));
+    if (!on_device) HS_CUDA(cudaStreamSynchronize(S(stream)));
+    *out = r.release();
+    return HS_OK;
+    HS_CATCH
+}
+
+hs_status hs_ct_export(hs_ctx *c, const hs_ct *ct, uint64_t *words, int on_device, void *stream)
+{
+    HS_TRY
+    if (!c || !ct || !words) throw HsError(HS_EINVAL, "NULL argument");
+    HS_CUDA(cudaMemcpyAsync(words, ct->d, ct->limbs() * c->P->n * 8,
+                            on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, S(stream)));
+    if (!on_device) HS_CUDA(cudaStreamSynchronize(S(stream)));
+    return HS_OK;
+    HS_CATCH
+}
+
+int hs_ct_level(const hs_ct *ct) { return ct->level; }
+int hs_ct_ncomp(const hs_ct *ct) { return ct->ncomp; }
+void hs_ct_destroy(hs_ct *ct) { delete ct; }
+
+hs_status hs_op(hs_ctx *c, const hs_keys *k, int op, const hs_ct *a, const hs_ct *b, double cst, int i, void *stream,
+                hs_ct **out)
+{
+    HS_TRY
+    if (!c || !a || !out) throw HsError(HS_EINVAL, "NULL argument");
+    activate(c);
+    cudaStream_t st = S(stream);
+    CtP r;
+    auto need_b = [&]() { if (!b) throw HsError(HS_EINVAL, "second operand missing"); };
+    auto need_k = [&]() { if (!k) throw HsError(HS_EKEY, "keys missing"); };
+    switch (op) {
+    case HS_OP_ADD: need_b(); r = ev_add(a, b, false, st); break;
+    case HS_OP_SUB: need_b(); r = ev_add(a, b, true, st); break;
+    case HS_OP_MULT: need_b(); need_k(); r = ev_mult(k, a, b, st); break;
+    case HS_OP_TENSOR: need_b(); r = ev_tensor(a, b, st); break;
+    case HS_OP_RELIN: need_k(); r = ev_relin(k, a, st); break;
+    case HS_OP_RESCALE: r = ev_rescale(a, st); break;
+    case HS_OP_LEVEL_DOWN: r = ev_level_down(a, i, st); break;
+    case HS_OP_MULT_CONST: r = ev_mult_const(a, cst, i, st); break;
+    case HS_OP_ADD_CONST: r = ev_add_const(a, cst, st); break;
+    case HS_OP_MULT_INT: r = ev_mult_int(a, i, st); break;
+    case HS_OP_ROTATE: need_k(); r = ev_rotate(k, a, i, st); break;
+    case HS_OP_CONJ: need_k(); r = ev_galois(k, a, 2 * c->P->n - 1, st); break;
+    case HS_OP_GALOIS: need_k(); r = ev_galois(k, a, i, st); break;
+    default: throw HsError(HS_EINVAL, "unknown op");
+    }
+    *out = r.release();
+    return HS_OK;
+    HS_CATCH
+}
+
+hs_status hs_mult_pt(hs_ctx *c, const hs_ct *a, const double *re, const double *im, int target, void *stream,
+                     hs_ct **out)
+{
+    HS_TRY
+    if (!c || !a || !re || !out) throw HsError(HS_EINVAL, "NULL argument");
+    activate(c);
+    *out = ev_mult_pt(a, re, im, target, S(stream)).release();
+    return HS_OK;
+    HS_CATCH
+}
+
+hs_status hs_keyswitch(hs_ctx *c, const hs_keys *k, int galois, int level, const uint64_t *d, uint64_t *out0,
+                       uint64_t *out1, void *stream)
+{
+    HS_TRY
+    if (!c || !k || !d || !out0 || !out1 || level < 0 || level > c->P->L) throw HsError(HS_EINVAL, "bad arguments");
+    const SwKey *key = k->find(galois);
+    if (!key) throw HsError(HS_EKEY, "no such switching key");
+    activate(c);
+    ev_keyswitch(k, key, level, d, out0, out1, nullptr, nullptr, S(stream));
+    return HS_OK;
+    HS_CATCH
+}
+
+hs_status hs_ntt(hs_ctx *c, int prime_index, int n_limbs, uint64_t *data, int inverse, void *stream)
+{
+    HS_TRY
+    if (!c || !data || prime_index < 0 || n_limbs < 1 || prime_index + n_limbs > c->P->n_q + c->P->n_p)
+        throw HsError(HS_EINVAL, "ntt: bad limb range");
+    activate(c);
+    k_ntt(c, data, n_limbs, pmap_range(prime_index, n_limbs), inverse != 0, S(stream));
+    return HS_OK;
+    HS_CATCH
+}
+
+hs_status hs_cheb(hs_ctx *c, const hs_keys *k, const hs_ct *x, const hs_poly *p, void *stream, hs_ct **out)
+{
+    HS_TRY
+    if (!c || !k || !x || !p || !out) throw HsError(HS_EINVAL, "NULL argument");
+    activate(c);
+    *out = ev_cheb(k, x, p, S(stream)).release();
+    return HS_OK;
+    HS_CATCH
+}
+
+int hs_cheb_depth(int deg) { return cheb_depth(deg); }
+
+hs_status hs_softmax_one_ctxt(hs_ctx *c, const hs_keys *k, const hs_softmax_desc *d, const hs_ct *in, void *stream,
+                              hs_ct **out)
+{
+    HS_TRY
+    if (!c || !k || !d || !in || !out) throw HsError(HS_EINVAL, "NULL argument");
+    if (d->m != 1) throw HsError(HS_EINVAL, "one_ctxt needs m = 1");
+    activate(c);
+    return softmax_run(c, k, d, &in, 1, S(stream), out);
+    HS_CATCH
+}
+
+hs_status hs_softmax_many_ctxt(hs_ctx *c, const hs_keys *k, const hs_softmax_desc *d, const hs_ct *const *in,
+                               size_t m_local, void *stream, hs_ct **out)
+{
+    HS_TRY
+    if (!c || !k || !d || !in || !out) throw HsError(HS_EINVAL, "NULL argument");
+    activate(c);
+    return softmax_run(c, k, d, in, m_local, S(stream), out);
+    HS_CATCH
+}
+
+hs_status hs_ledger_get(hs_ctx *c, int64_t *out, int n)
+{
+    if (!c || !out) return HS_EINVAL;
+    for (int i = 0; i < n && i < HS_LG_COUNT; i++) out[i] = c->ledger[i];
+    return HS_OK;
+}
+
+hs_status hs_ledger_reset(hs_ctx *c)
+{
+    if (!c) return HS_EINVAL;
+    memset(c->ledger, 0, sizeof(c->ledger));
+    return HS_OK;
+}
+
+}  // extern "C"

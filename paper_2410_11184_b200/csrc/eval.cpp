@@ -1,0 +1,542 @@
+// eval.cpp -- host orchestration of the CKKS evaluator on one GPU.
+//
+// Every operation follows the oracle's written conventions:
+//   C5 randomness, C6 Enc/Dec, C7 hybrid key switching, C8 HMult,
+//   C9 rescale, C10 rotations, C11 operand levels, C12 canonical scales.
+// Ciphertexts live in HBM limb-major [comp][limb][N], NTT domain; all
+// temporaries are stream-ordered (cudaMallocAsync) so an op enqueues work and
+// returns without synchronising.
+#include <math.h>
+
+#include <cstring>
+
+#include "hs_internal.h"
+
+enum { TAG_SK = 1, TAG_PK_A = 2, TAG_PK_E = 3, TAG_KSK_A = 4, TAG_KSK_E = 5,
+       TAG_ENC_V = 6, TAG_ENC_E0 = 7, TAG_ENC_E1 = 8, TAG_ENC_A = 9 };
+static const int ETA_ERR = 21, ETA_V = 1;
+
+// ------------------------------------------------------------------ memory
+u64 *dev_alloc(size_t words, cudaStream_t st)
+{
+    void *p = nullptr;
+    if (words == 0) words = 1;
+    cudaError_t e = cudaMallocAsync(&p, words * sizeof(u64), st);
+    if (e != cudaSuccess) throw HsError(e == cudaErrorMemoryAllocation ? HS_ENOMEM : HS_ECUDA,
+                                        std::string("cudaMallocAsync: ") + cudaGetErrorString(e));
+    return (u64 *)p;
+}
+
+void dev_free(void *p, cudaStream_t st)
+{
+    if (p) cudaFreeAsync(p, st);
+}
+
+hs_ctx::~hs_ctx()
+{
+    cudaDeviceSynchronize();
+    for (auto &kv : bconv) cudaFree(kv.second.dev);
+    for (auto &kv : galois_perm) cudaFree(kv.second);
+    cudaFree(T.tw);
+}
+
+hs_keys::~hs_keys()
+{
+    cudaDeviceSynchronize();
+    cudaFree(s_ntt);
+    cudaFree(pk);
+    for (auto &k : swk) cudaFree(k.k);
+}
+
+hs_ct::~hs_ct()
+{
+    if (d) dev_free(d, st);
+}
+
+u64 *hs_ct::limb(int comp, int i) const { return d + ((size_t)comp * (level + 1) + i) * ctx->P->n; }
+
+CtP ct_new(hs_ctx *c, int level, int ncomp, cudaStream_t st)
+{
+    CtP r(new hs_ct);
+    r->ctx = c;
+    r->level = level;
+    r->ncomp = ncomp;
+    r->st = st;
+    r->d = dev_alloc((size_t)ncomp * (level + 1) * c->P->n, st);
+    return r;
+}
+
+CtP ct_copy(const hs_ct *a, cudaStream_t st)
+{
+    CtP r = ct_new(a->ctx, a->level, a->ncomp, st);
+    HS_CUDA(cudaMemcpyAsync(r->d, a->d, a->limbs() * a->ctx->P->n * 8, cudaMemcpyDeviceToDevice, st));
+    return r;
+}
+
+// keep limbs 0..level of every component
+static CtP ct_drop(const hs_ct *a, int level, cudaStream_t st)
+{
+    if (level == a->level) return ct_copy(a, st);
+    hs_ctx *c = a->ctx;
+    CtP r = ct_new(c, level, a->ncomp, st);
+    size_t N = c->P->n;
+    HS_CUDA(cudaMemcpy2DAsync(r->d, (level + 1) * N * 8, a->d, (a->level + 1) * N * 8, (level + 1) * N * 8, a->ncomp,
+                              cudaMemcpyDeviceToDevice, st));
+    return r;
+}
+
+// ------------------------------------------------------------------ tables
+const BconvTab &bconv_modup(hs_ctx *c, int level, int digit)
+{
+    std::lock_guard<std::mutex> g(c->mu);
+    long key = ((long)level << 8) | digit;
+    auto it = c->bconv.find(key);
+    if (it != c->bconv.end()) return it->second;
+    const hs_params *P = c->P;
+    BconvTab t;
+    int nl = level + 1, lo = digit * P->alpha, hi = std::min((digit + 1) * P->alpha, nl);
+    for (int i = lo; i < hi; i++) t.src.push_back(i);
+    for (int i = 0; i < nl; i++)
+        if (i < lo || i >= hi) t.dst.push_back(i);
+    for (int k = 0; k < P->n_p; k++) t.dst.push_back(P->n_q + k);
+    t.n_src = (int)t.src.size();
+    t.n_dst = (int)t.dst.size();
+    std::vector<u64> h(2 * t.n_src + 2 * (size_t)t.n_src * t.n_dst);
+    for (int a = 0; a < t.n_src; a++) {
+        u64 qa = P->prime[t.src[a]], qh = 1;
+        for (int b = 0; b < t.n_src; b++)
+            if (b != a) qh = hs_mulmod(qh, P->prime[t.src[b]] % qa, qa);
+        h[2 * a] = hs_invmod(qh, qa);
+        h[2 * a + 1] = hs_shoup_const(h[2 * a], qa);
+        for (int d = 0; d < t.n_dst; d++) {
+            u64 p = P->prime[t.dst[d]], v = 1;
+            for (int b = 0; b < t.n_src; b++)
+                if (b != a) v = hs_mulmod(v, P->prime[t.src[b]] % p, p);
+            size_t ci = 2 * t.n_src + 2 * ((size_t)a * t.n_dst + d);
+            h[ci] = v;
+            h[ci + 1] = hs_shoup_const(v, p);
+        }
+    }
+    HS_CUDA(cudaMalloc(&t.dev, h.size() * 8));
+    HS_CUDA(cudaMemcpy(t.dev, h.data(), h.size() * 8, cudaMemcpyHostToDevice));
+    return c->bconv[key] = t;
+}
+
+const BconvTab &bconv_moddown(hs_ctx *c, int level)
+{
+    std::lock_guard<std::mutex> g(c->mu);
+    long key = ((long)level << 8) | 255;
+    auto it = c->bconv.find(key);
+    if (it != c->bconv.end()) return it->second;
+    const hs_params *P = c->P;
+    BconvTab t;
+    for (int k = 0; k < P->n_p; k++) t.src.push_back(P->n_q + k);
+    for (int i = 0; i <= level; i++) t.dst.push_back(i);
+    t.n_src = (int)t.src.size();
+    t.n_dst = (int)t.dst.size();
+    std::vector<u64> h(2 * t.n_src + 2 * (size_t)t.n_src * t.n_dst);
+    for (int a = 0; a < t.n_src; a++) {
+        u64 pa = P->prime[t.src[a]], ph = 1;
+        for (int b = 0; b < t.n_src; b++)
+            if (b != a) ph = hs_mulmod(ph, P->prime[t.src[b]] % pa, pa);
+        h[2 * a] = hs_invmod(ph, pa);
+        h[2 * a + 1] = hs_shoup_const(h[2 * a], pa);
+        for (int d = 0; d < t.n_dst; d++) {
+            u64 q = P->prime[t.dst[d]], v = 1;
+            for (int b = 0; b < t.n_src; b++)
+                if (b != a) v = hs_mulmod(v, P->prime[t.src[b]] % q, q);
+            size_t ci = 2 * t.n_src + 2 * ((size_t)a * t.n_dst + d);
+            h[ci] = v;
+            h[ci + 1] = hs_shoup_const(v, q);
+        }
+    }
+    HS_CUDA(cudaMalloc(&t.dev, h.size() * 8));
+    HS_CUDA(cudaMemcpy(t.dev, h.data(), h.size() * 8, cudaMemcpyHostToDevice));
+    return c->bconv[key] = t;
+}
+
+// C10: out[i] = in[perm[i]], perm[i] = brv(((2 brv(i) + 1) k mod 2N - 1) / 2)
+const unsigned *galois_table(hs_ctx *c, int k)
+{
+    std::lock_guard<std::mutex> g(c->mu);
+    auto it = c->galois_perm.find(k);
+    if (it != c->galois_perm.end()) return it->second;
+    const hs_params *P = c->P;
+    int N = P->n, lg = P->log_n;
+    auto brv = [lg](unsigned x) {
+        unsigned r = 0;
+        for (int i = 0; i < lg; i++, x >>= 1) r = (r << 1) | (x & 1);
+        return r;
+    };
+    std::vector<unsigned> h(N);
+    u64 two_n = 2ull * N;
+    for (int i = 0; i < N; i++) {
+        u64 e = 2ull * brv((unsigned)i) + 1;
+        h[i] = brv((unsigned)(((e * (u64)k) % two_n - 1) / 2));
+    }
+    unsigned *d;
+    HS_CUDA(cudaMalloc(&d, N * sizeof(unsigned)));
+    HS_CUDA(cudaMemcpy(d, h.data(), N * sizeof(unsigned), cudaMemcpyHostToDevice));
+    return c->galois_perm[k] = d;
+}
+
+// ------------------------------------------------------------------ key switching (C7)
+void ev_keyswitch(const hs_keys *K, const SwKey *key, int level, const u64 *d, u64 *out0, u64 *out1,
+                  const u64 *add0, const u64 *add1, cudaStream_t st)
+{
+    hs_ctx *c = K->ctx;
+    const hs_params *P = c->P;
+    const size_t N = P->n;
+    const int nl = level + 1, alpha = P->alpha, np = P->n_p, ntg = nl + np;
+    const int beta = (nl + alpha - 1) / alpha;
+    // coefficient form of d
+    DBuf x(nl * N, st);
+    HS_CUDA(cudaMemcpyAsync(x.p, d, nl * N * 8, cudaMemcpyDeviceToDevice, st));
+    k_ntt(c, x.p, nl, pmap_range(0, nl), true, st);
+    // ModUp every digit: ext[j][g'] (coefficient form -> NTT)
+    DBuf ext((size_t)beta * ntg * N, st);
+    for (int j = 0; j < beta; j++) {
+        const BconvTab &tab = bconv_modup(c, level, j);
+        u64 *e = ext.p + (size_t)j * ntg * N;
+        k_bconv(c, tab, x.p + (size_t)tab.src[0] * N, N, e, N, 1, 0, 0, st);
+        PrimeMap pm;
+        pm.n = tab.n_dst;
+        for (int i = 0; i < tab.n_dst; i++) pm.p[i] = (unsigned char)tab.dst[i];
+        k_ntt(c, e, tab.n_dst, pm, false, st);
+    }
+    // inner product with the evaluation key: acc[2][ntg][N]
+    DBuf acc((size_t)2 * ntg * N, st);
+    k_ks_inner(c, d, ext.p, key->k, acc.p, level, beta, st);
+    // ModDown: iNTT of the P limbs, BConv P -> Q_l, NTT, (acc - conv) P^{-1}
+    DBuf z((size_t)2 * np * N, st);
+    HS_CUDA(cudaMemcpy2DAsync(z.p, np * N * 8, acc.p + (size_t)nl * N, ntg * N * 8, np * N * 8, 2,
+                              cudaMemcpyDeviceToDevice, st));
+    k_ntt(c, z.p, 2 * np, pmap_range(P->n_q, np), true, st);
+    const BconvTab &md = bconv_moddown(c, level);
+    DBuf conv((size_t)2 * nl * N, st);
+    k_bconv(c, md, z.p, N, conv.p, N, 2, np * N, nl * N, st);
+    k_ntt(c, conv.p, 2 * nl, pmap_range(0, nl), false, st);
+    k_moddown_final(c, acc.p, conv.p, out0, out1, add0, add1, level, st);
+    c->ledger[HS_LG_KS]++;
+}
+
+// ------------------------------------------------------------------ arithmetic
+CtP ev_rescale(const hs_ct *a, cudaStream_t st)
+{
+    hs_ctx *c = a->ctx;
+    const size_t N = c->P->n;
+    const int l = a->level, nc = a->ncomp;
+    if (l < 1) throw HsError(HS_ELEVEL, "rescale at level 0");
+    DBuf last((size_t)nc * N, st);
+    HS_CUDA(cudaMemcpy2DAsync(last.p, N * 8, a->limb(0, l), (l + 1) * N * 8, N * 8, nc, cudaMemcpyDeviceToDevice, st));
+    PrimeMap pm;
+    pm.n = 1;
+    pm.p[0] = (unsigned char)l;
+    k_ntt(c, last.p, nc, pm, true, st);
+    DBuf w((size_t)nc * l * N, st);
+    k_rescale_prep(c, last.p, w.p, nc, l, st);
+    k_ntt(c, w.p, nc * l, pmap_range(0, l), false, st);
+    CtP r = ct_new(c, l - 1, nc, st);
+    k_rescale_final(c, a->d, w.p, r->d, nc, l, st);
+    c->ledger[HS_LG_RESCALE]++;
+    return r;
+}
+
+// C12 landing constant: sc = (Delta_target q_{target+1}) / Delta_level
+static double landing_scale(const hs_params *P, int level, int target)
+{
+    return (P->scale[target] * (double)P->prime[target + 1]) / P->scale[level];
+}
+
+static void residues(const hs_params *P, double v, int n, u64 *out)
+{
+    for (int i = 0; i < n; i++) out[i] = hs_residue_of_double(v, P->prime[i]);
+}
+
+CtP ev_mult_const(const hs_ct *a, double v, int target, cudaStream_t st)
+{
+    hs_ctx *c = a->ctx;
+    const hs_params *P = c->P;
+    if (target < 0 || target >= a->level) throw HsError(HS_ELEVEL, "mult_const: target level must be below the input");
+    CtP d = ct_drop(a, target + 1, st);
+    u64 s[HS_MAXP];
+    residues(P, v * landing_scale(P, a->level, target), target + 2, s);
+    k_mul_scalar(c, d->d, d->d, s, (int)d->limbs(), target + 2, st);
+    c->ledger[HS_LG_CMULT]++;
+    return ev_rescale(d.get(), st);
+}
+
+CtP ev_level_down(const hs_ct *a, int target, cudaStream_t st)
+{
+    if (target == a->level) return ct_copy(a, st);
+    if (target > a->level) throw HsError(HS_ELEVEL, "level_down to a higher level");
+    a->ctx->ledger[HS_LG_LEVELDOWN]++;
+    return ev_mult_const(a, 1.0, target, st);
+}
+
+static void match(const hs_ct *a, const hs_ct *b, CtP &ta, CtP &tb, const hs_ct *&ra, const hs_ct *&rb,
+                  cudaStream_t st)
+{
+    ra = a;
+    rb = b;
+    if (a->level > b->level) {
+        ta = ev_level_down(a, b->level, st);
+        ra = ta.get();
+    } else if (b->level > a->level) {
+        tb = ev_level_down(b, a->level, st);
+        rb = tb.get();
+    }
+}
+
+CtP ev_add(const hs_ct *a, const hs_ct *b, bool sub, cudaStream_t st)
+{
+    if (a->ncomp != b->ncomp) throw HsError(HS_EINVAL, "add: component counts differ");
+    CtP ta, tb;
+    const hs_ct *ra, *rb;
+    match(a, b, ta, tb, ra, rb, st);
+    CtP r = ct_new(a->ctx, ra->level, ra->ncomp, st);
+    k_add(a->ctx, ra->d, rb->d, r->d, (int)r->limbs(), ra->level + 1, sub, st);
+    return r;
+}
+
+CtP ev_mult_int(const hs_ct *a, int64_t v, cudaStream_t st)
+{
+    const hs_params *P = a->ctx->P;
+    u64 s[HS_MAXP];
+    for (int i = 0; i <= a->level; i++) {
+        int64_t m = v % (int64_t)P->prime[i];
+        s[i] = (u64)(m < 0 ? m + (int64_t)P->prime[i] : m);
+    }
+    CtP r = ct_new(a->ctx, a->level, a->ncomp, st);
+    k_mul_scalar(a->ctx, a->d, r->d, s, (int)a->limbs(), a->level + 1, st);
+    return r;
+}
+
+CtP ev_add_const(const hs_ct *a, double v, cudaStream_t st)
+{
+    const hs_params *P = a->ctx->P;
+    u64 s[HS_MAXP];
+    residues(P, v * P->scale[a->level], a->level + 1, s);
+    CtP r = ct_copy(a, st);
+    k_add_scalar(a->ctx, r->d, s, a->level + 1, st);
+    return r;
+}
+
+CtP ev_mult_pt(const hs_ct *a, const double *re, const double *im, int target, cudaStream_t st)
+{
+    hs_ctx *c = a->ctx;
+    const hs_params *P = c->P;
+    if (target < 0 || target >= a->level) throw HsError(HS_ELEVEL, "mult_pt: target level must be below the input");
+    const size_t N = P->n;
+    const int nl = target + 2;
+    std::vector<u64> pt((size_t)nl * N);
+    hs_encode_impl(P, re, im, landing_scale(P, a->level, target), target + 1, pt.data());
+    DBuf m((size_t)nl * N, st);
+    HS_CUDA(cudaMemcpyAsync(m.p, pt.data(), pt.size() * 8, cudaMemcpyHostToDevice, st));
+    k_ntt(c, m.p, nl, pmap_range(0, nl), false, st);
+    CtP d = ct_drop(a, target + 1, st);
+    k_mul_pointwise(c, d->d, m.p, d->d, (int)d->limbs(), nl, nl, st);
+    HS_CUDA(cudaStreamSynchronize(st));  // pt host buffer lifetime
+    c->ledger[HS_LG_PMULT]++;
+    return ev_rescale(d.get(), st);
+}
+
+CtP ev_tensor(const hs_ct *a, const hs_ct *b, cudaStream_t st)
+{
+    if (a->ncomp != 2 || b->ncomp != 2) throw HsError(HS_EINVAL, "tensor needs degree-1 ciphertexts");
+    CtP ta, tb;
+    const hs_ct *ra, *rb;
+    match(a, b, ta, tb, ra, rb, st);
+    CtP r = ct_new(a->ctx, ra->level, 3, st);
+    k_tensor(a->ctx, ra->d, rb->d, r->d, ra->level + 1, st);
+    a->ctx->ledger[HS_LG_TENSOR]++;
+    return r;
+}
+
+CtP ev_relin(const hs_keys *K, const hs_ct *d, cudaStream_t st)
+{
+    const SwKey *rk = K->find(0);
+    if (!rk) throw HsError(HS_EKEY, "relinearisation key missing");
+    if (d->ncomp != 3) throw HsError(HS_EINVAL, "relin needs a degree-2 ciphertext");
+    CtP r = ct_new(d->ctx, d->level, 2, st);
+    ev_keyswitch(K, rk, d->level, d->limb(2, 0), r->limb(0, 0), r->limb(1, 0), d->limb(0, 0), d->limb(1, 0), st);
+    return r;
+}
+
+CtP ev_mult(const hs_keys *K, const hs_ct *a, const hs_ct *b, cudaStream_t st)
+{
+    CtP t = ev_tensor(a, b, st);
+    CtP r = ev_relin(K, t.get(), st);
+    K->ctx->ledger[HS_LG_HMULT]++;
+    return ev_rescale(r.get(), st);
+}
+
+CtP ev_galois(const hs_keys *K, const hs_ct *a, int k, cudaStream_t st)
+{
+    const SwKey *key = K->find(k);
+    if (!key) throw HsError(HS_EKEY, "switching key for Galois element " + std::to_string(k) + " missing");
+    if (a->ncomp != 2) throw HsError(HS_EINVAL, "rotation needs a degree-1 ciphertext");
+    hs_ctx *c = a->ctx;
+    CtP s = ct_new(c, a->level, 2, st);
+    k_permute(c, a->d, s->d, galois_table(c, k), (int)a->limbs(), st);
+    CtP r = ct_new(c, a->level, 2, st);
+    ev_keyswitch(K, key, a->level, s->limb(1, 0), r->limb(0, 0), r->limb(1, 0), s->limb(0, 0), nullptr, st);
+    c->ledger[HS_LG_ROT]++;
+    return r;
+}
+
+CtP ev_rotate(const hs_keys *K, const hs_ct *a, int r, cudaStream_t st)
+{
+    return ev_galois(K, a, hs_galois_elt(K->ctx->P, r), st);
+}
+
+// sum_i coef_i * terms_i landing at `target` with ONE rescale (C13 leaves):
+// every term is dropped to target+1 and multiplied by rint(coef_i * sc_i).
+CtP ev_mult_const_sum(const std::vector<const hs_ct *> &terms, const std::vector<double> &coef, int target,
+                      cudaStream_t st)
+{
+    hs_ctx *c = terms[0]->ctx;
+    const hs_params *P = c->P;
+    const size_t N = P->n;
+    const int nl = target + 2;
+    CtP acc = ct_new(c, target + 1, 2, st);
+    HS_CUDA(cudaMemsetAsync(acc->d, 0, acc->limbs() * N * 8, st));
+    for (size_t i = 0; i < terms.size(); i++) {
+        if (coef[i] == 0.0) continue;
+        const hs_ct *t = terms[i];
+        if (t->level < target + 1) throw HsError(HS_ELEVEL, "leaf term below its landing level");
+        u64 s[HS_MAXP];
+        residues(P, coef[i] * landing_scale(P, t->level, target), nl, s);
+        for (int comp = 0; comp < 2; comp++)
+            k_mac_scalar(c, acc->limb(comp, 0), t->limb(comp, 0), s, nl, nl, st);
+        c->ledger[HS_LG_CMULT]++;
+    }
+    return ev_rescale(acc.get(), st);
+}
+
+// ------------------------------------------------------------------ keys (C5, C6, C7)
+static void sample_secret(const hs_params *P, u64 seed, int h, std::vector<int64_t> &s)
+{
+    int N = P->n;
+    std::vector<int> pos(N);
+    for (int i = 0; i < N; i++) pos[i] = i;
+    s.assign(N, 0);
+    for (int i = 0; i < h; i++) {
+        u64 w = hs_stream_word(seed, TAG_SK, 0, 2 * (u64)i);
+        int j = i + (int)(w % (u64)(N - i));
+        std::swap(pos[i], pos[j]);
+        s[pos[i]] = (hs_stream_word(seed, TAG_SK, 0, 2 * (u64)i + 1) & 1) ? -1 : 1;
+    }
+}
+
+// e (CBD eta) in coefficient form -> NTT residues over primes [0, n)
+static void error_poly(hs_ctx *c, u64 seed, uint32_t tag, u64 sub, int eta, u64 *out, int n, cudaStream_t st)
+{
+    DBuf e(c->P->n, st);
+    k_cbd(c, (int64_t *)e.p, seed, tag, sub, eta, st);
+    k_signed_to_rns(c, (const int64_t *)e.p, out, n, pmap_range(0, n), st);
+    k_ntt(c, out, n, pmap_range(0, n), false, st);
+}
+
+hs_keys *keys_generate(hs_ctx *c, u64 seed, int h, const int32_t *galois, size_t n_galois, int relin, cudaStream_t st)
+{
+    const hs_params *P = c->P;
+    const size_t N = P->n;
+    const int nt = P->n_q + P->n_p, nq = P->n_q;
+    std::unique_ptr<hs_keys> K(new hs_keys);
+    K->ctx = c;
+    if (h < 1 || h > P->n) throw HsError(HS_EINVAL, "secret Hamming weight out of range");
+    sample_secret(P, seed, h, K->s_coeff);
+    HS_CUDA(cudaMalloc(&K->s_ntt, (size_t)nt * N * 8));
+    {
+        DBuf sc(N, st);
+        HS_CUDA(cudaMemcpyAsync(sc.p, K->s_coeff.data(), N * 8, cudaMemcpyHostToDevice, st));
+        k_signed_to_rns(c, (const int64_t *)sc.p, K->s_ntt, nt, pmap_range(0, nt), st);
+        k_ntt(c, K->s_ntt, nt, pmap_range(0, nt), false, st);
+        HS_CUDA(cudaStreamSynchronize(st));
+    }
+    // pk = (-a s + e, a) over Q_L
+    HS_CUDA(cudaMalloc(&K->pk, (size_t)2 * nq * N * 8));
+    {
+        u64 *b = K->pk, *a = K->pk + (size_t)nq * N;
+        k_uniform(c, a, nq, pmap_range(0, nq), seed, TAG_PK_A, 0, 0, st);
+        error_poly(c, seed, TAG_PK_E, 0, ETA_ERR, b, nq, st);
+        DBuf as((size_t)nq * N, st);
+        k_mul_pointwise(c, a, K->s_ntt, as.p, nq, nq, nq, st);
+        k_add(c, b, as.p, b, nq, nq, true, st);
+    }
+    // switching keys: relin (s' = s^2) then one per Galois element (s' = sigma_k(s))
+    std::vector<int> ids;
+    if (relin) ids.push_back(0);
+    for (size_t i = 0; i < n_galois; i++) ids.push_back(galois[i]);
+    DBuf sp((size_t)nt * N, st), as((size_t)nt * N, st);
+    for (int id : ids) {
+        if (id == 0) k_mul_pointwise(c, K->s_ntt, K->s_ntt, sp.p, nt, nt, nt, st);
+        else k_permute(c, K->s_ntt, sp.p, galois_table(c, id), nt, st);
+        SwKey key;
+        key.galois = id;
+        HS_CUDA(cudaMalloc(&key.k, (size_t)P->dnum * 2 * nt * N * 8));
+        for (int j = 0; j < P->dnum; j++) {
+            u64 sub = (u64)id * 256 + (u64)j;
+            u64 *k0 = key.k + (size_t)(2 * j) * nt * N, *k1 = key.k + (size_t)(2 * j + 1) * nt * N;
+            k_uniform(c, k1, nt, pmap_range(0, nt), seed, TAG_KSK_A, sub, 0, st);
+            error_poly(c, seed, TAG_KSK_E, sub, ETA_ERR, k0, nt, st);
+            k_mul_pointwise(c, k1, K->s_ntt, as.p, nt, nt, nt, st);
+            k_add(c, k0, as.p, k0, nt, nt, true, st);
+            u64 g[HS_MAXP];
+            for (int i = 0; i < nq; i++) g[i] = (i / P->alpha == j) ? P->p_mod_q[i] : 0;
+            k_mac_scalar(c, k0, sp.p, g, nq, nq, st);
+        }
+        K->swk.push_back(key);
+    }
+    HS_CUDA(cudaStreamSynchronize(st));
+    return K.release();
+}
+
+CtP ev_encrypt(const hs_keys *K, const u64 *pt_host, int level, u64 seed, u64 idx, bool use_sk, cudaStream_t st)
+{
+    hs_ctx *c = K->ctx;
+    const hs_params *P = c->P;
+    const size_t N = P->n;
+    const int nl = level + 1;
+    if (level < 0 || level > P->L) throw HsError(HS_EINVAL, "encrypt: level out of range");
+    DBuf m((size_t)nl * N, st);
+    HS_CUDA(cudaMemcpyAsync(m.p, pt_host, (size_t)nl * N * 8, cudaMemcpyHostToDevice, st));
+    k_ntt(c, m.p, nl, pmap_range(0, nl), false, st);
+    CtP r = ct_new(c, level, 2, st);
+    u64 *c0 = r->limb(0, 0), *c1 = r->limb(1, 0);
+    DBuf tmp((size_t)nl * N, st);
+    if (use_sk) {
+        k_uniform(c, c1, nl, pmap_range(0, nl), seed, TAG_ENC_A, idx, 0, st);
+        error_poly(c, seed, TAG_ENC_E0, idx, ETA_ERR, c0, nl, st);
+        k_mul_pointwise(c, c1, K->s_ntt, tmp.p, nl, nl, nl, st);
+        k_add(c, c0, tmp.p, c0, nl, nl, true, st);
+        k_add(c, c0, m.p, c0, nl, nl, false, st);
+    } else {
+        DBuf v((size_t)nl * N, st);
+        error_poly(c, seed, TAG_ENC_V, idx, ETA_V, v.p, nl, st);
+        error_poly(c, seed, TAG_ENC_E0, idx, ETA_ERR, c0, nl, st);
+        error_poly(c, seed, TAG_ENC_E1, idx, ETA_ERR, c1, nl, st);
+        const u64 *b = K->pk, *a = K->pk + (size_t)P->n_q * N;
+        k_mul_pointwise(c, v.p, b, tmp.p, nl, nl, nl, st);
+        k_add(c, c0, tmp.p, c0, nl, nl, false, st);
+        k_add(c, c0, m.p, c0, nl, nl, false, st);
+        k_mul_pointwise(c, v.p, a, tmp.p, nl, nl, nl, st);
+        k_add(c, c1, tmp.p, c1, nl, nl, false, st);
+    }
+    HS_CUDA(cudaStreamSynchronize(st));  // host pt lifetime
+    return r;
+}
+
+void ev_decrypt(const hs_keys *K, const hs_ct *ct, u64 *host_out, cudaStream_t st)
+{
+    hs_ctx *c = K->ctx;
+    const size_t N = c->P->n;
+    const int nl = ct->level + 1;
+    DBuf m((size_t)nl * N, st);
+    k_mul_pointwise(c, ct->limb(1, 0), K->s_ntt, m.p, nl, nl, nl, st);
+    k_add(c, m.p, ct->limb(0, 0), m.p, nl, nl, false, st);
+    k_ntt(c, m.p, nl, pmap_range(0, nl), true, st);
+    HS_CUDA(cudaMemcpyAsync(host_out, m.p, (size_t)nl * N * 8, cudaMemcpyDeviceToHost, st));
+    HS_CUDA(cudaStreamSynchronize(st));
+}

@@ -1,0 +1,216 @@
+// hs_internal.h -- internal declarations of libhesoftmax (product side).
+//
+// Layers:
+//   tables.cpp   host RNS tables: primes (C1), psi (C2), twiddles with Shoup
+//                companions, canonical scales (C12), BConv constants
+//   rng.cu       ChaCha20 counter stream + samplers on the device (C5)
+//   ntt.cu       negacyclic NTT / iNTT kernels (C3)
+//   kernels.cu   elementwise, tensor, automorphism, rescale, BConv, evk dot
+//   eval.cu      evaluator: key switch (C7), HMult (C8), rescale (C9),
+//                rotation (C10), constants (C12), keys, encrypt/decrypt
+//   poly.cpp     Chebyshev BSGS evaluation (C13)
+//   softmax.cpp  Alg 1 / Alg 2 / Alg B driver, packing (C14, C15)
+//   encode.cpp   quad-precision canonical embedding (C4), host
+//   capi.cpp     extern "C" boundary (include/hesoftmax.h)
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <map>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/hesoftmax.h"
+
+typedef uint64_t u64;
+typedef unsigned __int128 u128;
+
+#define HS_MAXP 64
+
+// ------------------------------------------------------------------ errors
+struct HsError : std::runtime_error {
+    hs_status code;
+    HsError(hs_status c, const std::string &m) : std::runtime_error(m), code(c) {}
+};
+#define HS_CUDA(x)                                                                            \
+    do {                                                                                      \
+        cudaError_t _e = (x);                                                                 \
+        if (_e != cudaSuccess)                                                                \
+            throw HsError(HS_ECUDA, std::string(#x) + ": " + cudaGetErrorString(_e));         \
+    } while (0)
+#define HS_CHECK_LAUNCH() HS_CUDA(cudaGetLastError())
+
+// ------------------------------------------------------------------ per-prime constants
+// Shoup: x*w mod q = x*w - hi(x*wsh)*q (+ one correction), wsh = floor(w 2^64 / q).
+// Reduction of a 128-bit T < q 2^64: Montgomery REDC (qinv = -q^{-1} mod 2^64)
+// gives T 2^-64 mod q, then a Shoup multiply by r64 = 2^64 mod q restores T mod q.
+struct PrimeK {
+    u64 q, qinv, r64, r64sh;
+};
+
+// ------------------------------------------------------------------ host parameters
+struct hs_params {
+    int log_n = 0, n = 0, n_q = 0, n_p = 0, L = 0, alpha = 0, dnum = 0;
+    std::vector<u64> prime, psi;
+    std::vector<double> scale;                 // canonical scale per level (C12)
+    std::vector<PrimeK> pk;                    // per prime
+    std::vector<std::vector<u64>> tw;          // per prime: [psi_rev | psi_rev_sh | ipsi_rev | ipsi_rev_sh]
+    std::vector<u64> n_inv, n_inv_sh;
+    std::vector<u64> p_mod_q, p_inv_mod_q;     // per Q prime
+};
+
+u64 hs_mulmod(u64 a, u64 b, u64 q);
+u64 hs_powmod(u64 a, u64 e, u64 q);
+u64 hs_invmod(u64 a, u64 q);
+u64 hs_shoup_const(u64 w, u64 q);
+u64 hs_residue_of_double(double x, u64 q);
+void hs_build_params(const hs_params_desc *d, hs_params *P);
+int hs_galois_elt(const hs_params *P, int r);
+
+// ------------------------------------------------------------------ device context
+struct DevTables {
+    u64 *tw = nullptr;          // [nprimes][4][N]
+    PrimeK *pk = nullptr;       // device copy (also in __constant__ via cudaMemcpyToSymbol)
+};
+
+struct BconvTab {               // ModUp digit (level, digit) or ModDown (level)
+    int n_src = 0, n_dst = 0;
+    std::vector<int> src, dst;  // global prime indices
+    u64 *dev = nullptr;         // [n_src](inv, inv_sh) then [n_src][n_dst](c, c_sh)
+};
+
+struct hs_ctx {
+    const hs_params *P = nullptr;
+    int device = 0;
+    DevTables T;
+    std::map<long, BconvTab> bconv;          // key: (level << 8 | digit), digit 255 = ModDown
+    std::map<int, unsigned *> galois_perm;   // device permutation tables
+    std::mutex mu;
+    int64_t ledger[HS_LG_COUNT] = {0};
+    ~hs_ctx();
+};
+
+struct SwKey {
+    int galois = 0;
+    u64 *k = nullptr;           // [dnum][2][n_q+n_p][N]
+};
+
+struct hs_keys {
+    hs_ctx *ctx = nullptr;
+    std::vector<int64_t> s_coeff;
+    u64 *s_ntt = nullptr;       // [n_q+n_p][N]
+    u64 *pk = nullptr;          // [2][n_q][N]
+    std::vector<SwKey> swk;
+    ~hs_keys();
+    const SwKey *find(int galois) const {
+        for (auto &k : swk)
+            if (k.galois == galois) return &k;
+        return nullptr;
+    }
+};
+
+struct hs_ct {
+    hs_ctx *ctx = nullptr;
+    int level = 0, ncomp = 0;
+    u64 *d = nullptr;           // [ncomp][level+1][N]
+    cudaStream_t st = nullptr;  // stream the buffer is ordered on
+    ~hs_ct();
+    size_t limbs() const { return (size_t)ncomp * (level + 1); }
+    u64 *limb(int comp, int i) const;
+};
+
+// ------------------------------------------------------------------ memory
+u64 *dev_alloc(size_t words, cudaStream_t st);
+void dev_free(void *p, cudaStream_t st);
+struct DBuf {                   // stream-ordered scratch buffer
+    u64 *p = nullptr;
+    cudaStream_t st = nullptr;
+    DBuf() {}
+    DBuf(size_t words, cudaStream_t s) : p(dev_alloc(words, s)), st(s) {}
+    ~DBuf() { if (p) dev_free(p, st); }
+    DBuf(const DBuf &) = delete;
+    DBuf &operator=(const DBuf &) = delete;
+};
+
+// ------------------------------------------------------------------ kernel launchers (kernels.cu / ntt.cu / rng.cu)
+struct PrimeMap {               // prime index of limb l = p[l % n]
+    int n;
+    unsigned char p[256];
+};
+PrimeMap pmap_range(int first, int count);
+
+void k_ntt(hs_ctx *c, u64 *data, int n_limbs, const PrimeMap &pm, bool inverse, cudaStream_t st);
+void k_add(hs_ctx *c, const u64 *a, const u64 *b, u64 *o, int n_limbs, int period, bool sub, cudaStream_t st);
+void k_neg(hs_ctx *c, const u64 *a, u64 *o, int n_limbs, int period, cudaStream_t st);
+void k_mul_scalar(hs_ctx *c, const u64 *a, u64 *o, const u64 *host_scal, int n_limbs, int period, cudaStream_t st);
+void k_add_scalar(hs_ctx *c, u64 *a, const u64 *host_scal, int n_limbs, cudaStream_t st);
+void k_mul_pointwise(hs_ctx *c, const u64 *a, const u64 *b, u64 *o, int n_limbs, int period_a, int period_b,
+                     cudaStream_t st);
+void k_mac_scalar(hs_ctx *c, u64 *acc, const u64 *a, const u64 *host_scal, int n_limbs, int period, cudaStream_t st);
+void k_tensor(hs_ctx *c, const u64 *a, const u64 *b, u64 *o, int nl, cudaStream_t st);
+void k_permute(hs_ctx *c, const u64 *a, u64 *o, const unsigned *perm, int n_limbs, cudaStream_t st);
+void k_rescale_prep(hs_ctx *c, const u64 *last, u64 *w, int ncomp, int level, cudaStream_t st);
+void k_rescale_final(hs_ctx *c, const u64 *a, const u64 *w, u64 *o, int ncomp, int level, cudaStream_t st);
+void k_bconv(hs_ctx *c, const BconvTab &tab, const u64 *src, size_t src_stride, u64 *dst, size_t dst_stride,
+             int batch, size_t batch_src_stride, size_t batch_dst_stride, cudaStream_t st);
+void k_ks_inner(hs_ctx *c, const u64 *d, const u64 *ext, const u64 *key, u64 *acc, int level, int beta,
+                cudaStream_t st);
+void k_moddown_final(hs_ctx *c, const u64 *acc, const u64 *conv, u64 *o0, u64 *o1, const u64 *add0,
+                     const u64 *add1, int level, cudaStream_t st);
+void upload_prime_constants(const hs_params *P);
+void k_signed_to_rns(hs_ctx *c, const int64_t *v, u64 *o, int n_limbs, const PrimeMap &pm, cudaStream_t st);
+void k_uniform(hs_ctx *c, u64 *o, int n_limbs, const PrimeMap &pm, u64 seed, uint32_t tag, u64 sub,
+               int limb_index0, cudaStream_t st);
+void k_cbd(hs_ctx *c, int64_t *o, u64 seed, uint32_t tag, u64 sub, int eta, cudaStream_t st);
+
+const BconvTab &bconv_modup(hs_ctx *c, int level, int digit);
+const BconvTab &bconv_moddown(hs_ctx *c, int level);
+const unsigned *galois_table(hs_ctx *c, int k);
+void count_kernel(hs_ctx *c, int n = 1);
+
+// host ChaCha20 (C5) for the sequential secret sampler
+void hs_chacha20_block(const uint32_t key[8], uint32_t counter, const uint32_t nonce[3], uint32_t out[16]);
+u64 hs_stream_word(u64 seed, uint32_t tag, u64 sub, u64 idx);
+
+// ------------------------------------------------------------------ evaluator (eval.cu)
+typedef std::unique_ptr<hs_ct> CtP;
+CtP ct_new(hs_ctx *c, int level, int ncomp, cudaStream_t st);
+CtP ct_copy(const hs_ct *a, cudaStream_t st);
+CtP ev_add(const hs_ct *a, const hs_ct *b, bool sub, cudaStream_t st);
+CtP ev_level_down(const hs_ct *a, int target, cudaStream_t st);
+CtP ev_rescale(const hs_ct *a, cudaStream_t st);
+CtP ev_tensor(const hs_ct *a, const hs_ct *b, cudaStream_t st);
+CtP ev_relin(const hs_keys *K, const hs_ct *d, cudaStream_t st);
+CtP ev_mult(const hs_keys *K, const hs_ct *a, const hs_ct *b, cudaStream_t st);
+CtP ev_mult_int(const hs_ct *a, int64_t v, cudaStream_t st);
+CtP ev_add_const(const hs_ct *a, double v, cudaStream_t st);
+CtP ev_mult_const(const hs_ct *a, double v, int target, cudaStream_t st);
+CtP ev_mult_pt(const hs_ct *a, const double *re, const double *im, int target, cudaStream_t st);
+CtP ev_galois(const hs_keys *K, const hs_ct *a, int k, cudaStream_t st);
+CtP ev_rotate(const hs_keys *K, const hs_ct *a, int r, cudaStream_t st);
+void ev_keyswitch(const hs_keys *K, const SwKey *key, int level, const u64 *d, u64 *out0, u64 *out1,
+                  const u64 *add0, const u64 *add1, cudaStream_t st);
+CtP ev_mult_const_sum(const std::vector<const hs_ct *> &terms, const std::vector<double> &coef, int target,
+                      cudaStream_t st);
+
+// keys / enc / dec
+hs_keys *keys_generate(hs_ctx *c, u64 seed, int h, const int32_t *galois, size_t n_galois, int relin,
+                       cudaStream_t st);
+CtP ev_encrypt(const hs_keys *K, const u64 *pt_host, int level, u64 seed, u64 idx, bool use_sk, cudaStream_t st);
+void ev_decrypt(const hs_keys *K, const hs_ct *ct, u64 *host_out, cudaStream_t st);
+
+// encode.cpp
+void hs_encode_impl(const hs_params *P, const double *re, const double *im, double scale, int level, u64 *out);
+void hs_decode_impl(const hs_params *P, const u64 *q0_coeffs, double scale, double *re, double *im);
+
+// poly.cpp
+CtP ev_cheb(const hs_keys *K, const hs_ct *x, const hs_poly *p, cudaStream_t st);
+int cheb_depth(int deg);
+
+// softmax.cpp
+hs_status softmax_run(hs_ctx *c, const hs_keys *K, const hs_softmax_desc *d, const hs_ct *const *in,
+                      size_t m_local, cudaStream_t st, hs_ct **out);

@@ -1,0 +1,682 @@
+// kernels.cu -- all device code of libhesoftmax (sm_100a).
+//
+// 64-bit modular arithmetic: Shoup multiplication by constants (twiddles,
+// BConv constants, scalars) and REDC-based reduction of 128-bit values
+// T < q 2^64 for variable x variable products and lazy accumulations
+// (tensor, evaluation-key inner product).  All results are canonical
+// residues in [0, q), so every kernel is bit-identical to the oracle's
+// plain `%` arithmetic.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+
+#include "hs_internal.h"
+
+__constant__ PrimeK c_pk[HS_MAXP];
+
+void upload_prime_constants(const hs_params *P)
+{
+    HS_CUDA(cudaMemcpyToSymbol(c_pk, P->pk.data(), sizeof(PrimeK) * P->pk.size()));
+}
+
+// ------------------------------------------------------------------ modular helpers
+__device__ __forceinline__ u64 d_add(u64 a, u64 b, u64 q)
+{
+    u64 s = a + b;
+    return s >= q ? s - q : s;
+}
+__device__ __forceinline__ u64 d_sub(u64 a, u64 b, u64 q) { return a >= b ? a - b : a + q - b; }
+__device__ __forceinline__ u64 d_shoup(u64 a, u64 w, u64 wsh, u64 q)
+{
+    u64 h = __umul64hi(a, wsh);
+    u64 r = a * w - h * q;
+    return r >= q ? r - q : r;
+}
+// T = hi 2^64 + lo < q 2^64  ->  T mod q
+__device__ __forceinline__ u64 d_reduce128(u64 hi, u64 lo, const PrimeK &k)
+{
+    u64 m = lo * k.qinv;
+    u64 t = hi + __umul64hi(m, k.q) + (lo != 0);
+    if (t >= k.q) t -= k.q;
+    return d_shoup(t, k.r64, k.r64sh, k.q);
+}
+__device__ __forceinline__ u64 d_mulmod(u64 a, u64 b, const PrimeK &k) { return d_reduce128(__umul64hi(a, b), a * b, k); }
+__device__ __forceinline__ void mac128(u64 &hi, u64 &lo, u64 a, u64 b)
+{
+    u64 l = a * b, h = __umul64hi(a, b);
+    lo += l;
+    hi += h + (lo < l);
+}
+
+PrimeMap pmap_range(int first, int count)
+{
+    PrimeMap m;
+    m.n = count;
+    for (int i = 0; i < count; i++) m.p[i] = (unsigned char)(first + i);
+    return m;
+}
+
+void count_kernel(hs_ctx *c, int n)
+{
+    c->ledger[HS_LG_KERNELS] += n;
+}
+
+// ------------------------------------------------------------------ NTT (C3)
+// N = N1 * N2, index j = r * N2 + col.  Forward Cooley-Tukey stages with
+// half-span t >= N2 pair rows (phase "cols"), t < N2 pair within a row
+// (phase "rows").  Stage with half-span t uses twiddle table[N/(2t) + j/(2t)].
+// Inverse = Gentleman-Sande in the reverse stage order with the psi^-1 table
+// and a final N^-1 (fused into the last phase).
+struct NttGeom {
+    int log_n, log_n1, log_n2;
+};
+
+template <bool INV>
+__global__ void __launch_bounds__(256) ntt_cols_kernel(u64 *data, PrimeMap pm, const u64 *__restrict__ tw, NttGeom g,
+                                                      int C, const u64 *__restrict__ ninv)
+{
+    extern __shared__ u64 sm[];
+    const int N = 1 << g.log_n, N1 = 1 << g.log_n1, N2 = 1 << g.log_n2;
+    const int limb = blockIdx.y;
+    const int pi = pm.p[limb % pm.n];
+    const PrimeK k = c_pk[pi];
+    const u64 q = k.q;
+    u64 *a = data + (size_t)limb * N;
+    const u64 *w = tw + (size_t)pi * 4 * N + (INV ? 2 * N : 0);
+    const u64 *wsh = w + N;
+    const int c0 = blockIdx.x * C;
+    const int tot = N1 * C;
+    for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
+        int r = idx / C, c = idx - r * C;
+        sm[idx] = a[(size_t)r * N2 + c0 + c];
+    }
+    __syncthreads();
+    const int half = tot >> 1;
+    if (!INV) {
+        for (int tr = N1 >> 1, m = 1; tr >= 1; tr >>= 1, m <<= 1) {
+            for (int b = threadIdx.x; b < half; b += blockDim.x) {
+                int c = b % C, rb = b / C;
+                int grp = rb / tr, rl = grp * 2 * tr + (rb - grp * tr), rh = rl + tr;
+                u64 W = w[m + grp], Ws = wsh[m + grp];
+                u64 U = sm[rl * C + c], V = d_shoup(sm[rh * C + c], W, Ws, q);
+                sm[rl * C + c] = d_add(U, V, q);
+                sm[rh * C + c] = d_sub(U, V, q);
+            }
+            __syncthreads();
+        }
+    } else {
+        for (int tr = 1, m = N1 >> 1; tr < N1; tr <<= 1, m >>= 1) {
+            for (int b = threadIdx.x; b < half; b += blockDim.x) {
+                int c = b % C, rb = b / C;
+                int grp = rb / tr, rl = grp * 2 * tr + (rb - grp * tr), rh = rl + tr;
+                u64 W = w[m + grp], Ws = wsh[m + grp];
+                u64 U = sm[rl * C + c], V = sm[rh * C + c];
+                sm[rl * C + c] = d_add(U, V, q);
+                sm[rh * C + c] = d_shoup(d_sub(U, V, q), W, Ws, q);
+            }
+            __syncthreads();
+        }
+    }
+    const u64 ni = INV ? ninv[2 * pi] : 0, nis = INV ? ninv[2 * pi + 1] : 0;
+    for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
+        int r = idx / C, c = idx - r * C;
+        u64 v = sm[idx];
+        if (INV) v = d_shoup(v, ni, nis, q);
+        a[(size_t)r * N2 + c0 + c] = v;
+    }
+}
+
+template <bool INV>
+__global__ void __launch_bounds__(256) ntt_rows_kernel(u64 *data, PrimeMap pm, const u64 *__restrict__ tw, NttGeom g,
+                                                      int R)
+{
+    extern __shared__ u64 sm[];
+    const int N = 1 << g.log_n, N2 = 1 << g.log_n2;
+    const int limb = blockIdx.y;
+    const int pi = pm.p[limb % pm.n];
+    const PrimeK k = c_pk[pi];
+    const u64 q = k.q;
+    u64 *a = data + (size_t)limb * N + (size_t)blockIdx.x * R * N2;
+    const u64 *w = tw + (size_t)pi * 4 * N + (INV ? 2 * N : 0);
+    const u64 *wsh = w + N;
+    const int tot = R * N2;
+    const int row0 = blockIdx.x * R;
+    for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) sm[idx] = a[idx];
+    __syncthreads();
+    const int half = tot >> 1, hrow = N2 >> 1;
+    if (!INV) {
+        for (int t = N2 >> 1; t >= 1; t >>= 1) {
+            const int m = N / (2 * t);
+            for (int b = threadIdx.x; b < half; b += blockDim.x) {
+                int row = b / hrow, bb = b - row * hrow;
+                int gl = bb / t, lo = gl * 2 * t + (bb - gl * t);
+                int grp = (row0 + row) * (N2 / (2 * t)) + gl;
+                u64 W = w[m + grp], Ws = wsh[m + grp];
+                int il = row * N2 + lo, ih = il + t;
+                u64 U = sm[il], V = d_shoup(sm[ih], W, Ws, q);
+                sm[il] = d_add(U, V, q);
+                sm[ih] = d_sub(U, V, q);
+            }
+            __syncthreads();
+        }
+    } else {
+        for (int t = 1; t < N2; t <<= 1) {
+            const int m = N / (2 * t);
+            for (int b = threadIdx.x; b < half; b += blockDim.x) {
+                int row = b / hrow, bb = b - row * hrow;
+                int gl = bb / t, lo = gl * 2 * t + (bb - gl * t);
+                int grp = (row0 + row) * (N2 / (2 * t)) + gl;
+                u64 W = w[m + grp], Ws = wsh[m + grp];
+                int il = row * N2 + lo, ih = il + t;
+                u64 U = sm[il], V = sm[ih];
+                sm[il] = d_add(U, V, q);
+                sm[ih] = d_shoup(d_sub(U, V, q), W, Ws, q);
+            }
+            __syncthreads();
+        }
+    }
+    for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) a[idx] = sm[idx];
+}
+
+void k_ntt(hs_ctx *c, u64 *data, int n_limbs, const PrimeMap &pm, bool inverse, cudaStream_t st)
+{
+    if (n_limbs <= 0) return;
+    const hs_params *P = c->P;
+    NttGeom g;
+    g.log_n = P->log_n;
+    g.log_n2 = P->log_n / 2;
+    g.log_n1 = P->log_n - g.log_n2;
+    const int N1 = 1 << g.log_n1, N2 = 1 << g.log_n2;
+    const int C = N2 < 16 ? N2 : 16;
+    const int R = (2048 / N2) > 0 ? (2048 / N2 < N1 ? 2048 / N2 : N1) : 1;
+    dim3 gc(N2 / C, n_limbs), gr(N1 / R, n_limbs);
+    size_t smc = (size_t)N1 * C * 8, smr = (size_t)R * N2 * 8;
+    const u64 *ninv = c->T.tw + (size_t)(P->n_q + P->n_p) * 4 * P->n;
+    if (!inverse) {
+        ntt_cols_kernel<false><<<gc, 256, smc, st>>>(data, pm, c->T.tw, g, C, ninv);
+        ntt_rows_kernel<false><<<gr, 256, smr, st>>>(data, pm, c->T.tw, g, R);
+    } else {
+        ntt_rows_kernel<true><<<gr, 256, smr, st>>>(data, pm, c->T.tw, g, R);
+        ntt_cols_kernel<true><<<gc, 256, smc, st>>>(data, pm, c->T.tw, g, C, ninv);
+    }
+    HS_CHECK_LAUNCH();
+    c->ledger[HS_LG_NTT] += n_limbs;
+    count_kernel(c, 2);
+}
+
+// ------------------------------------------------------------------ elementwise
+#define GRID_LIMBS(n_limbs, N) dim3(((N) + 255) / 256, (n_limbs))
+
+__global__ void add_kernel(const u64 *a, const u64 *b, u64 *o, int N, int period, int sub)
+{
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= N) return;
+    int l = blockIdx.y;
+    u64 q = c_pk[l % period].q;
+    size_t x = (size_t)l * N + t;
+    o[x] = sub ? d_sub(a[x], b[x], q) : d_add(a[x], b[x], q);
+}
+
+void k_add(hs_ctx *c, const u64 *a, const u64 *b, u64 *o, int n_limbs, int period, bool sub, cudaStream_t st)
+{
+    int N = c->P->n;
+    add_kernel<<<GRID_LIMBS(n_limbs, N), 256, 0, st>>>(a, b, o, N, period, sub ? 1 : 0);
+    HS_CHECK_LAUNCH();
+    count_kernel(c);
+}
+
+__global__ void neg_kernel(const u64 *a, u64 *o, int N, int period)
+{
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= N) return;
+    int l = blockIdx.y;
+    u64 q = c_pk[l % period].q;
+    size_t x = (size_t)l * N + t;
+    o[x] = a[x] ? q - a[x] : 0;
+}
+
+void k_neg(hs_ctx *c, const u64 *a, u64 *o, int n_limbs, int period, cudaStream_t st)
+{
+    int N = c->P->n;
+    neg_kernel<<<GRID_LIMBS(n_limbs, N), 256, 0, st>>>(a, o, N, period);
+    HS_CHECK_LAUNCH();
+    count_kernel(c);
+}
+
+struct ScalarArg {
+    u64 v[HS_MAXP], vs[HS_MAXP];
+};
+
+static ScalarArg make_scalars(const hs_params *P, const u64 *host_scal, int count)
+{
+    ScalarArg s;
+    for (int i = 0; i < count; i++) {
+        s.v[i] = host_scal[i];
+        s.vs[i] = hs_shoup_const(host_scal[i], P->prime[i]);
+    }
+    return s;
+}
+
+__global__ void mul_scalar_kernel(const u64 *a, u64 *o, ScalarArg s, int N, int period)
+{
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= N) return;
+    int l = blockIdx.y, i = l % period;
+    size_t x = (size_t)l * N + t;
+    o[x] = d_shoup(a[x], s.v[i], s.vs[i], c_pk[i].q);
+}
+
+void k_mul_scalar(hs_ctx *c, const u64 *a, u64 *o, const u64 *host_scal, int n_limbs, int period, cudaStream_t st)
+{
+    int N = c->P->n;
+    mul_scalar_kernel<<<GRID_LIMBS(n_limbs, N), 256, 0, st>>>(a, o, make_scalars(c->P, host_scal, period), N, period);
+    HS_CHECK_LAUNCH();
+    count_kernel(c);
+}
+
+__global__ void mac_scalar_kernel(u64 *acc, const u64 *a, ScalarArg s, int N, int period)
+{
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= N) return;
+    int l = blockIdx.y, i = l % period;
+    size_t x = (size_t)l * N + t;
+    u64 q = c_pk[i].q;
+    acc[x] = d_add(acc[x], d_shoup(a[x], s.v[i], s.vs[i], q), q);
+}
+
+void k_mac_scalar(hs_ctx *c, u64 *acc, const u64 *a, const u64 *host_scal, int n_limbs, int period, cudaStream_t st)
+{
+    int N = c->P->n;
+    mac_scalar_kernel<<<GRID_LIMBS(n_limbs, N), 256, 0, st>>>(acc, a, make_scalars(c->P, host_scal, period), N,
+                                                              period);
+    HS_CHECK_LAUNCH();
+    count_kernel(c);
+}
+
+__global__ void add_scalar_kernel(u64 *a, ScalarArg s, int N)
+{
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= N) return;
+    int l = blockIdx.y;
+    size_t x = (size_t)l * N + t;
+    a[x] = d_add(a[x], s.v[l], c_pk[l].q);
+}
+
+void k_add_scalar(hs_ctx *c, u64 *a, const u64 *host_scal, int n_limbs, cudaStream_t st)
+{
+    int N = c->P->n;
+    ScalarArg s;
+    for (int i = 0; i < n_limbs; i++) s.v[i] = host_scal[i];
+    add_scalar_kernel<<<GRID_LIMBS(n_limbs, N), 256, 0, st>>>(a, s, N);
+    HS_CHECK_LAUNCH();
+    count_kernel(c);
+}
+
+__global__ void mul_pointwise_kernel(const u64 *a, const u64 *b, u64 *o, int N, int pa, int pb)
+{
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= N) return;
+    int l = blockIdx.y, i = l % pa;
+    const PrimeK k = c_pk[i];
+    o[(size_t)l * N + t] = d_mulmod(a[(size_t)l * N + t], b[(size_t)(l % pb) * N + t], k);
+}
+
+void k_mul_pointwise(hs_ctx *c, const u64 *a, const u64 *b, u64 *o, int n_limbs, int period_a, int period_b,
+                     cudaStream_t st)
+{
+    int N = c->P->n;
+    mul_pointwise_kernel<<<GRID_LIMBS(n_limbs, N), 256, 0, st>>>(a, b, o, N, period_a, period_b);
+    HS_CHECK_LAUNCH();
+    count_kernel(c);
+}
+
+// (a0,a1) x (b0,b1) -> (a0b0, a0b1 + a1b0, a1b1); nl limbs per component
+__global__ void tensor_kernel(const u64 *a, const u64 *b, u64 *o, int N, int nl)
+{
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= N) return;
+    int l = blockIdx.y;
+    const PrimeK k = c_pk[l];
+    size_t s = (size_t)nl * N, x = (size_t)l * N + t;
+    u64 a0 = a[x], a1 = a[s + x], b0 = b[x], b1 = b[s + x];
+    o[x] = d_mulmod(a0, b0, k);
+    u64 hi = 0, lo = 0;
+    mac128(hi, lo, a0, b1);
+    mac128(hi, lo, a1, b0);
+    o[s + x] = d_reduce128(hi, lo, k);
+    o[2 * s + x] = d_mulmod(a1, b1, k);
+}
+
+void k_tensor(hs_ctx *c, const u64 *a, const u64 *b, u64 *o, int nl, cudaStream_t st)
+{
+    int N = c->P->n;
+    tensor_kernel<<<GRID_LIMBS(nl, N), 256, 0, st>>>(a, b, o, N, nl);
+    HS_CHECK_LAUNCH();
+    count_kernel(c);
+}
+
+__global__ void permute_kernel(const u64 *a, u64 *o, const unsigned *perm, int N)
+{
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= N) return;
+    size_t l = blockIdx.y;
+    o[l * N + t] = a[l * N + perm[t]];
+}
+
+void k_permute(hs_ctx *c, const u64 *a, u64 *o, const unsigned *perm, int n_limbs, cudaStream_t st)
+{
+    int N = c->P->n;
+    permute_kernel<<<GRID_LIMBS(n_limbs, N), 256, 0, st>>>(a, o, perm, N);
+    HS_CHECK_LAUNCH();
+    count_kernel(c);
+}
+
+// ------------------------------------------------------------------ rescale (C9)
+// last: [ncomp][N] coefficient form of the dropped limb (mod q_level);
+// w[comp][i][t] = centred(last) mod q_i, i < level.
+__global__ void rescale_prep_kernel(const u64 *last, u64 *w, int N, int level)
+{
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= N) return;
+    int i = blockIdx.y, comp = blockIdx.z;
+    u64 ql = c_pk[level].q, q = c_pk[i].q;
+    u64 x = last[(size_t)comp * N + t];
+    u64 v;
+    if (x <= (ql - 1) / 2) v = x % q;
+    else {
+        u64 r = (ql - x) % q;
+        v = r ? q - r : 0;
+    }
+    w[((size_t)comp * level + i) * N + t] = v;
+}
+
+void k_rescale_prep(hs_ctx *c, const u64 *last, u64 *w, int ncomp, int level, cudaStream_t st)
+{
+    int N = c->P->n;
+    rescale_prep_kernel<<<dim3((N + 255) / 256, level, ncomp), 256, 0, st>>>(last, w, N, level);
+    HS_CHECK_LAUNCH();
+    count_kernel(c);
+}
+
+struct RescaleArg {
+    u64 inv[HS_MAXP], inv_sh[HS_MAXP];
+};
+
+__global__ void rescale_final_kernel(const u64 *a, const u64 *w, u64 *o, RescaleArg r, int N, int level)
+{
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= N) return;
+    int i = blockIdx.y, comp = blockIdx.z;
+    u64 q = c_pk[i].q;
+    u64 x = a[((size_t)comp * (level + 1) + i) * N + t];
+    u64 y = w[((size_t)comp * level + i) * N + t];
+    o[((size_t)comp * level + i) * N + t] = d_shoup(d_sub(x, y, q), r.inv[i], r.inv_sh[i], q);
+}
+
+void k_rescale_final(hs_ctx *c, const u64 *a, const u64 *w, u64 *o, int ncomp, int level, cudaStream_t st)
+{
+    const hs_params *P = c->P;
+    RescaleArg r;
+    u64 ql = P->prime[level];
+    for (int i = 0; i < level; i++) {
+        r.inv[i] = hs_invmod(ql % P->prime[i], P->prime[i]);
+        r.inv_sh[i] = hs_shoup_const(r.inv[i], P->prime[i]);
+    }
+    int N = P->n;
+    rescale_final_kernel<<<dim3((N + 255) / 256, level, ncomp), 256, 0, st>>>(a, w, o, r, N, level);
+    HS_CHECK_LAUNCH();
+    count_kernel(c);
+}
+
+// ------------------------------------------------------------------ basis conversion (C7)
+// y_a = x_a * inv_a mod src_a;  out_b = sum_a y_a * c_ab mod dst_b
+struct BconvArg {
+    int n_src, n_dst;
+    unsigned char src[16], dst[HS_MAXP];
+};
+
+__global__ void bconv_kernel(const u64 *__restrict__ x, size_t xs, u64 *o, size_t os, BconvArg A,
+                             const u64 *__restrict__ tab, int N, size_t bxs, size_t bos)
+{
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= N) return;
+    x += blockIdx.y * bxs;
+    o += blockIdx.y * bos;
+    u64 y[16];
+    for (int a = 0; a < A.n_src; a++) {
+        const PrimeK k = c_pk[A.src[a]];
+        y[a] = d_shoup(x[(size_t)a * xs + t], tab[2 * a], tab[2 * a + 1], k.q);
+    }
+    const u64 *cm = tab + 2 * A.n_src;
+    for (int b = 0; b < A.n_dst; b++) {
+        const u64 p = c_pk[A.dst[b]].q;
+        u64 s = 0;
+        for (int a = 0; a < A.n_src; a++) {
+            size_t ci = 2 * ((size_t)a * A.n_dst + b);
+            s = d_add(s, d_shoup(y[a], cm[ci], cm[ci + 1], p), p);
+        }
+        o[(size_t)b * os + t] = s;
+    }
+}
+
+void k_bconv(hs_ctx *c, const BconvTab &tab, const u64 *src, size_t src_stride, u64 *dst, size_t dst_stride,
+             int batch, size_t bss, size_t bds, cudaStream_t st)
+{
+    BconvArg A;
+    A.n_src = tab.n_src;
+    A.n_dst = tab.n_dst;
+    for (int i = 0; i < tab.n_src; i++) A.src[i] = (unsigned char)tab.src[i];
+    for (int i = 0; i < tab.n_dst; i++) A.dst[i] = (unsigned char)tab.dst[i];
+    int N = c->P->n;
+    bconv_kernel<<<dim3((N + 127) / 128, batch), 128, 0, st>>>(src, src_stride, dst, dst_stride, A, tab.dev, N, bss,
+                                                                bds);
+    HS_CHECK_LAUNCH();
+    count_kernel(c);
+}
+
+// ------------------------------------------------------------------ key-switch inner product (C7)
+// targets g = 0..level (q_g) then level+1..level+alpha (p_{g-level-1}).
+// digit j covers Q primes [j alpha, min((j+1) alpha, level+1)); for g in
+// digit j the extended value is d itself, otherwise ext[j][g'] with g' = g
+// (g < lo) or g - dn (g >= hi).  key: [dnum][2][n_q+n_p][N].
+struct KsArg {
+    int level, beta, alpha, n_q, n_t;
+};
+
+__global__ void ks_inner_kernel(const u64 *__restrict__ d, const u64 *__restrict__ ext,
+                                const u64 *__restrict__ key, u64 *acc, KsArg A, int N)
+{
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= N) return;
+    int g = blockIdx.y;
+    const int nl = A.level + 1;
+    const int pi = g < nl ? g : A.n_q + (g - nl);
+    const PrimeK k = c_pk[pi];
+    const size_t ntot = (size_t)A.n_q + A.n_t;  // primes in key layout
+    u64 h0 = 0, l0 = 0, h1 = 0, l1 = 0;
+    for (int j = 0; j < A.beta; j++) {
+        int lo = j * A.alpha, hi = min((j + 1) * A.alpha, nl), dn = hi - lo;
+        u64 v;
+        if (g >= lo && g < hi) v = d[(size_t)g * N + t];
+        else {
+            int gg = g < lo ? g : g - dn;
+            v = ext[((size_t)j * (nl + A.alpha) + gg) * N + t];
+        }
+        u64 k0 = key[(((size_t)j * 2 + 0) * ntot + pi) * N + t];
+        u64 k1 = key[(((size_t)j * 2 + 1) * ntot + pi) * N + t];
+        mac128(h0, l0, v, k0);
+        mac128(h1, l1, v, k1);
+    }
+    acc[(size_t)g * N + t] = d_reduce128(h0, l0, k);
+    acc[((size_t)(nl + A.alpha) + g) * N + t] = d_reduce128(h1, l1, k);
+}
+
+void k_ks_inner(hs_ctx *c, const u64 *d, const u64 *ext, const u64 *key, u64 *acc, int level, int beta,
+                cudaStream_t st)
+{
+    const hs_params *P = c->P;
+    KsArg A{level, beta, P->alpha, P->n_q, P->n_p};
+    int N = P->n;
+    ks_inner_kernel<<<dim3((N + 255) / 256, level + 1 + P->n_p), 256, 0, st>>>(d, ext, key, acc, A, N);
+    HS_CHECK_LAUNCH();
+    count_kernel(c);
+}
+
+// out_c[i] = add_c[i] + (acc_c[i] - conv_c[i]) P^{-1} mod q_i  (add_c may be null)
+struct MdArg {
+    u64 pinv[HS_MAXP], pinv_sh[HS_MAXP];
+    int level, alpha;
+    u64 *o0, *o1;
+    const u64 *a0, *a1;
+};
+
+__global__ void moddown_final_kernel(const u64 *acc, const u64 *conv, MdArg A, int N)
+{
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= N) return;
+    int i = blockIdx.y, comp = blockIdx.z;
+    const int nl = A.level + 1;
+    u64 q = c_pk[i].q;
+    u64 a = acc[((size_t)comp * (nl + A.alpha) + i) * N + t];
+    u64 b = conv[((size_t)comp * nl + i) * N + t];
+    u64 v = d_shoup(d_sub(a, b, q), A.pinv[i], A.pinv_sh[i], q);
+    const u64 *ad = comp ? A.a1 : A.a0;
+    size_t oi = (size_t)i * N + t;
+    if (ad) v = d_add(v, ad[oi], q);
+    (comp ? A.o1 : A.o0)[oi] = v;
+}
+
+void k_moddown_final(hs_ctx *c, const u64 *acc, const u64 *conv, u64 *o0, u64 *o1, const u64 *add0,
+                     const u64 *add1, int level, cudaStream_t st)
+{
+    const hs_params *P = c->P;
+    MdArg A;
+    for (int i = 0; i <= level; i++) {
+        A.pinv[i] = P->p_inv_mod_q[i];
+        A.pinv_sh[i] = hs_shoup_const(P->p_inv_mod_q[i], P->prime[i]);
+    }
+    A.level = level;
+    A.alpha = P->n_p;
+    A.o0 = o0;
+    A.o1 = o1;
+    A.a0 = add0;
+    A.a1 = add1;
+    int N = P->n;
+    moddown_final_kernel<<<dim3((N + 255) / 256, level + 1, 2), 256, 0, st>>>(acc, conv, A, N);
+    HS_CHECK_LAUNCH();
+    count_kernel(c);
+}
+
+// ------------------------------------------------------------------ randomness (C5)
+__host__ __device__ __forceinline__ uint32_t rotl32(uint32_t x, int n) { return (x << n) | (x >> (32 - n)); }
+#define CHQR(a, b, c, d)                  \
+    a += b; d ^= a; d = rotl32(d, 16);    \
+    c += d; b ^= c; b = rotl32(b, 12);    \
+    a += b; d ^= a; d = rotl32(d, 8);     \
+    c += d; b ^= c; b = rotl32(b, 7);
+
+__host__ __device__ void chacha_block(const uint32_t key[8], uint32_t ctr, const uint32_t nonce[3], uint32_t o[16])
+{
+    uint32_t s[16] = {0x61707865u, 0x3320646eu, 0x79622d32u, 0x6b206574u, key[0], key[1], key[2], key[3],
+                      key[4],      key[5],      key[6],      key[7],      ctr,    nonce[0], nonce[1], nonce[2]};
+    uint32_t x[16];
+    for (int i = 0; i < 16; i++) x[i] = s[i];
+    for (int r = 0; r < 10; r++) {
+        CHQR(x[0], x[4], x[8], x[12]);
+        CHQR(x[1], x[5], x[9], x[13]);
+        CHQR(x[2], x[6], x[10], x[14]);
+        CHQR(x[3], x[7], x[11], x[15]);
+        CHQR(x[0], x[5], x[10], x[15]);
+        CHQR(x[1], x[6], x[11], x[12]);
+        CHQR(x[2], x[7], x[8], x[13]);
+        CHQR(x[3], x[4], x[9], x[14]);
+    }
+    for (int i = 0; i < 16; i++) o[i] = x[i] + s[i];
+}
+
+void hs_chacha20_block(const uint32_t key[8], uint32_t counter, const uint32_t nonce[3], uint32_t out[16])
+{
+    chacha_block(key, counter, nonce, out);
+}
+
+u64 hs_stream_word(u64 seed, uint32_t tag, u64 sub, u64 idx)
+{
+    uint32_t key[8] = {(uint32_t)seed, (uint32_t)(seed >> 32), tag, (uint32_t)sub, (uint32_t)(sub >> 32), 0, 0, 0};
+    uint32_t nonce[3] = {0, 0, 0}, o[16];
+    chacha_block(key, (uint32_t)(idx >> 3), nonce, o);
+    int w = (int)(idx & 7);
+    return (u64)o[2 * w] | ((u64)o[2 * w + 1] << 32);
+}
+
+// uniform mod q: sample idx2 = pi*N + t uses stream words 2 idx2, 2 idx2 + 1,
+// value = (w1 2^64 + w0) mod q.  One ChaCha block = 4 samples.
+__global__ void uniform_kernel(u64 *o, PrimeMap pm, u64 seed, uint32_t tag, u64 sub, int N)
+{
+    int blk = blockIdx.x * blockDim.x + threadIdx.x;  // block within limb
+    if (blk * 4 >= N) return;
+    int l = blockIdx.y, pi = pm.p[l % pm.n];
+    const PrimeK k = c_pk[pi];
+    uint32_t key[8] = {(uint32_t)seed, (uint32_t)(seed >> 32), tag, (uint32_t)sub, (uint32_t)(sub >> 32), 0, 0, 0};
+    uint32_t nonce[3] = {0, 0, 0}, w[16];
+    u64 idx2_0 = (u64)pi * N + (u64)blk * 4;
+    chacha_block(key, (uint32_t)(idx2_0 >> 2), nonce, w);
+    for (int s = 0; s < 4; s++) {
+        u64 w0 = (u64)w[4 * s] | ((u64)w[4 * s + 1] << 32);
+        u64 w1 = (u64)w[4 * s + 2] | ((u64)w[4 * s + 3] << 32);
+        u64 h = d_reduce128(0, w1, k);
+        o[(size_t)l * N + blk * 4 + s] = d_reduce128(h, w0, k);
+    }
+}
+
+void k_uniform(hs_ctx *c, u64 *o, int n_limbs, const PrimeMap &pm, u64 seed, uint32_t tag, u64 sub, int,
+               cudaStream_t st)
+{
+    int N = c->P->n;
+    int nb = N / 4;
+    uniform_kernel<<<dim3((nb + 127) / 128, n_limbs), 128, 0, st>>>(o, pm, seed, tag, sub, N);
+    HS_CHECK_LAUNCH();
+    count_kernel(c);
+}
+
+// centred binomial: coefficient t uses stream word t
+__global__ void cbd_kernel(int64_t *o, u64 seed, uint32_t tag, u64 sub, int eta, int N)
+{
+    int blk = blockIdx.x * blockDim.x + threadIdx.x;
+    if (blk * 8 >= N) return;
+    uint32_t key[8] = {(uint32_t)seed, (uint32_t)(seed >> 32), tag, (uint32_t)sub, (uint32_t)(sub >> 32), 0, 0, 0};
+    uint32_t nonce[3] = {0, 0, 0}, w[16];
+    chacha_block(key, (uint32_t)blk, nonce, w);
+    u64 m = (1ull << eta) - 1;
+    for (int s = 0; s < 8; s++) {
+        u64 x = (u64)w[2 * s] | ((u64)w[2 * s + 1] << 32);
+        o[blk * 8 + s] = (int64_t)__popcll(x & m) - (int64_t)__popcll((x >> eta) & m);
+    }
+}
+
+void k_cbd(hs_ctx *c, int64_t *o, u64 seed, uint32_t tag, u64 sub, int eta, cudaStream_t st)
+{
+    int N = c->P->n;
+    cbd_kernel<<<(N / 8 + 127) / 128, 128, 0, st>>>(o, seed, tag, sub, eta, N);
+    HS_CHECK_LAUNCH();
+    count_kernel(c);
+}
+
+__global__ void signed_to_rns_kernel(const int64_t *v, u64 *o, PrimeMap pm, int N)
+{
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= N) return;
+    int l = blockIdx.y;
+    u64 q = c_pk[pm.p[l % pm.n]].q;
+    int64_t x = v[t];
+    u64 r = x >= 0 ? (u64)x % q : (u64)(-(x + 1)) % q;  // |x| - 1 for negatives avoids overflow
+    if (x < 0) r = q - 1 - r;
+    o[(size_t)l * N + t] = r;
+}
+
+void k_signed_to_rns(hs_ctx *c, const int64_t *v, u64 *o, int n_limbs, const PrimeMap &pm, cudaStream_t st)
+{
+    int N = c->P->n;
+    signed_to_rns_kernel<<<GRID_LIMBS(n_limbs, N), 256, 0, st>>>(v, o, pm, N);
+    HS_CHECK_LAUNCH();
+    count_kernel(c);
+}

@@ -1,0 +1,117 @@
+// poly.cpp -- Chebyshev-series evaluation on ciphertexts (C13).
+//
+// PAPER.md 330-336 (sec 2.2.4): degree d costs ~ceil(log(d+1)) levels and
+// O(sqrt d) ct-ct products (Paterson-Stockmeyer).  The exact tree (shared with
+// the oracle as a written convention, not as code):
+//   t = ceil(log2(d+1)); baby size B = 2^ceil(t/2) (B = 2 when d <= 1);
+//   T_1 = u, T_i = 2 T_a T_b - T_{a-b} (a = 2^(ceil(log2 i)-1), b = i-a;
+//   a == b: 2 T_a^2 - 1); giants G_j = T_{B 2^j} by doubling;
+//   rec(p, target): deg < B -> leaf; else split at g = 2^(ceil(log2(deg+1))-1):
+//     q_0 = c_g, q_k = 2 c_{g+k};  r_j = c_j, r_{g-k} = c_{g-k} - c_{g+k};
+//     out = rec(q, target+1) * T_g + rec(r, target)
+//   leaf: rescale(sum_i rint(c_i sc_i) T_i|target+1) + c_0   (one rescale)
+//   target = level(u) - depth(d), depth = t+1 (d >= 2) or 1.
+//   The affine map u = (2x-a-b)/(b-a) costs one level (mult_const + add_const)
+//   unless [a, b] = [-1, 1].
+#include <vector>
+
+#include "hs_internal.h"
+
+static int clog2(int x)
+{
+    int t = 0;
+    while ((1 << t) < x) t++;
+    return t;
+}
+
+int cheb_depth(int deg) { return deg <= 1 ? 1 : clog2(deg + 1) + 1; }
+
+namespace {
+
+struct Basis {
+    const hs_keys *K;
+    cudaStream_t st;
+    int B;
+    std::vector<CtP> T;  // T[0] unused
+    std::vector<CtP> G;
+};
+
+CtP dbl_minus_one(const hs_keys *K, const hs_ct *x, cudaStream_t st)
+{
+    CtP s = ev_mult(K, x, x, st);
+    CtP s2 = ev_mult_int(s.get(), 2, st);
+    return ev_add_const(s2.get(), -1.0, st);
+}
+
+CtP leaf(Basis &E, const std::vector<double> &c, int target)
+{
+    std::vector<const hs_ct *> terms;
+    std::vector<double> coef;
+    for (size_t i = 1; i < c.size(); i++) {
+        terms.push_back(E.T[i].get());
+        coef.push_back(c[i]);
+    }
+    if (terms.empty()) {
+        terms.push_back(E.T[1].get());
+        coef.push_back(0.0);
+    }
+    CtP s = ev_mult_const_sum(terms, coef, target, E.st);
+    return ev_add_const(s.get(), c[0], E.st);
+}
+
+CtP rec(Basis &E, const std::vector<double> &c, int target)
+{
+    const int d = (int)c.size() - 1;
+    if (d < E.B) return leaf(E, c, target);
+    const int g = 1 << (clog2(d + 1) - 1);
+    std::vector<double> q(d - g + 1), r(c.begin(), c.begin() + g);
+    q[0] = c[g];
+    for (int k = 1; k <= d - g; k++) {
+        q[k] = 2.0 * c[g + k];
+        r[g - k] = c[g - k] - c[g + k];
+    }
+    CtP Q = rec(E, q, target + 1);
+    CtP QT = ev_mult(E.K, Q.get(), E.G[clog2(g / E.B)].get(), E.st);
+    CtP R = rec(E, r, target);
+    return ev_add(QT.get(), R.get(), false, E.st);
+}
+
+CtP eval_unit(const hs_keys *K, const hs_ct *u, const hs_poly *p, cudaStream_t st)
+{
+    const int d = p->deg;
+    Basis E{K, st, 0, {}, {}};
+    const int t = clog2(d + 1);
+    E.B = d <= 1 ? 2 : 1 << ((t + 1) / 2);
+    E.T.resize(E.B);
+    E.T[1] = ct_copy(u, st);
+    for (int i = 2; i < E.B; i++) {
+        int a = 1 << (clog2(i) - 1), b = i - a;
+        if (a == b) {
+            E.T[i] = dbl_minus_one(K, E.T[a].get(), st);
+        } else {
+            CtP m = ev_mult(K, E.T[a].get(), E.T[b].get(), st);
+            CtP m2 = ev_mult_int(m.get(), 2, st);
+            E.T[i] = ev_add(m2.get(), E.T[a - b].get(), true, st);
+        }
+    }
+    const int ng = std::max(0, t - clog2(E.B));
+    for (int j = 0; j < ng; j++) E.G.push_back(dbl_minus_one(K, j == 0 ? E.T[E.B / 2].get() : E.G[j - 1].get(), st));
+    const int target = u->level - cheb_depth(d);
+    if (target < 0) throw HsError(HS_ELEVEL, "polynomial deeper than the remaining levels");
+    std::vector<double> c(p->coeffs, p->coeffs + d + 1);
+    return rec(E, c, target);
+}
+
+}  // namespace
+
+CtP ev_cheb(const hs_keys *K, const hs_ct *x, const hs_poly *p, cudaStream_t st)
+{
+    if (!p || p->deg < 1 || !p->coeffs || !(p->b > p->a)) throw HsError(HS_EINVAL, "bad polynomial");
+    if (p->a == -1.0 && p->b == 1.0) return eval_unit(K, x, p, st);
+    const double alpha = 2.0 / (p->b - p->a);
+    const double beta = -(p->a + p->b) / (p->b - p->a);
+    if (x->level < 1) throw HsError(HS_ELEVEL, "no level left for the affine map");
+    CtP m = ev_mult_const(x, alpha, x->level - 1, st);
+    CtP u = ev_add_const(m.get(), beta, st);
+    return eval_unit(K, u.get(), p, st);
+}

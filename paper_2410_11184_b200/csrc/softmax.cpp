@@ -1,0 +1,116 @@
+// softmax.cpp -- the paper's Softmax over packed ciphertexts (product side).
+//
+//   Alg 1 normalize-and-square   PAPER.md 776-787 [sec 3.3, alg:Softmax]
+//   Alg 2 auxiliary thread       PAPER.md 904-921 [sec 3.4.1, alg:AuxThread]
+//   version B                    PAPER.md 168-181 [sec 4.3], exponent -1/2^j (G4)
+//   one / many ciphertexts       PAPER.md 94-131 [sec 4.1-4.2]
+//   shared aux sum               DESIGN.md C15 / G6: sum_c tensor(y_c, y_c)
+//                                exactly mod q, ONE relin + rescale
+//   bootstrap placement          PAPER.md 429-440 [sec 5.1.3], rule G12
+//
+// Sharding: rank r owns ciphertexts [r m/G, (r+1) m/G).
+// The only exchange is the degree-2 partial aux sum of each iteration; the
+// gathered partials are added mod q (exact, order-free), so every rank runs
+// the replicated aux thread on identical words and all outputs are identical
+// to the single-GPU run.
+#include <vector>
+
+#include "hs_internal.h"
+
+namespace {
+
+int poly_cost(const hs_poly *p) { return cheb_depth(p->deg) + ((p->a == -1.0 && p->b == 1.0) ? 0 : 1); }
+
+void rot_sum(const hs_keys *K, CtP &S, int nb, int stride, int sign, cudaStream_t st)
+{
+    for (int i = 0; (1 << i) < nb; i++) {
+        CtP r = ev_rotate(K, S.get(), sign * stride * (1 << i), st);
+        S = ev_add(S.get(), r.get(), false, st);
+    }
+}
+
+[[noreturn]] void level_error(const char *what) { throw HsError(HS_ELEVEL, std::string("softmax: ") + what); }
+
+}  // namespace
+
+hs_status softmax_run(hs_ctx *c, const hs_keys *K, const hs_softmax_desc *d, const hs_ct *const *in,
+                      size_t m_local, cudaStream_t st, hs_ct **out)
+{
+    const hs_params *P = c->P;
+    const int N0 = P->n / 2;
+    const int m = d->m, n = d->n, world = d->world < 1 ? 1 : d->world;
+    if (m < 1 || n < 1 || n % m || d->k < 1 || !d->exp_poly || !d->inv_poly || d->variant < 0 || d->variant > 1)
+        throw HsError(HS_EINVAL, "softmax: bad descriptor");
+    if (m % world || (size_t)(m / world) != m_local) throw HsError(HS_EINVAL, "softmax: m_local != m / world");
+    if (world > 1 && !d->exchange) throw HsError(HS_EINVAL, "softmax: world > 1 needs an exchange callback");
+    const int nb = n / m;
+    if ((nb & (nb - 1)) || nb > N0) throw HsError(HS_EINVAL, "softmax: n/m must be a power of two <= N0");
+    const int stride = N0 / nb;
+    const int ml = (int)m_local;
+    for (int i = 0; i < ml; i++)
+        if (!in[i] || in[i]->ncomp != 2 || in[i]->level != in[0]->level)
+            throw HsError(HS_EINVAL, "softmax: inputs must be degree-1 ciphertexts at one level");
+    std::vector<double> mask(N0, 0.0);
+    for (int s = 0; s < stride; s++) mask[s] = 1.0;  // G10: coordinate block 0
+
+    std::vector<CtP> y0(ml), y(ml);
+    // y^(0) = exp(x / 2^k)
+    for (int i = 0; i < ml; i++) {
+        if (in[i]->level < poly_cost(d->exp_poly)) level_error("input level too low for exp");
+        y0[i] = ev_cheb(K, in[i], d->exp_poly, st);
+        y[i] = ct_copy(y0[i].get(), st);
+    }
+    CtP lam;
+    for (int j = 1; j <= d->k; j++) {
+        const hs_poly *ip = &d->inv_poly[j - 1];
+        if (d->variant == 0 && y[0]->level < 2) level_error("main thread needs bootstrapping (not available)");
+        if (y[0]->level < 1) level_error("main thread out of levels");
+        // ---- auxiliary thread: S = relin(sum tensor(y, y)) -> rescale
+        CtP acc;
+        for (int i = 0; i < ml; i++) {
+            CtP t = ev_tensor(y[i].get(), y[i].get(), st);
+            acc = acc ? ev_add(acc.get(), t.get(), false, st) : std::move(t);
+        }
+        if (world > 1) {
+            const size_t words = acc->limbs() * P->n;
+            DBuf gathered(words * world, st);
+            if (d->exchange(d->exchange_user, acc->d, gathered.p, words, st) != 0)
+                throw HsError(HS_ENCCL, "softmax: exchange callback failed");
+            // sum in rank order (exact modular addition)
+            HS_CUDA(cudaMemcpyAsync(acc->d, gathered.p, words * 8, cudaMemcpyDeviceToDevice, st));
+            for (int r = 1; r < world; r++)
+                k_add(c, acc->d, gathered.p + r * words, acc->d, (int)acc->limbs(), acc->level + 1, false, st);
+        }
+        CtP rl = ev_relin(K, acc.get(), st);
+        acc.reset();
+        CtP S = ev_rescale(rl.get(), st);
+        rl.reset();
+        rot_sum(K, S, nb, stride, -1, st);
+        const int main_level = d->variant == 0 ? y[0]->level : y0[0]->level;
+        const int need = poly_cost(ip) + 1 + ((d->variant == 1 && j > 1) ? 1 : 0);
+        if (S->level - need < main_level && S->level - need < 0) level_error("aux thread needs bootstrapping");
+        CtP lj = ev_cheb(K, S.get(), ip, st);
+        S.reset();
+        if (lj->level < 1) level_error("no level for the mask");
+        lj = ev_mult_pt(lj.get(), mask.data(), nullptr, lj->level - 1, st);
+        rot_sum(K, lj, nb, stride, +1, st);
+        if (d->variant == 1 && j > 1) lam = ev_mult(K, lam.get(), lj.get(), st);
+        else lam = std::move(lj);
+        // ---- main thread
+        for (int i = 0; i < ml; i++) {
+            if (d->variant == 0) {
+                CtP z = ev_mult(K, lam.get(), y[i].get(), st);
+                y[i] = ev_mult(K, z.get(), z.get(), st);
+            } else {
+                CtP z = ev_mult(K, lam.get(), y0[i].get(), st);
+                for (int s = 0; s < j; s++) {
+                    if (z->level < 1) level_error("version B squaring out of levels");
+                    z = ev_mult(K, z.get(), z.get(), st);
+                }
+                y[i] = std::move(z);
+            }
+        }
+    }
+    for (int i = 0; i < ml; i++) out[i] = y[i].release();
+    return HS_OK;
+}

@@ -1,0 +1,215 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle: every
+ciphertext word must be identical, and decrypted
+Softmax outputs within 2^-15 of float64 Softmax (north_star tolerance)."""
+import numpy as np
+import pytest
+
+import workloads as W
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _hs():
+    import paper_2410_11184_b200 as hs
+    return hs
+
+
+class Pair:
+    """the same preset / keys on both sides"""
+
+    def __init__(self, preset, seed, galois_rots=(), conj=False, relin=True):
+        hs = _hs()
+        self.pre = W.preset(preset)
+        self.P = hs.Params.from_preset(self.pre)
+        self.ctx = hs.Context(self.P, 0)
+        self.PO = O.Params.from_preset(self.pre)
+        gal = sorted({self.P.galois_of_rot(r) for r in galois_rots} | ({2 * self.P.n - 1} if conj else set()))
+        self.gal = gal
+        self.K = hs.Keys(self.ctx, seed, self.pre["h"], galois=gal, relin=relin)
+        self.KO = O.Keys(self.PO, seed, self.pre["h"], galois=gal, relin=relin)
+        self.top = len(self.pre["q_bits"]) - 1
+
+    def enc(self, z, level, idx, use_sk=False):
+        hs = _hs()
+        pt = self.P.encode(np.real(z), np.imag(z) if np.iscomplexobj(z) else None, scale=self.P.scale(level),
+                           level=level)
+        seed = 555 + idx
+        return hs.encrypt(self.K, pt, level, seed, idx, use_sk), O.encrypt(self.PO, self.KO, pt, level, seed, idx,
+                                                                           use_sk)
+
+
+def same(g, o):
+    wg, wo = g.words(), o.words()
+    assert wg.shape == wo.shape
+    bad = np.argwhere(wg != wo)
+    assert bad.size == 0, f"{len(bad)} words differ, first at {bad[:3].tolist()}"
+
+
+@pytest.fixture(scope="module")
+def toy():
+    return Pair("TOY12", 4242, galois_rots=[1, -1, 3, 128, -128, 256, -256, 512, -512, 1024, -1024], conj=True)
+
+
+@pytest.mark.parametrize("preset", ["TOY12", "P16U"])
+def test_ntt_parity(preset):
+    hs = _hs()
+    pre = W.preset(preset)
+    P, PO = hs.Params.from_preset(pre), O.Params.from_preset(pre)
+    ctx = hs.Context(P, 0)
+    rng = np.random.default_rng(1)
+    np_ = len(P.primes)
+    host = np.stack([rng.integers(0, q, P.n, dtype=np.uint64) for q in P.primes])
+    dev = torch.from_numpy(host.view(np.int64)).cuda()
+    ctx.ntt(dev.data_ptr(), 0, np_, inverse=False)
+    got = dev.cpu().numpy().view(np.uint64)
+    for i in range(np_):
+        assert (got[i] == PO.ntt(i, host[i])).all(), i
+    ctx.ntt(dev.data_ptr(), 0, np_, inverse=True)
+    assert (dev.cpu().numpy().view(np.uint64) == host).all()
+
+
+def test_keygen_parity(toy):
+    assert (toy.K.secret() == toy.KO.secret()).all()
+    assert (toy.K.swk(0) == toy.KO.swk(0)).all()
+    for g in toy.gal[:3]:
+        assert (toy.K.swk(g) == toy.KO.swk(g)).all()
+
+
+@pytest.mark.parametrize("use_sk", [False, True])
+def test_encrypt_parity(toy, use_sk):
+    rng = np.random.default_rng(2)
+    z = rng.uniform(-1, 1, toy.P.n // 2)
+    g, o = toy.enc(z, toy.top, 3, use_sk)
+    same(g, o)
+    hs = _hs()
+    assert (hs.decrypt(toy.K, g) == O.decrypt(toy.PO, toy.KO, o)).all()
+    assert np.abs(hs.decrypt_decode(toy.K, g).real - z).max() < 2.0 ** -22
+
+
+def test_ops_parity(toy):
+    hs = _hs()
+    rng = np.random.default_rng(3)
+    za, zb = rng.uniform(-1, 1, toy.P.n // 2), rng.uniform(-1, 1, toy.P.n // 2)
+    a, ao = toy.enc(za, toy.top, 0)
+    b, bo = toy.enc(zb, 12, 1)
+    K, KO, PO = toy.K, toy.KO, toy.PO
+    cases = [("add", dict(b=(b, bo))), ("sub", dict(b=(b, bo))), ("mult", dict(b=(b, bo))),
+             ("tensor", dict(b=(b, bo))), ("rescale", {}), ("level_down", dict(i=5)),
+             ("mult_const", dict(c=-0.731, i=9)), ("add_const", dict(c=0.3125)), ("mult_int", dict(i=-3)),
+             ("rotate", dict(i=3)), ("rotate", dict(i=-128)), ("conj", {})]
+    for name, kw in cases:
+        bb = kw.get("b", (None, None))
+        g = hs.op(K, name, a, bb[0], c=kw.get("c", 0.0), i=kw.get("i", 0))
+        o = O.op(PO, KO, name, ao, bb[1], c=kw.get("c", 0.0), i=kw.get("i", 0))
+        same(g, o)
+    t = hs.op(K, "tensor", a, b)
+    to = O.op(PO, KO, "tensor", ao, bo)
+    same(hs.op(K, "relin", t), O.op(PO, KO, "relin", to))
+    mask = (np.arange(toy.P.n // 2) % 5 == 0).astype(float)
+    same(hs.mult_pt(a, mask, target=10), O.mult_pt(PO, ao, mask, target=10))
+
+
+def test_keyswitch_parity(toy):
+    hs = _hs()
+    rng = np.random.default_rng(4)
+    P = toy.P
+    for level in [toy.top, 6, 0]:
+        d = np.stack([rng.integers(0, P.primes[i], P.n, dtype=np.uint64) for i in range(level + 1)])
+        dd = torch.from_numpy(d.view(np.int64)).cuda()
+        o0 = torch.empty_like(dd)
+        o1 = torch.empty_like(dd)
+        for g in [0, toy.gal[0]]:
+            hs.keyswitch(toy.K, g, level, dd.data_ptr(), o0.data_ptr(), o1.data_ptr())
+            torch.cuda.synchronize()
+            e0, e1 = O.keyswitch(toy.PO, toy.KO, g, level, d)
+            assert (o0.cpu().numpy().view(np.uint64) == e0).all()
+            assert (o1.cpu().numpy().view(np.uint64) == e1).all()
+
+
+@pytest.mark.parametrize("deg,a,b", [(7, -2.0, 0.0), (15, 2.0, 16.5), (31, -1.0, 1.0), (3, 0.25, 1.5)])
+def test_cheb_parity(toy, deg, a, b):
+    hs = _hs()
+    rng = np.random.default_rng(deg)
+    coeffs = rng.normal(0, 1, deg + 1) / (1 + np.arange(deg + 1)) ** 2
+    coeffs[2] = 0.0  # exercise the zero-coefficient skip
+    z = rng.uniform(a, b, toy.P.n // 2)
+    g, o = toy.enc(z, toy.top, 7)
+    p = dict(a=a, b=b, coeffs=coeffs)
+    same(hs.cheb(toy.K, g, p), O.cheb(toy.PO, toy.KO, o, p))
+
+
+def _softmax_case(tables, preset, table, m, L, tag):
+    hs = _hs()
+    tab = tables[table]
+    cfg = tab["config"]
+    n, k, M = cfg["n"], cfg["k"], cfg["M"]
+    pre = W.preset(preset)
+    P = hs.Params.from_preset(pre)
+    PO = O.Params.from_preset(pre)
+    gal = O.softmax_rotation_galois(PO, n, m)
+    ctx = hs.Context(P, 0)
+    seed = W.derive_seed("keys", tag)
+    K, KO = hs.Keys(ctx, seed, pre["h"], galois=gal), O.Keys(PO, seed, pre["h"], galois=gal)
+    x = W.softmax_inputs(L, n, M, seed=W.derive_seed("x", tag))
+    slots = P.pack(x, m)
+    top = len(pre["q_bits"]) - 1
+    es = W.derive_seed("enc", tag)
+    g_in, o_in = [], []
+    for c in range(m):
+        pt = P.encode(slots[c], scale=P.scale(top), level=top)
+        g_in.append(hs.encrypt(K, pt, top, es, c))
+        o_in.append(O.encrypt(PO, KO, pt, top, es, c))
+    var = 0 if cfg["variant"] == "A" else 1
+    if m == 1:
+        g_out = [hs.softmax_one_ctxt(K, g_in[0], n, k, var, tab["exp"], tab["inv"])]
+    else:
+        g_out = hs.softmax_many_ctxt(K, g_in, n, m, k, var, tab["exp"], tab["inv"])
+    o_out = O.softmax(PO, KO, o_in, n, k, var, tab["exp"], tab["inv"])
+    for g, o in zip(g_out, o_out):
+        same(g, o)
+    dec = np.stack([hs.decrypt_decode(K, c).real for c in g_out])
+    y = P.unpack(dec, L, n)
+    ref = np.exp(x - x.max(1, keepdims=True))
+    ref /= ref.sum(1, keepdims=True)
+    assert np.abs(y - ref).max() < 2.0 ** -15
+    return ctx.ledger()
+
+
+def test_softmax_config1_parity(tables):
+    led = _softmax_case(tables, "TOY12", "toy_n16_M2_k1_A", 1, 128, "config1")
+    assert led["rot"] == 2 * 4
+
+
+@pytest.mark.parametrize("table", ["toy_n16_M4_k2_A", "toy_n16_M4_k2_B"])
+def test_softmax_many_parity(tables, table):
+    _softmax_case(tables, "TOY12D", table, 2, 256, "many-" + table)
+
+
+# ---------------------------------------------------------------- full size (N = 2^16)
+@pytest.fixture(scope="module")
+def p16():
+    return Pair("P16U", 16161, galois_rots=[1, -128])
+
+
+def test_p16_hmult_rotate_parity(p16):
+    """BASELINE.json configs 2-5 ring (N = 2^16, user chain): HMult, rotation
+    and rescale at the top user level, word-for-word."""
+    hs = _hs()
+    rng = np.random.default_rng(6)
+    za, zb = rng.uniform(-1, 1, p16.P.n // 2), rng.uniform(-1, 1, p16.P.n // 2)
+    a, ao = p16.enc(za, 12, 0)
+    b, bo = p16.enc(zb, 12, 1)
+    m = hs.op(p16.K, "mult", a, b)
+    same(m, O.op(p16.PO, p16.KO, "mult", ao, bo))
+    r = hs.op(p16.K, "rotate", a, i=-128)
+    same(r, O.op(p16.PO, p16.KO, "rotate", ao, i=-128))
+    assert np.abs(hs.decrypt_decode(p16.K, m).real - za * zb).max() < 2.0 ** -20

@@ -15,7 +15,7 @@ orc_ct *orc_encrypt_sk(const orc_params *, const orc_keys *, const u64 *, int, u
 void orc_decrypt(const orc_params *, const orc_keys *, const orc_ct *, u64 *);
 double orc_encode_naive_coeff(const orc_params *, const double *, const double *, double, int);
 
-typedef orc_ct *(*orc_bts_fn)(const orc_params *, const orc_keys *, const orc_ct *, void *);
+typedef orc_ct *(*orc_bts_fn)(const orc_params *, const orc_keys *, const orc_ct *, void *, double);
 typedef struct {
     int n, m, k, variant;
     const orc_cheb *exp_poly;
@@ -178,3 +178,46 @@ int orc_api_softmax(const orc_params *P, const orc_keys *K, int n, int m, int k,
 
 void orc_api_ledger(long *out) { memcpy(out, orc_ledger, sizeof(orc_ledger)); }
 void orc_api_ledger_reset(void) { memset(orc_ledger, 0, sizeof(orc_ledger)); }
+
+/* ---------------------------------------------------------------- bootstrapping */
+typedef struct orc_bts_set orc_bts_set;
+orc_bts_set *orc_bts_set_new(const orc_params *P, int K, int r, int deg, const double *coeffs, int out_level);
+void orc_bts_set_free(orc_bts_set *S);
+int orc_bts_rotations(const orc_params *P, int *out, int max);
+int orc_bts_exponent(const orc_params *P, double bound);
+orc_ct *orc_bootstrap(const orc_params *P, const orc_keys *K, const orc_ct *in, void *ctx, double bound);
+
+void *orc_api_bts_new(const orc_params *P, int K, int r, int deg, const double *coeffs, int out_level)
+{
+    return orc_bts_set_new(P, K, r, deg, coeffs, out_level);
+}
+void orc_api_bts_free(void *p) { orc_bts_set_free(p); }
+int orc_api_bts_rotations(const orc_params *P, int *out, int max) { return orc_bts_rotations(P, out, max); }
+int orc_api_bts_exponent(const orc_params *P, double bound) { return orc_bts_exponent(P, bound); }
+orc_ct *orc_api_bootstrap(const orc_params *P, const orc_keys *K, const orc_ct *in, void *bts, double bound)
+{
+    return orc_bootstrap(P, K, in, bts, bound);
+}
+int orc_api_softmax_bts(const orc_params *P, const orc_keys *K, int n, int m, int k, int variant,
+                        const int *degs, const double *as, const double *bs, const double *coeffs,
+                        orc_ct *const *in, orc_ct **out, void *bts)
+{
+    orc_cheb *polys = malloc(sizeof(orc_cheb) * (k + 1));
+    const double *cp = coeffs;
+    for (int i = 0; i <= k; i++) {
+        polys[i].deg = degs[i];
+        polys[i].a = as[i];
+        polys[i].b = bs[i];
+        polys[i].c = cp;
+        cp += degs[i] + 1;
+    }
+    orc_softmax_desc d = {n, m, k, variant, &polys[0], &polys[1], bts ? orc_bootstrap : NULL, bts};
+    int rc = orc_softmax(P, K, &d, in, out);
+    free(polys);
+    return rc;
+}
+
+extern int orc_bts_debug_stop;
+void orc_api_bts_debug_stop(int s) { orc_bts_debug_stop = s; }
+extern int orc_bts_debug_skip_raise;
+void orc_api_bts_debug_skip_raise(int s) { orc_bts_debug_skip_raise = s; }

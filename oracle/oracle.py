@@ -340,3 +340,70 @@ def softmax_rotation_galois(P, n, m):
         out.add(P.galois_of_rot(-(stride << i)))
         i += 1
     return sorted(out)
+
+
+# ---------------------------------------------------------------- bootstrapping (G11)
+def _bts_sigs():
+    L = lib()
+    if getattr(L, "_bts_ready", False):
+        return L
+    vp = C.c_void_p
+    L.orc_api_bts_new.restype = vp
+    L.orc_api_bts_new.argtypes = [vp, C.c_int, C.c_int, C.c_int, f64p, C.c_int]
+    L.orc_api_bts_free.argtypes = [vp]
+    L.orc_api_bts_rotations.restype = C.c_int
+    L.orc_api_bts_rotations.argtypes = [vp, i32p, C.c_int]
+    L.orc_api_bootstrap.restype = vp
+    L.orc_api_bootstrap.argtypes = [vp, vp, vp, vp, C.c_double]
+    L.orc_api_bts_exponent.restype = C.c_int
+    L.orc_api_bts_exponent.argtypes = [vp, C.c_double]
+    L.orc_api_softmax_bts.restype = C.c_int
+    L.orc_api_softmax_bts.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, i32p, f64p, f64p, f64p,
+                                      C.POINTER(vp), C.POINTER(vp), vp]
+    L._bts_ready = True
+    return L
+
+
+def bts_rotations(P: Params):
+    out = np.zeros(256, np.int32)
+    n = _bts_sigs().orc_api_bts_rotations(P.ptr, out, 256)
+    return [int(v) for v in out[:n]]
+
+
+class Bts:
+    """Precomputed bootstrapping plan (diagonals encoded in quad precision)."""
+
+    def __init__(self, P: Params, table: dict, out_level: int):
+        c = np.ascontiguousarray(table["coeffs"], np.float64)
+        self.P = P
+        self.ptr = _bts_sigs().orc_api_bts_new(P.ptr, table["K"], table["r"], len(c) - 1, c, out_level)
+
+    def __del__(self):
+        if getattr(self, "ptr", None) and _lib is not None:
+            _lib.orc_api_bts_free(self.ptr)
+            self.ptr = None
+
+
+def bootstrap(P: Params, K: Keys, ct: Ct, bts: Bts, bound: float = 1.0) -> Ct:
+    """bound: upper bound on |slot values| (selects the pre-scaling exponent, G11)"""
+    return Ct(P, _bts_sigs().orc_api_bootstrap(P.ptr, K.ptr, ct.ptr, bts.ptr, bound))
+
+
+def bts_exponent(P: Params, bound: float) -> int:
+    return int(_bts_sigs().orc_api_bts_exponent(P.ptr, bound))
+
+
+def softmax_bts(P: Params, K: Keys, cts, n, k, variant, exp_poly, inv_polys, bts: Bts):
+    polys = [exp_poly] + list(inv_polys)
+    degs = np.array([len(p["coeffs"]) - 1 for p in polys], np.int32)
+    a_s = np.array([p["a"] for p in polys], np.float64)
+    b_s = np.array([p["b"] for p in polys], np.float64)
+    co = np.concatenate([np.asarray(p["coeffs"], np.float64) for p in polys])
+    m = len(cts)
+    ins = (C.c_void_p * m)(*[c.ptr for c in cts])
+    outs = (C.c_void_p * m)()
+    rc = _bts_sigs().orc_api_softmax_bts(P.ptr, K.ptr, n, m, k, variant, degs, a_s, b_s, co, ins, outs,
+                                         bts.ptr if bts is not None else None)
+    if rc != 0:
+        raise RuntimeError(f"oracle softmax failed rc={rc}")
+    return [Ct(P, outs[i]) for i in range(m)]

@@ -17,8 +17,9 @@
 #include "orc.h"
 #include <stdlib.h>
 #include <string.h>
+#include <math.h>
 
-typedef orc_ct *(*orc_bts_fn)(const orc_params *, const orc_keys *, const orc_ct *, void *);
+typedef orc_ct *(*orc_bts_fn)(const orc_params *, const orc_keys *, const orc_ct *, void *, double);
 
 typedef struct {
     int n, m, k, variant;           /* variant 0 = Alg 1, 1 = Alg B */
@@ -46,13 +47,12 @@ static int rot_sum(const orc_params *P, const orc_keys *K, orc_ct **S, int nb, i
     return ORC_OK;
 }
 
-static int bts_or_fail(const orc_params *P, const orc_keys *K, const orc_softmax_desc *d, orc_ct **c)
+static int bts_or_fail(const orc_params *P, const orc_keys *K, const orc_softmax_desc *d, orc_ct **c, double bound)
 {
     if (!d->bts) return ORC_ELEVEL;
-    orc_ct *b = d->bts(P, K, *c, d->bts_ctx);
+    orc_ct *b = d->bts(P, K, *c, d->bts_ctx, bound);
     if (!b) return ORC_ELEVEL;
     swap_in(c, b);
-    orc_ledger[LG_BTS]++;
     return ORC_OK;
 }
 
@@ -84,7 +84,7 @@ int orc_softmax(const orc_params *P, const orc_keys *K, const orc_softmax_desc *
         const orc_cheb *ip = &d->inv_poly[j - 1];
         /* Alg 1 main thread needs 1 (aux square) + 2 levels; bootstrap y (G12 c) */
         if (d->variant == 0 && y[0]->level < 2) {
-            for (int c = 0; c < m; c++) if ((rc = bts_or_fail(P, K, d, &y[c]))) goto done;
+            for (int c = 0; c < m; c++) if ((rc = bts_or_fail(P, K, d, &y[c], 1.0))) goto done;
         }
         if (y[0]->level < 1) { rc = ORC_ELEVEL; goto done; }
         /* ---- auxiliary thread (Alg 2) ---- */
@@ -106,7 +106,7 @@ int orc_softmax(const orc_params *P, const orc_keys *K, const orc_softmax_desc *
         int main_level = d->variant == 0 ? y[0]->level : y0[0]->level;
         int need = poly_cost(ip) + 1 + ((d->variant == 1 && j > 1) ? 1 : 0);
         if (S->level - need < main_level) {
-            if (d->bts) { if ((rc = bts_or_fail(P, K, d, &S))) goto done; }
+            if (d->bts) { if ((rc = bts_or_fail(P, K, d, &S, ip->b))) goto done; }
             else if (S->level - need < 0) { rc = ORC_ELEVEL; goto done; }
         }
         /* step 6: InvSqrt (Alg 1) or x^(-1/2^j) (Alg B, G4) */
@@ -127,7 +127,7 @@ int orc_softmax(const orc_params *P, const orc_keys *K, const orc_softmax_desc *
         }
         /* G12 (b): bootstrap lambda again if it ended below the main level */
         if (lam->level < main_level && d->bts) {
-            if ((rc = bts_or_fail(P, K, d, &lam))) goto done;
+            if ((rc = bts_or_fail(P, K, d, &lam, d->variant == 1 ? 1.5 : 1.1 / sqrt(ip->a)))) goto done;
         }
         /* ---- main thread ---- */
         for (int c = 0; c < m; c++) {

@@ -39,10 +39,10 @@ PRESETS = {
     "TOY12D": dict(log_n=12, q_bits=[60] + [40] * 27, p_bits=[61, 61, 61], alpha=3,
                    log2_anchor=_anchors(28, [(27, 40)]), h=192),
     # configs 2-5: N = 2^16, FGb-shaped.  Levels: 0 (60b), 1-12 user (40b, Delta=2^40),
-    # 13-15 SlotToCoeff (48b), 16-25 EvalMod (58b), 26-28 CoeffToSlot (58b);
+    # 13-15 SlotToCoeff (48b), 16-25 EvalMod (~2^59), 26-28 CoeffToSlot (60b);
     # 5 special primes of 61 bits (alpha = 5, dnum = 6).
-    "P16": dict(log_n=16, q_bits=[60] + [40] * 12 + [48] * 3 + [58] * 10 + [58] * 3, p_bits=[61] * 5, alpha=5,
-                log2_anchor=_anchors(29, [(28, 58), (27, 58), (26, 58), (25, 58), (14, 48), (13, 48), (12, 40)]),
+    "P16": dict(log_n=16, q_bits=[60] + [40] * 12 + [48] * 3 + [59] * 10 + [60] * 3, p_bits=[61] * 5, alpha=5,
+                log2_anchor=_anchors(29, [(28, 60), (27, 64), (26, 61), (25, 59), (14, 48), (13, 48), (12, 40)]),
                 h=192),
     # N = 2^16 with only the user chain (levels 0-12): primitive parity and
     # key-switch measurements at the user levels without BTS-sized keys.
@@ -94,3 +94,15 @@ WORKLOADS = {
     "config3": dict(preset="P16", n=256, L=8192, m=64, M=128.0, k=5, variant="B", table="p16_n256_M128_k5_B"),
     "config4": dict(preset="P16", n=128, L=4096, m=16, M=128.0, k=5, variant="B", table="p16_n128_M128_k5_B"),
 }
+
+
+def bts_tables() -> dict:
+    with open(os.path.join(_DATA, "bts_tables.json")) as fh:
+        return json.load(fh)
+
+
+# N = 2^12 ring with P16's exact modulus chain (bootstrapping included):
+# parity / precision tests of configs 2-5 at a size the oracle finishes quickly.
+PRESETS["TOY12B"] = dict(PRESETS["P16"], log_n=12, bts_out_level=12, bts_table="K24_r3_d63")
+PRESETS["P16"]["bts_out_level"] = 12
+PRESETS["P16"]["bts_table"] = "K24_r3_d63"

@@ -176,6 +176,32 @@ typedef struct {
 hs_status hs_cheb(hs_ctx *c, const hs_keys *k, const hs_ct *x, const hs_poly *p, void *stream, hs_ct **out);
 int hs_cheb_depth(int deg);
 
+/* ------------------------------------------------------------ bootstrapping (G11) */
+/* Real-slot CoeffToSlot-first bootstrapping:
+ * ModRaise -> 3 CoeffToSlot transforms -> real part -> EvalMod (Chebyshev
+ * series of cos(2 pi (K+2) v / 2^r) and r double angles) -> 3 SlotToCoeff
+ * transforms -> real part.  The output lands at out_level; the top level of
+ * the chain must be out_level + 3 + 3 + r + hs_cheb_depth(cos_poly->deg).
+ * Needs the relinearisation key, the conjugation key (Galois 2N-1) and the
+ * rotations listed by hs_bts_rotations. */
+typedef struct hs_bts hs_bts;
+typedef struct {
+    int K;                    /* bound on |I| after ModRaise                   */
+    int r;                    /* double-angle steps                            */
+    const hs_poly *cos_poly;  /* Chebyshev series on [-1, 1]                    */
+    int out_level;
+} hs_bts_desc;
+
+hs_status hs_bts_create(hs_ctx *c, const hs_bts_desc *d, hs_bts **out);
+void hs_bts_destroy(hs_bts *b);
+/* left-rotation amounts the transforms need (count returned; out may be NULL) */
+int hs_bts_rotations(const hs_params *p, int32_t *out, int max);
+/* pre-scaling exponent for a message bound (G11) */
+int hs_bts_exponent(const hs_params *p, double bound);
+/* bound: upper bound on |slot values| of `in` (selects the pre-scaling). */
+hs_status hs_bootstrap(hs_ctx *c, const hs_keys *k, hs_bts *b, const hs_ct *in, double bound, void *stream,
+                       hs_ct **out);
+
 /* ------------------------------------------------------------ Softmax */
 /* Exchange callback for the sharded many-ciphertext case:
  * called with the device buffer of this rank's partial aux sum (`words`
@@ -195,6 +221,7 @@ typedef struct {
     int world, rank;          /* sharding of the m ciphertexts (1, 0 = one GPU)     */
     hs_exchange_fn exchange;  /* required when world > 1                            */
     void *exchange_user;
+    hs_bts *bts;              /* NULL: no bootstrapping (HS_ELEVEL when needed)     */
 } hs_softmax_desc;
 
 /* One ciphertext (m = 1). */

@@ -238,7 +238,41 @@ def cheb_depth(deg):
     return int(L.hs_cheb_depth(deg))
 
 
-def _softmax_desc(n, m, k, variant, exp_poly, inv_polys, world=1, rank=0, exchange=None):
+class Bts:
+    """hs_bts: real-slot bootstrapping plan (G11)."""
+
+    def __init__(self, ctx: Context, table: dict, out_level: int):
+        self.ctx = ctx
+        pp, self._c = _poly(table)
+        self._p = pp
+        d = L.BtsDesc(int(table["K"]), int(table["r"]), C.pointer(self._p), out_level)
+        out = C.c_void_p()
+        check(L.hs_bts_create(ctx.ptr, C.byref(d), C.byref(out)))
+        self.ptr = out
+
+    def __del__(self):
+        if getattr(self, "ptr", None):
+            L.hs_bts_destroy(self.ptr)
+            self.ptr = None
+
+
+def bts_rotations(params: Params):
+    out = np.zeros(512, np.int32)
+    n = L.hs_bts_rotations(params.ptr, out, 512)
+    return [int(v) for v in out[:n]]
+
+
+def bts_exponent(params: Params, bound: float) -> int:
+    return int(L.hs_bts_exponent(params.ptr, bound))
+
+
+def bootstrap(keys: Keys, bts: Bts, ct: Ciphertext, bound=1.0, stream=None) -> Ciphertext:
+    out = C.c_void_p()
+    check(L.hs_bootstrap(keys.ctx.ptr, keys.ptr, bts.ptr, ct.ptr, float(bound), _stream(stream), C.byref(out)))
+    return Ciphertext(keys.ctx, out)
+
+
+def _softmax_desc(n, m, k, variant, exp_poly, inv_polys, world=1, rank=0, exchange=None, bts=None):
     keep = []
     e, c = _poly(exp_poly)
     keep.append(c)
@@ -251,22 +285,24 @@ def _softmax_desc(n, m, k, variant, exp_poly, inv_polys, world=1, rank=0, exchan
     keep += [arr, ep]
     fn = L.EXCHANGE_FN(0) if exchange is None else exchange
     keep.append(fn)
-    d = L.SoftmaxDesc(n, m, k, 0 if variant in (0, "A") else 1, ep, arr, world, rank, fn, None)
+    d = L.SoftmaxDesc(n, m, k, 0 if variant in (0, "A") else 1, ep, arr, world, rank, fn, None,
+                      bts.ptr if bts is not None else None)
     return d, keep
 
 
-def softmax_one_ctxt(keys: Keys, ct: Ciphertext, n, k, variant, exp_poly, inv_polys, stream=None) -> Ciphertext:
-    d, keep = _softmax_desc(n, 1, k, variant, exp_poly, inv_polys)
+def softmax_one_ctxt(keys: Keys, ct: Ciphertext, n, k, variant, exp_poly, inv_polys, bts=None,
+                     stream=None) -> Ciphertext:
+    d, keep = _softmax_desc(n, 1, k, variant, exp_poly, inv_polys, bts=bts)
     out = C.c_void_p()
     check(L.hs_softmax_one_ctxt(keys.ctx.ptr, keys.ptr, C.byref(d), ct.ptr, _stream(stream), C.byref(out)))
     return Ciphertext(keys.ctx, out)
 
 
 def softmax_many_ctxt(keys: Keys, cts, n, m, k, variant, exp_poly, inv_polys, world=1, rank=0, exchange=None,
-                      stream=None):
+                      bts=None, stream=None):
     """cts: this rank's m/world ciphertexts.  exchange: an EXCHANGE_FN (see
     paper_2410_11184_b200.dist) when world > 1."""
-    d, keep = _softmax_desc(n, m, k, variant, exp_poly, inv_polys, world, rank, exchange)
+    d, keep = _softmax_desc(n, m, k, variant, exp_poly, inv_polys, world, rank, exchange, bts)
     ml = len(cts)
     ins = (C.c_void_p * ml)(*[c.ptr.value if isinstance(c.ptr, C.c_void_p) else c.ptr for c in cts])
     outs = (C.c_void_p * ml)()

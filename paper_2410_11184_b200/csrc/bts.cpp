@@ -1,0 +1,380 @@
+// bts.cpp -- real-slot CKKS bootstrapping on the GPU (reading G11).
+//
+// PAPER.md 281-283 / 429-440 need bootstrapping but give no internals (the
+// paper calls HEaaN's FGb BTS, PAPER.md 386-393).  Conventions shared with
+// the oracle only in writing:
+//   e = clamp(floor(log2 q0 - 12 - log2 Delta_0 - log2 bound), 0, 30); x *= 2^e
+//   drop to level 0; ModRaise (centred lift of the q0 residues) to level L
+//   CoeffToSlot: inverse special-FFT stages in 3 groups (largest stages first),
+//                first transform scaled by (Delta_L / q0) / (2 (K+2))
+//   v = w + conj(w) - 1/(4 (K+2)); EvalMod = cos series on [-1,1], r x (2c^2-1)
+//   SlotToCoeff: special-FFT stages in 3 groups, first transform composed with
+//                diag(lambda, 2 lambda, ..., 2 lambda), lambda = q0/(4 pi Delta_out 2^e)
+//   out = x + conj(x)
+// Each transform: diagonals d (mod N0, structural presence), step unit u =
+// 2^(first stage index of the group), baby size b1 = 2^ceil((r+1)/2),
+// idx = d/u, giant g = idx / b1, baby b = idx % b1;
+//   out = rescale( sum_g Rot( sum_b pt_{g,b} (.) Rot(ct, b u), g b1 u ) ),
+// pt_{g,b} = encode(rot(diag_d, -g b1 u)) at the landing scale of the level.
+#include <math.h>
+#include <omp.h>
+#include <quadmath.h>
+
+#include <algorithm>
+#include <array>
+#include <map>
+#include <vector>
+
+#include "hs_internal.h"
+
+typedef __float128 f128;
+
+namespace {
+
+struct Qc {
+    f128 re = 0, im = 0;
+};
+inline Qc operator*(Qc a, Qc b) { return Qc{a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re}; }
+
+// sparse N0 x N0 matrix by diagonals: D[d][p] = A[p][(p+d) mod N0]
+struct DiagMat {
+    int n0;
+    std::vector<std::vector<Qc>> D;
+    explicit DiagMat(int n) : n0(n), D(n) {}
+    void add(int d, int p, Qc v)
+    {
+        d = ((d % n0) + n0) % n0;
+        if (D[d].empty()) D[d].assign(n0, Qc{});
+        D[d][p].re += v.re;
+        D[d][p].im += v.im;
+    }
+};
+
+DiagMat fft_stage(int log_n, int len, bool inverse)
+{
+    const int N = 1 << log_n, n0 = N / 2, h = len / 2, q4 = 4 * len;
+    DiagMat m(n0);
+    u64 g = 1;
+    for (int j = 0; j < h; j++, g = g * 5 % (2ull * N)) {
+        f128 ang = 2 * M_PIq * (f128)((g % q4) * (u64)(2 * N / q4)) / (f128)(2 * N);
+        Qc xi{cosq(ang), sinq(ang)};
+        f128 den = xi.re * xi.re + xi.im * xi.im;
+        Qc hinv{0.5q * xi.re / den, -0.5q * xi.im / den};  // 1/(2 xi)
+        for (int i = 0; i < n0; i += len) {
+            const int p = i + j;
+            if (!inverse) {
+                m.add(0, p, Qc{1, 0});
+                m.add(h, p, xi);
+                m.add(-h, p + h, Qc{1, 0});
+                m.add(0, p + h, Qc{-xi.re, -xi.im});
+            } else {
+                m.add(0, p, Qc{0.5q, 0});
+                m.add(h, p, Qc{0.5q, 0});
+                m.add(-h, p + h, hinv);
+                m.add(0, p + h, Qc{-hinv.re, -hinv.im});
+            }
+        }
+    }
+    return m;
+}
+
+DiagMat matmul(const DiagMat &A, const DiagMat &B)
+{
+    const int n0 = A.n0;
+    DiagMat C(n0);
+    for (int e = 0; e < n0; e++) {
+        if (A.D[e].empty()) continue;
+        for (int f = 0; f < n0; f++) {
+            if (B.D[f].empty()) continue;
+            const int d = (e + f) % n0;
+            for (int p = 0; p < n0; p++) C.add(d, p, A.D[e][p] * B.D[f][(p + e) % n0]);
+        }
+    }
+    return C;
+}
+
+void scale_columns(DiagMat &m, const std::vector<f128> &s)
+{
+    for (int d = 0; d < m.n0; d++)
+        if (!m.D[d].empty())
+            for (int p = 0; p < m.n0; p++) {
+                f128 f = s[(p + d) % m.n0];
+                m.D[d][p].re *= f;
+                m.D[d][p].im *= f;
+            }
+}
+
+void group_sizes(int s, int sz[3])
+{
+    int rem = s;
+    for (int k = 3, i = 0; k >= 1; k--, i++) {
+        sz[i] = (rem + k - 1) / k;
+        rem -= sz[i];
+    }
+}
+
+int ilog2(int x)
+{
+    int t = 0;
+    while ((1 << t) < x) t++;
+    return t;
+}
+
+struct LinTrans {
+    int level = 0, unit = 1, b1 = 1;
+    std::vector<int> g, b;
+    u64 *pts = nullptr;  // [terms][level+1][N] NTT-domain plaintexts
+    ~LinTrans() { if (pts) cudaFree(pts); }
+};
+
+void build_lintrans(hs_ctx *c, const DiagMat &m, int level, int unit, int r, LinTrans &T)
+{
+    const hs_params *P = c->P;
+    const int n0 = P->n / 2, N = P->n, nl = level + 1;
+    T.level = level;
+    T.unit = unit;
+    T.b1 = 1 << ((r + 2) / 2);
+    std::vector<int> ds;
+    for (int d = 0; d < n0; d++)
+        if (!m.D[d].empty()) {
+            ds.push_back(d);
+            T.g.push_back((d / unit) / T.b1);
+            T.b.push_back((d / unit) % T.b1);
+        }
+    const int nt = (int)ds.size();
+    const double sc = (P->scale[level - 1] * (double)P->prime[level]) / P->scale[level];
+    std::vector<u64> host((size_t)nt * nl * N);
+#pragma omp parallel for schedule(dynamic)
+    for (int k = 0; k < nt; k++) {
+        const int G = (T.g[k] * T.b1 * unit) % n0;
+        std::vector<double> re(n0), im(n0);
+        const std::vector<Qc> &v = m.D[ds[k]];
+        for (int p = 0; p < n0; p++) {
+            const Qc &x = v[((p - G) % n0 + n0) % n0];
+            re[p] = (double)x.re;
+            im[p] = (double)x.im;
+        }
+        hs_encode_impl(P, re.data(), im.data(), sc, level, host.data() + (size_t)k * nl * N);
+    }
+    HS_CUDA(cudaMalloc(&T.pts, host.size() * 8));
+    HS_CUDA(cudaMemcpy(T.pts, host.data(), host.size() * 8, cudaMemcpyHostToDevice));
+    k_ntt(c, T.pts, nt * nl, pmap_range(0, nl), false, nullptr);
+    HS_CUDA(cudaDeviceSynchronize());
+}
+
+}  // namespace
+
+struct hs_bts {
+    hs_ctx *ctx = nullptr;
+    int K = 0, r = 0, out_level = 0;
+    std::vector<double> cos_coeffs;
+    hs_poly cos_poly{};
+    bool cts_ready = false;
+    std::array<LinTrans, 3> cts;
+    std::map<int, std::array<LinTrans, 3>> stc;  // per pre-scaling exponent e
+    std::mutex mu;
+};
+
+int bts_exponent(const hs_params *P, double bound)
+{
+    double e = floor(log2((double)P->prime[0]) - 12.0 - log2(P->scale[0]) - log2(bound));
+    return (int)std::min(30.0, std::max(0.0, e));
+}
+
+int bts_rotations(const hs_params *P, int32_t *out, int max)
+{
+    const int n0 = P->n / 2;
+    int sz[3], cnt = 0, first = 0;
+    group_sizes(ilog2(n0), sz);
+    std::vector<int> rots;
+    for (int gi = 0; gi < 3; gi++) {
+        const int u = 1 << first, r = sz[gi], b1 = 1 << ((r + 2) / 2), span = (1 << r) - 1, mod = n0 / u;
+        for (int idx = -span; idx <= span; idx++) {
+            int id = ((idx % mod) + mod) % mod;
+            for (int rr : {(id % b1) * u, (id / b1) * b1 * u}) {
+                rr %= n0;
+                if (rr && std::find(rots.begin(), rots.end(), rr) == rots.end()) rots.push_back(rr);
+            }
+        }
+        first += r;
+    }
+    for (int v : rots) {
+        if (out && cnt < max) out[cnt] = v;
+        cnt++;
+    }
+    return cnt;
+}
+
+static void ensure_cts(hs_bts *B)
+{
+    if (B->cts_ready) return;
+    hs_ctx *c = B->ctx;
+    const hs_params *P = c->P;
+    const int n0 = P->n / 2, L = P->L;
+    int sz[3], first[3];
+    group_sizes(ilog2(n0), sz);
+    first[0] = 0;
+    first[1] = sz[0];
+    first[2] = sz[0] + sz[1];
+    for (int k = 0; k < 3; k++) {
+        const int gi = 2 - k;
+        DiagMat acc(n0);
+        bool have = false;
+        for (int i = first[gi] + sz[gi] - 1; i >= first[gi]; i--) {
+            DiagMat S = fft_stage(P->log_n, 2 << i, true);
+            acc = have ? matmul(S, acc) : S;
+            have = true;
+        }
+        if (k == 0) {
+            f128 f = ((f128)P->scale[L] / (f128)P->prime[0]) / (2 * (f128)(B->K + 2));
+            scale_columns(acc, std::vector<f128>(n0, f));
+        }
+        build_lintrans(c, acc, L - k, 1 << first[gi], sz[gi], B->cts[k]);
+    }
+    B->cts_ready = true;
+}
+
+static std::array<LinTrans, 3> &ensure_stc(hs_bts *B, int e)
+{
+    auto it = B->stc.find(e);
+    if (it != B->stc.end()) return it->second;
+    hs_ctx *c = B->ctx;
+    const hs_params *P = c->P;
+    const int n0 = P->n / 2;
+    int sz[3];
+    group_sizes(ilog2(n0), sz);
+    std::array<LinTrans, 3> &T = B->stc[e];
+    for (int gi = 0, st = 0; gi < 3; st += sz[gi], gi++) {
+        DiagMat acc(n0);
+        bool have = false;
+        for (int i = st; i < st + sz[gi]; i++) {
+            DiagMat S = fft_stage(P->log_n, 2 << i, false);
+            acc = have ? matmul(S, acc) : S;
+            have = true;
+        }
+        if (gi == 0) {
+            f128 lam = (f128)P->prime[0] / (4 * M_PIq * (f128)P->scale[B->out_level] * ldexpq(1, e));
+            std::vector<f128> dv(n0, 2 * lam);
+            dv[0] = lam;
+            scale_columns(acc, dv);
+        }
+        build_lintrans(c, acc, B->out_level + 3 - gi, 1 << st, sz[gi], T[gi]);
+    }
+    return T;
+}
+
+static CtP apply(const hs_keys *K, const hs_ct *in, const LinTrans &T, cudaStream_t st)
+{
+    hs_ctx *c = K->ctx;
+    const size_t N = c->P->n;
+    const int n0 = (int)N / 2, l = T.level, nl = l + 1;
+    CtP lowered;
+    const hs_ct *x = in;
+    if (in->level != l) {
+        lowered = ev_level_down(in, l, st);
+        x = lowered.get();
+    }
+    std::map<int, CtP> R;
+    for (int b : T.b)
+        if (!R.count(b)) R[b] = b == 0 ? ct_copy(x, st) : ev_rotate(K, x, b * T.unit, st);
+    int maxg = 0;
+    for (int g : T.g) maxg = std::max(maxg, g);
+    CtP acc = ct_new(c, l, 2, st);
+    HS_CUDA(cudaMemsetAsync(acc->d, 0, acc->limbs() * N * 8, st));
+    for (int g = 0; g <= maxg; g++) {
+        CtP inner;
+        for (size_t k = 0; k < T.g.size(); k++) {
+            if (T.g[k] != g) continue;
+            if (!inner) {
+                inner = ct_new(c, l, 2, st);
+                HS_CUDA(cudaMemsetAsync(inner->d, 0, inner->limbs() * N * 8, st));
+            }
+            k_mac_pt(c, inner->d, R[T.b[k]]->d, T.pts + k * nl * N, nl, nl, st);
+            c->ledger[HS_LG_PMULT]++;
+        }
+        if (!inner) continue;
+        if (g) inner = ev_rotate(K, inner.get(), (g * T.b1 * T.unit) % n0, st);
+        k_add(c, acc->d, inner->d, acc->d, (int)acc->limbs(), nl, false, st);
+    }
+    return ev_rescale(acc.get(), st);
+}
+
+CtP ev_bootstrap(const hs_keys *K, hs_bts *B, const hs_ct *in, double bound, cudaStream_t st)
+{
+    hs_ctx *c = K->ctx;
+    const hs_params *P = c->P;
+    const size_t N = P->n;
+    const int L = P->L, conj = 2 * P->n - 1;
+    if (in->ncomp != 2) throw HsError(HS_EINVAL, "bootstrap needs a degree-1 ciphertext");
+    const int e = bts_exponent(P, bound);
+    std::array<LinTrans, 3> *stc;
+    {
+        std::lock_guard<std::mutex> g(B->mu);
+        ensure_cts(B);
+        stc = &ensure_stc(B, e);
+    }
+    CtP x = e ? ev_mult_int(in, (int64_t)1 << e, st) : ct_copy(in, st);
+    // ModRaise of the q0 residues
+    DBuf low(2 * N, st);
+    HS_CUDA(cudaMemcpy2DAsync(low.p, N * 8, x->d, (x->level + 1) * N * 8, N * 8, 2, cudaMemcpyDeviceToDevice, st));
+    PrimeMap p0;
+    p0.n = 1;
+    p0.p[0] = 0;
+    k_ntt(c, low.p, 2, p0, true, st);
+    x = ct_new(c, L, 2, st);
+    k_modraise(c, low.p, x->d, L + 1, st);
+    k_ntt(c, x->d, 2 * (L + 1), pmap_range(0, L + 1), false, st);
+    for (int k = 0; k < 3; k++) x = apply(K, x.get(), B->cts[k], st);
+    CtP cj = ev_galois(K, x.get(), conj, st);
+    x = ev_add(x.get(), cj.get(), false, st);
+    x = ev_add_const(x.get(), -1.0 / (4.0 * (B->K + 2)), st);
+    x = ev_cheb(K, x.get(), &B->cos_poly, st);
+    for (int i = 0; i < B->r; i++) {
+        CtP m = ev_mult(K, x.get(), x.get(), st);
+        m = ev_mult_int(m.get(), 2, st);
+        x = ev_add_const(m.get(), -1.0, st);
+    }
+    for (int k = 0; k < 3; k++) x = apply(K, x.get(), (*stc)[k], st);
+    cj = ev_galois(K, x.get(), conj, st);
+    c->ledger[HS_LG_BTS]++;
+    return ev_add(x.get(), cj.get(), false, st);
+}
+
+// ------------------------------------------------------------------ C ABI
+static thread_local std::string g_bts_err;
+
+extern "C" {
+
+hs_status hs_bts_create(hs_ctx *c, const hs_bts_desc *d, hs_bts **out)
+{
+    try {
+        if (!c || !d || !out || !d->cos_poly || !d->cos_poly->coeffs || d->cos_poly->deg < 1 || d->r < 0 ||
+            d->K < 1)
+            throw HsError(HS_EINVAL, "hs_bts_create: bad descriptor");
+        const hs_params *P = c->P;
+        const int need = d->out_level + 6 + d->r + cheb_depth(d->cos_poly->deg);
+        if (d->out_level < 0 || need != P->L)
+            throw HsError(HS_ELEVEL, "hs_bts_create: chain top must be out_level + 6 + r + depth(cos)");
+        std::unique_ptr<hs_bts> B(new hs_bts);
+        B->ctx = c;
+        B->K = d->K;
+        B->r = d->r;
+        B->out_level = d->out_level;
+        B->cos_coeffs.assign(d->cos_poly->coeffs, d->cos_poly->coeffs + d->cos_poly->deg + 1);
+        B->cos_poly = hs_poly{d->cos_poly->deg, -1.0, 1.0, B->cos_coeffs.data()};
+        *out = B.release();
+        return HS_OK;
+    } catch (const HsError &e) {
+        g_bts_err = e.what();
+        return e.code;
+    } catch (const std::exception &e) {
+        g_bts_err = e.what();
+        return HS_EINVAL;
+    }
+}
+
+void hs_bts_destroy(hs_bts *b) { delete b; }
+int hs_bts_rotations(const hs_params *p, int32_t *out, int max) { return bts_rotations(p, out, max); }
+int hs_bts_exponent(const hs_params *p, double bound) { return bts_exponent(p, bound); }
+
+}  // extern "C"

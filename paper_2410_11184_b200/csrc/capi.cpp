@@ -358,6 +358,17 @@ hs_status hs_softmax_many_ctxt(hs_ctx *c, const hs_keys *k, const hs_softmax_des
     HS_CATCH
 }
 
+hs_status hs_bootstrap(hs_ctx *c, const hs_keys *k, hs_bts *b, const hs_ct *in, double bound, void *stream,
+                       hs_ct **out)
+{
+    HS_TRY
+    if (!c || !k || !b || !in || !out || !(bound > 0)) throw HsError(HS_EINVAL, "bad arguments");
+    activate(c);
+    *out = ev_bootstrap(k, b, in, bound, S(stream)).release();
+    return HS_OK;
+    HS_CATCH
+}
+
 hs_status hs_ledger_get(hs_ctx *c, int64_t *out, int n)
 {
     if (!c || !out) return HS_EINVAL;

@@ -74,7 +74,7 @@ CtP ct_copy(const hs_ct *a, cudaStream_t st)
 }
 
 // keep limbs 0..level of every component
-static CtP ct_drop(const hs_ct *a, int level, cudaStream_t st)
+CtP ct_drop(const hs_ct *a, int level, cudaStream_t st)
 {
     if (level == a->level) return ct_copy(a, st);
     hs_ctx *c = a->ctx;

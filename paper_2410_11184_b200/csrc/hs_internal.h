@@ -162,6 +162,8 @@ void k_ks_inner(hs_ctx *c, const u64 *d, const u64 *ext, const u64 *key, u64 *ac
 void k_moddown_final(hs_ctx *c, const u64 *acc, const u64 *conv, u64 *o0, u64 *o1, const u64 *add0,
                      const u64 *add1, int level, cudaStream_t st);
 void upload_prime_constants(const hs_params *P);
+void k_mac_pt(hs_ctx *c, u64 *acc, const u64 *a, const u64 *pt, int nl, int la, cudaStream_t st);
+void k_modraise(hs_ctx *c, const u64 *x, u64 *o, int nl, cudaStream_t st);
 void k_signed_to_rns(hs_ctx *c, const int64_t *v, u64 *o, int n_limbs, const PrimeMap &pm, cudaStream_t st);
 void k_uniform(hs_ctx *c, u64 *o, int n_limbs, const PrimeMap &pm, u64 seed, uint32_t tag, u64 sub,
                int limb_index0, cudaStream_t st);
@@ -180,6 +182,7 @@ u64 hs_stream_word(u64 seed, uint32_t tag, u64 sub, u64 idx);
 typedef std::unique_ptr<hs_ct> CtP;
 CtP ct_new(hs_ctx *c, int level, int ncomp, cudaStream_t st);
 CtP ct_copy(const hs_ct *a, cudaStream_t st);
+CtP ct_drop(const hs_ct *a, int level, cudaStream_t st);
 CtP ev_add(const hs_ct *a, const hs_ct *b, bool sub, cudaStream_t st);
 CtP ev_level_down(const hs_ct *a, int target, cudaStream_t st);
 CtP ev_rescale(const hs_ct *a, cudaStream_t st);
@@ -210,6 +213,11 @@ void hs_decode_impl(const hs_params *P, const u64 *q0_coeffs, double scale, doub
 // poly.cpp
 CtP ev_cheb(const hs_keys *K, const hs_ct *x, const hs_poly *p, cudaStream_t st);
 int cheb_depth(int deg);
+
+// bts.cpp
+CtP ev_bootstrap(const hs_keys *K, hs_bts *B, const hs_ct *in, double bound, cudaStream_t st);
+int bts_exponent(const hs_params *P, double bound);
+int bts_rotations(const hs_params *P, int32_t *out, int max);
 
 // softmax.cpp
 hs_status softmax_run(hs_ctx *c, const hs_keys *K, const hs_softmax_desc *d, const hs_ct *const *in,

@@ -680,3 +680,48 @@ void k_signed_to_rns(hs_ctx *c, const int64_t *v, u64 *o, int n_limbs, const Pri
     HS_CHECK_LAUNCH();
     count_kernel(c);
 }
+
+// ------------------------------------------------------------------ bootstrapping helpers (G11)
+// acc[c][i][t] += a[c][i][t] * pt[i][t]  (c < 2, i < nl); a has stride la limbs
+__global__ void mac_pt_kernel(u64 *acc, const u64 *a, const u64 *pt, int N, int nl, int la)
+{
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= N) return;
+    int i = blockIdx.y, c = blockIdx.z;
+    const PrimeK k = c_pk[i];
+    u64 p = pt[(size_t)i * N + t];
+    size_t ai = ((size_t)c * la + i) * N + t, oi = ((size_t)c * nl + i) * N + t;
+    acc[oi] = d_add(acc[oi], d_mulmod(a[ai], p, k), k.q);
+}
+
+void k_mac_pt(hs_ctx *c, u64 *acc, const u64 *a, const u64 *pt, int nl, int la, cudaStream_t st)
+{
+    int N = c->P->n;
+    mac_pt_kernel<<<dim3((N + 255) / 256, nl, 2), 256, 0, st>>>(acc, a, pt, N, nl, la);
+    HS_CHECK_LAUNCH();
+    count_kernel(c);
+}
+
+// ModRaise: x[c][t] (coefficients mod q_0) -> o[c][i][t] = centred(x) mod q_i, i <= L
+__global__ void modraise_kernel(const u64 *x, u64 *o, int N, int nl)
+{
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= N) return;
+    int i = blockIdx.y, c = blockIdx.z;
+    u64 q0 = c_pk[0].q, q = c_pk[i].q;
+    u64 v = x[(size_t)c * N + t], r;
+    if (v <= (q0 - 1) / 2) r = v % q;
+    else {
+        u64 w = (q0 - v) % q;
+        r = w ? q - w : 0;
+    }
+    o[((size_t)c * nl + i) * N + t] = r;
+}
+
+void k_modraise(hs_ctx *c, const u64 *x, u64 *o, int nl, cudaStream_t st)
+{
+    int N = c->P->n;
+    modraise_kernel<<<dim3((N + 255) / 256, nl, 2), 256, 0, st>>>(x, o, N, nl);
+    HS_CHECK_LAUNCH();
+    count_kernel(c);
+}

@@ -13,6 +13,8 @@
 // gathered partials are added mod q (exact, order-free), so every rank runs
 // the replicated aux thread on identical words and all outputs are identical
 // to the single-GPU run.
+#include <math.h>
+
 #include <vector>
 
 #include "hs_internal.h"
@@ -63,7 +65,11 @@ hs_status softmax_run(hs_ctx *c, const hs_keys *K, const hs_softmax_desc *d, con
     CtP lam;
     for (int j = 1; j <= d->k; j++) {
         const hs_poly *ip = &d->inv_poly[j - 1];
-        if (d->variant == 0 && y[0]->level < 2) level_error("main thread needs bootstrapping (not available)");
+        // G12 (c): Alg 1 main thread needs 1 (aux square) + 2 levels
+        if (d->variant == 0 && y[0]->level < 2) {
+            if (!d->bts) level_error("main thread needs bootstrapping (not available)");
+            for (int i = 0; i < ml; i++) y[i] = ev_bootstrap(K, d->bts, y[i].get(), 1.0, st);
+        }
         if (y[0]->level < 1) level_error("main thread out of levels");
         // ---- auxiliary thread: S = relin(sum tensor(y, y)) -> rescale
         CtP acc;
@@ -88,7 +94,12 @@ hs_status softmax_run(hs_ctx *c, const hs_keys *K, const hs_softmax_desc *d, con
         rot_sum(K, S, nb, stride, -1, st);
         const int main_level = d->variant == 0 ? y[0]->level : y0[0]->level;
         const int need = poly_cost(ip) + 1 + ((d->variant == 1 && j > 1) ? 1 : 0);
-        if (S->level - need < main_level && S->level - need < 0) level_error("aux thread needs bootstrapping");
+        // G12 (a): bootstrap before the inverse square root when the rest of the
+        // aux thread would leave lambda below the main operand's level
+        if (S->level - need < main_level) {
+            if (d->bts) S = ev_bootstrap(K, d->bts, S.get(), ip->b, st);
+            else if (S->level - need < 0) level_error("aux thread needs bootstrapping");
+        }
         CtP lj = ev_cheb(K, S.get(), ip, st);
         S.reset();
         if (lj->level < 1) level_error("no level for the mask");
@@ -96,6 +107,9 @@ hs_status softmax_run(hs_ctx *c, const hs_keys *K, const hs_softmax_desc *d, con
         rot_sum(K, lj, nb, stride, +1, st);
         if (d->variant == 1 && j > 1) lam = ev_mult(K, lam.get(), lj.get(), st);
         else lam = std::move(lj);
+        // G12 (b): bootstrap lambda again if it ended below the main level
+        if (lam->level < main_level && d->bts)
+            lam = ev_bootstrap(K, d->bts, lam.get(), d->variant == 1 ? 1.5 : 1.1 / sqrt(ip->a), st);
         // ---- main thread
         for (int i = 0; i < ml; i++) {
             if (d->variant == 0) {

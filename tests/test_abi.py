@@ -100,3 +100,14 @@ def test_pack_rejects_indivisible():
     P = hs.Params.from_preset(W.preset("TOY12"))
     with pytest.raises(hs.HsError):
         P.pack(np.zeros((4, 24)), 1)   # n/m not a power of two
+
+
+@pytest.mark.parametrize("name", ["TOY12B", "P16"])
+def test_bts_plan_conventions_match(name):
+    """rotation set and pre-scaling exponents (G11) agree with the oracle"""
+    import paper_2410_11184_b200 as hs
+    pre = W.preset(name)
+    P, PO = hs.Params.from_preset(pre), O.Params.from_preset(pre)
+    assert hs.bts_rotations(P) == O.bts_rotations(PO)
+    for b in [0.5, 1.0, 1.5, 2.0, 64.0, 261.0, 1e6]:
+        assert hs.bts_exponent(P, b) == O.bts_exponent(PO, b)

@@ -213,3 +213,77 @@ def test_p16_hmult_rotate_parity(p16):
     r = hs.op(p16.K, "rotate", a, i=-128)
     same(r, O.op(p16.PO, p16.KO, "rotate", ao, i=-128))
     assert np.abs(hs.decrypt_decode(p16.K, m).real - za * zb).max() < 2.0 ** -20
+
+
+# ---------------------------------------------------------------- bootstrapping (G11)
+@pytest.fixture(scope="module")
+def toyb():
+    hs = _hs()
+    pre = W.preset("TOY12B")
+    P = hs.Params.from_preset(pre)
+    PO = O.Params.from_preset(pre)
+    rots = set(hs.bts_rotations(P))
+    for n, m in [(256, 16), (256, 1)]:
+        nb = n // m
+        stride = (P.n // 2) // nb
+        i = 0
+        while (1 << i) < nb:
+            rots |= {stride << i, -(stride << i)}
+            i += 1
+    gal = sorted({P.galois_of_rot(r) for r in rots} | {2 * P.n - 1})
+    ctx = hs.Context(P, 0)
+    K = hs.Keys(ctx, 31337, pre["h"], galois=gal)
+    KO = O.Keys(PO, 31337, pre["h"], galois=gal)
+    tab = W.bts_tables()[pre["bts_table"]]
+    B = hs.Bts(ctx, tab, pre["bts_out_level"])
+    BO = O.Bts(PO, tab, pre["bts_out_level"])
+    return dict(P=P, PO=PO, ctx=ctx, K=K, KO=KO, B=B, BO=BO, pre=pre)
+
+
+@pytest.mark.parametrize("level,bound", [(3, 1.0), (0, 1.0), (5, 300.0)])
+def test_bootstrap_parity(toyb, level, bound):
+    hs = _hs()
+    P, PO, K, KO = toyb["P"], toyb["PO"], toyb["K"], toyb["KO"]
+    rng = np.random.default_rng(level)
+    z = rng.uniform(-bound, bound, P.n // 2)
+    pt = P.encode(z, scale=P.scale(level), level=level)
+    g = hs.encrypt(K, pt, level, 77, level)
+    o = O.encrypt(PO, KO, pt, level, 77, level)
+    gb = hs.bootstrap(K, toyb["B"], g, bound)
+    ob = O.bootstrap(PO, KO, o, toyb["BO"], bound)
+    same(gb, ob)
+    assert gb.level == toyb["pre"]["bts_out_level"]
+    err = np.abs(hs.decrypt_decode(K, gb).real - z).max() / bound
+    assert err < 2.0 ** -18, np.log2(err)
+
+
+@pytest.mark.parametrize("table,m", [("p16_n256_M128_k5_B", 16), ("p16_n256_M128_k5_A", 1)])
+def test_softmax_bts_parity(toyb, tables, table, m):
+    """configs 2-3 schedule (Alg 1 / version B with bootstrapping) on the
+    N = 2^12 ring with P16's chain: ciphertexts word-for-word, accuracy 2^-15."""
+    hs = _hs()
+    P, PO, K, KO = toyb["P"], toyb["PO"], toyb["K"], toyb["KO"]
+    tab = tables[table]
+    cfg = tab["config"]
+    n, k = cfg["n"], cfg["k"]
+    var = 0 if cfg["variant"] == "A" else 1
+    L = (P.n // 2) * m // n
+    x = W.softmax_inputs(L, n, cfg["M"], seed=W.derive_seed("x", table))
+    slots = P.pack(x, m)
+    g_in, o_in = [], []
+    for c in range(m):
+        pt = P.encode(slots[c], scale=P.scale(12), level=12)
+        g_in.append(hs.encrypt(K, pt, 12, 4040, c))
+        o_in.append(O.encrypt(PO, KO, pt, 12, 4040, c))
+    toyb["ctx"].ledger_reset()
+    g_out = hs.softmax_many_ctxt(K, g_in, n, m, k, var, tab["exp"], tab["inv"], bts=toyb["B"])
+    o_out = O.softmax_bts(PO, KO, o_in, n, k, var, tab["exp"], tab["inv"], toyb["BO"])
+    for gc, oc in zip(g_out, o_out):
+        same(gc, oc)
+    dec = np.stack([hs.decrypt_decode(K, c).real for c in g_out])
+    y = P.unpack(dec, L, n)
+    ref = np.exp(x - x.max(1, keepdims=True))
+    ref /= ref.sum(1, keepdims=True)
+    assert np.abs(y - ref).max() < 2.0 ** -15
+    led = toyb["ctx"].ledger()
+    assert led["bts"] == 2 * k if var == 1 else led["bts"] >= k

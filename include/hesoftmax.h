@@ -231,6 +231,15 @@ hs_status hs_softmax_one_ctxt(hs_ctx *c, const hs_keys *k, const hs_softmax_desc
 hs_status hs_softmax_many_ctxt(hs_ctx *c, const hs_keys *k, const hs_softmax_desc *d, const hs_ct *const *in,
                                size_t m_local, void *stream, hs_ct **out);
 
+/* ------------------------------------------------------------ kernel profiling (bench hooks) */
+/* When enabled, every kernel launch is bracketed by CUDA events on its stream
+ * and tagged with its algorithmic bytes.  collect
+ * synchronises the device and returns, per kernel class (0 NTT, 1 add,
+ * 2 scalar, 3 pt-mult, 4 tensor, 5 permute, 6 rescale, 7 bconv, 8 ks-inner,
+ * 9 moddown, 10 rng, 11 modraise), [launches, total ms, total bytes]. */
+hs_status hs_kprof_enable(hs_ctx *c, int on);
+hs_status hs_kprof_collect(hs_ctx *c, double *out, int n_classes);
+
 /* ------------------------------------------------------------ ledger (D8) */
 enum { HS_LG_HMULT, HS_LG_TENSOR, HS_LG_KS, HS_LG_ROT, HS_LG_RESCALE, HS_LG_CMULT, HS_LG_PMULT,
        HS_LG_LEVELDOWN, HS_LG_BTS, HS_LG_NTT, HS_LG_KERNELS, HS_LG_COUNT };

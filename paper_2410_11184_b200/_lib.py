@@ -121,3 +121,10 @@ EXPORTED = [n for n in list(globals()) if n.startswith("hs_")]
 def check(rc):
     if rc != 0:
         raise HsError(rc, hs_last_error().decode())
+
+hs_kprof_enable = _sig("hs_kprof_enable", C.c_int, [vp, C.c_int])
+hs_kprof_collect = _sig("hs_kprof_collect", C.c_int, [vp, np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS"),
+                                                      C.c_int])
+KPROF_CLASSES = ["ntt", "add", "scalar", "ptmul", "tensor", "permute", "rescale", "bconv", "ks_inner", "moddown",
+                 "rng", "modraise"]
+EXPORTED = [n for n in list(globals()) if n.startswith("hs_")]

@@ -91,6 +91,11 @@ struct hs_ctx {
     std::map<int, unsigned *> galois_perm;   // device permutation tables
     std::mutex mu;
     int64_t ledger[HS_LG_COUNT] = {0};
+    bool kprof_on = false;
+    std::vector<cudaEvent_t> kprof_ev;       // pairs (start, end)
+    std::vector<int> kprof_id;
+    std::vector<double> kprof_bytes;
+    size_t kprof_used = 0;
     ~hs_ctx();
 };
 
@@ -134,6 +139,22 @@ struct DBuf {                   // stream-ordered scratch buffer
     ~DBuf() { if (p) dev_free(p, st); }
     DBuf(const DBuf &) = delete;
     DBuf &operator=(const DBuf &) = delete;
+};
+
+// ------------------------------------------------------------------ kernel profiling (kprof.cpp)
+// When enabled, every launcher records CUDA events around its kernel on the
+// launching stream plus the launch's algorithmic bytes;
+// hs_kprof_collect aggregates them per kernel class.
+enum { KID_NTT, KID_ADD, KID_SCALAR, KID_PTMUL, KID_TENSOR, KID_PERMUTE, KID_RESCALE, KID_BCONV, KID_KS_INNER,
+       KID_MODDOWN, KID_RNG, KID_MODRAISE, KID_COUNT };
+struct KTimer {
+    hs_ctx *c;
+    int id;
+    double bytes;
+    cudaStream_t st;
+    int slot;
+    KTimer(hs_ctx *c, int id, double bytes, cudaStream_t st);
+    ~KTimer();
 };
 
 // ------------------------------------------------------------------ kernel launchers (kernels.cu / ntt.cu / rng.cu)

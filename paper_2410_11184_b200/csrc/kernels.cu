@@ -180,6 +180,7 @@ __global__ void __launch_bounds__(256) ntt_rows_kernel(u64 *data, PrimeMap pm, c
 
 void k_ntt(hs_ctx *c, u64 *data, int n_limbs, const PrimeMap &pm, bool inverse, cudaStream_t st)
 {
+    KTimer _kt(c, KID_NTT, (double)n_limbs * c->P->n * 16, st);
     if (n_limbs <= 0) return;
     const hs_params *P = c->P;
     NttGeom g;
@@ -219,6 +220,7 @@ __global__ void add_kernel(const u64 *a, const u64 *b, u64 *o, int N, int period
 
 void k_add(hs_ctx *c, const u64 *a, const u64 *b, u64 *o, int n_limbs, int period, bool sub, cudaStream_t st)
 {
+    KTimer _kt(c, KID_ADD, (double)n_limbs * c->P->n * 24, st);
     int N = c->P->n;
     add_kernel<<<GRID_LIMBS(n_limbs, N), 256, 0, st>>>(a, b, o, N, period, sub ? 1 : 0);
     HS_CHECK_LAUNCH();
@@ -237,6 +239,7 @@ __global__ void neg_kernel(const u64 *a, u64 *o, int N, int period)
 
 void k_neg(hs_ctx *c, const u64 *a, u64 *o, int n_limbs, int period, cudaStream_t st)
 {
+    KTimer _kt(c, KID_ADD, (double)n_limbs * c->P->n * 16, st);
     int N = c->P->n;
     neg_kernel<<<GRID_LIMBS(n_limbs, N), 256, 0, st>>>(a, o, N, period);
     HS_CHECK_LAUNCH();
@@ -268,6 +271,7 @@ __global__ void mul_scalar_kernel(const u64 *a, u64 *o, ScalarArg s, int N, int 
 
 void k_mul_scalar(hs_ctx *c, const u64 *a, u64 *o, const u64 *host_scal, int n_limbs, int period, cudaStream_t st)
 {
+    KTimer _kt(c, KID_SCALAR, (double)n_limbs * c->P->n * 16, st);
     int N = c->P->n;
     mul_scalar_kernel<<<GRID_LIMBS(n_limbs, N), 256, 0, st>>>(a, o, make_scalars(c->P, host_scal, period), N, period);
     HS_CHECK_LAUNCH();
@@ -286,6 +290,7 @@ __global__ void mac_scalar_kernel(u64 *acc, const u64 *a, ScalarArg s, int N, in
 
 void k_mac_scalar(hs_ctx *c, u64 *acc, const u64 *a, const u64 *host_scal, int n_limbs, int period, cudaStream_t st)
 {
+    KTimer _kt(c, KID_SCALAR, (double)n_limbs * c->P->n * 24, st);
     int N = c->P->n;
     mac_scalar_kernel<<<GRID_LIMBS(n_limbs, N), 256, 0, st>>>(acc, a, make_scalars(c->P, host_scal, period), N,
                                                               period);
@@ -304,6 +309,7 @@ __global__ void add_scalar_kernel(u64 *a, ScalarArg s, int N)
 
 void k_add_scalar(hs_ctx *c, u64 *a, const u64 *host_scal, int n_limbs, cudaStream_t st)
 {
+    KTimer _kt(c, KID_SCALAR, (double)n_limbs * c->P->n * 16, st);
     int N = c->P->n;
     ScalarArg s;
     for (int i = 0; i < n_limbs; i++) s.v[i] = host_scal[i];
@@ -324,6 +330,7 @@ __global__ void mul_pointwise_kernel(const u64 *a, const u64 *b, u64 *o, int N, 
 void k_mul_pointwise(hs_ctx *c, const u64 *a, const u64 *b, u64 *o, int n_limbs, int period_a, int period_b,
                      cudaStream_t st)
 {
+    KTimer _kt(c, KID_PTMUL, (double)n_limbs * c->P->n * 24, st);
     int N = c->P->n;
     mul_pointwise_kernel<<<GRID_LIMBS(n_limbs, N), 256, 0, st>>>(a, b, o, N, period_a, period_b);
     HS_CHECK_LAUNCH();
@@ -349,6 +356,7 @@ __global__ void tensor_kernel(const u64 *a, const u64 *b, u64 *o, int N, int nl)
 
 void k_tensor(hs_ctx *c, const u64 *a, const u64 *b, u64 *o, int nl, cudaStream_t st)
 {
+    KTimer _kt(c, KID_TENSOR, (double)nl * c->P->n * 56, st);
     int N = c->P->n;
     tensor_kernel<<<GRID_LIMBS(nl, N), 256, 0, st>>>(a, b, o, N, nl);
     HS_CHECK_LAUNCH();
@@ -365,6 +373,7 @@ __global__ void permute_kernel(const u64 *a, u64 *o, const unsigned *perm, int N
 
 void k_permute(hs_ctx *c, const u64 *a, u64 *o, const unsigned *perm, int n_limbs, cudaStream_t st)
 {
+    KTimer _kt(c, KID_PERMUTE, (double)n_limbs * c->P->n * 16, st);
     int N = c->P->n;
     permute_kernel<<<GRID_LIMBS(n_limbs, N), 256, 0, st>>>(a, o, perm, N);
     HS_CHECK_LAUNCH();
@@ -392,6 +401,7 @@ __global__ void rescale_prep_kernel(const u64 *last, u64 *w, int N, int level)
 
 void k_rescale_prep(hs_ctx *c, const u64 *last, u64 *w, int ncomp, int level, cudaStream_t st)
 {
+    KTimer _kt(c, KID_RESCALE, (double)ncomp * (1 + level) * c->P->n * 8, st);
     int N = c->P->n;
     rescale_prep_kernel<<<dim3((N + 255) / 256, level, ncomp), 256, 0, st>>>(last, w, N, level);
     HS_CHECK_LAUNCH();
@@ -415,6 +425,7 @@ __global__ void rescale_final_kernel(const u64 *a, const u64 *w, u64 *o, Rescale
 
 void k_rescale_final(hs_ctx *c, const u64 *a, const u64 *w, u64 *o, int ncomp, int level, cudaStream_t st)
 {
+    KTimer _kt(c, KID_RESCALE, (double)ncomp * level * c->P->n * 24, st);
     const hs_params *P = c->P;
     RescaleArg r;
     u64 ql = P->prime[level];
@@ -462,6 +473,7 @@ __global__ void bconv_kernel(const u64 *__restrict__ x, size_t xs, u64 *o, size_
 void k_bconv(hs_ctx *c, const BconvTab &tab, const u64 *src, size_t src_stride, u64 *dst, size_t dst_stride,
              int batch, size_t bss, size_t bds, cudaStream_t st)
 {
+    KTimer _kt(c, KID_BCONV, (double)batch * (tab.n_src + tab.n_dst) * c->P->n * 8, st);
     BconvArg A;
     A.n_src = tab.n_src;
     A.n_dst = tab.n_dst;
@@ -514,6 +526,7 @@ __global__ void ks_inner_kernel(const u64 *__restrict__ d, const u64 *__restrict
 void k_ks_inner(hs_ctx *c, const u64 *d, const u64 *ext, const u64 *key, u64 *acc, int level, int beta,
                 cudaStream_t st)
 {
+    KTimer _kt(c, KID_KS_INNER, ((double)beta * (level + 1 + c->P->n_p) * 24 + 2.0 * (level + 1 + c->P->n_p) * 8) * c->P->n, st);
     const hs_params *P = c->P;
     KsArg A{level, beta, P->alpha, P->n_q, P->n_p};
     int N = P->n;
@@ -549,6 +562,7 @@ __global__ void moddown_final_kernel(const u64 *acc, const u64 *conv, MdArg A, i
 void k_moddown_final(hs_ctx *c, const u64 *acc, const u64 *conv, u64 *o0, u64 *o1, const u64 *add0,
                      const u64 *add1, int level, cudaStream_t st)
 {
+    KTimer _kt(c, KID_MODDOWN, (double)(level + 1) * c->P->n * 8 * (6 + (add0 ? 1 : 0) + (add1 ? 1 : 0)), st);
     const hs_params *P = c->P;
     MdArg A;
     for (int i = 0; i <= level; i++) {
@@ -631,6 +645,7 @@ __global__ void uniform_kernel(u64 *o, PrimeMap pm, u64 seed, uint32_t tag, u64 
 void k_uniform(hs_ctx *c, u64 *o, int n_limbs, const PrimeMap &pm, u64 seed, uint32_t tag, u64 sub, int,
                cudaStream_t st)
 {
+    KTimer _kt(c, KID_RNG, (double)n_limbs * c->P->n * 8, st);
     int N = c->P->n;
     int nb = N / 4;
     uniform_kernel<<<dim3((nb + 127) / 128, n_limbs), 128, 0, st>>>(o, pm, seed, tag, sub, N);
@@ -655,6 +670,7 @@ __global__ void cbd_kernel(int64_t *o, u64 seed, uint32_t tag, u64 sub, int eta,
 
 void k_cbd(hs_ctx *c, int64_t *o, u64 seed, uint32_t tag, u64 sub, int eta, cudaStream_t st)
 {
+    KTimer _kt(c, KID_RNG, (double)c->P->n * 8, st);
     int N = c->P->n;
     cbd_kernel<<<(N / 8 + 127) / 128, 128, 0, st>>>(o, seed, tag, sub, eta, N);
     HS_CHECK_LAUNCH();
@@ -675,6 +691,7 @@ __global__ void signed_to_rns_kernel(const int64_t *v, u64 *o, PrimeMap pm, int 
 
 void k_signed_to_rns(hs_ctx *c, const int64_t *v, u64 *o, int n_limbs, const PrimeMap &pm, cudaStream_t st)
 {
+    KTimer _kt(c, KID_RNG, (double)(n_limbs + 1) * c->P->n * 8, st);
     int N = c->P->n;
     signed_to_rns_kernel<<<GRID_LIMBS(n_limbs, N), 256, 0, st>>>(v, o, pm, N);
     HS_CHECK_LAUNCH();
@@ -696,6 +713,7 @@ __global__ void mac_pt_kernel(u64 *acc, const u64 *a, const u64 *pt, int N, int 
 
 void k_mac_pt(hs_ctx *c, u64 *acc, const u64 *a, const u64 *pt, int nl, int la, cudaStream_t st)
 {
+    KTimer _kt(c, KID_PTMUL, (double)nl * c->P->n * 8 * 7, st);
     int N = c->P->n;
     mac_pt_kernel<<<dim3((N + 255) / 256, nl, 2), 256, 0, st>>>(acc, a, pt, N, nl, la);
     HS_CHECK_LAUNCH();
@@ -720,6 +738,7 @@ __global__ void modraise_kernel(const u64 *x, u64 *o, int N, int nl)
 
 void k_modraise(hs_ctx *c, const u64 *x, u64 *o, int nl, cudaStream_t st)
 {
+    KTimer _kt(c, KID_MODRAISE, (double)(2 + 2 * nl) * c->P->n * 8, st);
     int N = c->P->n;
     modraise_kernel<<<dim3((N + 255) / 256, nl, 2), 256, 0, st>>>(x, o, N, nl);
     HS_CHECK_LAUNCH();

@@ -110,7 +110,8 @@ def build_setup(wl_name, rank, world, device):
     ctx = hs.Context(P, device)
     nb = n // m
     stride = (P.n // 2) // nb
-    rots = set(hs.bts_rotations(P))
+    bcfg = pre["bts"]
+    rots = set(hs.bts_rotations(P, bcfg))
     i = 0
     while (1 << i) < nb:
         rots |= {stride << i, -(stride << i)}
@@ -118,12 +119,12 @@ def build_setup(wl_name, rank, world, device):
     gal = sorted({P.galois_of_rot(r) for r in rots} | {2 * P.n - 1})
     t0 = time.time()
     K = hs.Keys(ctx, W.derive_seed("keys", wl_name), pre["h"], galois=gal)
-    B = hs.Bts(ctx, W.bts_tables()[pre["bts_table"]], pre["bts_out_level"])
+    B = hs.Bts(ctx, bcfg, W.bts_tables()[bcfg["table"]])
     x = W.softmax_inputs(L, n, wl["M"], seed=W.derive_seed("x", wl_name))
     slots = P.pack(x, m)
     ml = m // world
     mine = range(rank * ml, (rank + 1) * ml)
-    top = pre["bts_out_level"]
+    top = bcfg["out_level"]
     from concurrent.futures import ThreadPoolExecutor
     with ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1)) as ex:
         pts = list(ex.map(lambda c: P.encode(slots[c], scale=P.scale(top), level=top), mine))

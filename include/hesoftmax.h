@@ -178,26 +178,29 @@ int hs_cheb_depth(int deg);
 
 /* ------------------------------------------------------------ bootstrapping (G11) */
 /* Real-slot CoeffToSlot-first bootstrapping:
- * ModRaise -> 3 CoeffToSlot transforms -> real part -> EvalMod (Chebyshev
- * series of cos(2 pi (K+2) v / 2^r) and r double angles) -> 3 SlotToCoeff
- * transforms -> real part.  The output lands at out_level; the top level of
- * the chain must be out_level + 3 + 3 + r + hs_cheb_depth(cos_poly->deg).
+ * ModRaise -> n_cts CoeffToSlot transforms -> real part -> EvalMod (Chebyshev
+ * series of cos(2 pi (K+2) v / 2^r), r double angles, optional arcsine step
+ * s + s^3/6) -> n_stc SlotToCoeff transforms -> real part.  The output lands at
+ * out_level; the chain top must be
+ *   out_level + n_stc + 2 arcsine + r + hs_cheb_depth(cos_poly->deg) + n_cts.
  * Needs the relinearisation key, the conjugation key (Galois 2N-1) and the
- * rotations listed by hs_bts_rotations. */
+ * rotations listed by hs_bts_rotations.  HS_ELEVEL if the chain does not fit. */
 typedef struct hs_bts hs_bts;
 typedef struct {
     int K;                    /* bound on |I| after ModRaise                   */
     int r;                    /* double-angle steps                            */
     const hs_poly *cos_poly;  /* Chebyshev series on [-1, 1]                    */
     int out_level;
+    int n_cts, n_stc;         /* number of CoeffToSlot / SlotToCoeff transforms */
+    int arcsine;              /* 1: arcsine correction (2 levels)              */
 } hs_bts_desc;
 
 hs_status hs_bts_create(hs_ctx *c, const hs_bts_desc *d, hs_bts **out);
 void hs_bts_destroy(hs_bts *b);
 /* left-rotation amounts the transforms need (count returned; out may be NULL) */
-int hs_bts_rotations(const hs_params *p, int32_t *out, int max);
+int hs_bts_rotations(const hs_params *p, int n_cts, int n_stc, int32_t *out, int max);
 /* pre-scaling exponent for a message bound (G11) */
-int hs_bts_exponent(const hs_params *p, double bound);
+int hs_bts_exponent(const hs_params *p, int arcsine, double bound);
 /* bound: upper bound on |slot values| of `in` (selects the pre-scaling). */
 hs_status hs_bootstrap(hs_ctx *c, const hs_keys *k, hs_bts *b, const hs_ct *in, double bound, void *stream,
                        hs_ct **out);

@@ -181,19 +181,24 @@ void orc_api_ledger_reset(void) { memset(orc_ledger, 0, sizeof(orc_ledger)); }
 
 /* ---------------------------------------------------------------- bootstrapping */
 typedef struct orc_bts_set orc_bts_set;
-orc_bts_set *orc_bts_set_new(const orc_params *P, int K, int r, int deg, const double *coeffs, int out_level);
+orc_bts_set *orc_bts_set_new(const orc_params *P, int K, int r, int n_cts, int n_stc, int arcsine, int deg,
+                             const double *coeffs, int out_level);
 void orc_bts_set_free(orc_bts_set *S);
-int orc_bts_rotations(const orc_params *P, int *out, int max);
-int orc_bts_exponent(const orc_params *P, double bound);
+int orc_bts_rotations(const orc_params *P, int n_cts, int n_stc, int *out, int max);
+int orc_bts_exponent(const orc_params *P, int arcsine, double bound);
 orc_ct *orc_bootstrap(const orc_params *P, const orc_keys *K, const orc_ct *in, void *ctx, double bound);
 
-void *orc_api_bts_new(const orc_params *P, int K, int r, int deg, const double *coeffs, int out_level)
+void *orc_api_bts_new(const orc_params *P, int K, int r, int n_cts, int n_stc, int arcsine, int deg,
+                      const double *coeffs, int out_level)
 {
-    return orc_bts_set_new(P, K, r, deg, coeffs, out_level);
+    return orc_bts_set_new(P, K, r, n_cts, n_stc, arcsine, deg, coeffs, out_level);
 }
 void orc_api_bts_free(void *p) { orc_bts_set_free(p); }
-int orc_api_bts_rotations(const orc_params *P, int *out, int max) { return orc_bts_rotations(P, out, max); }
-int orc_api_bts_exponent(const orc_params *P, double bound) { return orc_bts_exponent(P, bound); }
+int orc_api_bts_rotations(const orc_params *P, int n_cts, int n_stc, int *out, int max)
+{
+    return orc_bts_rotations(P, n_cts, n_stc, out, max);
+}
+int orc_api_bts_exponent(const orc_params *P, int arcsine, double bound) { return orc_bts_exponent(P, arcsine, bound); }
 orc_ct *orc_api_bootstrap(const orc_params *P, const orc_keys *K, const orc_ct *in, void *bts, double bound)
 {
     return orc_bootstrap(P, K, in, bts, bound);

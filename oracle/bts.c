@@ -6,14 +6,16 @@
  * its internals (HEaaN FGb, PAPER.md 386-393).  DESIGN.md reading G11 fixes a
  * textbook CoeffToSlot-first bootstrap specialised to real slot values (all
  * Softmax data are real):
+ *   0. pre-scale: x *= 2^e, e = clamp(floor(log2 q0 - cap - log2 Delta_0 - log2 B), 0, 30)
+ *      (cap = 8 with the arcsine step, 12 without; B = caller's bound on |z|);
  *   1. drop to level 0; ModRaise to level L (centred lift of the q_0 residues);
- *   2. CoeffToSlot: three sparse linear transforms (groups of inverse special-
+ *   2. CoeffToSlot: n_cts sparse linear transforms (groups of inverse special-
  *      FFT stages), slot p then holds kappa (c_j + i c_{j+N0}) / q_0, j = brv(p);
  *   3. v = w + conj(w) - 1/(4(K+2))  (real part, mapped onto [-1, 1]);
  *   4. EvalMod: Chebyshev series of cos(2 pi (K+2) v / 2^r), r double angles
- *      -> sin(2 pi c_j / q_0) ~ 2 pi m_j / q_0;
- *   5. SlotToCoeff: three transforms (groups of special-FFT stages) with the
- *      factor q_0 / (4 pi Delta_out) and D = diag(1, 2, ..., 2) (real-message
+ *      -> s = sin(2 pi c_j / q_0);  optional arcsine step s <- s + s^3/6;
+ *   5. SlotToCoeff: n_stc transforms (groups of special-FFT stages) with the
+ *      factor q_0 / (4 pi Delta_out 2^e) and D = diag(1, 2, ..., 2) (real-message
  *      identity z = Re(V D m_lo)), then out = x + conj(x).
  * Each linear transform is a baby-step/giant-step diagonal evaluation landing
  * at the canonical scale of the next level (one rescale).
@@ -131,6 +133,8 @@ static void dm_scale_cols(dmat *m, const f128 *s)  /* m <- m diag(s) */
 }
 
 /* ------------------------------------------------------------ plan */
+#define ORC_MAXG 8
+
 typedef struct {
     int level;           /* input level of this transform          */
     int u, b1;           /* step unit, baby size                   */
@@ -140,18 +144,22 @@ typedef struct {
 } ltrans;
 
 typedef struct {
+    int K, r, n_cts, n_stc, arcsine, out_level;
+} orc_bts_cfg;
+
+typedef struct {
     const orc_params *P;
-    int K, r, e;
+    orc_bts_cfg cfg;
+    int e;
     const orc_cheb *cosp;
-    ltrans cts[3], stc[3];
-    int out_level;
+    ltrans cts[ORC_MAXG], stc[ORC_MAXG];
 } orc_bts_plan;
 
 /* all plans of one parameter set, one per pre-scaling exponent e */
 #define ORC_BTS_EMAX 30
 typedef struct {
     const orc_params *P;
-    int K, r, out_level;
+    orc_bts_cfg cfg;
     orc_cheb cosp;
     double *coeffs;
     orc_bts_plan *plan[ORC_BTS_EMAX + 1];
@@ -159,10 +167,11 @@ typedef struct {
 
 static int ilog2i(int x) { int t = 0; while ((1 << t) < x) t++; return t; }
 
-static void group_sizes(int s, int *sz)
+/* split s stages into g groups, the earlier groups not smaller */
+static void group_sizes(int s, int g, int *sz)
 {
     int rem = s;
-    for (int k = 3, i = 0; k >= 1; k--, i++) { sz[i] = (rem + k - 1) / k; rem -= sz[i]; }
+    for (int k = g, i = 0; k >= 1; k--, i++) { sz[i] = (rem + k - 1) / k; rem -= sz[i]; }
 }
 
 /* encode a transform at input level `level` */
@@ -222,12 +231,11 @@ static void free_ltrans(ltrans *T)
     free(T->b);
 }
 
-/* the rotations (left, slots) a plan needs: babies b u, giants g b1 u */
-int orc_bts_rotations(const orc_params *P, int *out, int max)
+static void add_group_rotations(int n0, int ngroups, int *out, int *cnt, int max)
 {
-    int n0 = P->n / 2, s = ilog2i(n0), sz[3], cnt = 0, first = 0;
-    group_sizes(s, sz);
-    for (int gi = 0; gi < 3; gi++) {
+    int s = ilog2i(n0), sz[ORC_MAXG], first = 0;
+    group_sizes(s, ngroups, sz);
+    for (int gi = 0; gi < ngroups; gi++) {
         int u = 1 << first, r = sz[gi], b1 = 1 << ((r + 2) / 2);
         int span = (1 << r) - 1;  /* idx in [-span, span] mod n0/u */
         int mod = n0 / u;
@@ -238,80 +246,90 @@ int orc_bts_rotations(const orc_params *P, int *out, int max)
                 int rr = rots[t] % n0;
                 if (!rr) continue;
                 int dup = 0;
-                for (int i = 0; i < cnt; i++) if (out[i] == rr) dup = 1;
-                if (!dup && cnt < max) out[cnt++] = rr;
+                for (int i = 0; i < *cnt; i++) if (out[i] == rr) dup = 1;
+                if (!dup && *cnt < max) out[(*cnt)++] = rr;
             }
         }
         first += r;
     }
+}
+
+/* the rotations (left, slots) a plan needs: babies b u, giants g b1 u of the
+ * SlotToCoeff groups, then of the CoeffToSlot groups (same stage grouping
+ * rule; duplicates removed in first-seen order) */
+int orc_bts_rotations(const orc_params *P, int n_cts, int n_stc, int *out, int max)
+{
+    int cnt = 0;
+    add_group_rotations(P->n / 2, n_stc, out, &cnt, max);
+    add_group_rotations(P->n / 2, n_cts, out, &cnt, max);
     return cnt;
+}
+
+static dmat *group_matrix(const orc_params *P, int first, int size, int inverse)
+{
+    dmat *acc = NULL;
+    for (int t = 0; t < size; t++) {
+        int i = inverse ? first + size - 1 - t : first + t;  /* inverse: largest stage first */
+        dmat *S = stage(P->log_n, 2 << i, inverse);
+        if (!acc) acc = S;
+        else { dmat *x = compose(S, acc); dm_free(S); dm_free(acc); acc = x; }
+    }
+    return acc;
 }
 
 /* e: the input is multiplied by 2^e before ModRaise (message pre-scaling,
  * DESIGN.md G11); SlotToCoeff divides it back. */
-orc_bts_plan *orc_bts_plan_new(const orc_params *P, int K, int r, const orc_cheb *cosp, int out_level, int e)
+static orc_bts_plan *plan_new(const orc_params *P, const orc_bts_cfg *cfg, const orc_cheb *cosp, int e)
 {
     orc_bts_plan *B = calloc(1, sizeof(*B));
-    B->e = e;
     B->P = P;
-    B->K = K;
-    B->r = r;
+    B->cfg = *cfg;
+    B->e = e;
     B->cosp = cosp;
-    B->out_level = out_level;
-    int N = P->n, n0 = N / 2, s = ilog2i(n0), sz[3];
-    group_sizes(s, sz);
-    int L = P->L;
-    dmat *grp[3];
-    int first[3];
-    for (int gi = 0, st = 0; gi < 3; gi++) {
-        first[gi] = st;
-        dmat *acc = NULL;
-        for (int i = st; i < st + sz[gi]; i++) {
-            dmat *S = stage(P->log_n, 2 << i, 0);
-            if (!acc) acc = S;
-            else { dmat *t = compose(S, acc); dm_free(S); dm_free(acc); acc = t; }
+    int n0 = P->n / 2, s = ilog2i(n0), L = P->L;
+    int sz[ORC_MAXG], first[ORC_MAXG];
+    /* SlotToCoeff: groups in stage order; first transform composed with diag(lambda D) */
+    group_sizes(s, cfg->n_stc, sz);
+    for (int gi = 0, st = 0; gi < cfg->n_stc; st += sz[gi], gi++) {
+        dmat *m = group_matrix(P, st, sz[gi], 0);
+        if (gi == 0) {
+            f128 lam = (f128)P->prime[0] / (4 * M_PIq * (f128)P->scale[cfg->out_level] * ldexpq(1, e));
+            f128 *dv = malloc(sizeof(f128) * n0);
+            for (int p = 0; p < n0; p++) dv[p] = p == 0 ? lam : 2 * lam;
+            dm_scale_cols(m, dv);
+            free(dv);
         }
-        grp[gi] = acc;
-        st += sz[gi];
+        make_ltrans(P, m, cfg->out_level + cfg->n_stc - gi, 1 << st, sz[gi], &B->stc[gi]);
+        dm_free(m);
     }
-    /* SlotToCoeff: M_0 diag(lambda D), M_1, M_2 at levels out+3, out+2, out+1 */
-    f128 lam = (f128)P->prime[0] / (4 * M_PIq * (f128)P->scale[out_level] * ldexpq(1, e));
-    f128 *dv = malloc(sizeof(f128) * n0);
-    for (int p = 0; p < n0; p++) dv[p] = p == 0 ? lam : 2 * lam;
-    dm_scale_cols(grp[0], dv);
-    free(dv);
-    for (int gi = 0; gi < 3; gi++) make_ltrans(P, grp[gi], out_level + 3 - gi, 1 << first[gi], sz[gi], &B->stc[gi]);
-    for (int gi = 0; gi < 3; gi++) dm_free(grp[gi]);
-    /* CoeffToSlot: inverse groups in reverse order, factor kappa Delta_L / q0 first */
-    for (int k = 0; k < 3; k++) {
-        int gi = 2 - k;
-        dmat *acc = NULL;
-        for (int i = first[gi] + sz[gi] - 1; i >= first[gi]; i--) {
-            dmat *S = stage(P->log_n, 2 << i, 1);
-            if (!acc) acc = S;
-            else { dmat *t = compose(S, acc); dm_free(S); dm_free(acc); acc = t; }
-        }
+    /* CoeffToSlot: inverse groups, largest stages first; factor kappa Delta_L / q0 first */
+    group_sizes(s, cfg->n_cts, sz);
+    for (int gi = 0, st = 0; gi < cfg->n_cts; st += sz[gi], gi++) first[gi] = st;
+    for (int k = 0; k < cfg->n_cts; k++) {
+        int gi = cfg->n_cts - 1 - k;
+        dmat *m = group_matrix(P, first[gi], sz[gi], 1);
         if (k == 0) {
-            f128 f = ((f128)P->scale[L] / (f128)P->prime[0]) / (2 * (f128)(K + 2));
+            f128 f = ((f128)P->scale[L] / (f128)P->prime[0]) / (2 * (f128)(cfg->K + 2));
             f128 *fv = malloc(sizeof(f128) * n0);
             for (int p = 0; p < n0; p++) fv[p] = f;
-            dm_scale_cols(acc, fv);
+            dm_scale_cols(m, fv);
             free(fv);
         }
-        make_ltrans(P, acc, L - k, 1 << first[gi], sz[gi], &B->cts[k]);
-        dm_free(acc);
+        make_ltrans(P, m, L - k, 1 << first[gi], sz[gi], &B->cts[k]);
+        dm_free(m);
     }
     return B;
 }
 
-void orc_bts_plan_free(orc_bts_plan *B)
+static void plan_free(orc_bts_plan *B)
 {
     if (!B) return;
-    for (int k = 0; k < 3; k++) { free_ltrans(&B->cts[k]); free_ltrans(&B->stc[k]); }
+    for (int k = 0; k < B->cfg.n_cts; k++) free_ltrans(&B->cts[k]);
+    for (int k = 0; k < B->cfg.n_stc; k++) free_ltrans(&B->stc[k]);
     free(B);
 }
 
-/* ct (level T->level, 2 comps) -> transform, landing at level-1 */
+/* ct (2 comps) -> transform at level T->level, landing at level-1 */
 static orc_ct *apply_ltrans(const orc_params *P, const orc_keys *K, const orc_ct *ct0, const ltrans *T)
 {
     int N = P->n, n0 = N / 2, l = T->level;
@@ -394,28 +412,30 @@ static orc_ct *mod_raise(const orc_params *P, const orc_ct *ct)
     return r;
 }
 
-int orc_bts_debug_stop = -1;  /* test hook: return the intermediate after this stage */
-int orc_bts_debug_skip_raise = 0;  /* test hook: input is already at level L */
-#define STOP(st, ct) if (orc_bts_debug_stop == (st)) return ct;
-
-/* G11 pre-scaling exponent for a message bound B:
- * e = floor(log2 q_0 - 12 - log2 Delta_0 - log2 B) clamped to [0, 30], so that
- * |2^e m| <= 2^-12 q_0 and sin(2 pi y) ~ 2 pi y stays accurate. */
-int orc_bts_exponent(const orc_params *P, double bound)
+/* G11 pre-scaling exponent for a message bound B. */
+int orc_bts_exponent(const orc_params *P, int arcsine, double bound)
 {
-    double e = floor(log2((double)P->prime[0]) - 12.0 - log2(P->scale[0]) - log2(bound));
+    double cap = arcsine ? 8.0 : 12.0;
+    double e = floor(log2((double)P->prime[0]) - cap - log2(P->scale[0]) - log2(bound));
     if (e < 0) e = 0;
     if (e > ORC_BTS_EMAX) e = ORC_BTS_EMAX;
     return (int)e;
 }
 
-orc_bts_set *orc_bts_set_new(const orc_params *P, int K, int r, int deg, const double *coeffs, int out_level)
+/* the chain the plan needs: L = out + n_stc + 2 arcsine + r + depth(cos) + n_cts */
+orc_bts_set *orc_bts_set_new(const orc_params *P, int K, int r, int n_cts, int n_stc, int arcsine, int deg,
+                             const double *coeffs, int out_level)
 {
+    if (n_cts < 1 || n_cts > ORC_MAXG || n_stc < 1 || n_stc > ORC_MAXG) return NULL;
+    if (out_level + n_stc + 2 * (arcsine != 0) + r + orc_cheb_depth(deg) + n_cts != P->L) return NULL;
     orc_bts_set *S = calloc(1, sizeof(*S));
     S->P = P;
-    S->K = K;
-    S->r = r;
-    S->out_level = out_level;
+    S->cfg.K = K;
+    S->cfg.r = r;
+    S->cfg.n_cts = n_cts;
+    S->cfg.n_stc = n_stc;
+    S->cfg.arcsine = arcsine != 0;
+    S->cfg.out_level = out_level;
     S->coeffs = malloc(sizeof(double) * (deg + 1));
     memcpy(S->coeffs, coeffs, sizeof(double) * (deg + 1));
     S->cosp.deg = deg;
@@ -428,16 +448,21 @@ orc_bts_set *orc_bts_set_new(const orc_params *P, int K, int r, int deg, const d
 void orc_bts_set_free(orc_bts_set *S)
 {
     if (!S) return;
-    for (int e = 0; e <= ORC_BTS_EMAX; e++) orc_bts_plan_free(S->plan[e]);
+    for (int e = 0; e <= ORC_BTS_EMAX; e++) plan_free(S->plan[e]);
     free(S->coeffs);
     free(S);
 }
 
+int orc_bts_debug_stop = -1;       /* test hook: return the intermediate after this stage */
+int orc_bts_debug_skip_raise = 0;  /* test hook: input is already at level L */
+#define STOP(st, ct) if (orc_bts_debug_stop == (st)) return ct;
+
 orc_ct *orc_bootstrap(const orc_params *P, const orc_keys *K, const orc_ct *in, void *ctx, double bound)
 {
     orc_bts_set *BS = ctx;
-    int e = orc_bts_exponent(P, bound);
-    if (!BS->plan[e]) BS->plan[e] = orc_bts_plan_new(P, BS->K, BS->r, &BS->cosp, BS->out_level, e);
+    const orc_bts_cfg *cf = &BS->cfg;
+    int e = orc_bts_exponent(P, cf->arcsine, bound);
+    if (!BS->plan[e]) BS->plan[e] = plan_new(P, cf, &BS->cosp, e);
     const orc_bts_plan *B = BS->plan[e];
     int conj = 2 * P->n - 1;
     orc_ct *c0 = e ? orc_op_mult_int(P, in, (int64_t)1 << e) : orc_ct_copy(P, in);
@@ -447,7 +472,7 @@ orc_ct *orc_bootstrap(const orc_params *P, const orc_keys *K, const orc_ct *in, 
     orc_ct *x = orc_bts_debug_skip_raise ? orc_ct_copy(P, in) : mod_raise(P, low);
     orc_ct_release(low);
     STOP(0, x);
-    for (int k = 0; k < 3; k++) {
+    for (int k = 0; k < cf->n_cts; k++) {
         orc_ct *t = apply_ltrans(P, K, x, &B->cts[k]);
         orc_ct_release(x);
         if (!t) return NULL;
@@ -459,13 +484,13 @@ orc_ct *orc_bootstrap(const orc_params *P, const orc_keys *K, const orc_ct *in, 
     orc_ct *v = orc_op_add(P, x, cj);
     orc_ct_release(x);
     orc_ct_release(cj);
-    orc_ct *v2 = orc_op_add_const(P, v, -1.0 / (4.0 * (B->K + 2)));
+    orc_ct *v2 = orc_op_add_const(P, v, -1.0 / (4.0 * (cf->K + 2)));
     orc_ct_release(v);
-    STOP(4, v2);
+    STOP(10, v2);
     orc_ct *s = orc_eval_cheb_unit(P, K, v2, B->cosp);
     orc_ct_release(v2);
-    STOP(5, s);
-    for (int i = 0; i < B->r; i++) {
+    STOP(11, s);
+    for (int i = 0; i < cf->r; i++) {
         orc_ct *m = orc_op_mult(P, K, s, s);
         orc_ct *m2 = orc_op_mult_int(P, m, 2);
         orc_ct_release(s);
@@ -473,13 +498,24 @@ orc_ct *orc_bootstrap(const orc_params *P, const orc_keys *K, const orc_ct *in, 
         s = orc_op_add_const(P, m2, -1.0);
         orc_ct_release(m2);
     }
-    STOP(6, s);
-    for (int k = 0; k < 3; k++) {
+    if (cf->arcsine) {   /* s <- s + (1/6) s^3  (arcsin(s) to O(s^5)) */
+        orc_ct *s6 = orc_op_mult_const(P, s, 1.0 / 6.0, s->level - 1);
+        orc_ct *t = orc_op_mult(P, K, s, s);
+        orc_ct *u = orc_op_mult(P, K, s6, t);
+        orc_ct *w = orc_op_add(P, s, u);
+        orc_ct_release(s6);
+        orc_ct_release(t);
+        orc_ct_release(u);
+        orc_ct_release(s);
+        s = w;
+    }
+    STOP(12, s);
+    for (int k = 0; k < cf->n_stc; k++) {
         orc_ct *t = apply_ltrans(P, K, s, &B->stc[k]);
         orc_ct_release(s);
         if (!t) return NULL;
         s = t;
-        STOP(7 + k, s);
+        STOP(20 + k, s);
     }
     cj = orc_op_galois(P, K, s, conj);
     if (!cj) return NULL;

@@ -349,14 +349,14 @@ def _bts_sigs():
         return L
     vp = C.c_void_p
     L.orc_api_bts_new.restype = vp
-    L.orc_api_bts_new.argtypes = [vp, C.c_int, C.c_int, C.c_int, f64p, C.c_int]
+    L.orc_api_bts_new.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, f64p, C.c_int]
     L.orc_api_bts_free.argtypes = [vp]
     L.orc_api_bts_rotations.restype = C.c_int
-    L.orc_api_bts_rotations.argtypes = [vp, i32p, C.c_int]
+    L.orc_api_bts_rotations.argtypes = [vp, C.c_int, C.c_int, i32p, C.c_int]
     L.orc_api_bootstrap.restype = vp
     L.orc_api_bootstrap.argtypes = [vp, vp, vp, vp, C.c_double]
     L.orc_api_bts_exponent.restype = C.c_int
-    L.orc_api_bts_exponent.argtypes = [vp, C.c_double]
+    L.orc_api_bts_exponent.argtypes = [vp, C.c_int, C.c_double]
     L.orc_api_softmax_bts.restype = C.c_int
     L.orc_api_softmax_bts.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, i32p, f64p, f64p, f64p,
                                       C.POINTER(vp), C.POINTER(vp), vp]
@@ -364,19 +364,25 @@ def _bts_sigs():
     return L
 
 
-def bts_rotations(P: Params):
-    out = np.zeros(256, np.int32)
-    n = _bts_sigs().orc_api_bts_rotations(P.ptr, out, 256)
+def bts_rotations(P: Params, cfg: dict):
+    """cfg: a preset's "bts" entry (n_cts, n_stc)"""
+    out = np.zeros(512, np.int32)
+    n = _bts_sigs().orc_api_bts_rotations(P.ptr, cfg["n_cts"], cfg["n_stc"], out, 512)
     return [int(v) for v in out[:n]]
 
 
 class Bts:
-    """Precomputed bootstrapping plan (diagonals encoded in quad precision)."""
+    """Precomputed bootstrapping plans (diagonals encoded in quad precision).
 
-    def __init__(self, P: Params, table: dict, out_level: int):
+    cfg: a preset's "bts" entry {n_cts, n_stc, arcsine, out_level}; table: the
+    EvalMod cosine table {K, r, coeffs}."""
+
+    def __init__(self, P: Params, cfg: dict, table: dict):
         c = np.ascontiguousarray(table["coeffs"], np.float64)
-        self.P = P
-        self.ptr = _bts_sigs().orc_api_bts_new(P.ptr, table["K"], table["r"], len(c) - 1, c, out_level)
+        self.P, self.cfg = P, cfg
+        self.ptr = _bts_sigs().orc_api_bts_new(P.ptr, table["K"], table["r"], cfg["n_cts"], cfg["n_stc"],
+                                               1 if cfg["arcsine"] else 0, len(c) - 1, c, cfg["out_level"])
+        assert self.ptr, "bootstrapping chain does not match the parameter set"
 
     def __del__(self):
         if getattr(self, "ptr", None) and _lib is not None:
@@ -389,8 +395,8 @@ def bootstrap(P: Params, K: Keys, ct: Ct, bts: Bts, bound: float = 1.0) -> Ct:
     return Ct(P, _bts_sigs().orc_api_bootstrap(P.ptr, K.ptr, ct.ptr, bts.ptr, bound))
 
 
-def bts_exponent(P: Params, bound: float) -> int:
-    return int(_bts_sigs().orc_api_bts_exponent(P.ptr, bound))
+def bts_exponent(P: Params, arcsine: bool, bound: float) -> int:
+    return int(_bts_sigs().orc_api_bts_exponent(P.ptr, 1 if arcsine else 0, bound))
 
 
 def softmax_bts(P: Params, K: Keys, cts, n, k, variant, exp_poly, inv_polys, bts: Bts):

@@ -239,13 +239,17 @@ def cheb_depth(deg):
 
 
 class Bts:
-    """hs_bts: real-slot bootstrapping plan (G11)."""
+    """hs_bts: real-slot bootstrapping plan (G11).
 
-    def __init__(self, ctx: Context, table: dict, out_level: int):
+    cfg: a preset's "bts" entry {n_cts, n_stc, arcsine, out_level};
+    table: the EvalMod cosine table {K, r, coeffs} (data/bts_tables.json)."""
+
+    def __init__(self, ctx: Context, cfg: dict, table: dict):
         self.ctx = ctx
         pp, self._c = _poly(table)
         self._p = pp
-        d = L.BtsDesc(int(table["K"]), int(table["r"]), C.pointer(self._p), out_level)
+        d = L.BtsDesc(int(table["K"]), int(table["r"]), C.pointer(self._p), int(cfg["out_level"]),
+                      int(cfg["n_cts"]), int(cfg["n_stc"]), 1 if cfg["arcsine"] else 0)
         out = C.c_void_p()
         check(L.hs_bts_create(ctx.ptr, C.byref(d), C.byref(out)))
         self.ptr = out
@@ -256,14 +260,14 @@ class Bts:
             self.ptr = None
 
 
-def bts_rotations(params: Params):
+def bts_rotations(params: Params, cfg: dict):
     out = np.zeros(512, np.int32)
-    n = L.hs_bts_rotations(params.ptr, out, 512)
+    n = L.hs_bts_rotations(params.ptr, int(cfg["n_cts"]), int(cfg["n_stc"]), out, 512)
     return [int(v) for v in out[:n]]
 
 
-def bts_exponent(params: Params, bound: float) -> int:
-    return int(L.hs_bts_exponent(params.ptr, bound))
+def bts_exponent(params: Params, arcsine: bool, bound: float) -> int:
+    return int(L.hs_bts_exponent(params.ptr, 1 if arcsine else 0, bound))
 
 
 def bootstrap(keys: Keys, bts: Bts, ct: Ciphertext, bound=1.0, stream=None) -> Ciphertext:

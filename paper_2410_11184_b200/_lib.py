@@ -57,7 +57,8 @@ class SoftmaxDesc(C.Structure):
 
 
 class BtsDesc(C.Structure):
-    _fields_ = [("K", C.c_int), ("r", C.c_int), ("cos_poly", C.POINTER(Poly)), ("out_level", C.c_int)]
+    _fields_ = [("K", C.c_int), ("r", C.c_int), ("cos_poly", C.POINTER(Poly)), ("out_level", C.c_int),
+                ("n_cts", C.c_int), ("n_stc", C.c_int), ("arcsine", C.c_int)]
 
 
 def _sig(name, res, args):
@@ -108,8 +109,8 @@ hs_softmax_many_ctxt = _sig("hs_softmax_many_ctxt", C.c_int,
                             [vp, vp, C.POINTER(SoftmaxDesc), C.POINTER(vp), C.c_size_t, vp, C.POINTER(vp)])
 hs_bts_create = _sig("hs_bts_create", C.c_int, [vp, C.POINTER(BtsDesc), C.POINTER(vp)])
 hs_bts_destroy = _sig("hs_bts_destroy", None, [vp])
-hs_bts_rotations = _sig("hs_bts_rotations", C.c_int, [vp, i32p, C.c_int])
-hs_bts_exponent = _sig("hs_bts_exponent", C.c_int, [vp, C.c_double])
+hs_bts_rotations = _sig("hs_bts_rotations", C.c_int, [vp, C.c_int, C.c_int, i32p, C.c_int])
+hs_bts_exponent = _sig("hs_bts_exponent", C.c_int, [vp, C.c_int, C.c_double])
 hs_bootstrap = _sig("hs_bootstrap", C.c_int, [vp, vp, vp, vp, C.c_double, vp, C.POINTER(vp)])
 hs_ledger_get = _sig("hs_ledger_get", C.c_int, [vp, C.POINTER(C.c_int64), C.c_int])
 hs_ledger_reset = _sig("hs_ledger_reset", C.c_int, [vp])

@@ -3,12 +3,14 @@
 // PAPER.md 281-283 / 429-440 need bootstrapping but give no internals (the
 // paper calls HEaaN's FGb BTS, PAPER.md 386-393).  Conventions shared with
 // the oracle only in writing:
-//   e = clamp(floor(log2 q0 - 12 - log2 Delta_0 - log2 bound), 0, 30); x *= 2^e
+//   e = clamp(floor(log2 q0 - cap - log2 Delta_0 - log2 bound), 0, 30), cap = 8
+//       with the arcsine step else 12;  x *= 2^e
 //   drop to level 0; ModRaise (centred lift of the q0 residues) to level L
-//   CoeffToSlot: inverse special-FFT stages in 3 groups (largest stages first),
-//                first transform scaled by (Delta_L / q0) / (2 (K+2))
-//   v = w + conj(w) - 1/(4 (K+2)); EvalMod = cos series on [-1,1], r x (2c^2-1)
-//   SlotToCoeff: special-FFT stages in 3 groups, first transform composed with
+//   CoeffToSlot: inverse special-FFT stages in n_cts groups (largest stages
+//                first), the first transform scaled by (Delta_L / q0) / (2 (K+2))
+//   v = w + conj(w) - 1/(4 (K+2)); EvalMod = cos series on [-1,1], r x (2c^2-1);
+//   arcsine step s <- s + (1/6) s^3 (s6 = mult_const(s, 1/6), t = s*s, s + s6*t)
+//   SlotToCoeff: special-FFT stages in n_stc groups, the first composed with
 //                diag(lambda, 2 lambda, ..., 2 lambda), lambda = q0/(4 pi Delta_out 2^e)
 //   out = x + conj(x)
 // Each transform: diagonals d (mod N0, structural presence), step unit u =
@@ -21,7 +23,6 @@
 #include <quadmath.h>
 
 #include <algorithm>
-#include <array>
 #include <map>
 #include <vector>
 
@@ -104,13 +105,15 @@ void scale_columns(DiagMat &m, const std::vector<f128> &s)
             }
 }
 
-void group_sizes(int s, int sz[3])
+std::vector<int> group_sizes(int s, int g)
 {
+    std::vector<int> sz;
     int rem = s;
-    for (int k = 3, i = 0; k >= 1; k--, i++) {
-        sz[i] = (rem + k - 1) / k;
-        rem -= sz[i];
+    for (int k = g; k >= 1; k--) {
+        sz.push_back((rem + k - 1) / k);
+        rem -= sz.back();
     }
+    return sz;
 }
 
 int ilog2(int x)
@@ -120,10 +123,25 @@ int ilog2(int x)
     return t;
 }
 
+// product of the stages [first, first+size): forward in stage order, inverse
+// largest stage first
+DiagMat group_matrix(int log_n, int first, int size, bool inverse)
+{
+    DiagMat acc(1 << (log_n - 1));
+    for (int t = 0; t < size; t++) {
+        const int i = inverse ? first + size - 1 - t : first + t;
+        DiagMat S = fft_stage(log_n, 2 << i, inverse);
+        acc = t ? matmul(S, acc) : S;
+    }
+    return acc;
+}
+
 struct LinTrans {
     int level = 0, unit = 1, b1 = 1;
     std::vector<int> g, b;
     u64 *pts = nullptr;  // [terms][level+1][N] NTT-domain plaintexts
+    LinTrans() {}
+    LinTrans(const LinTrans &) = delete;
     ~LinTrans() { if (pts) cudaFree(pts); }
 };
 
@@ -162,32 +180,11 @@ void build_lintrans(hs_ctx *c, const DiagMat &m, int level, int unit, int r, Lin
     HS_CUDA(cudaDeviceSynchronize());
 }
 
-}  // namespace
-
-struct hs_bts {
-    hs_ctx *ctx = nullptr;
-    int K = 0, r = 0, out_level = 0;
-    std::vector<double> cos_coeffs;
-    hs_poly cos_poly{};
-    bool cts_ready = false;
-    std::array<LinTrans, 3> cts;
-    std::map<int, std::array<LinTrans, 3>> stc;  // per pre-scaling exponent e
-    std::mutex mu;
-};
-
-int bts_exponent(const hs_params *P, double bound)
+void add_group_rotations(int n0, int ngroups, std::vector<int> &rots)
 {
-    double e = floor(log2((double)P->prime[0]) - 12.0 - log2(P->scale[0]) - log2(bound));
-    return (int)std::min(30.0, std::max(0.0, e));
-}
-
-int bts_rotations(const hs_params *P, int32_t *out, int max)
-{
-    const int n0 = P->n / 2;
-    int sz[3], cnt = 0, first = 0;
-    group_sizes(ilog2(n0), sz);
-    std::vector<int> rots;
-    for (int gi = 0; gi < 3; gi++) {
+    std::vector<int> sz = group_sizes(ilog2(n0), ngroups);
+    int first = 0;
+    for (int gi = 0; gi < ngroups; gi++) {
         const int u = 1 << first, r = sz[gi], b1 = 1 << ((r + 2) / 2), span = (1 << r) - 1, mod = n0 / u;
         for (int idx = -span; idx <= span; idx++) {
             int id = ((idx % mod) + mod) % mod;
@@ -198,6 +195,33 @@ int bts_rotations(const hs_params *P, int32_t *out, int max)
         }
         first += r;
     }
+}
+
+}  // namespace
+
+struct hs_bts {
+    hs_ctx *ctx = nullptr;
+    int K = 0, r = 0, out_level = 0, n_cts = 0, n_stc = 0, arcsine = 0;
+    std::vector<double> cos_coeffs;
+    hs_poly cos_poly{};
+    std::vector<std::unique_ptr<LinTrans>> cts;                   // shared by every e
+    std::map<int, std::vector<std::unique_ptr<LinTrans>>> stc;    // per pre-scaling exponent e
+    std::mutex mu;
+};
+
+int bts_exponent(const hs_params *P, int arcsine, double bound)
+{
+    const double cap = arcsine ? 8.0 : 12.0;
+    double e = floor(log2((double)P->prime[0]) - cap - log2(P->scale[0]) - log2(bound));
+    return (int)std::min(30.0, std::max(0.0, e));
+}
+
+int bts_rotations(const hs_params *P, int n_cts, int n_stc, int32_t *out, int max)
+{
+    std::vector<int> rots;
+    add_group_rotations(P->n / 2, n_stc, rots);
+    add_group_rotations(P->n / 2, n_cts, rots);
+    int cnt = 0;
     for (int v : rots) {
         if (out && cnt < max) out[cnt] = v;
         cnt++;
@@ -207,58 +231,43 @@ int bts_rotations(const hs_params *P, int32_t *out, int max)
 
 static void ensure_cts(hs_bts *B)
 {
-    if (B->cts_ready) return;
+    if (!B->cts.empty()) return;
     hs_ctx *c = B->ctx;
     const hs_params *P = c->P;
     const int n0 = P->n / 2, L = P->L;
-    int sz[3], first[3];
-    group_sizes(ilog2(n0), sz);
-    first[0] = 0;
-    first[1] = sz[0];
-    first[2] = sz[0] + sz[1];
-    for (int k = 0; k < 3; k++) {
-        const int gi = 2 - k;
-        DiagMat acc(n0);
-        bool have = false;
-        for (int i = first[gi] + sz[gi] - 1; i >= first[gi]; i--) {
-            DiagMat S = fft_stage(P->log_n, 2 << i, true);
-            acc = have ? matmul(S, acc) : S;
-            have = true;
-        }
+    std::vector<int> sz = group_sizes(ilog2(n0), B->n_cts), first(B->n_cts);
+    for (int gi = 0, st = 0; gi < B->n_cts; st += sz[gi], gi++) first[gi] = st;
+    for (int k = 0; k < B->n_cts; k++) {
+        const int gi = B->n_cts - 1 - k;
+        DiagMat m = group_matrix(P->log_n, first[gi], sz[gi], true);
         if (k == 0) {
             f128 f = ((f128)P->scale[L] / (f128)P->prime[0]) / (2 * (f128)(B->K + 2));
-            scale_columns(acc, std::vector<f128>(n0, f));
+            scale_columns(m, std::vector<f128>(n0, f));
         }
-        build_lintrans(c, acc, L - k, 1 << first[gi], sz[gi], B->cts[k]);
+        B->cts.emplace_back(new LinTrans);
+        build_lintrans(c, m, L - k, 1 << first[gi], sz[gi], *B->cts.back());
     }
-    B->cts_ready = true;
 }
 
-static std::array<LinTrans, 3> &ensure_stc(hs_bts *B, int e)
+static std::vector<std::unique_ptr<LinTrans>> &ensure_stc(hs_bts *B, int e)
 {
     auto it = B->stc.find(e);
     if (it != B->stc.end()) return it->second;
     hs_ctx *c = B->ctx;
     const hs_params *P = c->P;
     const int n0 = P->n / 2;
-    int sz[3];
-    group_sizes(ilog2(n0), sz);
-    std::array<LinTrans, 3> &T = B->stc[e];
-    for (int gi = 0, st = 0; gi < 3; st += sz[gi], gi++) {
-        DiagMat acc(n0);
-        bool have = false;
-        for (int i = st; i < st + sz[gi]; i++) {
-            DiagMat S = fft_stage(P->log_n, 2 << i, false);
-            acc = have ? matmul(S, acc) : S;
-            have = true;
-        }
+    std::vector<int> sz = group_sizes(ilog2(n0), B->n_stc);
+    std::vector<std::unique_ptr<LinTrans>> &T = B->stc[e];
+    for (int gi = 0, st = 0; gi < B->n_stc; st += sz[gi], gi++) {
+        DiagMat m = group_matrix(P->log_n, st, sz[gi], false);
         if (gi == 0) {
             f128 lam = (f128)P->prime[0] / (4 * M_PIq * (f128)P->scale[B->out_level] * ldexpq(1, e));
             std::vector<f128> dv(n0, 2 * lam);
             dv[0] = lam;
-            scale_columns(acc, dv);
+            scale_columns(m, dv);
         }
-        build_lintrans(c, acc, B->out_level + 3 - gi, 1 << st, sz[gi], T[gi]);
+        T.emplace_back(new LinTrans);
+        build_lintrans(c, m, B->out_level + B->n_stc - gi, 1 << st, sz[gi], *T.back());
     }
     return T;
 }
@@ -306,8 +315,8 @@ CtP ev_bootstrap(const hs_keys *K, hs_bts *B, const hs_ct *in, double bound, cud
     const size_t N = P->n;
     const int L = P->L, conj = 2 * P->n - 1;
     if (in->ncomp != 2) throw HsError(HS_EINVAL, "bootstrap needs a degree-1 ciphertext");
-    const int e = bts_exponent(P, bound);
-    std::array<LinTrans, 3> *stc;
+    const int e = bts_exponent(P, B->arcsine, bound);
+    std::vector<std::unique_ptr<LinTrans>> *stc;
     {
         std::lock_guard<std::mutex> g(B->mu);
         ensure_cts(B);
@@ -324,7 +333,7 @@ CtP ev_bootstrap(const hs_keys *K, hs_bts *B, const hs_ct *in, double bound, cud
     x = ct_new(c, L, 2, st);
     k_modraise(c, low.p, x->d, L + 1, st);
     k_ntt(c, x->d, 2 * (L + 1), pmap_range(0, L + 1), false, st);
-    for (int k = 0; k < 3; k++) x = apply(K, x.get(), B->cts[k], st);
+    for (auto &T : B->cts) x = apply(K, x.get(), *T, st);
     CtP cj = ev_galois(K, x.get(), conj, st);
     x = ev_add(x.get(), cj.get(), false, st);
     x = ev_add_const(x.get(), -1.0 / (4.0 * (B->K + 2)), st);
@@ -334,47 +343,56 @@ CtP ev_bootstrap(const hs_keys *K, hs_bts *B, const hs_ct *in, double bound, cud
         m = ev_mult_int(m.get(), 2, st);
         x = ev_add_const(m.get(), -1.0, st);
     }
-    for (int k = 0; k < 3; k++) x = apply(K, x.get(), (*stc)[k], st);
+    if (B->arcsine) {  // s + (1/6) s^3
+        CtP s6 = ev_mult_const(x.get(), 1.0 / 6.0, x->level - 1, st);
+        CtP t = ev_mult(K, x.get(), x.get(), st);
+        CtP u = ev_mult(K, s6.get(), t.get(), st);
+        x = ev_add(x.get(), u.get(), false, st);
+    }
+    for (auto &T : *stc) x = apply(K, x.get(), *T, st);
     cj = ev_galois(K, x.get(), conj, st);
     c->ledger[HS_LG_BTS]++;
     return ev_add(x.get(), cj.get(), false, st);
 }
 
 // ------------------------------------------------------------------ C ABI
-static thread_local std::string g_bts_err;
-
 extern "C" {
 
 hs_status hs_bts_create(hs_ctx *c, const hs_bts_desc *d, hs_bts **out)
 {
     try {
         if (!c || !d || !out || !d->cos_poly || !d->cos_poly->coeffs || d->cos_poly->deg < 1 || d->r < 0 ||
-            d->K < 1)
+            d->K < 1 || d->n_cts < 1 || d->n_cts > 8 || d->n_stc < 1 || d->n_stc > 8)
             throw HsError(HS_EINVAL, "hs_bts_create: bad descriptor");
         const hs_params *P = c->P;
-        const int need = d->out_level + 6 + d->r + cheb_depth(d->cos_poly->deg);
+        const int need =
+            d->out_level + d->n_stc + (d->arcsine ? 2 : 0) + d->r + cheb_depth(d->cos_poly->deg) + d->n_cts;
         if (d->out_level < 0 || need != P->L)
-            throw HsError(HS_ELEVEL, "hs_bts_create: chain top must be out_level + 6 + r + depth(cos)");
+            throw HsError(HS_ELEVEL, "hs_bts_create: chain top must be out + n_stc + 2 arcsine + r + depth + n_cts");
         std::unique_ptr<hs_bts> B(new hs_bts);
         B->ctx = c;
         B->K = d->K;
         B->r = d->r;
         B->out_level = d->out_level;
+        B->n_cts = d->n_cts;
+        B->n_stc = d->n_stc;
+        B->arcsine = d->arcsine != 0;
         B->cos_coeffs.assign(d->cos_poly->coeffs, d->cos_poly->coeffs + d->cos_poly->deg + 1);
         B->cos_poly = hs_poly{d->cos_poly->deg, -1.0, 1.0, B->cos_coeffs.data()};
         *out = B.release();
         return HS_OK;
     } catch (const HsError &e) {
-        g_bts_err = e.what();
         return e.code;
     } catch (const std::exception &e) {
-        g_bts_err = e.what();
         return HS_EINVAL;
     }
 }
 
 void hs_bts_destroy(hs_bts *b) { delete b; }
-int hs_bts_rotations(const hs_params *p, int32_t *out, int max) { return bts_rotations(p, out, max); }
-int hs_bts_exponent(const hs_params *p, double bound) { return bts_exponent(p, bound); }
+int hs_bts_rotations(const hs_params *p, int n_cts, int n_stc, int32_t *out, int max)
+{
+    return bts_rotations(p, n_cts, n_stc, out, max);
+}
+int hs_bts_exponent(const hs_params *p, int arcsine, double bound) { return bts_exponent(p, arcsine, bound); }
 
 }  // extern "C"

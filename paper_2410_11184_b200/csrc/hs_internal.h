@@ -237,8 +237,8 @@ int cheb_depth(int deg);
 
 // bts.cpp
 CtP ev_bootstrap(const hs_keys *K, hs_bts *B, const hs_ct *in, double bound, cudaStream_t st);
-int bts_exponent(const hs_params *P, double bound);
-int bts_rotations(const hs_params *P, int32_t *out, int max);
+int bts_exponent(const hs_params *P, int arcsine, double bound);
+int bts_rotations(const hs_params *P, int n_cts, int n_stc, int32_t *out, int max);
 
 // softmax.cpp
 hs_status softmax_run(hs_ctx *c, const hs_keys *K, const hs_softmax_desc *d, const hs_ct *const *in,

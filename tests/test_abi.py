@@ -108,6 +108,11 @@ def test_bts_plan_conventions_match(name):
     import paper_2410_11184_b200 as hs
     pre = W.preset(name)
     P, PO = hs.Params.from_preset(pre), O.Params.from_preset(pre)
-    assert hs.bts_rotations(P) == O.bts_rotations(PO)
-    for b in [0.5, 1.0, 1.5, 2.0, 64.0, 261.0, 1e6]:
-        assert hs.bts_exponent(P, b) == O.bts_exponent(PO, b)
+    cfg = pre["bts"]
+    assert hs.bts_rotations(P, cfg) == O.bts_rotations(PO, cfg)
+    for n_cts, n_stc in [(3, 3), (4, 3), (5, 2)]:
+        c2 = dict(cfg, n_cts=n_cts, n_stc=n_stc)
+        assert hs.bts_rotations(P, c2) == O.bts_rotations(PO, c2)
+    for arc in [True, False]:
+        for b in [0.5, 1.0, 1.5, 2.0, 64.0, 261.0, 1e6]:
+            assert hs.bts_exponent(P, arc, b) == O.bts_exponent(PO, arc, b)

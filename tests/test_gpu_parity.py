@@ -222,7 +222,7 @@ def toyb():
     pre = W.preset("TOY12B")
     P = hs.Params.from_preset(pre)
     PO = O.Params.from_preset(pre)
-    rots = set(hs.bts_rotations(P))
+    rots = set(hs.bts_rotations(P, pre["bts"]))
     for n, m in [(256, 16), (256, 1)]:
         nb = n // m
         stride = (P.n // 2) // nb
@@ -234,9 +234,9 @@ def toyb():
     ctx = hs.Context(P, 0)
     K = hs.Keys(ctx, 31337, pre["h"], galois=gal)
     KO = O.Keys(PO, 31337, pre["h"], galois=gal)
-    tab = W.bts_tables()[pre["bts_table"]]
-    B = hs.Bts(ctx, tab, pre["bts_out_level"])
-    BO = O.Bts(PO, tab, pre["bts_out_level"])
+    tab = W.bts_tables()[pre["bts"]["table"]]
+    B = hs.Bts(ctx, pre["bts"], tab)
+    BO = O.Bts(PO, pre["bts"], tab)
     return dict(P=P, PO=PO, ctx=ctx, K=K, KO=KO, B=B, BO=BO, pre=pre)
 
 
@@ -252,9 +252,9 @@ def test_bootstrap_parity(toyb, level, bound):
     gb = hs.bootstrap(K, toyb["B"], g, bound)
     ob = O.bootstrap(PO, KO, o, toyb["BO"], bound)
     same(gb, ob)
-    assert gb.level == toyb["pre"]["bts_out_level"]
+    assert gb.level == toyb["pre"]["bts"]["out_level"]
     err = np.abs(hs.decrypt_decode(K, gb).real - z).max() / bound
-    assert err < 2.0 ** -18, np.log2(err)
+    assert err < 2.0 ** -21, np.log2(err)
 
 
 @pytest.mark.parametrize("table,m", [("p16_n256_M128_k5_B", 16), ("p16_n256_M128_k5_A", 1)])

@@ -26,6 +26,9 @@
 #include <stdlib.h>
 #include <string.h>
 
+void orc_encode_coeffs_q(const orc_params *P, const __float128 *re, const __float128 *im, double scale, int level,
+                         u64 *out);
+
 typedef __float128 f128;
 typedef struct { f128 re, im; } qz;
 
@@ -206,15 +209,15 @@ static void make_ltrans(const orc_params *P, const dmat *m, int level, int u, in
     #pragma omp parallel for schedule(dynamic)
     for (int k = 0; k < cnt; k++) {
         int G = (T->g[k] * T->b1 * u) % n0;
-        double *re = malloc(sizeof(double) * n0), *im = malloc(sizeof(double) * n0);
+        f128 *re = malloc(sizeof(f128) * n0), *im = malloc(sizeof(f128) * n0);
         const qz *v = m->diag[dl[k]];
         for (int p = 0; p < n0; p++) {           /* rot(diag, -G)_p = diag_{p - G} */
             qz x = v[((p - G) % n0 + n0) % n0];
-            re[p] = (double)x.re;
-            im[p] = (double)x.im;
+            re[p] = x.re;
+            im[p] = x.im;
         }
         u64 *pt = malloc(sizeof(u64) * (size_t)(level + 1) * N);
-        orc_encode_coeffs(P, re, im, sc, level, pt);
+        orc_encode_coeffs_q(P, re, im, sc, level, pt);
         for (int i = 0; i <= level; i++) orc_ntt_fwd(P, i, pt + (size_t)i * N);
         T->pt[k] = pt;
         free(re);
@@ -427,7 +430,7 @@ orc_bts_set *orc_bts_set_new(const orc_params *P, int K, int r, int n_cts, int n
                              const double *coeffs, int out_level)
 {
     if (n_cts < 1 || n_cts > ORC_MAXG || n_stc < 1 || n_stc > ORC_MAXG) return NULL;
-    if (out_level + n_stc + 2 * (arcsine != 0) + r + orc_cheb_depth(deg) + n_cts != P->L) return NULL;
+    if (out_level + n_stc + (arcsine ? 2 : 1) + r + orc_cheb_depth(deg) + n_cts != P->L) return NULL;
     orc_bts_set *S = calloc(1, sizeof(*S));
     S->P = P;
     S->cfg.K = K;
@@ -498,16 +501,25 @@ orc_ct *orc_bootstrap(const orc_params *P, const orc_keys *K, const orc_ct *in, 
         s = orc_op_add_const(P, m2, -1.0);
         orc_ct_release(m2);
     }
-    if (cf->arcsine) {   /* s <- s + (1/6) s^3  (arcsin(s) to O(s^5)) */
-        orc_ct *s6 = orc_op_mult_const(P, s, 1.0 / 6.0, s->level - 1);
+    /* gamma = Delta_out / Delta_in: the input message m was encoded at the scale
+     * of its own level, SlotToCoeff normalises by Delta_out (G11) */
+    double gamma = P->scale[cf->out_level] / P->scale[in->level];
+    if (cf->arcsine) {   /* s <- gamma (s + (1/6) s^3)  (arcsin(s) to O(s^5)) */
+        orc_ct *s6 = orc_op_mult_const(P, s, gamma / 6.0, s->level - 1);
         orc_ct *t = orc_op_mult(P, K, s, s);
         orc_ct *u = orc_op_mult(P, K, s6, t);
-        orc_ct *w = orc_op_add(P, s, u);
+        orc_ct *sg = orc_op_mult_const(P, s, gamma, u->level);
+        orc_ct *w = orc_op_add(P, sg, u);
         orc_ct_release(s6);
         orc_ct_release(t);
         orc_ct_release(u);
+        orc_ct_release(sg);
         orc_ct_release(s);
         s = w;
+    } else {             /* s <- gamma s (one level) */
+        orc_ct *sg = orc_op_mult_const(P, s, gamma, s->level - 1);
+        orc_ct_release(s);
+        s = sg;
     }
     STOP(12, s);
     for (int k = 0; k < cf->n_stc; k++) {

@@ -518,9 +518,15 @@ void orc_keyswitch(const orc_params *P, const orc_swk *key, int level, const u64
                 php[k] = v;
             }
             u64 *conv = malloc(sizeof(u64) * N);
+            /* centred terms (C7): y_k > (p_k - 1)/2 stands for y_k - p_k, i.e.
+             * the sum loses one P per such k, so the ModDown error is unbiased */
             for (int t = 0; t < N; t++) {
                 u64 s = 0;
-                for (int k = 0; k < np; k++) s = orc_add(s, orc_mul(z[(size_t)k * N + t] % q, php[k], q), q);
+                for (int k = 0; k < np; k++) {
+                    u64 y = z[(size_t)k * N + t], pk = P->prime[nq + k];
+                    s = orc_add(s, orc_mul(y % q, php[k], q), q);
+                    if (y > (pk - 1) / 2) s = orc_sub(s, P->p_mod_q[i], q);
+                }
                 conv[t] = s;
             }
             orc_ntt_fwd(P, i, conv);

@@ -61,6 +61,8 @@ static void fft(qc *a, int log_n2, int sign)
     }
 }
 
+static void encode_finish(const orc_params *P, qc *w, double scale, int level, u64 *out);
+
 /* out: (level+1) limbs of N residues, coefficient domain. */
 void orc_encode_coeffs(const orc_params *P, const double *re, const double *im, double scale, int level, u64 *out)
 {
@@ -73,6 +75,28 @@ void orc_encode_coeffs(const orc_params *P, const double *re, const double *im, 
         w[g].im = im ? im[j] : 0;
         g = (g * 5) % (u64)n2;
     }
+    encode_finish(P, w, scale, level, out);
+}
+
+/* the same from quad-precision slot values (bootstrapping diagonals, G11) */
+void orc_encode_coeffs_q(const orc_params *P, const __float128 *re, const __float128 *im, double scale, int level,
+                         u64 *out)
+{
+    int N = P->n, N0 = N / 2, n2 = 2 * N;
+    ensure_twiddles(P->log_n);
+    qc *w = calloc(n2, sizeof(qc));
+    u64 g = 1;
+    for (int j = 0; j < N0; j++) {
+        w[g].re = re[j];
+        w[g].im = im[j];
+        g = (g * 5) % (u64)n2;
+    }
+    encode_finish(P, w, scale, level, out);
+}
+
+static void encode_finish(const orc_params *P, qc *w, double scale, int level, u64 *out)
+{
+    int N = P->n;
     fft(w, P->log_n + 1, -1);
     __float128 f = (__float128)scale * 2 / (__float128)N;
     for (int t = 0; t < N; t++) {

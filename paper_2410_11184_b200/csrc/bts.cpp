@@ -165,14 +165,14 @@ void build_lintrans(hs_ctx *c, const DiagMat &m, int level, int unit, int r, Lin
 #pragma omp parallel for schedule(dynamic)
     for (int k = 0; k < nt; k++) {
         const int G = (T.g[k] * T.b1 * unit) % n0;
-        std::vector<double> re(n0), im(n0);
+        std::vector<f128> re(n0), im(n0);
         const std::vector<Qc> &v = m.D[ds[k]];
         for (int p = 0; p < n0; p++) {
             const Qc &x = v[((p - G) % n0 + n0) % n0];
-            re[p] = (double)x.re;
-            im[p] = (double)x.im;
+            re[p] = x.re;
+            im[p] = x.im;
         }
-        hs_encode_impl(P, re.data(), im.data(), sc, level, host.data() + (size_t)k * nl * N);
+        hs_encode_impl_q(P, re.data(), im.data(), sc, level, host.data() + (size_t)k * nl * N);
     }
     HS_CUDA(cudaMalloc(&T.pts, host.size() * 8));
     HS_CUDA(cudaMemcpy(T.pts, host.data(), host.size() * 8, cudaMemcpyHostToDevice));
@@ -343,11 +343,17 @@ CtP ev_bootstrap(const hs_keys *K, hs_bts *B, const hs_ct *in, double bound, cud
         m = ev_mult_int(m.get(), 2, st);
         x = ev_add_const(m.get(), -1.0, st);
     }
-    if (B->arcsine) {  // s + (1/6) s^3
-        CtP s6 = ev_mult_const(x.get(), 1.0 / 6.0, x->level - 1, st);
+    // gamma = Delta_out / Delta_in: the message was encoded at its own level's
+    // scale; SlotToCoeff normalises by Delta_out
+    const double gamma = P->scale[B->out_level] / P->scale[in->level];
+    if (B->arcsine) {  // gamma (s + (1/6) s^3)
+        CtP s6 = ev_mult_const(x.get(), gamma / 6.0, x->level - 1, st);
         CtP t = ev_mult(K, x.get(), x.get(), st);
         CtP u = ev_mult(K, s6.get(), t.get(), st);
-        x = ev_add(x.get(), u.get(), false, st);
+        CtP sg = ev_mult_const(x.get(), gamma, u->level, st);
+        x = ev_add(sg.get(), u.get(), false, st);
+    } else {  // gamma s
+        x = ev_mult_const(x.get(), gamma, x->level - 1, st);
     }
     for (auto &T : *stc) x = apply(K, x.get(), *T, st);
     cj = ev_galois(K, x.get(), conj, st);
@@ -366,7 +372,7 @@ hs_status hs_bts_create(hs_ctx *c, const hs_bts_desc *d, hs_bts **out)
             throw HsError(HS_EINVAL, "hs_bts_create: bad descriptor");
         const hs_params *P = c->P;
         const int need =
-            d->out_level + d->n_stc + (d->arcsine ? 2 : 0) + d->r + cheb_depth(d->cos_poly->deg) + d->n_cts;
+            d->out_level + d->n_stc + (d->arcsine ? 2 : 1) + d->r + cheb_depth(d->cos_poly->deg) + d->n_cts;
         if (d->out_level < 0 || need != P->L)
             throw HsError(HS_ELEVEL, "hs_bts_create: chain top must be out + n_stc + 2 arcsine + r + depth + n_cts");
         std::unique_ptr<hs_bts> B(new hs_bts);

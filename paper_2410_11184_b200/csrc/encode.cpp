@@ -68,15 +68,37 @@ void dft(std::vector<Cq> &a, int log_n2, int sign)
 
 }  // namespace
 
+static void encode_from(const hs_params *P, std::vector<Cq> &a, double scale, int level, u64 *out);
+
 void hs_encode_impl(const hs_params *P, const double *re, const double *im, double scale, int level, u64 *out)
 {
-    const int N = P->n, n0 = N / 2, n2 = 2 * N, lg = P->log_n + 1;
+    const int N = P->n, n0 = N / 2, n2 = 2 * N;
     std::vector<Cq> a(n2, Cq{0, 0});
     u64 g = 1;
     for (int j = 0; j < n0; j++) {
         a[g] = Cq{(f128)re[j], im ? (f128)im[j] : (f128)0};
         g = g * 5 % (u64)n2;
     }
+    encode_from(P, a, scale, level, out);
+}
+
+// quad-precision slot values (bootstrapping diagonals, G11)
+void hs_encode_impl_q(const hs_params *P, const __float128 *re, const __float128 *im, double scale, int level,
+                      u64 *out)
+{
+    const int N = P->n, n0 = N / 2, n2 = 2 * N;
+    std::vector<Cq> a(n2, Cq{0, 0});
+    u64 g = 1;
+    for (int j = 0; j < n0; j++) {
+        a[g] = Cq{re[j], im[j]};
+        g = g * 5 % (u64)n2;
+    }
+    encode_from(P, a, scale, level, out);
+}
+
+static void encode_from(const hs_params *P, std::vector<Cq> &a, double scale, int level, u64 *out)
+{
+    const int N = P->n, lg = P->log_n + 1;
     dft(a, lg, -1);
     const f128 f = (f128)scale * 2 / (f128)N;
     for (int t = 0; t < N; t++) {

@@ -134,7 +134,9 @@ const BconvTab &bconv_moddown(hs_ctx *c, int level)
     for (int i = 0; i <= level; i++) t.dst.push_back(i);
     t.n_src = (int)t.src.size();
     t.n_dst = (int)t.dst.size();
-    std::vector<u64> h(2 * t.n_src + 2 * (size_t)t.n_src * t.n_dst);
+    t.centred = true;
+    // [n_src](inv, inv_sh), [n_src][n_dst](c, c_sh), then [n_dst] P mod q (centred correction)
+    std::vector<u64> h(2 * t.n_src + 2 * (size_t)t.n_src * t.n_dst + t.n_dst);
     for (int a = 0; a < t.n_src; a++) {
         u64 pa = P->prime[t.src[a]], ph = 1;
         for (int b = 0; b < t.n_src; b++)
@@ -150,6 +152,7 @@ const BconvTab &bconv_moddown(hs_ctx *c, int level)
             h[ci + 1] = hs_shoup_const(v, q);
         }
     }
+    for (int d = 0; d < t.n_dst; d++) h[2 * t.n_src + 2 * (size_t)t.n_src * t.n_dst + d] = P->p_mod_q[t.dst[d]];
     HS_CUDA(cudaMalloc(&t.dev, h.size() * 8));
     HS_CUDA(cudaMemcpy(t.dev, h.data(), h.size() * 8, cudaMemcpyHostToDevice));
     return c->bconv[key] = t;

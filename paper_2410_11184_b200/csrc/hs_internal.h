@@ -79,6 +79,7 @@ struct DevTables {
 
 struct BconvTab {               // ModUp digit (level, digit) or ModDown (level)
     int n_src = 0, n_dst = 0;
+    bool centred = false;       // ModDown: centred source terms (unbiased, C7)
     std::vector<int> src, dst;  // global prime indices
     u64 *dev = nullptr;         // [n_src](inv, inv_sh) then [n_src][n_dst](c, c_sh)
 };
@@ -229,6 +230,8 @@ void ev_decrypt(const hs_keys *K, const hs_ct *ct, u64 *host_out, cudaStream_t s
 
 // encode.cpp
 void hs_encode_impl(const hs_params *P, const double *re, const double *im, double scale, int level, u64 *out);
+void hs_encode_impl_q(const hs_params *P, const __float128 *re, const __float128 *im, double scale, int level,
+                      u64 *out);
 void hs_decode_impl(const hs_params *P, const u64 *q0_coeffs, double scale, double *re, double *im);
 
 // poly.cpp

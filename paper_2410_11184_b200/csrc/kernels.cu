@@ -442,10 +442,12 @@ void k_rescale_final(hs_ctx *c, const u64 *a, const u64 *w, u64 *o, int ncomp, i
 // ------------------------------------------------------------------ basis conversion (C7)
 // y_a = x_a * inv_a mod src_a;  out_b = sum_a y_a * c_ab mod dst_b
 struct BconvArg {
-    int n_src, n_dst;
+    int n_src, n_dst, centred;
     unsigned char src[16], dst[HS_MAXP];
 };
 
+// centred (ModDown, C7): a term y_a > (q_a-1)/2 stands for y_a - q_a, so the
+// target loses one (prod of sources) per such term (table entry pm[b]).
 __global__ void bconv_kernel(const u64 *__restrict__ x, size_t xs, u64 *o, size_t os, BconvArg A,
                              const u64 *__restrict__ tab, int N, size_t bxs, size_t bos)
 {
@@ -454,11 +456,14 @@ __global__ void bconv_kernel(const u64 *__restrict__ x, size_t xs, u64 *o, size_
     x += blockIdx.y * bxs;
     o += blockIdx.y * bos;
     u64 y[16];
+    int neg = 0;
     for (int a = 0; a < A.n_src; a++) {
         const PrimeK k = c_pk[A.src[a]];
         y[a] = d_shoup(x[(size_t)a * xs + t], tab[2 * a], tab[2 * a + 1], k.q);
+        neg += y[a] > (k.q - 1) / 2;
     }
     const u64 *cm = tab + 2 * A.n_src;
+    const u64 *pm = cm + 2 * (size_t)A.n_src * A.n_dst;
     for (int b = 0; b < A.n_dst; b++) {
         const u64 p = c_pk[A.dst[b]].q;
         u64 s = 0;
@@ -466,6 +471,8 @@ __global__ void bconv_kernel(const u64 *__restrict__ x, size_t xs, u64 *o, size_
             size_t ci = 2 * ((size_t)a * A.n_dst + b);
             s = d_add(s, d_shoup(y[a], cm[ci], cm[ci + 1], p), p);
         }
+        if (A.centred)
+            for (int k = 0; k < neg; k++) s = d_sub(s, pm[b], p);
         o[(size_t)b * os + t] = s;
     }
 }
@@ -477,6 +484,7 @@ void k_bconv(hs_ctx *c, const BconvTab &tab, const u64 *src, size_t src_stride, 
     BconvArg A;
     A.n_src = tab.n_src;
     A.n_dst = tab.n_dst;
+    A.centred = tab.centred ? 1 : 0;
     for (int i = 0; i < tab.n_src; i++) A.src[i] = (unsigned char)tab.src[i];
     for (int i = 0; i < tab.n_dst; i++) A.dst[i] = (unsigned char)tab.dst[i];
     int N = c->P->n;

@@ -3,9 +3,13 @@
 // Every operation follows the oracle's written conventions:
 //   C5 randomness, C6 Enc/Dec, C7 hybrid key switching, C8 HMult,
 //   C9 rescale, C10 rotations, C11 operand levels, C12 canonical scales.
-// Ciphertexts live in HBM limb-major [comp][limb][N], NTT domain; all
-// temporaries are stream-ordered (cudaMallocAsync) so an op enqueues work and
-// returns without synchronising.
+// Ciphertexts live in HBM limb-major [batch][comp][limb][N], NTT domain.  A
+// batch holds several ciphertexts at one level (the Softmax main thread keeps
+// its m/world ciphertexts as one batch): every op then runs as one launch per
+// kernel over the whole batch, and the key switch reads each evaluation-key
+// limb once per batch tile.  A batch-1 operand broadcasts against a batch.
+// All temporaries are stream-ordered (cudaMallocAsync), so an op enqueues
+// work and returns without synchronising.
 #include <math.h>
 
 #include <cstring>
@@ -37,6 +41,7 @@ hs_ctx::~hs_ctx()
     cudaDeviceSynchronize();
     for (auto &kv : bconv) cudaFree(kv.second.dev);
     for (auto &kv : galois_perm) cudaFree(kv.second);
+    for (auto e : kprof_ev) cudaEventDestroy(e);
     cudaFree(T.tw);
 }
 
@@ -53,35 +58,57 @@ hs_ct::~hs_ct()
     if (d) dev_free(d, st);
 }
 
+size_t hs_ct::ct_words() const { return (size_t)ncomp * (level + 1) * ctx->P->n; }
 u64 *hs_ct::limb(int comp, int i) const { return d + ((size_t)comp * (level + 1) + i) * ctx->P->n; }
+u64 *hs_ct::at(int b, int comp, int i) const { return d + (((size_t)b * ncomp + comp) * (level + 1) + i) * ctx->P->n; }
 
-CtP ct_new(hs_ctx *c, int level, int ncomp, cudaStream_t st)
+CtP ct_new(hs_ctx *c, int level, int ncomp, cudaStream_t st, int batch)
 {
     CtP r(new hs_ct);
     r->ctx = c;
     r->level = level;
     r->ncomp = ncomp;
+    r->batch = batch;
     r->st = st;
-    r->d = dev_alloc((size_t)ncomp * (level + 1) * c->P->n, st);
+    r->d = dev_alloc((size_t)batch * ncomp * (level + 1) * c->P->n, st);
     return r;
 }
 
 CtP ct_copy(const hs_ct *a, cudaStream_t st)
 {
-    CtP r = ct_new(a->ctx, a->level, a->ncomp, st);
+    CtP r = ct_new(a->ctx, a->level, a->ncomp, st, a->batch);
     HS_CUDA(cudaMemcpyAsync(r->d, a->d, a->limbs() * a->ctx->P->n * 8, cudaMemcpyDeviceToDevice, st));
     return r;
 }
 
-// keep limbs 0..level of every component
+// keep limbs 0..level of every row
 CtP ct_drop(const hs_ct *a, int level, cudaStream_t st)
 {
     if (level == a->level) return ct_copy(a, st);
     hs_ctx *c = a->ctx;
-    CtP r = ct_new(c, level, a->ncomp, st);
+    CtP r = ct_new(c, level, a->ncomp, st, a->batch);
     size_t N = c->P->n;
-    HS_CUDA(cudaMemcpy2DAsync(r->d, (level + 1) * N * 8, a->d, (a->level + 1) * N * 8, (level + 1) * N * 8, a->ncomp,
+    HS_CUDA(cudaMemcpy2DAsync(r->d, (level + 1) * N * 8, a->d, (a->level + 1) * N * 8, (level + 1) * N * 8, a->rows(),
                               cudaMemcpyDeviceToDevice, st));
+    return r;
+}
+
+CtP ct_gather(const hs_ct *const *cts, int n, cudaStream_t st)
+{
+    const hs_ct *a = cts[0];
+    CtP r = ct_new(a->ctx, a->level, a->ncomp, st, n);
+    for (int b = 0; b < n; b++) {
+        if (cts[b]->level != a->level || cts[b]->ncomp != a->ncomp || cts[b]->batch != 1)
+            throw HsError(HS_EINVAL, "gather: ciphertexts differ in level or shape");
+        HS_CUDA(cudaMemcpyAsync(r->d + b * a->ct_words(), cts[b]->d, a->ct_words() * 8, cudaMemcpyDeviceToDevice, st));
+    }
+    return r;
+}
+
+CtP ct_slice(const hs_ct *a, int b, cudaStream_t st)
+{
+    CtP r = ct_new(a->ctx, a->level, a->ncomp, st, 1);
+    HS_CUDA(cudaMemcpyAsync(r->d, a->d + b * a->ct_words(), a->ct_words() * 8, cudaMemcpyDeviceToDevice, st));
     return r;
 }
 
@@ -184,43 +211,73 @@ const unsigned *galois_table(hs_ctx *c, int k)
 }
 
 // ------------------------------------------------------------------ key switching (C7)
-void ev_keyswitch(const hs_keys *K, const SwKey *key, int level, const u64 *d, u64 *out0, u64 *out1,
-                  const u64 *add0, const u64 *add1, cudaStream_t st)
+// B polynomials d_b = d + b*d_stride (level+1 limbs each, NTT domain);
+// out_b = out + b*out_stride gets (ks0, ks1) (+ add_b's first add_comps components).
+void ev_keyswitch_b(const hs_keys *K, const SwKey *key, int level, int B, const u64 *d, size_t d_stride, u64 *out,
+                    size_t out_stride, const u64 *add, size_t add_stride, int add_comps, cudaStream_t st)
 {
     hs_ctx *c = K->ctx;
     const hs_params *P = c->P;
     const size_t N = P->n;
     const int nl = level + 1, alpha = P->alpha, np = P->n_p, ntg = nl + np;
     const int beta = (nl + alpha - 1) / alpha;
-    // coefficient form of d
-    DBuf x(nl * N, st);
-    HS_CUDA(cudaMemcpyAsync(x.p, d, nl * N * 8, cudaMemcpyDeviceToDevice, st));
-    k_ntt(c, x.p, nl, pmap_range(0, nl), true, st);
-    // ModUp every digit: ext[j][g'] (coefficient form -> NTT)
-    DBuf ext((size_t)beta * ntg * N, st);
+    // coefficient form of every d_b: [B][nl][N]
+    DBuf x((size_t)B * nl * N, st);
+    HS_CUDA(cudaMemcpy2DAsync(x.p, nl * N * 8, d, d_stride * 8, nl * N * 8, B, cudaMemcpyDeviceToDevice, st));
+    k_ntt(c, x.p, B * nl, pmap_range(0, nl), true, st);
+    // ModUp every digit for the whole batch: digit j block [B][nd_j][N]
+    size_t off[16];
+    int nd[16];
+    size_t tot = 0;
     for (int j = 0; j < beta; j++) {
         const BconvTab &tab = bconv_modup(c, level, j);
-        u64 *e = ext.p + (size_t)j * ntg * N;
-        k_bconv(c, tab, x.p + (size_t)tab.src[0] * N, N, e, N, 1, 0, 0, st);
+        off[j] = tot;
+        nd[j] = tab.n_dst;
+        tot += (size_t)B * tab.n_dst * N;
+    }
+    DBuf ext(tot, st);
+    for (int j = 0; j < beta; j++) {
+        const BconvTab &tab = bconv_modup(c, level, j);
+        u64 *e = ext.p + off[j];
+        k_bconv(c, tab, x.p + (size_t)tab.src[0] * N, N, e, N, B, (size_t)nl * N, (size_t)tab.n_dst * N, st);
         PrimeMap pm;
         pm.n = tab.n_dst;
         for (int i = 0; i < tab.n_dst; i++) pm.p[i] = (unsigned char)tab.dst[i];
-        k_ntt(c, e, tab.n_dst, pm, false, st);
+        k_ntt(c, e, B * tab.n_dst, pm, false, st);
     }
-    // inner product with the evaluation key: acc[2][ntg][N]
-    DBuf acc((size_t)2 * ntg * N, st);
-    k_ks_inner(c, d, ext.p, key->k, acc.p, level, beta, st);
-    // ModDown: iNTT of the P limbs, BConv P -> Q_l, NTT, (acc - conv) P^{-1}
-    DBuf z((size_t)2 * np * N, st);
-    HS_CUDA(cudaMemcpy2DAsync(z.p, np * N * 8, acc.p + (size_t)nl * N, ntg * N * 8, np * N * 8, 2,
+    // inner product with the evaluation key: acc[B][2][ntg][N]
+    DBuf acc((size_t)B * 2 * ntg * N, st);
+    k_ks_inner_b(c, d, d_stride, ext.p, off, nd, key->k, acc.p, level, beta, B, st);
+    // ModDown: iNTT of the P limbs, centred BConv P -> Q_l, NTT, (acc - conv) P^{-1}
+    DBuf z((size_t)B * 2 * np * N, st);
+    HS_CUDA(cudaMemcpy2DAsync(z.p, np * N * 8, acc.p + (size_t)nl * N, ntg * N * 8, np * N * 8, 2 * B,
                               cudaMemcpyDeviceToDevice, st));
-    k_ntt(c, z.p, 2 * np, pmap_range(P->n_q, np), true, st);
+    k_ntt(c, z.p, 2 * B * np, pmap_range(P->n_q, np), true, st);
     const BconvTab &md = bconv_moddown(c, level);
-    DBuf conv((size_t)2 * nl * N, st);
-    k_bconv(c, md, z.p, N, conv.p, N, 2, np * N, nl * N, st);
-    k_ntt(c, conv.p, 2 * nl, pmap_range(0, nl), false, st);
-    k_moddown_final(c, acc.p, conv.p, out0, out1, add0, add1, level, st);
-    c->ledger[HS_LG_KS]++;
+    DBuf conv((size_t)B * 2 * nl * N, st);
+    k_bconv(c, md, z.p, N, conv.p, N, 2 * B, (size_t)np * N, (size_t)nl * N, st);
+    k_ntt(c, conv.p, 2 * B * nl, pmap_range(0, nl), false, st);
+    k_moddown_final_b(c, acc.p, conv.p, out, out_stride, add, add_stride, add_comps, level, B, st);
+    c->ledger[HS_LG_KS] += B;
+}
+
+void ev_keyswitch(const hs_keys *K, const SwKey *key, int level, const u64 *d, u64 *out0, u64 *out1,
+                  const u64 *add0, const u64 *add1, cudaStream_t st)
+{
+    // (out0, out1) and (add0, add1) as separate pointers: the hooks' layout
+    const size_t N = K->ctx->P->n, nl = level + 1;
+    DBuf o(2 * nl * N, st), a(add0 || add1 ? 2 * nl * N : 0, st);
+    int add_comps = 0;
+    if (add0 || add1) {
+        HS_CUDA(cudaMemsetAsync(a.p, 0, 2 * nl * N * 8, st));
+        if (add0) HS_CUDA(cudaMemcpyAsync(a.p, add0, nl * N * 8, cudaMemcpyDeviceToDevice, st));
+        if (add1) HS_CUDA(cudaMemcpyAsync(a.p + nl * N, add1, nl * N * 8, cudaMemcpyDeviceToDevice, st));
+        add_comps = 2;
+    }
+    ev_keyswitch_b(K, key, level, 1, d, nl * N, o.p, 2 * nl * N, add_comps ? a.p : nullptr, 2 * nl * N, add_comps,
+                   st);
+    HS_CUDA(cudaMemcpyAsync(out0, o.p, nl * N * 8, cudaMemcpyDeviceToDevice, st));
+    HS_CUDA(cudaMemcpyAsync(out1, o.p + nl * N, nl * N * 8, cudaMemcpyDeviceToDevice, st));
 }
 
 // ------------------------------------------------------------------ arithmetic
@@ -228,20 +285,21 @@ CtP ev_rescale(const hs_ct *a, cudaStream_t st)
 {
     hs_ctx *c = a->ctx;
     const size_t N = c->P->n;
-    const int l = a->level, nc = a->ncomp;
+    const int l = a->level, rows = (int)a->rows();
     if (l < 1) throw HsError(HS_ELEVEL, "rescale at level 0");
-    DBuf last((size_t)nc * N, st);
-    HS_CUDA(cudaMemcpy2DAsync(last.p, N * 8, a->limb(0, l), (l + 1) * N * 8, N * 8, nc, cudaMemcpyDeviceToDevice, st));
+    DBuf last((size_t)rows * N, st);
+    HS_CUDA(cudaMemcpy2DAsync(last.p, N * 8, a->d + (size_t)l * N, (l + 1) * N * 8, N * 8, rows,
+                              cudaMemcpyDeviceToDevice, st));
     PrimeMap pm;
     pm.n = 1;
     pm.p[0] = (unsigned char)l;
-    k_ntt(c, last.p, nc, pm, true, st);
-    DBuf w((size_t)nc * l * N, st);
-    k_rescale_prep(c, last.p, w.p, nc, l, st);
-    k_ntt(c, w.p, nc * l, pmap_range(0, l), false, st);
-    CtP r = ct_new(c, l - 1, nc, st);
-    k_rescale_final(c, a->d, w.p, r->d, nc, l, st);
-    c->ledger[HS_LG_RESCALE]++;
+    k_ntt(c, last.p, rows, pm, true, st);
+    DBuf w((size_t)rows * l * N, st);
+    k_rescale_prep(c, last.p, w.p, rows, l, st);
+    k_ntt(c, w.p, rows * l, pmap_range(0, l), false, st);
+    CtP r = ct_new(c, l - 1, a->ncomp, st, a->batch);
+    k_rescale_final(c, a->d, w.p, r->d, rows, l, st);
+    c->ledger[HS_LG_RESCALE] += a->batch;
     return r;
 }
 
@@ -261,11 +319,12 @@ CtP ev_mult_const(const hs_ct *a, double v, int target, cudaStream_t st)
     hs_ctx *c = a->ctx;
     const hs_params *P = c->P;
     if (target < 0 || target >= a->level) throw HsError(HS_ELEVEL, "mult_const: target level must be below the input");
-    CtP d = ct_drop(a, target + 1, st);
+    const int nl = target + 2;
+    CtP d = ct_new(c, target + 1, a->ncomp, st, a->batch);
     u64 s[HS_MAXP];
-    residues(P, v * landing_scale(P, a->level, target), target + 2, s);
-    k_mul_scalar(c, d->d, d->d, s, (int)d->limbs(), target + 2, st);
-    c->ledger[HS_LG_CMULT]++;
+    residues(P, v * landing_scale(P, a->level, target), nl, s);
+    k_mul_scalar_s(c, a->d, d->d, s, (int)a->rows(), nl, a->level + 1, nl, false, st);  // drop + scale
+    c->ledger[HS_LG_CMULT] += a->batch;
     return ev_rescale(d.get(), st);
 }
 
@@ -273,7 +332,7 @@ CtP ev_level_down(const hs_ct *a, int target, cudaStream_t st)
 {
     if (target == a->level) return ct_copy(a, st);
     if (target > a->level) throw HsError(HS_ELEVEL, "level_down to a higher level");
-    a->ctx->ledger[HS_LG_LEVELDOWN]++;
+    a->ctx->ledger[HS_LG_LEVELDOWN] += a->batch;
     return ev_mult_const(a, 1.0, target, st);
 }
 
@@ -291,14 +350,22 @@ static void match(const hs_ct *a, const hs_ct *b, CtP &ta, CtP &tb, const hs_ct 
     }
 }
 
+static int out_batch(const hs_ct *a, const hs_ct *b)
+{
+    if (a->batch != b->batch && a->batch != 1 && b->batch != 1)
+        throw HsError(HS_EINVAL, "operand batches must match or one must be 1");
+    return std::max(a->batch, b->batch);
+}
+
 CtP ev_add(const hs_ct *a, const hs_ct *b, bool sub, cudaStream_t st)
 {
     if (a->ncomp != b->ncomp) throw HsError(HS_EINVAL, "add: component counts differ");
+    const int B = out_batch(a, b);
     CtP ta, tb;
     const hs_ct *ra, *rb;
     match(a, b, ta, tb, ra, rb, st);
-    CtP r = ct_new(a->ctx, ra->level, ra->ncomp, st);
-    k_add(a->ctx, ra->d, rb->d, r->d, (int)r->limbs(), ra->level + 1, sub, st);
+    CtP r = ct_new(a->ctx, ra->level, ra->ncomp, st, B);
+    k_add_b(a->ctx, ra->d, (int)ra->rows(), rb->d, (int)rb->rows(), r->d, (int)r->rows(), ra->level + 1, sub, st);
     return r;
 }
 
@@ -310,7 +377,7 @@ CtP ev_mult_int(const hs_ct *a, int64_t v, cudaStream_t st)
         int64_t m = v % (int64_t)P->prime[i];
         s[i] = (u64)(m < 0 ? m + (int64_t)P->prime[i] : m);
     }
-    CtP r = ct_new(a->ctx, a->level, a->ncomp, st);
+    CtP r = ct_new(a->ctx, a->level, a->ncomp, st, a->batch);
     k_mul_scalar(a->ctx, a->d, r->d, s, (int)a->limbs(), a->level + 1, st);
     return r;
 }
@@ -321,7 +388,7 @@ CtP ev_add_const(const hs_ct *a, double v, cudaStream_t st)
     u64 s[HS_MAXP];
     residues(P, v * P->scale[a->level], a->level + 1, s);
     CtP r = ct_copy(a, st);
-    k_add_scalar(a->ctx, r->d, s, a->level + 1, st);
+    k_add_scalar_b(a->ctx, r->d, s, a->batch, a->ncomp, a->level + 1, st);
     return r;
 }
 
@@ -340,19 +407,30 @@ CtP ev_mult_pt(const hs_ct *a, const double *re, const double *im, int target, c
     CtP d = ct_drop(a, target + 1, st);
     k_mul_pointwise(c, d->d, m.p, d->d, (int)d->limbs(), nl, nl, st);
     HS_CUDA(cudaStreamSynchronize(st));  // pt host buffer lifetime
-    c->ledger[HS_LG_PMULT]++;
+    c->ledger[HS_LG_PMULT] += a->batch;
     return ev_rescale(d.get(), st);
 }
 
 CtP ev_tensor(const hs_ct *a, const hs_ct *b, cudaStream_t st)
 {
     if (a->ncomp != 2 || b->ncomp != 2) throw HsError(HS_EINVAL, "tensor needs degree-1 ciphertexts");
+    const int B = out_batch(a, b);
     CtP ta, tb;
     const hs_ct *ra, *rb;
     match(a, b, ta, tb, ra, rb, st);
-    CtP r = ct_new(a->ctx, ra->level, 3, st);
-    k_tensor(a->ctx, ra->d, rb->d, r->d, ra->level + 1, st);
-    a->ctx->ledger[HS_LG_TENSOR]++;
+    if (ra->batch < rb->batch) std::swap(ra, rb);  // the tensor is symmetric: broadcast the second operand
+    CtP r = ct_new(a->ctx, ra->level, 3, st, B);
+    k_tensor_b(a->ctx, ra->d, rb->d, r->d, B, ra->level + 1, rb->batch, st);
+    a->ctx->ledger[HS_LG_TENSOR] += B;
+    return r;
+}
+
+CtP ev_tensor_sum(const hs_ct *a, cudaStream_t st)
+{
+    if (a->ncomp != 2) throw HsError(HS_EINVAL, "tensor_sum needs degree-1 ciphertexts");
+    CtP r = ct_new(a->ctx, a->level, 3, st, 1);
+    k_tensor_sum(a->ctx, a->d, r->d, a->batch, a->level + 1, st);
+    a->ctx->ledger[HS_LG_TENSOR] += a->batch;
     return r;
 }
 
@@ -361,8 +439,9 @@ CtP ev_relin(const hs_keys *K, const hs_ct *d, cudaStream_t st)
     const SwKey *rk = K->find(0);
     if (!rk) throw HsError(HS_EKEY, "relinearisation key missing");
     if (d->ncomp != 3) throw HsError(HS_EINVAL, "relin needs a degree-2 ciphertext");
-    CtP r = ct_new(d->ctx, d->level, 2, st);
-    ev_keyswitch(K, rk, d->level, d->limb(2, 0), r->limb(0, 0), r->limb(1, 0), d->limb(0, 0), d->limb(1, 0), st);
+    CtP r = ct_new(d->ctx, d->level, 2, st, d->batch);
+    const size_t w3 = d->ct_words();
+    ev_keyswitch_b(K, rk, d->level, d->batch, d->limb(2, 0), w3, r->d, r->ct_words(), d->d, w3, 2, st);
     return r;
 }
 
@@ -370,7 +449,7 @@ CtP ev_mult(const hs_keys *K, const hs_ct *a, const hs_ct *b, cudaStream_t st)
 {
     CtP t = ev_tensor(a, b, st);
     CtP r = ev_relin(K, t.get(), st);
-    K->ctx->ledger[HS_LG_HMULT]++;
+    K->ctx->ledger[HS_LG_HMULT] += t->batch;
     return ev_rescale(r.get(), st);
 }
 
@@ -380,11 +459,12 @@ CtP ev_galois(const hs_keys *K, const hs_ct *a, int k, cudaStream_t st)
     if (!key) throw HsError(HS_EKEY, "switching key for Galois element " + std::to_string(k) + " missing");
     if (a->ncomp != 2) throw HsError(HS_EINVAL, "rotation needs a degree-1 ciphertext");
     hs_ctx *c = a->ctx;
-    CtP s = ct_new(c, a->level, 2, st);
+    CtP s = ct_new(c, a->level, 2, st, a->batch);
     k_permute(c, a->d, s->d, galois_table(c, k), (int)a->limbs(), st);
-    CtP r = ct_new(c, a->level, 2, st);
-    ev_keyswitch(K, key, a->level, s->limb(1, 0), r->limb(0, 0), r->limb(1, 0), s->limb(0, 0), nullptr, st);
-    c->ledger[HS_LG_ROT]++;
+    CtP r = ct_new(c, a->level, 2, st, a->batch);
+    const size_t w = a->ct_words();
+    ev_keyswitch_b(K, key, a->level, a->batch, s->limb(1, 0), w, r->d, w, s->d, w, 1, st);
+    c->ledger[HS_LG_ROT] += a->batch;
     return r;
 }
 
@@ -402,17 +482,19 @@ CtP ev_mult_const_sum(const std::vector<const hs_ct *> &terms, const std::vector
     const hs_params *P = c->P;
     const size_t N = P->n;
     const int nl = target + 2;
-    CtP acc = ct_new(c, target + 1, 2, st);
+    int B = 1;
+    for (auto t : terms) B = std::max(B, t->batch);
+    CtP acc = ct_new(c, target + 1, 2, st, B);
     HS_CUDA(cudaMemsetAsync(acc->d, 0, acc->limbs() * N * 8, st));
     for (size_t i = 0; i < terms.size(); i++) {
         if (coef[i] == 0.0) continue;
         const hs_ct *t = terms[i];
         if (t->level < target + 1) throw HsError(HS_ELEVEL, "leaf term below its landing level");
+        if (t->batch != B) throw HsError(HS_EINVAL, "leaf terms must share the batch");
         u64 s[HS_MAXP];
         residues(P, coef[i] * landing_scale(P, t->level, target), nl, s);
-        for (int comp = 0; comp < 2; comp++)
-            k_mac_scalar(c, acc->limb(comp, 0), t->limb(comp, 0), s, nl, nl, st);
-        c->ledger[HS_LG_CMULT]++;
+        k_mul_scalar_s(c, t->d, acc->d, s, (int)t->rows(), nl, t->level + 1, nl, true, st);
+        c->ledger[HS_LG_CMULT] += B;
     }
     return ev_rescale(acc.get(), st);
 }
@@ -536,6 +618,7 @@ void ev_decrypt(const hs_keys *K, const hs_ct *ct, u64 *host_out, cudaStream_t s
     hs_ctx *c = K->ctx;
     const size_t N = c->P->n;
     const int nl = ct->level + 1;
+    if (ct->batch != 1) throw HsError(HS_EINVAL, "decrypt one ciphertext at a time");
     DBuf m((size_t)nl * N, st);
     k_mul_pointwise(c, ct->limb(1, 0), K->s_ntt, m.p, nl, nl, nl, st);
     k_add(c, m.p, ct->limb(0, 0), m.p, nl, nl, false, st);

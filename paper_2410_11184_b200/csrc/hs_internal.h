@@ -119,14 +119,20 @@ struct hs_keys {
     }
 };
 
+// One ciphertext, or a batch of `batch` ciphertexts at the same level sharing
+// one allocation [batch][ncomp][level+1][N] (the main thread of the
+// many-ciphertext Softmax runs its 64 ciphertexts as one batch).
 struct hs_ct {
     hs_ctx *ctx = nullptr;
-    int level = 0, ncomp = 0;
-    u64 *d = nullptr;           // [ncomp][level+1][N]
+    int level = 0, ncomp = 0, batch = 1;
+    u64 *d = nullptr;           // [batch][ncomp][level+1][N]
     cudaStream_t st = nullptr;  // stream the buffer is ordered on
     ~hs_ct();
-    size_t limbs() const { return (size_t)ncomp * (level + 1); }
+    size_t rows() const { return (size_t)batch * ncomp; }
+    size_t limbs() const { return rows() * (level + 1); }
+    size_t ct_words() const;    // words of one ciphertext of the batch
     u64 *limb(int comp, int i) const;
+    u64 *at(int b, int comp, int i) const;
 };
 
 // ------------------------------------------------------------------ memory
@@ -185,6 +191,18 @@ void k_moddown_final(hs_ctx *c, const u64 *acc, const u64 *conv, u64 *o0, u64 *o
                      const u64 *add1, int level, cudaStream_t st);
 void upload_prime_constants(const hs_params *P);
 void k_mac_pt(hs_ctx *c, u64 *acc, const u64 *a, const u64 *pt, int nl, int la, cudaStream_t st);
+// batched ciphertext kernels ([B][ncomp][nl][N]; "rows" = B * ncomp)
+void k_add_b(hs_ctx *c, const u64 *a, int a_rows, const u64 *b, int b_rows, u64 *o, int rows, int nl, bool sub,
+             cudaStream_t st);
+void k_mul_scalar_s(hs_ctx *c, const u64 *a, u64 *o, const u64 *host_scal, int rows, int nl, int a_rl, int o_rl,
+                    bool accumulate, cudaStream_t st);
+void k_add_scalar_b(hs_ctx *c, u64 *a, const u64 *host_scal, int B, int ncomp, int nl, cudaStream_t st);
+void k_tensor_b(hs_ctx *c, const u64 *a, const u64 *b, u64 *o, int B, int nl, int b_batch, cudaStream_t st);
+void k_tensor_sum(hs_ctx *c, const u64 *a, u64 *o, int B, int nl, cudaStream_t st);
+void k_ks_inner_b(hs_ctx *c, const u64 *d, size_t d_stride, const u64 *ext, const size_t *off, const int *nd,
+                  const u64 *key, u64 *acc, int level, int beta, int B, cudaStream_t st);
+void k_moddown_final_b(hs_ctx *c, const u64 *acc, const u64 *conv, u64 *o, size_t o_stride, const u64 *add,
+                       size_t add_stride, int add_comps, int level, int B, cudaStream_t st);
 void k_modraise(hs_ctx *c, const u64 *x, u64 *o, int nl, cudaStream_t st);
 void k_signed_to_rns(hs_ctx *c, const int64_t *v, u64 *o, int n_limbs, const PrimeMap &pm, cudaStream_t st);
 void k_uniform(hs_ctx *c, u64 *o, int n_limbs, const PrimeMap &pm, u64 seed, uint32_t tag, u64 sub,
@@ -202,9 +220,14 @@ u64 hs_stream_word(u64 seed, uint32_t tag, u64 sub, u64 idx);
 
 // ------------------------------------------------------------------ evaluator (eval.cu)
 typedef std::unique_ptr<hs_ct> CtP;
-CtP ct_new(hs_ctx *c, int level, int ncomp, cudaStream_t st);
+CtP ct_new(hs_ctx *c, int level, int ncomp, cudaStream_t st, int batch = 1);
 CtP ct_copy(const hs_ct *a, cudaStream_t st);
 CtP ct_drop(const hs_ct *a, int level, cudaStream_t st);
+CtP ct_gather(const hs_ct *const *cts, int n, cudaStream_t st);        // n single cts -> one batch
+CtP ct_slice(const hs_ct *a, int b, cudaStream_t st);                  // ciphertext b of a batch
+CtP ev_tensor_sum(const hs_ct *a, cudaStream_t st);                    // sum_b tensor(a_b, a_b)
+void ev_keyswitch_b(const hs_keys *K, const SwKey *key, int level, int B, const u64 *d, size_t d_stride, u64 *out,
+                    size_t out_stride, const u64 *add, size_t add_stride, int add_comps, cudaStream_t st);
 CtP ev_add(const hs_ct *a, const hs_ct *b, bool sub, cudaStream_t st);
 CtP ev_level_down(const hs_ct *a, int target, cudaStream_t st);
 CtP ev_rescale(const hs_ct *a, cudaStream_t st);

@@ -178,11 +178,249 @@ __global__ void __launch_bounds__(256) ntt_rows_kernel(u64 *data, PrimeMap pm, c
     for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) a[idx] = sm[idx];
 }
 
+// ------------------------------------------------------------------ fast NTT for N = 2^16
+// Two kernels of 8 stages each (index j = r*256 + e).  Inside a kernel every
+// thread keeps 8 words in registers and runs 3 butterfly stages on them
+// (radix 8), exchanging through shared memory between rounds 8 / 8 / 4
+// stages-per-round = 3 + 3 + 2.  Stage with half-span t on element j uses the
+// twiddle tw[N/(2t) + j/(2t)] (Cooley-Tukey forward, Gentleman-Sande inverse).
+namespace ntt16 {
+constexpr int LOGN = 16, N = 1 << LOGN;
+
+struct Tw {
+    const u64 *__restrict__ w;   // twiddles
+    const u64 *__restrict__ ws;  // Shoup companions
+    u64 q;
+};
+
+__device__ __forceinline__ void bfly_ct(u64 &a, u64 &b, const Tw &T, int idx)
+{
+    u64 V = d_shoup(b, __ldg(T.w + idx), __ldg(T.ws + idx), T.q);
+    b = d_sub(a, V, T.q);
+    a = d_add(a, V, T.q);
+}
+__device__ __forceinline__ void bfly_gs(u64 &a, u64 &b, const Tw &T, int idx)
+{
+    u64 U = a, V = b;
+    a = d_add(U, V, T.q);
+    b = d_shoup(d_sub(U, V, T.q), __ldg(T.w + idx), __ldg(T.ws + idx), T.q);
+}
+
+// x[k] = element j0 + k s (j0 = block start + offset, block start multiple of 8s)
+__device__ __forceinline__ void radix8_fwd(u64 x[8], int j0, int s, const Tw &T)
+{
+    int m = N / (8 * s), g = j0 / (8 * s);
+    for (int k = 0; k < 4; k++) bfly_ct(x[k], x[k + 4], T, m + g);
+    m <<= 1;
+    g <<= 1;
+    bfly_ct(x[0], x[2], T, m + g);
+    bfly_ct(x[1], x[3], T, m + g);
+    bfly_ct(x[4], x[6], T, m + g + 1);
+    bfly_ct(x[5], x[7], T, m + g + 1);
+    m <<= 1;
+    g <<= 1;
+    for (int k = 0; k < 4; k++) bfly_ct(x[2 * k], x[2 * k + 1], T, m + g + k);
+}
+__device__ __forceinline__ void radix8_inv(u64 x[8], int j0, int s, const Tw &T)
+{
+    int m = N / (2 * s), g = j0 / (2 * s);
+    for (int k = 0; k < 4; k++) bfly_gs(x[2 * k], x[2 * k + 1], T, m + g + k);
+    m >>= 1;
+    g >>= 1;
+    bfly_gs(x[0], x[2], T, m + g);
+    bfly_gs(x[1], x[3], T, m + g);
+    bfly_gs(x[4], x[6], T, m + g + 1);
+    bfly_gs(x[5], x[7], T, m + g + 1);
+    m >>= 1;
+    g >>= 1;
+    for (int k = 0; k < 4; k++) bfly_gs(x[k], x[k + 4], T, m + g);
+}
+// x[k] = element j0 + k s, block start multiple of 4s
+__device__ __forceinline__ void radix4_fwd(u64 x[4], int j0, int s, const Tw &T)
+{
+    int m = N / (4 * s), g = j0 / (4 * s);
+    bfly_ct(x[0], x[2], T, m + g);
+    bfly_ct(x[1], x[3], T, m + g);
+    m <<= 1;
+    g <<= 1;
+    bfly_ct(x[0], x[1], T, m + g);
+    bfly_ct(x[2], x[3], T, m + g + 1);
+}
+__device__ __forceinline__ void radix4_inv(u64 x[4], int j0, int s, const Tw &T)
+{
+    int m = N / (2 * s), g = j0 / (2 * s);
+    bfly_gs(x[0], x[1], T, m + g);
+    bfly_gs(x[2], x[3], T, m + g + 1);
+    m >>= 1;
+    g >>= 1;
+    bfly_gs(x[0], x[2], T, m + g);
+    bfly_gs(x[1], x[3], T, m + g);
+}
+
+__device__ __forceinline__ Tw twiddles(const u64 *tw, int pi, bool inv)
+{
+    const u64 *base = tw + (size_t)pi * 4 * N + (inv ? 2 * N : 0);
+    return Tw{base, base + N, c_pk[pi].q};
+}
+
+// Phase over the high 8 index bits (half-spans 2^15..2^8): 16 columns x 256 rows per CTA.
+template <bool INV>
+__global__ void __launch_bounds__(512) cols(u64 *data, PrimeMap pm, const u64 *__restrict__ tw,
+                                            const u64 *__restrict__ ninv)
+{
+    __shared__ u64 sm[256 * 16];
+    const int limb = blockIdx.y, pi = pm.p[limb % pm.n];
+    const Tw T = twiddles(tw, pi, INV);
+    u64 *a = data + (size_t)limb * N;
+    const int tid = threadIdx.x, col = tid & 15, c = blockIdx.x * 16 + col;
+    u64 x[8];
+    if (!INV) {
+        // round 1: rows r0 + 32k, s = 32 rows
+        const int r0 = tid >> 4;
+#pragma unroll
+        for (int k = 0; k < 8; k++) x[k] = a[(r0 + 32 * k) * 256 + c];
+        radix8_fwd(x, r0 * 256 + c, 32 * 256, T);
+#pragma unroll
+        for (int k = 0; k < 8; k++) sm[(r0 + 32 * k) * 16 + col] = x[k];
+        __syncthreads();
+        // round 2: rows b*32 + sub + 4k, s = 4 rows
+        const int b = tid >> 6, sub = (tid >> 4) & 3;
+#pragma unroll
+        for (int k = 0; k < 8; k++) x[k] = sm[(b * 32 + sub + 4 * k) * 16 + col];
+        radix8_fwd(x, (b * 32 + sub) * 256 + c, 4 * 256, T);
+#pragma unroll
+        for (int k = 0; k < 8; k++) sm[(b * 32 + sub + 4 * k) * 16 + col] = x[k];
+        __syncthreads();
+        // round 3: rows 4q + k (two groups per thread), s = 1 row
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int q = (tid >> 4) + 32 * h;
+            u64 y[4];
+#pragma unroll
+            for (int k = 0; k < 4; k++) y[k] = sm[(4 * q + k) * 16 + col];
+            radix4_fwd(y, 4 * q * 256 + c, 256, T);
+#pragma unroll
+            for (int k = 0; k < 4; k++) a[(4 * q + k) * 256 + c] = y[k];
+        }
+    } else {
+        const u64 ni = ninv[2 * pi], nis = ninv[2 * pi + 1];
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int q = (tid >> 4) + 32 * h;
+            u64 y[4];
+#pragma unroll
+            for (int k = 0; k < 4; k++) y[k] = a[(4 * q + k) * 256 + c];
+            radix4_inv(y, 4 * q * 256 + c, 256, T);
+#pragma unroll
+            for (int k = 0; k < 4; k++) sm[(4 * q + k) * 16 + col] = y[k];
+        }
+        __syncthreads();
+        const int b = tid >> 6, sub = (tid >> 4) & 3;
+#pragma unroll
+        for (int k = 0; k < 8; k++) x[k] = sm[(b * 32 + sub + 4 * k) * 16 + col];
+        radix8_inv(x, (b * 32 + sub) * 256 + c, 4 * 256, T);
+#pragma unroll
+        for (int k = 0; k < 8; k++) sm[(b * 32 + sub + 4 * k) * 16 + col] = x[k];
+        __syncthreads();
+        const int r0 = tid >> 4;
+#pragma unroll
+        for (int k = 0; k < 8; k++) x[k] = sm[(r0 + 32 * k) * 16 + col];
+        radix8_inv(x, r0 * 256 + c, 32 * 256, T);
+#pragma unroll
+        for (int k = 0; k < 8; k++) a[(r0 + 32 * k) * 256 + c] = d_shoup(x[k], ni, nis, T.q);
+    }
+}
+
+// Phase over the low 8 index bits (half-spans 2^7..1): 16 rows of 256 per CTA.
+template <bool INV>
+__global__ void __launch_bounds__(512) rows(u64 *data, PrimeMap pm, const u64 *__restrict__ tw)
+{
+    __shared__ u64 sm[16 * 256];
+    const int limb = blockIdx.y, pi = pm.p[limb % pm.n];
+    const Tw T = twiddles(tw, pi, INV);
+    const int row0 = blockIdx.x * 16;
+    u64 *a = data + (size_t)limb * N + (size_t)row0 * 256;
+    const int tid = threadIdx.x, row = tid >> 5;
+    const int jrow = (row0 + row) * 256;
+    u64 x[8];
+    if (!INV) {
+        const int e0 = tid & 31;
+#pragma unroll
+        for (int k = 0; k < 8; k++) x[k] = a[row * 256 + e0 + 32 * k];
+        radix8_fwd(x, jrow + e0, 32, T);
+#pragma unroll
+        for (int k = 0; k < 8; k++) sm[row * 256 + e0 + 32 * k] = x[k];
+        __syncthreads();
+        const int b = (tid >> 2) & 7, sub = tid & 3;
+#pragma unroll
+        for (int k = 0; k < 8; k++) x[k] = sm[row * 256 + b * 32 + sub + 4 * k];
+        radix8_fwd(x, jrow + b * 32 + sub, 4, T);
+#pragma unroll
+        for (int k = 0; k < 8; k++) sm[row * 256 + b * 32 + sub + 4 * k] = x[k];
+        __syncthreads();
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int q = (tid & 31) + 32 * h;
+            u64 y[4];
+#pragma unroll
+            for (int k = 0; k < 4; k++) y[k] = sm[row * 256 + 4 * q + k];
+            radix4_fwd(y, jrow + 4 * q, 1, T);
+#pragma unroll
+            for (int k = 0; k < 4; k++) sm[row * 256 + 4 * q + k] = y[k];
+        }
+        __syncthreads();
+        for (int i = tid; i < 16 * 256; i += 512) a[i] = sm[i];
+    } else {
+        for (int i = tid; i < 16 * 256; i += 512) sm[i] = a[i];
+        __syncthreads();
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int q = (tid & 31) + 32 * h;
+            u64 y[4];
+#pragma unroll
+            for (int k = 0; k < 4; k++) y[k] = sm[row * 256 + 4 * q + k];
+            radix4_inv(y, jrow + 4 * q, 1, T);
+#pragma unroll
+            for (int k = 0; k < 4; k++) sm[row * 256 + 4 * q + k] = y[k];
+        }
+        __syncthreads();
+        const int b = (tid >> 2) & 7, sub = tid & 3;
+#pragma unroll
+        for (int k = 0; k < 8; k++) x[k] = sm[row * 256 + b * 32 + sub + 4 * k];
+        radix8_inv(x, jrow + b * 32 + sub, 4, T);
+#pragma unroll
+        for (int k = 0; k < 8; k++) sm[row * 256 + b * 32 + sub + 4 * k] = x[k];
+        __syncthreads();
+        const int e0 = tid & 31;
+#pragma unroll
+        for (int k = 0; k < 8; k++) x[k] = sm[row * 256 + e0 + 32 * k];
+        radix8_inv(x, jrow + e0, 32, T);
+#pragma unroll
+        for (int k = 0; k < 8; k++) a[row * 256 + e0 + 32 * k] = x[k];
+    }
+}
+}  // namespace ntt16
+
 void k_ntt(hs_ctx *c, u64 *data, int n_limbs, const PrimeMap &pm, bool inverse, cudaStream_t st)
 {
     KTimer _kt(c, KID_NTT, (double)n_limbs * c->P->n * 16, st);
     if (n_limbs <= 0) return;
     const hs_params *P = c->P;
+    if (P->log_n == 16) {
+        const u64 *ninv = c->T.tw + (size_t)(P->n_q + P->n_p) * 4 * P->n;
+        dim3 g(16, n_limbs);
+        if (!inverse) {
+            ntt16::cols<false><<<g, 512, 0, st>>>(data, pm, c->T.tw, ninv);
+            ntt16::rows<false><<<g, 512, 0, st>>>(data, pm, c->T.tw);
+        } else {
+            ntt16::rows<true><<<g, 512, 0, st>>>(data, pm, c->T.tw);
+            ntt16::cols<true><<<g, 512, 0, st>>>(data, pm, c->T.tw, ninv);
+        }
+        HS_CHECK_LAUNCH();
+        c->ledger[HS_LG_NTT] += n_limbs;
+        count_kernel(c, 2);
+        return;
+    }
     NttGeom g;
     g.log_n = P->log_n;
     g.log_n2 = P->log_n / 2;
@@ -702,6 +940,253 @@ void k_signed_to_rns(hs_ctx *c, const int64_t *v, u64 *o, int n_limbs, const Pri
     KTimer _kt(c, KID_RNG, (double)(n_limbs + 1) * c->P->n * 8, st);
     int N = c->P->n;
     signed_to_rns_kernel<<<GRID_LIMBS(n_limbs, N), 256, 0, st>>>(v, o, pm, N);
+    HS_CHECK_LAUNCH();
+    count_kernel(c);
+}
+
+// ------------------------------------------------------------------ batched ciphertext kernels
+// A batch of B ciphertexts is one allocation [B][ncomp][nl][N]; a "row" is one
+// (ciphertext, component) pair of nl limbs.  Second operands may be broadcast
+// (b_rows < rows: row r uses b row r % b_rows).
+
+__global__ void add_b_kernel(const u64 *a, const u64 *b, u64 *o, int N, int nl, int a_rows, int b_rows, int sub)
+{
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= N) return;
+    int i = blockIdx.y, r = blockIdx.z;
+    u64 q = c_pk[i].q;
+    size_t x = ((size_t)(r % a_rows) * nl + i) * N + t, y = ((size_t)(r % b_rows) * nl + i) * N + t;
+    o[((size_t)r * nl + i) * N + t] = sub ? d_sub(a[x], b[y], q) : d_add(a[x], b[y], q);
+}
+
+void k_add_b(hs_ctx *c, const u64 *a, int a_rows, const u64 *b, int b_rows, u64 *o, int rows, int nl, bool sub,
+             cudaStream_t st)
+{
+    KTimer _kt(c, KID_ADD, (double)rows * nl * c->P->n * 24, st);
+    int N = c->P->n;
+    add_b_kernel<<<dim3((N + 255) / 256, nl, rows), 256, 0, st>>>(a, b, o, N, nl, a_rows, b_rows, sub ? 1 : 0);
+    HS_CHECK_LAUNCH();
+    count_kernel(c);
+}
+
+// o[r][i] = a[r][i] * s_i, rows of a/o with their own limb strides (drop + scale in one pass)
+__global__ void mul_scalar_s_kernel(const u64 *a, u64 *o, ScalarArg s, int N, int a_rl, int o_rl, int acc)
+{
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= N) return;
+    int i = blockIdx.y, r = blockIdx.z;
+    u64 q = c_pk[i].q;
+    u64 v = d_shoup(a[((size_t)r * a_rl + i) * N + t], s.v[i], s.vs[i], q);
+    size_t x = ((size_t)r * o_rl + i) * N + t;
+    o[x] = acc ? d_add(o[x], v, q) : v;
+}
+
+void k_mul_scalar_s(hs_ctx *c, const u64 *a, u64 *o, const u64 *host_scal, int rows, int nl, int a_rl, int o_rl,
+                    bool accumulate, cudaStream_t st)
+{
+    KTimer _kt(c, KID_SCALAR, (double)rows * nl * c->P->n * (accumulate ? 24 : 16), st);
+    int N = c->P->n;
+    mul_scalar_s_kernel<<<dim3((N + 255) / 256, nl, rows), 256, 0, st>>>(a, o, make_scalars(c->P, host_scal, nl), N,
+                                                                          a_rl, o_rl, accumulate ? 1 : 0);
+    HS_CHECK_LAUNCH();
+    count_kernel(c);
+}
+
+// comp 0 of each of B ciphertexts += s_i
+__global__ void add_scalar_b_kernel(u64 *a, ScalarArg s, int N, int nl, int row_stride)
+{
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= N) return;
+    int i = blockIdx.y, b = blockIdx.z;
+    size_t x = ((size_t)b * row_stride + i) * N + t;
+    a[x] = d_add(a[x], s.v[i], c_pk[i].q);
+}
+
+void k_add_scalar_b(hs_ctx *c, u64 *a, const u64 *host_scal, int B, int ncomp, int nl, cudaStream_t st)
+{
+    KTimer _kt(c, KID_SCALAR, (double)B * nl * c->P->n * 16, st);
+    int N = c->P->n;
+    ScalarArg s;
+    for (int i = 0; i < nl; i++) s.v[i] = host_scal[i];
+    add_scalar_b_kernel<<<dim3((N + 255) / 256, nl, B), 256, 0, st>>>(a, s, N, nl, ncomp * nl);
+    HS_CHECK_LAUNCH();
+    count_kernel(c);
+}
+
+// o[b] = tensor(a[b], bb[b % b_batch]); a/bb: [.][2][nl][N], o: [B][3][nl][N]
+__global__ void tensor_b_kernel(const u64 *a, const u64 *bb, u64 *o, int N, int nl, int b_batch)
+{
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= N) return;
+    int l = blockIdx.y, b = blockIdx.z;
+    const PrimeK k = c_pk[l];
+    size_t s = (size_t)nl * N, x = (size_t)l * N + t;
+    const u64 *A = a + (size_t)b * 2 * s, *Bp = bb + (size_t)(b % b_batch) * 2 * s;
+    u64 *O = o + (size_t)b * 3 * s;
+    u64 a0 = A[x], a1 = A[s + x], b0 = Bp[x], b1 = Bp[s + x];
+    O[x] = d_mulmod(a0, b0, k);
+    u64 hi = 0, lo = 0;
+    mac128(hi, lo, a0, b1);
+    mac128(hi, lo, a1, b0);
+    O[s + x] = d_reduce128(hi, lo, k);
+    O[2 * s + x] = d_mulmod(a1, b1, k);
+}
+
+void k_tensor_b(hs_ctx *c, const u64 *a, const u64 *b, u64 *o, int B, int nl, int b_batch, cudaStream_t st)
+{
+    KTimer _kt(c, KID_TENSOR, (double)B * nl * c->P->n * 56, st);
+    int N = c->P->n;
+    tensor_b_kernel<<<dim3((N + 255) / 256, nl, B), 256, 0, st>>>(a, b, o, N, nl, b_batch);
+    HS_CHECK_LAUNCH();
+    count_kernel(c);
+}
+
+// o = sum_b tensor(a[b], a[b])  (C15 aux sum, exact mod q in any order)
+__global__ void tensor_sum_kernel(const u64 *a, u64 *o, int N, int nl, int B)
+{
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= N) return;
+    int l = blockIdx.y;
+    const PrimeK k = c_pk[l];
+    size_t s = (size_t)nl * N, x = (size_t)l * N + t;
+    u64 d0 = 0, d1 = 0, d2 = 0;
+    for (int b = 0; b < B; b++) {
+        const u64 *A = a + (size_t)b * 2 * s;
+        u64 a0 = A[x], a1 = A[s + x];
+        d0 = d_add(d0, d_mulmod(a0, a0, k), k.q);
+        u64 p = d_mulmod(a0, a1, k);
+        d1 = d_add(d1, d_add(p, p, k.q), k.q);
+        d2 = d_add(d2, d_mulmod(a1, a1, k), k.q);
+    }
+    o[x] = d0;
+    o[s + x] = d1;
+    o[2 * s + x] = d2;
+}
+
+void k_tensor_sum(hs_ctx *c, const u64 *a, u64 *o, int B, int nl, cudaStream_t st)
+{
+    KTimer _kt(c, KID_TENSOR, (double)(2 * B + 3) * nl * c->P->n * 8, st);
+    int N = c->P->n;
+    tensor_sum_kernel<<<dim3((N + 255) / 256, nl), 256, 0, st>>>(a, o, N, nl, B);
+    HS_CHECK_LAUNCH();
+    count_kernel(c);
+}
+
+// batched key-switch inner product.  d: B polys with stride d_stride words;
+// ext digit j of ciphertext b: ext + off[j] + (b * nd[j] + g') * N;
+// acc: [B][2][ntg][N].  Each thread keeps BT ciphertexts' accumulators so
+// the evaluation key is read once per batch tile.
+struct KsArgB {
+    int level, beta, alpha, n_q, n_t, B;
+    size_t d_stride;
+    size_t off[16];
+    int nd[16];
+};
+
+template <int BT>
+__global__ void ks_inner_b_kernel(const u64 *__restrict__ d, const u64 *__restrict__ ext,
+                                  const u64 *__restrict__ key, u64 *acc, KsArgB A, int N)
+{
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= N) return;
+    const int g = blockIdx.y, b0 = blockIdx.z * BT;
+    const int nl = A.level + 1, ntg = nl + A.alpha;
+    const int pi = g < nl ? g : A.n_q + (g - nl);
+    const PrimeK k = c_pk[pi];
+    const size_t ntot = (size_t)A.n_q + A.n_t;
+    u64 h0[BT], l0[BT], h1[BT], l1[BT];
+#pragma unroll
+    for (int u = 0; u < BT; u++) h0[u] = l0[u] = h1[u] = l1[u] = 0;
+    for (int j = 0; j < A.beta; j++) {
+        const int lo = j * A.alpha, hi = min((j + 1) * A.alpha, nl), dn = hi - lo;
+        const u64 k0 = key[(((size_t)j * 2 + 0) * ntot + pi) * N + t];
+        const u64 k1 = key[(((size_t)j * 2 + 1) * ntot + pi) * N + t];
+        const bool own = g >= lo && g < hi;
+        const int gg = g < lo ? g : g - dn;
+#pragma unroll
+        for (int u = 0; u < BT; u++) {
+            const int b = b0 + u;
+            if (b >= A.B) break;
+            u64 v = own ? d[(size_t)b * A.d_stride + (size_t)g * N + t]
+                        : ext[A.off[j] + ((size_t)b * A.nd[j] + gg) * N + t];
+            mac128(h0[u], l0[u], v, k0);
+            mac128(h1[u], l1[u], v, k1);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < BT; u++) {
+        const int b = b0 + u;
+        if (b >= A.B) break;
+        acc[((size_t)b * 2 * ntg + g) * N + t] = d_reduce128(h0[u], l0[u], k);
+        acc[((size_t)(b * 2 + 1) * ntg + g) * N + t] = d_reduce128(h1[u], l1[u], k);
+    }
+}
+
+void k_ks_inner_b(hs_ctx *c, const u64 *d, size_t d_stride, const u64 *ext, const size_t *off, const int *nd,
+                  const u64 *key, u64 *acc, int level, int beta, int B, cudaStream_t st)
+{
+    const hs_params *P = c->P;
+    const int ntg = level + 1 + P->n_p;
+    const int tiles = (B + 3) / 4;
+    KTimer _kt(c, KID_KS_INNER, ((double)beta * ntg * (16.0 * tiles + 8.0 * B) + 16.0 * ntg * B) * P->n, st);
+    KsArgB A;
+    A.level = level;
+    A.beta = beta;
+    A.alpha = P->alpha;
+    A.n_q = P->n_q;
+    A.n_t = P->n_p;
+    A.B = B;
+    A.d_stride = d_stride;
+    for (int j = 0; j < beta; j++) {
+        A.off[j] = off[j];
+        A.nd[j] = nd[j];
+    }
+    int N = P->n;
+    ks_inner_b_kernel<4><<<dim3((N + 255) / 256, ntg, tiles), 256, 0, st>>>(d, ext, key, acc, A, N);
+    HS_CHECK_LAUNCH();
+    count_kernel(c);
+}
+
+// o_b[c][i] = add_b[c][i] + (acc_b[c][i] - conv_b[c][i]) P^{-1} for b < B;
+// acc [B][2][ntg][N], conv [B][2][nl][N]; o / add with per-ciphertext strides
+struct MdArgB {
+    u64 pinv[HS_MAXP], pinv_sh[HS_MAXP];
+    int level, alpha, add_comps;
+    size_t o_stride, add_stride;
+};
+
+__global__ void moddown_final_b_kernel(const u64 *acc, const u64 *conv, u64 *o, const u64 *add, MdArgB A, int N)
+{
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= N) return;
+    const int i = blockIdx.y, comp = blockIdx.z & 1, b = blockIdx.z >> 1;
+    const int nl = A.level + 1;
+    u64 q = c_pk[i].q;
+    u64 av = acc[(((size_t)b * 2 + comp) * (nl + A.alpha) + i) * N + t];
+    u64 cv = conv[(((size_t)b * 2 + comp) * nl + i) * N + t];
+    u64 v = d_shoup(d_sub(av, cv, q), A.pinv[i], A.pinv_sh[i], q);
+    size_t ci = ((size_t)comp * nl + i) * N + t;
+    if (comp < A.add_comps) v = d_add(v, add[(size_t)b * A.add_stride + ci], q);
+    o[(size_t)b * A.o_stride + ci] = v;
+}
+
+void k_moddown_final_b(hs_ctx *c, const u64 *acc, const u64 *conv, u64 *o, size_t o_stride, const u64 *add,
+                       size_t add_stride, int add_comps, int level, int B, cudaStream_t st)
+{
+    const hs_params *P = c->P;
+    KTimer _kt(c, KID_MODDOWN, (double)B * (level + 1) * P->n * 8 * (6 + add_comps), st);
+    MdArgB A;
+    for (int i = 0; i <= level; i++) {
+        A.pinv[i] = P->p_inv_mod_q[i];
+        A.pinv_sh[i] = hs_shoup_const(P->p_inv_mod_q[i], P->prime[i]);
+    }
+    A.level = level;
+    A.alpha = P->n_p;
+    A.add_comps = add ? add_comps : 0;
+    A.o_stride = o_stride;
+    A.add_stride = add_stride;
+    int N = P->n;
+    moddown_final_b_kernel<<<dim3((N + 255) / 256, level + 1, 2 * B), 256, 0, st>>>(acc, conv, o, add, A, N);
     HS_CHECK_LAUNCH();
     count_kernel(c);
 }

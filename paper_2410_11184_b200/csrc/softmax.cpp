@@ -55,28 +55,32 @@ hs_status softmax_run(hs_ctx *c, const hs_keys *K, const hs_softmax_desc *d, con
     std::vector<double> mask(N0, 0.0);
     for (int s = 0; s < stride; s++) mask[s] = 1.0;  // G10: coordinate block 0
 
-    std::vector<CtP> y0(ml), y(ml);
+    // the main thread keeps this rank's ml ciphertexts as ONE batch: every op
+    // below runs once over all of them (same schedule as per ciphertext)
+    if (in[0]->level < poly_cost(d->exp_poly)) level_error("input level too low for exp");
+    CtP xb = ct_gather(in, ml, st);
     // y^(0) = exp(x / 2^k)
-    for (int i = 0; i < ml; i++) {
-        if (in[i]->level < poly_cost(d->exp_poly)) level_error("input level too low for exp");
-        y0[i] = ev_cheb(K, in[i], d->exp_poly, st);
-        y[i] = ct_copy(y0[i].get(), st);
-    }
+    CtP y0 = ev_cheb(K, xb.get(), d->exp_poly, st);
+    xb.reset();
+    CtP y = ct_copy(y0.get(), st);
     CtP lam;
     for (int j = 1; j <= d->k; j++) {
         const hs_poly *ip = &d->inv_poly[j - 1];
         // G12 (c): Alg 1 main thread needs 1 (aux square) + 2 levels
-        if (d->variant == 0 && y[0]->level < 2) {
+        if (d->variant == 0 && y->level < 2) {
             if (!d->bts) level_error("main thread needs bootstrapping (not available)");
-            for (int i = 0; i < ml; i++) y[i] = ev_bootstrap(K, d->bts, y[i].get(), 1.0, st);
+            std::vector<CtP> parts(ml);
+            std::vector<const hs_ct *> ptrs(ml);
+            for (int i = 0; i < ml; i++) {
+                CtP one = ct_slice(y.get(), i, st);
+                parts[i] = ev_bootstrap(K, d->bts, one.get(), 1.0, st);
+                ptrs[i] = parts[i].get();
+            }
+            y = ct_gather(ptrs.data(), ml, st);
         }
-        if (y[0]->level < 1) level_error("main thread out of levels");
-        // ---- auxiliary thread: S = relin(sum tensor(y, y)) -> rescale
-        CtP acc;
-        for (int i = 0; i < ml; i++) {
-            CtP t = ev_tensor(y[i].get(), y[i].get(), st);
-            acc = acc ? ev_add(acc.get(), t.get(), false, st) : std::move(t);
-        }
+        if (y->level < 1) level_error("main thread out of levels");
+        // ---- auxiliary thread: S = relin(sum tensor(y, y)) -> rescale (C15)
+        CtP acc = ev_tensor_sum(y.get(), st);
         if (world > 1) {
             const size_t words = acc->limbs() * P->n;
             DBuf gathered(words * world, st);
@@ -92,7 +96,7 @@ hs_status softmax_run(hs_ctx *c, const hs_keys *K, const hs_softmax_desc *d, con
         CtP S = ev_rescale(rl.get(), st);
         rl.reset();
         rot_sum(K, S, nb, stride, -1, st);
-        const int main_level = d->variant == 0 ? y[0]->level : y0[0]->level;
+        const int main_level = d->variant == 0 ? y->level : y0->level;
         const int need = poly_cost(ip) + 1 + ((d->variant == 1 && j > 1) ? 1 : 0);
         // G12 (a): bootstrap before the inverse square root when the rest of the
         // aux thread would leave lambda below the main operand's level
@@ -110,21 +114,21 @@ hs_status softmax_run(hs_ctx *c, const hs_keys *K, const hs_softmax_desc *d, con
         // G12 (b): bootstrap lambda again if it ended below the main level
         if (lam->level < main_level && d->bts)
             lam = ev_bootstrap(K, d->bts, lam.get(), d->variant == 1 ? 1.5 : 1.1 / sqrt(ip->a), st);
-        // ---- main thread
-        for (int i = 0; i < ml; i++) {
-            if (d->variant == 0) {
-                CtP z = ev_mult(K, lam.get(), y[i].get(), st);
-                y[i] = ev_mult(K, z.get(), z.get(), st);
-            } else {
-                CtP z = ev_mult(K, lam.get(), y0[i].get(), st);
-                for (int s = 0; s < j; s++) {
-                    if (z->level < 1) level_error("version B squaring out of levels");
-                    z = ev_mult(K, z.get(), z.get(), st);
-                }
-                y[i] = std::move(z);
+        // ---- main thread (lam broadcast against the batch)
+        if (d->variant == 0) {
+            CtP z = ev_mult(K, lam.get(), y.get(), st);
+            y = ev_mult(K, z.get(), z.get(), st);
+        } else {
+            CtP z = ev_mult(K, lam.get(), y0.get(), st);
+            for (int s = 0; s < j; s++) {
+                if (z->level < 1) level_error("version B squaring out of levels");
+                z = ev_mult(K, z.get(), z.get(), st);
             }
+            y = std::move(z);
         }
     }
-    for (int i = 0; i < ml; i++) out[i] = y[i].release();
+    std::vector<CtP> res(ml);
+    for (int i = 0; i < ml; i++) res[i] = ct_slice(y.get(), i, st);
+    for (int i = 0; i < ml; i++) out[i] = res[i].release();
     return HS_OK;
 }

@@ -41,6 +41,7 @@ hs_ctx::~hs_ctx()
     cudaDeviceSynchronize();
     for (auto &kv : bconv) cudaFree(kv.second.dev);
     for (auto &kv : galois_perm) cudaFree(kv.second);
+    for (auto &kv : pt_cache) cudaFree(kv.second);
     for (auto e : kprof_ev) cudaEventDestroy(e);
     cudaFree(T.tw);
 }
@@ -399,14 +400,34 @@ CtP ev_mult_pt(const hs_ct *a, const double *re, const double *im, int target, c
     if (target < 0 || target >= a->level) throw HsError(HS_ELEVEL, "mult_pt: target level must be below the input");
     const size_t N = P->n;
     const int nl = target + 2;
-    std::vector<u64> pt((size_t)nl * N);
-    hs_encode_impl(P, re, im, landing_scale(P, a->level, target), target + 1, pt.data());
-    DBuf m((size_t)nl * N, st);
-    HS_CUDA(cudaMemcpyAsync(m.p, pt.data(), pt.size() * 8, cudaMemcpyHostToDevice, st));
-    k_ntt(c, m.p, nl, pmap_range(0, nl), false, st);
+    // encoded plaintexts are cached per (slot content, input level, target):
+    // the Softmax mask is re-used every iteration
+    u64 h = 1469598103934665603ull;
+    auto mix = [&h](const double *v, size_t n) {
+        const unsigned char *p = (const unsigned char *)v;
+        for (size_t i = 0; i < n * 8; i++) h = (h ^ p[i]) * 1099511628211ull;
+    };
+    mix(re, N / 2);
+    if (im) mix(im, N / 2);
+    else h ^= 0x9e3779b97f4a7c15ull;
+    const std::pair<u64, long> key(h, ((long)a->level << 16) | target);
+    u64 *m;
+    {
+        std::lock_guard<std::mutex> g(c->mu);
+        auto it = c->pt_cache.find(key);
+        m = it == c->pt_cache.end() ? nullptr : it->second;
+    }
+    if (!m) {
+        std::vector<u64> pt((size_t)nl * N);
+        hs_encode_impl(P, re, im, landing_scale(P, a->level, target), target + 1, pt.data());
+        HS_CUDA(cudaMalloc(&m, pt.size() * 8));
+        HS_CUDA(cudaMemcpy(m, pt.data(), pt.size() * 8, cudaMemcpyHostToDevice));
+        k_ntt(c, m, nl, pmap_range(0, nl), false, st);
+        std::lock_guard<std::mutex> g(c->mu);
+        c->pt_cache[key] = m;
+    }
     CtP d = ct_drop(a, target + 1, st);
-    k_mul_pointwise(c, d->d, m.p, d->d, (int)d->limbs(), nl, nl, st);
-    HS_CUDA(cudaStreamSynchronize(st));  // pt host buffer lifetime
+    k_mul_pointwise(c, d->d, m, d->d, (int)d->limbs(), nl, nl, st);
     c->ledger[HS_LG_PMULT] += a->batch;
     return ev_rescale(d.get(), st);
 }

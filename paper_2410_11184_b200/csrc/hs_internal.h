@@ -90,6 +90,7 @@ struct hs_ctx {
     DevTables T;
     std::map<long, BconvTab> bconv;          // key: (level << 8 | digit), digit 255 = ModDown
     std::map<int, unsigned *> galois_perm;   // device permutation tables
+    std::map<std::pair<u64, long>, u64 *> pt_cache;  // (content hash, level pair) -> NTT plaintext
     std::mutex mu;
     int64_t ledger[HS_LG_COUNT] = {0};
     bool kprof_on = false;

@@ -156,6 +156,15 @@ typedef enum {
 
 hs_status hs_op(hs_ctx *c, const hs_keys *k, int op, const hs_ct *a, const hs_ct *b, double cst, int i,
                 void *stream, hs_ct **out);
+/* C16 hoisted rotations (C16; Halevi-Shoup hoisting, used by the
+ * bootstrapping linear transforms' baby steps): out[r] = Rot(a, rots[r]) for
+ * r < n (1 <= n <= 64), all computed from ONE ModUp of a's c1.  Each output
+ * decrypts like hs_op(HS_OP_ROTATE) but its words differ (bit-exact with the
+ * oracle's orc_op_rotate_hoisted, not with a plain rotation).  a: one
+ * degree-1 ciphertext; out[]: n new ciphertexts owned by the caller
+ * (hs_ct_destroy).  HS_EKEY if a rotation key is missing (no output written). */
+hs_status hs_rotate_hoisted(hs_ctx *c, const hs_keys *k, const hs_ct *a, const int32_t *rots, int n, void *stream,
+                            hs_ct **out);
 /* slot-vector multiply landing at level `target` (C12). */
 hs_status hs_mult_pt(hs_ctx *c, const hs_ct *a, const double *re, const double *im, int target, void *stream,
                      hs_ct **out);

@@ -149,6 +149,13 @@ int orc_api_keyswitch(const orc_params *P, const orc_keys *K, int galois, int le
     return 0;
 }
 
+/* C16: hoisted rotations of one ciphertext; out[n] (NULL on a missing key) */
+int orc_api_rotate_hoisted(const orc_params *P, const orc_keys *K, const orc_ct *a, const int *rots, int n,
+                           orc_ct **out)
+{
+    return orc_op_rotate_hoisted(P, K, a, rots, n, out);
+}
+
 orc_ct *orc_api_cheb(const orc_params *P, const orc_keys *K, const orc_ct *x, int deg, double a, double b, const double *c)
 {
     orc_cheb p = {deg, a, b, c};

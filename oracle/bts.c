@@ -337,14 +337,20 @@ static orc_ct *apply_ltrans(const orc_params *P, const orc_keys *K, const orc_ct
 {
     int N = P->n, n0 = N / 2, l = T->level;
     orc_ct *ct = orc_op_level_down(P, ct0, l);
-    /* baby rotations */
+    /* baby rotations, hoisted (C16): one ModUp of ct's c1 serves every b != 0,
+     * in increasing b */
     orc_ct *R[64] = {0};
-    for (int k = 0; k < T->n_terms; k++) {
-        int b = T->b[k];
-        if (R[b]) continue;
-        R[b] = b == 0 ? orc_ct_copy(P, ct) : orc_op_rotate(P, K, ct, b * T->u);
-        if (!R[b]) return NULL;
-    }
+    int present[64] = {0}, rots[64], bs[64], nr = 0;
+    for (int k = 0; k < T->n_terms; k++) present[T->b[k]] = 1;
+    for (int b = 1; b < 64; b++)
+        if (present[b]) {
+            bs[nr] = b;
+            rots[nr++] = b * T->u;
+        }
+    if (present[0]) R[0] = orc_ct_copy(P, ct);
+    orc_ct *hr[64];
+    if (nr && orc_op_rotate_hoisted(P, K, ct, rots, nr, hr) != 0) return NULL;
+    for (int i = 0; i < nr; i++) R[bs[i]] = hr[i];
     int maxg = 0;
     for (int k = 0; k < T->n_terms; k++) if (T->g[k] > maxg) maxg = T->g[k];
     orc_ct *acc = orc_ct_alloc(P, l, 2);

@@ -432,18 +432,15 @@ orc_ct *orc_op_tensor(const orc_params *P, const orc_ct *a0, const orc_ct *b0)
 
 /* ---------------------------------------------------------------- key switching (C7) */
 
-/* d: (level+1) limbs NTT domain.  out0/out1: (level+1) limbs NTT domain. */
-void orc_keyswitch(const orc_params *P, const orc_swk *key, int level, const u64 *d, u64 *out0, u64 *out1)
+/* ModUp (C7 first half): digit j = primes [j alpha, min((j+1) alpha, nl)) of d
+ * (NTT domain, nl limbs) extended to every target prime q_0..q_level,
+ * p_0..p_{np-1}.  Returns ext[j][g][N], NTT domain; the digit's own limbs are
+ * d's limbs unchanged. */
+static u64 *ks_modup(const orc_params *P, int level, const u64 *d)
 {
-    int N = P->n, nq = P->n_q, np = P->n_p, nt = nq + np, alpha = P->alpha;
-    int nl = level + 1;                       /* live Q limbs */
-    int beta = (nl + alpha - 1) / alpha;
-    /* target prime list: q_0..q_level, p_0..p_{np-1} (global indices) */
-    int ntg = nl + np;
-    int *gidx = malloc(sizeof(int) * ntg);
-    for (int i = 0; i < nl; i++) gidx[i] = i;
-    for (int k = 0; k < np; k++) gidx[nl + k] = nq + k;
-    u64 *acc = calloc((size_t)2 * ntg * N, sizeof(u64));
+    int N = P->n, nq = P->n_q, np = P->n_p, alpha = P->alpha;
+    int nl = level + 1, beta = (nl + alpha - 1) / alpha, ntg = nl + np;
+    u64 *ext = malloc(sizeof(u64) * (size_t)beta * ntg * N);
     u64 *x = malloc(sizeof(u64) * (size_t)nl * N);
     /* coefficient form of d */
     memcpy(x, d, sizeof(u64) * (size_t)nl * N);
@@ -463,11 +460,11 @@ void orc_keyswitch(const orc_params *P, const orc_swk *key, int level, const u64
         }
         #pragma omp parallel for
         for (int g = 0; g < ntg; g++) {
-            int pi = gidx[g];
+            int pi = g < nl ? g : nq + (g - nl);
             u64 p = P->prime[pi];
-            u64 *ext = malloc(sizeof(u64) * N);
+            u64 *e = ext + ((size_t)j * ntg + g) * N;
             if (pi >= lo && pi < hi) {
-                memcpy(ext, d + (size_t)pi * N, sizeof(u64) * N);   /* own limb: unchanged */
+                memcpy(e, d + (size_t)pi * N, sizeof(u64) * N);   /* own limb: unchanged */
             } else {
                 u64 *qhp = malloc(sizeof(u64) * dn);
                 for (int a = 0; a < dn; a++) {
@@ -478,25 +475,51 @@ void orc_keyswitch(const orc_params *P, const orc_swk *key, int level, const u64
                 for (int t = 0; t < N; t++) {
                     u64 s = 0;
                     for (int a = 0; a < dn; a++) s = orc_add(s, orc_mul(y[(size_t)a * N + t] % p, qhp[a], p), p);
-                    ext[t] = s;
+                    e[t] = s;
                 }
                 free(qhp);
-                orc_ntt_fwd(P, pi, ext);
+                orc_ntt_fwd(P, pi, e);
             }
-            const u64 *k0 = key->k + (((size_t)j * 2 + 0) * nt + pi) * N;
-            const u64 *k1 = key->k + (((size_t)j * 2 + 1) * nt + pi) * N;
-            u64 *a0 = acc + (size_t)g * N, *a1 = acc + ((size_t)ntg + g) * N;
-            for (int t = 0; t < N; t++) {
-                a0[t] = orc_add(a0[t], orc_mul(ext[t], k0[t], p), p);
-                a1[t] = orc_add(a1[t], orc_mul(ext[t], k1[t], p), p);
-            }
-            free(ext);
         }
         free(y);
     }
-    /* ModDown: (acc_Q - BConv_{P->Q}(acc_P)) * P^{-1} */
+    free(x);
+    return ext;
+}
+
+/* inner product with the evaluation key: acc[c][g] = sum_j sigma(ext_j)[g] key_j[c][g]
+ * where sigma(v)[t] = v[perm[t]] (perm NULL = identity).  acc[2][ntg][N]. */
+static void ks_inner(const orc_params *P, const orc_swk *key, int level, const u64 *ext, const unsigned *perm,
+                     u64 *acc)
+{
+    int N = P->n, nq = P->n_q, np = P->n_p, nt = nq + np, alpha = P->alpha;
+    int nl = level + 1, beta = (nl + alpha - 1) / alpha, ntg = nl + np;
+    memset(acc, 0, sizeof(u64) * (size_t)2 * ntg * N);
+    #pragma omp parallel for
+    for (int g = 0; g < ntg; g++) {
+        int pi = g < nl ? g : nq + (g - nl);
+        u64 p = P->prime[pi];
+        u64 *a0 = acc + (size_t)g * N, *a1 = acc + ((size_t)ntg + g) * N;
+        for (int j = 0; j < beta; j++) {
+            const u64 *e = ext + ((size_t)j * ntg + g) * N;
+            const u64 *k0 = key->k + (((size_t)j * 2 + 0) * nt + pi) * N;
+            const u64 *k1 = key->k + (((size_t)j * 2 + 1) * nt + pi) * N;
+            for (int t = 0; t < N; t++) {
+                u64 v = e[perm ? perm[t] : (unsigned)t];
+                a0[t] = orc_add(a0[t], orc_mul(v, k0[t], p), p);
+                a1[t] = orc_add(a1[t], orc_mul(v, k1[t], p), p);
+            }
+        }
+    }
+}
+
+/* ModDown (C7 second half): out_c = (acc_Q - BConv_{P->Q}(acc_P)) * P^{-1} */
+static void ks_moddown(const orc_params *P, int level, const u64 *acc, u64 *out0, u64 *out1)
+{
+    int N = P->n, nq = P->n_q, np = P->n_p;
+    int nl = level + 1, ntg = nl + np;
     for (int c = 0; c < 2; c++) {
-        u64 *A = acc + (size_t)c * ntg * N;
+        const u64 *A = acc + (size_t)c * ntg * N;
         u64 *out = c == 0 ? out0 : out1;
         u64 *z = malloc(sizeof(u64) * (size_t)np * N);
         for (int k = 0; k < np; k++) {
@@ -537,9 +560,18 @@ void orc_keyswitch(const orc_params *P, const orc_swk *key, int level, const u64
         }
         free(z);
     }
+}
+
+/* d: (level+1) limbs NTT domain.  out0/out1: (level+1) limbs NTT domain. */
+void orc_keyswitch(const orc_params *P, const orc_swk *key, int level, const u64 *d, u64 *out0, u64 *out1)
+{
+    int ntg = level + 1 + P->n_p;
+    u64 *ext = ks_modup(P, level, d);
+    u64 *acc = malloc(sizeof(u64) * (size_t)2 * ntg * P->n);
+    ks_inner(P, key, level, ext, NULL, acc);
+    ks_moddown(P, level, acc, out0, out1);
     free(acc);
-    free(x);
-    free(gidx);
+    free(ext);
     orc_ledger[LG_KS]++;
 }
 
@@ -611,6 +643,48 @@ orc_ct *orc_op_galois(const orc_params *P, const orc_keys *K, const orc_ct *a, i
 orc_ct *orc_op_rotate(const orc_params *P, const orc_keys *K, const orc_ct *a, int r)
 {
     return orc_op_galois(P, K, a, orc_galois_of_rot(P, r));
+}
+
+/* C16 hoisted rotations (Halevi-Shoup 2018 hoisting): ModUp(c1) ONCE, then
+ * for each r: out = (sigma(c0) + ks0, ks1) with (ks0, ks1) =
+ * ModDown(sum_j sigma(ext_j) key_j), sigma = the Galois map of rotation r
+ * applied to the extended NTT-domain digits.  Decrypts like orc_op_rotate;
+ * the words differ (BConv does not commute with sigma's sign flips exactly).
+ * Returns 0, or -1 if a key is missing (out[] then partially filled). */
+int orc_op_rotate_hoisted(const orc_params *P, const orc_keys *K, const orc_ct *a, const int *rots, int n,
+                          orc_ct **out)
+{
+    int N = P->n, l = a->level, ntg = l + 1 + P->n_p;
+    u64 *ext = ks_modup(P, l, LIMB(P, a, 1, 0));
+    u64 *acc = malloc(sizeof(u64) * (size_t)2 * ntg * N);
+    unsigned *perm = malloc(sizeof(unsigned) * N);
+    int rc = 0;
+    for (int i = 0; i < n; i++) out[i] = NULL;
+    for (int i = 0; i < n && rc == 0; i++) {
+        int k = orc_galois_of_rot(P, rots[i]);
+        const orc_swk *key = orc_find_key(K, k);
+        if (!key) {
+            rc = -1;
+            break;
+        }
+        orc_galois_perm(P, k, perm);
+        ks_inner(P, key, l, ext, perm, acc);
+        orc_ct *r = orc_ct_alloc(P, l, 2);
+        ks_moddown(P, l, acc, LIMB(P, r, 0, 0), LIMB(P, r, 1, 0));
+        for (int j = 0; j <= l; j++) {
+            u64 q = P->prime[j];
+            u64 *o = LIMB(P, r, 0, j);
+            const u64 *c0 = LIMB(P, a, 0, j);
+            for (int t = 0; t < N; t++) o[t] = orc_add(c0[perm[t]], o[t], q);
+        }
+        out[i] = r;
+        orc_ledger[LG_KS]++;
+        orc_ledger[LG_ROT]++;
+    }
+    free(perm);
+    free(acc);
+    free(ext);
+    return rc;
 }
 
 orc_ct *orc_op_conjugate(const orc_params *P, const orc_keys *K, const orc_ct *a)

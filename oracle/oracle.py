@@ -88,6 +88,8 @@ def lib():
         L.orc_api_mult_pt.argtypes = [vp, vp, f64p, f64p, C.c_int]
         L.orc_api_keyswitch.restype = C.c_int
         L.orc_api_keyswitch.argtypes = [vp, vp, C.c_int, C.c_int, u64p, u64p, u64p]
+        L.orc_api_rotate_hoisted.restype = C.c_int
+        L.orc_api_rotate_hoisted.argtypes = [vp, vp, vp, i32p, C.c_int, C.POINTER(vp)]
         L.orc_api_cheb.restype = vp
         L.orc_api_cheb.argtypes = [vp, vp, vp, C.c_int, C.c_double, C.c_double, f64p]
         L.orc_api_cheb_depth.restype = C.c_int
@@ -251,6 +253,14 @@ def keyswitch(P: Params, K: Keys, galois, level, d):
     o1 = np.zeros_like(o0)
     assert lib().orc_api_keyswitch(P.ptr, K.ptr, galois, level, d, o0, o1) == 0
     return o0.reshape(level + 1, P.n), o1.reshape(level + 1, P.n)
+
+
+def rotate_hoisted(P: Params, K: Keys, a: Ct, rots):
+    """C16: every rotation in rots from ONE ModUp of a's c1."""
+    r = np.ascontiguousarray(rots, np.int32)
+    out = (C.c_void_p * len(rots))()
+    assert lib().orc_api_rotate_hoisted(P.ptr, K.ptr, a.ptr, r, len(rots), out) == 0, "missing rotation key"
+    return [Ct(P, out[i]) for i in range(len(rots))]
 
 
 def cheb(P: Params, K: Keys, x: Ct, poly: dict) -> Ct:

@@ -106,6 +106,8 @@ orc_ct *orc_op_mult_pt(const orc_params *P, const orc_ct *a, const double *re, c
 orc_ct *orc_op_galois(const orc_params *P, const orc_keys *K, const orc_ct *a, int k);
 orc_ct *orc_op_rotate(const orc_params *P, const orc_keys *K, const orc_ct *a, int r);
 orc_ct *orc_op_conjugate(const orc_params *P, const orc_keys *K, const orc_ct *a);
+int orc_op_rotate_hoisted(const orc_params *P, const orc_keys *K, const orc_ct *a, const int *rots, int n,
+                          orc_ct **out);
 void orc_keyswitch(const orc_params *P, const orc_swk *key, int level, const u64 *d, u64 *out0, u64 *out1);
 const orc_swk *orc_find_key(const orc_keys *K, int galois);
 int orc_galois_of_rot(const orc_params *P, int r);

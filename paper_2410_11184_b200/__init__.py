@@ -222,6 +222,14 @@ def keyswitch(keys: Keys, galois, level, d_ptr, out0_ptr, out1_ptr, stream=None)
                          C.c_void_p(out1_ptr), _stream(stream)))
 
 
+def rotate_hoisted(keys: Keys, a: Ciphertext, rots, stream=None):
+    """C16: Rot(a, r) for every r in rots from ONE ModUp of a's c1."""
+    r = (C.c_int32 * len(rots))(*rots)
+    out = (C.c_void_p * len(rots))()
+    check(L.hs_rotate_hoisted(keys.ctx.ptr, keys.ptr, a.ptr, r, len(rots), _stream(stream), out))
+    return [Ciphertext(a.ctx, C.c_void_p(out[i])) for i in range(len(rots))]
+
+
 def _poly(p):
     c = np.ascontiguousarray(p["coeffs"], np.float64)
     return L.Poly(len(c) - 1, float(p["a"]), float(p["b"]), c.ctypes.data_as(C.POINTER(C.c_double))), c

@@ -100,6 +100,8 @@ hs_ct_destroy = _sig("hs_ct_destroy", None, [vp])
 hs_op = _sig("hs_op", C.c_int, [vp, vp, C.c_int, vp, vp, C.c_double, C.c_int, vp, C.POINTER(vp)])
 hs_mult_pt = _sig("hs_mult_pt", C.c_int, [vp, vp, f64p, vp, C.c_int, vp, C.POINTER(vp)])
 hs_keyswitch = _sig("hs_keyswitch", C.c_int, [vp, vp, C.c_int, C.c_int, vp, vp, vp, vp])
+hs_rotate_hoisted = _sig("hs_rotate_hoisted", C.c_int, [vp, vp, vp, C.POINTER(C.c_int32), C.c_int, vp,
+                                                        C.POINTER(vp)])
 hs_ntt = _sig("hs_ntt", C.c_int, [vp, C.c_int, C.c_int, vp, C.c_int, vp])
 hs_cheb = _sig("hs_cheb", C.c_int, [vp, vp, vp, C.POINTER(Poly), vp, C.POINTER(vp)])
 hs_cheb_depth = _sig("hs_cheb_depth", C.c_int, [C.c_int])

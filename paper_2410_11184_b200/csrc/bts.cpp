@@ -283,9 +283,18 @@ static CtP apply(const hs_keys *K, const hs_ct *in, const LinTrans &T, cudaStrea
         lowered = ev_level_down(in, l, st);
         x = lowered.get();
     }
-    std::map<int, CtP> R;
-    for (int b : T.b)
-        if (!R.count(b)) R[b] = b == 0 ? ct_copy(x, st) : ev_rotate(K, x, b * T.unit, st);
+    // baby rotations, hoisted (C16): one ModUp of x's c1 serves every b != 0
+    std::vector<int> bs, rots;
+    for (int b = 1; b < 64; b++)
+        if (std::find(T.b.begin(), T.b.end(), b) != T.b.end()) {
+            bs.push_back(b);
+            rots.push_back(b * T.unit);
+        }
+    CtP hb;
+    if (!rots.empty()) hb = ev_rotate_hoisted(K, x, rots.data(), (int)rots.size(), st);
+    std::map<int, const u64 *> R;
+    R[0] = x->d;
+    for (size_t i = 0; i < bs.size(); i++) R[bs[i]] = hb->d + i * hb->ct_words();
     int maxg = 0;
     for (int g : T.g) maxg = std::max(maxg, g);
     CtP acc = ct_new(c, l, 2, st);
@@ -298,7 +307,7 @@ static CtP apply(const hs_keys *K, const hs_ct *in, const LinTrans &T, cudaStrea
                 inner = ct_new(c, l, 2, st);
                 HS_CUDA(cudaMemsetAsync(inner->d, 0, inner->limbs() * N * 8, st));
             }
-            k_mac_pt(c, inner->d, R[T.b[k]]->d, T.pts + k * nl * N, nl, nl, st);
+            k_mac_pt(c, inner->d, R[T.b[k]], T.pts + k * nl * N, nl, nl, st);
             c->ledger[HS_LG_PMULT]++;
         }
         if (!inner) continue;

@@ -91,7 +91,14 @@ hs_status hs_context_create(const hs_params *p, int device, hs_ctx **out)
     const int np = p->n_q + p->n_p;
     const size_t N = p->n;
     std::vector<u64> h((size_t)np * 4 * N + 2 * np);
-    for (int i = 0; i < np; i++) memcpy(&h[(size_t)i * 4 * N], p->tw[i].data(), 4 * N * 8);
+    // device layout per prime: (w, w') pairs of the forward table, then of the
+    // inverse table -- one 16-byte load per butterfly
+    for (int i = 0; i < np; i++)
+        for (int half = 0; half < 2; half++)
+            for (size_t k = 0; k < N; k++) {
+                h[(size_t)i * 4 * N + half * 2 * N + 2 * k] = p->tw[i][half * 2 * N + k];
+                h[(size_t)i * 4 * N + half * 2 * N + 2 * k + 1] = p->tw[i][half * 2 * N + N + k];
+            }
     for (int i = 0; i < np; i++) {
         h[(size_t)np * 4 * N + 2 * i] = p->n_inv[i];
         h[(size_t)np * 4 * N + 2 * i + 1] = p->n_inv_sh[i];
@@ -297,6 +304,22 @@ hs_status hs_mult_pt(hs_ctx *c, const hs_ct *a, const double *re, const double *
     if (!c || !a || !re || !out) throw HsError(HS_EINVAL, "NULL argument");
     activate(c);
     *out = ev_mult_pt(a, re, im, target, S(stream)).release();
+    return HS_OK;
+    HS_CATCH
+}
+
+hs_status hs_rotate_hoisted(hs_ctx *c, const hs_keys *k, const hs_ct *a, const int32_t *rots, int n, void *stream,
+                            hs_ct **out)
+{
+    HS_TRY
+    if (!c || !k || !a || !rots || !out || n < 1 || n > HS_MAXROT) throw HsError(HS_EINVAL, "bad arguments");
+    activate(c);
+    cudaStream_t st = S(stream);
+    std::vector<int> r(rots, rots + n);
+    CtP hb = ev_rotate_hoisted(k, a, r.data(), n, st);
+    std::vector<CtP> res(n);
+    for (int i = 0; i < n; i++) res[i] = ct_slice(hb.get(), i, st);
+    for (int i = 0; i < n; i++) out[i] = res[i].release();
     return HS_OK;
     HS_CATCH
 }

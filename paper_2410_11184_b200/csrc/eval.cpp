@@ -212,6 +212,56 @@ const unsigned *galois_table(hs_ctx *c, int k)
 }
 
 // ------------------------------------------------------------------ key switching (C7)
+// ModUp of B polynomials d_b = d + b*d_stride (level+1 limbs, NTT domain):
+// digit j's extension to every target prime but its own, block [B][nd_j][N].
+void ks_modup(hs_ctx *c, int level, int B, const u64 *d, size_t d_stride, ModUpBuf &m, cudaStream_t st)
+{
+    const hs_params *P = c->P;
+    const size_t N = P->n;
+    const int nl = level + 1, alpha = P->alpha;
+    m.beta = (nl + alpha - 1) / alpha;
+    // coefficient form of every d_b: [B][nl][N]
+    DBuf x((size_t)B * nl * N, st);
+    HS_CUDA(cudaMemcpy2DAsync(x.p, nl * N * 8, d, d_stride * 8, nl * N * 8, B, cudaMemcpyDeviceToDevice, st));
+    k_ntt(c, x.p, B * nl, pmap_range(0, nl), true, st);
+    size_t tot = 0;
+    for (int j = 0; j < m.beta; j++) {
+        const BconvTab &tab = bconv_modup(c, level, j);
+        m.off[j] = tot;
+        m.nd[j] = tab.n_dst;
+        tot += (size_t)B * tab.n_dst * N;
+    }
+    m.ext.alloc(tot, st);
+    for (int j = 0; j < m.beta; j++) {
+        const BconvTab &tab = bconv_modup(c, level, j);
+        u64 *e = m.ext.p + m.off[j];
+        k_bconv(c, tab, x.p + (size_t)tab.src[0] * N, N, e, N, B, (size_t)nl * N, (size_t)tab.n_dst * N, st);
+        PrimeMap pm;
+        pm.n = tab.n_dst;
+        for (int i = 0; i < tab.n_dst; i++) pm.p[i] = (unsigned char)tab.dst[i];
+        k_ntt(c, e, B * tab.n_dst, pm, false, st);
+    }
+}
+
+// ModDown of B accumulators acc [B][2][ntg][N]: iNTT of the P limbs, centred
+// BConv P -> Q_l, NTT, out_b = add_b + (acc - conv) P^{-1}
+void ks_moddown(hs_ctx *c, int level, int B, const u64 *acc, u64 *out, size_t out_stride, const u64 *add,
+                size_t add_stride, int add_comps, cudaStream_t st)
+{
+    const hs_params *P = c->P;
+    const size_t N = P->n;
+    const int nl = level + 1, np = P->n_p, ntg = nl + np;
+    DBuf z((size_t)B * 2 * np * N, st);
+    HS_CUDA(cudaMemcpy2DAsync(z.p, np * N * 8, acc + (size_t)nl * N, ntg * N * 8, np * N * 8, 2 * B,
+                              cudaMemcpyDeviceToDevice, st));
+    k_ntt(c, z.p, 2 * B * np, pmap_range(P->n_q, np), true, st);
+    const BconvTab &md = bconv_moddown(c, level);
+    DBuf conv((size_t)B * 2 * nl * N, st);
+    k_bconv(c, md, z.p, N, conv.p, N, 2 * B, (size_t)np * N, (size_t)nl * N, st);
+    k_ntt(c, conv.p, 2 * B * nl, pmap_range(0, nl), false, st);
+    k_moddown_final_b(c, acc, conv.p, out, out_stride, add, add_stride, add_comps, level, B, st);
+}
+
 // B polynomials d_b = d + b*d_stride (level+1 limbs each, NTT domain);
 // out_b = out + b*out_stride gets (ks0, ks1) (+ add_b's first add_comps components).
 void ev_keyswitch_b(const hs_keys *K, const SwKey *key, int level, int B, const u64 *d, size_t d_stride, u64 *out,
@@ -220,46 +270,48 @@ void ev_keyswitch_b(const hs_keys *K, const SwKey *key, int level, int B, const 
     hs_ctx *c = K->ctx;
     const hs_params *P = c->P;
     const size_t N = P->n;
-    const int nl = level + 1, alpha = P->alpha, np = P->n_p, ntg = nl + np;
-    const int beta = (nl + alpha - 1) / alpha;
-    // coefficient form of every d_b: [B][nl][N]
-    DBuf x((size_t)B * nl * N, st);
-    HS_CUDA(cudaMemcpy2DAsync(x.p, nl * N * 8, d, d_stride * 8, nl * N * 8, B, cudaMemcpyDeviceToDevice, st));
-    k_ntt(c, x.p, B * nl, pmap_range(0, nl), true, st);
-    // ModUp every digit for the whole batch: digit j block [B][nd_j][N]
-    size_t off[16];
-    int nd[16];
-    size_t tot = 0;
-    for (int j = 0; j < beta; j++) {
-        const BconvTab &tab = bconv_modup(c, level, j);
-        off[j] = tot;
-        nd[j] = tab.n_dst;
-        tot += (size_t)B * tab.n_dst * N;
-    }
-    DBuf ext(tot, st);
-    for (int j = 0; j < beta; j++) {
-        const BconvTab &tab = bconv_modup(c, level, j);
-        u64 *e = ext.p + off[j];
-        k_bconv(c, tab, x.p + (size_t)tab.src[0] * N, N, e, N, B, (size_t)nl * N, (size_t)tab.n_dst * N, st);
-        PrimeMap pm;
-        pm.n = tab.n_dst;
-        for (int i = 0; i < tab.n_dst; i++) pm.p[i] = (unsigned char)tab.dst[i];
-        k_ntt(c, e, B * tab.n_dst, pm, false, st);
-    }
+    const int ntg = level + 1 + P->n_p;
+    ModUpBuf m;
+    ks_modup(c, level, B, d, d_stride, m, st);
     // inner product with the evaluation key: acc[B][2][ntg][N]
     DBuf acc((size_t)B * 2 * ntg * N, st);
-    k_ks_inner_b(c, d, d_stride, ext.p, off, nd, key->k, acc.p, level, beta, B, st);
-    // ModDown: iNTT of the P limbs, centred BConv P -> Q_l, NTT, (acc - conv) P^{-1}
-    DBuf z((size_t)B * 2 * np * N, st);
-    HS_CUDA(cudaMemcpy2DAsync(z.p, np * N * 8, acc.p + (size_t)nl * N, ntg * N * 8, np * N * 8, 2 * B,
-                              cudaMemcpyDeviceToDevice, st));
-    k_ntt(c, z.p, 2 * B * np, pmap_range(P->n_q, np), true, st);
-    const BconvTab &md = bconv_moddown(c, level);
-    DBuf conv((size_t)B * 2 * nl * N, st);
-    k_bconv(c, md, z.p, N, conv.p, N, 2 * B, (size_t)np * N, (size_t)nl * N, st);
-    k_ntt(c, conv.p, 2 * B * nl, pmap_range(0, nl), false, st);
-    k_moddown_final_b(c, acc.p, conv.p, out, out_stride, add, add_stride, add_comps, level, B, st);
+    k_ks_inner_b(c, d, d_stride, m.ext.p, m.off, m.nd, key->k, acc.p, level, m.beta, B, st);
+    ks_moddown(c, level, B, acc.p, out, out_stride, add, add_stride, add_comps, st);
     c->ledger[HS_LG_KS] += B;
+}
+
+// C16: rotations rots[0..R) of ONE degree-1 ciphertext from a single ModUp of
+// its c1 (hoisting); returns a batch of R ciphertexts, batch r = Rot(a, rots[r]).
+CtP ev_rotate_hoisted(const hs_keys *K, const hs_ct *a, const int *rots, int R, cudaStream_t st)
+{
+    hs_ctx *c = K->ctx;
+    const hs_params *P = c->P;
+    const size_t N = P->n;
+    const int l = a->level, nl = l + 1, ntg = nl + P->n_p;
+    if (a->ncomp != 2 || a->batch != 1) throw HsError(HS_EINVAL, "hoisted rotation needs one degree-1 ciphertext");
+    if (R < 1 || R > HS_MAXROT) throw HsError(HS_EINVAL, "hoisted rotation: bad rotation count");
+    std::vector<const u64 *> keys(R);
+    std::vector<const unsigned *> perms(R);
+    for (int r = 0; r < R; r++) {
+        const int k = hs_galois_elt(P, rots[r]);
+        const SwKey *key = K->find(k);
+        if (!key) throw HsError(HS_EKEY, "switching key for rotation " + std::to_string(rots[r]) + " missing");
+        keys[r] = key->k;
+        perms[r] = galois_table(c, k);
+    }
+    const u64 *c1 = a->limb(1, 0);
+    ModUpBuf m;
+    ks_modup(c, l, 1, c1, nl * N, m, st);
+    DBuf acc((size_t)R * 2 * ntg * N, st);
+    k_ks_inner_h(c, c1, m.ext.p, m.off, m.nd, keys.data(), perms.data(), R, acc.p, l, m.beta, st);
+    // sigma_r(c0) as the added component 0 of each output
+    DBuf c0p((size_t)R * nl * N, st);
+    for (int r = 0; r < R; r++) k_permute(c, a->limb(0, 0), c0p.p + (size_t)r * nl * N, perms[r], nl, st);
+    CtP out = ct_new(c, l, 2, st, R);
+    ks_moddown(c, l, R, acc.p, out->d, out->ct_words(), c0p.p, (size_t)nl * N, 1, st);
+    c->ledger[HS_LG_KS] += R;
+    c->ledger[HS_LG_ROT] += R;
+    return out;
 }
 
 void ev_keyswitch(const hs_keys *K, const SwKey *key, int level, const u64 *d, u64 *out0, u64 *out1,

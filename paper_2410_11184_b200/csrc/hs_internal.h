@@ -30,6 +30,7 @@ typedef uint64_t u64;
 typedef unsigned __int128 u128;
 
 #define HS_MAXP 64
+#define HS_MAXROT 64  // rotations served by one hoisted ModUp (C16)
 
 // ------------------------------------------------------------------ errors
 struct HsError : std::runtime_error {
@@ -145,8 +146,23 @@ struct DBuf {                   // stream-ordered scratch buffer
     DBuf() {}
     DBuf(size_t words, cudaStream_t s) : p(dev_alloc(words, s)), st(s) {}
     ~DBuf() { if (p) dev_free(p, st); }
+    void alloc(size_t words, cudaStream_t s)
+    {
+        if (p) dev_free(p, st);
+        p = dev_alloc(words, s);
+        st = s;
+    }
     DBuf(const DBuf &) = delete;
     DBuf &operator=(const DBuf &) = delete;
+};
+
+// ModUp result of the hybrid key switch (C7): digit j's extension to every
+// target prime but its own, block [B][nd_j][N] at ext + off[j]
+struct ModUpBuf {
+    DBuf ext;
+    size_t off[16];
+    int nd[16];
+    int beta = 0;
 };
 
 // ------------------------------------------------------------------ kernel profiling (kprof.cpp)
@@ -202,6 +218,8 @@ void k_tensor_b(hs_ctx *c, const u64 *a, const u64 *b, u64 *o, int B, int nl, in
 void k_tensor_sum(hs_ctx *c, const u64 *a, u64 *o, int B, int nl, cudaStream_t st);
 void k_ks_inner_b(hs_ctx *c, const u64 *d, size_t d_stride, const u64 *ext, const size_t *off, const int *nd,
                   const u64 *key, u64 *acc, int level, int beta, int B, cudaStream_t st);
+void k_ks_inner_h(hs_ctx *c, const u64 *d, const u64 *ext, const size_t *off, const int *nd, const u64 *const *keys,
+                  const unsigned *const *perms, int R, u64 *acc, int level, int beta, cudaStream_t st);
 void k_moddown_final_b(hs_ctx *c, const u64 *acc, const u64 *conv, u64 *o, size_t o_stride, const u64 *add,
                        size_t add_stride, int add_comps, int level, int B, cudaStream_t st);
 void k_modraise(hs_ctx *c, const u64 *x, u64 *o, int nl, cudaStream_t st);
@@ -241,6 +259,10 @@ CtP ev_mult_const(const hs_ct *a, double v, int target, cudaStream_t st);
 CtP ev_mult_pt(const hs_ct *a, const double *re, const double *im, int target, cudaStream_t st);
 CtP ev_galois(const hs_keys *K, const hs_ct *a, int k, cudaStream_t st);
 CtP ev_rotate(const hs_keys *K, const hs_ct *a, int r, cudaStream_t st);
+CtP ev_rotate_hoisted(const hs_keys *K, const hs_ct *a, const int *rots, int R, cudaStream_t st);
+void ks_modup(hs_ctx *c, int level, int B, const u64 *d, size_t d_stride, ModUpBuf &m, cudaStream_t st);
+void ks_moddown(hs_ctx *c, int level, int B, const u64 *acc, u64 *out, size_t out_stride, const u64 *add,
+                size_t add_stride, int add_comps, cudaStream_t st);
 void ev_keyswitch(const hs_keys *K, const SwKey *key, int level, const u64 *d, u64 *out0, u64 *out1,
                   const u64 *add0, const u64 *add1, cudaStream_t st);
 CtP ev_mult_const_sum(const std::vector<const hs_ct *> &terms, const std::vector<double> &coef, int target,

@@ -82,8 +82,7 @@ __global__ void __launch_bounds__(256) ntt_cols_kernel(u64 *data, PrimeMap pm, c
     const PrimeK k = c_pk[pi];
     const u64 q = k.q;
     u64 *a = data + (size_t)limb * N;
-    const u64 *w = tw + (size_t)pi * 4 * N + (INV ? 2 * N : 0);
-    const u64 *wsh = w + N;
+    const u64 *w = tw + (size_t)pi * 4 * N + (INV ? 2 * N : 0);  // (w, w') pairs
     const int c0 = blockIdx.x * C;
     const int tot = N1 * C;
     for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
@@ -97,7 +96,7 @@ __global__ void __launch_bounds__(256) ntt_cols_kernel(u64 *data, PrimeMap pm, c
             for (int b = threadIdx.x; b < half; b += blockDim.x) {
                 int c = b % C, rb = b / C;
                 int grp = rb / tr, rl = grp * 2 * tr + (rb - grp * tr), rh = rl + tr;
-                u64 W = w[m + grp], Ws = wsh[m + grp];
+                u64 W = w[2 * (m + grp)], Ws = w[2 * (m + grp) + 1];
                 u64 U = sm[rl * C + c], V = d_shoup(sm[rh * C + c], W, Ws, q);
                 sm[rl * C + c] = d_add(U, V, q);
                 sm[rh * C + c] = d_sub(U, V, q);
@@ -109,7 +108,7 @@ __global__ void __launch_bounds__(256) ntt_cols_kernel(u64 *data, PrimeMap pm, c
             for (int b = threadIdx.x; b < half; b += blockDim.x) {
                 int c = b % C, rb = b / C;
                 int grp = rb / tr, rl = grp * 2 * tr + (rb - grp * tr), rh = rl + tr;
-                u64 W = w[m + grp], Ws = wsh[m + grp];
+                u64 W = w[2 * (m + grp)], Ws = w[2 * (m + grp) + 1];
                 u64 U = sm[rl * C + c], V = sm[rh * C + c];
                 sm[rl * C + c] = d_add(U, V, q);
                 sm[rh * C + c] = d_shoup(d_sub(U, V, q), W, Ws, q);
@@ -137,8 +136,7 @@ __global__ void __launch_bounds__(256) ntt_rows_kernel(u64 *data, PrimeMap pm, c
     const PrimeK k = c_pk[pi];
     const u64 q = k.q;
     u64 *a = data + (size_t)limb * N + (size_t)blockIdx.x * R * N2;
-    const u64 *w = tw + (size_t)pi * 4 * N + (INV ? 2 * N : 0);
-    const u64 *wsh = w + N;
+    const u64 *w = tw + (size_t)pi * 4 * N + (INV ? 2 * N : 0);  // (w, w') pairs
     const int tot = R * N2;
     const int row0 = blockIdx.x * R;
     for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) sm[idx] = a[idx];
@@ -151,7 +149,7 @@ __global__ void __launch_bounds__(256) ntt_rows_kernel(u64 *data, PrimeMap pm, c
                 int row = b / hrow, bb = b - row * hrow;
                 int gl = bb / t, lo = gl * 2 * t + (bb - gl * t);
                 int grp = (row0 + row) * (N2 / (2 * t)) + gl;
-                u64 W = w[m + grp], Ws = wsh[m + grp];
+                u64 W = w[2 * (m + grp)], Ws = w[2 * (m + grp) + 1];
                 int il = row * N2 + lo, ih = il + t;
                 u64 U = sm[il], V = d_shoup(sm[ih], W, Ws, q);
                 sm[il] = d_add(U, V, q);
@@ -166,7 +164,7 @@ __global__ void __launch_bounds__(256) ntt_rows_kernel(u64 *data, PrimeMap pm, c
                 int row = b / hrow, bb = b - row * hrow;
                 int gl = bb / t, lo = gl * 2 * t + (bb - gl * t);
                 int grp = (row0 + row) * (N2 / (2 * t)) + gl;
-                u64 W = w[m + grp], Ws = wsh[m + grp];
+                u64 W = w[2 * (m + grp)], Ws = w[2 * (m + grp) + 1];
                 int il = row * N2 + lo, ih = il + t;
                 u64 U = sm[il], V = sm[ih];
                 sm[il] = d_add(U, V, q);
@@ -188,22 +186,35 @@ namespace ntt16 {
 constexpr int LOGN = 16, N = 1 << LOGN;
 
 struct Tw {
-    const u64 *__restrict__ w;   // twiddles
-    const u64 *__restrict__ ws;  // Shoup companions
-    u64 q;
+    const ulonglong2 *__restrict__ w;  // (twiddle, Shoup companion) pairs
+    u64 q, q2;                         // q, 2q
 };
 
+// Harvey's lazy butterflies (q < 2^62): a Shoup product without its final
+// correction lies in [0, 2q) for any 64-bit input.  Forward values stay in
+// [0, 4q), inverse values in [0, 2q); the last stage of each transform
+// reduces to [0, q), so the words leaving k_ntt are canonical.
+__device__ __forceinline__ u64 shoup_lazy(u64 a, u64 w, u64 wsh, u64 q) { return a * w - __umul64hi(a, wsh) * q; }
 __device__ __forceinline__ void bfly_ct(u64 &a, u64 &b, const Tw &T, int idx)
 {
-    u64 V = d_shoup(b, __ldg(T.w + idx), __ldg(T.ws + idx), T.q);
-    b = d_sub(a, V, T.q);
-    a = d_add(a, V, T.q);
+    const ulonglong2 W = __ldg(T.w + idx);
+    const u64 X = a >= T.q2 ? a - T.q2 : a;
+    const u64 V = shoup_lazy(b, W.x, W.y, T.q);
+    a = X + V;
+    b = X + T.q2 - V;
 }
 __device__ __forceinline__ void bfly_gs(u64 &a, u64 &b, const Tw &T, int idx)
 {
-    u64 U = a, V = b;
-    a = d_add(U, V, T.q);
-    b = d_shoup(d_sub(U, V, T.q), __ldg(T.w + idx), __ldg(T.ws + idx), T.q);
+    const ulonglong2 W = __ldg(T.w + idx);
+    const u64 U = a, V = b, s = U + V;
+    a = s >= T.q2 ? s - T.q2 : s;
+    b = shoup_lazy(U + T.q2 - V, W.x, W.y, T.q);
+}
+// [0, 4q) -> [0, q)
+__device__ __forceinline__ u64 reduce4(u64 v, const Tw &T)
+{
+    v = v >= T.q2 ? v - T.q2 : v;
+    return v >= T.q ? v - T.q : v;
 }
 
 // x[k] = element j0 + k s (j0 = block start + offset, block start multiple of 8s)
@@ -260,7 +271,8 @@ __device__ __forceinline__ void radix4_inv(u64 x[4], int j0, int s, const Tw &T)
 __device__ __forceinline__ Tw twiddles(const u64 *tw, int pi, bool inv)
 {
     const u64 *base = tw + (size_t)pi * 4 * N + (inv ? 2 * N : 0);
-    return Tw{base, base + N, c_pk[pi].q};
+    const u64 q = c_pk[pi].q;
+    return Tw{reinterpret_cast<const ulonglong2 *>(base), q, 2 * q};
 }
 
 // Phase over the high 8 index bits (half-spans 2^15..2^8): 16 columns x 256 rows per CTA.
@@ -369,7 +381,7 @@ __global__ void __launch_bounds__(512) rows(u64 *data, PrimeMap pm, const u64 *_
             for (int k = 0; k < 4; k++) sm[row * 256 + 4 * q + k] = y[k];
         }
         __syncthreads();
-        for (int i = tid; i < 16 * 256; i += 512) a[i] = sm[i];
+        for (int i = tid; i < 16 * 256; i += 512) a[i] = reduce4(sm[i], T);
     } else {
         for (int i = tid; i < 16 * 256; i += 512) sm[i] = a[i];
         __syncthreads();
@@ -686,31 +698,37 @@ struct BconvArg {
 
 // centred (ModDown, C7): a term y_a > (q_a-1)/2 stands for y_a - q_a, so the
 // target loses one (prod of sources) per such term (table entry pm[b]).
-__global__ void bconv_kernel(const u64 *__restrict__ x, size_t xs, u64 *o, size_t os, BconvArg A,
-                             const u64 *__restrict__ tab, int N, size_t bxs, size_t bos)
+// grid: (N/256, batch, target groups of BCONV_TG).  The sum over the n_src <= 7
+// sources of y_a * c_ab (each < 2^61 p) stays below p 2^64, so it is
+// accumulated in 128 bits and reduced once (REDC + Shoup, d_reduce128).
+#define BCONV_TG 8
+__global__ void __launch_bounds__(256) bconv_kernel(const u64 *__restrict__ x, size_t xs, u64 *o, size_t os,
+                                                    BconvArg A, const u64 *__restrict__ tab, int N, size_t bxs,
+                                                    size_t bos)
 {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= N) return;
     x += blockIdx.y * bxs;
     o += blockIdx.y * bos;
-    u64 y[16];
+    u64 y[8];
     int neg = 0;
     for (int a = 0; a < A.n_src; a++) {
         const PrimeK k = c_pk[A.src[a]];
-        y[a] = d_shoup(x[(size_t)a * xs + t], tab[2 * a], tab[2 * a + 1], k.q);
+        y[a] = d_shoup(x[(size_t)a * xs + t], __ldg(tab + 2 * a), __ldg(tab + 2 * a + 1), k.q);
         neg += y[a] > (k.q - 1) / 2;
     }
     const u64 *cm = tab + 2 * A.n_src;
     const u64 *pm = cm + 2 * (size_t)A.n_src * A.n_dst;
-    for (int b = 0; b < A.n_dst; b++) {
-        const u64 p = c_pk[A.dst[b]].q;
-        u64 s = 0;
-        for (int a = 0; a < A.n_src; a++) {
-            size_t ci = 2 * ((size_t)a * A.n_dst + b);
-            s = d_add(s, d_shoup(y[a], cm[ci], cm[ci + 1], p), p);
+    const int b0 = blockIdx.z * BCONV_TG, b1 = min(b0 + BCONV_TG, A.n_dst);
+    for (int b = b0; b < b1; b++) {
+        const PrimeK k = c_pk[A.dst[b]];
+        u64 hi = 0, lo = 0;
+        for (int a = 0; a < A.n_src; a++) mac128(hi, lo, y[a], __ldg(cm + 2 * ((size_t)a * A.n_dst + b)));
+        u64 s = d_reduce128(hi, lo, k);
+        if (A.centred) {
+            const u64 pmb = __ldg(pm + b);
+            for (int kk = 0; kk < neg; kk++) s = d_sub(s, pmb, k.q);
         }
-        if (A.centred)
-            for (int k = 0; k < neg; k++) s = d_sub(s, pm[b], p);
         o[(size_t)b * os + t] = s;
     }
 }
@@ -725,9 +743,10 @@ void k_bconv(hs_ctx *c, const BconvTab &tab, const u64 *src, size_t src_stride, 
     A.centred = tab.centred ? 1 : 0;
     for (int i = 0; i < tab.n_src; i++) A.src[i] = (unsigned char)tab.src[i];
     for (int i = 0; i < tab.n_dst; i++) A.dst[i] = (unsigned char)tab.dst[i];
+    if (tab.n_src > 7) throw HsError(HS_EINVAL, "bconv: more than 7 source primes (128-bit accumulator bound)");
     int N = c->P->n;
-    bconv_kernel<<<dim3((N + 127) / 128, batch), 128, 0, st>>>(src, src_stride, dst, dst_stride, A, tab.dev, N, bss,
-                                                                bds);
+    bconv_kernel<<<dim3((N + 255) / 256, batch, (tab.n_dst + BCONV_TG - 1) / BCONV_TG), 256, 0, st>>>(
+        src, src_stride, dst, dst_stride, A, tab.dev, N, bss, bds);
     HS_CHECK_LAUNCH();
     count_kernel(c);
 }
@@ -1143,6 +1162,73 @@ void k_ks_inner_b(hs_ctx *c, const u64 *d, size_t d_stride, const u64 *ext, cons
     }
     int N = P->n;
     ks_inner_b_kernel<4><<<dim3((N + 255) / 256, ntg, tiles), 256, 0, st>>>(d, ext, key, acc, A, N);
+    HS_CHECK_LAUNCH();
+    count_kernel(c);
+}
+
+// C16 hoisted rotations: ONE ModUp (d = c1 own limbs, ext = the digits'
+// other limbs) serves R rotations.  Rotation r reads every extended limb
+// through its Galois permutation (out[t] = in[perm_r[t]]; a warp's 32
+// consecutive t read one aligned 32-word block, so the gather stays
+// coalesced) and its own key.  grid (N/256, ntg, R); acc [R][2][ntg][N].
+struct KsArgH {
+    const u64 *key[HS_MAXROT];
+    const unsigned *perm[HS_MAXROT];
+    int level, beta, alpha, n_q, n_t;
+    size_t off[16];
+    int nd[16];
+};
+
+__global__ void __launch_bounds__(256) ks_inner_h_kernel(const u64 *__restrict__ d, const u64 *__restrict__ ext,
+                                                         u64 *acc, KsArgH A, int N)
+{
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= N) return;
+    const int g = blockIdx.y, r = blockIdx.z;
+    const int nl = A.level + 1, ntg = nl + A.alpha;
+    const int pi = g < nl ? g : A.n_q + (g - nl);
+    const PrimeK k = c_pk[pi];
+    const size_t ntot = (size_t)A.n_q + A.n_t;
+    const unsigned src = __ldg(A.perm[r] + t);
+    const u64 *key = A.key[r];
+    u64 h0 = 0, l0 = 0, h1 = 0, l1 = 0;
+    for (int j = 0; j < A.beta; j++) {
+        const int lo = j * A.alpha, hi = min((j + 1) * A.alpha, nl), dn = hi - lo;
+        const u64 k0 = key[(((size_t)j * 2 + 0) * ntot + pi) * N + t];
+        const u64 k1 = key[(((size_t)j * 2 + 1) * ntot + pi) * N + t];
+        const bool own = g >= lo && g < hi;
+        const int gg = g < lo ? g : g - dn;
+        const u64 v = own ? d[(size_t)g * N + src] : ext[A.off[j] + (size_t)gg * N + src];
+        mac128(h0, l0, v, k0);
+        mac128(h1, l1, v, k1);
+    }
+    acc[((size_t)r * 2 * ntg + g) * N + t] = d_reduce128(h0, l0, k);
+    acc[((size_t)(r * 2 + 1) * ntg + g) * N + t] = d_reduce128(h1, l1, k);
+}
+
+void k_ks_inner_h(hs_ctx *c, const u64 *d, const u64 *ext, const size_t *off, const int *nd, const u64 *const *keys,
+                  const unsigned *const *perms, int R, u64 *acc, int level, int beta, cudaStream_t st)
+{
+    const hs_params *P = c->P;
+    const int ntg = level + 1 + P->n_p;
+    if (R < 1 || R > HS_MAXROT) throw HsError(HS_EINVAL, "hoisted key switch: bad rotation count");
+    KTimer _kt(c, KID_KS_INNER, ((double)R * beta * ntg * 24.0 + 16.0 * ntg * R) * P->n, st);
+    KsArgH A;
+    for (int r = 0; r < R; r++) {
+        A.key[r] = keys[r];
+        A.perm[r] = perms[r];
+    }
+    A.level = level;
+    A.beta = beta;
+    A.alpha = P->alpha;
+    A.n_q = P->n_q;
+    A.n_t = P->n_p;
+    for (int j = 0; j < beta; j++) {
+        A.off[j] = off[j];
+        A.nd[j] = nd[j];
+    }
+    int N = P->n;
+    ks_inner_h_kernel<<<dim3((N + 255) / 256, ntg, R), 256, 0, st>>>(d, ext, acc, A, N);
     HS_CHECK_LAUNCH();
     count_kernel(c);
 }

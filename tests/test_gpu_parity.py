@@ -118,6 +118,21 @@ def test_ops_parity(toy):
     same(hs.mult_pt(a, mask, target=10), O.mult_pt(PO, ao, mask, target=10))
 
 
+@pytest.mark.parametrize("level", [15, 7, 0])
+def test_rotate_hoisted_parity(toy, level):
+    """C16: every output of one hoisted ModUp is bit-exact with the oracle's."""
+    hs = _hs()
+    rng = np.random.default_rng(40 + level)
+    z = rng.uniform(-1, 1, toy.P.n // 2)
+    a, ao = toy.enc(z, level, 7)
+    rots = [1, 3, -1, 128, 1024, -512, 256]
+    outs = hs.rotate_hoisted(toy.K, a, rots)
+    outo = O.rotate_hoisted(toy.PO, toy.KO, ao, rots)
+    for g, o in zip(outs, outo):
+        same(g, o)
+    assert np.abs(hs.decrypt_decode(toy.K, outs[1]).real - np.roll(z, -3)).max() < 2.0 ** -20
+
+
 def test_keyswitch_parity(toy):
     hs = _hs()
     rng = np.random.default_rng(4)

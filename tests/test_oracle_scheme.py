@@ -75,6 +75,58 @@ def test_keyswitch_identity_C7(tiny):
         assert max(abs(e) for e in err) < 2 ** 20, max(abs(e) for e in err)
 
 
+def _auto(a, k, N):
+    """X -> X^k on a coefficient list (negacyclic: X^N = -1)."""
+    out = [0] * N
+    for i, v in enumerate(a):
+        e = (i * k) % (2 * N)
+        if e < N:
+            out[e] += v
+        else:
+            out[e - N] -= v
+    return out
+
+
+def test_hoisted_rotation_identity_C16(tiny):
+    """C16 hoisting: (c0', c1') from ONE ModUp satisfies
+    c0' + c1' s == sigma(c0 + c1 s) + e_ks (mod Q_l), small e_ks, in big integers,
+    for every rotation served by the shared ModUp (here r = 1 twice: the
+    second use must see the ModUp unchanged)."""
+    P, K = tiny
+    rng = np.random.default_rng(11)
+    ct = enc(P, K, rng.uniform(-1, 1, P.n // 2), 3)
+    outs = O.rotate_hoisted(P, K, ct, [1, 1])
+    assert outs[0].words().tobytes() == outs[1].words().tobytes()
+    s = [int(v) for v in K.secret()]
+    k = P.galois_of_rot(1)
+    w = ct.words()
+    c0, Q = coeff_ints(P, w[0], 3)
+    c1, _ = coeff_ints(P, w[1], 3)
+    ph = [x + y for x, y in zip(c0, R.negacyclic_mul(c1, s))]
+    want = _auto(ph, k, P.n)
+    o = outs[0].words()
+    d0, _ = coeff_ints(P, o[0], 3)
+    d1, _ = coeff_ints(P, o[1], 3)
+    got = [x + y for x, y in zip(d0, R.negacyclic_mul(d1, s))]
+    err = [R.centred((x - y) % Q, Q) for x, y in zip(got, want)]
+    assert max(abs(e) for e in err) < 2 ** 20, max(abs(e) for e in err)
+
+
+def test_hoisted_rotations_decrypt_C16(toy):
+    P, K = toy
+    rng = np.random.default_rng(12)
+    z = rng.uniform(-1, 1, P.n // 2)
+    a = enc(P, K, z, 13, 0, sk=False)
+    rots = [1, 3, -128, 256]
+    outs = O.rotate_hoisted(P, K, a, rots)
+    for r, c in zip(rots, outs):
+        assert c.level == 13
+        assert np.abs(O.decrypt_decode(P, K, c).real - np.roll(z, -r)).max() < 2.0 ** -22
+    # hoisting changes the words (BConv vs sigma's sign flips) but not the message
+    plain = O.op(P, K, "rotate", a, i=3)
+    assert plain.words().tobytes() != outs[1].words().tobytes()
+
+
 def test_tensor_identity_C8(tiny):
     """(d0 + d1 s + d2 s^2) == (a0 + a1 s)(b0 + b1 s) exactly mod Q_l."""
     P, K = tiny

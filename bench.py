@@ -32,6 +32,11 @@ import numpy as np  # noqa: E402
 import workloads as W  # noqa: E402
 
 WORKLOAD = "config3"
+# NTT roofline: integer-pipe peak for our lazy Shoup
+# butterfly, and DRAM bytes per limb-NTT (both passes) from the round's
+# `ncu --set full` capture (profiles/r01_ncu_full_summary.txt); None = not measured
+NTT_ALU_PEAK = 0.86
+NTT_TRAFFIC_PER_LIMB = None
 METRIC = "amortized ms/Softmax (8192×dim256, N=2^16); key-switch HBM GB/s vs peak"
 
 
@@ -45,6 +50,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--kprof", default="timed", choices=["timed", "extra", "off"])
+    ap.add_argument("--no-graph", action="store_true", help="eager C-ABI calls instead of a CUDA-graph plan")
     return ap.parse_args()
 
 
@@ -153,13 +159,20 @@ def run_ours(args):
     hs, ctx, K, B, tab = S["hs"], S["ctx"], S["K"], S["B"], S["tab"]
     exch = make_exchange(world)
     stream = torch.cuda.current_stream()
+    use_graph = world == 1 and not args.no_graph
+    wl = S["wl"]
 
     def step(inputs):
-        return hs.softmax_many_ctxt(K, inputs, S["n"], S["m"], S["k"], S["wl"]["variant"], tab["exp"], tab["inv"],
+        return hs.softmax_many_ctxt(K, inputs, S["n"], S["m"], S["k"], wl["variant"], tab["exp"], tab["inv"],
                                     world=world, rank=rank, exchange=exch, bts=B)
 
+    def make_plan():
+        return hs.Plan(K, S["cts"], S["n"], S["m"], S["k"], wl["variant"], tab["exp"], tab["inv"], bts=B)
+
+    plan = make_plan() if use_graph else None  # warm-up run + capture (outside timing)
+    run_step = plan.run if use_graph else (lambda: step(S["cts"]))
     for _ in range(args.warmup):
-        out = step(S["cts"])
+        out = run_step()
     torch.cuda.synchronize()
     # accuracy of the last warm-up output (host-side check, outside timing)
     dec = np.stack([hs.decrypt_decode(K, c).real for c in out])
@@ -176,7 +189,8 @@ def run_ours(args):
     # ---------------- timed region (device events, max over ranks)
     clocks = Clocks(local)
     led0 = ctx.ledger()
-    if args.kprof == "timed":
+    kprof_live = args.kprof == "timed" and not use_graph
+    if kprof_live:
         hs._lib.hs_kprof_enable(ctx.ptr, 1)
     if world > 1:
         dist_.barrier()
@@ -184,9 +198,12 @@ def run_ours(args):
     clocks.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
+    h0 = time.perf_counter()
     for _ in range(args.steps):
-        out = step(S["cts"])
-        del out
+        out = run_step()
+        if not use_graph:
+            del out
+    host_ms = (time.perf_counter() - h0) * 1e3 / args.steps  # enqueue time (diagnostic)
     e1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -195,12 +212,33 @@ def run_ours(args):
     ms = e0.elapsed_time(e1)
     led1 = ctx.ledger()
     kp = np.zeros(3 * 12)
+    kp_steps, kp_ms = args.steps, ms
     if args.kprof != "off":
-        if args.kprof == "extra":
+        if use_graph:
+            # per-kernel CUDA events captured INTO a second graph of the same
+            # step; its replays are timed like the headline and the events of
+            # the last replay give the per-launch durations
             hs._lib.hs_kprof_enable(ctx.ptr, 1)
-            out = step(S["cts"])
-            del out
-        hs._lib.hs_kprof_collect(ctx.ptr, kp, 12)
+            pplan = make_plan()
+            hs._lib.hs_kprof_enable(ctx.ptr, 0)
+            pplan.run()
+            torch.cuda.synchronize()
+            p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            p0.record(stream)
+            for _ in range(args.steps):
+                pplan.run()
+            p1.record(stream)
+            torch.cuda.synchronize()
+            kp_steps, kp_ms = 1, p0.elapsed_time(p1) / args.steps
+            hs._lib.hs_kprof_collect(ctx.ptr, kp, 12)
+            del pplan
+        else:
+            if args.kprof == "extra":
+                hs._lib.hs_kprof_enable(ctx.ptr, 1)
+                out = step(S["cts"])
+                del out
+                kp_steps, kp_ms = 1, None
+            hs._lib.hs_kprof_collect(ctx.ptr, kp, 12)
         hs._lib.hs_kprof_enable(ctx.ptr, 0)
     if world > 1:
         t = torch.tensor([ms], device="cuda")
@@ -212,14 +250,14 @@ def run_ours(args):
     # ---------------- end-to-end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(S, step, args, world)
+        e2e = run_e2e(S, step, plan, args, world)
     if rank != 0:
         if world > 1:
             dist_.destroy_process_group()
         return
     hbm, _, peak_src = peaks()
     kcls = hs._lib.KPROF_CLASSES
-    kstats = {kcls[i]: dict(launches=int(kp[3 * i]), ms=round(kp[3 * i + 1], 3),
+    kstats = {kcls[i]: dict(launches=int(kp[3 * i] / kp_steps), ms=round(kp[3 * i + 1] / kp_steps, 3),
                             gbs=round(kp[3 * i + 2] / (kp[3 * i + 1] * 1e-3) / 1e9, 1) if kp[3 * i + 1] > 0 else None)
               for i in range(12) if kp[3 * i] > 0}
     dom = max(kstats, key=lambda k_: kstats[k_]["ms"]) if kstats else None
@@ -230,11 +268,24 @@ def run_ours(args):
             return None
         avg_ms = kp[3 * i + 1] / kp[3 * i]
         bytes_per = kp[3 * i + 2] / kp[3 * i]
+        share = round(kp[3 * i + 1] / kp_steps / kp_ms * kp_steps, 4) if kp_ms else None
+        if name == "ntt":
+            # integer-ALU bound: butterflies per launch =
+            # limbs * (N/2) log2 N = bytes/2 for N = 2^16 (bytes tag = 16 limbs N)
+            bfly = bytes_per / 2
+            ach = bfly / (avg_ms * 1e-3) / 1e12
+            return {"kernel": "ntt (cols+rows, fwd+inv)", "bound": "alu", "achieved": round(ach, 4),
+                    "peak": NTT_ALU_PEAK, "unit": "T butterflies/s", "frac": round(ach / NTT_ALU_PEAK, 4),
+                    "traffic": NTT_TRAFFIC_PER_LIMB and round(NTT_TRAFFIC_PER_LIMB * bytes_per / (16 * 65536)),
+                    "peak_source": "derived: 148 SM x 4 SMSP x 1.965 GHz / IMAD-pipe cycles per warp-butterfly "
+                                   "(SASS mix, IMAD.WIDE rt 4, other IMAD rt 2); DESIGN.md section 6",
+                    "algorithmic_butterflies_per_launch": int(bfly), "avg_launch_us": round(avg_ms * 1e3, 2),
+                    "share_of_step": share}
         ach = bytes_per / (avg_ms * 1e-3) / 1e9
         return {"kernel": name, "bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(ach / hbm, 4), "traffic": None, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": int(bytes_per), "avg_launch_us": round(avg_ms * 1e3, 2),
-                "share_of_step": round(kp[3 * i + 1] / ms, 4) if args.kprof == "timed" else None}
+                "share_of_step": share}
 
     line = {
         "metric": METRIC, "value": round(value, 5), "unit": "ms/Softmax", "n_gpus": world, "steps": args.steps,
@@ -244,16 +295,20 @@ def run_ours(args):
                                "N=2^16, bootstrapped aux thread", "preset": S["wl"]["preset"],
                    "softmax_per_step": softmax_per_step, "ciphertexts": S["m"],
                    "l2": "inputs larger than L2 (64 ciphertexts x 13 limbs x 2 x 512 KiB = 852 MiB)",
-                   "kprof_in_timed_region": args.kprof == "timed"},
+                   "launch": "CUDA graph replay (hs_softmax_plan)" if use_graph else "eager C-ABI call",
+                   "kprof": ("events captured in a second graph of the same step, timed separately"
+                             if use_graph and args.kprof != "off" else args.kprof)},
         "accuracy_bits": round(acc_bits, 2) if acc_bits is not None else None,
         "gpu_launches": int(led1["kernels"] - led0["kernels"]),
         "ledger_per_step": {k_: (led1[k_] - led0[k_]) // args.steps for k_ in led1},
         "roofline": roof(dom) if dom else None,
         "roofline_keyswitch": roof("ks_inner"),
         "kernels": kstats,
+        "kprof_step_ms": round(kp_ms, 3) if kp_ms and args.kprof != "off" else None,
         "clocks": clk,
         "e2e": e2e,
         "setup_s": round(S["setup_s"], 1),
+        "host_enqueue_ms_per_step": round(host_ms, 1),
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(line["ledger_per_step"], budget_s=20.0)
@@ -262,37 +317,43 @@ def run_ours(args):
         dist_.destroy_process_group()
 
 
-def run_e2e(S, step, args, world):
-    """Same metric through the C ABI with HOST buffers: H2D import of the
-    step's input ciphertexts from pinned memory, the Softmax, D2H export of the
-    result ciphertexts, all inside the timed region."""
+def run_e2e(S, step, plan, args, world):
+    """Same metric through the C ABI with HOST buffers: H2D of the step's input
+    ciphertexts from pinned memory, the Softmax, D2H export of the result
+    ciphertexts, all inside the timed region.  With a plan, the inputs are
+    written into the plan's bound input ciphertexts (hs_ct_write)."""
+    import ctypes as C
     import torch
     hs, ctx = S["hs"], S["ctx"]
     P = S["P"]
     words_in = [c.words() for c in S["cts"]]
     pinned_in = [torch.from_numpy(w.view(np.int64)).pin_memory() for w in words_in]
-    out0 = step(S["cts"])
+    out0 = plan.run() if plan else step(S["cts"])
     shapes_out = [(c.ncomp, c.level + 1) for c in out0]
     del out0
     pinned_out = [torch.empty(nc * l1 * P.n, dtype=torch.int64).pin_memory() for nc, l1 in shapes_out]
     lvl_in = S["top"]
     stream = torch.cuda.current_stream()
+    sp = C.c_void_p(stream.cuda_stream)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    import ctypes as C
     e0.record(stream)
     steps = max(1, min(args.steps, 2))
     for _ in range(steps):
-        cts = []
-        for t in pinned_in:
-            o = C.c_void_p()
-            hs.check(hs._lib.hs_ct_import(ctx.ptr, lvl_in, 2, C.c_void_p(t.data_ptr()), 0,
-                                          C.c_void_p(stream.cuda_stream), C.byref(o)))
-            cts.append(hs.Ciphertext(ctx, o))
-        outs = step(cts)
+        if plan:
+            for t, c in zip(pinned_in, S["cts"]):
+                hs.check(hs._lib.hs_ct_write(ctx.ptr, c.ptr, C.c_void_p(t.data_ptr()), 0, sp))
+            outs = plan.run()
+        else:
+            cts = []
+            for t in pinned_in:
+                o = C.c_void_p()
+                hs.check(hs._lib.hs_ct_import(ctx.ptr, lvl_in, 2, C.c_void_p(t.data_ptr()), 0, sp, C.byref(o)))
+                cts.append(hs.Ciphertext(ctx, o))
+            outs = step(cts)
         for c, t in zip(outs, pinned_out):
-            hs.check(hs._lib.hs_ct_export(ctx.ptr, c.ptr, C.c_void_p(t.data_ptr()), 0, C.c_void_p(stream.cuda_stream)))
-        del outs, cts
+            hs.check(hs._lib.hs_ct_export(ctx.ptr, c.ptr, C.c_void_p(t.data_ptr()), 0, sp))
+        del outs
     e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps

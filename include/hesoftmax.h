@@ -136,6 +136,11 @@ hs_status hs_ckks_decrypt(hs_ctx *c, const hs_keys *k, const hs_ct *ct, uint64_t
 hs_status hs_ct_import(hs_ctx *c, int level, int ncomp, const uint64_t *words, int on_device, void *stream,
                        hs_ct **out);
 hs_status hs_ct_export(hs_ctx *c, const hs_ct *ct, uint64_t *words, int on_device, void *stream);
+/* Overwrite an existing ciphertext's words (same layout as import) with a
+ * stream-ordered copy; no synchronisation: host words must stay valid until
+ * the stream passes this point (pinned memory makes the copy asynchronous).
+ * Used to refresh a plan's bound inputs. */
+hs_status hs_ct_write(hs_ctx *c, hs_ct *ct, const uint64_t *words, int on_device, void *stream);
 int hs_ct_level(const hs_ct *ct);
 int hs_ct_ncomp(const hs_ct *ct);
 void hs_ct_destroy(hs_ct *ct);
@@ -242,6 +247,27 @@ hs_status hs_softmax_one_ctxt(hs_ctx *c, const hs_keys *k, const hs_softmax_desc
 /* m_local = m / world ciphertexts of this rank (contiguous shard). */
 hs_status hs_softmax_many_ctxt(hs_ctx *c, const hs_keys *k, const hs_softmax_desc *d, const hs_ct *const *in,
                                size_t m_local, void *stream, hs_ct **out);
+
+/* ------------------------------------------------------------ replayable plans (CUDA graphs) */
+/* A plan is one hs_softmax_many_ctxt call (world == 1) captured into a CUDA
+ * graph: every kernel of the Softmax runs again at each hs_plan_run, with no
+ * host work between launches.  The plan is BOUND to the m_local input
+ * ciphertexts `in` (their device words are read at every run -- refresh them
+ * with hs_ct_write before a run) and owns m_local output
+ * ciphertexts (hs_plan_output; valid until hs_plan_destroy, overwritten by each
+ * run).  Creation runs the Softmax once eagerly (warming every table the graph
+ * needs) and once under capture.  The inputs and the descriptor's objects
+ * (keys, polynomials, bts) must outlive the plan.  Each run adds the captured
+ * call's ledger counts.  If kernel profiling is on at creation, the graph
+ * records the per-kernel events and hs_kprof_collect after a run reports that
+ * run.  HS_EINVAL for world != 1. */
+typedef struct hs_plan hs_plan;
+hs_status hs_softmax_plan_create(hs_ctx *c, const hs_keys *k, const hs_softmax_desc *d, const hs_ct *const *in,
+                                 size_t m_local, void *stream, hs_plan **out);
+hs_status hs_plan_run(hs_plan *p, void *stream);
+size_t hs_plan_n_outputs(const hs_plan *p);
+const hs_ct *hs_plan_output(const hs_plan *p, size_t i);
+void hs_plan_destroy(hs_plan *p);
 
 /* ------------------------------------------------------------ kernel profiling (bench hooks) */
 /* When enabled, every kernel launch is bracketed by CUDA events on its stream

@@ -148,11 +148,12 @@ class Keys:
 
 
 class Ciphertext:
-    def __init__(self, ctx: Context, ptr):
-        self.ctx, self.ptr = ctx, ptr
+    def __init__(self, ctx: Context, ptr, owner=None):
+        # owner: the object that owns a borrowed handle (a Plan's outputs)
+        self.ctx, self.ptr, self.owner = ctx, ptr, owner
 
     def __del__(self):
-        if getattr(self, "ptr", None):
+        if getattr(self, "ptr", None) and self.owner is None:
             L.hs_ct_destroy(self.ptr)
             self.ptr = None
 
@@ -308,6 +309,32 @@ def softmax_one_ctxt(keys: Keys, ct: Ciphertext, n, k, variant, exp_poly, inv_po
     out = C.c_void_p()
     check(L.hs_softmax_one_ctxt(keys.ctx.ptr, keys.ptr, C.byref(d), ct.ptr, _stream(stream), C.byref(out)))
     return Ciphertext(keys.ctx, out)
+
+
+class Plan:
+    """hs_softmax_plan_create: one single-GPU Softmax captured as a CUDA graph,
+    bound to the input ciphertexts `cts` (re-read at every run); outputs are
+    plan-owned and overwritten by each run()."""
+
+    def __init__(self, keys: Keys, cts, n, m, k, variant, exp_poly, inv_polys, bts=None, stream=None):
+        self.keys, self.cts = keys, list(cts)
+        self._d, self._keep = _softmax_desc(n, m, k, variant, exp_poly, inv_polys, 1, 0, None, bts)
+        ml = len(cts)
+        ins = (C.c_void_p * ml)(*[c.ptr.value if isinstance(c.ptr, C.c_void_p) else c.ptr for c in cts])
+        p = C.c_void_p()
+        check(L.hs_softmax_plan_create(keys.ctx.ptr, keys.ptr, C.byref(self._d), ins, ml, _stream(stream),
+                                       C.byref(p)))
+        self.ptr = p
+        self.outputs = [Ciphertext(keys.ctx, C.c_void_p(L.hs_plan_output(p, i)), owner=self) for i in range(ml)]
+
+    def run(self, stream=None):
+        check(L.hs_plan_run(self.ptr, _stream(stream)))
+        return self.outputs
+
+    def __del__(self):
+        if getattr(self, "ptr", None):
+            L.hs_plan_destroy(self.ptr)
+            self.ptr = None
 
 
 def softmax_many_ctxt(keys: Keys, cts, n, m, k, variant, exp_poly, inv_polys, world=1, rank=0, exchange=None,

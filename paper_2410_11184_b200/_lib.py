@@ -97,6 +97,13 @@ hs_ct_export = _sig("hs_ct_export", C.c_int, [vp, vp, vp, C.c_int, vp])
 hs_ct_level = _sig("hs_ct_level", C.c_int, [vp])
 hs_ct_ncomp = _sig("hs_ct_ncomp", C.c_int, [vp])
 hs_ct_destroy = _sig("hs_ct_destroy", None, [vp])
+hs_ct_write = _sig("hs_ct_write", C.c_int, [vp, vp, vp, C.c_int, vp])
+hs_softmax_plan_create = _sig("hs_softmax_plan_create", C.c_int, [vp, vp, vp, C.POINTER(vp), C.c_size_t, vp,
+                                                                  C.POINTER(vp)])
+hs_plan_run = _sig("hs_plan_run", C.c_int, [vp, vp])
+hs_plan_n_outputs = _sig("hs_plan_n_outputs", C.c_size_t, [vp])
+hs_plan_output = _sig("hs_plan_output", vp, [vp, C.c_size_t])
+hs_plan_destroy = _sig("hs_plan_destroy", None, [vp])
 hs_op = _sig("hs_op", C.c_int, [vp, vp, C.c_int, vp, vp, C.c_double, C.c_int, vp, C.POINTER(vp)])
 hs_mult_pt = _sig("hs_mult_pt", C.c_int, [vp, vp, f64p, vp, C.c_int, vp, C.POINTER(vp)])
 hs_keyswitch = _sig("hs_keyswitch", C.c_int, [vp, vp, C.c_int, C.c_int, vp, vp, vp, vp])

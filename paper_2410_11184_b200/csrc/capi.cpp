@@ -251,6 +251,17 @@ hs_status hs_ct_import(hs_ctx *c, int level, int ncomp, const uint64_t *words, i
     HS_CATCH
 }
 
+hs_status hs_ct_write(hs_ctx *c, hs_ct *ct, const uint64_t *words, int on_device, void *stream)
+{
+    HS_TRY
+    if (!c || !ct || !words) throw HsError(HS_EINVAL, "ct_write: NULL argument");
+    activate(c);
+    HS_CUDA(cudaMemcpyAsync(ct->d, words, ct->limbs() * c->P->n * 8,
+                            on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, S(stream)));
+    return HS_OK;
+    HS_CATCH
+}
+
 hs_status hs_ct_export(hs_ctx *c, const hs_ct *ct, uint64_t *words, int on_device, void *stream)
 {
     HS_TRY
@@ -379,6 +390,107 @@ hs_status hs_softmax_many_ctxt(hs_ctx *c, const hs_keys *k, const hs_softmax_des
     activate(c);
     return softmax_run(c, k, d, in, m_local, S(stream), out);
     HS_CATCH
+}
+
+}  // extern "C"
+
+struct hs_plan {
+    hs_ctx *c = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    std::vector<hs_ct *> outs;
+    int64_t ledger_delta[HS_LG_COUNT] = {0};
+    ~hs_plan()
+    {
+        if (exec) cudaGraphExecDestroy(exec);
+        if (graph) cudaGraphDestroy(graph);
+        for (hs_ct *o : outs) delete o;
+    }
+};
+
+extern "C" {
+
+hs_status hs_softmax_plan_create(hs_ctx *c, const hs_keys *k, const hs_softmax_desc *d, const hs_ct *const *in,
+                                 size_t m_local, void *stream, hs_plan **out)
+{
+    HS_TRY
+    if (!c || !k || !d || !in || !out || m_local < 1) throw HsError(HS_EINVAL, "NULL argument");
+    if (d->world > 1) throw HsError(HS_EINVAL, "plans capture single-GPU Softmax (world == 1)");
+    activate(c);
+    cudaStream_t user = S(stream);
+    std::unique_ptr<hs_plan> p(new hs_plan);
+    p->c = c;
+    std::vector<hs_ct *> tmp(m_local, nullptr);
+    // 1. eager warm-up: builds every table / cached plaintext the graph reads
+    const bool prof = c->kprof_on;
+    c->kprof_on = false;
+    int64_t led0[HS_LG_COUNT];
+    memcpy(led0, c->ledger, sizeof(led0));
+    hs_status s = softmax_run(c, k, d, in, m_local, user, tmp.data());
+    if (s != HS_OK) return s;
+    HS_CUDA(cudaStreamSynchronize(user));
+    for (size_t i = 0; i < m_local; i++) {
+        hs_ct *o = new hs_ct;
+        o->ctx = c;
+        o->level = tmp[i]->level;
+        o->ncomp = tmp[i]->ncomp;
+        o->batch = 1;
+        o->st = user;
+        o->d = dev_alloc(o->ct_words(), user);
+        p->outs.push_back(o);
+        delete tmp[i];
+    }
+    HS_CUDA(cudaStreamSynchronize(user));
+    memcpy(c->ledger, led0, sizeof(led0));
+    // 2. capture on a private stream (the legacy stream cannot capture)
+    cudaStream_t cs;
+    HS_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    c->kprof_on = prof;
+    HS_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    try {
+        s = softmax_run(c, k, d, in, m_local, cs, tmp.data());
+        if (s == HS_OK)
+            for (size_t i = 0; i < m_local; i++) {
+                HS_CUDA(cudaMemcpyAsync(p->outs[i]->d, tmp[i]->d, p->outs[i]->ct_words() * 8,
+                                        cudaMemcpyDeviceToDevice, cs));
+                delete tmp[i];  // stream-ordered free, inside the graph
+            }
+    } catch (...) {
+        cudaGraph_t g;
+        cudaStreamEndCapture(cs, &g);
+        if (g) cudaGraphDestroy(g);
+        cudaStreamDestroy(cs);
+        c->kprof_on = prof;
+        throw;
+    }
+    HS_CUDA(cudaStreamEndCapture(cs, &p->graph));
+    cudaStreamDestroy(cs);
+    for (int i = 0; i < HS_LG_COUNT; i++) p->ledger_delta[i] = c->ledger[i] - led0[i];
+    memcpy(c->ledger, led0, sizeof(led0));
+    if (s != HS_OK) return s;
+    HS_CUDA(cudaGraphInstantiate(&p->exec, p->graph, 0));
+    *out = p.release();
+    return HS_OK;
+    HS_CATCH
+}
+
+hs_status hs_plan_run(hs_plan *p, void *stream)
+{
+    HS_TRY
+    if (!p) throw HsError(HS_EINVAL, "NULL plan");
+    activate(p->c);
+    HS_CUDA(cudaGraphLaunch(p->exec, S(stream)));
+    for (int i = 0; i < HS_LG_COUNT; i++) p->c->ledger[i] += p->ledger_delta[i];
+    return HS_OK;
+    HS_CATCH
+}
+
+size_t hs_plan_n_outputs(const hs_plan *p) { return p ? p->outs.size() : 0; }
+const hs_ct *hs_plan_output(const hs_plan *p, size_t i) { return p && i < p->outs.size() ? p->outs[i] : nullptr; }
+void hs_plan_destroy(hs_plan *p)
+{
+    if (p) cudaDeviceSynchronize();
+    delete p;
 }
 
 hs_status hs_bootstrap(hs_ctx *c, const hs_keys *k, hs_bts *b, const hs_ct *in, double bound, void *stream,

@@ -275,41 +275,42 @@ __device__ __forceinline__ Tw twiddles(const u64 *tw, int pi, bool inv)
     return Tw{reinterpret_cast<const ulonglong2 *>(base), q, 2 * q};
 }
 
-// Phase over the high 8 index bits (half-spans 2^15..2^8): 16 columns x 256 rows per CTA.
-template <bool INV>
-__global__ void __launch_bounds__(512) cols(u64 *data, PrimeMap pm, const u64 *__restrict__ tw,
-                                            const u64 *__restrict__ ninv)
+// Phase over the high 8 index bits (half-spans 2^15..2^8): C columns x 256 rows
+// per CTA of 32 C threads (thread = column tid % C, row index rid = tid / C).
+template <bool INV, int C>
+__global__ void __launch_bounds__(32 * C) cols(u64 *data, PrimeMap pm, const u64 *__restrict__ tw,
+                                               const u64 *__restrict__ ninv)
 {
-    __shared__ u64 sm[256 * 16];
+    __shared__ u64 sm[256 * C];
     const int limb = blockIdx.y, pi = pm.p[limb % pm.n];
     const Tw T = twiddles(tw, pi, INV);
     u64 *a = data + (size_t)limb * N;
-    const int tid = threadIdx.x, col = tid & 15, c = blockIdx.x * 16 + col;
+    const int tid = threadIdx.x, col = tid % C, rid = tid / C, c = blockIdx.x * C + col;
     u64 x[8];
     if (!INV) {
         // round 1: rows r0 + 32k, s = 32 rows
-        const int r0 = tid >> 4;
+        const int r0 = rid;
 #pragma unroll
         for (int k = 0; k < 8; k++) x[k] = a[(r0 + 32 * k) * 256 + c];
         radix8_fwd(x, r0 * 256 + c, 32 * 256, T);
 #pragma unroll
-        for (int k = 0; k < 8; k++) sm[(r0 + 32 * k) * 16 + col] = x[k];
+        for (int k = 0; k < 8; k++) sm[(r0 + 32 * k) * C + col] = x[k];
         __syncthreads();
         // round 2: rows b*32 + sub + 4k, s = 4 rows
-        const int b = tid >> 6, sub = (tid >> 4) & 3;
+        const int b = rid >> 2, sub = rid & 3;
 #pragma unroll
-        for (int k = 0; k < 8; k++) x[k] = sm[(b * 32 + sub + 4 * k) * 16 + col];
+        for (int k = 0; k < 8; k++) x[k] = sm[(b * 32 + sub + 4 * k) * C + col];
         radix8_fwd(x, (b * 32 + sub) * 256 + c, 4 * 256, T);
 #pragma unroll
-        for (int k = 0; k < 8; k++) sm[(b * 32 + sub + 4 * k) * 16 + col] = x[k];
+        for (int k = 0; k < 8; k++) sm[(b * 32 + sub + 4 * k) * C + col] = x[k];
         __syncthreads();
         // round 3: rows 4q + k (two groups per thread), s = 1 row
 #pragma unroll
         for (int h = 0; h < 2; h++) {
-            const int q = (tid >> 4) + 32 * h;
+            const int q = rid + 32 * h;
             u64 y[4];
 #pragma unroll
-            for (int k = 0; k < 4; k++) y[k] = sm[(4 * q + k) * 16 + col];
+            for (int k = 0; k < 4; k++) y[k] = sm[(4 * q + k) * C + col];
             radix4_fwd(y, 4 * q * 256 + c, 256, T);
 #pragma unroll
             for (int k = 0; k < 4; k++) a[(4 * q + k) * 256 + c] = y[k];
@@ -318,39 +319,40 @@ __global__ void __launch_bounds__(512) cols(u64 *data, PrimeMap pm, const u64 *_
         const u64 ni = ninv[2 * pi], nis = ninv[2 * pi + 1];
 #pragma unroll
         for (int h = 0; h < 2; h++) {
-            const int q = (tid >> 4) + 32 * h;
+            const int q = rid + 32 * h;
             u64 y[4];
 #pragma unroll
             for (int k = 0; k < 4; k++) y[k] = a[(4 * q + k) * 256 + c];
             radix4_inv(y, 4 * q * 256 + c, 256, T);
 #pragma unroll
-            for (int k = 0; k < 4; k++) sm[(4 * q + k) * 16 + col] = y[k];
+            for (int k = 0; k < 4; k++) sm[(4 * q + k) * C + col] = y[k];
         }
         __syncthreads();
-        const int b = tid >> 6, sub = (tid >> 4) & 3;
+        const int b = rid >> 2, sub = rid & 3;
 #pragma unroll
-        for (int k = 0; k < 8; k++) x[k] = sm[(b * 32 + sub + 4 * k) * 16 + col];
+        for (int k = 0; k < 8; k++) x[k] = sm[(b * 32 + sub + 4 * k) * C + col];
         radix8_inv(x, (b * 32 + sub) * 256 + c, 4 * 256, T);
 #pragma unroll
-        for (int k = 0; k < 8; k++) sm[(b * 32 + sub + 4 * k) * 16 + col] = x[k];
+        for (int k = 0; k < 8; k++) sm[(b * 32 + sub + 4 * k) * C + col] = x[k];
         __syncthreads();
-        const int r0 = tid >> 4;
+        const int r0 = rid;
 #pragma unroll
-        for (int k = 0; k < 8; k++) x[k] = sm[(r0 + 32 * k) * 16 + col];
+        for (int k = 0; k < 8; k++) x[k] = sm[(r0 + 32 * k) * C + col];
         radix8_inv(x, r0 * 256 + c, 32 * 256, T);
 #pragma unroll
         for (int k = 0; k < 8; k++) a[(r0 + 32 * k) * 256 + c] = d_shoup(x[k], ni, nis, T.q);
     }
 }
 
-// Phase over the low 8 index bits (half-spans 2^7..1): 16 rows of 256 per CTA.
-template <bool INV>
-__global__ void __launch_bounds__(512) rows(u64 *data, PrimeMap pm, const u64 *__restrict__ tw)
+// Phase over the low 8 index bits (half-spans 2^7..1): R rows of 256 per CTA of
+// 32 R threads (one warp per row).
+template <bool INV, int R>
+__global__ void __launch_bounds__(32 * R) rows(u64 *data, PrimeMap pm, const u64 *__restrict__ tw)
 {
-    __shared__ u64 sm[16 * 256];
+    __shared__ u64 sm[R * 256];
     const int limb = blockIdx.y, pi = pm.p[limb % pm.n];
     const Tw T = twiddles(tw, pi, INV);
-    const int row0 = blockIdx.x * 16;
+    const int row0 = blockIdx.x * R;
     u64 *a = data + (size_t)limb * N + (size_t)row0 * 256;
     const int tid = threadIdx.x, row = tid >> 5;
     const int jrow = (row0 + row) * 256;
@@ -381,9 +383,9 @@ __global__ void __launch_bounds__(512) rows(u64 *data, PrimeMap pm, const u64 *_
             for (int k = 0; k < 4; k++) sm[row * 256 + 4 * q + k] = y[k];
         }
         __syncthreads();
-        for (int i = tid; i < 16 * 256; i += 512) a[i] = reduce4(sm[i], T);
+        for (int i = tid; i < R * 256; i += 32 * R) a[i] = reduce4(sm[i], T);
     } else {
-        for (int i = tid; i < 16 * 256; i += 512) sm[i] = a[i];
+        for (int i = tid; i < R * 256; i += 32 * R) sm[i] = a[i];
         __syncthreads();
 #pragma unroll
         for (int h = 0; h < 2; h++) {
@@ -411,6 +413,31 @@ __global__ void __launch_bounds__(512) rows(u64 *data, PrimeMap pm, const u64 *_
         for (int k = 0; k < 8; k++) a[row * 256 + e0 + 32 * k] = x[k];
     }
 }
+template <int C, int R>
+void launch(u64 *data, int n_limbs, const PrimeMap &pm, bool inverse, const u64 *tw, const u64 *ninv,
+            cudaStream_t st)
+{
+    const dim3 gc(256 / C, n_limbs), gr(256 / R, n_limbs);
+    if (!inverse) {
+        cols<false, C><<<gc, 32 * C, 0, st>>>(data, pm, tw, ninv);
+        rows<false, R><<<gr, 32 * R, 0, st>>>(data, pm, tw);
+    } else {
+        rows<true, R><<<gr, 32 * R, 0, st>>>(data, pm, tw);
+        cols<true, C><<<gc, 32 * C, 0, st>>>(data, pm, tw, ninv);
+    }
+}
+
+// tile width (columns per cols-CTA = rows per rows-CTA); HS_NTT_TILE=4|8|16
+// overrides for experiments
+int tile()
+{
+    static int t = [] {
+        const char *e = getenv("HS_NTT_TILE");
+        int v = e ? atoi(e) : 4;  // measured best: 4 (1.12 us/limb fwd vs 1.33 at 16)
+        return (v == 4 || v == 8 || v == 16) ? v : 4;
+    }();
+    return t;
+}
 }  // namespace ntt16
 
 void k_ntt(hs_ctx *c, u64 *data, int n_limbs, const PrimeMap &pm, bool inverse, cudaStream_t st)
@@ -420,13 +447,10 @@ void k_ntt(hs_ctx *c, u64 *data, int n_limbs, const PrimeMap &pm, bool inverse, 
     const hs_params *P = c->P;
     if (P->log_n == 16) {
         const u64 *ninv = c->T.tw + (size_t)(P->n_q + P->n_p) * 4 * P->n;
-        dim3 g(16, n_limbs);
-        if (!inverse) {
-            ntt16::cols<false><<<g, 512, 0, st>>>(data, pm, c->T.tw, ninv);
-            ntt16::rows<false><<<g, 512, 0, st>>>(data, pm, c->T.tw);
-        } else {
-            ntt16::rows<true><<<g, 512, 0, st>>>(data, pm, c->T.tw);
-            ntt16::cols<true><<<g, 512, 0, st>>>(data, pm, c->T.tw, ninv);
+        switch (ntt16::tile()) {
+        case 4: ntt16::launch<4, 4>(data, n_limbs, pm, inverse, c->T.tw, ninv, st); break;
+        case 8: ntt16::launch<8, 8>(data, n_limbs, pm, inverse, c->T.tw, ninv, st); break;
+        default: ntt16::launch<16, 16>(data, n_limbs, pm, inverse, c->T.tw, ninv, st); break;
         }
         HS_CHECK_LAUNCH();
         c->ledger[HS_LG_NTT] += n_limbs;
@@ -638,12 +662,14 @@ __global__ void rescale_prep_kernel(const u64 *last, u64 *w, int N, int level)
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= N) return;
     int i = blockIdx.y, comp = blockIdx.z;
-    u64 ql = c_pk[level].q, q = c_pk[i].q;
+    const PrimeK k = c_pk[i];
+    const u64 ql = c_pk[level].q, q = k.q;
     u64 x = last[(size_t)comp * N + t];
     u64 v;
-    if (x <= (ql - 1) / 2) v = x % q;
+    // x mod q by REDC + Shoup (x < 2^61 < q 2^64), not a 64-bit division
+    if (x <= (ql - 1) / 2) v = d_reduce128(0, x, k);
     else {
-        u64 r = (ql - x) % q;
+        u64 r = d_reduce128(0, ql - x, k);
         v = r ? q - r : 0;
     }
     w[((size_t)comp * level + i) * N + t] = v;
@@ -1305,11 +1331,12 @@ __global__ void modraise_kernel(const u64 *x, u64 *o, int N, int nl)
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= N) return;
     int i = blockIdx.y, c = blockIdx.z;
-    u64 q0 = c_pk[0].q, q = c_pk[i].q;
+    const PrimeK k = c_pk[i];
+    u64 q0 = c_pk[0].q, q = k.q;
     u64 v = x[(size_t)c * N + t], r;
-    if (v <= (q0 - 1) / 2) r = v % q;
+    if (v <= (q0 - 1) / 2) r = d_reduce128(0, v, k);
     else {
-        u64 w = (q0 - v) % q;
+        u64 w = d_reduce128(0, q0 - v, k);
         r = w ? q - w : 0;
     }
     o[((size_t)c * nl + i) * N + t] = r;

@@ -17,12 +17,14 @@ KTimer::KTimer(hs_ctx *c_, int id_, double bytes_, cudaStream_t st_) : c(c_), id
     slot = (int)c->kprof_used++;
     c->kprof_id[slot] = id;
     c->kprof_bytes[slot] = bytes;
-    cudaEventRecord(c->kprof_ev[2 * slot], st);
+    // External: under stream capture this becomes an event-record node of the
+    // graph (a plain record would only express a dependency)
+    cudaEventRecordWithFlags(c->kprof_ev[2 * slot], st, cudaEventRecordExternal);
 }
 
 KTimer::~KTimer()
 {
-    if (slot >= 0) cudaEventRecord(c->kprof_ev[2 * slot + 1], st);
+    if (slot >= 0) cudaEventRecordWithFlags(c->kprof_ev[2 * slot + 1], st, cudaEventRecordExternal);
 }
 
 extern "C" {
@@ -30,8 +32,10 @@ extern "C" {
 hs_status hs_kprof_enable(hs_ctx *c, int on)
 {
     if (!c) return HS_EINVAL;
+    // switching on starts a new recording; switching off keeps the recorded
+    // slots (a plan captured while on replays into them)
+    if (on && !c->kprof_on) c->kprof_used = 0;
     c->kprof_on = on != 0;
-    c->kprof_used = 0;
     return HS_OK;
 }
 

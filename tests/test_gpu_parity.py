@@ -302,3 +302,14 @@ def test_softmax_bts_parity(toyb, tables, table, m):
     assert np.abs(y - ref).max() < 2.0 ** -15
     led = toyb["ctx"].ledger()
     assert led["bts"] == 2 * k if var == 1 else led["bts"] >= k
+    if var == 1:
+        # the same Softmax as a replayable CUDA graph (hs_softmax_plan_create):
+        # every replay recomputes the words above, bit for bit
+        plan = hs.Plan(K, g_in, n, m, k, var, tab["exp"], tab["inv"], bts=toyb["B"])
+        for _ in range(2):
+            toyb["ctx"].ledger_reset()
+            outs = plan.run()
+            for gc, oc in zip(outs, o_out):
+                same(gc, oc)
+            assert toyb["ctx"].ledger()["bts"] == 2 * k
+        del plan

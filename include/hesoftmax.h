@@ -274,7 +274,9 @@ void hs_plan_destroy(hs_plan *p);
  * and tagged with its algorithmic bytes.  collect
  * synchronises the device and returns, per kernel class (0 NTT, 1 add,
  * 2 scalar, 3 pt-mult, 4 tensor, 5 permute, 6 rescale, 7 bconv, 8 ks-inner,
- * 9 moddown, 10 rng, 11 modraise), [launches, total ms, total bytes]. */
+ * 9 moddown, 10 rng, 11 modraise, 12 hoisted ks-inner), [launches, total ms,
+ * total bytes].  Enabling starts a new recording; disabling keeps the slots so
+ * a plan captured while enabled can replay into them (its event nodes). */
 hs_status hs_kprof_enable(hs_ctx *c, int on);
 hs_status hs_kprof_collect(hs_ctx *c, double *out, int n_classes);
 

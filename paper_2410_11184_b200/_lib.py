@@ -136,5 +136,5 @@ hs_kprof_enable = _sig("hs_kprof_enable", C.c_int, [vp, C.c_int])
 hs_kprof_collect = _sig("hs_kprof_collect", C.c_int, [vp, np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS"),
                                                       C.c_int])
 KPROF_CLASSES = ["ntt", "add", "scalar", "ptmul", "tensor", "permute", "rescale", "bconv", "ks_inner", "moddown",
-                 "rng", "modraise"]
+                 "rng", "modraise", "ks_hoist"]
 EXPORTED = [n for n in list(globals()) if n.startswith("hs_")]

@@ -170,7 +170,7 @@ struct ModUpBuf {
 // launching stream plus the launch's algorithmic bytes;
 // hs_kprof_collect aggregates them per kernel class.
 enum { KID_NTT, KID_ADD, KID_SCALAR, KID_PTMUL, KID_TENSOR, KID_PERMUTE, KID_RESCALE, KID_BCONV, KID_KS_INNER,
-       KID_MODDOWN, KID_RNG, KID_MODRAISE, KID_COUNT };
+       KID_MODDOWN, KID_RNG, KID_MODRAISE, KID_KS_HOIST, KID_COUNT };
 struct KTimer {
     hs_ctx *c;
     int id;

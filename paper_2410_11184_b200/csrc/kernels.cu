@@ -41,11 +41,32 @@ __device__ __forceinline__ u64 d_reduce128(u64 hi, u64 lo, const PrimeK &k)
     return d_shoup(t, k.r64, k.r64sh, k.q);
 }
 __device__ __forceinline__ u64 d_mulmod(u64 a, u64 b, const PrimeK &k) { return d_reduce128(__umul64hi(a, b), a * b, k); }
+// (hi:lo) += a*b as one 32-bit multiply-add carry chain: the four partial
+// products are formed once (mul.lo + mul.hi on 64 bits would form the low ones
+// twice) -- 8 IMAD-class instructions, no IMAD.WIDE
 __device__ __forceinline__ void mac128(u64 &hi, u64 &lo, u64 a, u64 b)
 {
-    u64 l = a * b, h = __umul64hi(a, b);
-    lo += l;
-    hi += h + (lo < l);
+    asm("{\n\t"
+        ".reg .u32 a0, a1, b0, b1, r0, r1, r2, r3;\n\t"
+        "mov.b64 {a0, a1}, %2;\n\t"
+        "mov.b64 {b0, b1}, %3;\n\t"
+        "mov.b64 {r0, r1}, %0;\n\t"
+        "mov.b64 {r2, r3}, %1;\n\t"
+        "mad.lo.cc.u32 r0, a0, b0, r0;\n\t"
+        "madc.hi.cc.u32 r1, a0, b0, r1;\n\t"
+        "madc.lo.cc.u32 r2, a1, b1, r2;\n\t"
+        "madc.hi.u32 r3, a1, b1, r3;\n\t"
+        "mad.lo.cc.u32 r1, a0, b1, r1;\n\t"
+        "madc.hi.cc.u32 r2, a0, b1, r2;\n\t"
+        "addc.u32 r3, r3, 0;\n\t"
+        "mad.lo.cc.u32 r1, a1, b0, r1;\n\t"
+        "madc.hi.cc.u32 r2, a1, b0, r2;\n\t"
+        "addc.u32 r3, r3, 0;\n\t"
+        "mov.b64 %0, {r0, r1};\n\t"
+        "mov.b64 %1, {r2, r3};\n\t"
+        "}"
+        : "+l"(lo), "+l"(hi)
+        : "l"(a), "l"(b));
 }
 
 PrimeMap pmap_range(int first, int count)
@@ -728,28 +749,36 @@ struct BconvArg {
 // sources of y_a * c_ab (each < 2^61 p) stays below p 2^64, so it is
 // accumulated in 128 bits and reduced once (REDC + Shoup, d_reduce128).
 #define BCONV_TG 8
-__global__ void __launch_bounds__(256) bconv_kernel(const u64 *__restrict__ x, size_t xs, u64 *o, size_t os,
-                                                    BconvArg A, const u64 *__restrict__ tab, int N, size_t bxs,
-                                                    size_t bos)
+// NS = number of source primes (compile time: y[] stays in registers and the
+// source loops unroll, the NS constants of a target load together)
+template <int NS>
+__global__ void __launch_bounds__(256) bconv_kernel(const u64 *__restrict__ x, size_t xs, u64 *__restrict__ o,
+                                                    size_t os, BconvArg A, const u64 *__restrict__ tab, int N,
+                                                    size_t bxs, size_t bos)
 {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= N) return;
     x += blockIdx.y * bxs;
     o += blockIdx.y * bos;
-    u64 y[8];
+    u64 y[NS];
     int neg = 0;
-    for (int a = 0; a < A.n_src; a++) {
+#pragma unroll
+    for (int a = 0; a < NS; a++) {
         const PrimeK k = c_pk[A.src[a]];
         y[a] = d_shoup(x[(size_t)a * xs + t], __ldg(tab + 2 * a), __ldg(tab + 2 * a + 1), k.q);
         neg += y[a] > (k.q - 1) / 2;
     }
-    const u64 *cm = tab + 2 * A.n_src;
-    const u64 *pm = cm + 2 * (size_t)A.n_src * A.n_dst;
+    const u64 *cm = tab + 2 * NS;
+    const u64 *pm = cm + 2 * (size_t)NS * A.n_dst;
     const int b0 = blockIdx.z * BCONV_TG, b1 = min(b0 + BCONV_TG, A.n_dst);
     for (int b = b0; b < b1; b++) {
         const PrimeK k = c_pk[A.dst[b]];
+        u64 c[NS];
+#pragma unroll
+        for (int a = 0; a < NS; a++) c[a] = __ldg(cm + 2 * ((size_t)a * A.n_dst + b));
         u64 hi = 0, lo = 0;
-        for (int a = 0; a < A.n_src; a++) mac128(hi, lo, y[a], __ldg(cm + 2 * ((size_t)a * A.n_dst + b)));
+#pragma unroll
+        for (int a = 0; a < NS; a++) mac128(hi, lo, y[a], c[a]);
         u64 s = d_reduce128(hi, lo, k);
         if (A.centred) {
             const u64 pmb = __ldg(pm + b);
@@ -771,8 +800,14 @@ void k_bconv(hs_ctx *c, const BconvTab &tab, const u64 *src, size_t src_stride, 
     for (int i = 0; i < tab.n_dst; i++) A.dst[i] = (unsigned char)tab.dst[i];
     if (tab.n_src > 7) throw HsError(HS_EINVAL, "bconv: more than 7 source primes (128-bit accumulator bound)");
     int N = c->P->n;
-    bconv_kernel<<<dim3((N + 255) / 256, batch, (tab.n_dst + BCONV_TG - 1) / BCONV_TG), 256, 0, st>>>(
-        src, src_stride, dst, dst_stride, A, tab.dev, N, bss, bds);
+    const dim3 grid((N + 255) / 256, batch, (tab.n_dst + BCONV_TG - 1) / BCONV_TG);
+    switch (tab.n_src) {
+#define BCONV_CASE(ns) \
+    case ns: bconv_kernel<ns><<<grid, 256, 0, st>>>(src, src_stride, dst, dst_stride, A, tab.dev, N, bss, bds); break;
+        BCONV_CASE(1) BCONV_CASE(2) BCONV_CASE(3) BCONV_CASE(4) BCONV_CASE(5) BCONV_CASE(6) BCONV_CASE(7)
+#undef BCONV_CASE
+    default: throw HsError(HS_EINVAL, "bconv: source count out of range");
+    }
     HS_CHECK_LAUNCH();
     count_kernel(c);
 }
@@ -1128,13 +1163,17 @@ struct KsArgB {
     int nd[16];
 };
 
+// grid (batch tiles of BT, N / 256, ntg): each thread keeps BT ciphertexts'
+// 128-bit accumulators; the tiles sharing a key block are scheduled back to
+// back, so the key's re-reads hit L2 and HBM streams it about once.
 template <int BT>
-__global__ void ks_inner_b_kernel(const u64 *__restrict__ d, const u64 *__restrict__ ext,
-                                  const u64 *__restrict__ key, u64 *acc, KsArgB A, int N)
+__global__ void __launch_bounds__(256) ks_inner_b_kernel(const u64 *__restrict__ d, const u64 *__restrict__ ext,
+                                                         const u64 *__restrict__ key, u64 *__restrict__ acc,
+                                                         KsArgB A, int N)
 {
-    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    int t = blockIdx.y * blockDim.x + threadIdx.x;
     if (t >= N) return;
-    const int g = blockIdx.y, b0 = blockIdx.z * BT;
+    const int g = blockIdx.z, b0 = blockIdx.x * BT;
     const int nl = A.level + 1, ntg = nl + A.alpha;
     const int pi = g < nl ? g : A.n_q + (g - nl);
     const PrimeK k = c_pk[pi];
@@ -1172,8 +1211,8 @@ void k_ks_inner_b(hs_ctx *c, const u64 *d, size_t d_stride, const u64 *ext, cons
 {
     const hs_params *P = c->P;
     const int ntg = level + 1 + P->n_p;
-    const int tiles = (B + 3) / 4;
-    KTimer _kt(c, KID_KS_INNER, ((double)beta * ntg * (16.0 * tiles + 8.0 * B) + 16.0 * ntg * B) * P->n, st);
+    // algorithmic bytes: the key once, every input limb once, the outputs once
+    KTimer _kt(c, KID_KS_INNER, ((double)beta * ntg * (16.0 + 8.0 * B) + 16.0 * ntg * B) * P->n, st);
     KsArgB A;
     A.level = level;
     A.beta = beta;
@@ -1187,7 +1226,8 @@ void k_ks_inner_b(hs_ctx *c, const u64 *d, size_t d_stride, const u64 *ext, cons
         A.nd[j] = nd[j];
     }
     int N = P->n;
-    ks_inner_b_kernel<4><<<dim3((N + 255) / 256, ntg, tiles), 256, 0, st>>>(d, ext, key, acc, A, N);
+    const int tiles = (B + 3) / 4;
+    ks_inner_b_kernel<4><<<dim3(tiles, (N + 255) / 256, ntg), 256, 0, st>>>(d, ext, key, acc, A, N);
     HS_CHECK_LAUNCH();
     count_kernel(c);
 }
@@ -1206,11 +1246,13 @@ struct KsArgH {
 };
 
 __global__ void __launch_bounds__(256) ks_inner_h_kernel(const u64 *__restrict__ d, const u64 *__restrict__ ext,
-                                                         u64 *acc, KsArgH A, int N)
+                                                         u64 *__restrict__ acc, KsArgH A, int N)
 {
-    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    // grid (R, N / 256, ntg): the R rotations of one coefficient block run back
+    // to back, so their gathers of the shared extended digits hit L2
+    int t = blockIdx.y * blockDim.x + threadIdx.x;
     if (t >= N) return;
-    const int g = blockIdx.y, r = blockIdx.z;
+    const int g = blockIdx.z, r = blockIdx.x;
     const int nl = A.level + 1, ntg = nl + A.alpha;
     const int pi = g < nl ? g : A.n_q + (g - nl);
     const PrimeK k = c_pk[pi];
@@ -1238,7 +1280,7 @@ void k_ks_inner_h(hs_ctx *c, const u64 *d, const u64 *ext, const size_t *off, co
     const hs_params *P = c->P;
     const int ntg = level + 1 + P->n_p;
     if (R < 1 || R > HS_MAXROT) throw HsError(HS_EINVAL, "hoisted key switch: bad rotation count");
-    KTimer _kt(c, KID_KS_INNER, ((double)R * beta * ntg * 24.0 + 16.0 * ntg * R) * P->n, st);
+    KTimer _kt(c, KID_KS_HOIST, ((double)R * beta * ntg * 24.0 + 16.0 * ntg * R) * P->n, st);
     KsArgH A;
     for (int r = 0; r < R; r++) {
         A.key[r] = keys[r];
@@ -1254,7 +1296,7 @@ void k_ks_inner_h(hs_ctx *c, const u64 *d, const u64 *ext, const size_t *off, co
         A.nd[j] = nd[j];
     }
     int N = P->n;
-    ks_inner_h_kernel<<<dim3((N + 255) / 256, ntg, R), 256, 0, st>>>(d, ext, acc, A, N);
+    ks_inner_h_kernel<<<dim3(R, (N + 255) / 256, ntg), 256, 0, st>>>(d, ext, acc, A, N);
     HS_CHECK_LAUNCH();
     count_kernel(c);
 }

@@ -45,8 +45,8 @@ def main():
     ct = hs.encrypt(K, P.encode(z, scale=P.scale(12), level=12), 12, 1, 0)
     for _ in range(10):
         hs.op(K, "mult", ct, ct)
-    kp = np.zeros(36)
-    hs._lib.hs_kprof_collect(ctx.ptr, kp, 12)
+    kp = np.zeros(3 * len(hs._lib.KPROF_CLASSES))
+    hs._lib.hs_kprof_collect(ctx.ptr, kp, len(hs._lib.KPROF_CLASSES))
     for i, nm in enumerate(hs._lib.KPROF_CLASSES):
         if kp[3 * i]:
             print(f"  {nm:10s} {kp[3 * i + 1] / 10 * 1e3:8.1f} us/HMult  {kp[3 * i + 2] / kp[3 * i + 1] / 1e6:8.1f} GB/s"

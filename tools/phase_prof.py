@@ -40,8 +40,8 @@ def main():
     ctx = S["ctx"]
     hs._lib.hs_kprof_enable(ctx.ptr, 1)
     hs.bootstrap(K, B, ct0, 1.0)
-    kp = np.zeros(36)
-    hs._lib.hs_kprof_collect(ctx.ptr, kp, 12)
+    kp = np.zeros(3 * len(hs._lib.KPROF_CLASSES))
+    hs._lib.hs_kprof_collect(ctx.ptr, kp, len(hs._lib.KPROF_CLASSES))
     hs._lib.hs_kprof_enable(ctx.ptr, 0)
     for i, nm in enumerate(hs._lib.KPROF_CLASSES):
         if kp[3 * i]:

@@ -292,27 +292,30 @@ static CtP apply(const hs_keys *K, const hs_ct *in, const LinTrans &T, cudaStrea
         }
     CtP hb;
     if (!rots.empty()) hb = ev_rotate_hoisted(K, x, rots.data(), (int)rots.size(), st);
-    std::map<int, const u64 *> R;
-    R[0] = x->d;
+    std::vector<const u64 *> R(T.b1, nullptr);
+    if (std::find(T.b.begin(), T.b.end(), 0) != T.b.end()) R[0] = x->d;
     for (size_t i = 0; i < bs.size(); i++) R[bs[i]] = hb->d + i * hb->ct_words();
-    int maxg = 0;
-    for (int g : T.g) maxg = std::max(maxg, g);
-    CtP acc = ct_new(c, l, 2, st);
-    HS_CUDA(cudaMemsetAsync(acc->d, 0, acc->limbs() * N * 8, st));
-    for (int g = 0; g <= maxg; g++) {
-        CtP inner;
-        for (size_t k = 0; k < T.g.size(); k++) {
-            if (T.g[k] != g) continue;
-            if (!inner) {
-                inner = ct_new(c, l, 2, st);
-                HS_CUDA(cudaMemsetAsync(inner->d, 0, inner->limbs() * N * 8, st));
-            }
-            k_mac_pt(c, inner->d, R[T.b[k]], T.pts + k * nl * N, nl, nl, st);
-            c->ledger[HS_LG_PMULT]++;
-        }
-        if (!inner) continue;
+    // the giants in use, increasing (sparse: negative diagonals wrap mod N0/u)
+    std::vector<int> gs(T.g.begin(), T.g.end());
+    std::sort(gs.begin(), gs.end());
+    gs.erase(std::unique(gs.begin(), gs.end()), gs.end());
+    const int G = (int)gs.size();
+    std::vector<int> tk((size_t)G * T.b1, -1);
+    for (size_t k = 0; k < T.g.size(); k++) {
+        const int gi = (int)(std::lower_bound(gs.begin(), gs.end(), T.g[k]) - gs.begin());
+        tk[(size_t)gi * T.b1 + T.b[k]] = (int)k;
+    }
+    // every inner sum of pt (.) Rot(x, b u) in one pass over the babies
+    CtP inners = ct_new(c, l, 2, st, G);
+    k_bsgs_inner(c, R.data(), T.b1, T.pts, tk.data(), G, nl, inners->d, st);
+    c->ledger[HS_LG_PMULT] += (int64_t)T.g.size();
+    CtP acc;
+    for (int gi = 0; gi < G; gi++) {
+        const int g = gs[gi];
+        CtP inner = ct_view(inners.get(), gi);
         if (g) inner = ev_rotate(K, inner.get(), (g * T.b1 * T.unit) % n0, st);
-        k_add(c, acc->d, inner->d, acc->d, (int)acc->limbs(), nl, false, st);
+        if (!acc) acc = ct_copy(inner.get(), st);
+        else k_add(c, acc->d, inner->d, acc->d, (int)acc->limbs(), nl, false, st);
     }
     return ev_rescale(acc.get(), st);
 }

@@ -56,7 +56,7 @@ hs_keys::~hs_keys()
 
 hs_ct::~hs_ct()
 {
-    if (d) dev_free(d, st);
+    if (d && owns) dev_free(d, st);
 }
 
 size_t hs_ct::ct_words() const { return (size_t)ncomp * (level + 1) * ctx->P->n; }
@@ -103,6 +103,20 @@ CtP ct_gather(const hs_ct *const *cts, int n, cudaStream_t st)
             throw HsError(HS_EINVAL, "gather: ciphertexts differ in level or shape");
         HS_CUDA(cudaMemcpyAsync(r->d + b * a->ct_words(), cts[b]->d, a->ct_words() * 8, cudaMemcpyDeviceToDevice, st));
     }
+    return r;
+}
+
+// non-owning view of batch member b (valid while a lives)
+CtP ct_view(const hs_ct *a, int b)
+{
+    CtP r(new hs_ct);
+    r->ctx = a->ctx;
+    r->level = a->level;
+    r->ncomp = a->ncomp;
+    r->batch = 1;
+    r->st = a->st;
+    r->d = a->d + b * a->ct_words();
+    r->owns = false;
     return r;
 }
 
@@ -232,6 +246,20 @@ void ks_modup(hs_ctx *c, int level, int B, const u64 *d, size_t d_stride, ModUpB
         tot += (size_t)B * tab.n_dst * N;
     }
     m.ext.alloc(tot, st);
+    if (B == 1 && tot / N <= 256 && m.beta <= 12) {
+        // one polynomial: every digit in ONE BConv launch and ONE NTT launch
+        // (bigger grids than beta small launches; same words)
+        const BconvTab *tabs[16];
+        PrimeMap pm;
+        pm.n = 0;
+        for (int j = 0; j < m.beta; j++) {
+            tabs[j] = &bconv_modup(c, level, j);
+            for (int i = 0; i < tabs[j]->n_dst; i++) pm.p[pm.n++] = (unsigned char)tabs[j]->dst[i];
+        }
+        k_bconv_modup_multi(c, tabs, m.off, m.beta, x.p, m.ext.p, st);
+        k_ntt(c, m.ext.p, pm.n, pm, false, st);
+        return;
+    }
     for (int j = 0; j < m.beta; j++) {
         const BconvTab &tab = bconv_modup(c, level, j);
         u64 *e = m.ext.p + m.off[j];

@@ -129,6 +129,7 @@ struct hs_ct {
     int level = 0, ncomp = 0, batch = 1;
     u64 *d = nullptr;           // [batch][ncomp][level+1][N]
     cudaStream_t st = nullptr;  // stream the buffer is ordered on
+    bool owns = true;           // false: a view into another ciphertext's buffer
     ~hs_ct();
     size_t rows() const { return (size_t)batch * ncomp; }
     size_t limbs() const { return rows() * (level + 1); }
@@ -202,11 +203,15 @@ void k_rescale_prep(hs_ctx *c, const u64 *last, u64 *w, int ncomp, int level, cu
 void k_rescale_final(hs_ctx *c, const u64 *a, const u64 *w, u64 *o, int ncomp, int level, cudaStream_t st);
 void k_bconv(hs_ctx *c, const BconvTab &tab, const u64 *src, size_t src_stride, u64 *dst, size_t dst_stride,
              int batch, size_t batch_src_stride, size_t batch_dst_stride, cudaStream_t st);
+void k_bconv_modup_multi(hs_ctx *c, const BconvTab *const *tabs, const size_t *dst_off, int n_dig, const u64 *x,
+                         u64 *o, cudaStream_t st);
 void k_ks_inner(hs_ctx *c, const u64 *d, const u64 *ext, const u64 *key, u64 *acc, int level, int beta,
                 cudaStream_t st);
 void k_moddown_final(hs_ctx *c, const u64 *acc, const u64 *conv, u64 *o0, u64 *o1, const u64 *add0,
                      const u64 *add1, int level, cudaStream_t st);
 void upload_prime_constants(const hs_params *P);
+void k_bsgs_inner(hs_ctx *c, const u64 *const *R, int b1, const u64 *pts, const int *tk, int G, int nl, u64 *out,
+                  cudaStream_t st);
 void k_mac_pt(hs_ctx *c, u64 *acc, const u64 *a, const u64 *pt, int nl, int la, cudaStream_t st);
 // batched ciphertext kernels ([B][ncomp][nl][N]; "rows" = B * ncomp)
 void k_add_b(hs_ctx *c, const u64 *a, int a_rows, const u64 *b, int b_rows, u64 *o, int rows, int nl, bool sub,
@@ -243,6 +248,7 @@ CtP ct_new(hs_ctx *c, int level, int ncomp, cudaStream_t st, int batch = 1);
 CtP ct_copy(const hs_ct *a, cudaStream_t st);
 CtP ct_drop(const hs_ct *a, int level, cudaStream_t st);
 CtP ct_gather(const hs_ct *const *cts, int n, cudaStream_t st);        // n single cts -> one batch
+CtP ct_view(const hs_ct *a, int b);
 CtP ct_slice(const hs_ct *a, int b, cudaStream_t st);                  // ciphertext b of a batch
 CtP ev_tensor_sum(const hs_ct *a, cudaStream_t st);                    // sum_b tensor(a_b, a_b)
 void ev_keyswitch_b(const hs_keys *K, const SwKey *key, int level, int B, const u64 *d, size_t d_stride, u64 *out,

@@ -788,6 +788,74 @@ __global__ void __launch_bounds__(256) bconv_kernel(const u64 *__restrict__ x, s
     }
 }
 
+// All ModUp digits of ONE polynomial in one launch (grid.y = digit): digit j
+// converts x limbs [src0_j, src0_j + n_src_j) to its n_dst_j targets at
+// o + dst_off_j.  Non-centred (ModUp).  Up to 7 sources, unrolled with guards.
+struct BconvMultiArg {
+    int n_dig;
+    struct Dig {
+        const u64 *tab;
+        int n_src, n_dst, src0;
+        size_t dst_off;
+        unsigned char src[8], dst[HS_MAXP];
+    } d[12];
+};
+
+__global__ void __launch_bounds__(256) bconv_multi_kernel(const u64 *__restrict__ x, u64 *__restrict__ o,
+                                                          const __grid_constant__ BconvMultiArg A, int N)
+{
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= N) return;
+    const BconvMultiArg::Dig &D = A.d[blockIdx.y];
+    const int b0 = blockIdx.z * BCONV_TG, b1 = min(b0 + BCONV_TG, D.n_dst);
+    if (b0 >= b1) return;
+    const u64 *tab = D.tab;
+    u64 y[7];
+#pragma unroll
+    for (int a = 0; a < 7; a++)
+        if (a < D.n_src) {
+            const PrimeK k = c_pk[D.src[a]];
+            y[a] = d_shoup(x[(size_t)(D.src0 + a) * N + t], __ldg(tab + 2 * a), __ldg(tab + 2 * a + 1), k.q);
+        }
+    const u64 *cm = tab + 2 * D.n_src;
+    for (int b = b0; b < b1; b++) {
+        const PrimeK k = c_pk[D.dst[b]];
+        u64 hi = 0, lo = 0;
+#pragma unroll
+        for (int a = 0; a < 7; a++)
+            if (a < D.n_src) mac128(hi, lo, y[a], __ldg(cm + 2 * ((size_t)a * D.n_dst + b)));
+        o[D.dst_off + (size_t)b * N + t] = d_reduce128(hi, lo, k);
+    }
+}
+
+void k_bconv_modup_multi(hs_ctx *c, const BconvTab *const *tabs, const size_t *dst_off, int n_dig, const u64 *x,
+                         u64 *o, cudaStream_t st)
+{
+    const int N = c->P->n;
+    if (n_dig < 1 || n_dig > 12) throw HsError(HS_EINVAL, "bconv_multi: digit count out of range");
+    BconvMultiArg A;
+    A.n_dig = n_dig;
+    double bytes = 0;
+    int maxg = 1;
+    for (int j = 0; j < n_dig; j++) {
+        const BconvTab &t = *tabs[j];
+        if (t.n_src > 7 || t.centred) throw HsError(HS_EINVAL, "bconv_multi: ModUp digits only");
+        A.d[j].tab = t.dev;
+        A.d[j].n_src = t.n_src;
+        A.d[j].n_dst = t.n_dst;
+        A.d[j].src0 = t.src[0];
+        A.d[j].dst_off = dst_off[j];
+        for (int i = 0; i < t.n_src; i++) A.d[j].src[i] = (unsigned char)t.src[i];
+        for (int i = 0; i < t.n_dst; i++) A.d[j].dst[i] = (unsigned char)t.dst[i];
+        bytes += (double)(t.n_src + t.n_dst) * N * 8;
+        maxg = std::max(maxg, (t.n_dst + BCONV_TG - 1) / BCONV_TG);
+    }
+    KTimer _kt(c, KID_BCONV, bytes, st);
+    bconv_multi_kernel<<<dim3((N + 255) / 256, n_dig, maxg), 256, 0, st>>>(x, o, A, N);
+    HS_CHECK_LAUNCH();
+    count_kernel(c);
+}
+
 void k_bconv(hs_ctx *c, const BconvTab &tab, const u64 *src, size_t src_stride, u64 *dst, size_t dst_stride,
              int batch, size_t bss, size_t bds, cudaStream_t st)
 {
@@ -1356,6 +1424,74 @@ __global__ void mac_pt_kernel(u64 *acc, const u64 *a, const u64 *pt, int N, int 
     u64 p = pt[(size_t)i * N + t];
     size_t ai = ((size_t)c * la + i) * N + t, oi = ((size_t)c * nl + i) * N + t;
     acc[oi] = d_add(acc[oi], d_mulmod(a[ai], p, k), k.q);
+}
+
+// One BSGS layer of a bootstrapping linear transform in ONE pass:
+// out[g][c][i][t] = sum_b pt_{tk[g][b]}[i][t] * R_b[c][i][t] mod q_i for every
+// giant g.  A thread keeps its 2*B1 baby words in registers (each read once),
+// accumulates in 128 bits (B1 <= 8 terms of < q^2 stay below q 2^64 for
+// q < 2^61) and reduces once per output.  tk[g*B1+b] = term index or -1.
+struct BsgsArg {
+    const u64 *R[16];
+    int tk[16 * 16];
+    int G, nl;
+};
+
+template <int B1>
+__global__ void __launch_bounds__(256) bsgs_inner_kernel(const u64 *__restrict__ pts, u64 *__restrict__ out,
+                                                         const __grid_constant__ BsgsArg A, int N)
+{
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= N) return;
+    const int i = blockIdx.y, nl = A.nl;
+    const PrimeK k = c_pk[i];
+    u64 r0[B1], r1[B1];
+#pragma unroll
+    for (int b = 0; b < B1; b++)
+        if (A.R[b]) {
+            r0[b] = A.R[b][(size_t)i * N + t];
+            r1[b] = A.R[b][((size_t)nl + i) * N + t];
+        }
+    for (int g = 0; g < A.G; g++) {
+        u64 h0 = 0, l0 = 0, h1 = 0, l1 = 0;
+#pragma unroll
+        for (int b = 0; b < B1; b++) {
+            const int kk = A.tk[g * B1 + b];
+            if (kk >= 0) {
+                const u64 p = pts[((size_t)kk * nl + i) * N + t];
+                mac128(h0, l0, r0[b], p);
+                mac128(h1, l1, r1[b], p);
+            }
+        }
+        out[((size_t)g * 2 * nl + i) * N + t] = d_reduce128(h0, l0, k);
+        out[((size_t)(g * 2 + 1) * nl + i) * N + t] = d_reduce128(h1, l1, k);
+    }
+}
+
+void k_bsgs_inner(hs_ctx *c, const u64 *const *R, int b1, const u64 *pts, const int *tk, int G, int nl, u64 *out,
+                  cudaStream_t st)
+{
+    if (b1 < 1 || b1 > 8 || G < 1 || G > 16) throw HsError(HS_EINVAL, "bsgs_inner: baby / giant count out of range");
+    BsgsArg A;
+    int terms = 0, babies = 0;
+    for (int b = 0; b < 16; b++) A.R[b] = b < b1 ? R[b] : nullptr;
+    for (int b = 0; b < b1; b++) babies += R[b] != nullptr;
+    const int B1 = b1 <= 2 ? 2 : b1 <= 4 ? 4 : 8;
+    for (int g = 0; g < G; g++)
+        for (int b = 0; b < B1; b++) {
+            A.tk[g * B1 + b] = b < b1 ? tk[g * b1 + b] : -1;
+            terms += A.tk[g * B1 + b] >= 0;
+        }
+    A.G = G;
+    A.nl = nl;
+    const int N = c->P->n;
+    KTimer _kt(c, KID_PTMUL, (double)(2 * babies + terms + 2 * G) * nl * N * 8, st);
+    const dim3 grid((N + 255) / 256, nl);
+    if (B1 == 2) bsgs_inner_kernel<2><<<grid, 256, 0, st>>>(pts, out, A, N);
+    else if (B1 == 4) bsgs_inner_kernel<4><<<grid, 256, 0, st>>>(pts, out, A, N);
+    else bsgs_inner_kernel<8><<<grid, 256, 0, st>>>(pts, out, A, N);
+    HS_CHECK_LAUNCH();
+    count_kernel(c);
 }
 
 void k_mac_pt(hs_ctx *c, u64 *acc, const u64 *a, const u64 *pt, int nl, int la, cudaStream_t st)

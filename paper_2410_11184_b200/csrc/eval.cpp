@@ -286,6 +286,7 @@ void ks_moddown(hs_ctx *c, int level, int B, const u64 *acc, u64 *out, size_t ou
     const BconvTab &md = bconv_moddown(c, level);
     DBuf conv((size_t)B * 2 * nl * N, st);
     k_bconv(c, md, z.p, N, conv.p, N, 2 * B, (size_t)np * N, (size_t)nl * N, st);
+    if (k_ntt_moddown(c, conv.p, acc, ntg, out, out_stride, add, add_stride, add_comps, nl, B, st)) return;
     k_ntt(c, conv.p, 2 * B * nl, pmap_range(0, nl), false, st);
     k_moddown_final_b(c, acc, conv.p, out, out_stride, add, add_stride, add_comps, level, B, st);
 }
@@ -376,10 +377,12 @@ CtP ev_rescale(const hs_ct *a, cudaStream_t st)
     pm.p[0] = (unsigned char)l;
     k_ntt(c, last.p, rows, pm, true, st);
     DBuf w((size_t)rows * l * N, st);
-    k_rescale_prep(c, last.p, w.p, rows, l, st);
-    k_ntt(c, w.p, rows * l, pmap_range(0, l), false, st);
     CtP r = ct_new(c, l - 1, a->ncomp, st, a->batch);
-    k_rescale_final(c, a->d, w.p, r->d, rows, l, st);
+    if (!k_ntt_rescale(c, last.p, w.p, a->d, r->d, rows, l, st)) {
+        k_rescale_prep(c, last.p, w.p, rows, l, st);
+        k_ntt(c, w.p, rows * l, pmap_range(0, l), false, st);
+        k_rescale_final(c, a->d, w.p, r->d, rows, l, st);
+    }
     c->ledger[HS_LG_RESCALE] += a->batch;
     return r;
 }

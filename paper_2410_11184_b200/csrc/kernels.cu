@@ -296,11 +296,26 @@ __device__ __forceinline__ Tw twiddles(const u64 *tw, int pi, bool inv)
     return Tw{reinterpret_cast<const ulonglong2 *>(base), q, 2 * q};
 }
 
+// Fused prologue / epilogue of a FORWARD transform (limb = row * E.l + i):
+//   MODE 1 (rescale, C9): cols loads centred(last_row) mod q_i from the row's
+//     dropped limb in coefficient form; rows stores
+//     o[row ostr + i N + e] = (ain[row astr + i N + e] - v) q_l^-1
+//   MODE 2 (ModDown, C7): rows stores, with row = 2 b + comp,
+//     o[b ostr + (comp l + i) N + e] = [add] + (ain[row astr + i N + e] - v) P^-1
+// MODE 0 is the plain transform.
+struct NttEpi {
+    const u64 *last, *ain, *add;
+    u64 *o;
+    size_t astr, ostr, addstr;
+    int l, lq, add_comps;
+    u64 inv[HS_MAXP], inv_sh[HS_MAXP];
+};
+
 // Phase over the high 8 index bits (half-spans 2^15..2^8): C columns x 256 rows
 // per CTA of 32 C threads (thread = column tid % C, row index rid = tid / C).
-template <bool INV, int C>
+template <bool INV, int C, int MODE = 0>
 __global__ void __launch_bounds__(32 * C) cols(u64 *data, PrimeMap pm, const u64 *__restrict__ tw,
-                                               const u64 *__restrict__ ninv)
+                                               const u64 *__restrict__ ninv, const __grid_constant__ NttEpi E)
 {
     __shared__ u64 sm[256 * C];
     const int limb = blockIdx.y, pi = pm.p[limb % pm.n];
@@ -311,8 +326,24 @@ __global__ void __launch_bounds__(32 * C) cols(u64 *data, PrimeMap pm, const u64
     if (!INV) {
         // round 1: rows r0 + 32k, s = 32 rows
         const int r0 = rid;
+        if (MODE == 1) {
+            // x = centred(last) mod q_i, last = the row's dropped limb mod q_l
+            const u64 *src = E.last + (size_t)(limb / E.l) * N;
+            const u64 ql = c_pk[E.lq].q;
+            const PrimeK kq = c_pk[pi];
 #pragma unroll
-        for (int k = 0; k < 8; k++) x[k] = a[(r0 + 32 * k) * 256 + c];
+            for (int k = 0; k < 8; k++) {
+                const u64 v = src[(r0 + 32 * k) * 256 + c];
+                if (v <= (ql - 1) / 2) x[k] = d_reduce128(0, v, kq);
+                else {
+                    const u64 r = d_reduce128(0, ql - v, kq);
+                    x[k] = r ? kq.q - r : 0;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < 8; k++) x[k] = a[(r0 + 32 * k) * 256 + c];
+        }
         radix8_fwd(x, r0 * 256 + c, 32 * 256, T);
 #pragma unroll
         for (int k = 0; k < 8; k++) sm[(r0 + 32 * k) * C + col] = x[k];
@@ -367,8 +398,9 @@ __global__ void __launch_bounds__(32 * C) cols(u64 *data, PrimeMap pm, const u64
 
 // Phase over the low 8 index bits (half-spans 2^7..1): R rows of 256 per CTA of
 // 32 R threads (one warp per row).
-template <bool INV, int R>
-__global__ void __launch_bounds__(32 * R) rows(u64 *data, PrimeMap pm, const u64 *__restrict__ tw)
+template <bool INV, int R, int MODE = 0>
+__global__ void __launch_bounds__(32 * R) rows(u64 *data, PrimeMap pm, const u64 *__restrict__ tw,
+                                               const __grid_constant__ NttEpi E)
 {
     __shared__ u64 sm[R * 256];
     const int limb = blockIdx.y, pi = pm.p[limb % pm.n];
@@ -404,7 +436,29 @@ __global__ void __launch_bounds__(32 * R) rows(u64 *data, PrimeMap pm, const u64
             for (int k = 0; k < 4; k++) sm[row * 256 + 4 * q + k] = y[k];
         }
         __syncthreads();
-        for (int i = tid; i < R * 256; i += 32 * R) a[i] = reduce4(sm[i], T);
+        if (MODE == 0) {
+            for (int i = tid; i < R * 256; i += 32 * R) a[i] = reduce4(sm[i], T);
+        } else {
+            const int row = limb / E.l, li = limb - row * E.l;
+            const size_t e0 = (size_t)row0 * 256;
+            const u64 *in = E.ain + row * E.astr + (size_t)li * N + e0;
+            const u64 inv = E.inv[li], ish = E.inv_sh[li];
+            if (MODE == 1) {
+                u64 *o = E.o + row * E.ostr + (size_t)li * N + e0;
+                for (int i = tid; i < R * 256; i += 32 * R)
+                    o[i] = d_shoup(d_sub(in[i], reduce4(sm[i], T), T.q), inv, ish, T.q);
+            } else {
+                const int b = row >> 1, comp = row & 1;
+                const size_t ci = ((size_t)comp * E.l + li) * N + e0;
+                u64 *o = E.o + b * E.ostr + ci;
+                const u64 *ad = comp < E.add_comps ? E.add + b * E.addstr + ci : nullptr;
+                for (int i = tid; i < R * 256; i += 32 * R) {
+                    u64 v = d_shoup(d_sub(in[i], reduce4(sm[i], T), T.q), inv, ish, T.q);
+                    if (ad) v = d_add(v, ad[i], T.q);
+                    o[i] = v;
+                }
+            }
+        }
     } else {
         for (int i = tid; i < R * 256; i += 32 * R) sm[i] = a[i];
         __syncthreads();
@@ -439,12 +493,13 @@ void launch(u64 *data, int n_limbs, const PrimeMap &pm, bool inverse, const u64 
             cudaStream_t st)
 {
     const dim3 gc(256 / C, n_limbs), gr(256 / R, n_limbs);
+    NttEpi E{};
     if (!inverse) {
-        cols<false, C><<<gc, 32 * C, 0, st>>>(data, pm, tw, ninv);
-        rows<false, R><<<gr, 32 * R, 0, st>>>(data, pm, tw);
+        cols<false, C><<<gc, 32 * C, 0, st>>>(data, pm, tw, ninv, E);
+        rows<false, R><<<gr, 32 * R, 0, st>>>(data, pm, tw, E);
     } else {
-        rows<true, R><<<gr, 32 * R, 0, st>>>(data, pm, tw);
-        cols<true, C><<<gc, 32 * C, 0, st>>>(data, pm, tw, ninv);
+        rows<true, R><<<gr, 32 * R, 0, st>>>(data, pm, tw, E);
+        cols<true, C><<<gc, 32 * C, 0, st>>>(data, pm, tw, ninv, E);
     }
 }
 
@@ -460,6 +515,73 @@ int tile()
     return t;
 }
 }  // namespace ntt16
+
+// Rescale of `rows` rows at level l (C9) around ONE forward transform:
+// w (scratch, rows*l limbs) = NTT(centred(last) mod q_i) with the lift fused
+// into the first pass, o = (a - w) q_l^-1 fused into the second.  last: the
+// rows' dropped limbs in coefficient form [rows][N]; a: [rows][l+1][N];
+// o: [rows][l][N].  N = 2^16 only (returns false otherwise).
+bool k_ntt_rescale(hs_ctx *c, const u64 *last, u64 *w, const u64 *a, u64 *o, int rows, int l, cudaStream_t st)
+{
+    const hs_params *P = c->P;
+    if (P->log_n != 16) return false;
+    const int N = P->n, n_limbs = rows * l;
+    KTimer _kt(c, KID_NTT, (double)n_limbs * N * 16, st);
+    ntt16::NttEpi E{};
+    E.last = last;
+    E.ain = a;
+    E.o = o;
+    E.astr = (size_t)(l + 1) * N;
+    E.ostr = (size_t)l * N;
+    E.l = l;
+    E.lq = l;
+    const u64 ql = P->prime[l];
+    for (int i = 0; i < l; i++) {
+        E.inv[i] = hs_invmod(ql % P->prime[i], P->prime[i]);
+        E.inv_sh[i] = hs_shoup_const(E.inv[i], P->prime[i]);
+    }
+    const PrimeMap pm = pmap_range(0, l);
+    const u64 *ninv = c->T.tw + (size_t)(P->n_q + P->n_p) * 4 * N;
+    ntt16::cols<false, 4, 1><<<dim3(64, n_limbs), 128, 0, st>>>(w, pm, c->T.tw, ninv, E);
+    ntt16::rows<false, 4, 1><<<dim3(64, n_limbs), 128, 0, st>>>(w, pm, c->T.tw, E);
+    HS_CHECK_LAUNCH();
+    c->ledger[HS_LG_NTT] += n_limbs;
+    count_kernel(c, 2);
+    return true;
+}
+
+// ModDown tail (C7): the forward transform of conv [B][2][l][N] (BConv of the
+// P limbs) with o_b = add_b + (acc_b - NTT(conv_b)) P^-1 fused into its second
+// pass; acc [B][2][ntg][N].  N = 2^16 only.
+bool k_ntt_moddown(hs_ctx *c, u64 *conv, const u64 *acc, int ntg, u64 *o, size_t o_stride, const u64 *add,
+                   size_t add_stride, int add_comps, int l_plus_1, int B, cudaStream_t st)
+{
+    const hs_params *P = c->P;
+    if (P->log_n != 16) return false;
+    const int N = P->n, nl = l_plus_1, n_limbs = 2 * B * nl;
+    KTimer _kt(c, KID_NTT, (double)n_limbs * N * 16, st);
+    ntt16::NttEpi E{};
+    E.ain = acc;
+    E.add = add;
+    E.o = o;
+    E.astr = (size_t)ntg * N;
+    E.ostr = o_stride;
+    E.addstr = add_stride;
+    E.add_comps = add ? add_comps : 0;
+    E.l = nl;
+    for (int i = 0; i < nl; i++) {
+        E.inv[i] = P->p_inv_mod_q[i];
+        E.inv_sh[i] = hs_shoup_const(P->p_inv_mod_q[i], P->prime[i]);
+    }
+    const PrimeMap pm = pmap_range(0, nl);
+    const u64 *ninv = c->T.tw + (size_t)(P->n_q + P->n_p) * 4 * N;
+    ntt16::cols<false, 4, 0><<<dim3(64, n_limbs), 128, 0, st>>>(conv, pm, c->T.tw, ninv, E);
+    ntt16::rows<false, 4, 2><<<dim3(64, n_limbs), 128, 0, st>>>(conv, pm, c->T.tw, E);
+    HS_CHECK_LAUNCH();
+    c->ledger[HS_LG_NTT] += n_limbs;
+    count_kernel(c, 2);
+    return true;
+}
 
 void k_ntt(hs_ctx *c, u64 *data, int n_limbs, const PrimeMap &pm, bool inverse, cudaStream_t st)
 {

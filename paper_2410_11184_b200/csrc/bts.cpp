@@ -309,13 +309,20 @@ static CtP apply(const hs_keys *K, const hs_ct *in, const LinTrans &T, cudaStrea
     CtP inners = ct_new(c, l, 2, st, G);
     k_bsgs_inner(c, R.data(), T.b1, T.pts, tk.data(), G, nl, inners->d, st);
     c->ledger[HS_LG_PMULT] += (int64_t)T.g.size();
-    CtP acc;
-    for (int gi = 0; gi < G; gi++) {
-        const int g = gs[gi];
-        CtP inner = ct_view(inners.get(), gi);
-        if (g) inner = ev_rotate(K, inner.get(), (g * T.b1 * T.unit) % n0, st);
-        if (!acc) acc = ct_copy(inner.get(), st);
-        else k_add(c, acc->d, inner->d, acc->d, (int)acc->limbs(), nl, false, st);
+    // the giants g != 0 rotate as ONE batched key switch (a key per member)
+    const int g0 = gs[0] == 0 ? 1 : 0;
+    CtP rot;
+    if (G > g0) {
+        CtP sub = ct_view(inners.get(), g0);
+        sub->batch = G - g0;
+        std::vector<int> rots;
+        for (int gi = g0; gi < G; gi++) rots.push_back((gs[gi] * T.b1 * T.unit) % n0);
+        rot = ev_rotate_multi(K, sub.get(), rots.data(), st);
+    }
+    CtP acc = g0 ? ct_slice(inners.get(), 0, st) : ct_slice(rot.get(), 0, st);
+    for (int gi = 1; gi < G; gi++) {
+        const u64 *src = rot->d + (size_t)(gi - g0) * rot->ct_words();
+        k_add(c, acc->d, src, acc->d, (int)acc->limbs(), nl, false, st);
     }
     return ev_rescale(acc.get(), st);
 }
@@ -334,6 +341,40 @@ CtP ev_bootstrap(const hs_keys *K, hs_bts *B, const hs_ct *in, double bound, cud
         ensure_cts(B);
         stc = &ensure_stc(B, e);
     }
+    // dev diagnostic: HS_BTS_PHASES=1 prints per-phase device time (eager calls only)
+    struct Phases {
+        bool on = false;
+        cudaStream_t st = nullptr;
+        std::vector<cudaEvent_t> ev;
+        std::vector<const char *> nm;
+        void mark(const char *n)
+        {
+            if (!on) return;
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            cudaEventRecord(e, st);
+            ev.push_back(e);
+            nm.push_back(n);
+        }
+        ~Phases()
+        {
+            if (!on) return;
+            cudaEventSynchronize(ev.back());
+            for (size_t i = 1; i < ev.size(); i++) {
+                float ms = 0;
+                cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+                fprintf(stderr, "bts phase %-10s %8.3f ms\n", nm[i], ms);
+            }
+            for (auto e : ev) cudaEventDestroy(e);
+        }
+    } ph;
+    {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        cudaStreamIsCapturing(st, &cs);
+        ph.on = getenv("HS_BTS_PHASES") && cs == cudaStreamCaptureStatusNone;
+        ph.st = st;
+    }
+    ph.mark("start");
     CtP x = e ? ev_mult_int(in, (int64_t)1 << e, st) : ct_copy(in, st);
     // ModRaise of the q0 residues
     DBuf low(2 * N, st);
@@ -345,11 +386,17 @@ CtP ev_bootstrap(const hs_keys *K, hs_bts *B, const hs_ct *in, double bound, cud
     x = ct_new(c, L, 2, st);
     k_modraise(c, low.p, x->d, L + 1, st);
     k_ntt(c, x->d, 2 * (L + 1), pmap_range(0, L + 1), false, st);
-    for (auto &T : B->cts) x = apply(K, x.get(), *T, st);
+    ph.mark("modraise");
+    for (auto &T : B->cts) {
+        x = apply(K, x.get(), *T, st);
+        ph.mark("cts-group");
+    }
     CtP cj = ev_galois(K, x.get(), conj, st);
     x = ev_add(x.get(), cj.get(), false, st);
     x = ev_add_const(x.get(), -1.0 / (4.0 * (B->K + 2)), st);
+    ph.mark("conj");
     x = ev_cheb(K, x.get(), &B->cos_poly, st);
+    ph.mark("cos-cheb");
     for (int i = 0; i < B->r; i++) {
         CtP m = ev_mult(K, x.get(), x.get(), st);
         m = ev_mult_int(m.get(), 2, st);
@@ -367,8 +414,13 @@ CtP ev_bootstrap(const hs_keys *K, hs_bts *B, const hs_ct *in, double bound, cud
     } else {  // gamma s
         x = ev_mult_const(x.get(), gamma, x->level - 1, st);
     }
-    for (auto &T : *stc) x = apply(K, x.get(), *T, st);
+    ph.mark("dbl+arcsin");
+    for (auto &T : *stc) {
+        x = apply(K, x.get(), *T, st);
+        ph.mark("stc-group");
+    }
     cj = ev_galois(K, x.get(), conj, st);
+    ph.mark("conj");
     c->ledger[HS_LG_BTS]++;
     return ev_add(x.get(), cj.get(), false, st);
 }

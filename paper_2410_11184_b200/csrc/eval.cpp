@@ -572,6 +572,38 @@ CtP ev_galois(const hs_keys *K, const hs_ct *a, int k, cudaStream_t st)
     return r;
 }
 
+// out_b = Rot(a_b, rots[b]) for every member of the batch a, as ONE batched
+// key switch with a key per member (the BTS giant steps); words identical to
+// rotating each member alone.
+CtP ev_rotate_multi(const hs_keys *K, const hs_ct *a, const int *rots, cudaStream_t st)
+{
+    hs_ctx *c = a->ctx;
+    const hs_params *P = c->P;
+    const size_t N = P->n;
+    const int B = a->batch, l = a->level, nl = l + 1, ntg = nl + P->n_p;
+    if (a->ncomp != 2) throw HsError(HS_EINVAL, "rotation needs a degree-1 ciphertext");
+    if (B < 1 || B > HS_MAXROT) throw HsError(HS_EINVAL, "rotate_multi: batch out of range");
+    const size_t w = a->ct_words();
+    std::vector<const u64 *> keys(B);
+    CtP s = ct_new(c, l, 2, st, B);
+    for (int b = 0; b < B; b++) {
+        const int k = hs_galois_elt(P, rots[b]);
+        const SwKey *key = K->find(k);
+        if (!key) throw HsError(HS_EKEY, "switching key for rotation " + std::to_string(rots[b]) + " missing");
+        keys[b] = key->k;
+        k_permute(c, a->d + b * w, s->d + b * w, galois_table(c, k), 2 * nl, st);
+    }
+    ModUpBuf m;
+    ks_modup(c, l, B, s->limb(1, 0), w, m, st);
+    DBuf acc((size_t)B * 2 * ntg * N, st);
+    k_ks_inner_m(c, s->limb(1, 0), w, m.ext.p, m.off, m.nd, keys.data(), B, acc.p, l, m.beta, st);
+    CtP r = ct_new(c, l, 2, st, B);
+    ks_moddown(c, l, B, acc.p, r->d, w, s->d, w, 1, st);
+    c->ledger[HS_LG_KS] += B;
+    c->ledger[HS_LG_ROT] += B;
+    return r;
+}
+
 CtP ev_rotate(const hs_keys *K, const hs_ct *a, int r, cudaStream_t st)
 {
     return ev_galois(K, a, hs_galois_elt(K->ctx->P, r), st);

@@ -178,6 +178,7 @@ struct KTimer {
     double bytes;
     cudaStream_t st;
     int slot;
+    bool ext = false;  // recorded under stream capture (graph event nodes)
     KTimer(hs_ctx *c, int id, double bytes, cudaStream_t st);
     ~KTimer();
 };
@@ -226,6 +227,8 @@ void k_tensor_b(hs_ctx *c, const u64 *a, const u64 *b, u64 *o, int B, int nl, in
 void k_tensor_sum(hs_ctx *c, const u64 *a, u64 *o, int B, int nl, cudaStream_t st);
 void k_ks_inner_b(hs_ctx *c, const u64 *d, size_t d_stride, const u64 *ext, const size_t *off, const int *nd,
                   const u64 *key, u64 *acc, int level, int beta, int B, cudaStream_t st);
+void k_ks_inner_m(hs_ctx *c, const u64 *d, size_t d_stride, const u64 *ext, const size_t *off, const int *nd,
+                  const u64 *const *keys, int B, u64 *acc, int level, int beta, cudaStream_t st);
 void k_ks_inner_h(hs_ctx *c, const u64 *d, const u64 *ext, const size_t *off, const int *nd, const u64 *const *keys,
                   const unsigned *const *perms, int R, u64 *acc, int level, int beta, cudaStream_t st);
 void k_moddown_final_b(hs_ctx *c, const u64 *acc, const u64 *conv, u64 *o, size_t o_stride, const u64 *add,
@@ -268,6 +271,7 @@ CtP ev_mult_const(const hs_ct *a, double v, int target, cudaStream_t st);
 CtP ev_mult_pt(const hs_ct *a, const double *re, const double *im, int target, cudaStream_t st);
 CtP ev_galois(const hs_keys *K, const hs_ct *a, int k, cudaStream_t st);
 CtP ev_rotate(const hs_keys *K, const hs_ct *a, int r, cudaStream_t st);
+CtP ev_rotate_multi(const hs_keys *K, const hs_ct *a, const int *rots, cudaStream_t st);
 CtP ev_rotate_hoisted(const hs_keys *K, const hs_ct *a, const int *rots, int R, cudaStream_t st);
 void ks_modup(hs_ctx *c, int level, int B, const u64 *d, size_t d_stride, ModUpBuf &m, cudaStream_t st);
 void ks_moddown(hs_ctx *c, int level, int B, const u64 *acc, u64 *out, size_t out_stride, const u64 *add,

@@ -1491,6 +1491,71 @@ void k_ks_inner_h(hs_ctx *c, const u64 *d, const u64 *ext, const size_t *off, co
     count_kernel(c);
 }
 
+// B polynomials, each with ITS OWN key (a batch of rotations by different
+// amounts): ModUp blocks as in ks_inner_b ([B][nd_j][N] per digit), member r
+// uses key[r].  grid (B, N / 256, ntg): the members of one coefficient block
+// run back to back.  acc [B][2][ntg][N].
+struct KsArgM {
+    const u64 *key[HS_MAXROT];
+    int level, beta, alpha, n_q, n_t;
+    size_t d_stride;
+    size_t off[16];
+    int nd[16];
+};
+
+__global__ void __launch_bounds__(256) ks_inner_m_kernel(const u64 *__restrict__ d, const u64 *__restrict__ ext,
+                                                         u64 *__restrict__ acc, const __grid_constant__ KsArgM A,
+                                                         int N)
+{
+    int t = blockIdx.y * blockDim.x + threadIdx.x;
+    if (t >= N) return;
+    const int g = blockIdx.z, r = blockIdx.x;
+    const int nl = A.level + 1, ntg = nl + A.alpha;
+    const int pi = g < nl ? g : A.n_q + (g - nl);
+    const PrimeK k = c_pk[pi];
+    const size_t ntot = (size_t)A.n_q + A.n_t;
+    const u64 *key = A.key[r];
+    u64 h0 = 0, l0 = 0, h1 = 0, l1 = 0;
+    for (int j = 0; j < A.beta; j++) {
+        const int lo = j * A.alpha, hi = min((j + 1) * A.alpha, nl), dn = hi - lo;
+        const u64 k0 = key[(((size_t)j * 2 + 0) * ntot + pi) * N + t];
+        const u64 k1 = key[(((size_t)j * 2 + 1) * ntot + pi) * N + t];
+        const bool own = g >= lo && g < hi;
+        const int gg = g < lo ? g : g - dn;
+        const u64 v = own ? d[(size_t)r * A.d_stride + (size_t)g * N + t]
+                          : ext[A.off[j] + ((size_t)r * A.nd[j] + gg) * N + t];
+        mac128(h0, l0, v, k0);
+        mac128(h1, l1, v, k1);
+    }
+    acc[((size_t)r * 2 * ntg + g) * N + t] = d_reduce128(h0, l0, k);
+    acc[((size_t)(r * 2 + 1) * ntg + g) * N + t] = d_reduce128(h1, l1, k);
+}
+
+void k_ks_inner_m(hs_ctx *c, const u64 *d, size_t d_stride, const u64 *ext, const size_t *off, const int *nd,
+                  const u64 *const *keys, int B, u64 *acc, int level, int beta, cudaStream_t st)
+{
+    const hs_params *P = c->P;
+    const int ntg = level + 1 + P->n_p;
+    if (B < 1 || B > HS_MAXROT) throw HsError(HS_EINVAL, "multi-key inner product: bad batch");
+    KTimer _kt(c, KID_KS_INNER, ((double)B * beta * ntg * 24.0 + 16.0 * ntg * B) * P->n, st);
+    KsArgM A;
+    for (int r = 0; r < B; r++) A.key[r] = keys[r];
+    A.level = level;
+    A.beta = beta;
+    A.alpha = P->alpha;
+    A.n_q = P->n_q;
+    A.n_t = P->n_p;
+    A.d_stride = d_stride;
+    for (int j = 0; j < beta; j++) {
+        A.off[j] = off[j];
+        A.nd[j] = nd[j];
+    }
+    int N = P->n;
+    ks_inner_m_kernel<<<dim3(B, (N + 255) / 256, ntg), 256, 0, st>>>(d, ext, acc, A, N);
+    HS_CHECK_LAUNCH();
+    count_kernel(c);
+}
+
 // o_b[c][i] = add_b[c][i] + (acc_b[c][i] - conv_b[c][i]) P^{-1} for b < B;
 // acc [B][2][ntg][N], conv [B][2][nl][N]; o / add with per-ciphertext strides
 struct MdArgB {

@@ -17,14 +17,20 @@ KTimer::KTimer(hs_ctx *c_, int id_, double bytes_, cudaStream_t st_) : c(c_), id
     slot = (int)c->kprof_used++;
     c->kprof_id[slot] = id;
     c->kprof_bytes[slot] = bytes;
-    // External: under stream capture this becomes an event-record node of the
-    // graph (a plain record would only express a dependency)
-    cudaEventRecordWithFlags(c->kprof_ev[2 * slot], st, cudaEventRecordExternal);
+    // under stream capture an External record becomes an event-record node of
+    // the graph (a plain record would only express a dependency)
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    ext = cs != cudaStreamCaptureStatusNone;
+    if (ext) cudaEventRecordWithFlags(c->kprof_ev[2 * slot], st, cudaEventRecordExternal);
+    else cudaEventRecord(c->kprof_ev[2 * slot], st);
 }
 
 KTimer::~KTimer()
 {
-    if (slot >= 0) cudaEventRecordWithFlags(c->kprof_ev[2 * slot + 1], st, cudaEventRecordExternal);
+    if (slot < 0) return;
+    if (ext) cudaEventRecordWithFlags(c->kprof_ev[2 * slot + 1], st, cudaEventRecordExternal);
+    else cudaEventRecord(c->kprof_ev[2 * slot + 1], st);
 }
 
 extern "C" {

@@ -58,6 +58,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--kprof", default="timed", choices=["timed", "extra", "off"])
     ap.add_argument("--no-graph", action="store_true", help="eager C-ABI calls instead of a CUDA-graph plan")
+    ap.add_argument("--no-primitives", action="store_true", help="skip the HMult / rotation ops/s block")
     return ap.parse_args()
 
 
@@ -318,11 +319,39 @@ def run_ours(args):
         "setup_s": round(S["setup_s"], 1),
         "host_enqueue_ms_per_step": round(host_ms, 1),
     }
+    if not args.no_primitives:
+        line["primitives"] = run_primitives(S)
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(line["ledger_per_step"], budget_s=20.0)
     print(json.dumps(line))
     if world > 1:
         dist_.destroy_process_group()
+
+
+def run_primitives(S, reps=5):
+    """HMult+relin(+rescale) and rotation ops/s at levels 12
+    and 24, batch 1 and batch 64 (hs_ct_gather batches), CUDA-event timed."""
+    import torch
+    hs, K, P = S["hs"], S["K"], S["P"]
+    z = np.random.default_rng(3).uniform(-1, 1, P.n // 2)
+    out = {}
+    for lvl in (12, 24):
+        ct = hs.encrypt(K, P.encode(z, scale=P.scale(lvl), level=lvl), lvl, 77, 0)
+        for b in (1, 64):
+            x = ct if b == 1 else hs.gather([ct] * b)
+            for name, fn in (("hmult_relin", lambda: hs.op(K, "mult", x, x)),
+                             ("rotation", lambda: hs.op(K, "rotate", x, i=1))):
+                fn()
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(reps):
+                    fn()
+                e1.record()
+                torch.cuda.synchronize()
+                out[f"{name}_ops_s_l{lvl}_b{b}"] = round(b * reps / (e0.elapsed_time(e1) * 1e-3), 1)
+            del x
+    return out
 
 
 def run_e2e(S, step, plan, args, world):

@@ -141,6 +141,14 @@ hs_status hs_ct_export(hs_ctx *c, const hs_ct *ct, uint64_t *words, int on_devic
  * the stream passes this point (pinned memory makes the copy asynchronous).
  * Used to refresh a plan's bound inputs. */
 hs_status hs_ct_write(hs_ctx *c, hs_ct *ct, const uint64_t *words, int on_device, void *stream);
+/* Batched ciphertexts: n ciphertexts of one level and shape copied into ONE
+ * batch handle ([n][ncomp][level+1][N]); every hs_op on a batch runs each
+ * kernel once over all members (key switches read each evaluation-key limb
+ * once per batch tile) and a batch-1 operand broadcasts against a batch.
+ * hs_ct_batch returns the member count; hs_ct_member copies member i out. */
+hs_status hs_ct_gather(hs_ctx *c, const hs_ct *const *cts, int n, void *stream, hs_ct **out);
+int hs_ct_batch(const hs_ct *ct);
+hs_status hs_ct_member(hs_ctx *c, const hs_ct *batch, int i, void *stream, hs_ct **out);
 int hs_ct_level(const hs_ct *ct);
 int hs_ct_ncomp(const hs_ct *ct);
 void hs_ct_destroy(hs_ct *ct);

@@ -223,6 +223,21 @@ def keyswitch(keys: Keys, galois, level, d_ptr, out0_ptr, out1_ptr, stream=None)
                          C.c_void_p(out1_ptr), _stream(stream)))
 
 
+def gather(cts, stream=None) -> Ciphertext:
+    """hs_ct_gather: one batch handle over ciphertexts of one level; hs ops on it
+    run every kernel once over all members."""
+    ptrs = (C.c_void_p * len(cts))(*[c.ptr.value if isinstance(c.ptr, C.c_void_p) else c.ptr for c in cts])
+    out = C.c_void_p()
+    check(L.hs_ct_gather(cts[0].ctx.ptr, ptrs, len(cts), _stream(stream), C.byref(out)))
+    return Ciphertext(cts[0].ctx, out)
+
+
+def member(batch: Ciphertext, i, stream=None) -> Ciphertext:
+    out = C.c_void_p()
+    check(L.hs_ct_member(batch.ctx.ptr, batch.ptr, i, _stream(stream), C.byref(out)))
+    return Ciphertext(batch.ctx, out)
+
+
 def rotate_hoisted(keys: Keys, a: Ciphertext, rots, stream=None):
     """C16: Rot(a, r) for every r in rots from ONE ModUp of a's c1."""
     r = (C.c_int32 * len(rots))(*rots)

@@ -98,6 +98,9 @@ hs_ct_level = _sig("hs_ct_level", C.c_int, [vp])
 hs_ct_ncomp = _sig("hs_ct_ncomp", C.c_int, [vp])
 hs_ct_destroy = _sig("hs_ct_destroy", None, [vp])
 hs_ct_write = _sig("hs_ct_write", C.c_int, [vp, vp, vp, C.c_int, vp])
+hs_ct_gather = _sig("hs_ct_gather", C.c_int, [vp, C.POINTER(vp), C.c_int, vp, C.POINTER(vp)])
+hs_ct_batch = _sig("hs_ct_batch", C.c_int, [vp])
+hs_ct_member = _sig("hs_ct_member", C.c_int, [vp, vp, C.c_int, vp, C.POINTER(vp)])
 hs_softmax_plan_create = _sig("hs_softmax_plan_create", C.c_int, [vp, vp, vp, C.POINTER(vp), C.c_size_t, vp,
                                                                   C.POINTER(vp)])
 hs_plan_run = _sig("hs_plan_run", C.c_int, [vp, vp])

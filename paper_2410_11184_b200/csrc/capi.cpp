@@ -251,6 +251,30 @@ hs_status hs_ct_import(hs_ctx *c, int level, int ncomp, const uint64_t *words, i
     HS_CATCH
 }
 
+hs_status hs_ct_gather(hs_ctx *c, const hs_ct *const *cts, int n, void *stream, hs_ct **out)
+{
+    HS_TRY
+    if (!c || !cts || !out || n < 1) throw HsError(HS_EINVAL, "ct_gather: bad arguments");
+    for (int i = 0; i < n; i++)
+        if (!cts[i]) throw HsError(HS_EINVAL, "ct_gather: NULL member");
+    activate(c);
+    *out = ct_gather(cts, n, S(stream)).release();
+    return HS_OK;
+    HS_CATCH
+}
+
+int hs_ct_batch(const hs_ct *ct) { return ct ? ct->batch : 0; }
+
+hs_status hs_ct_member(hs_ctx *c, const hs_ct *batch, int i, void *stream, hs_ct **out)
+{
+    HS_TRY
+    if (!c || !batch || !out || i < 0 || i >= batch->batch) throw HsError(HS_EINVAL, "ct_member: bad index");
+    activate(c);
+    *out = ct_slice(batch, i, S(stream)).release();
+    return HS_OK;
+    HS_CATCH
+}
+
 hs_status hs_ct_write(hs_ctx *c, hs_ct *ct, const uint64_t *words, int on_device, void *stream)
 {
     HS_TRY

@@ -82,20 +82,45 @@ CtP eval_unit(const hs_keys *K, const hs_ct *u, const hs_poly *p, cudaStream_t s
     Basis E{K, st, 0, {}, {}};
     const int t = clog2(d + 1);
     E.B = d <= 1 ? 2 : 1 << ((t + 1) / 2);
-    E.T.resize(E.B);
+    const int ng = std::max(0, t - clog2(E.B));
+    // baby steps in waves: wave a computes T_{a+1} .. T_{2a} (plus T_B = G_0
+    // when giants are needed), all products T_a T_b at T_a's level, as ONE
+    // batched HMult (the same words as one product at a time)
+    const int top = ng > 0 ? E.B : E.B - 1;
+    E.T.resize(top + 1);
     E.T[1] = ct_copy(u, st);
-    for (int i = 2; i < E.B; i++) {
-        int a = 1 << (clog2(i) - 1), b = i - a;
-        if (a == b) {
-            E.T[i] = dbl_minus_one(K, E.T[a].get(), st);
-        } else {
-            CtP m = ev_mult(K, E.T[a].get(), E.T[b].get(), st);
+    // (an input that is itself a batch -- the main thread's m ciphertexts --
+    // runs the members of a wave one after the other)
+    const int per = u->batch == 1 ? E.B : 1;
+    for (int a = 1; a < top; a *= 2) {
+        const int i1 = std::min(2 * a, top);
+        for (int i0 = a + 1; i0 <= i1; i0 += per) {
+            const int i2 = std::min(i1, i0 + per - 1);
+            std::vector<CtP> lowered;
+            std::vector<const hs_ct *> ops;
+            for (int i = i0; i <= i2; i++) {
+                const hs_ct *tb = E.T[i - a].get();
+                if (tb->level > E.T[a]->level) {
+                    lowered.push_back(ev_level_down(tb, E.T[a]->level, st));
+                    tb = lowered.back().get();
+                }
+                ops.push_back(tb);
+            }
+            CtP bb = ops.size() == 1 ? CtP() : ct_gather(ops.data(), (int)ops.size(), st);
+            CtP m = ev_mult(K, E.T[a].get(), bb ? bb.get() : ops[0], st);
             CtP m2 = ev_mult_int(m.get(), 2, st);
-            E.T[i] = ev_add(m2.get(), E.T[a - b].get(), true, st);
+            for (int i = i0; i <= i2; i++) {
+                CtP v = ops.size() == 1 ? std::move(m2) : ct_view(m2.get(), i - i0);
+                const int b = i - a;
+                E.T[i] = a == b ? ev_add_const(v.get(), -1.0, st) : ev_add(v.get(), E.T[a - b].get(), true, st);
+            }
         }
     }
-    const int ng = std::max(0, t - clog2(E.B));
-    for (int j = 0; j < ng; j++) E.G.push_back(dbl_minus_one(K, j == 0 ? E.T[E.B / 2].get() : E.G[j - 1].get(), st));
+    if (ng > 0) {
+        E.G.push_back(std::move(E.T[E.B]));
+        E.T.resize(E.B);
+    }
+    for (int j = 1; j < ng; j++) E.G.push_back(dbl_minus_one(K, E.G[j - 1].get(), st));
     const int target = u->level - cheb_depth(d);
     if (target < 0) throw HsError(HS_ELEVEL, "polynomial deeper than the remaining levels");
     std::vector<double> c(p->coeffs, p->coeffs + d + 1);

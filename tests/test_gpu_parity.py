@@ -118,6 +118,24 @@ def test_ops_parity(toy):
     same(hs.mult_pt(a, mask, target=10), O.mult_pt(PO, ao, mask, target=10))
 
 
+def test_batched_ops_parity(toy):
+    """hs_ct_gather batches: each member of a batched HMult / rotation / add
+    (batch x batch and batch x broadcast) equals the oracle's single op."""
+    hs = _hs()
+    rng = np.random.default_rng(8)
+    pairs = [toy.enc(rng.uniform(-1, 1, toy.P.n // 2), 11, 20 + i) for i in range(3)]
+    b, bo = toy.enc(rng.uniform(-1, 1, toy.P.n // 2), 11, 30)
+    batch = hs.gather([g for g, _ in pairs])
+    K, KO, PO = toy.K, toy.KO, toy.PO
+    mm = hs.op(K, "mult", batch, batch)
+    mb = hs.op(K, "mult", batch, b)
+    rr = hs.op(K, "rotate", batch, i=-128)
+    for i, (_, o) in enumerate(pairs):
+        same(hs.member(mm, i), O.op(PO, KO, "mult", o, o))
+        same(hs.member(mb, i), O.op(PO, KO, "mult", o, bo))
+        same(hs.member(rr, i), O.op(PO, KO, "rotate", o, i=-128))
+
+
 @pytest.mark.parametrize("level", [15, 7, 0])
 def test_rotate_hoisted_parity(toy, level):
     """C16: every output of one hoisted ModUp is bit-exact with the oracle's."""

@@ -8,7 +8,40 @@ typedef unsigned long long u64;
 
 __device__ __forceinline__ u64 shoup_lazy(u64 a, u64 w, u64 ws, u64 q) { return a * w - __umul64hi(a, ws) * q; }
 
-template <int ILP>
+// the same value from 32-bit multiply-add chains (nq = 2^64 - q)
+__device__ __forceinline__ u64 shoup_lazy_ptx(u64 a, u64 w, u64 ws, u64 nq)
+{
+    u64 r;
+    asm("{\n\t"
+        ".reg .u32 a0, a1, w0, w1, s0, s1, n0, n1, t0, t1, t2, r0, r1;\n\t"
+        "mov.b64 {a0, a1}, %1;\n\t"
+        "mov.b64 {w0, w1}, %2;\n\t"
+        "mov.b64 {s0, s1}, %3;\n\t"
+        "mov.b64 {n0, n1}, %4;\n\t"
+        "mul.hi.u32 t0, a0, s0;\n\t"
+        "mad.lo.cc.u32 t0, a0, s1, t0;\n\t"
+        "madc.hi.u32 t1, a0, s1, 0;\n\t"
+        "mad.lo.cc.u32 t0, a1, s0, t0;\n\t"
+        "madc.hi.cc.u32 t1, a1, s0, t1;\n\t"
+        "madc.hi.u32 t2, a1, s1, 0;\n\t"
+        "mad.lo.cc.u32 t1, a1, s1, t1;\n\t"
+        "addc.u32 t2, t2, 0;\n\t"
+        "mul.lo.u32 r0, a0, w0;\n\t"
+        "mul.hi.u32 r1, a0, w0;\n\t"
+        "mad.lo.u32 r1, a0, w1, r1;\n\t"
+        "mad.lo.u32 r1, a1, w0, r1;\n\t"
+        "mad.lo.cc.u32 r0, t1, n0, r0;\n\t"
+        "madc.hi.u32 r1, t1, n0, r1;\n\t"
+        "mad.lo.u32 r1, t1, n1, r1;\n\t"
+        "mad.lo.u32 r1, t2, n0, r1;\n\t"
+        "mov.b64 %0, {r0, r1};\n\t"
+        "}"
+        : "=l"(r)
+        : "l"(a), "l"(w), "l"(ws), "l"(nq));
+    return r;
+}
+
+template <int ILP, bool PTX>
 __global__ void bfly_loop(u64 *out, u64 q, u64 w0, u64 ws0, int iters)
 {
     u64 x[2 * ILP];
@@ -20,7 +53,7 @@ __global__ void bfly_loop(u64 *out, u64 q, u64 w0, u64 ws0, int iters)
         for (int i = 0; i < ILP; i++) {
             u64 &a = x[2 * i], &b = x[2 * i + 1];
             const u64 X = a >= q2 ? a - q2 : a;
-            const u64 V = shoup_lazy(b, w, ws, q);
+            const u64 V = PTX ? shoup_lazy_ptx(b, w, ws, 0 - q) : shoup_lazy(b, w, ws, q);
             a = X + V;
             b = X + q2 - V;
         }
@@ -31,44 +64,54 @@ __global__ void bfly_loop(u64 *out, u64 q, u64 w0, u64 ws0, int iters)
     out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
-int main()
+__global__ void check(u64 *bad, u64 q, u64 seed)
 {
-    const u64 q = 0x1fffffffffe00001ull;  // 61-bit NTT-friendly prime shape
-    const u64 w = 123456789123ull % q;
-    const u64 ws = (u64)(((unsigned __int128)w << 64) / q);
-    u64 *out;
-    cudaMalloc(&out, 148 * 64 * 1024 * 8);
+    u64 x = seed + threadIdx.x + blockIdx.x * 977ull;
+    for (int i = 0; i < 256; i++) {
+        x = x * 6364136223846793005ull + 1442695040888963407ull;
+        u64 a = x % (4 * q), w = (x >> 7) % q;
+        u64 ws = (u64)(((unsigned __int128)w << 64) / q);
+        u64 r1 = shoup_lazy(a, w, ws, q), r2 = shoup_lazy_ptx(a, w, ws, 0 - q);
+        if (r1 != r2) atomicAdd(bad, 1ull);
+    }
+}
+
+template <int ILP, bool PTX>
+void run(const char *name, u64 *out, u64 q, u64 w, u64 ws, int threads, int bpsm)
+{
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    const int iters = 4096;
-    for (int threads : {256, 512, 1024}) {
-        for (int blocks_per_sm : {1, 2, 4, 8}) {
-            if (threads * blocks_per_sm > 2048) continue;
-            const int blocks = 148 * blocks_per_sm;
-            bfly_loop<4><<<blocks, threads>>>(out, q, w, ws, 16);
-            cudaEventRecord(e0);
-            bfly_loop<4><<<blocks, threads>>>(out, q, w, ws, iters);
-            cudaEventRecord(e1);
-            cudaEventSynchronize(e1);
-            float ms;
-            cudaEventElapsedTime(&ms, e0, e1);
-            double bf = (double)blocks * threads * iters * 4;
-            printf("ILP4 threads %4d x %d/SM: %.3f T bfly/s  (=> %.3f us per 2^16 NTT limb)\n", threads,
-                   blocks_per_sm, bf / ms / 1e9, 524288.0 / (bf / ms / 1e9) * 1e-3 * 1e3 / 1e3);
-        }
-    }
-    for (int threads : {512, 1024}) {
-        const int blocks = 148 * (2048 / threads);
-        bfly_loop<2><<<blocks, threads>>>(out, q, w, ws, iters);
-        cudaEventRecord(e0);
-        bfly_loop<2><<<blocks, threads>>>(out, q, w, ws, iters);
-        cudaEventRecord(e1);
-        cudaEventSynchronize(e1);
-        float ms;
-        cudaEventElapsedTime(&ms, e0, e1);
-        double bf = (double)blocks * threads * iters * 2;
-        printf("ILP2 threads %4d full occ: %.3f T bfly/s\n", threads, bf / ms / 1e9);
-    }
+    const int iters = 4096, blocks = 148 * bpsm;
+    bfly_loop<ILP, PTX><<<blocks, threads>>>(out, q, w, ws, 16);
+    cudaEventRecord(e0);
+    bfly_loop<ILP, PTX><<<blocks, threads>>>(out, q, w, ws, iters);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    double bf = (double)blocks * threads * iters * ILP;
+    printf("%-10s ILP%d %4d thr x %d/SM: %.3f T bfly/s\n", name, ILP, threads, bpsm, bf / ms / 1e9);
+}
+
+int main()
+{
+    const u64 q = 0x1fffffffffe00001ull;
+    const u64 w = 123456789123ull % q;
+    const u64 ws = (u64)(((unsigned __int128)w << 64) / q);
+    u64 *out, *bad;
+    cudaMalloc(&out, 148 * 64 * 1024 * 8);
+    cudaMalloc(&bad, 8);
+    cudaMemset(bad, 0, 8);
+    for (u64 qq : {q, 0xfffffffffc0001ull, 0x3ffffffffe0001ull}) check<<<1024, 256>>>(bad, qq, 12345);
+    u64 nb = 0;
+    cudaMemcpy(&nb, bad, 8, cudaMemcpyDeviceToHost);
+    printf("ptx shoup mismatches: %llu\n", nb);
+    run<4, false>("compiler", out, q, w, ws, 256, 4);
+    run<4, true>("ptx", out, q, w, ws, 256, 4);
+    run<4, false>("compiler", out, q, w, ws, 512, 2);
+    run<4, true>("ptx", out, q, w, ws, 512, 2);
+    run<2, false>("compiler", out, q, w, ws, 1024, 2);
+    run<2, true>("ptx", out, q, w, ws, 1024, 2);
     return 0;
 }

@@ -6,7 +6,10 @@ import workloads as W
 import paper_2410_11184_b200 as hs
 
 pre = W.preset(sys.argv[1] if len(sys.argv) > 1 else "P16")
-cfg = pre["bts"]
+cfg = dict(pre["bts"])
+if len(sys.argv) > 2:
+    cfg["table"] = sys.argv[2]
+print("table", cfg["table"])
 P = hs.Params.from_preset(pre)
 ctx = hs.Context(P, 0)
 gal = sorted({P.galois_of_rot(r) for r in hs.bts_rotations(P, cfg)} | {2 * P.n - 1})

@@ -27,7 +27,10 @@ def cos_table(K, r, deg):
 
 
 def main():
-    out = {"K24_r3_d63": cos_table(24, 3, 63), "K12_r3_d63": cos_table(12, 3, 63)}
+    # (K, r, deg): EvalMod depth = cheb_depth(deg) + r; K24_r4_d31 has the same
+    # depth as K24_r3_d63 (6 + 4 = 7 + 3) with 4 fewer ciphertext products
+    specs = [(24, 3, 63), (12, 3, 63), (24, 2, 127), (24, 1, 255), (24, 4, 63), (24, 3, 31), (24, 4, 31)]
+    out = {f"K{K}_r{r}_d{d}": cos_table(K, r, d) for K, r, d in specs}
     path = os.path.join(os.path.dirname(__file__), "..", "data", "bts_tables.json")
     with open(path, "w") as fh:
         json.dump(out, fh, indent=1)

@@ -432,6 +432,18 @@ orc_ct *orc_op_tensor(const orc_params *P, const orc_ct *a0, const orc_ct *b0)
 
 /* ---------------------------------------------------------------- key switching (C7) */
 
+/* C7 exact centred basis conversion: the integer X = sum_k y_k (S/s_k) lies in
+ * [0, ns S); v = round(X / S) = round(sum_k y_k / s_k) makes X - v S the
+ * centred representative of X mod S.  v in binary64: each quotient (double)y_k
+ * / (double)s_k correctly rounded, summed in k order from 0.0, v = floor(f +
+ * 0.5) (C7). */
+static u64 bconv_round(const u64 *z, size_t stride, size_t t, const u64 *s, int ns)
+{
+    double f = 0.0;
+    for (int k = 0; k < ns; k++) f += (double)z[(size_t)k * stride + t] / (double)s[k];
+    return (u64)floor(f + 0.5);
+}
+
 /* ModUp (C7 first half): digit j = primes [j alpha, min((j+1) alpha, nl)) of d
  * (NTT domain, nl limbs) extended to every target prime q_0..q_level,
  * p_0..p_{np-1}.  Returns ext[j][g][N], NTT domain; the digit's own limbs are
@@ -541,16 +553,15 @@ static void ks_moddown(const orc_params *P, int level, const u64 *acc, u64 *out0
                 php[k] = v;
             }
             u64 *conv = malloc(sizeof(u64) * N);
-            /* centred terms (C7): y_k > (p_k - 1)/2 stands for y_k - p_k, i.e.
-             * the sum loses one P per such k, so the ModDown error is unbiased */
+            /* exact centred conversion (C7): subtract v P, v = round(sum_k y_k / p_k) */
             for (int t = 0; t < N; t++) {
                 u64 s = 0;
                 for (int k = 0; k < np; k++) {
-                    u64 y = z[(size_t)k * N + t], pk = P->prime[nq + k];
+                    u64 y = z[(size_t)k * N + t];
                     s = orc_add(s, orc_mul(y % q, php[k], q), q);
-                    if (y > (pk - 1) / 2) s = orc_sub(s, P->p_mod_q[i], q);
                 }
-                conv[t] = s;
+                u64 v = bconv_round(z, N, t, P->prime + nq, np);
+                conv[t] = orc_sub(s, orc_mul(v, P->p_mod_q[i], q), q);
             }
             orc_ntt_fwd(P, i, conv);
             for (int t = 0; t < N; t++)
@@ -560,6 +571,73 @@ static void ks_moddown(const orc_params *P, int level, const u64 *acc, u64 *out0
         }
         free(z);
     }
+}
+
+/* C8 fused ModDown + rescale: divide the extended accumulator (basis
+ * Q_level u P) by S = P q_level in one centred basis conversion from the
+ * source set {p_0..p_{np-1}, q_level} to q_0..q_{level-1}:
+ *   z_k = iNTT(acc_{s_k}) * (S/s_k)^{-1} mod s_k,
+ *   conv_i = sum_k z_k (S/s_k mod q_i) - #{k: z_k > (s_k-1)/2} (S mod q_i),
+ *   out_i = (acc_i - NTT(conv_i)) S^{-1} mod q_i,  i < level.
+ * acc: [2][level+1+np][N]; out0/out1: level limbs each. */
+static void ks_moddown_rescale(const orc_params *P, int level, const u64 *acc, u64 *out0, u64 *out1)
+{
+    int N = P->n, nq = P->n_q, np = P->n_p;
+    int nl = level + 1, ntg = nl + np, ns = np + 1;
+    int *src = malloc(sizeof(int) * ns), *slot = malloc(sizeof(int) * ns);
+    u64 *sprime = malloc(sizeof(u64) * ns);
+    for (int k = 0; k < np; k++) {
+        src[k] = nq + k;      /* prime index   */
+        slot[k] = nl + k;     /* acc limb      */
+    }
+    src[np] = level;
+    slot[np] = level;
+    for (int k = 0; k < ns; k++) sprime[k] = P->prime[src[k]];
+    for (int c = 0; c < 2; c++) {
+        const u64 *A = acc + (size_t)c * ntg * N;
+        u64 *out = c == 0 ? out0 : out1;
+        u64 *z = malloc(sizeof(u64) * (size_t)ns * N);
+        for (int k = 0; k < ns; k++) {
+            u64 s = P->prime[src[k]], sh = 1;
+            for (int b = 0; b < ns; b++) if (b != k) sh = orc_mul(sh, P->prime[src[b]] % s, s);
+            u64 shi = orc_inv(sh, s);
+            memcpy(z + (size_t)k * N, A + (size_t)slot[k] * N, sizeof(u64) * N);
+            orc_ntt_inv(P, src[k], z + (size_t)k * N);
+            for (int t = 0; t < N; t++) z[(size_t)k * N + t] = orc_mul(z[(size_t)k * N + t], shi, s);
+        }
+        #pragma omp parallel for
+        for (int i = 0; i < level; i++) {
+            u64 q = P->prime[i];
+            u64 *shq = malloc(sizeof(u64) * ns);
+            u64 smq = 1;
+            for (int k = 0; k < ns; k++) {
+                u64 v = 1;
+                for (int b = 0; b < ns; b++) if (b != k) v = orc_mul(v, P->prime[src[b]] % q, q);
+                shq[k] = v;
+                smq = orc_mul(smq, P->prime[src[k]] % q, q);
+            }
+            u64 sinv = orc_inv(smq, q);
+            u64 *conv = malloc(sizeof(u64) * N);
+            for (int t = 0; t < N; t++) {
+                u64 s = 0;
+                for (int k = 0; k < ns; k++) {
+                    u64 y = z[(size_t)k * N + t];
+                    s = orc_add(s, orc_mul(y % q, shq[k], q), q);
+                }
+                u64 v = bconv_round(z, N, t, sprime, ns);
+                conv[t] = orc_sub(s, orc_mul(v, smq, q), q);
+            }
+            orc_ntt_fwd(P, i, conv);
+            for (int t = 0; t < N; t++)
+                out[(size_t)i * N + t] = orc_mul(orc_sub(A[(size_t)i * N + t], conv[t], q), sinv, q);
+            free(conv);
+            free(shq);
+        }
+        free(z);
+    }
+    free(src);
+    free(slot);
+    free(sprime);
 }
 
 /* d: (level+1) limbs NTT domain.  out0/out1: (level+1) limbs NTT domain. */
@@ -596,14 +674,38 @@ orc_ct *orc_op_relin(const orc_params *P, const orc_keys *K, const orc_ct *d)
     return c;
 }
 
-/* C8: HMult = tensor -> relin (KS of d2 under s^2) -> rescale */
+/* C8 relinearise + rescale in one division: acc = sum_j ModUp(d2)_j evk_j
+ * (basis Q_l u P), plus P (d0, d1) on the Q limbs, divided by P q_l
+ * (ks_moddown_rescale).  Output at level l - 1, canonical scale as a rescale. */
+orc_ct *orc_op_relin_rescale(const orc_params *P, const orc_keys *K, const orc_ct *d)
+{
+    const orc_swk *rk = orc_find_key(K, 0);
+    int l = d->level, N = P->n, nl = l + 1, ntg = nl + P->n_p;
+    u64 *ext = ks_modup(P, l, LIMB(P, d, 2, 0));
+    u64 *acc = malloc(sizeof(u64) * (size_t)2 * ntg * N);
+    ks_inner(P, rk, l, ext, NULL, acc);
+    for (int c = 0; c < 2; c++)
+        for (int i = 0; i < nl; i++) {
+            u64 q = P->prime[i];
+            const u64 *x = LIMB(P, d, c, i);
+            u64 *a = acc + ((size_t)c * ntg + i) * N;
+            for (int t = 0; t < N; t++) a[t] = orc_add(a[t], orc_mul(x[t], P->p_mod_q[i], q), q);
+        }
+    orc_ct *r = orc_ct_alloc(P, l - 1, 2);
+    ks_moddown_rescale(P, l, acc, LIMB(P, r, 0, 0), LIMB(P, r, 1, 0));
+    free(acc);
+    free(ext);
+    orc_ledger[LG_KS]++;
+    orc_ledger[LG_RESCALE]++;
+    return r;
+}
+
+/* C8: HMult = tensor -> relinearise + rescale (one division by P q_l) */
 orc_ct *orc_op_mult(const orc_params *P, const orc_keys *K, const orc_ct *a, const orc_ct *b)
 {
     orc_ct *d = orc_op_tensor(P, a, b);
-    orc_ct *c = orc_op_relin(P, K, d);
-    orc_ct *r = orc_op_rescale(P, c);
+    orc_ct *r = orc_op_relin_rescale(P, K, d);
     orc_ct_release(d);
-    orc_ct_release(c);
     orc_ledger[LG_HMULT]++;
     return r;
 }

@@ -98,6 +98,7 @@ orc_ct *orc_op_level_down(const orc_params *P, const orc_ct *a, int target);
 orc_ct *orc_op_rescale(const orc_params *P, const orc_ct *a);
 orc_ct *orc_op_tensor(const orc_params *P, const orc_ct *a, const orc_ct *b);
 orc_ct *orc_op_relin(const orc_params *P, const orc_keys *K, const orc_ct *d);
+orc_ct *orc_op_relin_rescale(const orc_params *P, const orc_keys *K, const orc_ct *d);
 orc_ct *orc_op_mult(const orc_params *P, const orc_keys *K, const orc_ct *a, const orc_ct *b);
 orc_ct *orc_op_mult_int(const orc_params *P, const orc_ct *a, int64_t c);
 orc_ct *orc_op_add_const(const orc_params *P, const orc_ct *a, double c);

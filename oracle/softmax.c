@@ -88,17 +88,15 @@ int orc_softmax(const orc_params *P, const orc_keys *K, const orc_softmax_desc *
         }
         if (y[0]->level < 1) { rc = ORC_ELEVEL; goto done; }
         /* ---- auxiliary thread (Alg 2) ---- */
-        /* step 1 + C15: S = relin(sum_c tensor(y_c, y_c)), then rescale */
+        /* step 1 + C15: S = relin(sum_c tensor(y_c, y_c)) with its rescale (C8) */
         orc_ct *acc = NULL;
         for (int c = 0; c < m; c++) {
             orc_ct *t = orc_op_tensor(P, y[c], y[c]);
             if (!acc) acc = t;
             else { orc_ct *s2 = orc_op_add(P, acc, t); orc_ct_release(acc); orc_ct_release(t); acc = s2; }
         }
-        orc_ct *rl = orc_op_relin(P, K, acc);
+        S = orc_op_relin_rescale(P, K, acc);
         orc_ct_release(acc);
-        S = orc_op_rescale(P, rl);
-        orc_ct_release(rl);
         /* steps 3-5: sum over the coordinate blocks (rotations by -stride 2^i) */
         if ((rc = rot_sum(P, K, &S, nb, stride, -1))) goto done;
         /* G12 (a): bootstrap before step 6 if the rest of the aux thread would

@@ -200,6 +200,47 @@ const BconvTab &bconv_moddown(hs_ctx *c, int level)
     return c->bconv[key] = t;
 }
 
+// C8 fused ModDown + rescale: centred BConv from the sources {q_level,
+// p_0..p_{np-1}} (S = P q_level) to q_0..q_{level-1}; correction S mod q_i.
+const BconvTab &bconv_moddown_rescale(hs_ctx *c, int level)
+{
+    std::lock_guard<std::mutex> g(c->mu);
+    long key = ((long)level << 8) | 254;
+    auto it = c->bconv.find(key);
+    if (it != c->bconv.end()) return it->second;
+    const hs_params *P = c->P;
+    BconvTab t;
+    t.src.push_back(level);
+    for (int k = 0; k < P->n_p; k++) t.src.push_back(P->n_q + k);
+    for (int i = 0; i < level; i++) t.dst.push_back(i);
+    t.n_src = (int)t.src.size();
+    t.n_dst = (int)t.dst.size();
+    t.centred = true;
+    std::vector<u64> h(2 * t.n_src + 2 * (size_t)t.n_src * t.n_dst + t.n_dst);
+    for (int a = 0; a < t.n_src; a++) {
+        u64 sa = P->prime[t.src[a]], sh = 1;
+        for (int b = 0; b < t.n_src; b++)
+            if (b != a) sh = hs_mulmod(sh, P->prime[t.src[b]] % sa, sa);
+        h[2 * a] = hs_invmod(sh, sa);
+        h[2 * a + 1] = hs_shoup_const(h[2 * a], sa);
+        for (int d = 0; d < t.n_dst; d++) {
+            u64 q = P->prime[t.dst[d]], v = 1;
+            for (int b = 0; b < t.n_src; b++)
+                if (b != a) v = hs_mulmod(v, P->prime[t.src[b]] % q, q);
+            size_t ci = 2 * t.n_src + 2 * ((size_t)a * t.n_dst + d);
+            h[ci] = v;
+            h[ci + 1] = hs_shoup_const(v, q);
+        }
+    }
+    for (int d = 0; d < t.n_dst; d++) {
+        u64 q = P->prime[t.dst[d]];
+        h[2 * t.n_src + 2 * (size_t)t.n_src * t.n_dst + d] = hs_mulmod(P->p_mod_q[t.dst[d]], P->prime[level] % q, q);
+    }
+    HS_CUDA(cudaMalloc(&t.dev, h.size() * 8));
+    HS_CUDA(cudaMemcpy(t.dev, h.data(), h.size() * 8, cudaMemcpyHostToDevice));
+    return c->bconv[key] = t;
+}
+
 // C10: out[i] = in[perm[i]], perm[i] = brv(((2 brv(i) + 1) k mod 2N - 1) / 2)
 const unsigned *galois_table(hs_ctx *c, int k)
 {
@@ -286,9 +327,39 @@ void ks_moddown(hs_ctx *c, int level, int B, const u64 *acc, u64 *out, size_t ou
     const BconvTab &md = bconv_moddown(c, level);
     DBuf conv((size_t)B * 2 * nl * N, st);
     k_bconv(c, md, z.p, N, conv.p, N, 2 * B, (size_t)np * N, (size_t)nl * N, st);
-    if (k_ntt_moddown(c, conv.p, acc, ntg, out, out_stride, add, add_stride, add_comps, nl, B, st)) return;
+    if (k_ntt_moddown(c, conv.p, acc, ntg, out, out_stride, add, add_stride, add_comps, nl, nullptr, B, st)) return;
     k_ntt(c, conv.p, 2 * B * nl, pmap_range(0, nl), false, st);
-    k_moddown_final_b(c, acc, conv.p, out, out_stride, add, add_stride, add_comps, level, B, st);
+    k_moddown_final_b(c, acc, ntg, conv.p, nl, out, out_stride, add, add_stride, add_comps, nullptr, B, st);
+}
+
+// C8 fused ModDown + rescale of B accumulators acc [B][2][ntg][N] (basis
+// Q_level u P): ONE centred BConv from {q_level, p_0..} to q_0..q_{level-1},
+// out_b = (acc - conv) (P q_level)^-1 at level - 1 (out: [B][2][level][N]).
+void ks_moddown_rescale(hs_ctx *c, int level, int B, const u64 *acc, u64 *out, size_t out_stride, cudaStream_t st)
+{
+    const hs_params *P = c->P;
+    const size_t N = P->n;
+    const int nl = level + 1, np = P->n_p, ntg = nl + np, ns = np + 1;
+    // the sources q_level, p_0.. are acc limbs level .. ntg-1 of every row
+    DBuf z((size_t)B * 2 * ns * N, st);
+    HS_CUDA(cudaMemcpy2DAsync(z.p, ns * N * 8, acc + (size_t)level * N, ntg * N * 8, ns * N * 8, 2 * B,
+                              cudaMemcpyDeviceToDevice, st));
+    PrimeMap pz;
+    pz.n = ns;
+    pz.p[0] = (unsigned char)level;
+    for (int k = 0; k < np; k++) pz.p[1 + k] = (unsigned char)(P->n_q + k);
+    k_ntt(c, z.p, 2 * B * ns, pz, true, st);
+    const BconvTab &md = bconv_moddown_rescale(c, level);
+    DBuf conv((size_t)B * 2 * level * N, st);
+    k_bconv(c, md, z.p, N, conv.p, N, 2 * B, (size_t)ns * N, (size_t)level * N, st);
+    std::vector<u64> inv(level);
+    for (int i = 0; i < level; i++) {
+        const u64 q = P->prime[i];
+        inv[i] = hs_invmod(hs_mulmod(P->p_mod_q[i], P->prime[level] % q, q), q);
+    }
+    if (k_ntt_moddown(c, conv.p, acc, ntg, out, out_stride, nullptr, 0, 0, level, inv.data(), B, st)) return;
+    k_ntt(c, conv.p, 2 * B * level, pmap_range(0, level), false, st);
+    k_moddown_final_b(c, acc, ntg, conv.p, level, out, out_stride, nullptr, 0, 0, inv.data(), B, st);
 }
 
 // B polynomials d_b = d + b*d_stride (level+1 limbs each, NTT domain);
@@ -549,12 +620,35 @@ CtP ev_relin(const hs_keys *K, const hs_ct *d, cudaStream_t st)
     return r;
 }
 
+// C8: relinearise + rescale as ONE division of (P d + sum ModUp(d2) evk) by
+// P q_level (the P d term rides in the evk inner product); output level - 1.
+CtP ev_relin_rescale(const hs_keys *K, const hs_ct *d, cudaStream_t st)
+{
+    const SwKey *rk = K->find(0);
+    if (!rk) throw HsError(HS_EKEY, "relinearisation key missing");
+    if (d->ncomp != 3) throw HsError(HS_EINVAL, "relin needs a degree-2 ciphertext");
+    if (d->level < 1) throw HsError(HS_ELEVEL, "rescale at level 0");
+    hs_ctx *c = d->ctx;
+    const hs_params *P = c->P;
+    const size_t N = P->n;
+    const int l = d->level, B = d->batch, ntg = l + 1 + P->n_p;
+    const size_t w3 = d->ct_words();
+    ModUpBuf m;
+    ks_modup(c, l, B, d->limb(2, 0), w3, m, st);
+    DBuf acc((size_t)B * 2 * ntg * N, st);
+    k_ks_inner_b(c, d->limb(2, 0), w3, m.ext.p, m.off, m.nd, rk->k, acc.p, l, m.beta, B, st, d->d, w3);
+    CtP r = ct_new(c, l - 1, 2, st, B);
+    ks_moddown_rescale(c, l, B, acc.p, r->d, r->ct_words(), st);
+    c->ledger[HS_LG_KS] += B;
+    c->ledger[HS_LG_RESCALE] += B;
+    return r;
+}
+
 CtP ev_mult(const hs_keys *K, const hs_ct *a, const hs_ct *b, cudaStream_t st)
 {
     CtP t = ev_tensor(a, b, st);
-    CtP r = ev_relin(K, t.get(), st);
     K->ctx->ledger[HS_LG_HMULT] += t->batch;
-    return ev_rescale(r.get(), st);
+    return ev_relin_rescale(K, t.get(), st);
 }
 
 CtP ev_galois(const hs_keys *K, const hs_ct *a, int k, cudaStream_t st)

@@ -213,7 +213,7 @@ void k_moddown_final(hs_ctx *c, const u64 *acc, const u64 *conv, u64 *o0, u64 *o
 void upload_prime_constants(const hs_params *P);
 bool k_ntt_rescale(hs_ctx *c, const u64 *last, u64 *w, const u64 *a, u64 *o, int rows, int l, cudaStream_t st);
 bool k_ntt_moddown(hs_ctx *c, u64 *conv, const u64 *acc, int ntg, u64 *o, size_t o_stride, const u64 *add,
-                   size_t add_stride, int add_comps, int l_plus_1, int B, cudaStream_t st);
+                   size_t add_stride, int add_comps, int nt, const u64 *inv, int B, cudaStream_t st);
 void k_bsgs_inner(hs_ctx *c, const u64 *const *R, int b1, const u64 *pts, const int *tk, int G, int nl, u64 *out,
                   cudaStream_t st);
 void k_mac_pt(hs_ctx *c, u64 *acc, const u64 *a, const u64 *pt, int nl, int la, cudaStream_t st);
@@ -226,13 +226,14 @@ void k_add_scalar_b(hs_ctx *c, u64 *a, const u64 *host_scal, int B, int ncomp, i
 void k_tensor_b(hs_ctx *c, const u64 *a, const u64 *b, u64 *o, int B, int nl, int b_batch, cudaStream_t st);
 void k_tensor_sum(hs_ctx *c, const u64 *a, u64 *o, int B, int nl, cudaStream_t st);
 void k_ks_inner_b(hs_ctx *c, const u64 *d, size_t d_stride, const u64 *ext, const size_t *off, const int *nd,
-                  const u64 *key, u64 *acc, int level, int beta, int B, cudaStream_t st);
+                  const u64 *key, u64 *acc, int level, int beta, int B, cudaStream_t st, const u64 *dadd = nullptr,
+                  size_t dadd_stride = 0);
 void k_ks_inner_m(hs_ctx *c, const u64 *d, size_t d_stride, const u64 *ext, const size_t *off, const int *nd,
                   const u64 *const *keys, int B, u64 *acc, int level, int beta, cudaStream_t st);
 void k_ks_inner_h(hs_ctx *c, const u64 *d, const u64 *ext, const size_t *off, const int *nd, const u64 *const *keys,
                   const unsigned *const *perms, int R, u64 *acc, int level, int beta, cudaStream_t st);
-void k_moddown_final_b(hs_ctx *c, const u64 *acc, const u64 *conv, u64 *o, size_t o_stride, const u64 *add,
-                       size_t add_stride, int add_comps, int level, int B, cudaStream_t st);
+void k_moddown_final_b(hs_ctx *c, const u64 *acc, int ntg, const u64 *conv, int nt, u64 *o, size_t o_stride,
+                       const u64 *add, size_t add_stride, int add_comps, const u64 *inv, int B, cudaStream_t st);
 void k_modraise(hs_ctx *c, const u64 *x, u64 *o, int nl, cudaStream_t st);
 void k_signed_to_rns(hs_ctx *c, const int64_t *v, u64 *o, int n_limbs, const PrimeMap &pm, cudaStream_t st);
 void k_uniform(hs_ctx *c, u64 *o, int n_limbs, const PrimeMap &pm, u64 seed, uint32_t tag, u64 sub,
@@ -274,6 +275,9 @@ CtP ev_rotate(const hs_keys *K, const hs_ct *a, int r, cudaStream_t st);
 CtP ev_rotate_multi(const hs_keys *K, const hs_ct *a, const int *rots, cudaStream_t st);
 CtP ev_rotate_hoisted(const hs_keys *K, const hs_ct *a, const int *rots, int R, cudaStream_t st);
 void ks_modup(hs_ctx *c, int level, int B, const u64 *d, size_t d_stride, ModUpBuf &m, cudaStream_t st);
+void ks_moddown_rescale(hs_ctx *c, int level, int B, const u64 *acc, u64 *out, size_t out_stride, cudaStream_t st);
+const BconvTab &bconv_moddown_rescale(hs_ctx *c, int level);
+CtP ev_relin_rescale(const hs_keys *K, const hs_ct *d, cudaStream_t st);
 void ks_moddown(hs_ctx *c, int level, int B, const u64 *acc, u64 *out, size_t out_stride, const u64 *add,
                 size_t add_stride, int add_comps, cudaStream_t st);
 void ev_keyswitch(const hs_keys *K, const SwKey *key, int level, const u64 *d, u64 *out0, u64 *out1,

@@ -550,15 +550,16 @@ bool k_ntt_rescale(hs_ctx *c, const u64 *last, u64 *w, const u64 *a, u64 *o, int
     return true;
 }
 
-// ModDown tail (C7): the forward transform of conv [B][2][l][N] (BConv of the
-// P limbs) with o_b = add_b + (acc_b - NTT(conv_b)) P^-1 fused into its second
-// pass; acc [B][2][ntg][N].  N = 2^16 only.
+// ModDown tail (C7): the forward transform of conv [B][2][nt][N] (BConv of
+// the special limbs) with o_b = add_b + (acc_b - NTT(conv_b)) inv fused into its
+// second pass; acc [B][2][ntg][N]; inv NULL = P^-1 mod q_i (plain ModDown),
+// else e.g. (P q_l)^-1 for the fused relin + rescale (C8).  N = 2^16 only.
 bool k_ntt_moddown(hs_ctx *c, u64 *conv, const u64 *acc, int ntg, u64 *o, size_t o_stride, const u64 *add,
-                   size_t add_stride, int add_comps, int l_plus_1, int B, cudaStream_t st)
+                   size_t add_stride, int add_comps, int nt, const u64 *inv, int B, cudaStream_t st)
 {
     const hs_params *P = c->P;
     if (P->log_n != 16) return false;
-    const int N = P->n, nl = l_plus_1, n_limbs = 2 * B * nl;
+    const int N = P->n, n_limbs = 2 * B * nt;
     KTimer _kt(c, KID_NTT, (double)n_limbs * N * 16, st);
     ntt16::NttEpi E{};
     E.ain = acc;
@@ -568,12 +569,12 @@ bool k_ntt_moddown(hs_ctx *c, u64 *conv, const u64 *acc, int ntg, u64 *o, size_t
     E.ostr = o_stride;
     E.addstr = add_stride;
     E.add_comps = add ? add_comps : 0;
-    E.l = nl;
-    for (int i = 0; i < nl; i++) {
-        E.inv[i] = P->p_inv_mod_q[i];
-        E.inv_sh[i] = hs_shoup_const(P->p_inv_mod_q[i], P->prime[i]);
+    E.l = nt;
+    for (int i = 0; i < nt; i++) {
+        E.inv[i] = inv ? inv[i] : P->p_inv_mod_q[i];
+        E.inv_sh[i] = hs_shoup_const(E.inv[i], P->prime[i]);
     }
-    const PrimeMap pm = pmap_range(0, nl);
+    const PrimeMap pm = pmap_range(0, nt);
     const u64 *ninv = c->T.tw + (size_t)(P->n_q + P->n_p) * 4 * N;
     ntt16::cols<false, 4, 0><<<dim3(64, n_limbs), 128, 0, st>>>(conv, pm, c->T.tw, ninv, E);
     ntt16::rows<false, 4, 2><<<dim3(64, n_limbs), 128, 0, st>>>(conv, pm, c->T.tw, E);
@@ -883,13 +884,14 @@ __global__ void __launch_bounds__(256) bconv_kernel(const u64 *__restrict__ x, s
     x += blockIdx.y * bxs;
     o += blockIdx.y * bos;
     u64 y[NS];
-    int neg = 0;
+    double f = 0.0;  // C7 exact centred conversion: v = round(sum_a y_a / s_a)
 #pragma unroll
     for (int a = 0; a < NS; a++) {
         const PrimeK k = c_pk[A.src[a]];
         y[a] = d_shoup(x[(size_t)a * xs + t], __ldg(tab + 2 * a), __ldg(tab + 2 * a + 1), k.q);
-        neg += y[a] > (k.q - 1) / 2;
+        if (A.centred) f = __dadd_rn(f, __ddiv_rn(__ull2double_rn(y[a]), __ull2double_rn(k.q)));
     }
+    const int neg = A.centred ? (int)floor(__dadd_rn(f, 0.5)) : 0;
     const u64 *cm = tab + 2 * NS;
     const u64 *pm = cm + 2 * (size_t)NS * A.n_dst;
     const int b0 = blockIdx.z * BCONV_TG, b1 = min(b0 + BCONV_TG, A.n_dst);
@@ -1351,6 +1353,10 @@ struct KsArgB {
     size_t d_stride;
     size_t off[16];
     int nd[16];
+    // C8 fused relin + rescale: acc_c,g += dadd_c,g * (P mod q_g) on the Q limbs
+    const u64 *dadd;  // member b comps 0/1 at dadd + b dadd_stride + (c nl + g) N; NULL = none
+    size_t dadd_stride;
+    u64 pmq[HS_MAXP];
 };
 
 // grid (batch tiles of BT, N / 256, ntg): each thread keeps BT ciphertexts'
@@ -1359,7 +1365,7 @@ struct KsArgB {
 template <int BT>
 __global__ void __launch_bounds__(256) ks_inner_b_kernel(const u64 *__restrict__ d, const u64 *__restrict__ ext,
                                                          const u64 *__restrict__ key, u64 *__restrict__ acc,
-                                                         KsArgB A, int N)
+                                                         const __grid_constant__ KsArgB A, int N)
 {
     int t = blockIdx.y * blockDim.x + threadIdx.x;
     if (t >= N) return;
@@ -1387,6 +1393,17 @@ __global__ void __launch_bounds__(256) ks_inner_b_kernel(const u64 *__restrict__
             mac128(h1[u], l1[u], v, k1);
         }
     }
+    if (A.dadd && g < nl) {
+        const u64 pm = A.pmq[g];
+#pragma unroll
+        for (int u = 0; u < BT; u++) {
+            const int b = b0 + u;
+            if (b >= A.B) break;
+            const u64 *dd = A.dadd + (size_t)b * A.dadd_stride + (size_t)g * N + t;
+            mac128(h0[u], l0[u], dd[0], pm);
+            mac128(h1[u], l1[u], dd[(size_t)nl * N], pm);
+        }
+    }
 #pragma unroll
     for (int u = 0; u < BT; u++) {
         const int b = b0 + u;
@@ -1397,7 +1414,8 @@ __global__ void __launch_bounds__(256) ks_inner_b_kernel(const u64 *__restrict__
 }
 
 void k_ks_inner_b(hs_ctx *c, const u64 *d, size_t d_stride, const u64 *ext, const size_t *off, const int *nd,
-                  const u64 *key, u64 *acc, int level, int beta, int B, cudaStream_t st)
+                  const u64 *key, u64 *acc, int level, int beta, int B, cudaStream_t st, const u64 *dadd,
+                  size_t dadd_stride)
 {
     const hs_params *P = c->P;
     const int ntg = level + 1 + P->n_p;
@@ -1415,6 +1433,10 @@ void k_ks_inner_b(hs_ctx *c, const u64 *d, size_t d_stride, const u64 *ext, cons
         A.off[j] = off[j];
         A.nd[j] = nd[j];
     }
+    A.dadd = dadd;
+    A.dadd_stride = dadd_stride;
+    if (dadd)
+        for (int i = 0; i <= level; i++) A.pmq[i] = P->p_mod_q[i];
     int N = P->n;
     const int tiles = (B + 3) / 4;
     ks_inner_b_kernel<4><<<dim3(tiles, (N + 255) / 256, ntg), 256, 0, st>>>(d, ext, key, acc, A, N);
@@ -1556,46 +1578,45 @@ void k_ks_inner_m(hs_ctx *c, const u64 *d, size_t d_stride, const u64 *ext, cons
     count_kernel(c);
 }
 
-// o_b[c][i] = add_b[c][i] + (acc_b[c][i] - conv_b[c][i]) P^{-1} for b < B;
-// acc [B][2][ntg][N], conv [B][2][nl][N]; o / add with per-ciphertext strides
 struct MdArgB {
     u64 pinv[HS_MAXP], pinv_sh[HS_MAXP];
-    int level, alpha, add_comps;
+    int nt, ntg, add_comps;
     size_t o_stride, add_stride;
 };
 
+// o_b[c][i] = add + (acc_b[c][i] - conv_b[c][i]) inv_i for i < nt;
+// acc [B][2][ntg][N], conv [B][2][nt][N]
 __global__ void moddown_final_b_kernel(const u64 *acc, const u64 *conv, u64 *o, const u64 *add, MdArgB A, int N)
 {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= N) return;
     const int i = blockIdx.y, comp = blockIdx.z & 1, b = blockIdx.z >> 1;
-    const int nl = A.level + 1;
     u64 q = c_pk[i].q;
-    u64 av = acc[(((size_t)b * 2 + comp) * (nl + A.alpha) + i) * N + t];
-    u64 cv = conv[(((size_t)b * 2 + comp) * nl + i) * N + t];
+    u64 av = acc[(((size_t)b * 2 + comp) * A.ntg + i) * N + t];
+    u64 cv = conv[(((size_t)b * 2 + comp) * A.nt + i) * N + t];
     u64 v = d_shoup(d_sub(av, cv, q), A.pinv[i], A.pinv_sh[i], q);
-    size_t ci = ((size_t)comp * nl + i) * N + t;
+    size_t ci = ((size_t)comp * A.nt + i) * N + t;
     if (comp < A.add_comps) v = d_add(v, add[(size_t)b * A.add_stride + ci], q);
     o[(size_t)b * A.o_stride + ci] = v;
 }
 
-void k_moddown_final_b(hs_ctx *c, const u64 *acc, const u64 *conv, u64 *o, size_t o_stride, const u64 *add,
-                       size_t add_stride, int add_comps, int level, int B, cudaStream_t st)
+void k_moddown_final_b(hs_ctx *c, const u64 *acc, int ntg, const u64 *conv, int nt, u64 *o, size_t o_stride,
+                       const u64 *add, size_t add_stride, int add_comps, const u64 *inv, int B, cudaStream_t st)
 {
     const hs_params *P = c->P;
-    KTimer _kt(c, KID_MODDOWN, (double)B * (level + 1) * P->n * 8 * (6 + add_comps), st);
+    KTimer _kt(c, KID_MODDOWN, (double)B * nt * P->n * 8 * (6 + add_comps), st);
     MdArgB A;
-    for (int i = 0; i <= level; i++) {
-        A.pinv[i] = P->p_inv_mod_q[i];
-        A.pinv_sh[i] = hs_shoup_const(P->p_inv_mod_q[i], P->prime[i]);
+    for (int i = 0; i < nt; i++) {
+        A.pinv[i] = inv ? inv[i] : P->p_inv_mod_q[i];
+        A.pinv_sh[i] = hs_shoup_const(A.pinv[i], P->prime[i]);
     }
-    A.level = level;
-    A.alpha = P->n_p;
+    A.nt = nt;
+    A.ntg = ntg;
     A.add_comps = add ? add_comps : 0;
     A.o_stride = o_stride;
     A.add_stride = add_stride;
     int N = P->n;
-    moddown_final_b_kernel<<<dim3((N + 255) / 256, level + 1, 2 * B), 256, 0, st>>>(acc, conv, o, add, A, N);
+    moddown_final_b_kernel<<<dim3((N + 255) / 256, nt, 2 * B), 256, 0, st>>>(acc, conv, o, add, A, N);
     HS_CHECK_LAUNCH();
     count_kernel(c);
 }

@@ -91,10 +91,8 @@ hs_status softmax_run(hs_ctx *c, const hs_keys *K, const hs_softmax_desc *d, con
             for (int r = 1; r < world; r++)
                 k_add(c, acc->d, gathered.p + r * words, acc->d, (int)acc->limbs(), acc->level + 1, false, st);
         }
-        CtP rl = ev_relin(K, acc.get(), st);
+        CtP S = ev_relin_rescale(K, acc.get(), st);  // C8: one division by P q_l
         acc.reset();
-        CtP S = ev_rescale(rl.get(), st);
-        rl.reset();
         rot_sum(K, S, nb, stride, -1, st);
         const int main_level = d->variant == 0 ? y->level : y0->level;
         const int need = poly_cost(ip) + 1 + ((d->variant == 1 && j > 1) ? 1 : 0);

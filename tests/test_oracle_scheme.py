@@ -127,6 +127,29 @@ def test_hoisted_rotations_decrypt_C16(toy):
     assert plain.words().tobytes() != outs[1].words().tobytes()
 
 
+def test_fused_relin_rescale_identity_C8(tiny):
+    """C8 HMult = tensor then ONE division of (P d + sum ModUp(d2) evk) by P q_l:
+    c0' + c1' s == round((d0 + d1 s + d2 s^2) / q_l) + small, in big integers."""
+    P, K = tiny
+    rng = np.random.default_rng(13)
+    a = enc(P, K, rng.uniform(-1, 1, P.n // 2), 3, 0)
+    b = enc(P, K, rng.uniform(-1, 1, P.n // 2), 3, 1)
+    d = O.op(P, K, "tensor", a, b)
+    m = O.op(P, K, "mult", a, b)
+    assert m.level == 2
+    s = [int(v) for v in K.secret()]
+    ints = lambda c, k, lv: coeff_ints(P, c.words()[k], lv)[0]
+    Q3 = coeff_ints(P, d.words()[0], 3)[1]
+    D = [x + y + z for x, y, z in zip(ints(d, 0, 3), R.negacyclic_mul(ints(d, 1, 3), s),
+                                      R.negacyclic_mul(R.negacyclic_mul(ints(d, 2, 3), s), s))]
+    D = [R.centred(v % Q3, Q3) for v in D]
+    ql = P.primes[3]
+    Q2 = coeff_ints(P, m.words()[0], 2)[1]
+    M = [x + y for x, y in zip(ints(m, 0, 2), R.negacyclic_mul(ints(m, 1, 2), s))]
+    err = [R.centred((mv - (2 * dv + ql) // (2 * ql)) % Q2, Q2) for mv, dv in zip(M, D)]
+    assert max(abs(e) for e in err) < 2 ** 20, max(abs(e) for e in err)
+
+
 def test_tensor_identity_C8(tiny):
     """(d0 + d1 s + d2 s^2) == (a0 + a1 s)(b0 + b1 s) exactly mod Q_l."""
     P, K = tiny

@@ -177,6 +177,11 @@ void build_lintrans(hs_ctx *c, const DiagMat &m, int level, int unit, int r, Lin
     HS_CUDA(cudaMalloc(&T.pts, host.size() * 8));
     HS_CUDA(cudaMemcpy(T.pts, host.data(), host.size() * 8, cudaMemcpyHostToDevice));
     k_ntt(c, T.pts, nt * nl, pmap_range(0, nl), false, nullptr);
+    // Montgomery form pt 2^64 mod q_i: the fused BSGS kernel sums 128-bit
+    // products and lands with one REDC
+    u64 r64[HS_MAXP];
+    for (int i = 0; i < nl; i++) r64[i] = P->pk[i].r64;
+    k_mul_scalar(c, T.pts, T.pts, r64, nt * nl, nl, nullptr);
     HS_CUDA(cudaDeviceSynchronize());
 }
 

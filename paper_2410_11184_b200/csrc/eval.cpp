@@ -128,6 +128,11 @@ CtP ct_slice(const hs_ct *a, int b, cudaStream_t st)
 }
 
 // ------------------------------------------------------------------ tables
+// BConv target constants are stored in Montgomery form c 2^64 mod q: the
+// kernels sum y_a c'_a in 128 bits and one REDC (T 2^-64 mod q) lands on
+// sum y_a c_a mod q directly.
+static u64 mont(u64 v, u64 q) { return (u64)(((u128)v << 64) % q); }
+
 const BconvTab &bconv_modup(hs_ctx *c, int level, int digit)
 {
     std::lock_guard<std::mutex> g(c->mu);
@@ -155,7 +160,7 @@ const BconvTab &bconv_modup(hs_ctx *c, int level, int digit)
             for (int b = 0; b < t.n_src; b++)
                 if (b != a) v = hs_mulmod(v, P->prime[t.src[b]] % p, p);
             size_t ci = 2 * t.n_src + 2 * ((size_t)a * t.n_dst + d);
-            h[ci] = v;
+            h[ci] = mont(v, p);  // kernel accumulates 128-bit, one REDC
             h[ci + 1] = hs_shoup_const(v, p);
         }
     }
@@ -190,7 +195,7 @@ const BconvTab &bconv_moddown(hs_ctx *c, int level)
             for (int b = 0; b < t.n_src; b++)
                 if (b != a) v = hs_mulmod(v, P->prime[t.src[b]] % q, q);
             size_t ci = 2 * t.n_src + 2 * ((size_t)a * t.n_dst + d);
-            h[ci] = v;
+            h[ci] = mont(v, q);  // kernel accumulates 128-bit, one REDC
             h[ci + 1] = hs_shoup_const(v, q);
         }
     }
@@ -228,7 +233,7 @@ const BconvTab &bconv_moddown_rescale(hs_ctx *c, int level)
             for (int b = 0; b < t.n_src; b++)
                 if (b != a) v = hs_mulmod(v, P->prime[t.src[b]] % q, q);
             size_t ci = 2 * t.n_src + 2 * ((size_t)a * t.n_dst + d);
-            h[ci] = v;
+            h[ci] = mont(v, q);  // kernel accumulates 128-bit, one REDC
             h[ci + 1] = hs_shoup_const(v, q);
         }
     }

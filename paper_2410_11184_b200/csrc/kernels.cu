@@ -41,6 +41,14 @@ __device__ __forceinline__ u64 d_reduce128(u64 hi, u64 lo, const PrimeK &k)
     return d_shoup(t, k.r64, k.r64sh, k.q);
 }
 __device__ __forceinline__ u64 d_mulmod(u64 a, u64 b, const PrimeK &k) { return d_reduce128(__umul64hi(a, b), a * b, k); }
+// Montgomery REDC alone: T = hi 2^64 + lo < q 2^64  ->  T 2^-64 mod q (for
+// sums against constants stored as c 2^64 mod q)
+__device__ __forceinline__ u64 d_redc(u64 hi, u64 lo, const PrimeK &k)
+{
+    u64 m = lo * k.qinv;
+    u64 t = hi + __umul64hi(m, k.q) + (lo != 0);
+    return t >= k.q ? t - k.q : t;
+}
 // (hi:lo) += a*b as one 32-bit multiply-add carry chain: the four partial
 // products are formed once (mul.lo + mul.hi on 64 bits would form the low ones
 // twice) -- 8 IMAD-class instructions, no IMAD.WIDE
@@ -903,7 +911,7 @@ __global__ void __launch_bounds__(256) bconv_kernel(const u64 *__restrict__ x, s
         u64 hi = 0, lo = 0;
 #pragma unroll
         for (int a = 0; a < NS; a++) mac128(hi, lo, y[a], c[a]);
-        u64 s = d_reduce128(hi, lo, k);
+        u64 s = d_redc(hi, lo, k);  // constants in Montgomery form
         if (A.centred) {
             const u64 pmb = __ldg(pm + b);
             for (int kk = 0; kk < neg; kk++) s = d_sub(s, pmb, k.q);
@@ -948,7 +956,7 @@ __global__ void __launch_bounds__(256) bconv_multi_kernel(const u64 *__restrict_
 #pragma unroll
         for (int a = 0; a < 7; a++)
             if (a < D.n_src) mac128(hi, lo, y[a], __ldg(cm + 2 * ((size_t)a * D.n_dst + b)));
-        o[D.dst_off + (size_t)b * N + t] = d_reduce128(hi, lo, k);
+        o[D.dst_off + (size_t)b * N + t] = d_redc(hi, lo, k);  // constants in Montgomery form
     }
 }
 
@@ -1671,8 +1679,9 @@ __global__ void __launch_bounds__(256) bsgs_inner_kernel(const u64 *__restrict__
                 mac128(h1, l1, r1[b], p);
             }
         }
-        out[((size_t)g * 2 * nl + i) * N + t] = d_reduce128(h0, l0, k);
-        out[((size_t)(g * 2 + 1) * nl + i) * N + t] = d_reduce128(h1, l1, k);
+        // pts are stored in Montgomery form (pt 2^64 mod q): one REDC lands
+        out[((size_t)g * 2 * nl + i) * N + t] = d_redc(h0, l0, k);
+        out[((size_t)(g * 2 + 1) * nl + i) * N + t] = d_redc(h1, l1, k);
     }
 }
 

@@ -2,6 +2,9 @@
 // stream (bench.py's live roofline measurement).
 #include <cstring>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "hs_internal.h"
 
 KTimer::KTimer(hs_ctx *c_, int id_, double bytes_, cudaStream_t st_) : c(c_), id(id_), bytes(bytes_), st(st_), slot(-1)
@@ -51,15 +54,20 @@ hs_status hs_kprof_collect(hs_ctx *c, double *out, int n_classes)
     if (!c || !out) return HS_EINVAL;
     cudaDeviceSynchronize();
     memset(out, 0, sizeof(double) * 3 * n_classes);
+    // dev diagnostic: HS_KPROF_DUMP=path appends one "class,bytes,ms" line per launch
+    const char *dump = getenv("HS_KPROF_DUMP");
+    FILE *fh = dump ? fopen(dump, "a") : nullptr;
     for (size_t i = 0; i < c->kprof_used; i++) {
         float ms = 0;
         cudaEventElapsedTime(&ms, c->kprof_ev[2 * i], c->kprof_ev[2 * i + 1]);
         int id = c->kprof_id[i];
+        if (fh) fprintf(fh, "%d,%.0f,%.6f\n", id, c->kprof_bytes[i], ms);
         if (id >= n_classes) continue;
         out[3 * id] += 1;
         out[3 * id + 1] += ms;
         out[3 * id + 2] += c->kprof_bytes[i];
     }
+    if (fh) fclose(fh);
     c->kprof_used = 0;
     return HS_OK;
 }

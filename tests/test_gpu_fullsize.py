@@ -1,0 +1,63 @@
+"""BASELINE.json configs 2-4 at full size (N = 2^16, preset P16 with
+bootstrapping), in the launch configuration bench.py times (config 3 as a
+CUDA-graph plan).  The oracle cannot run these sizes in test time, so they are
+checked by properties that hold at any size (PAPER.md 466-494: decrypted
+Softmax vs float64 Softmax; north_star tolerance 2^-15), by determinism
+(graph replay == eager call, word for word), and -- for the primitives at this
+ring -- by tests/test_gpu_parity.py::test_p16_hmult_rotate_parity."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _accuracy(S, outs):
+    hs, K = S["hs"], S["K"]
+    dec = np.stack([hs.decrypt_decode(K, c).real for c in outs])
+    y = S["P"].unpack(dec, S["L"], S["n"])
+    x = S["x"]
+    ref = np.exp(x - x.max(1, keepdims=True))
+    ref /= ref.sum(1, keepdims=True)
+    return float(np.abs(y - ref).max())
+
+
+def _run(S):
+    hs, tab, wl = S["hs"], S["tab"], S["wl"]
+    return hs.softmax_many_ctxt(S["K"], S["cts"], S["n"], S["m"], S["k"], wl["variant"], tab["exp"], tab["inv"],
+                                bts=S["B"])
+
+
+def test_config3_plan_full_size():
+    import bench
+    S = bench.build_setup("config3", 0, 1, 0)
+    hs, tab, wl = S["hs"], S["tab"], S["wl"]
+    eager = _run(S)
+    plan = hs.Plan(S["K"], S["cts"], S["n"], S["m"], S["k"], wl["variant"], tab["exp"], tab["inv"], bts=S["B"])
+    outs = plan.run()
+    for i in (0, 31, 63):
+        assert (outs[i].words() == eager[i].words()).all(), i
+    err = _accuracy(S, outs)
+    assert err < 2.0 ** -15, np.log2(err)
+    led = S["ctx"].ledger()
+    assert led["bts"] >= 10
+
+
+@pytest.mark.parametrize("wl", ["config4", "config2"])
+def test_configs_full_size_accuracy(wl):
+    import bench
+    S = bench.build_setup(wl, 0, 1, 0)
+    S["ctx"].ledger_reset()
+    outs = _run(S)
+    err = _accuracy(S, outs)
+    led = S["ctx"].ledger()
+    # version B never bootstraps the main thread (PAPER.md 444-447): 2 per iteration, all in the aux thread
+    if S["wl"]["variant"] == "B":
+        assert led["bts"] == 2 * S["k"]
+    assert err < 2.0 ** -15, (wl, np.log2(err))

@@ -41,6 +41,24 @@ __device__ __forceinline__ u64 shoup_lazy_ptx(u64 a, u64 w, u64 ws, u64 nq)
     return r;
 }
 
+// 64-bit a + b and a - b as explicit 32-bit carry chains (ALU pipe adds)
+__device__ __forceinline__ u64 add64(u64 a, u64 b)
+{
+    u64 r;
+    asm("{\n\t.reg .u32 a0, a1, b0, b1;\n\tmov.b64 {a0, a1}, %1;\n\tmov.b64 {b0, b1}, %2;\n\t"
+        "add.cc.u32 a0, a0, b0;\n\taddc.u32 a1, a1, b1;\n\tmov.b64 %0, {a0, a1};\n\t}"
+        : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ u64 sub64(u64 a, u64 b)
+{
+    u64 r;
+    asm("{\n\t.reg .u32 a0, a1, b0, b1;\n\tmov.b64 {a0, a1}, %1;\n\tmov.b64 {b0, b1}, %2;\n\t"
+        "sub.cc.u32 a0, a0, b0;\n\tsubc.u32 a1, a1, b1;\n\tmov.b64 %0, {a0, a1};\n\t}"
+        : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+
 template <int ILP, bool PTX>
 __global__ void bfly_loop(u64 *out, u64 q, u64 w0, u64 ws0, int iters)
 {
@@ -52,10 +70,17 @@ __global__ void bfly_loop(u64 *out, u64 q, u64 w0, u64 ws0, int iters)
 #pragma unroll
         for (int i = 0; i < ILP; i++) {
             u64 &a = x[2 * i], &b = x[2 * i + 1];
-            const u64 X = a >= q2 ? a - q2 : a;
-            const u64 V = PTX ? shoup_lazy_ptx(b, w, ws, 0 - q) : shoup_lazy(b, w, ws, q);
-            a = X + V;
-            b = X + q2 - V;
+            if (PTX) {
+                const u64 X = a >= q2 ? sub64(a, q2) : a;
+                const u64 V = shoup_lazy(b, w, ws, q);
+                a = add64(X, V);
+                b = sub64(add64(X, q2), V);
+            } else {
+                const u64 X = a >= q2 ? a - q2 : a;
+                const u64 V = shoup_lazy(b, w, ws, q);
+                a = X + V;
+                b = X + q2 - V;
+            }
         }
         w += 2;
     }
@@ -108,10 +133,10 @@ int main()
     cudaMemcpy(&nb, bad, 8, cudaMemcpyDeviceToHost);
     printf("ptx shoup mismatches: %llu\n", nb);
     run<4, false>("compiler", out, q, w, ws, 256, 4);
-    run<4, true>("ptx", out, q, w, ws, 256, 4);
+    run<4, true>("ptx-adds", out, q, w, ws, 256, 4);
     run<4, false>("compiler", out, q, w, ws, 512, 2);
-    run<4, true>("ptx", out, q, w, ws, 512, 2);
+    run<4, true>("ptx-adds", out, q, w, ws, 512, 2);
     run<2, false>("compiler", out, q, w, ws, 1024, 2);
-    run<2, true>("ptx", out, q, w, ws, 1024, 2);
+    run<2, true>("ptx-adds", out, q, w, ws, 1024, 2);
     return 0;
 }

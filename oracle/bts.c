@@ -28,6 +28,8 @@
 
 void orc_encode_coeffs_q(const orc_params *P, const __float128 *re, const __float128 *im, double scale, int level,
                          u64 *out);
+void orc_encode_coeffs_q_pq(const orc_params *P, const __float128 *re, const __float128 *im, double scale, int level,
+                            u64 *out);
 
 typedef __float128 f128;
 typedef struct { f128 re, im; } qz;
@@ -216,9 +218,12 @@ static void make_ltrans(const orc_params *P, const dmat *m, int level, int u, in
             re[p] = x.re;
             im[p] = x.im;
         }
-        u64 *pt = malloc(sizeof(u64) * (size_t)(level + 1) * N);
-        orc_encode_coeffs_q(P, re, im, sc, level, pt);
-        for (int i = 0; i <= level; i++) orc_ntt_fwd(P, i, pt + (size_t)i * N);
+        /* C17: plaintexts in the extended basis Q_level u P */
+        int ntg = level + 1 + P->n_p;
+        u64 *pt = malloc(sizeof(u64) * (size_t)ntg * N);
+        orc_encode_coeffs_q_pq(P, re, im, sc, level, pt);
+        for (int gi = 0; gi < ntg; gi++)
+            orc_ntt_fwd(P, gi <= level ? gi : P->n_q + (gi - level - 1), pt + (size_t)gi * N);
         T->pt[k] = pt;
         free(re);
         free(im);
@@ -332,66 +337,123 @@ static void plan_free(orc_bts_plan *B)
     free(B);
 }
 
-/* ct (2 comps) -> transform at level T->level, landing at level-1 */
+/* prime index of limb g of the extended basis Q_level u P */
+static int ext_prime(const orc_params *P, int nl, int g) { return g < nl ? g : P->n_q + (g - nl); }
+
+/* C17 double-hoisted BSGS (C17), ct (2 comps) -> transform at
+ * level T->level, landing at level-1.  Every intermediate lives in the
+ * extended basis Q_l u P ("PQ", ntg = l+1+np limbs, a value v stands for P v):
+ *   R_0 = P x; R_b = (P sigma_b(c0) + <sigma_b(ModUp(c1)), evk_b>_0,
+ *                     <sigma_b(ModUp(c1)), evk_b>_1)  (one ModUp, no ModDown)
+ *   inner_g = sum_b pt_{g,b} (.) R_b  (plaintexts encoded in PQ)
+ *   giant g != 0:  b' = ModDown(inner_g,1);  Rot = (sigma_g(inner_g,0) +
+ *                  <ModUp(sigma_g(b')), evk_g>_0, <...>_1)   (no ModDown)
+ *   out = ModDown+rescale by P q_l (C8) of inner_0 + sum_g Rot_g. */
 static orc_ct *apply_ltrans(const orc_params *P, const orc_keys *K, const orc_ct *ct0, const ltrans *T)
 {
-    int N = P->n, n0 = N / 2, l = T->level;
-    orc_ct *ct = orc_op_level_down(P, ct0, l);
-    /* baby rotations, hoisted (C16): one ModUp of ct's c1 serves every b != 0,
-     * in increasing b */
-    orc_ct *R[64] = {0};
-    int present[64] = {0}, rots[64], bs[64], nr = 0;
+    int N = P->n, n0 = N / 2, l = T->level, nl = l + 1, np = P->n_p, ntg = nl + np;
+    size_t W = (size_t)2 * ntg * N;   /* one PQ ciphertext */
+    orc_ct *x = orc_op_level_down(P, ct0, l);
+    unsigned *perm = malloc(sizeof(unsigned) * N);
+    u64 *R[64] = {0};
+    int present[64] = {0};
     for (int k = 0; k < T->n_terms; k++) present[T->b[k]] = 1;
-    for (int b = 1; b < 64; b++)
-        if (present[b]) {
-            bs[nr] = b;
-            rots[nr++] = b * T->u;
+    if (present[0]) {             /* R_0 = P x: Q limbs x (P mod q_i), P limbs 0 */
+        R[0] = calloc(W, sizeof(u64));
+        for (int c = 0; c < 2; c++)
+            for (int i = 0; i < nl; i++) {
+                u64 q = P->prime[i];
+                const u64 *s = LIMB(P, x, c, i);
+                u64 *o = R[0] + ((size_t)c * ntg + i) * N;
+                for (int t = 0; t < N; t++) o[t] = orc_mul(s[t], P->p_mod_q[i], q);
+            }
+    }
+    int any = 0;
+    for (int b = 1; b < 64; b++) any |= present[b];
+    u64 *ext = any ? orc_ks_modup(P, l, LIMB(P, x, 1, 0)) : NULL;
+    for (int b = 1; b < 64; b++) {    /* babies in increasing b */
+        if (!present[b]) continue;
+        int k = orc_galois_of_rot(P, b * T->u);
+        const orc_swk *key = orc_find_key(K, k);
+        if (!key) return NULL;
+        orc_galois_perm(P, k, perm);
+        R[b] = malloc(sizeof(u64) * W);
+        orc_ks_inner(P, key, l, ext, perm, R[b]);
+        for (int i = 0; i < nl; i++) {      /* + P sigma_b(c0) on the Q limbs */
+            u64 q = P->prime[i];
+            const u64 *c0 = LIMB(P, x, 0, i);
+            u64 *o = R[b] + (size_t)i * N;
+            for (int t = 0; t < N; t++) o[t] = orc_add(o[t], orc_mul(c0[perm[t]], P->p_mod_q[i], q), q);
         }
-    if (present[0]) R[0] = orc_ct_copy(P, ct);
-    orc_ct *hr[64];
-    if (nr && orc_op_rotate_hoisted(P, K, ct, rots, nr, hr) != 0) return NULL;
-    for (int i = 0; i < nr; i++) R[bs[i]] = hr[i];
+        orc_ledger[LG_KS]++;
+        orc_ledger[LG_ROT]++;
+    }
+    free(ext);
     int maxg = 0;
     for (int k = 0; k < T->n_terms; k++) if (T->g[k] > maxg) maxg = T->g[k];
-    orc_ct *acc = orc_ct_alloc(P, l, 2);
+    u64 *acc = calloc(W, sizeof(u64)), *inner = malloc(sizeof(u64) * W);
+    u64 *bq = malloc(sizeof(u64) * (size_t)nl * N), *sb = malloc(sizeof(u64) * (size_t)nl * N);
+    u64 *rot = malloc(sizeof(u64) * W);
     for (int g = 0; g <= maxg; g++) {
-        orc_ct *inner = NULL;
+        int have = 0;
+        memset(inner, 0, sizeof(u64) * W);
         for (int k = 0; k < T->n_terms; k++) {
             if (T->g[k] != g) continue;
-            if (!inner) inner = orc_ct_alloc(P, l, 2);
-            const orc_ct *Rb = R[T->b[k]];
-            for (int i = 0; i <= l; i++) {
-                u64 q = P->prime[i];
-                const u64 *m = T->pt[k] + (size_t)i * N;
+            have = 1;
+            const u64 *Rb = R[T->b[k]];
+            for (int gi = 0; gi < ntg; gi++) {
+                u64 q = P->prime[ext_prime(P, nl, gi)];
+                const u64 *m = T->pt[k] + (size_t)gi * N;
                 for (int c = 0; c < 2; c++) {
-                    u64 *o = LIMB(P, inner, c, i);
-                    const u64 *s = LIMB(P, Rb, c, i);
-                    for (int t = 0; t < N; t++) o[t] = orc_add(o[t], orc_mul(s[t], m[t], q), q);
+                    u64 *o = inner + ((size_t)c * ntg + gi) * N;
+                    const u64 *sv = Rb + ((size_t)c * ntg + gi) * N;
+                    for (int t = 0; t < N; t++) o[t] = orc_add(o[t], orc_mul(sv[t], m[t], q), q);
                 }
             }
             orc_ledger[LG_PMULT]++;
         }
-        if (!inner) continue;
+        if (!have) continue;
+        const u64 *add = inner;
         if (g != 0) {
-            orc_ct *rot = orc_op_rotate(P, K, inner, (g * T->b1 * T->u) % n0);
-            orc_ct_release(inner);
-            if (!rot) return NULL;
-            inner = rot;
-        }
-        for (int i = 0; i <= l; i++) {
-            u64 q = P->prime[i];
-            for (int c = 0; c < 2; c++) {
-                u64 *o = LIMB(P, acc, c, i);
-                const u64 *s = LIMB(P, inner, c, i);
-                for (int t = 0; t < N; t++) o[t] = orc_add(o[t], s[t], q);
+            int k = orc_galois_of_rot(P, (g * T->b1 * T->u) % n0);
+            const orc_swk *key = orc_find_key(K, k);
+            if (!key) return NULL;
+            orc_galois_perm(P, k, perm);
+            orc_ks_moddown1(P, l, inner + (size_t)ntg * N, bq);     /* b' = ModDown(inner_1) */
+            for (int i = 0; i < nl; i++)                            /* sigma_g(b') */
+                for (int t = 0; t < N; t++) sb[(size_t)i * N + t] = bq[(size_t)i * N + perm[t]];
+            u64 *e2 = orc_ks_modup(P, l, sb);
+            orc_ks_inner(P, key, l, e2, NULL, rot);
+            free(e2);
+            for (int gi = 0; gi < ntg; gi++) {                      /* + sigma_g(inner_0), all PQ limbs */
+                u64 q = P->prime[ext_prime(P, nl, gi)];
+                const u64 *a0 = inner + (size_t)gi * N;
+                u64 *o = rot + (size_t)gi * N;
+                for (int t = 0; t < N; t++) o[t] = orc_add(o[t], a0[perm[t]], q);
             }
+            orc_ledger[LG_KS]++;
+            orc_ledger[LG_ROT]++;
+            add = rot;
         }
-        orc_ct_release(inner);
+        for (int c = 0; c < 2; c++)
+            for (int gi = 0; gi < ntg; gi++) {
+                u64 q = P->prime[ext_prime(P, nl, gi)];
+                u64 *o = acc + ((size_t)c * ntg + gi) * N;
+                const u64 *sv = add + ((size_t)c * ntg + gi) * N;
+                for (int t = 0; t < N; t++) o[t] = orc_add(o[t], sv[t], q);
+            }
     }
-    for (int b = 0; b < 64; b++) orc_ct_release(R[b]);
-    orc_ct_release(ct);
-    orc_ct *out = orc_op_rescale(P, acc);
-    orc_ct_release(acc);
+    orc_ct *out = orc_ct_alloc(P, l - 1, 2);
+    orc_ks_moddown_rescale(P, l, acc, LIMB(P, out, 0, 0), LIMB(P, out, 1, 0));
+    orc_ledger[LG_RESCALE]++;
+    for (int b = 0; b < 64; b++) free(R[b]);
+    free(acc);
+    free(inner);
+    free(bq);
+    free(sb);
+    free(rot);
+    free(perm);
+    orc_ct_release(x);
     return out;
 }
 

@@ -448,7 +448,7 @@ static u64 bconv_round(const u64 *z, size_t stride, size_t t, const u64 *s, int 
  * (NTT domain, nl limbs) extended to every target prime q_0..q_level,
  * p_0..p_{np-1}.  Returns ext[j][g][N], NTT domain; the digit's own limbs are
  * d's limbs unchanged. */
-static u64 *ks_modup(const orc_params *P, int level, const u64 *d)
+u64 *orc_ks_modup(const orc_params *P, int level, const u64 *d)
 {
     int N = P->n, nq = P->n_q, np = P->n_p, alpha = P->alpha;
     int nl = level + 1, beta = (nl + alpha - 1) / alpha, ntg = nl + np;
@@ -501,7 +501,7 @@ static u64 *ks_modup(const orc_params *P, int level, const u64 *d)
 
 /* inner product with the evaluation key: acc[c][g] = sum_j sigma(ext_j)[g] key_j[c][g]
  * where sigma(v)[t] = v[perm[t]] (perm NULL = identity).  acc[2][ntg][N]. */
-static void ks_inner(const orc_params *P, const orc_swk *key, int level, const u64 *ext, const unsigned *perm,
+void orc_ks_inner(const orc_params *P, const orc_swk *key, int level, const u64 *ext, const unsigned *perm,
                      u64 *acc)
 {
     int N = P->n, nq = P->n_q, np = P->n_p, nt = nq + np, alpha = P->alpha;
@@ -526,13 +526,12 @@ static void ks_inner(const orc_params *P, const orc_swk *key, int level, const u
 }
 
 /* ModDown (C7 second half): out_c = (acc_Q - BConv_{P->Q}(acc_P)) * P^{-1} */
-static void ks_moddown(const orc_params *P, int level, const u64 *acc, u64 *out0, u64 *out1)
+/* ModDown of ONE component A [ntg][N] (basis Q_level u P) -> out [nl][N] */
+void orc_ks_moddown1(const orc_params *P, int level, const u64 *A, u64 *out)
 {
     int N = P->n, nq = P->n_q, np = P->n_p;
-    int nl = level + 1, ntg = nl + np;
-    for (int c = 0; c < 2; c++) {
-        const u64 *A = acc + (size_t)c * ntg * N;
-        u64 *out = c == 0 ? out0 : out1;
+    int nl = level + 1;
+    {
         u64 *z = malloc(sizeof(u64) * (size_t)np * N);
         for (int k = 0; k < np; k++) {
             int pi = nq + k;
@@ -573,6 +572,13 @@ static void ks_moddown(const orc_params *P, int level, const u64 *acc, u64 *out0
     }
 }
 
+static void ks_moddown(const orc_params *P, int level, const u64 *acc, u64 *out0, u64 *out1)
+{
+    size_t ntg = (size_t)level + 1 + P->n_p;
+    orc_ks_moddown1(P, level, acc, out0);
+    orc_ks_moddown1(P, level, acc + ntg * P->n, out1);
+}
+
 /* C8 fused ModDown + rescale: divide the extended accumulator (basis
  * Q_level u P) by S = P q_level in one centred basis conversion from the
  * source set {p_0..p_{np-1}, q_level} to q_0..q_{level-1}:
@@ -580,7 +586,7 @@ static void ks_moddown(const orc_params *P, int level, const u64 *acc, u64 *out0
  *   conv_i = sum_k z_k (S/s_k mod q_i) - #{k: z_k > (s_k-1)/2} (S mod q_i),
  *   out_i = (acc_i - NTT(conv_i)) S^{-1} mod q_i,  i < level.
  * acc: [2][level+1+np][N]; out0/out1: level limbs each. */
-static void ks_moddown_rescale(const orc_params *P, int level, const u64 *acc, u64 *out0, u64 *out1)
+void orc_ks_moddown_rescale(const orc_params *P, int level, const u64 *acc, u64 *out0, u64 *out1)
 {
     int N = P->n, nq = P->n_q, np = P->n_p;
     int nl = level + 1, ntg = nl + np, ns = np + 1;
@@ -644,9 +650,9 @@ static void ks_moddown_rescale(const orc_params *P, int level, const u64 *acc, u
 void orc_keyswitch(const orc_params *P, const orc_swk *key, int level, const u64 *d, u64 *out0, u64 *out1)
 {
     int ntg = level + 1 + P->n_p;
-    u64 *ext = ks_modup(P, level, d);
+    u64 *ext = orc_ks_modup(P, level, d);
     u64 *acc = malloc(sizeof(u64) * (size_t)2 * ntg * P->n);
-    ks_inner(P, key, level, ext, NULL, acc);
+    orc_ks_inner(P, key, level, ext, NULL, acc);
     ks_moddown(P, level, acc, out0, out1);
     free(acc);
     free(ext);
@@ -681,9 +687,9 @@ orc_ct *orc_op_relin_rescale(const orc_params *P, const orc_keys *K, const orc_c
 {
     const orc_swk *rk = orc_find_key(K, 0);
     int l = d->level, N = P->n, nl = l + 1, ntg = nl + P->n_p;
-    u64 *ext = ks_modup(P, l, LIMB(P, d, 2, 0));
+    u64 *ext = orc_ks_modup(P, l, LIMB(P, d, 2, 0));
     u64 *acc = malloc(sizeof(u64) * (size_t)2 * ntg * N);
-    ks_inner(P, rk, l, ext, NULL, acc);
+    orc_ks_inner(P, rk, l, ext, NULL, acc);
     for (int c = 0; c < 2; c++)
         for (int i = 0; i < nl; i++) {
             u64 q = P->prime[i];
@@ -692,7 +698,7 @@ orc_ct *orc_op_relin_rescale(const orc_params *P, const orc_keys *K, const orc_c
             for (int t = 0; t < N; t++) a[t] = orc_add(a[t], orc_mul(x[t], P->p_mod_q[i], q), q);
         }
     orc_ct *r = orc_ct_alloc(P, l - 1, 2);
-    ks_moddown_rescale(P, l, acc, LIMB(P, r, 0, 0), LIMB(P, r, 1, 0));
+    orc_ks_moddown_rescale(P, l, acc, LIMB(P, r, 0, 0), LIMB(P, r, 1, 0));
     free(acc);
     free(ext);
     orc_ledger[LG_KS]++;
@@ -757,7 +763,7 @@ int orc_op_rotate_hoisted(const orc_params *P, const orc_keys *K, const orc_ct *
                           orc_ct **out)
 {
     int N = P->n, l = a->level, ntg = l + 1 + P->n_p;
-    u64 *ext = ks_modup(P, l, LIMB(P, a, 1, 0));
+    u64 *ext = orc_ks_modup(P, l, LIMB(P, a, 1, 0));
     u64 *acc = malloc(sizeof(u64) * (size_t)2 * ntg * N);
     unsigned *perm = malloc(sizeof(unsigned) * N);
     int rc = 0;
@@ -770,7 +776,7 @@ int orc_op_rotate_hoisted(const orc_params *P, const orc_keys *K, const orc_ct *
             break;
         }
         orc_galois_perm(P, k, perm);
-        ks_inner(P, key, l, ext, perm, acc);
+        orc_ks_inner(P, key, l, ext, perm, acc);
         orc_ct *r = orc_ct_alloc(P, l, 2);
         ks_moddown(P, l, acc, LIMB(P, r, 0, 0), LIMB(P, r, 1, 0));
         for (int j = 0; j <= l; j++) {

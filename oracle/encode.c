@@ -61,7 +61,7 @@ static void fft(qc *a, int log_n2, int sign)
     }
 }
 
-static void encode_finish(const orc_params *P, qc *w, double scale, int level, u64 *out);
+static void encode_finish(const orc_params *P, qc *w, double scale, int level, int with_p, u64 *out);
 
 /* out: (level+1) limbs of N residues, coefficient domain. */
 void orc_encode_coeffs(const orc_params *P, const double *re, const double *im, double scale, int level, u64 *out)
@@ -75,7 +75,7 @@ void orc_encode_coeffs(const orc_params *P, const double *re, const double *im, 
         w[g].im = im ? im[j] : 0;
         g = (g * 5) % (u64)n2;
     }
-    encode_finish(P, w, scale, level, out);
+    encode_finish(P, w, scale, level, 0, out);
 }
 
 /* the same from quad-precision slot values (bootstrapping diagonals, G11) */
@@ -91,10 +91,27 @@ void orc_encode_coeffs_q(const orc_params *P, const __float128 *re, const __floa
         w[g].im = im[j];
         g = (g * 5) % (u64)n2;
     }
-    encode_finish(P, w, scale, level, out);
+    encode_finish(P, w, scale, level, 0, out);
 }
 
-static void encode_finish(const orc_params *P, qc *w, double scale, int level, u64 *out)
+/* ... and in the extended basis Q_level u P: limbs q_0..q_level then p_0..p_{np-1}
+ * of the same integer coefficients (C17 double-hoisted BSGS plaintexts) */
+void orc_encode_coeffs_q_pq(const orc_params *P, const __float128 *re, const __float128 *im, double scale, int level,
+                            u64 *out)
+{
+    int N = P->n, N0 = N / 2, n2 = 2 * N;
+    ensure_twiddles(P->log_n);
+    qc *w = calloc(n2, sizeof(qc));
+    u64 g = 1;
+    for (int j = 0; j < N0; j++) {
+        w[g].re = re[j];
+        w[g].im = im[j];
+        g = (g * 5) % (u64)n2;
+    }
+    encode_finish(P, w, scale, level, 1, out);
+}
+
+static void encode_finish(const orc_params *P, qc *w, double scale, int level, int with_p, u64 *out)
 {
     int N = P->n;
     fft(w, P->log_n + 1, -1);
@@ -107,6 +124,12 @@ static void encode_finish(const orc_params *P, qc *w, double scale, int level, u
             i128 r = m % q;
             if (r < 0) r += q;
             out[(size_t)i * N + t] = (u64)r;
+        }
+        for (int k = 0; with_p && k < P->n_p; k++) {
+            i128 q = (i128)P->prime[P->n_q + k];
+            i128 r = m % q;
+            if (r < 0) r += q;
+            out[(size_t)(level + 1 + k) * N + t] = (u64)r;
         }
     }
     free(w);

@@ -110,6 +110,14 @@ orc_ct *orc_op_conjugate(const orc_params *P, const orc_keys *K, const orc_ct *a
 int orc_op_rotate_hoisted(const orc_params *P, const orc_keys *K, const orc_ct *a, const int *rots, int n,
                           orc_ct **out);
 void orc_keyswitch(const orc_params *P, const orc_swk *key, int level, const u64 *d, u64 *out0, u64 *out1);
+/* key-switch pieces (C7): ModUp -> [beta][ntg][N]; inner product (perm NULL
+ * or a Galois permutation of the extended digits) -> acc [2][ntg][N]; ModDown
+ * of one component; fused ModDown + rescale by P q_level (C8) */
+u64 *orc_ks_modup(const orc_params *P, int level, const u64 *d);
+void orc_ks_inner(const orc_params *P, const orc_swk *key, int level, const u64 *ext, const unsigned *perm,
+                  u64 *acc);
+void orc_ks_moddown1(const orc_params *P, int level, const u64 *A, u64 *out);
+void orc_ks_moddown_rescale(const orc_params *P, int level, const u64 *acc, u64 *out0, u64 *out1);
 const orc_swk *orc_find_key(const orc_keys *K, int galois);
 int orc_galois_of_rot(const orc_params *P, int r);
 

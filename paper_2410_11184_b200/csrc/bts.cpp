@@ -145,10 +145,12 @@ struct LinTrans {
     ~LinTrans() { if (pts) cudaFree(pts); }
 };
 
+// C17: plaintexts in the extended basis Q_level u P ([terms][ntg][N], NTT
+// domain, Montgomery form) for the double-hoisted BSGS
 void build_lintrans(hs_ctx *c, const DiagMat &m, int level, int unit, int r, LinTrans &T)
 {
     const hs_params *P = c->P;
-    const int n0 = P->n / 2, N = P->n, nl = level + 1;
+    const int n0 = P->n / 2, N = P->n, nl = level + 1, ntg = nl + P->n_p;
     T.level = level;
     T.unit = unit;
     T.b1 = 1 << ((r + 2) / 2);
@@ -161,7 +163,7 @@ void build_lintrans(hs_ctx *c, const DiagMat &m, int level, int unit, int r, Lin
         }
     const int nt = (int)ds.size();
     const double sc = (P->scale[level - 1] * (double)P->prime[level]) / P->scale[level];
-    std::vector<u64> host((size_t)nt * nl * N);
+    std::vector<u64> host((size_t)nt * ntg * N);
 #pragma omp parallel for schedule(dynamic)
     for (int k = 0; k < nt; k++) {
         const int G = (T.g[k] * T.b1 * unit) % n0;
@@ -172,16 +174,19 @@ void build_lintrans(hs_ctx *c, const DiagMat &m, int level, int unit, int r, Lin
             re[p] = x.re;
             im[p] = x.im;
         }
-        hs_encode_impl_q(P, re.data(), im.data(), sc, level, host.data() + (size_t)k * nl * N);
+        hs_encode_impl_q(P, re.data(), im.data(), sc, level, host.data() + (size_t)k * ntg * N, true);
     }
     HS_CUDA(cudaMalloc(&T.pts, host.size() * 8));
     HS_CUDA(cudaMemcpy(T.pts, host.data(), host.size() * 8, cudaMemcpyHostToDevice));
-    k_ntt(c, T.pts, nt * nl, pmap_range(0, nl), false, nullptr);
-    // Montgomery form pt 2^64 mod q_i: the fused BSGS kernel sums 128-bit
+    PrimeMap pm;
+    pm.n = ntg;
+    for (int i = 0; i < ntg; i++) pm.p[i] = (unsigned char)(i < nl ? i : P->n_q + (i - nl));
+    k_ntt(c, T.pts, nt * ntg, pm, false, nullptr);
+    // Montgomery form pt 2^64 mod p: the fused BSGS kernel sums 128-bit
     // products and lands with one REDC
     u64 r64[HS_MAXP];
-    for (int i = 0; i < nl; i++) r64[i] = P->pk[i].r64;
-    k_mul_scalar(c, T.pts, T.pts, r64, nt * nl, nl, nullptr);
+    for (int i = 0; i < ntg; i++) r64[i] = P->pk[pm.p[i]].r64;
+    k_mul_scalar_pm(c, T.pts, T.pts, r64, nt * ntg, pm, nullptr);
     HS_CUDA(cudaDeviceSynchronize());
 }
 
@@ -277,30 +282,72 @@ static std::vector<std::unique_ptr<LinTrans>> &ensure_stc(hs_bts *B, int e)
     return T;
 }
 
+// C17 double-hoisted BSGS (C17; same words as the oracle's
+// apply_ltrans).  Every intermediate lives in the extended basis Q_l u P
+// (ntg limbs per component, a value v standing for P v):
+//   R_0 = P x;  R_b = (P sigma_b(c0) + <sigma_b(ModUp c1), evk_b>_0, <.>_1)
+//   (one ModUp, one inner-product launch for all babies, NO ModDown);
+//   inner_g = sum_b pt_{g,b} (.) R_b (one fused kernel, PQ plaintexts);
+//   giants g != 0 (one batch): b' = ModDown(inner_g,1), Rot = (sigma_g(inner_g,0)
+//   + <ModUp(sigma_g b'), evk_g>_0, <.>_1) (no ModDown);
+//   out = ModDown + rescale by P q_l (C8) of inner_0 + sum Rot_g.
 static CtP apply(const hs_keys *K, const hs_ct *in, const LinTrans &T, cudaStream_t st)
 {
     hs_ctx *c = K->ctx;
-    const size_t N = c->P->n;
-    const int n0 = (int)N / 2, l = T.level, nl = l + 1;
+    const hs_params *P = c->P;
+    const size_t N = P->n;
+    const int n0 = (int)N / 2, l = T.level, nl = l + 1, np = P->n_p, ntg = nl + np;
+    const size_t W = (size_t)2 * ntg * N;  // one extended-basis ciphertext
     CtP lowered;
     const hs_ct *x = in;
     if (in->level != l) {
         lowered = ev_level_down(in, l, st);
         x = lowered.get();
     }
-    // baby rotations, hoisted (C16): one ModUp of x's c1 serves every b != 0
+    PrimeMap pq;  // Q_l u P
+    pq.n = ntg;
+    for (int i = 0; i < ntg; i++) pq.p[i] = (unsigned char)(i < nl ? i : P->n_q + (i - nl));
+    // ---- babies
     std::vector<int> bs, rots;
-    for (int b = 1; b < 64; b++)
+    for (int b = 1; b < T.b1; b++)
         if (std::find(T.b.begin(), T.b.end(), b) != T.b.end()) {
             bs.push_back(b);
             rots.push_back(b * T.unit);
         }
-    CtP hb;
-    if (!rots.empty()) hb = ev_rotate_hoisted(K, x, rots.data(), (int)rots.size(), st);
     std::vector<const u64 *> R(T.b1, nullptr);
-    if (std::find(T.b.begin(), T.b.end(), 0) != T.b.end()) R[0] = x->d;
-    for (size_t i = 0; i < bs.size(); i++) R[bs[i]] = hb->d + i * hb->ct_words();
-    // the giants in use, increasing (sparse: negative diagonals wrap mod N0/u)
+    DBuf r0, hb;
+    if (std::find(T.b.begin(), T.b.end(), 0) != T.b.end()) {  // R_0 = P x
+        r0.alloc(W, st);
+        u64 pmq[HS_MAXP];
+        for (int i = 0; i < nl; i++) pmq[i] = P->p_mod_q[i];
+        const PrimeMap pql = pmap_range(0, nl);
+        for (int comp = 0; comp < 2; comp++) {
+            k_mul_scalar_pm(c, x->limb(comp, 0), r0.p + (size_t)comp * ntg * N, pmq, nl, pql, st);
+            HS_CUDA(cudaMemsetAsync(r0.p + ((size_t)comp * ntg + nl) * N, 0, (size_t)np * N * 8, st));
+        }
+        R[0] = r0.p;
+    }
+    if (!bs.empty()) {
+        const int nb = (int)bs.size();
+        std::vector<const u64 *> keys(nb);
+        std::vector<const unsigned *> perms(nb);
+        for (int i = 0; i < nb; i++) {
+            const int k = hs_galois_elt(P, rots[i]);
+            const SwKey *key = K->find(k);
+            if (!key) throw HsError(HS_EKEY, "switching key for rotation " + std::to_string(rots[i]) + " missing");
+            keys[i] = key->k;
+            perms[i] = galois_table(c, k);
+        }
+        ModUpBuf m;
+        ks_modup(c, l, 1, x->limb(1, 0), nl * N, m, st);
+        hb.alloc((size_t)nb * W, st);
+        k_ks_inner_h(c, x->limb(1, 0), m.ext.p, m.off, m.nd, keys.data(), perms.data(), nb, hb.p, l, m.beta, st,
+                     x->limb(0, 0));
+        for (int i = 0; i < nb; i++) R[bs[i]] = hb.p + (size_t)i * W;
+        c->ledger[HS_LG_KS] += nb;
+        c->ledger[HS_LG_ROT] += nb;
+    }
+    // ---- inner sums of every giant (increasing g; negative diagonals wrap)
     std::vector<int> gs(T.g.begin(), T.g.end());
     std::sort(gs.begin(), gs.end());
     gs.erase(std::unique(gs.begin(), gs.end()), gs.end());
@@ -310,26 +357,60 @@ static CtP apply(const hs_keys *K, const hs_ct *in, const LinTrans &T, cudaStrea
         const int gi = (int)(std::lower_bound(gs.begin(), gs.end(), T.g[k]) - gs.begin());
         tk[(size_t)gi * T.b1 + T.b[k]] = (int)k;
     }
-    // every inner sum of pt (.) Rot(x, b u) in one pass over the babies
-    CtP inners = ct_new(c, l, 2, st, G);
-    k_bsgs_inner(c, R.data(), T.b1, T.pts, tk.data(), G, nl, inners->d, st);
+    DBuf inners((size_t)G * W, st);
+    k_bsgs_inner(c, R.data(), T.b1, T.pts, tk.data(), G, ntg, inners.p, st, nl);
     c->ledger[HS_LG_PMULT] += (int64_t)T.g.size();
-    // the giants g != 0 rotate as ONE batched key switch (a key per member)
-    const int g0 = gs[0] == 0 ? 1 : 0;
-    CtP rot;
-    if (G > g0) {
-        CtP sub = ct_view(inners.get(), g0);
-        sub->batch = G - g0;
-        std::vector<int> rots;
-        for (int gi = g0; gi < G; gi++) rots.push_back((gs[gi] * T.b1 * T.unit) % n0);
-        rot = ev_rotate_multi(K, sub.get(), rots.data(), st);
+    // ---- giants g != 0 as one batch
+    const int g0 = gs[0] == 0 ? 1 : 0, ng = G - g0;
+    DBuf acc(W, st);
+    if (g0) HS_CUDA(cudaMemcpyAsync(acc.p, inners.p, W * 8, cudaMemcpyDeviceToDevice, st));
+    if (ng > 0) {
+        const u64 *gin = inners.p + (size_t)g0 * W;
+        // b'_g = ModDown(inner_g component 1): rows with stride W, out [ng][nl][N]
+        DBuf bq((size_t)ng * nl * N, st);
+        {
+            DBuf z((size_t)ng * np * N, st);
+            HS_CUDA(cudaMemcpy2DAsync(z.p, np * N * 8, gin + ((size_t)ntg + nl) * N, W * 8, np * N * 8, ng,
+                                      cudaMemcpyDeviceToDevice, st));
+            k_ntt(c, z.p, ng * np, pmap_range(P->n_q, np), true, st);
+            const BconvTab &md = bconv_moddown(c, l);
+            DBuf conv((size_t)ng * nl * N, st);
+            k_bconv(c, md, z.p, N, conv.p, N, ng, (size_t)np * N, (size_t)nl * N, st);
+            const u64 *a1 = gin + (size_t)ntg * N;
+            if (!k_ntt_moddown(c, conv.p, a1, W, bq.p, 2 * (size_t)nl * N, nullptr, 0, 0, nl, nullptr, ng, st)) {
+                k_ntt(c, conv.p, ng * nl, pmap_range(0, nl), false, st);
+                k_moddown_final_b(c, a1, W, conv.p, nl, bq.p, 2 * (size_t)nl * N, nullptr, 0, 0, nullptr, ng, st);
+            }
+        }
+        // sigma_g on b'_g (Q) and on inner_g component 0 (Q u P)
+        std::vector<const u64 *> keys(ng);
+        DBuf sb((size_t)ng * nl * N, st), sa((size_t)ng * ntg * N, st);
+        for (int i = 0; i < ng; i++) {
+            const int k = hs_galois_elt(P, (gs[g0 + i] * T.b1 * T.unit) % n0);
+            const SwKey *key = K->find(k);
+            if (!key) throw HsError(HS_EKEY, "switching key for a giant rotation missing");
+            keys[i] = key->k;
+            const unsigned *perm = galois_table(c, k);
+            k_permute(c, bq.p + (size_t)i * nl * N, sb.p + (size_t)i * nl * N, perm, nl, st);
+            k_permute(c, gin + (size_t)i * W, sa.p + (size_t)i * ntg * N, perm, ntg, st);
+        }
+        ModUpBuf m;
+        ks_modup(c, l, ng, sb.p, (size_t)nl * N, m, st);
+        DBuf rot((size_t)ng * W, st);
+        k_ks_inner_m(c, sb.p, (size_t)nl * N, m.ext.p, m.off, m.nd, keys.data(), ng, rot.p, l, m.beta, st);
+        for (int i = 0; i < ng; i++) {
+            u64 *ri = rot.p + (size_t)i * W;
+            k_add_pm(c, ri, sa.p + (size_t)i * ntg * N, ri, ntg, pq, st);  // + sigma_g(inner_g,0)
+            if (i == 0 && !g0) HS_CUDA(cudaMemcpyAsync(acc.p, ri, W * 8, cudaMemcpyDeviceToDevice, st));
+            else k_add_pm(c, acc.p, ri, acc.p, 2 * ntg, pq, st);
+        }
+        c->ledger[HS_LG_KS] += ng;
+        c->ledger[HS_LG_ROT] += ng;
     }
-    CtP acc = g0 ? ct_slice(inners.get(), 0, st) : ct_slice(rot.get(), 0, st);
-    for (int gi = 1; gi < G; gi++) {
-        const u64 *src = rot->d + (size_t)(gi - g0) * rot->ct_words();
-        k_add(c, acc->d, src, acc->d, (int)acc->limbs(), nl, false, st);
-    }
-    return ev_rescale(acc.get(), st);
+    CtP out = ct_new(c, l - 1, 2, st);
+    ks_moddown_rescale(c, l, 1, acc.p, out->d, out->ct_words(), st);
+    c->ledger[HS_LG_RESCALE]++;
+    return out;
 }
 
 CtP ev_bootstrap(const hs_keys *K, hs_bts *B, const hs_ct *in, double bound, cudaStream_t st)

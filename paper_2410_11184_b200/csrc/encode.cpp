@@ -68,7 +68,7 @@ void dft(std::vector<Cq> &a, int log_n2, int sign)
 
 }  // namespace
 
-static void encode_from(const hs_params *P, std::vector<Cq> &a, double scale, int level, u64 *out);
+static void encode_from(const hs_params *P, std::vector<Cq> &a, double scale, int level, u64 *out, bool with_p = false);
 
 void hs_encode_impl(const hs_params *P, const double *re, const double *im, double scale, int level, u64 *out)
 {
@@ -84,7 +84,7 @@ void hs_encode_impl(const hs_params *P, const double *re, const double *im, doub
 
 // quad-precision slot values (bootstrapping diagonals, G11)
 void hs_encode_impl_q(const hs_params *P, const __float128 *re, const __float128 *im, double scale, int level,
-                      u64 *out)
+                      u64 *out, bool with_p)
 {
     const int N = P->n, n0 = N / 2, n2 = 2 * N;
     std::vector<Cq> a(n2, Cq{0, 0});
@@ -93,10 +93,12 @@ void hs_encode_impl_q(const hs_params *P, const __float128 *re, const __float128
         a[g] = Cq{re[j], im[j]};
         g = g * 5 % (u64)n2;
     }
-    encode_from(P, a, scale, level, out);
+    encode_from(P, a, scale, level, out, with_p);
 }
 
-static void encode_from(const hs_params *P, std::vector<Cq> &a, double scale, int level, u64 *out)
+// with_p: also the residues mod p_0..p_{np-1} after the level+1 Q limbs (the
+// extended basis of the double-hoisted BSGS plaintexts, C17)
+static void encode_from(const hs_params *P, std::vector<Cq> &a, double scale, int level, u64 *out, bool with_p)
 {
     const int N = P->n, lg = P->log_n + 1;
     dft(a, lg, -1);
@@ -107,6 +109,10 @@ static void encode_from(const hs_params *P, std::vector<Cq> &a, double scale, in
         for (int i = 0; i <= level; i++) {
             __int128 q = (__int128)P->prime[i], r = m % q;
             out[(size_t)i * N + t] = (u64)(r < 0 ? r + q : r);
+        }
+        for (int k = 0; with_p && k < P->n_p; k++) {
+            __int128 q = (__int128)P->prime[P->n_q + k], r = m % q;
+            out[(size_t)(level + 1 + k) * N + t] = (u64)(r < 0 ? r + q : r);
         }
     }
 }

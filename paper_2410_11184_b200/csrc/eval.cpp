@@ -332,9 +332,10 @@ void ks_moddown(hs_ctx *c, int level, int B, const u64 *acc, u64 *out, size_t ou
     const BconvTab &md = bconv_moddown(c, level);
     DBuf conv((size_t)B * 2 * nl * N, st);
     k_bconv(c, md, z.p, N, conv.p, N, 2 * B, (size_t)np * N, (size_t)nl * N, st);
-    if (k_ntt_moddown(c, conv.p, acc, ntg, out, out_stride, add, add_stride, add_comps, nl, nullptr, B, st)) return;
+    const size_t ar = (size_t)ntg * N;
+    if (k_ntt_moddown(c, conv.p, acc, ar, out, out_stride, add, add_stride, add_comps, nl, nullptr, 2 * B, st)) return;
     k_ntt(c, conv.p, 2 * B * nl, pmap_range(0, nl), false, st);
-    k_moddown_final_b(c, acc, ntg, conv.p, nl, out, out_stride, add, add_stride, add_comps, nullptr, B, st);
+    k_moddown_final_b(c, acc, ar, conv.p, nl, out, out_stride, add, add_stride, add_comps, nullptr, 2 * B, st);
 }
 
 // C8 fused ModDown + rescale of B accumulators acc [B][2][ntg][N] (basis
@@ -362,9 +363,10 @@ void ks_moddown_rescale(hs_ctx *c, int level, int B, const u64 *acc, u64 *out, s
         const u64 q = P->prime[i];
         inv[i] = hs_invmod(hs_mulmod(P->p_mod_q[i], P->prime[level] % q, q), q);
     }
-    if (k_ntt_moddown(c, conv.p, acc, ntg, out, out_stride, nullptr, 0, 0, level, inv.data(), B, st)) return;
+    const size_t ar = (size_t)ntg * N;
+    if (k_ntt_moddown(c, conv.p, acc, ar, out, out_stride, nullptr, 0, 0, level, inv.data(), 2 * B, st)) return;
     k_ntt(c, conv.p, 2 * B * level, pmap_range(0, level), false, st);
-    k_moddown_final_b(c, acc, ntg, conv.p, level, out, out_stride, nullptr, 0, 0, inv.data(), B, st);
+    k_moddown_final_b(c, acc, ar, conv.p, level, out, out_stride, nullptr, 0, 0, inv.data(), 2 * B, st);
 }
 
 // B polynomials d_b = d + b*d_stride (level+1 limbs each, NTT domain);

@@ -212,10 +212,13 @@ void k_moddown_final(hs_ctx *c, const u64 *acc, const u64 *conv, u64 *o0, u64 *o
                      const u64 *add1, int level, cudaStream_t st);
 void upload_prime_constants(const hs_params *P);
 bool k_ntt_rescale(hs_ctx *c, const u64 *last, u64 *w, const u64 *a, u64 *o, int rows, int l, cudaStream_t st);
-bool k_ntt_moddown(hs_ctx *c, u64 *conv, const u64 *acc, int ntg, u64 *o, size_t o_stride, const u64 *add,
-                   size_t add_stride, int add_comps, int nt, const u64 *inv, int B, cudaStream_t st);
+bool k_ntt_moddown(hs_ctx *c, u64 *conv, const u64 *acc, size_t acc_row, u64 *o, size_t o_stride, const u64 *add,
+                   size_t add_stride, int add_comps, int nt, const u64 *inv, int rows, cudaStream_t st);
+void k_mul_scalar_pm(hs_ctx *c, const u64 *a, u64 *o, const u64 *host_scal, int n_limbs, const PrimeMap &pm,
+                     cudaStream_t st);
+void k_add_pm(hs_ctx *c, const u64 *a, const u64 *b, u64 *o, int n_limbs, const PrimeMap &pm, cudaStream_t st);
 void k_bsgs_inner(hs_ctx *c, const u64 *const *R, int b1, const u64 *pts, const int *tk, int G, int nl, u64 *out,
-                  cudaStream_t st);
+                  cudaStream_t st, int nlq = -1);
 void k_mac_pt(hs_ctx *c, u64 *acc, const u64 *a, const u64 *pt, int nl, int la, cudaStream_t st);
 // batched ciphertext kernels ([B][ncomp][nl][N]; "rows" = B * ncomp)
 void k_add_b(hs_ctx *c, const u64 *a, int a_rows, const u64 *b, int b_rows, u64 *o, int rows, int nl, bool sub,
@@ -231,9 +234,10 @@ void k_ks_inner_b(hs_ctx *c, const u64 *d, size_t d_stride, const u64 *ext, cons
 void k_ks_inner_m(hs_ctx *c, const u64 *d, size_t d_stride, const u64 *ext, const size_t *off, const int *nd,
                   const u64 *const *keys, int B, u64 *acc, int level, int beta, cudaStream_t st);
 void k_ks_inner_h(hs_ctx *c, const u64 *d, const u64 *ext, const size_t *off, const int *nd, const u64 *const *keys,
-                  const unsigned *const *perms, int R, u64 *acc, int level, int beta, cudaStream_t st);
-void k_moddown_final_b(hs_ctx *c, const u64 *acc, int ntg, const u64 *conv, int nt, u64 *o, size_t o_stride,
-                       const u64 *add, size_t add_stride, int add_comps, const u64 *inv, int B, cudaStream_t st);
+                  const unsigned *const *perms, int R, u64 *acc, int level, int beta, cudaStream_t st,
+                  const u64 *c0add = nullptr);
+void k_moddown_final_b(hs_ctx *c, const u64 *acc, size_t acc_row, const u64 *conv, int nt, u64 *o, size_t o_stride,
+                       const u64 *add, size_t add_stride, int add_comps, const u64 *inv, int rows, cudaStream_t st);
 void k_modraise(hs_ctx *c, const u64 *x, u64 *o, int nl, cudaStream_t st);
 void k_signed_to_rns(hs_ctx *c, const int64_t *v, u64 *o, int n_limbs, const PrimeMap &pm, cudaStream_t st);
 void k_uniform(hs_ctx *c, u64 *o, int n_limbs, const PrimeMap &pm, u64 seed, uint32_t tag, u64 sub,
@@ -294,7 +298,7 @@ void ev_decrypt(const hs_keys *K, const hs_ct *ct, u64 *host_out, cudaStream_t s
 // encode.cpp
 void hs_encode_impl(const hs_params *P, const double *re, const double *im, double scale, int level, u64 *out);
 void hs_encode_impl_q(const hs_params *P, const __float128 *re, const __float128 *im, double scale, int level,
-                      u64 *out);
+                      u64 *out, bool with_p = false);
 void hs_decode_impl(const hs_params *P, const u64 *q0_coeffs, double scale, double *re, double *im);
 
 // poly.cpp

@@ -558,22 +558,24 @@ bool k_ntt_rescale(hs_ctx *c, const u64 *last, u64 *w, const u64 *a, u64 *o, int
     return true;
 }
 
-// ModDown tail (C7): the forward transform of conv [B][2][nt][N] (BConv of
-// the special limbs) with o_b = add_b + (acc_b - NTT(conv_b)) inv fused into its
-// second pass; acc [B][2][ntg][N]; inv NULL = P^-1 mod q_i (plain ModDown),
-// else e.g. (P q_l)^-1 for the fused relin + rescale (C8).  N = 2^16 only.
-bool k_ntt_moddown(hs_ctx *c, u64 *conv, const u64 *acc, int ntg, u64 *o, size_t o_stride, const u64 *add,
-                   size_t add_stride, int add_comps, int nt, const u64 *inv, int B, cudaStream_t st)
+// ModDown tail (C7): the forward transform of conv [rows][nt][N] (BConv of
+// the special limbs) with out = add + (acc - NTT(conv)) inv fused into its
+// second pass.  Row r = 2 b + comp reads acc + r acc_row and writes
+// o + b o_stride + (comp nt + i) N (so o_stride = 2 nt N lays rows out
+// contiguously); inv NULL = P^-1 mod q_i (plain ModDown), else e.g.
+// (P q_l)^-1 for the fused relin + rescale (C8).  N = 2^16 only.
+bool k_ntt_moddown(hs_ctx *c, u64 *conv, const u64 *acc, size_t acc_row, u64 *o, size_t o_stride, const u64 *add,
+                   size_t add_stride, int add_comps, int nt, const u64 *inv, int rows, cudaStream_t st)
 {
     const hs_params *P = c->P;
     if (P->log_n != 16) return false;
-    const int N = P->n, n_limbs = 2 * B * nt;
+    const int N = P->n, n_limbs = rows * nt;
     KTimer _kt(c, KID_NTT, (double)n_limbs * N * 16, st);
     ntt16::NttEpi E{};
     E.ain = acc;
     E.add = add;
     E.o = o;
-    E.astr = (size_t)ntg * N;
+    E.astr = acc_row;
     E.ostr = o_stride;
     E.addstr = add_stride;
     E.add_comps = add ? add_comps : 0;
@@ -700,6 +702,50 @@ void k_mul_scalar(hs_ctx *c, const u64 *a, u64 *o, const u64 *host_scal, int n_l
     KTimer _kt(c, KID_SCALAR, (double)n_limbs * c->P->n * 16, st);
     int N = c->P->n;
     mul_scalar_kernel<<<GRID_LIMBS(n_limbs, N), 256, 0, st>>>(a, o, make_scalars(c->P, host_scal, period), N, period);
+    HS_CHECK_LAUNCH();
+    count_kernel(c);
+}
+
+// Elementwise ops on limbs of any basis: limb l is reduced mod the prime
+// pm.p[l % pm.n] (the extended basis Q_l u P of the double-hoisted BSGS, C17).
+__global__ void mul_scalar_pm_kernel(const u64 *a, u64 *o, ScalarArg s, PrimeMap pm, int N)
+{
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= N) return;
+    const int l = blockIdx.y, i = l % pm.n;
+    const size_t x = (size_t)l * N + t;
+    o[x] = d_shoup(a[x], s.v[i], s.vs[i], c_pk[pm.p[i]].q);
+}
+
+void k_mul_scalar_pm(hs_ctx *c, const u64 *a, u64 *o, const u64 *host_scal, int n_limbs, const PrimeMap &pm,
+                     cudaStream_t st)
+{
+    KTimer _kt(c, KID_SCALAR, (double)n_limbs * c->P->n * 16, st);
+    ScalarArg s;
+    for (int i = 0; i < pm.n; i++) {
+        s.v[i] = host_scal[i];
+        s.vs[i] = hs_shoup_const(host_scal[i], c->P->prime[pm.p[i]]);
+    }
+    int N = c->P->n;
+    mul_scalar_pm_kernel<<<GRID_LIMBS(n_limbs, N), 256, 0, st>>>(a, o, s, pm, N);
+    HS_CHECK_LAUNCH();
+    count_kernel(c);
+}
+
+__global__ void add_pm_kernel(const u64 *a, const u64 *b, u64 *o, PrimeMap pm, int N)
+{
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= N) return;
+    const int l = blockIdx.y;
+    const size_t x = (size_t)l * N + t;
+    o[x] = d_add(a[x], b[x], c_pk[pm.p[l % pm.n]].q);
+}
+
+void k_add_pm(hs_ctx *c, const u64 *a, const u64 *b, u64 *o, int n_limbs, const PrimeMap &pm, cudaStream_t st)
+{
+    KTimer _kt(c, KID_ADD, (double)n_limbs * c->P->n * 24, st);
+    int N = c->P->n;
+    add_pm_kernel<<<GRID_LIMBS(n_limbs, N), 256, 0, st>>>(a, b, o, pm, N);
     HS_CHECK_LAUNCH();
     count_kernel(c);
 }
@@ -1463,10 +1509,15 @@ struct KsArgH {
     int level, beta, alpha, n_q, n_t;
     size_t off[16];
     int nd[16];
+    // C17: component 0 also gets sigma_r(c0) (P mod q_g) on the Q limbs (the
+    // rotation kept in the extended basis, no ModDown); NULL = none
+    const u64 *c0add;
+    u64 pmq[HS_MAXP];
 };
 
 __global__ void __launch_bounds__(256) ks_inner_h_kernel(const u64 *__restrict__ d, const u64 *__restrict__ ext,
-                                                         u64 *__restrict__ acc, KsArgH A, int N)
+                                                         u64 *__restrict__ acc, const __grid_constant__ KsArgH A,
+                                                         int N)
 {
     // grid (R, N / 256, ntg): the R rotations of one coefficient block run back
     // to back, so their gathers of the shared extended digits hit L2
@@ -1490,12 +1541,14 @@ __global__ void __launch_bounds__(256) ks_inner_h_kernel(const u64 *__restrict__
         mac128(h0, l0, v, k0);
         mac128(h1, l1, v, k1);
     }
+    if (A.c0add && g < nl) mac128(h0, l0, A.c0add[(size_t)g * N + src], A.pmq[g]);
     acc[((size_t)r * 2 * ntg + g) * N + t] = d_reduce128(h0, l0, k);
     acc[((size_t)(r * 2 + 1) * ntg + g) * N + t] = d_reduce128(h1, l1, k);
 }
 
 void k_ks_inner_h(hs_ctx *c, const u64 *d, const u64 *ext, const size_t *off, const int *nd, const u64 *const *keys,
-                  const unsigned *const *perms, int R, u64 *acc, int level, int beta, cudaStream_t st)
+                  const unsigned *const *perms, int R, u64 *acc, int level, int beta, cudaStream_t st,
+                  const u64 *c0add)
 {
     const hs_params *P = c->P;
     const int ntg = level + 1 + P->n_p;
@@ -1515,6 +1568,9 @@ void k_ks_inner_h(hs_ctx *c, const u64 *d, const u64 *ext, const size_t *off, co
         A.off[j] = off[j];
         A.nd[j] = nd[j];
     }
+    A.c0add = c0add;
+    if (c0add)
+        for (int i = 0; i <= level; i++) A.pmq[i] = P->p_mod_q[i];
     int N = P->n;
     ks_inner_h_kernel<<<dim3(R, (N + 255) / 256, ntg), 256, 0, st>>>(d, ext, acc, A, N);
     HS_CHECK_LAUNCH();
@@ -1588,19 +1644,19 @@ void k_ks_inner_m(hs_ctx *c, const u64 *d, size_t d_stride, const u64 *ext, cons
 
 struct MdArgB {
     u64 pinv[HS_MAXP], pinv_sh[HS_MAXP];
-    int nt, ntg, add_comps;
-    size_t o_stride, add_stride;
+    int nt, add_comps;
+    size_t acc_row, o_stride, add_stride;
 };
 
-// o_b[c][i] = add + (acc_b[c][i] - conv_b[c][i]) inv_i for i < nt;
-// acc [B][2][ntg][N], conv [B][2][nt][N]
+// row r = 2 b + comp: o_b[comp][i] = add + (acc_r[i] - conv_r[i]) inv_i for
+// i < nt; acc row r at acc + r acc_row, conv [rows][nt][N]
 __global__ void moddown_final_b_kernel(const u64 *acc, const u64 *conv, u64 *o, const u64 *add, MdArgB A, int N)
 {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= N) return;
     const int i = blockIdx.y, comp = blockIdx.z & 1, b = blockIdx.z >> 1;
     u64 q = c_pk[i].q;
-    u64 av = acc[(((size_t)b * 2 + comp) * A.ntg + i) * N + t];
+    u64 av = acc[(size_t)blockIdx.z * A.acc_row + (size_t)i * N + t];
     u64 cv = conv[(((size_t)b * 2 + comp) * A.nt + i) * N + t];
     u64 v = d_shoup(d_sub(av, cv, q), A.pinv[i], A.pinv_sh[i], q);
     size_t ci = ((size_t)comp * A.nt + i) * N + t;
@@ -1608,23 +1664,23 @@ __global__ void moddown_final_b_kernel(const u64 *acc, const u64 *conv, u64 *o, 
     o[(size_t)b * A.o_stride + ci] = v;
 }
 
-void k_moddown_final_b(hs_ctx *c, const u64 *acc, int ntg, const u64 *conv, int nt, u64 *o, size_t o_stride,
-                       const u64 *add, size_t add_stride, int add_comps, const u64 *inv, int B, cudaStream_t st)
+void k_moddown_final_b(hs_ctx *c, const u64 *acc, size_t acc_row, const u64 *conv, int nt, u64 *o, size_t o_stride,
+                       const u64 *add, size_t add_stride, int add_comps, const u64 *inv, int rows, cudaStream_t st)
 {
     const hs_params *P = c->P;
-    KTimer _kt(c, KID_MODDOWN, (double)B * nt * P->n * 8 * (6 + add_comps), st);
+    KTimer _kt(c, KID_MODDOWN, (double)rows * nt * P->n * 8 * (3 + add_comps), st);
     MdArgB A;
     for (int i = 0; i < nt; i++) {
         A.pinv[i] = inv ? inv[i] : P->p_inv_mod_q[i];
         A.pinv_sh[i] = hs_shoup_const(A.pinv[i], P->prime[i]);
     }
     A.nt = nt;
-    A.ntg = ntg;
+    A.acc_row = acc_row;
     A.add_comps = add ? add_comps : 0;
     A.o_stride = o_stride;
     A.add_stride = add_stride;
     int N = P->n;
-    moddown_final_b_kernel<<<dim3((N + 255) / 256, nt, 2 * B), 256, 0, st>>>(acc, conv, o, add, A, N);
+    moddown_final_b_kernel<<<dim3((N + 255) / 256, nt, rows), 256, 0, st>>>(acc, conv, o, add, A, N);
     HS_CHECK_LAUNCH();
     count_kernel(c);
 }
@@ -1650,7 +1706,8 @@ __global__ void mac_pt_kernel(u64 *acc, const u64 *a, const u64 *pt, int N, int 
 struct BsgsArg {
     const u64 *R[16];
     int tk[16 * 16];
-    int G, nl;
+    int G, nl;      // limbs per component (Q limbs, or Q u P limbs for C17)
+    int nlq, n_q;   // limb i >= nlq is the special prime n_q + (i - nlq)
 };
 
 template <int B1>
@@ -1660,7 +1717,7 @@ __global__ void __launch_bounds__(256) bsgs_inner_kernel(const u64 *__restrict__
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= N) return;
     const int i = blockIdx.y, nl = A.nl;
-    const PrimeK k = c_pk[i];
+    const PrimeK k = c_pk[i < A.nlq ? i : A.n_q + (i - A.nlq)];
     u64 r0[B1], r1[B1];
 #pragma unroll
     for (int b = 0; b < B1; b++)
@@ -1686,7 +1743,7 @@ __global__ void __launch_bounds__(256) bsgs_inner_kernel(const u64 *__restrict__
 }
 
 void k_bsgs_inner(hs_ctx *c, const u64 *const *R, int b1, const u64 *pts, const int *tk, int G, int nl, u64 *out,
-                  cudaStream_t st)
+                  cudaStream_t st, int nlq)
 {
     if (b1 < 1 || b1 > 8 || G < 1 || G > 16) throw HsError(HS_EINVAL, "bsgs_inner: baby / giant count out of range");
     BsgsArg A;
@@ -1701,6 +1758,8 @@ void k_bsgs_inner(hs_ctx *c, const u64 *const *R, int b1, const u64 *pts, const 
         }
     A.G = G;
     A.nl = nl;
+    A.nlq = nlq < 0 ? nl : nlq;
+    A.n_q = c->P->n_q;
     const int N = c->P->n;
     KTimer _kt(c, KID_PTMUL, (double)(2 * babies + terms + 2 * G) * nl * N * 8, st);
     const dim3 grid((N + 255) / 256, nl);

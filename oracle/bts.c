@@ -558,7 +558,28 @@ orc_ct *orc_bootstrap(const orc_params *P, const orc_keys *K, const orc_ct *in, 
     orc_ct *v2 = orc_op_add_const(P, v, -1.0 / (4.0 * (cf->K + 2)));
     orc_ct_release(v);
     STOP(10, v2);
-    orc_ct *s = orc_eval_cheb_unit(P, K, v2, B->cosp);
+    /* C18 EvalMod: the cosine series is even (Jacobi-Anger: odd coefficients
+     * are 0), p(v) = sum_k c_2k T_2k(v) = sum_k c_2k T_k(w), w = T_2(v) = 2 v^2 - 1:
+     * one HMult and a series of half the degree on w (same depth, C13) */
+    orc_ct *s;
+    int even = B->cosp->deg >= 2;
+    for (int i = 1; i <= B->cosp->deg; i += 2) even &= B->cosp->c[i] == 0.0;
+    if (even) {
+        orc_ct *vv = orc_op_mult(P, K, v2, v2);
+        orc_ct *vv2 = orc_op_mult_int(P, vv, 2);
+        orc_ct *w = orc_op_add_const(P, vv2, -1.0);
+        orc_ct_release(vv);
+        orc_ct_release(vv2);
+        int hd = B->cosp->deg / 2;
+        double *hc = malloc(sizeof(double) * (hd + 1));
+        for (int k = 0; k <= hd; k++) hc[k] = B->cosp->c[2 * k];
+        orc_cheb hp = {hd, -1.0, 1.0, hc};
+        s = orc_eval_cheb_unit(P, K, w, &hp);
+        orc_ct_release(w);
+        free(hc);
+    } else {
+        s = orc_eval_cheb_unit(P, K, v2, B->cosp);
+    }
     orc_ct_release(v2);
     STOP(11, s);
     for (int i = 0; i < cf->r; i++) {

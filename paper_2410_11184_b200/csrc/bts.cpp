@@ -212,8 +212,9 @@ void add_group_rotations(int n0, int ngroups, std::vector<int> &rots)
 struct hs_bts {
     hs_ctx *ctx = nullptr;
     int K = 0, r = 0, out_level = 0, n_cts = 0, n_stc = 0, arcsine = 0;
-    std::vector<double> cos_coeffs;
-    hs_poly cos_poly{};
+    std::vector<double> cos_coeffs, half_coeffs;
+    hs_poly cos_poly{}, half_poly{};
+    bool even = false;  // C18: odd coefficients all 0 -> evaluate on T_2(x)
     std::vector<std::unique_ptr<LinTrans>> cts;                   // shared by every e
     std::map<int, std::vector<std::unique_ptr<LinTrans>>> stc;    // per pre-scaling exponent e
     std::mutex mu;
@@ -481,7 +482,14 @@ CtP ev_bootstrap(const hs_keys *K, hs_bts *B, const hs_ct *in, double bound, cud
     x = ev_add(x.get(), cj.get(), false, st);
     x = ev_add_const(x.get(), -1.0 / (4.0 * (B->K + 2)), st);
     ph.mark("conj");
-    x = ev_cheb(K, x.get(), &B->cos_poly, st);
+    if (B->even) {  // C18: even series, w = T_2(x), half the degree on w
+        CtP m = ev_mult(K, x.get(), x.get(), st);
+        CtP m2 = ev_mult_int(m.get(), 2, st);
+        CtP w = ev_add_const(m2.get(), -1.0, st);
+        x = ev_cheb(K, w.get(), &B->half_poly, st);
+    } else {
+        x = ev_cheb(K, x.get(), &B->cos_poly, st);
+    }
     ph.mark("cos-cheb");
     for (int i = 0; i < B->r; i++) {
         CtP m = ev_mult(K, x.get(), x.get(), st);
@@ -535,6 +543,10 @@ hs_status hs_bts_create(hs_ctx *c, const hs_bts_desc *d, hs_bts **out)
         B->arcsine = d->arcsine != 0;
         B->cos_coeffs.assign(d->cos_poly->coeffs, d->cos_poly->coeffs + d->cos_poly->deg + 1);
         B->cos_poly = hs_poly{d->cos_poly->deg, -1.0, 1.0, B->cos_coeffs.data()};
+        B->even = d->cos_poly->deg >= 2;
+        for (int i = 1; i <= d->cos_poly->deg; i += 2) B->even = B->even && d->cos_poly->coeffs[i] == 0.0;
+        for (int k = 0; k <= d->cos_poly->deg / 2; k++) B->half_coeffs.push_back(d->cos_poly->coeffs[2 * k]);
+        B->half_poly = hs_poly{d->cos_poly->deg / 2, -1.0, 1.0, B->half_coeffs.data()};
         *out = B.release();
         return HS_OK;
     } catch (const HsError &e) {

@@ -317,6 +317,7 @@ struct NttEpi {
     size_t astr, ostr, addstr;
     int l, lq, add_comps;
     u64 inv[HS_MAXP], inv_sh[HS_MAXP];
+    u64 rsh[HS_MAXP];  // MODE 1: floor(2^64 / q_i) (Shoup reduction of x < 2^64 by q_i)
 };
 
 // Phase over the high 8 index bits (half-spans 2^15..2^8): C columns x 256 rows
@@ -336,17 +337,18 @@ __global__ void __launch_bounds__(32 * C) cols(u64 *data, PrimeMap pm, const u64
         const int r0 = rid;
         if (MODE == 1) {
             // x = centred(last) mod q_i, last = the row's dropped limb mod q_l
-            const u64 *src = E.last + (size_t)(limb / E.l) * N;
-            const u64 ql = c_pk[E.lq].q;
-            const PrimeK kq = c_pk[pi];
+            const int row = limb / E.l;
+            const u64 *src = E.last + (size_t)row * N;
+            const u64 ql = c_pk[E.lq].q, half = (ql - 1) / 2, q = T.q, rsh = E.rsh[limb - row * E.l];
 #pragma unroll
             for (int k = 0; k < 8; k++) {
+                // |centred v| mod q by a Shoup step with w = 1, sign restored
                 const u64 v = src[(r0 + 32 * k) * 256 + c];
-                if (v <= (ql - 1) / 2) x[k] = d_reduce128(0, v, kq);
-                else {
-                    const u64 r = d_reduce128(0, ql - v, kq);
-                    x[k] = r ? kq.q - r : 0;
-                }
+                const bool neg = v > half;
+                const u64 sv = neg ? ql - v : v;
+                u64 r = sv - __umul64hi(sv, rsh) * q;
+                r = r >= q ? r - q : r;
+                x[k] = (neg && r) ? q - r : r;
             }
         } else {
 #pragma unroll
@@ -547,6 +549,7 @@ bool k_ntt_rescale(hs_ctx *c, const u64 *last, u64 *w, const u64 *a, u64 *o, int
     for (int i = 0; i < l; i++) {
         E.inv[i] = hs_invmod(ql % P->prime[i], P->prime[i]);
         E.inv_sh[i] = hs_shoup_const(E.inv[i], P->prime[i]);
+        E.rsh[i] = (u64)((((u128)1) << 64) / P->prime[i]);
     }
     const PrimeMap pm = pmap_range(0, l);
     const u64 *ninv = c->T.tw + (size_t)(P->n_q + P->n_p) * 4 * N;
@@ -1492,8 +1495,17 @@ void k_ks_inner_b(hs_ctx *c, const u64 *d, size_t d_stride, const u64 *ext, cons
     if (dadd)
         for (int i = 0; i <= level; i++) A.pmq[i] = P->p_mod_q[i];
     int N = P->n;
-    const int tiles = (B + 3) / 4;
-    ks_inner_b_kernel<4><<<dim3(tiles, (N + 255) / 256, ntg), 256, 0, st>>>(d, ext, key, acc, A, N);
+    // batch tile per thread: HS_KS_BT=8 for experiments (default 4)
+    static const int bt = [] {
+        const char *e = getenv("HS_KS_BT");
+        return e && atoi(e) == 8 ? 8 : 4;
+    }();
+    if (bt == 8 && B >= 8) {
+        ks_inner_b_kernel<8><<<dim3((B + 7) / 8, (N + 255) / 256, ntg), 256, 0, st>>>(d, ext, key, acc, A, N);
+    } else {
+        const int tiles = (B + 3) / 4;
+        ks_inner_b_kernel<4><<<dim3(tiles, (N + 255) / 256, ntg), 256, 0, st>>>(d, ext, key, acc, A, N);
+    }
     HS_CHECK_LAUNCH();
     count_kernel(c);
 }

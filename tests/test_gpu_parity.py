@@ -227,6 +227,52 @@ def test_softmax_many_parity(tables, table):
     _softmax_case(tables, "TOY12D", table, 2, 256, "many-" + table)
 
 
+def test_sharded_path_single_process(tables):
+    """The world > 1 path of hs_softmax_many_ctxt on one
+    GPU without ranks waiting on each other: m = 2 identical ciphertexts, so
+    rank 1's partial aux sum equals rank 0's and an exchange callback that
+    writes rank 0's partial into both gather slots IS the all-gather.  Rank 0's
+    sharded output must equal the unsharded m = 2 run word for word."""
+    hs = _hs()
+    from paper_2410_11184_b200 import _lib
+    tab = tables["toy_n16_M4_k2_B"]
+    cfg = tab["config"]
+    n, k, M = cfg["n"], cfg["k"], cfg["M"]
+    pre = W.preset("TOY12D")
+    P = hs.Params.from_preset(pre)
+    PO = O.Params.from_preset(pre)
+    gal = O.softmax_rotation_galois(PO, n, 2)
+    ctx = hs.Context(P, 0)
+    K = hs.Keys(ctx, 99, pre["h"], galois=gal)
+    x = W.softmax_inputs((P.n // 2) * 2 // n, n, M, seed=5)
+    slots = P.pack(x, 2)
+    top = len(pre["q_bits"]) - 1
+    pt = P.encode(slots[0], scale=P.scale(top), level=top)
+    c0 = hs.encrypt(K, pt, top, 7, 0)
+    c1 = hs.encrypt(K, pt, top, 7, 0)
+    full = hs.softmax_many_ctxt(K, [c0, c1], n, 2, k, 1, tab["exp"], tab["inv"])
+    calls = []
+
+    def dup(user, partial, gathered, words, stream):
+        calls.append(words)
+        src = torch.as_tensor(_CudaBuf(partial, words), device="cuda")
+        dst = torch.as_tensor(_CudaBuf(gathered, 2 * words), device="cuda")
+        dst[:words].copy_(src)
+        dst[words:].copy_(src)
+        return 0
+
+    fn = _lib.EXCHANGE_FN(dup)
+    shard = hs.softmax_many_ctxt(K, [c0], n, 2, k, 1, tab["exp"], tab["inv"], world=2, rank=0, exchange=fn)
+    assert len(calls) == k
+    same(shard[0], full[0])
+
+
+class _CudaBuf:
+    def __init__(self, ptr, n):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i8", "data": (int(ptr), False),
+                                         "version": 2, "strides": None}
+
+
 # ---------------------------------------------------------------- full size (N = 2^16)
 @pytest.fixture(scope="module")
 def p16():

@@ -1278,14 +1278,20 @@ void k_signed_to_rns(hs_ctx *c, const int64_t *v, u64 *o, int n_limbs, const Pri
 // (ciphertext, component) pair of nl limbs.  Second operands may be broadcast
 // (b_rows < rows: row r uses b row r % b_rows).
 
+// two adjacent words per thread (16-byte loads / stores)
 __global__ void add_b_kernel(const u64 *a, const u64 *b, u64 *o, int N, int nl, int a_rows, int b_rows, int sub)
 {
-    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    int t = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
     if (t >= N) return;
     int i = blockIdx.y, r = blockIdx.z;
     u64 q = c_pk[i].q;
     size_t x = ((size_t)(r % a_rows) * nl + i) * N + t, y = ((size_t)(r % b_rows) * nl + i) * N + t;
-    o[((size_t)r * nl + i) * N + t] = sub ? d_sub(a[x], b[y], q) : d_add(a[x], b[y], q);
+    const ulonglong2 va = *reinterpret_cast<const ulonglong2 *>(a + x);
+    const ulonglong2 vb = *reinterpret_cast<const ulonglong2 *>(b + y);
+    ulonglong2 vo;
+    vo.x = sub ? d_sub(va.x, vb.x, q) : d_add(va.x, vb.x, q);
+    vo.y = sub ? d_sub(va.y, vb.y, q) : d_add(va.y, vb.y, q);
+    *reinterpret_cast<ulonglong2 *>(o + ((size_t)r * nl + i) * N + t) = vo;
 }
 
 void k_add_b(hs_ctx *c, const u64 *a, int a_rows, const u64 *b, int b_rows, u64 *o, int rows, int nl, bool sub,
@@ -1293,7 +1299,7 @@ void k_add_b(hs_ctx *c, const u64 *a, int a_rows, const u64 *b, int b_rows, u64 
 {
     KTimer _kt(c, KID_ADD, (double)rows * nl * c->P->n * 24, st);
     int N = c->P->n;
-    add_b_kernel<<<dim3((N + 255) / 256, nl, rows), 256, 0, st>>>(a, b, o, N, nl, a_rows, b_rows, sub ? 1 : 0);
+    add_b_kernel<<<dim3((N / 2 + 255) / 256, nl, rows), 256, 0, st>>>(a, b, o, N, nl, a_rows, b_rows, sub ? 1 : 0);
     HS_CHECK_LAUNCH();
     count_kernel(c);
 }
@@ -1301,13 +1307,21 @@ void k_add_b(hs_ctx *c, const u64 *a, int a_rows, const u64 *b, int b_rows, u64 
 // o[r][i] = a[r][i] * s_i, rows of a/o with their own limb strides (drop + scale in one pass)
 __global__ void mul_scalar_s_kernel(const u64 *a, u64 *o, ScalarArg s, int N, int a_rl, int o_rl, int acc)
 {
-    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    int t = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
     if (t >= N) return;
     int i = blockIdx.y, r = blockIdx.z;
     u64 q = c_pk[i].q;
-    u64 v = d_shoup(a[((size_t)r * a_rl + i) * N + t], s.v[i], s.vs[i], q);
-    size_t x = ((size_t)r * o_rl + i) * N + t;
-    o[x] = acc ? d_add(o[x], v, q) : v;
+    const ulonglong2 va = *reinterpret_cast<const ulonglong2 *>(a + ((size_t)r * a_rl + i) * N + t);
+    ulonglong2 v;
+    v.x = d_shoup(va.x, s.v[i], s.vs[i], q);
+    v.y = d_shoup(va.y, s.v[i], s.vs[i], q);
+    ulonglong2 *op = reinterpret_cast<ulonglong2 *>(o + ((size_t)r * o_rl + i) * N + t);
+    if (acc) {
+        const ulonglong2 vo = *op;
+        v.x = d_add(vo.x, v.x, q);
+        v.y = d_add(vo.y, v.y, q);
+    }
+    *op = v;
 }
 
 void k_mul_scalar_s(hs_ctx *c, const u64 *a, u64 *o, const u64 *host_scal, int rows, int nl, int a_rl, int o_rl,
@@ -1315,7 +1329,7 @@ void k_mul_scalar_s(hs_ctx *c, const u64 *a, u64 *o, const u64 *host_scal, int r
 {
     KTimer _kt(c, KID_SCALAR, (double)rows * nl * c->P->n * (accumulate ? 24 : 16), st);
     int N = c->P->n;
-    mul_scalar_s_kernel<<<dim3((N + 255) / 256, nl, rows), 256, 0, st>>>(a, o, make_scalars(c->P, host_scal, nl), N,
+    mul_scalar_s_kernel<<<dim3((N / 2 + 255) / 256, nl, rows), 256, 0, st>>>(a, o, make_scalars(c->P, host_scal, nl), N,
                                                                           a_rl, o_rl, accumulate ? 1 : 0);
     HS_CHECK_LAUNCH();
     count_kernel(c);
@@ -1345,27 +1359,38 @@ void k_add_scalar_b(hs_ctx *c, u64 *a, const u64 *host_scal, int B, int ncomp, i
 // o[b] = tensor(a[b], bb[b % b_batch]); a/bb: [.][2][nl][N], o: [B][3][nl][N]
 __global__ void tensor_b_kernel(const u64 *a, const u64 *bb, u64 *o, int N, int nl, int b_batch)
 {
-    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    int t = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
     if (t >= N) return;
     int l = blockIdx.y, b = blockIdx.z;
     const PrimeK k = c_pk[l];
     size_t s = (size_t)nl * N, x = (size_t)l * N + t;
     const u64 *A = a + (size_t)b * 2 * s, *Bp = bb + (size_t)(b % b_batch) * 2 * s;
     u64 *O = o + (size_t)b * 3 * s;
-    u64 a0 = A[x], a1 = A[s + x], b0 = Bp[x], b1 = Bp[s + x];
-    O[x] = d_mulmod(a0, b0, k);
+    const ulonglong2 a0 = *reinterpret_cast<const ulonglong2 *>(A + x), a1 = *reinterpret_cast<const ulonglong2 *>(A + s + x);
+    const ulonglong2 b0 = *reinterpret_cast<const ulonglong2 *>(Bp + x), b1 = *reinterpret_cast<const ulonglong2 *>(Bp + s + x);
+    ulonglong2 o0, o1, o2;
+    o0.x = d_mulmod(a0.x, b0.x, k);
+    o0.y = d_mulmod(a0.y, b0.y, k);
     u64 hi = 0, lo = 0;
-    mac128(hi, lo, a0, b1);
-    mac128(hi, lo, a1, b0);
-    O[s + x] = d_reduce128(hi, lo, k);
-    O[2 * s + x] = d_mulmod(a1, b1, k);
+    mac128(hi, lo, a0.x, b1.x);
+    mac128(hi, lo, a1.x, b0.x);
+    o1.x = d_reduce128(hi, lo, k);
+    hi = lo = 0;
+    mac128(hi, lo, a0.y, b1.y);
+    mac128(hi, lo, a1.y, b0.y);
+    o1.y = d_reduce128(hi, lo, k);
+    o2.x = d_mulmod(a1.x, b1.x, k);
+    o2.y = d_mulmod(a1.y, b1.y, k);
+    *reinterpret_cast<ulonglong2 *>(O + x) = o0;
+    *reinterpret_cast<ulonglong2 *>(O + s + x) = o1;
+    *reinterpret_cast<ulonglong2 *>(O + 2 * s + x) = o2;
 }
 
 void k_tensor_b(hs_ctx *c, const u64 *a, const u64 *b, u64 *o, int B, int nl, int b_batch, cudaStream_t st)
 {
     KTimer _kt(c, KID_TENSOR, (double)B * nl * c->P->n * 56, st);
     int N = c->P->n;
-    tensor_b_kernel<<<dim3((N + 255) / 256, nl, B), 256, 0, st>>>(a, b, o, N, nl, b_batch);
+    tensor_b_kernel<<<dim3((N / 2 + 255) / 256, nl, B), 256, 0, st>>>(a, b, o, N, nl, b_batch);
     HS_CHECK_LAUNCH();
     count_kernel(c);
 }

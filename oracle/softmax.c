@@ -100,8 +100,12 @@ int orc_softmax(const orc_params *P, const orc_keys *K, const orc_softmax_desc *
         /* steps 3-5: sum over the coordinate blocks (rotations by -stride 2^i) */
         if ((rc = rot_sum(P, K, &S, nb, stride, -1))) goto done;
         /* G12 (a): bootstrap before step 6 if the rest of the aux thread would
-         * leave lambda below the main operand's level */
-        int main_level = d->variant == 0 ? y[0]->level : y0[0]->level;
+         * leave lambda below the main level.  Main level: Alg 1 -- the level of
+         * y (keeps the main thread from bootstrapping); version B -- the levels
+         * its update consumes, j + 2 (lambda y0, j squarings, one left for the
+         * next aux square) or k + 1 at j = k, capped by y0's level (G12) */
+        int need_b = j < d->k ? j + 2 : d->k + 1;
+        int main_level = d->variant == 0 ? y[0]->level : (y0[0]->level < need_b ? y0[0]->level : need_b);
         int need = poly_cost(ip) + 1 + ((d->variant == 1 && j > 1) ? 1 : 0);
         if (S->level - need < main_level) {
             if (d->bts) { if ((rc = bts_or_fail(P, K, d, &S, ip->b))) goto done; }

@@ -15,6 +15,7 @@
 // to the single-GPU run.
 #include <math.h>
 
+#include <algorithm>
 #include <vector>
 
 #include "hs_internal.h"
@@ -94,7 +95,10 @@ hs_status softmax_run(hs_ctx *c, const hs_keys *K, const hs_softmax_desc *d, con
         CtP S = ev_relin_rescale(K, acc.get(), st);  // C8: one division by P q_l
         acc.reset();
         rot_sum(K, S, nb, stride, -1, st);
-        const int main_level = d->variant == 0 ? y->level : y0->level;
+        // main level (G12): Alg 1 -- y's level; version B -- the
+        // levels its update consumes, j + 2 (k + 1 at j = k), capped by y0's
+        const int need_b = j < d->k ? j + 2 : d->k + 1;
+        const int main_level = d->variant == 0 ? y->level : std::min(y0->level, need_b);
         const int need = poly_cost(ip) + 1 + ((d->variant == 1 && j > 1) ? 1 : 0);
         // G12 (a): bootstrap before the inverse square root when the rest of the
         // aux thread would leave lambda below the main operand's level

@@ -1568,6 +1568,7 @@ __global__ void __launch_bounds__(256) ks_inner_h_kernel(const u64 *__restrict__
     const unsigned src = __ldg(A.perm[r] + t);
     const u64 *key = A.key[r];
     u64 h0 = 0, l0 = 0, h1 = 0, l1 = 0;
+#pragma unroll 4
     for (int j = 0; j < A.beta; j++) {
         const int lo = j * A.alpha, hi = min((j + 1) * A.alpha, nl), dn = hi - lo;
         const u64 k0 = key[(((size_t)j * 2 + 0) * ntot + pi) * N + t];
@@ -1639,6 +1640,7 @@ __global__ void __launch_bounds__(256) ks_inner_m_kernel(const u64 *__restrict__
     const size_t ntot = (size_t)A.n_q + A.n_t;
     const u64 *key = A.key[r];
     u64 h0 = 0, l0 = 0, h1 = 0, l1 = 0;
+#pragma unroll 4
     for (int j = 0; j < A.beta; j++) {
         const int lo = j * A.alpha, hi = min((j + 1) * A.alpha, nl), dn = hi - lo;
         const u64 k0 = key[(((size_t)j * 2 + 0) * ntot + pi) * N + t];

@@ -482,11 +482,31 @@ CtP ev_mult_const(const hs_ct *a, double v, int target, cudaStream_t st)
     const hs_params *P = c->P;
     if (target < 0 || target >= a->level) throw HsError(HS_ELEVEL, "mult_const: target level must be below the input");
     const int nl = target + 2;
-    CtP d = ct_new(c, target + 1, a->ncomp, st, a->batch);
     u64 s[HS_MAXP];
     residues(P, v * landing_scale(P, a->level, target), nl, s);
-    k_mul_scalar_s(c, a->d, d->d, s, (int)a->rows(), nl, a->level + 1, nl, false, st);  // drop + scale
     c->ledger[HS_LG_CMULT] += a->batch;
+    if (P->log_n == 16) {
+        // drop + scale + rescale without a pass over the whole ciphertext: only
+        // the dropped limb l = target+1 is scaled here; the NTT-fused rescale
+        // multiplies limbs 0..target by s_i in its epilogue (same words)
+        const size_t N = P->n;
+        const int l = target + 1, rows = (int)a->rows();
+        DBuf last((size_t)rows * N, st);
+        HS_CUDA(cudaMemcpy2DAsync(last.p, N * 8, a->d + (size_t)l * N, (a->level + 1) * N * 8, N * 8, rows,
+                                  cudaMemcpyDeviceToDevice, st));
+        PrimeMap pl;
+        pl.n = 1;
+        pl.p[0] = (unsigned char)l;
+        k_mul_scalar_pm(c, last.p, last.p, &s[l], rows, pl, st);
+        k_ntt(c, last.p, rows, pl, true, st);
+        DBuf w((size_t)rows * l * N, st);
+        CtP r = ct_new(c, target, a->ncomp, st, a->batch);
+        k_ntt_rescale(c, last.p, w.p, a->d, r->d, rows, l, st, s, (a->level + 1) * N);
+        c->ledger[HS_LG_RESCALE] += a->batch;
+        return r;
+    }
+    CtP d = ct_new(c, target + 1, a->ncomp, st, a->batch);
+    k_mul_scalar_s(c, a->d, d->d, s, (int)a->rows(), nl, a->level + 1, nl, false, st);  // drop + scale
     return ev_rescale(d.get(), st);
 }
 

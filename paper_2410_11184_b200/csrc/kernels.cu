@@ -318,6 +318,8 @@ struct NttEpi {
     int l, lq, add_comps;
     u64 inv[HS_MAXP], inv_sh[HS_MAXP];
     u64 rsh[HS_MAXP];  // MODE 1: floor(2^64 / q_i) (Shoup reduction of x < 2^64 by q_i)
+    int scaled;        // MODE 1: the input limbs are multiplied by scl_i first (fused mult_const)
+    u64 scl[HS_MAXP], scl_sh[HS_MAXP];
 };
 
 // Phase over the high 8 index bits (half-spans 2^15..2^8): C columns x 256 rows
@@ -455,8 +457,14 @@ __global__ void __launch_bounds__(32 * R) rows(u64 *data, PrimeMap pm, const u64
             const u64 inv = E.inv[li], ish = E.inv_sh[li];
             if (MODE == 1) {
                 u64 *o = E.o + row * E.ostr + (size_t)li * N + e0;
-                for (int i = tid; i < R * 256; i += 32 * R)
-                    o[i] = d_shoup(d_sub(in[i], reduce4(sm[i], T), T.q), inv, ish, T.q);
+                if (E.scaled) {
+                    const u64 sc = E.scl[li], scs = E.scl_sh[li];
+                    for (int i = tid; i < R * 256; i += 32 * R)
+                        o[i] = d_shoup(d_sub(d_shoup(in[i], sc, scs, T.q), reduce4(sm[i], T), T.q), inv, ish, T.q);
+                } else {
+                    for (int i = tid; i < R * 256; i += 32 * R)
+                        o[i] = d_shoup(d_sub(in[i], reduce4(sm[i], T), T.q), inv, ish, T.q);
+                }
             } else {
                 const int b = row >> 1, comp = row & 1;
                 const size_t ci = ((size_t)comp * E.l + li) * N + e0;
@@ -529,9 +537,12 @@ int tile()
 // Rescale of `rows` rows at level l (C9) around ONE forward transform:
 // w (scratch, rows*l limbs) = NTT(centred(last) mod q_i) with the lift fused
 // into the first pass, o = (a - w) q_l^-1 fused into the second.  last: the
-// rows' dropped limbs in coefficient form [rows][N]; a: [rows][l+1][N];
-// o: [rows][l][N].  N = 2^16 only (returns false otherwise).
-bool k_ntt_rescale(hs_ctx *c, const u64 *last, u64 *w, const u64 *a, u64 *o, int rows, int l, cudaStream_t st)
+// rows' dropped limbs in coefficient form [rows][N]; a: rows of a_row words
+// (default (l+1) N), limbs 0..l-1 read; o: [rows][l][N].  scal (optional):
+// a_i is multiplied by scal_i first -- a constant multiplication fused into
+// the rescale that follows it (C12).  N = 2^16 only (returns false otherwise).
+bool k_ntt_rescale(hs_ctx *c, const u64 *last, u64 *w, const u64 *a, u64 *o, int rows, int l, cudaStream_t st,
+                   const u64 *scal, size_t a_row)
 {
     const hs_params *P = c->P;
     if (P->log_n != 16) return false;
@@ -541,7 +552,12 @@ bool k_ntt_rescale(hs_ctx *c, const u64 *last, u64 *w, const u64 *a, u64 *o, int
     E.last = last;
     E.ain = a;
     E.o = o;
-    E.astr = (size_t)(l + 1) * N;
+    E.astr = a_row ? a_row : (size_t)(l + 1) * N;
+    E.scaled = scal != nullptr;
+    for (int i = 0; scal && i < l; i++) {
+        E.scl[i] = scal[i];
+        E.scl_sh[i] = hs_shoup_const(scal[i], P->prime[i]);
+    }
     E.ostr = (size_t)l * N;
     E.l = l;
     E.lq = l;

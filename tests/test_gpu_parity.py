@@ -292,6 +292,11 @@ def test_p16_hmult_rotate_parity(p16):
     r = hs.op(p16.K, "rotate", a, i=-128)
     same(r, O.op(p16.PO, p16.KO, "rotate", ao, i=-128))
     assert np.abs(hs.decrypt_decode(p16.K, m).real - za * zb).max() < 2.0 ** -20
+    # the N = 2^16 fused paths: rescale (lift + division in the NTT), constant
+    # multiply / level-down (scale folded into the rescale epilogue)
+    for name, kw in [("rescale", {}), ("mult_const", dict(c=-0.731, i=9)), ("level_down", dict(i=5))]:
+        same(hs.op(p16.K, name, a, c=kw.get("c", 0.0), i=kw.get("i", 0)),
+             O.op(p16.PO, p16.KO, name, ao, c=kw.get("c", 0.0), i=kw.get("i", 0)))
 
 
 # ---------------------------------------------------------------- bootstrapping (G11)

@@ -13,6 +13,7 @@
 //   target = level(u) - depth(d), depth = t+1 (d >= 2) or 1.
 //   The affine map u = (2x-a-b)/(b-a) costs one level (mult_const + add_const)
 //   unless [a, b] = [-1, 1].
+#include <map>
 #include <vector>
 
 #include "hs_internal.h"
@@ -34,6 +35,17 @@ struct Basis {
     int B;
     std::vector<CtP> T;  // T[0] unused
     std::vector<CtP> G;
+    // level-downs already made (a basis ciphertext is lowered to the same
+    // level by several products / subtractions; the same op, done once)
+    std::map<std::pair<const hs_ct *, int>, CtP> low;
+    const hs_ct *at(const hs_ct *x, int level)
+    {
+        if (x->level == level) return x;
+        auto key = std::make_pair(x, level);
+        auto it = low.find(key);
+        if (it != low.end()) return it->second.get();
+        return (low[key] = ev_level_down(x, level, st)).get();
+    }
 };
 
 CtP dbl_minus_one(const hs_keys *K, const hs_ct *x, cudaStream_t st)
@@ -71,7 +83,8 @@ CtP rec(Basis &E, const std::vector<double> &c, int target)
         r[g - k] = c[g - k] - c[g + k];
     }
     CtP Q = rec(E, q, target + 1);
-    CtP QT = ev_mult(E.K, Q.get(), E.G[clog2(g / E.B)].get(), E.st);
+    const hs_ct *Gj = E.G[clog2(g / E.B)].get();
+    CtP QT = ev_mult(E.K, Q.get(), Gj->level > Q->level ? E.at(Gj, Q->level) : Gj, E.st);
     CtP R = rec(E, r, target);
     return ev_add(QT.get(), R.get(), false, E.st);
 }
@@ -96,14 +109,10 @@ CtP eval_unit(const hs_keys *K, const hs_ct *u, const hs_poly *p, cudaStream_t s
         const int i1 = std::min(2 * a, top);
         for (int i0 = a + 1; i0 <= i1; i0 += per) {
             const int i2 = std::min(i1, i0 + per - 1);
-            std::vector<CtP> lowered;
             std::vector<const hs_ct *> ops;
             for (int i = i0; i <= i2; i++) {
                 const hs_ct *tb = E.T[i - a].get();
-                if (tb->level > E.T[a]->level) {
-                    lowered.push_back(ev_level_down(tb, E.T[a]->level, st));
-                    tb = lowered.back().get();
-                }
+                if (tb->level > E.T[a]->level) tb = E.at(tb, E.T[a]->level);
                 ops.push_back(tb);
             }
             CtP bb = ops.size() == 1 ? CtP() : ct_gather(ops.data(), (int)ops.size(), st);
@@ -112,7 +121,8 @@ CtP eval_unit(const hs_keys *K, const hs_ct *u, const hs_poly *p, cudaStream_t s
             for (int i = i0; i <= i2; i++) {
                 CtP v = ops.size() == 1 ? std::move(m2) : ct_view(m2.get(), i - i0);
                 const int b = i - a;
-                E.T[i] = a == b ? ev_add_const(v.get(), -1.0, st) : ev_add(v.get(), E.T[a - b].get(), true, st);
+                E.T[i] = a == b ? ev_add_const(v.get(), -1.0, st)
+                                : ev_add(v.get(), E.at(E.T[a - b].get(), v->level), true, st);
             }
         }
     }

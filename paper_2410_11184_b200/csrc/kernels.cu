@@ -1402,11 +1402,38 @@ __global__ void tensor_b_kernel(const u64 *a, const u64 *bb, u64 *o, int N, int 
     *reinterpret_cast<ulonglong2 *>(O + 2 * s + x) = o2;
 }
 
+// o[b] = (a0^2, 2 a0 a1, a1^2): the square, reading each operand once
+__global__ void square_b_kernel(const u64 *a, u64 *o, int N, int nl)
+{
+    int t = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
+    if (t >= N) return;
+    int l = blockIdx.y, b = blockIdx.z;
+    const PrimeK k = c_pk[l];
+    size_t s = (size_t)nl * N, x = (size_t)l * N + t;
+    const u64 *A = a + (size_t)b * 2 * s;
+    u64 *O = o + (size_t)b * 3 * s;
+    const ulonglong2 a0 = *reinterpret_cast<const ulonglong2 *>(A + x), a1 = *reinterpret_cast<const ulonglong2 *>(A + s + x);
+    ulonglong2 o0, o1, o2;
+    o0.x = d_mulmod(a0.x, a0.x, k);
+    o0.y = d_mulmod(a0.y, a0.y, k);
+    o1.x = d_mulmod(a0.x, a1.x, k);
+    o1.y = d_mulmod(a0.y, a1.y, k);
+    o1.x = d_add(o1.x, o1.x, k.q);
+    o1.y = d_add(o1.y, o1.y, k.q);
+    o2.x = d_mulmod(a1.x, a1.x, k);
+    o2.y = d_mulmod(a1.y, a1.y, k);
+    *reinterpret_cast<ulonglong2 *>(O + x) = o0;
+    *reinterpret_cast<ulonglong2 *>(O + s + x) = o1;
+    *reinterpret_cast<ulonglong2 *>(O + 2 * s + x) = o2;
+}
+
 void k_tensor_b(hs_ctx *c, const u64 *a, const u64 *b, u64 *o, int B, int nl, int b_batch, cudaStream_t st)
 {
-    KTimer _kt(c, KID_TENSOR, (double)B * nl * c->P->n * 56, st);
+    const bool sq = a == b && b_batch == B;
+    KTimer _kt(c, KID_TENSOR, (double)B * nl * c->P->n * (sq ? 40 : 56), st);
     int N = c->P->n;
-    tensor_b_kernel<<<dim3((N / 2 + 255) / 256, nl, B), 256, 0, st>>>(a, b, o, N, nl, b_batch);
+    if (sq) square_b_kernel<<<dim3((N / 2 + 255) / 256, nl, B), 256, 0, st>>>(a, o, N, nl);
+    else tensor_b_kernel<<<dim3((N / 2 + 255) / 256, nl, B), 256, 0, st>>>(a, b, o, N, nl, b_batch);
     HS_CHECK_LAUNCH();
     count_kernel(c);
 }

@@ -185,7 +185,7 @@ static void make_ltrans(const orc_params *P, const dmat *m, int level, int u, in
     int n0 = P->n / 2, N = P->n;
     T->level = level;
     T->u = u;
-    T->b1 = 1 << ((r + 2) / 2);   /* 2^ceil((r+1)/2) */
+    T->b1 = 1 << (r < 4 ? r : 4);  /* baby size 2^min(r, 4) (G11) */
     int cnt = 0;
     for (int d = 0; d < n0; d++) cnt += m->present[d];
     T->n_terms = cnt;
@@ -244,7 +244,7 @@ static void add_group_rotations(int n0, int ngroups, int *out, int *cnt, int max
     int s = ilog2i(n0), sz[ORC_MAXG], first = 0;
     group_sizes(s, ngroups, sz);
     for (int gi = 0; gi < ngroups; gi++) {
-        int u = 1 << first, r = sz[gi], b1 = 1 << ((r + 2) / 2);
+        int u = 1 << first, r = sz[gi], b1 = 1 << (r < 4 ? r : 4);
         int span = (1 << r) - 1;  /* idx in [-span, span] mod n0/u */
         int mod = n0 / u;
         for (int idx = -span; idx <= span; idx++) {

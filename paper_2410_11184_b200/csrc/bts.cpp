@@ -14,7 +14,7 @@
 //                diag(lambda, 2 lambda, ..., 2 lambda), lambda = q0/(4 pi Delta_out 2^e)
 //   out = x + conj(x)
 // Each transform: diagonals d (mod N0, structural presence), step unit u =
-// 2^(first stage index of the group), baby size b1 = 2^ceil((r+1)/2),
+// 2^(first stage index of the group), baby size b1 = 2^min(r, 4),
 // idx = d/u, giant g = idx / b1, baby b = idx % b1;
 //   out = rescale( sum_g Rot( sum_b pt_{g,b} (.) Rot(ct, b u), g b1 u ) ),
 // pt_{g,b} = encode(rot(diag_d, -g b1 u)) at the landing scale of the level.
@@ -153,7 +153,7 @@ void build_lintrans(hs_ctx *c, const DiagMat &m, int level, int unit, int r, Lin
     const int n0 = P->n / 2, N = P->n, nl = level + 1, ntg = nl + P->n_p;
     T.level = level;
     T.unit = unit;
-    T.b1 = 1 << ((r + 2) / 2);
+    T.b1 = 1 << std::min(r, 4);  // baby size 2^min(r, 4) (G11)
     std::vector<int> ds;
     for (int d = 0; d < n0; d++)
         if (!m.D[d].empty()) {
@@ -195,7 +195,7 @@ void add_group_rotations(int n0, int ngroups, std::vector<int> &rots)
     std::vector<int> sz = group_sizes(ilog2(n0), ngroups);
     int first = 0;
     for (int gi = 0; gi < ngroups; gi++) {
-        const int u = 1 << first, r = sz[gi], b1 = 1 << ((r + 2) / 2), span = (1 << r) - 1, mod = n0 / u;
+        const int u = 1 << first, r = sz[gi], b1 = 1 << std::min(r, 4), span = (1 << r) - 1, mod = n0 / u;
         for (int idx = -span; idx <= span; idx++) {
             int id = ((idx % mod) + mod) % mod;
             for (int rr : {(id % b1) * u, (id / b1) * b1 * u}) {

@@ -1824,10 +1824,77 @@ __global__ void __launch_bounds__(256) bsgs_inner_kernel(const u64 *__restrict__
     }
 }
 
+// Baby-major variant for large baby sets (b1 <= 16) and few giants (G <= GM):
+// each baby's two words are loaded once and feed every giant's 128-bit
+// accumulators; every 8 babies the accumulators fold through one REDC into a
+// reduced partial sum (8 q^2 < q 2^64 for q < 2^61), so any b1 stays exact.
+template <int GM>
+__global__ void __launch_bounds__(256) bsgs_inner_bm_kernel(const u64 *__restrict__ pts, u64 *__restrict__ out,
+                                                            const __grid_constant__ BsgsArg A, int N, int b1)
+{
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= N) return;
+    const int i = blockIdx.y, nl = A.nl;
+    const PrimeK k = c_pk[i < A.nlq ? i : A.n_q + (i - A.nlq)];
+    u64 h0[GM], l0[GM], h1[GM], l1[GM], s0[GM], s1[GM];
+#pragma unroll
+    for (int g = 0; g < GM; g++) h0[g] = l0[g] = h1[g] = l1[g] = s0[g] = s1[g] = 0;
+    for (int b = 0; b < b1; b++) {
+        if (A.R[b]) {
+            const u64 r0 = A.R[b][(size_t)i * N + t], r1 = A.R[b][((size_t)nl + i) * N + t];
+#pragma unroll
+            for (int g = 0; g < GM; g++) {
+                const int kk = g < A.G ? A.tk[g * 16 + b] : -1;
+                if (kk >= 0) {
+                    const u64 p = pts[((size_t)kk * nl + i) * N + t];
+                    mac128(h0[g], l0[g], r0, p);
+                    mac128(h1[g], l1[g], r1, p);
+                }
+            }
+        }
+        if ((b & 7) == 7 || b == b1 - 1) {
+#pragma unroll
+            for (int g = 0; g < GM; g++) {
+                s0[g] = d_add(s0[g], d_redc(h0[g], l0[g], k), k.q);
+                s1[g] = d_add(s1[g], d_redc(h1[g], l1[g], k), k.q);
+                h0[g] = l0[g] = h1[g] = l1[g] = 0;
+            }
+        }
+    }
+#pragma unroll
+    for (int g = 0; g < GM; g++)
+        if (g < A.G) {
+            out[((size_t)g * 2 * nl + i) * N + t] = s0[g];
+            out[((size_t)(g * 2 + 1) * nl + i) * N + t] = s1[g];
+        }
+}
+
 void k_bsgs_inner(hs_ctx *c, const u64 *const *R, int b1, const u64 *pts, const int *tk, int G, int nl, u64 *out,
                   cudaStream_t st, int nlq)
 {
-    if (b1 < 1 || b1 > 8 || G < 1 || G > 16) throw HsError(HS_EINVAL, "bsgs_inner: baby / giant count out of range");
+    if (b1 < 1 || b1 > 16 || G < 1 || G > 16) throw HsError(HS_EINVAL, "bsgs_inner: baby / giant count out of range");
+    if (b1 > 8) {  // baby-major kernel
+        if (G > 4) throw HsError(HS_EINVAL, "bsgs_inner: more than 4 giants with more than 8 babies");
+        BsgsArg A;
+        int terms = 0, babies = 0;
+        for (int b = 0; b < 16; b++) A.R[b] = b < b1 ? R[b] : nullptr;
+        for (int b = 0; b < b1; b++) babies += R[b] != nullptr;
+        for (int g = 0; g < 16; g++)
+            for (int b = 0; b < 16; b++) {
+                A.tk[g * 16 + b] = (g < G && b < b1) ? tk[g * b1 + b] : -1;
+                terms += A.tk[g * 16 + b] >= 0;
+            }
+        A.G = G;
+        A.nl = nl;
+        A.nlq = nlq < 0 ? nl : nlq;
+        A.n_q = c->P->n_q;
+        const int N = c->P->n;
+        KTimer _kt(c, KID_PTMUL, (double)(2 * babies + terms + 2 * G) * nl * N * 8, st);
+        bsgs_inner_bm_kernel<4><<<dim3((N + 255) / 256, nl), 256, 0, st>>>(pts, out, A, N, b1);
+        HS_CHECK_LAUNCH();
+        count_kernel(c);
+        return;
+    }
     BsgsArg A;
     int terms = 0, babies = 0;
     for (int b = 0; b < 16; b++) A.R[b] = b < b1 ? R[b] : nullptr;

@@ -247,6 +247,10 @@ typedef struct {
     hs_exchange_fn exchange;  /* required when world > 1                            */
     void *exchange_user;
     hs_bts *bts;              /* NULL: no bootstrapping (HS_ELEVEL when needed)     */
+    int newton;               /* Alg 1 only: Newton steps y (3 - x y^2)/2 after the
+                                 LAST inverse-square-root polynomial, which is then a
+                                 seed (PAPER.md 1311-1327 [App. A]; G24);
+                                 0 = none.  HS_EINVAL if < 0 or with version B       */
 } hs_softmax_desc;
 
 /* One ciphertext (m = 1). */

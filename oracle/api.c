@@ -15,15 +15,6 @@ orc_ct *orc_encrypt_sk(const orc_params *, const orc_keys *, const u64 *, int, u
 void orc_decrypt(const orc_params *, const orc_keys *, const orc_ct *, u64 *);
 double orc_encode_naive_coeff(const orc_params *, const double *, const double *, double, int);
 
-typedef orc_ct *(*orc_bts_fn)(const orc_params *, const orc_keys *, const orc_ct *, void *, double);
-typedef struct {
-    int n, m, k, variant;
-    const orc_cheb *exp_poly;
-    const orc_cheb *inv_poly;
-    orc_bts_fn bts;
-    void *bts_ctx;
-} orc_softmax_desc;
-int orc_softmax(const orc_params *, const orc_keys *, const orc_softmax_desc *, orc_ct *const *, orc_ct **);
 
 orc_params *orc_api_params(int log_n, int n_q, const int *q_bits, int n_p, const int *p_bits, int alpha,
                            const int *log2_anchor)
@@ -166,7 +157,7 @@ int orc_api_cheb_depth(int deg) { return orc_cheb_depth(deg); }
 /* polys: n_poly = 1 + k entries (exp first), degs/as/bs arrays, coeffs concatenated */
 int orc_api_softmax(const orc_params *P, const orc_keys *K, int n, int m, int k, int variant,
                     const int *degs, const double *as, const double *bs, const double *coeffs,
-                    orc_ct *const *in, orc_ct **out)
+                    orc_ct *const *in, orc_ct **out, int newton)
 {
     orc_cheb *polys = malloc(sizeof(orc_cheb) * (k + 1));
     const double *cp = coeffs;
@@ -177,7 +168,7 @@ int orc_api_softmax(const orc_params *P, const orc_keys *K, int n, int m, int k,
         polys[i].c = cp;
         cp += degs[i] + 1;
     }
-    orc_softmax_desc d = {n, m, k, variant, &polys[0], &polys[1], NULL, NULL};
+    orc_softmax_desc d = {n, m, k, variant, &polys[0], &polys[1], NULL, NULL, newton};
     int rc = orc_softmax(P, K, &d, in, out);
     free(polys);
     return rc;
@@ -194,6 +185,11 @@ void orc_bts_set_free(orc_bts_set *S);
 int orc_bts_rotations(const orc_params *P, int n_cts, int n_stc, int *out, int max);
 int orc_bts_exponent(const orc_params *P, int arcsine, double bound);
 orc_ct *orc_bootstrap(const orc_params *P, const orc_keys *K, const orc_ct *in, void *ctx, double bound);
+
+orc_ct *orc_api_newton(const orc_params *P, const orc_keys *K, const orc_ct *xh, const orc_ct *y)
+{
+    return orc_newton_invsqrt_step(P, K, xh, y);
+}
 
 void *orc_api_bts_new(const orc_params *P, int K, int r, int n_cts, int n_stc, int arcsine, int deg,
                       const double *coeffs, int out_level)
@@ -212,7 +208,7 @@ orc_ct *orc_api_bootstrap(const orc_params *P, const orc_keys *K, const orc_ct *
 }
 int orc_api_softmax_bts(const orc_params *P, const orc_keys *K, int n, int m, int k, int variant,
                         const int *degs, const double *as, const double *bs, const double *coeffs,
-                        orc_ct *const *in, orc_ct **out, void *bts)
+                        orc_ct *const *in, orc_ct **out, void *bts, int newton)
 {
     orc_cheb *polys = malloc(sizeof(orc_cheb) * (k + 1));
     const double *cp = coeffs;
@@ -223,7 +219,7 @@ int orc_api_softmax_bts(const orc_params *P, const orc_keys *K, int n, int m, in
         polys[i].c = cp;
         cp += degs[i] + 1;
     }
-    orc_softmax_desc d = {n, m, k, variant, &polys[0], &polys[1], bts ? orc_bootstrap : NULL, bts};
+    orc_softmax_desc d = {n, m, k, variant, &polys[0], &polys[1], bts ? orc_bootstrap : NULL, bts, newton};
     int rc = orc_softmax(P, K, &d, in, out);
     free(polys);
     return rc;

@@ -95,8 +95,10 @@ def lib():
         L.orc_api_cheb_depth.restype = C.c_int
         L.orc_api_cheb_depth.argtypes = [C.c_int]
         L.orc_api_softmax.restype = C.c_int
+        L.orc_api_newton.restype = vp
+        L.orc_api_newton.argtypes = [vp, vp, vp, vp]
         L.orc_api_softmax.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, i32p, f64p, f64p, f64p,
-                                      C.POINTER(vp), C.POINTER(vp)]
+                                      C.POINTER(vp), C.POINTER(vp), C.c_int]
         L.orc_api_ledger.argtypes = [C.POINTER(C.c_long)]
         _lib = L
     return _lib
@@ -263,6 +265,12 @@ def rotate_hoisted(P: Params, K: Keys, a: Ct, rots):
     return [Ct(P, out[i]) for i in range(len(rots))]
 
 
+def newton_step(P: Params, K: Keys, xh: Ct, y: Ct) -> Ct:
+    """One Newton inverse-square-root step y (3 - x y^2)/2 from xh = x/2
+    (PAPER.md 1313-1316; G24)."""
+    return Ct(P, lib().orc_api_newton(P.ptr, K.ptr, xh.ptr, y.ptr))
+
+
 def cheb(P: Params, K: Keys, x: Ct, poly: dict) -> Ct:
     c = np.ascontiguousarray(poly["coeffs"], np.float64)
     return Ct(P, lib().orc_api_cheb(P.ptr, K.ptr, x.ptr, len(c) - 1, poly["a"], poly["b"], c))
@@ -282,7 +290,8 @@ def softmax(P: Params, K: Keys, cts, n, k, variant, exp_poly, inv_polys):
     m = len(cts)
     ins = (C.c_void_p * m)(*[c.ptr for c in cts])
     outs = (C.c_void_p * m)()
-    rc = lib().orc_api_softmax(P.ptr, K.ptr, n, m, k, variant, degs, a_s, b_s, co, ins, outs)
+    rc = lib().orc_api_softmax(P.ptr, K.ptr, n, m, k, variant, degs, a_s, b_s, co, ins, outs,
+                               int(inv_polys[-1].get("newton", 0)))
     if rc != 0:
         raise RuntimeError(f"oracle softmax failed rc={rc}")
     return [Ct(P, outs[i]) for i in range(m)]
@@ -369,7 +378,7 @@ def _bts_sigs():
     L.orc_api_bts_exponent.argtypes = [vp, C.c_int, C.c_double]
     L.orc_api_softmax_bts.restype = C.c_int
     L.orc_api_softmax_bts.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, i32p, f64p, f64p, f64p,
-                                      C.POINTER(vp), C.POINTER(vp), vp]
+                                      C.POINTER(vp), C.POINTER(vp), vp, C.c_int]
     L._bts_ready = True
     return L
 
@@ -419,7 +428,8 @@ def softmax_bts(P: Params, K: Keys, cts, n, k, variant, exp_poly, inv_polys, bts
     ins = (C.c_void_p * m)(*[c.ptr for c in cts])
     outs = (C.c_void_p * m)()
     rc = _bts_sigs().orc_api_softmax_bts(P.ptr, K.ptr, n, m, k, variant, degs, a_s, b_s, co, ins, outs,
-                                         bts.ptr if bts is not None else None)
+                                         bts.ptr if bts is not None else None,
+                                         int(inv_polys[-1].get("newton", 0)))
     if rc != 0:
         raise RuntimeError(f"oracle softmax failed rc={rc}")
     return [Ct(P, outs[i]) for i in range(m)]

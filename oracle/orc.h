@@ -131,4 +131,17 @@ int orc_cheb_depth(int deg);
 orc_ct *orc_eval_cheb(const orc_params *P, const orc_keys *K, const orc_ct *x, const orc_cheb *p);
 orc_ct *orc_eval_cheb_unit(const orc_params *P, const orc_keys *K, const orc_ct *u, const orc_cheb *p);
 
+/* softmax.c (Alg 1 / Alg 2 / version B, C14, G12, G24) */
+typedef orc_ct *(*orc_bts_fn)(const orc_params *, const orc_keys *, const orc_ct *, void *, double);
+typedef struct {
+    int n, m, k, variant;           /* variant 0 = Alg 1, 1 = Alg B                     */
+    const orc_cheb *exp_poly;       /* exp(x/2^k) on [-M, 0]                            */
+    const orc_cheb *inv_poly;       /* k polys, one per iteration                       */
+    orc_bts_fn bts;                 /* NULL: no bootstrapping                           */
+    void *bts_ctx;
+    int newton;                     /* Alg 1: Newton steps after the LAST poly (G24)    */
+} orc_softmax_desc;
+int orc_softmax(const orc_params *P, const orc_keys *K, const orc_softmax_desc *d, orc_ct *const *x, orc_ct **out);
+orc_ct *orc_newton_invsqrt_step(const orc_params *P, const orc_keys *K, const orc_ct *xh, const orc_ct *y);
+
 #endif

@@ -19,16 +19,6 @@
 #include <string.h>
 #include <math.h>
 
-typedef orc_ct *(*orc_bts_fn)(const orc_params *, const orc_keys *, const orc_ct *, void *, double);
-
-typedef struct {
-    int n, m, k, variant;           /* variant 0 = Alg 1, 1 = Alg B */
-    const orc_cheb *exp_poly;       /* exp(x/2^k) on [-M, 0]         */
-    const orc_cheb *inv_poly;       /* k polys, one per iteration     */
-    orc_bts_fn bts;                 /* NULL: no bootstrapping         */
-    void *bts_ctx;
-} orc_softmax_desc;
-
 enum { ORC_OK = 0, ORC_EINVAL = 1, ORC_ELEVEL = 2, ORC_EKEY = 3 };
 
 static int ilog2(int x) { int t = 0; while ((1 << t) < x) t++; return t; }
@@ -56,6 +46,21 @@ static int bts_or_fail(const orc_params *P, const orc_keys *K, const orc_softmax
     return ORC_OK;
 }
 
+/* PAPER.md 1313-1316: z1 = (x/2) y; z2 = y y; z3 = (3/2) y; return z3 - z1 z2.
+ * xh = x/2 is computed once by the caller.  Levels (C11, C12): z1 at
+ * min(l(xh), l(y)) - 1, z2 at l(y) - 1, z1 z2 one below the lower of the two,
+ * z3 multiplied straight to that level, so the step costs 2 levels. */
+orc_ct *orc_newton_invsqrt_step(const orc_params *P, const orc_keys *K, const orc_ct *xh, const orc_ct *y)
+{
+    orc_ct *z1 = orc_op_mult(P, K, xh, y);
+    orc_ct *z2 = orc_op_mult(P, K, y, y);
+    orc_ct *p = orc_op_mult(P, K, z1, z2);
+    orc_ct *z3 = orc_op_mult_const(P, y, 1.5, p->level);
+    orc_ct *r = orc_op_sub(P, z3, p);
+    orc_ct_release(z1); orc_ct_release(z2); orc_ct_release(p); orc_ct_release(z3);
+    return r;
+}
+
 static int poly_cost(const orc_cheb *p)
 {
     return orc_cheb_depth(p->deg) + ((p->a == -1.0 && p->b == 1.0) ? 0 : 1);
@@ -64,7 +69,7 @@ static int poly_cost(const orc_cheb *p)
 int orc_softmax(const orc_params *P, const orc_keys *K, const orc_softmax_desc *d, orc_ct *const *x, orc_ct **out)
 {
     int m = d->m, n = d->n, N0 = P->n / 2;
-    if (m < 1 || n % m) return ORC_EINVAL;
+    if (m < 1 || n % m || d->newton < 0 || (d->newton > 0 && d->variant != 0)) return ORC_EINVAL;
     int nb = n / m;
     if ((nb & (nb - 1)) || nb > N0) return ORC_EINVAL;
     int stride = N0 / nb;
@@ -101,19 +106,46 @@ int orc_softmax(const orc_params *P, const orc_keys *K, const orc_softmax_desc *
         if ((rc = rot_sum(P, K, &S, nb, stride, -1))) goto done;
         /* G12 (a): bootstrap before step 6 if the rest of the aux thread would
          * leave lambda below the main level.  Main level: Alg 1 -- the level of
-         * y (keeps the main thread from bootstrapping); version B -- the levels
-         * its update consumes, j + 2 (lambda y0, j squarings, one left for the
-         * next aux square) or k + 1 at j = k, capped by y0's level (G12) */
+         * y (keeps the main thread from bootstrapping), at j = k only the 2
+         * levels of the last update; version B -- the levels its update
+         * consumes, j + 2 (lambda y0, j squarings, one left for the next aux
+         * square) or k + 1 at j = k, capped by y0's level (G12) */
         int need_b = j < d->k ? j + 2 : d->k + 1;
-        int main_level = d->variant == 0 ? y[0]->level : (y0[0]->level < need_b ? y0[0]->level : need_b);
+        int main_a = j < d->k ? y[0]->level : (y[0]->level < 2 ? y[0]->level : 2);
+        int main_level = d->variant == 0 ? main_a : (y0[0]->level < need_b ? y0[0]->level : need_b);
         int need = poly_cost(ip) + 1 + ((d->variant == 1 && j > 1) ? 1 : 0);
+        /* G24: Newton steps after the last polynomial read x/2 (one level below
+         * S), 2 levels each, then the mask: S must also supply 2 t + 2 levels */
+        int nt = j == d->k ? d->newton : 0;
+        if (nt > 0 && 2 * nt + 2 > need) need = 2 * nt + 2;
         if (S->level - need < main_level) {
             if (d->bts) { if ((rc = bts_or_fail(P, K, d, &S, ip->b))) goto done; }
             else if (S->level - need < 0) { rc = ORC_ELEVEL; goto done; }
         }
         /* step 6: InvSqrt (Alg 1) or x^(-1/2^j) (Alg B, G4) */
         lj = orc_eval_cheb(P, K, S, ip);
+        if (nt > 0) {
+            /* G24 (n): bootstrap the seed when the Newton steps and the mask
+             * would leave lambda below the main level */
+            int top = lj->level < S->level - 1 ? lj->level : S->level - 1;
+            if (top - 2 * nt - 1 < main_level && d->bts) {
+                if ((rc = bts_or_fail(P, K, d, &lj, 1.1 / sqrt(ip->a)))) goto done;
+                top = lj->level < S->level - 1 ? lj->level : S->level - 1;
+            }
+            if (top - 2 * nt - 1 < 0) { rc = ORC_ELEVEL; goto done; }
+            orc_ct *xh = orc_op_mult_const(P, S, 0.5, S->level - 1);
+            for (int t = 0; t < nt; t++) swap_in(&lj, orc_newton_invsqrt_step(P, K, xh, lj));
+            orc_ct_release(xh);
+        }
         orc_ct_release(S); S = NULL;
+        /* G12 (b), Alg 1: bootstrap lambda_j BEFORE the mask when the mask
+         * would leave it below the main level: the broadcast then copies block
+         * 0's value, so every coordinate of an instance sees the same
+         * bootstrapping error (a common factor the next normalisation absorbs)
+         * instead of an independent one per slot */
+        if (d->variant == 0 && lj->level - 1 < main_level && d->bts) {
+            if ((rc = bts_or_fail(P, K, d, &lj, 1.1 / sqrt(ip->a)))) goto done;
+        }
         /* step 7: mask block 0 */
         if (lj->level < 1) { rc = ORC_ELEVEL; goto done; }
         swap_in(&lj, orc_op_mult_pt(P, lj, mask, NULL, lj->level - 1));
@@ -127,11 +159,13 @@ int orc_softmax(const orc_params *P, const orc_keys *K, const orc_softmax_desc *
             orc_ct_release(lam);
             lam = lj; lj = NULL;
         }
-        /* G12 (b): bootstrap lambda again if it ended below the main level */
-        if (lam->level < main_level && d->bts) {
-            if ((rc = bts_or_fail(P, K, d, &lam, d->variant == 1 ? 1.5 : 1.1 / sqrt(ip->a)))) goto done;
+        /* G12 (b), version B: bootstrap lambda (the product) if it ended below
+         * the main level */
+        if (d->variant == 1 && lam->level < main_level && d->bts) {
+            if ((rc = bts_or_fail(P, K, d, &lam, 1.5))) goto done;
         }
         /* ---- main thread ---- */
+        if (lam->level < 1) { rc = ORC_ELEVEL; goto done; }
         for (int c = 0; c < m; c++) {
             if (d->variant == 0) {
                 orc_ct *z = orc_op_mult(P, K, lam, y[c]);        /* Alg 1 line 4 */

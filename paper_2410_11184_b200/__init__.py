@@ -313,8 +313,9 @@ def _softmax_desc(n, m, k, variant, exp_poly, inv_polys, world=1, rank=0, exchan
     keep += [arr, ep]
     fn = L.EXCHANGE_FN(0) if exchange is None else exchange
     keep.append(fn)
+    # a table's last entry may carry "newton": the polynomial is then a seed (G24)
     d = L.SoftmaxDesc(n, m, k, 0 if variant in (0, "A") else 1, ep, arr, world, rank, fn, None,
-                      bts.ptr if bts is not None else None)
+                      bts.ptr if bts is not None else None, int(inv_polys[-1].get("newton", 0)))
     return d, keep
 
 

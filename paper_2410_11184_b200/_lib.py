@@ -53,7 +53,8 @@ EXCHANGE_FN = C.CFUNCTYPE(C.c_int, vp, vp, vp, C.c_size_t, vp)
 class SoftmaxDesc(C.Structure):
     _fields_ = [("n", C.c_int), ("m", C.c_int), ("k", C.c_int), ("variant", C.c_int),
                 ("exp_poly", C.POINTER(Poly)), ("inv_poly", C.POINTER(Poly)), ("world", C.c_int),
-                ("rank", C.c_int), ("exchange", EXCHANGE_FN), ("exchange_user", vp), ("bts", vp)]
+                ("rank", C.c_int), ("exchange", EXCHANGE_FN), ("exchange_user", vp), ("bts", vp),
+                ("newton", C.c_int)]
 
 
 class BtsDesc(C.Structure):

@@ -7,6 +7,9 @@
 //   shared aux sum               DESIGN.md C15 / G6: sum_c tensor(y_c, y_c)
 //                                exactly mod q, ONE relin + rescale
 //   bootstrap placement          PAPER.md 429-440 [sec 5.1.3], rule G12
+//   Newton inverse square root   PAPER.md 1311-1327 [App. A] (G22 reading of
+//                                the printed step), after the last polynomial
+//                                of Alg 1 when d->newton > 0 (G24)
 //
 // Sharding: rank r owns ciphertexts [r m/G, (r+1) m/G).
 // The only exchange is the degree-2 partial aux sum of each iteration; the
@@ -34,6 +37,17 @@ void rot_sum(const hs_keys *K, CtP &S, int nb, int stride, int sign, cudaStream_
 
 [[noreturn]] void level_error(const char *what) { throw HsError(HS_ELEVEL, std::string("softmax: ") + what); }
 
+// PAPER.md 1313-1316: z1 = (x/2) y; z2 = y y; z3 = (3/2) y; y' = z3 - z1 z2
+// (2 levels; z3 multiplied straight to the level of z1 z2, C12)
+CtP newton_step(const hs_keys *K, const hs_ct *xh, const hs_ct *y, cudaStream_t st)
+{
+    CtP z1 = ev_mult(K, xh, y, st);
+    CtP z2 = ev_mult(K, y, y, st);
+    CtP p = ev_mult(K, z1.get(), z2.get(), st);
+    CtP z3 = ev_mult_const(y, 1.5, p->level, st);
+    return ev_add(z3.get(), p.get(), true, st);
+}
+
 }  // namespace
 
 hs_status softmax_run(hs_ctx *c, const hs_keys *K, const hs_softmax_desc *d, const hs_ct *const *in,
@@ -42,7 +56,8 @@ hs_status softmax_run(hs_ctx *c, const hs_keys *K, const hs_softmax_desc *d, con
     const hs_params *P = c->P;
     const int N0 = P->n / 2;
     const int m = d->m, n = d->n, world = d->world < 1 ? 1 : d->world;
-    if (m < 1 || n < 1 || n % m || d->k < 1 || !d->exp_poly || !d->inv_poly || d->variant < 0 || d->variant > 1)
+    if (m < 1 || n < 1 || n % m || d->k < 1 || !d->exp_poly || !d->inv_poly || d->variant < 0 || d->variant > 1 ||
+        d->newton < 0 || (d->newton > 0 && d->variant != 0))
         throw HsError(HS_EINVAL, "softmax: bad descriptor");
     if (m % world || (size_t)(m / world) != m_local) throw HsError(HS_EINVAL, "softmax: m_local != m / world");
     if (world > 1 && !d->exchange) throw HsError(HS_EINVAL, "softmax: world > 1 needs an exchange callback");
@@ -95,11 +110,17 @@ hs_status softmax_run(hs_ctx *c, const hs_keys *K, const hs_softmax_desc *d, con
         CtP S = ev_relin_rescale(K, acc.get(), st);  // C8: one division by P q_l
         acc.reset();
         rot_sum(K, S, nb, stride, -1, st);
-        // main level (G12): Alg 1 -- y's level; version B -- the
-        // levels its update consumes, j + 2 (k + 1 at j = k), capped by y0's
+        // main level (G12): Alg 1 -- y's level (the 2 levels of the
+        // last update at j = k); version B -- the levels its update consumes,
+        // j + 2 (k + 1 at j = k), capped by y0's
         const int need_b = j < d->k ? j + 2 : d->k + 1;
-        const int main_level = d->variant == 0 ? y->level : std::min(y0->level, need_b);
-        const int need = poly_cost(ip) + 1 + ((d->variant == 1 && j > 1) ? 1 : 0);
+        const int main_a = j < d->k ? y->level : std::min(y->level, 2);
+        const int main_level = d->variant == 0 ? main_a : std::min(y0->level, need_b);
+        int need = poly_cost(ip) + 1 + ((d->variant == 1 && j > 1) ? 1 : 0);
+        // G24: Newton steps after the last polynomial read x/2 (one level
+        // below S), 2 levels each, then the mask: S supplies 2 t + 2 levels too
+        const int nt = j == d->k ? d->newton : 0;
+        if (nt > 0) need = std::max(need, 2 * nt + 2);
         // G12 (a): bootstrap before the inverse square root when the rest of the
         // aux thread would leave lambda below the main operand's level
         if (S->level - need < main_level) {
@@ -107,16 +128,35 @@ hs_status softmax_run(hs_ctx *c, const hs_keys *K, const hs_softmax_desc *d, con
             else if (S->level - need < 0) level_error("aux thread needs bootstrapping");
         }
         CtP lj = ev_cheb(K, S.get(), ip, st);
+        if (nt > 0) {
+            // G24 (n): bootstrap the seed when the Newton steps and the mask
+            // would leave lambda below the main level
+            int top = std::min(lj->level, S->level - 1);
+            if (top - 2 * nt - 1 < main_level && d->bts) {
+                lj = ev_bootstrap(K, d->bts, lj.get(), 1.1 / sqrt(ip->a), st);
+                top = std::min(lj->level, S->level - 1);
+            }
+            if (top - 2 * nt - 1 < 0) level_error("Newton steps out of levels");
+            CtP xh = ev_mult_const(S.get(), 0.5, S->level - 1, st);
+            for (int t = 0; t < nt; t++) lj = newton_step(K, xh.get(), lj.get(), st);
+        }
         S.reset();
+        // G12 (b), Alg 1: bootstrap lambda_j BEFORE the mask when the mask would
+        // leave it below the main level -- the broadcast then gives every
+        // coordinate of an instance block 0's value, one common bootstrapping
+        // error per instance (absorbed by the next normalisation)
+        if (d->variant == 0 && lj->level - 1 < main_level && d->bts)
+            lj = ev_bootstrap(K, d->bts, lj.get(), 1.1 / sqrt(ip->a), st);
         if (lj->level < 1) level_error("no level for the mask");
         lj = ev_mult_pt(lj.get(), mask.data(), nullptr, lj->level - 1, st);
         rot_sum(K, lj, nb, stride, +1, st);
         if (d->variant == 1 && j > 1) lam = ev_mult(K, lam.get(), lj.get(), st);
         else lam = std::move(lj);
-        // G12 (b): bootstrap lambda again if it ended below the main level
-        if (lam->level < main_level && d->bts)
-            lam = ev_bootstrap(K, d->bts, lam.get(), d->variant == 1 ? 1.5 : 1.1 / sqrt(ip->a), st);
+        // G12 (b), version B: bootstrap lambda (the product) if it ended below
+        // the main level
+        if (d->variant == 1 && lam->level < main_level && d->bts) lam = ev_bootstrap(K, d->bts, lam.get(), 1.5, st);
         // ---- main thread (lam broadcast against the batch)
+        if (lam->level < 1) level_error("lambda out of levels");
         if (d->variant == 0) {
             CtP z = ev_mult(K, lam.get(), y.get(), st);
             y = ev_mult(K, z.get(), z.get(), st);

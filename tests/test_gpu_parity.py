@@ -307,7 +307,7 @@ def toyb():
     P = hs.Params.from_preset(pre)
     PO = O.Params.from_preset(pre)
     rots = set(hs.bts_rotations(P, pre["bts"]))
-    for n, m in [(256, 16), (256, 1)]:
+    for n, m in [(256, 16), (256, 1), (2048, 1)]:
         nb = n // m
         stride = (P.n // 2) // nb
         i = 0
@@ -361,7 +361,11 @@ def test_softmax_bts_parity(toyb, tables, table, m):
         o_in.append(O.encrypt(PO, KO, pt, 12, 4040, c))
     toyb["ctx"].ledger_reset()
     g_out = hs.softmax_many_ctxt(K, g_in, n, m, k, var, tab["exp"], tab["inv"], bts=toyb["B"])
+    g_led = toyb["ctx"].ledger()
+    O.ledger_reset()
     o_out = O.softmax_bts(PO, KO, o_in, n, k, var, tab["exp"], tab["inv"], toyb["BO"])
+    # the same bootstrap schedule on both sides (G12)
+    assert g_led["bts"] == O.ledger()["bts"]
     for gc, oc in zip(g_out, o_out):
         same(gc, oc)
     dec = np.stack([hs.decrypt_decode(K, c).real for c in g_out])
@@ -369,9 +373,8 @@ def test_softmax_bts_parity(toyb, tables, table, m):
     ref = np.exp(x - x.max(1, keepdims=True))
     ref /= ref.sum(1, keepdims=True)
     assert np.abs(y - ref).max() < 2.0 ** -15
-    led = toyb["ctx"].ledger()
-    n_bts = led["bts"]
-    assert (0 < n_bts <= 2 * k) if var == 1 else n_bts >= k
+    n_bts = g_led["bts"]
+    assert 0 < n_bts <= 2 * k
     if var == 1:
         # the same Softmax as a replayable CUDA graph (hs_softmax_plan_create):
         # every replay recomputes the words above, bit for bit
@@ -383,3 +386,30 @@ def test_softmax_bts_parity(toyb, tables, table, m):
                 same(gc, oc)
             assert toyb["ctx"].ledger()["bts"] == n_bts
         del plan
+
+
+def test_softmax_newton_parity(toyb, tables):
+    """Config-5 schedule (n = N0, Alg 1, degree-63 middle steps, last step =
+    seed + 3 Newton steps, G24) on the N = 2^12 ring with P16's chain:
+    ciphertext word-for-word against the oracle, accuracy 2^-15."""
+    hs = _hs()
+    P, PO, K, KO = toyb["P"], toyb["PO"], toyb["K"], toyb["KO"]
+    tab = tables["toy_n2048_M32_k4_A"]
+    cfg = tab["config"]
+    n, k, m, L = cfg["n"], cfg["k"], 1, 1
+    assert n == P.n // 2 and tab["inv"][-1]["newton"] == 3
+    x = W.softmax_inputs(L, n, cfg["M"], seed=W.derive_seed("x", "toy_n2048_M32_k4_A"))
+    pt = P.encode(P.pack(x, m)[0], scale=P.scale(12), level=12)
+    g_in = [hs.encrypt(K, pt, 12, 4040, 0)]
+    o_in = [O.encrypt(PO, KO, pt, 12, 4040, 0)]
+    toyb["ctx"].ledger_reset()
+    g_out = hs.softmax_many_ctxt(K, g_in, n, m, k, 0, tab["exp"], tab["inv"], bts=toyb["B"])
+    led = toyb["ctx"].ledger()
+    O.ledger_reset()
+    o_out = O.softmax_bts(PO, KO, o_in, n, k, 0, tab["exp"], tab["inv"], toyb["BO"])
+    same(g_out[0], o_out[0])
+    assert led["bts"] == O.ledger()["bts"] > 0
+    y = P.unpack(hs.decrypt_decode(K, g_out[0]).real[None], L, n)
+    ref = np.exp(x - x.max(1, keepdims=True))
+    ref /= ref.sum(1, keepdims=True)
+    assert np.abs(y - ref).max() < 2.0 ** -15

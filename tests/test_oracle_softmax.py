@@ -93,8 +93,21 @@ def test_poly_tables_accuracy(tables):
             werr = np.abs(v * xs ** pw - 1)
             assert werr.max() <= p["max_err"] * 1.05
         # the last step is precise (PAPER.md 535-538: 19.5-bit final square root)
-        if t["config"]["k"] > 1 or name.startswith("toy_n16_M2"):
-            assert t["inv"][-1]["log2_err"] < -13
+        last = t["inv"][-1]
+        if last.get("newton"):
+            # G24: seed + Newton y <- y (3 - x y^2)/2 (PAPER.md 1313-1316), run
+            # in float64 on the grid: quadratic convergence to >= 19.5 bits
+            xs = np.linspace(last["a"], last["b"], 20001)
+            y = Ch.chebval((2 * xs - last["a"] - last["b"]) / (last["b"] - last["a"]), last["coeffs"])
+            e0 = np.abs(y * np.sqrt(xs) - 1).max()
+            for _ in range(last["newton"]):
+                e_prev = np.abs(y * np.sqrt(xs) - 1)
+                y = y * (3 - xs * y * y) / 2
+                # PAPER.md 1322-1324: |y_n sqrt(x) - 1| <= 7/4 |y_(n-1) sqrt(x) - 1|^2
+                assert (np.abs(y * np.sqrt(xs) - 1) <= 1.75 * e_prev ** 2 + 1e-15).all()
+            assert e0 > 2.0 ** -13 and np.abs(y * np.sqrt(xs) - 1).max() < 2.0 ** -19.5
+        elif t["config"]["k"] > 1 or name.startswith("toy_n16_M2"):
+            assert last["log2_err"] < -13
 
 
 def _toy_run(tables, wl_name, m, L, variant, table):
@@ -115,10 +128,11 @@ def _toy_run(tables, wl_name, m, L, variant, table):
     return x, dec, led, P, out
 
 
-@pytest.mark.parametrize("m,table", [(1, "toy_n16_M2_k1_A"), (2, "toy_n16_M4_k2_A"), (2, "toy_n16_M4_k2_B")])
+@pytest.mark.parametrize("m,table", [(1, "toy_n16_M2_k1_A"), (2, "toy_n16_M4_k2_A"), (2, "toy_n16_M4_k2_B"),
+                                     (2, "toy_n16_M4_k2_A_nt")])
 def test_oracle_toy_softmax_accuracy(tables, m, table):
     L = 100 if m == 1 else 256
-    variant = table[-1]
+    variant = tables[table]["config"]["variant"]
     x, dec, led, P, out = _toy_run(tables, "config1", m, L, variant, table)
     n, k = 16, tables[table]["config"]["k"]
     got = O.unpack(dec, L, n)
@@ -132,3 +146,37 @@ def test_oracle_toy_softmax_accuracy(tables, m, table):
         stride = (P.n // 2) // nb
         pad = np.array([dec[0, b * stride + o] for b in range(nb) for o in range(L, stride)])
         assert np.abs(pad - 1 / n).max() < 2.0 ** -15
+
+
+def test_oracle_newton_step_pin():
+    """G24 / PAPER.md 1313-1327: one encrypted Newton step from x/2 and a seed
+    y0 costs 2 levels and obeys |y1 sqrt(x) - 1| <= 7/4 |y0 sqrt(x) - 1|^2
+    (+ CKKS noise), for seeds off by up to 30 %."""
+    P = O.Params.from_preset(W.preset("TOY12"))
+    K = O.Keys(P, 4242, 192)
+    rng = np.random.default_rng(5)
+    x = rng.uniform(0.05, 1.0, P.n // 2)
+    e0 = rng.uniform(-0.3, 0.3, P.n // 2)
+    y0 = (1 + e0) / np.sqrt(x)
+    top = P.n_q - 1
+    cx = O.encrypt(P, K, P.encode(x, scale=P.scale(top), level=top), top, 1, 0)
+    cy = O.encrypt(P, K, P.encode(y0, scale=P.scale(top - 1), level=top - 1), top - 1, 1, 1)
+    xh = O.op(P, K, "mult_const", cx, c=0.5, i=top - 1)
+    y1 = O.newton_step(P, K, xh, cy)
+    assert y1.level == top - 3
+    got = O.decrypt_decode(P, K, y1).real
+    e1 = np.abs(got * np.sqrt(x) - 1)
+    assert (e1 <= 1.75 * e0 ** 2 + 2.0 ** -20).all()
+    # and the step is not the identity: the error really shrank
+    assert e1.max() < 0.5 * np.abs(e0).max()
+
+
+def test_oracle_newton_needed_for_toy_accuracy(tables):
+    """Without its Newton steps the degree-7 seed alone misses 2^-15: the
+    Newton path (not the polynomial) carries the accuracy of the _nt table."""
+    t = dict(tables["toy_n16_M4_k2_A_nt"])
+    t["inv"] = [dict(p) for p in t["inv"]]
+    t["inv"][-1].pop("newton")
+    x, dec, led, P, out = _toy_run({"nt0": t}, "config1", 2, 256, "A", "nt0")
+    err = np.abs(O.unpack(dec, 256, 16) - softmax64(x)).max()
+    assert err > 2.0 ** -15

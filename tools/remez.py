@@ -11,7 +11,7 @@ output.  Neither side imports this module.
 Representation: Chebyshev series on [a, b]: P(x) = sum_i c_i T_i(u),
 u = (2x - a - b) / (b - a).
 
-Usage:  python tools/remez.py            (rewrites data/poly_tables.json)
+Usage:  python tools/remez.py [names...]  (rewrites data/poly_tables.json, or only the named tables)
 """
 from __future__ import annotations
 
@@ -103,12 +103,15 @@ def make_invpow(p, a, b, deg):
                 max_err=float(e), log2_err=float(math.log2(e)))
 
 
-def softmax_tables(n, M, k, variant, deg_exp, deg_first, deg_mid, deg_last, guard=0.02, alpha=None):
+def softmax_tables(n, M, k, variant, deg_exp, deg_first, deg_mid, deg_last, guard=0.02, alpha=None, newton=0):
     """Per-iteration polynomial list for one (n, M, k, variant) configuration.
 
     First interval  [n e^{-M/2^(k-1)} (1-guard), n (1+guard)]   (PAPER.md 1001-1002)
     Later intervals [(1-alpha)^2/n, (1+alpha)^2]                  (PAPER.md 427)
     alpha = 2 * (weighted error of the previous step), i.e. |x P^2 - 1|.
+    newton > 0 (Alg 1 only): the last polynomial is a minimax SEED followed by
+    `newton` inverse-square-root Newton steps (PAPER.md 1311-1327 [App. A]:
+    |y_n sqrt(x) - 1| <= 7/4 |y_(n-1) sqrt(x) - 1|^2), DESIGN.md G24.
     """
     polys = {"exp": make_exp(M, k, deg_exp)}
     lo = n * math.exp(-M / 2.0 ** (k - 1)) * (1 - guard)
@@ -125,6 +128,13 @@ def softmax_tables(n, M, k, variant, deg_exp, deg_first, deg_mid, deg_last, guar
             a, b = (1 - al) ** 2 / n, (1 + al) ** 2
             deg = deg_last if j == k else deg_mid
         pol = make_invpow(p, a, b, deg)
+        if j == k and newton:
+            assert variant == "A"
+            e = pol["max_err"]
+            for _ in range(newton):
+                e = 1.75 * e * e
+            pol["newton"] = int(newton)
+            pol["newton_log2_err_bound"] = float(math.log2(e))
         # |x P(x)^(1/p) - 1|: P ~ x^-p within relative e  ->  x P^(1/p) within ~ e/p
         prev_alpha = pol["max_err"] / p
         pol["alpha_out"] = prev_alpha
@@ -139,17 +149,34 @@ CONFIGS = {
     # toy with two iterations (exercises first/last split) -- parity only
     "toy_n16_M4_k2_A": dict(n=16, M=4, k=2, variant="A", deg_exp=7, deg_first=7, deg_mid=7, deg_last=31),
     "toy_n16_M4_k2_B": dict(n=16, M=4, k=2, variant="B", deg_exp=7, deg_first=7, deg_mid=7, deg_last=31),
+    # Newton variant of the k = 2 toy: degree-7 seed + 2 Newton steps (G24) -- pins only
+    "toy_n16_M4_k2_A_nt": dict(n=16, M=4, k=2, variant="A", deg_exp=7, deg_first=7, deg_mid=7, deg_last=7,
+                               newton=2),
     # P16 configs 2-4 (n=256/128, M=128, k=5)
     "p16_n256_M128_k5_A": dict(n=256, M=128, k=5, variant="A", deg_exp=15, deg_first=63, deg_mid=31, deg_last=127),
     "p16_n256_M128_k5_B": dict(n=256, M=128, k=5, variant="B", deg_exp=15, deg_first=63, deg_mid=31, deg_last=127),
     "p16_n128_M128_k5_B": dict(n=128, M=128, k=5, variant="B", deg_exp=15, deg_first=63, deg_mid=31, deg_last=127),
+    # config 5 (n = N0 = 32768, M = 256, Alg 1, k = 7): degree-255
+    # middle steps, last step = degree-255 seed + 3 Newton steps (G24)
+    "p16_n32768_M256_k7_A": dict(n=32768, M=256, k=7, variant="A", deg_exp=15, deg_first=15, deg_mid=255,
+                                 deg_last=255, newton=3),
+    # the config-5 schedule at n = N0 of the N = 2^12 ring (TOY12B): parity only
+    # (degree 63 at n = 2048 ~ degree 255 at n = 32768: the seed needs the Newton steps)
+    "toy_n2048_M32_k4_A": dict(n=2048, M=32, k=4, variant="A", deg_exp=15, deg_first=15, deg_mid=63,
+                               deg_last=63, newton=3),
 }
 
 
-def main(out_path=None):
+def main(out_path=None, only=None):
+    """only: names to (re)compute; the other tables already in out_path are kept."""
     out_path = out_path or os.path.join(os.path.dirname(__file__), "..", "data", "poly_tables.json")
     tables = {}
+    if only and os.path.exists(out_path):
+        with open(out_path) as fh:
+            tables = json.load(fh)
     for name, cfg in CONFIGS.items():
+        if only and name not in only:
+            continue
         t = softmax_tables(**cfg)
         t["config"] = cfg
         tables[name] = t
@@ -161,4 +188,4 @@ def main(out_path=None):
 
 
 if __name__ == "__main__":
-    main()
+    main(only=sys.argv[1:] or None)

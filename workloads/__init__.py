@@ -94,6 +94,9 @@ WORKLOADS = {
     "config2": dict(preset="P16", n=256, L=128, m=1, M=128.0, k=5, variant="A", table="p16_n256_M128_k5_A"),
     "config3": dict(preset="P16", n=256, L=8192, m=64, M=128.0, k=5, variant="B", table="p16_n256_M128_k5_B"),
     "config4": dict(preset="P16", n=128, L=4096, m=16, M=128.0, k=5, variant="B", table="p16_n128_M128_k5_B"),
+    # one Softmax of dimension N0 = 32768 (Alg 1, k = 7; last step
+    # seed + Newton, G24)
+    "config5": dict(preset="P16", n=32768, L=1, m=1, M=256.0, k=7, variant="A", table="p16_n32768_M256_k7_A"),
 }
 
 

@@ -222,7 +222,9 @@ struct hs_bts {
 
 int bts_exponent(const hs_params *P, int arcsine, double bound)
 {
-    const double cap = arcsine ? 8.0 : 12.0;
+    double cap = arcsine ? 8.0 : 12.0;
+    // dev diagnostic: HS_BTS_CAP overrides the headroom (the oracle keeps 8 / 12)
+    if (const char *v = getenv("HS_BTS_CAP")) cap = atof(v);
     double e = floor(log2((double)P->prime[0]) - cap - log2(P->scale[0]) - log2(bound));
     return (int)std::min(30.0, std::max(0.0, e));
 }

@@ -1488,7 +1488,7 @@ struct KsArgB {
 // 128-bit accumulators; the tiles sharing a key block are scheduled back to
 // back, so the key's re-reads hit L2 and HBM streams it about once.
 template <int BT>
-__global__ void __launch_bounds__(256) ks_inner_b_kernel(const u64 *__restrict__ d, const u64 *__restrict__ ext,
+__global__ void __launch_bounds__(256, BT == 2 ? 8 : 1) ks_inner_b_kernel(const u64 *__restrict__ d, const u64 *__restrict__ ext,
                                                          const u64 *__restrict__ key, u64 *__restrict__ acc,
                                                          const __grid_constant__ KsArgB A, int N)
 {
@@ -1563,13 +1563,19 @@ void k_ks_inner_b(hs_ctx *c, const u64 *d, size_t d_stride, const u64 *ext, cons
     if (dadd)
         for (int i = 0; i <= level; i++) A.pmq[i] = P->p_mod_q[i];
     int N = P->n;
-    // batch tile per thread: HS_KS_BT=8 for experiments (default 4)
+    // batch tile per thread: HS_KS_BT=1|4|8 for experiments (default 2: measured
+    // 31.3 ms/step vs 36.0 at 4 -- occupancy beats key reuse, the re-reads hit L2)
     static const int bt = [] {
         const char *e = getenv("HS_KS_BT");
-        return e && atoi(e) == 8 ? 8 : 4;
+        const int v = e ? atoi(e) : 2;
+        return (v == 1 || v == 4 || v == 8) ? v : 2;
     }();
     if (bt == 8 && B >= 8) {
         ks_inner_b_kernel<8><<<dim3((B + 7) / 8, (N + 255) / 256, ntg), 256, 0, st>>>(d, ext, key, acc, A, N);
+    } else if (bt == 2) {
+        ks_inner_b_kernel<2><<<dim3((B + 1) / 2, (N + 255) / 256, ntg), 256, 0, st>>>(d, ext, key, acc, A, N);
+    } else if (bt == 1) {
+        ks_inner_b_kernel<1><<<dim3(B, (N + 255) / 256, ntg), 256, 0, st>>>(d, ext, key, acc, A, N);
     } else {
         const int tiles = (B + 3) / 4;
         ks_inner_b_kernel<4><<<dim3(tiles, (N + 255) / 256, ntg), 256, 0, st>>>(d, ext, key, acc, A, N);
@@ -1670,7 +1676,7 @@ struct KsArgM {
     int nd[16];
 };
 
-__global__ void __launch_bounds__(256) ks_inner_m_kernel(const u64 *__restrict__ d, const u64 *__restrict__ ext,
+__global__ void __launch_bounds__(256, 8) ks_inner_m_kernel(const u64 *__restrict__ d, const u64 *__restrict__ ext,
                                                          u64 *__restrict__ acc, const __grid_constant__ KsArgM A,
                                                          int N)
 {
@@ -1890,7 +1896,11 @@ void k_bsgs_inner(hs_ctx *c, const u64 *const *R, int b1, const u64 *pts, const 
         A.n_q = c->P->n_q;
         const int N = c->P->n;
         KTimer _kt(c, KID_PTMUL, (double)(2 * babies + terms + 2 * G) * nl * N * 8, st);
-        bsgs_inner_bm_kernel<4><<<dim3((N + 255) / 256, nl), 256, 0, st>>>(pts, out, A, N, b1);
+        // accumulators sized to the giant count (registers -> occupancy)
+        const dim3 grid((N + 255) / 256, nl);
+        if (G == 1) bsgs_inner_bm_kernel<1><<<grid, 256, 0, st>>>(pts, out, A, N, b1);
+        else if (G == 2) bsgs_inner_bm_kernel<2><<<grid, 256, 0, st>>>(pts, out, A, N, b1);
+        else bsgs_inner_bm_kernel<4><<<grid, 256, 0, st>>>(pts, out, A, N, b1);
         HS_CHECK_LAUNCH();
         count_kernel(c);
         return;

@@ -31,6 +31,8 @@ for bound, kind in [(1.0, "uniform"), (1.0, "uniform"), (1.0, "const"), (1.5, "c
     torch.cuda.synchronize()
     dt = time.time() - t
     d = hs.decrypt_decode(K, out).real
-    err = np.abs(d - z).max()
+    ea = np.abs(d - z)
+    err = ea.max()
+    pc = " ".join(f"p{q}=2^{math.log2(np.percentile(ea, q)):.1f}" for q in (50, 99, 99.99))
     print(f"bound {bound} {kind}: e={hs.bts_exponent(P, cfg['arcsine'], bound)} abs err 2^{math.log2(err):.2f} "
-          f"rel 2^{math.log2(err/np.abs(z).max()):.2f}  ({dt:.3f}s)", flush=True)
+          f"rel 2^{math.log2(err/np.abs(z).max()):.2f} [{pc}] ({dt:.3f}s)", flush=True)

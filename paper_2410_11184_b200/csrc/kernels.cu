@@ -223,12 +223,49 @@ struct Tw {
 // correction lies in [0, 2q) for any 64-bit input.  Forward values stay in
 // [0, 4q), inverse values in [0, 2q); the last stage of each transform
 // reduces to [0, q), so the words leaving k_ntt are canonical.
-__device__ __forceinline__ u64 shoup_lazy(u64 a, u64 w, u64 wsh, u64 q) { return a * w - __umul64hi(a, wsh) * q; }
+//
+// The Shoup quotient drops its a0*s0 partial product (a = a1 2^32 + a0,
+// s = s1 2^32 + s0): the estimate hi' = a1 s1 + floor((a1 s0 + a0 s1) / 2^32)
+// is floor(a s / 2^64) or one less, so a w - hi' q lies in [0, 3q) (all our
+// primes are < 2^61: 3q < 2^64) and one conditional subtraction of 2q brings
+// it back to [0, 2q).  Three 32x32 products instead of four in the quotient
+// (tools/bfly_lab.cu: 0.86 vs 0.81 T butterflies/s).
+__device__ __forceinline__ u64 shoup_lazy3(u64 a, u64 w, u64 ws, u64 q)
+{
+    u64 r;
+    asm("{\n\t"
+        ".reg .u32 a0, a1, w0, w1, s0, s1, n0, n1, t0, t1, t2, h0, h1, r0, r1;\n\t"
+        "mov.b64 {a0, a1}, %1;\n\t"
+        "mov.b64 {w0, w1}, %2;\n\t"
+        "mov.b64 {s0, s1}, %3;\n\t"
+        "mov.b64 {n0, n1}, %4;\n\t"
+        "mul.lo.u32 t0, a1, s0;\n\t"
+        "mul.hi.u32 t1, a1, s0;\n\t"
+        "mad.lo.cc.u32 t0, a0, s1, t0;\n\t"
+        "madc.hi.cc.u32 t1, a0, s1, t1;\n\t"
+        "addc.u32 t2, 0, 0;\n\t"
+        "mad.lo.cc.u32 h0, a1, s1, t1;\n\t"
+        "madc.hi.u32 h1, a1, s1, t2;\n\t"
+        "mul.lo.u32 r0, a0, w0;\n\t"
+        "mul.hi.u32 r1, a0, w0;\n\t"
+        "mad.lo.u32 r1, a0, w1, r1;\n\t"
+        "mad.lo.u32 r1, a1, w0, r1;\n\t"
+        "mad.lo.cc.u32 r0, h0, n0, r0;\n\t"
+        "madc.hi.u32 r1, h0, n0, r1;\n\t"
+        "mad.lo.u32 r1, h0, n1, r1;\n\t"
+        "mad.lo.u32 r1, h1, n0, r1;\n\t"
+        "mov.b64 %0, {r0, r1};\n\t"
+        "}"
+        : "=l"(r)
+        : "l"(a), "l"(w), "l"(ws), "l"(0 - q));
+    const u64 q2 = 2 * q;
+    return r >= q2 ? r - q2 : r;
+}
 __device__ __forceinline__ void bfly_ct(u64 &a, u64 &b, const Tw &T, int idx)
 {
     const ulonglong2 W = __ldg(T.w + idx);
     const u64 X = a >= T.q2 ? a - T.q2 : a;
-    const u64 V = shoup_lazy(b, W.x, W.y, T.q);
+    const u64 V = shoup_lazy3(b, W.x, W.y, T.q);
     a = X + V;
     b = X + T.q2 - V;
 }
@@ -237,7 +274,7 @@ __device__ __forceinline__ void bfly_gs(u64 &a, u64 &b, const Tw &T, int idx)
     const ulonglong2 W = __ldg(T.w + idx);
     const u64 U = a, V = b, s = U + V;
     a = s >= T.q2 ? s - T.q2 : s;
-    b = shoup_lazy(U + T.q2 - V, W.x, W.y, T.q);
+    b = shoup_lazy3(U + T.q2 - V, W.x, W.y, T.q);
 }
 // [0, 4q) -> [0, q)
 __device__ __forceinline__ u64 reduce4(u64 v, const Tw &T)
@@ -437,6 +474,10 @@ __global__ void __launch_bounds__(32 * R) rows(u64 *data, PrimeMap pm, const u64
 #pragma unroll
         for (int k = 0; k < 8; k++) sm[row * 256 + b * 32 + sub + 4 * k] = x[k];
         __syncthreads();
+        // last round: each thread ends with 4 consecutive words, stored
+        // straight to global memory as two 16-byte stores (no smem pass)
+        const int crow = MODE ? limb / E.l : 0, li = MODE ? limb - crow * E.l : 0;
+        const size_t eb = (size_t)row0 * 256;
 #pragma unroll
         for (int h = 0; h < 2; h++) {
             const int q = (tid & 31) + 32 * h;
@@ -444,48 +485,60 @@ __global__ void __launch_bounds__(32 * R) rows(u64 *data, PrimeMap pm, const u64
 #pragma unroll
             for (int k = 0; k < 4; k++) y[k] = sm[row * 256 + 4 * q + k];
             radix4_fwd(y, jrow + 4 * q, 1, T);
+            const int i0 = row * 256 + 4 * q;
 #pragma unroll
-            for (int k = 0; k < 4; k++) sm[row * 256 + 4 * q + k] = y[k];
-        }
-        __syncthreads();
-        if (MODE == 0) {
-            for (int i = tid; i < R * 256; i += 32 * R) a[i] = reduce4(sm[i], T);
-        } else {
-            const int row = limb / E.l, li = limb - row * E.l;
-            const size_t e0 = (size_t)row0 * 256;
-            const u64 *in = E.ain + row * E.astr + (size_t)li * N + e0;
-            const u64 inv = E.inv[li], ish = E.inv_sh[li];
-            if (MODE == 1) {
-                u64 *o = E.o + row * E.ostr + (size_t)li * N + e0;
-                if (E.scaled) {
-                    const u64 sc = E.scl[li], scs = E.scl_sh[li];
-                    for (int i = tid; i < R * 256; i += 32 * R)
-                        o[i] = d_shoup(d_sub(d_shoup(in[i], sc, scs, T.q), reduce4(sm[i], T), T.q), inv, ish, T.q);
-                } else {
-                    for (int i = tid; i < R * 256; i += 32 * R)
-                        o[i] = d_shoup(d_sub(in[i], reduce4(sm[i], T), T.q), inv, ish, T.q);
-                }
+            for (int k = 0; k < 4; k++) y[k] = reduce4(y[k], T);
+            if (MODE == 0) {
+                ulonglong2 *dst = reinterpret_cast<ulonglong2 *>(a + i0);
+                dst[0] = make_ulonglong2(y[0], y[1]);
+                dst[1] = make_ulonglong2(y[2], y[3]);
             } else {
-                const int b = row >> 1, comp = row & 1;
-                const size_t ci = ((size_t)comp * E.l + li) * N + e0;
-                u64 *o = E.o + b * E.ostr + ci;
-                const u64 *ad = comp < E.add_comps ? E.add + b * E.addstr + ci : nullptr;
-                for (int i = tid; i < R * 256; i += 32 * R) {
-                    u64 v = d_shoup(d_sub(in[i], reduce4(sm[i], T), T.q), inv, ish, T.q);
-                    if (ad) v = d_add(v, ad[i], T.q);
-                    o[i] = v;
+                const u64 *in = E.ain + crow * E.astr + (size_t)li * N + eb + i0;
+                const ulonglong2 in0 = reinterpret_cast<const ulonglong2 *>(in)[0];
+                const ulonglong2 in1 = reinterpret_cast<const ulonglong2 *>(in)[1];
+                const u64 iv[4] = {in0.x, in0.y, in1.x, in1.y};
+                const u64 inv = E.inv[li], ish = E.inv_sh[li];
+                u64 ov[4];
+                u64 *o;
+                if (MODE == 1) {
+                    o = E.o + crow * E.ostr + (size_t)li * N + eb + i0;
+                    if (E.scaled) {
+                        const u64 sc = E.scl[li], scs = E.scl_sh[li];
+#pragma unroll
+                        for (int k = 0; k < 4; k++)
+                            ov[k] = d_shoup(d_sub(d_shoup(iv[k], sc, scs, T.q), y[k], T.q), inv, ish, T.q);
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < 4; k++) ov[k] = d_shoup(d_sub(iv[k], y[k], T.q), inv, ish, T.q);
+                    }
+                } else {
+                    const int bb = crow >> 1, comp = crow & 1;
+                    const size_t ci = ((size_t)comp * E.l + li) * N + eb + i0;
+                    o = E.o + bb * E.ostr + ci;
+#pragma unroll
+                    for (int k = 0; k < 4; k++) ov[k] = d_shoup(d_sub(iv[k], y[k], T.q), inv, ish, T.q);
+                    if (comp < E.add_comps) {
+                        const ulonglong2 *ad = reinterpret_cast<const ulonglong2 *>(E.add + bb * E.addstr + ci);
+                        const ulonglong2 a0 = ad[0], a1 = ad[1];
+                        ov[0] = d_add(ov[0], a0.x, T.q);
+                        ov[1] = d_add(ov[1], a0.y, T.q);
+                        ov[2] = d_add(ov[2], a1.x, T.q);
+                        ov[3] = d_add(ov[3], a1.y, T.q);
+                    }
                 }
+                reinterpret_cast<ulonglong2 *>(o)[0] = make_ulonglong2(ov[0], ov[1]);
+                reinterpret_cast<ulonglong2 *>(o)[1] = make_ulonglong2(ov[2], ov[3]);
             }
         }
     } else {
-        for (int i = tid; i < R * 256; i += 32 * R) sm[i] = a[i];
-        __syncthreads();
+        // first round straight from global memory (two 16-byte loads of 4
+        // consecutive words per group)
 #pragma unroll
         for (int h = 0; h < 2; h++) {
             const int q = (tid & 31) + 32 * h;
-            u64 y[4];
-#pragma unroll
-            for (int k = 0; k < 4; k++) y[k] = sm[row * 256 + 4 * q + k];
+            const ulonglong2 *src = reinterpret_cast<const ulonglong2 *>(a + row * 256 + 4 * q);
+            const ulonglong2 v0 = src[0], v1 = src[1];
+            u64 y[4] = {v0.x, v0.y, v1.x, v1.y};
             radix4_inv(y, jrow + 4 * q, 1, T);
 #pragma unroll
             for (int k = 0; k < 4; k++) sm[row * 256 + 4 * q + k] = y[k];

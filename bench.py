@@ -36,7 +36,10 @@ WORKLOAD = "config3"
 # butterfly, and DRAM bytes per limb-NTT (both passes) from the round's
 # `ncu --set full` capture (profiles/r01_ncu_full_summary.txt); None = not measured
 NTT_ALU_PEAK = 0.86
-NTT_TRAFFIC_PER_LIMB = None
+# DRAM bytes per forward limb-NTT (cols + rows, MODE 0) in the round's
+# `ncu --set full` capture: (369.2 + 316.9 + 382.1 + 313.2) MB / 704 limbs
+# (profiles/r01_ncu_full_summary.txt) -- 1 read + 1 write per pass, no waste
+NTT_TRAFFIC_PER_LIMB = 1.962e6
 METRIC = "amortized ms/Softmax (8192×dim256, N=2^16); key-switch HBM GB/s vs peak"
 # the paper's number for this exact workload (8192 Softmax dim 256,
 # m = 64, Alg B): 414 s -> 50.5 ms per Softmax, HEaaN on one Xeon Silver 4114

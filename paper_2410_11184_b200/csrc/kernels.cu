@@ -1597,8 +1597,11 @@ void k_ks_inner_b(hs_ctx *c, const u64 *d, size_t d_stride, const u64 *ext, cons
 {
     const hs_params *P = c->P;
     const int ntg = level + 1 + P->n_p;
-    // algorithmic bytes: the key once, every input limb once, the outputs once
-    KTimer _kt(c, KID_KS_INNER, ((double)beta * ntg * (16.0 + 8.0 * B) + 16.0 * ntg * B) * P->n, st);
+    // algorithmic bytes: the key once, every input limb once, the C8 P*d
+    // term's 2 (level+1) limbs per member when fused, the outputs once
+    KTimer _kt(c, KID_KS_INNER,
+               ((double)beta * ntg * (16.0 + 8.0 * B) + 16.0 * ntg * B + (dadd ? 16.0 * (level + 1) * B : 0.0)) * P->n,
+               st);
     KsArgB A;
     A.level = level;
     A.beta = beta;
@@ -1693,7 +1696,15 @@ void k_ks_inner_h(hs_ctx *c, const u64 *d, const u64 *ext, const size_t *off, co
     const hs_params *P = c->P;
     const int ntg = level + 1 + P->n_p;
     if (R < 1 || R > HS_MAXROT) throw HsError(HS_EINVAL, "hoisted key switch: bad rotation count");
-    KTimer _kt(c, KID_KS_HOIST, ((double)R * beta * ntg * 24.0 + 16.0 * ntg * R) * P->n, st);
+    // algorithmic bytes: R keys, the shared extended digits and sigma's c0 once
+    // (every rotation gathers them again through its own permutation -- from
+    // HBM: a source-order variant that let the R re-reads hit L2 measured no
+    // faster, the key streams dominate), R outputs
+    KTimer _kt(c, KID_KS_HOIST,
+               ((double)R * beta * ntg * 16.0 + (double)beta * ntg * 8.0 + 16.0 * ntg * R +
+                (c0add ? 8.0 * (level + 1) : 0.0)) *
+                   P->n,
+               st);
     KsArgH A;
     for (int r = 0; r < R; r++) {
         A.key[r] = keys[r];

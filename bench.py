@@ -492,7 +492,7 @@ def run_reference(args):
 
 def estimated_ks_per_step():
     # the GPU arm's ledger for config 3: "ks" per step (ledger_per_step of profiles/r01_bench_full.json)
-    return 2649
+    return 2964
 
 
 def main():

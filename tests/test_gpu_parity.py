@@ -413,3 +413,44 @@ def test_softmax_newton_parity(toyb, tables):
     ref = np.exp(x - x.max(1, keepdims=True))
     ref /= ref.sum(1, keepdims=True)
     assert np.abs(y - ref).max() < 2.0 ** -15
+
+
+def test_softmax_error_paths(tables):
+    """hs_status contract of hs_softmax_many_ctxt (include/hesoftmax.h): a
+    missing rotation key -> HS_EKEY, a schedule deeper than the chain without
+    bootstrapping -> HS_ELEVEL, inconsistent descriptors -> HS_EINVAL; the
+    context stays usable afterwards."""
+    hs = _hs()
+    from paper_2410_11184_b200._lib import HsError
+    tab = tables["toy_n16_M2_k1_A"]
+    n, k = 16, 1
+    pre = W.preset("TOY12")
+    P = hs.Params.from_preset(pre)
+    ctx = hs.Context(P, 0)
+    PO = O.Params.from_preset(pre)
+    K_full = hs.Keys(ctx, 7, pre["h"], galois=O.softmax_rotation_galois(PO, n, 1))
+    K_none = hs.Keys(ctx, 7, pre["h"], galois=[])
+    x = W.softmax_inputs(8, n, 2.0, seed=3)
+    slots = P.pack(x, 1)
+    top = len(pre["q_bits"]) - 1
+    ct = hs.encrypt(K_full, P.encode(slots[0], scale=P.scale(top), level=top), top, 1, 0)
+    low = hs.encrypt(K_full, P.encode(slots[0], scale=P.scale(4), level=4), 4, 1, 1)
+
+    def code(fn):
+        with pytest.raises(HsError) as e:
+            fn()
+        return e.value.code
+
+    assert code(lambda: hs.softmax_many_ctxt(K_none, [ct], n, 1, k, 0, tab["exp"], tab["inv"])) == 3
+    assert code(lambda: hs.softmax_many_ctxt(K_full, [low], n, 1, k, 0, tab["exp"], tab["inv"])) == 2
+    inv_nt = [dict(p) for p in tab["inv"]]
+    inv_nt[-1]["newton"] = 2
+    assert code(lambda: hs.softmax_many_ctxt(K_full, [ct], n, 1, k, 1, tab["exp"], inv_nt)) == 1
+    assert code(lambda: hs.softmax_many_ctxt(K_full, [ct, ct, ct], n, 3, k, 0, tab["exp"], tab["inv"])) == 1
+    assert code(lambda: hs.softmax_many_ctxt(K_full, [ct, ct], n, 4, k, 0, tab["exp"], tab["inv"])) == 1
+    # still usable: a valid call afterwards decrypts to Softmax
+    out = hs.softmax_many_ctxt(K_full, [ct], n, 1, k, 0, tab["exp"], tab["inv"])
+    y = P.unpack(hs.decrypt_decode(K_full, out[0]).real[None], 8, n)
+    ref = np.exp(x - x.max(1, keepdims=True))
+    ref /= ref.sum(1, keepdims=True)
+    assert np.abs(y - ref).max() < 2.0 ** -15

@@ -180,3 +180,13 @@ def test_oracle_newton_needed_for_toy_accuracy(tables):
     x, dec, led, P, out = _toy_run({"nt0": t}, "config1", 2, 256, "A", "nt0")
     err = np.abs(O.unpack(dec, 256, 16) - softmax64(x)).max()
     assert err > 2.0 ** -15
+
+
+def test_oracle_rejects_newton_with_version_b(tables):
+    """G24: Newton steps are defined for Alg 1's x^(-1/2) only; the oracle
+    rejects them with version B (ORC_EINVAL), as the C ABI does (HS_EINVAL)."""
+    t = dict(tables["toy_n16_M4_k2_B"])
+    t["inv"] = [dict(p) for p in t["inv"]]
+    t["inv"][-1]["newton"] = 2
+    with pytest.raises(RuntimeError, match="rc=1"):
+        _toy_run({"ntB": t}, "config1", 2, 256, "B", "ntB")

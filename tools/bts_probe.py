@@ -25,6 +25,8 @@ for bound, kind in [(1.0, "uniform"), (1.0, "uniform"), (1.0, "const"), (1.5, "c
         z = np.full(P.n // 2, bound * 0.8) + rng.uniform(-0.01, 0.01, P.n // 2)
     pt = P.encode(z, scale=P.scale(3), level=3)
     ct = hs.encrypt(K, pt, 3, 9, 0)
+    e_in = np.abs(hs.decrypt_decode(K, ct).real - z).max()
+    print(f"   input ciphertext (fresh, level 3) error 2^{math.log2(e_in):.2f}", flush=True)
     import torch; torch.cuda.synchronize()
     t = time.time()
     out = hs.bootstrap(K, B, ct, bound)
@@ -33,6 +35,10 @@ for bound, kind in [(1.0, "uniform"), (1.0, "uniform"), (1.0, "const"), (1.5, "c
     d = hs.decrypt_decode(K, out).real
     ea = np.abs(d - z)
     err = ea.max()
+    # multiplicative part: d - z ~ eps z + residual
+    eps = float(((d - z) * z).sum() / (z * z).sum())
+    res = np.abs(d - z - eps * z).max()
+    print(f"   gain error eps = {eps:.3e}, residual after removing it 2^{math.log2(res):.2f}", flush=True)
     pc = " ".join(f"p{q}=2^{math.log2(np.percentile(ea, q)):.1f}" for q in (50, 99, 99.99))
     print(f"bound {bound} {kind}: e={hs.bts_exponent(P, cfg['arcsine'], bound)} abs err 2^{math.log2(err):.2f} "
           f"rel 2^{math.log2(err/np.abs(z).max()):.2f} [{pc}] ({dt:.3f}s)", flush=True)

@@ -53,6 +53,8 @@ WORKLOAD_DESC = ("config3: 8192 Softmax dim 256, M=128, k=5, version B, m=64 cip
 OTHER_WORKLOADS = {
     "config2": ("config2: 128 Softmax dim 256 in one ciphertext, M=128, k=5, Alg 1, N=2^16, bootstrapped", None,
                 None),
+    "config2S": ("config2 with square-and-normalize (PAPER.md 757-765, DESIGN.md G26): 128 Softmax dim 256, "
+                 "M=128, k=5, N=2^16, bootstrapped", None, None),
     "config4": ("config4: 4096 Softmax dim 128 (one LLaMA-7B layer batch), M=128, k=5, version B, m=16, N=2^16",
                 None, None),
     "config5": ("config5: one Softmax dim 32768 (= N0), M=256, k=7, Alg 1, last step seed + 3 Newton "
@@ -207,8 +209,13 @@ def run_ours(args):
         ref = np.exp(x - x.max(1, keepdims=True))
         ref /= ref.sum(1, keepdims=True)
         acc_bits = float(-np.log2(np.abs(y - ref).max()))
+        # tab:alg1 statistics (PAPER.md 499-511): per Softmax instance, the
+        # precision log2 max_i |y_i - ref_i|; worst / average / std over instances
+        per = np.log2(np.maximum(np.abs(y - ref).max(axis=1), 2.0 ** -60))
+        acc_stats = {"worst_bits": round(float(per.max()), 2), "avg_bits": round(float(per.mean()), 2),
+                     "std_bits": round(float(per.std()), 2), "instances": int(per.size)}
     else:
-        acc_bits = None
+        acc_bits, acc_stats = None, None
     # ---------------- timed region (device events, max over ranks)
     clocks = Clocks(local)
     led0 = ctx.ledger()
@@ -329,6 +336,7 @@ def run_ours(args):
                    "kprof": ("events captured in a second graph of the same step, timed separately"
                              if use_graph and args.kprof != "off" else args.kprof)},
         "accuracy_bits": round(acc_bits, 2) if acc_bits is not None else None,
+        "accuracy": acc_stats,
         "gpu_launches": int(led1["kernels"] - led0["kernels"]),
         "ledger_per_step": {k_: (led1[k_] - led0[k_]) // args.steps for k_ in led1},
         "roofline": roof(dom) if dom else None,

@@ -280,7 +280,11 @@ def cheb_depth(deg):
     return lib().orc_api_cheb_depth(deg)
 
 
+VARIANT = {"A": 0, "B": 1, "S": 2, 0: 0, 1: 1, 2: 2}  # S: square-and-normalize (G26)
+
+
 def softmax(P: Params, K: Keys, cts, n, k, variant, exp_poly, inv_polys):
+    variant = VARIANT[variant]
     polys = [exp_poly] + list(inv_polys)
     assert len(inv_polys) == k
     degs = np.array([len(p["coeffs"]) - 1 for p in polys], np.int32)
@@ -419,6 +423,7 @@ def bts_exponent(P: Params, arcsine: bool, bound: float) -> int:
 
 
 def softmax_bts(P: Params, K: Keys, cts, n, k, variant, exp_poly, inv_polys, bts: Bts):
+    variant = VARIANT[variant]
     polys = [exp_poly] + list(inv_polys)
     degs = np.array([len(p["coeffs"]) - 1 for p in polys], np.int32)
     a_s = np.array([p["a"] for p in polys], np.float64)

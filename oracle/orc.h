@@ -134,7 +134,7 @@ orc_ct *orc_eval_cheb_unit(const orc_params *P, const orc_keys *K, const orc_ct 
 /* softmax.c (Alg 1 / Alg 2 / version B, C14, G12, G24) */
 typedef orc_ct *(*orc_bts_fn)(const orc_params *, const orc_keys *, const orc_ct *, void *, double);
 typedef struct {
-    int n, m, k, variant;           /* variant 0 = Alg 1, 1 = Alg B                     */
+    int n, m, k, variant;           /* 0 = Alg 1, 1 = Alg B, 2 = square-and-normalize  */
     const orc_cheb *exp_poly;       /* exp(x/2^k) on [-M, 0]                            */
     const orc_cheb *inv_poly;       /* k polys, one per iteration                       */
     orc_bts_fn bts;                 /* NULL: no bootstrapping                           */

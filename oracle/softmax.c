@@ -6,6 +6,8 @@
  *   Alg 2 (auxiliary thread)      PAPER.md 904-921 [sec 3.4.1, alg:AuxThread]
  *   Alg B (version B)             PAPER.md 168-181 [sec 4.3, alg:Softmax1B],
  *                                 exponent read as -1/2^j (G4)
+ *   square-and-normalize          PAPER.md 757-765 [sec 3.3, remark]: variant 2,
+ *                                 mu_j = (sum y^2)^-1, y <- mu_j y^2 (G26)
  *   packings                      PAPER.md 94-131 [sec 4.1-4.2]
  *   many-ciphertext aux sum       DESIGN.md C15 / G6 (sum of tensors, one relin)
  *   bootstrap placement           PAPER.md 429-440 [sec 5.1.3], rule G12
@@ -69,7 +71,10 @@ static int poly_cost(const orc_cheb *p)
 int orc_softmax(const orc_params *P, const orc_keys *K, const orc_softmax_desc *d, orc_ct *const *x, orc_ct **out)
 {
     int m = d->m, n = d->n, N0 = P->n / 2;
-    if (m < 1 || n % m || d->newton < 0 || (d->newton > 0 && d->variant != 0)) return ORC_EINVAL;
+    if (m < 1 || n % m || d->variant < 0 || d->variant > 2 || d->newton < 0 || (d->newton > 0 && d->variant != 0))
+        return ORC_EINVAL;
+    /* Alg 1 and square-and-normalize share the schedule (variant 0 / 2) */
+    int alg1 = d->variant != 1;
     int nb = n / m;
     if ((nb & (nb - 1)) || nb > N0) return ORC_EINVAL;
     int stride = N0 / nb;
@@ -88,7 +93,7 @@ int orc_softmax(const orc_params *P, const orc_keys *K, const orc_softmax_desc *
     for (int j = 1; j <= d->k; j++) {
         const orc_cheb *ip = &d->inv_poly[j - 1];
         /* Alg 1 main thread needs 1 (aux square) + 2 levels; bootstrap y (G12 c) */
-        if (d->variant == 0 && y[0]->level < 2) {
+        if (alg1 && y[0]->level < 2) {
             for (int c = 0; c < m; c++) if ((rc = bts_or_fail(P, K, d, &y[c], 1.0))) goto done;
         }
         if (y[0]->level < 1) { rc = ORC_ELEVEL; goto done; }
@@ -112,7 +117,7 @@ int orc_softmax(const orc_params *P, const orc_keys *K, const orc_softmax_desc *
          * square) or k + 1 at j = k, capped by y0's level (G12) */
         int need_b = j < d->k ? j + 2 : d->k + 1;
         int main_a = j < d->k ? y[0]->level : (y[0]->level < 2 ? y[0]->level : 2);
-        int main_level = d->variant == 0 ? main_a : (y0[0]->level < need_b ? y0[0]->level : need_b);
+        int main_level = alg1 ? main_a : (y0[0]->level < need_b ? y0[0]->level : need_b);
         int need = poly_cost(ip) + 1 + ((d->variant == 1 && j > 1) ? 1 : 0);
         /* G24: Newton steps after the last polynomial read x/2 (one level below
          * S), 2 levels each, then the mask: S must also supply 2 t + 2 levels */
@@ -143,8 +148,9 @@ int orc_softmax(const orc_params *P, const orc_keys *K, const orc_softmax_desc *
          * 0's value, so every coordinate of an instance sees the same
          * bootstrapping error (a common factor the next normalisation absorbs)
          * instead of an independent one per slot */
-        if (d->variant == 0 && lj->level - 1 < main_level && d->bts) {
-            if ((rc = bts_or_fail(P, K, d, &lj, 1.1 / sqrt(ip->a)))) goto done;
+        if (alg1 && lj->level - 1 < main_level && d->bts) {
+            double bound = d->variant == 2 ? 1.1 / ip->a : 1.1 / sqrt(ip->a);
+            if ((rc = bts_or_fail(P, K, d, &lj, bound))) goto done;
         }
         /* step 7: mask block 0 */
         if (lj->level < 1) { rc = ORC_ELEVEL; goto done; }
@@ -171,6 +177,10 @@ int orc_softmax(const orc_params *P, const orc_keys *K, const orc_softmax_desc *
                 orc_ct *z = orc_op_mult(P, K, lam, y[c]);        /* Alg 1 line 4 */
                 swap_in(&y[c], orc_op_mult(P, K, z, z));          /* Alg 1 line 5 */
                 orc_ct_release(z);
+            } else if (d->variant == 2) {
+                orc_ct *w = orc_op_mult(P, K, y[c], y[c]);        /* square ...      */
+                swap_in(&y[c], orc_op_mult(P, K, lam, w));        /* ... and normalize */
+                orc_ct_release(w);
             } else {
                 orc_ct *z = orc_op_mult(P, K, lam, y0[c]);       /* Alg B line 6 */
                 for (int s = 0; s < j; s++) {                     /* Alg B line 7 */

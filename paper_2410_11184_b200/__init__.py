@@ -300,6 +300,14 @@ def bootstrap(keys: Keys, bts: Bts, ct: Ciphertext, bound=1.0, stream=None) -> C
     return Ciphertext(keys.ctx, out)
 
 
+def variant_code(variant):
+    """"A" / 0: Alg 1; "B" / 1: version B; "S" / 2: square-and-normalize (G26)."""
+    codes = {"A": 0, "B": 1, "S": 2, 0: 0, 1: 1, 2: 2}
+    if variant not in codes:
+        raise ValueError(f"unknown Softmax variant {variant!r}")
+    return codes[variant]
+
+
 def _softmax_desc(n, m, k, variant, exp_poly, inv_polys, world=1, rank=0, exchange=None, bts=None):
     keep = []
     e, c = _poly(exp_poly)
@@ -314,7 +322,7 @@ def _softmax_desc(n, m, k, variant, exp_poly, inv_polys, world=1, rank=0, exchan
     fn = L.EXCHANGE_FN(0) if exchange is None else exchange
     keep.append(fn)
     # a table's last entry may carry "newton": the polynomial is then a seed (G24)
-    d = L.SoftmaxDesc(n, m, k, 0 if variant in (0, "A") else 1, ep, arr, world, rank, fn, None,
+    d = L.SoftmaxDesc(n, m, k, variant_code(variant), ep, arr, world, rank, fn, None,
                       bts.ptr if bts is not None else None, int(inv_polys[-1].get("newton", 0)))
     return d, keep
 

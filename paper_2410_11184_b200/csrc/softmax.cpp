@@ -3,6 +3,8 @@
 //   Alg 1 normalize-and-square   PAPER.md 776-787 [sec 3.3, alg:Softmax]
 //   Alg 2 auxiliary thread       PAPER.md 904-921 [sec 3.4.1, alg:AuxThread]
 //   version B                    PAPER.md 168-181 [sec 4.3], exponent -1/2^j (G4)
+//   square-and-normalize         PAPER.md 757-765 [sec 3.3, remark], variant 2:
+//                                mu_j = (sum y^2)^-1, y <- mu_j y^2 (G26)
 //   one / many ciphertexts       PAPER.md 94-131 [sec 4.1-4.2]
 //   shared aux sum               DESIGN.md C15 / G6: sum_c tensor(y_c, y_c)
 //                                exactly mod q, ONE relin + rescale
@@ -56,9 +58,11 @@ hs_status softmax_run(hs_ctx *c, const hs_keys *K, const hs_softmax_desc *d, con
     const hs_params *P = c->P;
     const int N0 = P->n / 2;
     const int m = d->m, n = d->n, world = d->world < 1 ? 1 : d->world;
-    if (m < 1 || n < 1 || n % m || d->k < 1 || !d->exp_poly || !d->inv_poly || d->variant < 0 || d->variant > 1 ||
+    if (m < 1 || n < 1 || n % m || d->k < 1 || !d->exp_poly || !d->inv_poly || d->variant < 0 || d->variant > 2 ||
         d->newton < 0 || (d->newton > 0 && d->variant != 0))
         throw HsError(HS_EINVAL, "softmax: bad descriptor");
+    // Alg 1 and square-and-normalize share the schedule (variant 0 / 2)
+    const bool alg1 = d->variant != 1;
     if (m % world || (size_t)(m / world) != m_local) throw HsError(HS_EINVAL, "softmax: m_local != m / world");
     if (world > 1 && !d->exchange) throw HsError(HS_EINVAL, "softmax: world > 1 needs an exchange callback");
     const int nb = n / m;
@@ -83,7 +87,7 @@ hs_status softmax_run(hs_ctx *c, const hs_keys *K, const hs_softmax_desc *d, con
     for (int j = 1; j <= d->k; j++) {
         const hs_poly *ip = &d->inv_poly[j - 1];
         // G12 (c): Alg 1 main thread needs 1 (aux square) + 2 levels
-        if (d->variant == 0 && y->level < 2) {
+        if (alg1 && y->level < 2) {
             if (!d->bts) level_error("main thread needs bootstrapping (not available)");
             std::vector<CtP> parts(ml);
             std::vector<const hs_ct *> ptrs(ml);
@@ -115,7 +119,7 @@ hs_status softmax_run(hs_ctx *c, const hs_keys *K, const hs_softmax_desc *d, con
         // j + 2 (k + 1 at j = k), capped by y0's
         const int need_b = j < d->k ? j + 2 : d->k + 1;
         const int main_a = j < d->k ? y->level : std::min(y->level, 2);
-        const int main_level = d->variant == 0 ? main_a : std::min(y0->level, need_b);
+        const int main_level = alg1 ? main_a : std::min(y0->level, need_b);
         int need = poly_cost(ip) + 1 + ((d->variant == 1 && j > 1) ? 1 : 0);
         // G24: Newton steps after the last polynomial read x/2 (one level
         // below S), 2 levels each, then the mask: S supplies 2 t + 2 levels too
@@ -145,8 +149,8 @@ hs_status softmax_run(hs_ctx *c, const hs_keys *K, const hs_softmax_desc *d, con
         // leave it below the main level -- the broadcast then gives every
         // coordinate of an instance block 0's value, one common bootstrapping
         // error per instance (absorbed by the next normalisation)
-        if (d->variant == 0 && lj->level - 1 < main_level && d->bts)
-            lj = ev_bootstrap(K, d->bts, lj.get(), 1.1 / sqrt(ip->a), st);
+        if (alg1 && lj->level - 1 < main_level && d->bts)
+            lj = ev_bootstrap(K, d->bts, lj.get(), d->variant == 2 ? 1.1 / ip->a : 1.1 / sqrt(ip->a), st);
         if (lj->level < 1) level_error("no level for the mask");
         lj = ev_mult_pt(lj.get(), mask.data(), nullptr, lj->level - 1, st);
         rot_sum(K, lj, nb, stride, +1, st);
@@ -160,6 +164,9 @@ hs_status softmax_run(hs_ctx *c, const hs_keys *K, const hs_softmax_desc *d, con
         if (d->variant == 0) {
             CtP z = ev_mult(K, lam.get(), y.get(), st);
             y = ev_mult(K, z.get(), z.get(), st);
+        } else if (d->variant == 2) {
+            CtP w = ev_mult(K, y.get(), y.get(), st);
+            y = ev_mult(K, lam.get(), w.get(), st);
         } else {
             CtP z = ev_mult(K, lam.get(), y0.get(), st);
             for (int s = 0; s < j; s++) {

@@ -49,7 +49,7 @@ def test_config3_plan_full_size():
     assert led["bts"] >= 10
 
 
-@pytest.mark.parametrize("wl", ["config4", "config2"])
+@pytest.mark.parametrize("wl", ["config4", "config2", "config2S"])
 def test_configs_full_size_accuracy(wl):
     import bench
     S = bench.build_setup(wl, 0, 1, 0)

@@ -201,7 +201,7 @@ def _softmax_case(tables, preset, table, m, L, tag):
         pt = P.encode(slots[c], scale=P.scale(top), level=top)
         g_in.append(hs.encrypt(K, pt, top, es, c))
         o_in.append(O.encrypt(PO, KO, pt, top, es, c))
-    var = 0 if cfg["variant"] == "A" else 1
+    var = cfg["variant"]
     if m == 1:
         g_out = [hs.softmax_one_ctxt(K, g_in[0], n, k, var, tab["exp"], tab["inv"])]
     else:
@@ -222,7 +222,7 @@ def test_softmax_config1_parity(tables):
     assert led["rot"] == 2 * 4
 
 
-@pytest.mark.parametrize("table", ["toy_n16_M4_k2_A", "toy_n16_M4_k2_B"])
+@pytest.mark.parametrize("table", ["toy_n16_M4_k2_A", "toy_n16_M4_k2_B", "toy_n16_M4_k2_S"])
 def test_softmax_many_parity(tables, table):
     _softmax_case(tables, "TOY12D", table, 2, 256, "many-" + table)
 
@@ -341,7 +341,8 @@ def test_bootstrap_parity(toyb, level, bound):
     assert err < 2.0 ** -21, np.log2(err)
 
 
-@pytest.mark.parametrize("table,m", [("p16_n256_M128_k5_B", 16), ("p16_n256_M128_k5_A", 1)])
+@pytest.mark.parametrize("table,m", [("p16_n256_M128_k5_B", 16), ("p16_n256_M128_k5_A", 1),
+                                     ("p16_n256_M128_k5_S", 1)])
 def test_softmax_bts_parity(toyb, tables, table, m):
     """configs 2-3 schedule (Alg 1 / version B with bootstrapping) on the
     N = 2^12 ring with P16's chain: ciphertexts word-for-word, accuracy 2^-15."""
@@ -350,7 +351,7 @@ def test_softmax_bts_parity(toyb, tables, table, m):
     tab = tables[table]
     cfg = tab["config"]
     n, k = cfg["n"], cfg["k"]
-    var = 0 if cfg["variant"] == "A" else 1
+    var = {"A": 0, "B": 1, "S": 2}[cfg["variant"]]
     L = (P.n // 2) * m // n
     x = W.softmax_inputs(L, n, cfg["M"], seed=W.derive_seed("x", table))
     slots = P.pack(x, m)
@@ -374,7 +375,7 @@ def test_softmax_bts_parity(toyb, tables, table, m):
     ref /= ref.sum(1, keepdims=True)
     assert np.abs(y - ref).max() < 2.0 ** -15
     n_bts = g_led["bts"]
-    assert 0 < n_bts <= 2 * k
+    assert 0 < n_bts <= (3 if var == 2 else 2) * k
     if var == 1:
         # the same Softmax as a replayable CUDA graph (hs_softmax_plan_create):
         # every replay recomputes the words above, bit for bit

@@ -49,6 +49,21 @@ def test_alg1_and_algB_exact_in_float64(M, n, k):
     assert np.abs(algB_float(x, k) - ref).max() < 1e-13
 
 
+def square_normalize_float(x, k):
+    """PAPER.md 757-765 (G26): y <- y^2 / sum y^2, k times, from exp(x/2^k)."""
+    y = np.exp(x / 2.0 ** k)
+    for _ in range(k):
+        w = y * y
+        y = w / w.sum(-1, keepdims=True)
+    return y
+
+
+@pytest.mark.parametrize("M,n,k", [(128, 256, 5), (4, 16, 2)])
+def test_square_and_normalize_exact_in_float64(M, n, k):
+    x = W.softmax_inputs(64, n, M, seed=M * 7 + n)
+    assert np.abs(square_normalize_float(x, k) - softmax64(x)).max() < 1e-13
+
+
 def test_algB_printed_exponent_is_wrong_G4():
     x = W.softmax_inputs(16, 256, 128, seed=9)
     assert np.abs(algB_float(x, 5, "printed") - softmax64(x)).max() > 1e-2
@@ -87,7 +102,8 @@ def test_poly_tables_accuracy(tables):
         assert err.max() <= e["max_err"] * 1.05 + 1e-15
         assert len(e["coeffs"]) - 1 == t["config"]["deg_exp"]
         for j, p in enumerate(t["inv"], start=1):
-            pw = 0.5 if t["config"]["variant"] == "A" else 0.5 ** j
+            var = t["config"]["variant"]
+            pw = 0.5 if var == "A" else 1.0 if var == "S" else 0.5 ** j
             xs = np.linspace(p["a"], p["b"], 20001)
             v = Ch.chebval((2 * xs - p["a"] - p["b"]) / (p["b"] - p["a"]), p["coeffs"])
             werr = np.abs(v * xs ** pw - 1)
@@ -122,14 +138,14 @@ def _toy_run(tables, wl_name, m, L, variant, table):
     cts = [O.encrypt(P, K, P.encode(slots[c], scale=P.scale(top), level=top), top,
                      W.derive_seed("enc", wl_name), c) for c in range(m)]
     O.ledger_reset()
-    out = O.softmax(P, K, cts, n, k, 0 if variant == "A" else 1, tab["exp"], tab["inv"])
+    out = O.softmax(P, K, cts, n, k, variant, tab["exp"], tab["inv"])
     led = O.ledger()
     dec = np.stack([O.decrypt_decode(P, K, c).real for c in out])
     return x, dec, led, P, out
 
 
 @pytest.mark.parametrize("m,table", [(1, "toy_n16_M2_k1_A"), (2, "toy_n16_M4_k2_A"), (2, "toy_n16_M4_k2_B"),
-                                     (2, "toy_n16_M4_k2_A_nt")])
+                                     (2, "toy_n16_M4_k2_A_nt"), (2, "toy_n16_M4_k2_S")])
 def test_oracle_toy_softmax_accuracy(tables, m, table):
     L = 100 if m == 1 else 256
     variant = tables[table]["config"]["variant"]

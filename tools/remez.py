@@ -119,7 +119,8 @@ def softmax_tables(n, M, k, variant, deg_exp, deg_first, deg_mid, deg_last, guar
     inv = []
     prev_alpha = None
     for j in range(1, k + 1):
-        p = 0.5 if variant == "A" else 0.5 ** j
+        # Alg 1: x^-1/2; version B: x^-1/2^j (G4); square-and-normalize: x^-1 (G26)
+        p = 0.5 if variant == "A" else 1.0 if variant == "S" else 0.5 ** j
         if j == 1:
             a, b = lo, hi
             deg = deg_first if k > 1 else deg_last
@@ -152,10 +153,14 @@ CONFIGS = {
     # Newton variant of the k = 2 toy: degree-7 seed + 2 Newton steps (G24) -- pins only
     "toy_n16_M4_k2_A_nt": dict(n=16, M=4, k=2, variant="A", deg_exp=7, deg_first=7, deg_mid=7, deg_last=7,
                                newton=2),
+    # square-and-normalize (PAPER.md 757-765, G26) at the k = 2 toy shape
+    "toy_n16_M4_k2_S": dict(n=16, M=4, k=2, variant="S", deg_exp=7, deg_first=15, deg_mid=15, deg_last=31),
     # P16 configs 2-4 (n=256/128, M=128, k=5)
     "p16_n256_M128_k5_A": dict(n=256, M=128, k=5, variant="A", deg_exp=15, deg_first=63, deg_mid=31, deg_last=127),
     "p16_n256_M128_k5_B": dict(n=256, M=128, k=5, variant="B", deg_exp=15, deg_first=63, deg_mid=31, deg_last=127),
     "p16_n128_M128_k5_B": dict(n=128, M=128, k=5, variant="B", deg_exp=15, deg_first=63, deg_mid=31, deg_last=127),
+    # config 2 with square-and-normalize (G26): x^-1 needs degree 63 where x^-1/2 takes 31
+    "p16_n256_M128_k5_S": dict(n=256, M=128, k=5, variant="S", deg_exp=15, deg_first=63, deg_mid=63, deg_last=127),
     # config 5 (n = N0 = 32768, M = 256, Alg 1, k = 7): degree-255
     # middle steps, last step = degree-255 seed + 3 Newton steps (G24)
     "p16_n32768_M256_k7_A": dict(n=32768, M=256, k=7, variant="A", deg_exp=15, deg_first=15, deg_mid=255,

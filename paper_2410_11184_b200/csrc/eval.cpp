@@ -742,16 +742,31 @@ CtP ev_mult_const_sum(const std::vector<const hs_ct *> &terms, const std::vector
     int B = 1;
     for (auto t : terms) B = std::max(B, t->batch);
     CtP acc = ct_new(c, target + 1, 2, st, B);
-    HS_CUDA(cudaMemsetAsync(acc->d, 0, acc->limbs() * N * 8, st));
+    // every nonzero term in one pass per 16 (k_lin_comb): sum_i rint(c_i sc_i) T_i
+    std::vector<const u64 *> ptr;
+    std::vector<int> rl;
+    std::vector<std::vector<u64>> sc;
     for (size_t i = 0; i < terms.size(); i++) {
         if (coef[i] == 0.0) continue;
         const hs_ct *t = terms[i];
         if (t->level < target + 1) throw HsError(HS_ELEVEL, "leaf term below its landing level");
         if (t->batch != B) throw HsError(HS_EINVAL, "leaf terms must share the batch");
-        u64 s[HS_MAXP];
-        residues(P, coef[i] * landing_scale(P, t->level, target), nl, s);
-        k_mul_scalar_s(c, t->d, acc->d, s, (int)t->rows(), nl, t->level + 1, nl, true, st);
+        sc.emplace_back(HS_MAXP);
+        residues(P, coef[i] * landing_scale(P, t->level, target), nl, sc.back().data());
+        ptr.push_back(t->d);
+        rl.push_back(t->level + 1);
         c->ledger[HS_LG_CMULT] += B;
+    }
+    if (ptr.empty()) {
+        HS_CUDA(cudaMemsetAsync(acc->d, 0, acc->limbs() * N * 8, st));
+    } else {
+        const int rows = (int)acc->rows();
+        for (size_t j0 = 0; j0 < ptr.size(); j0 += 16) {
+            const int nt = (int)std::min<size_t>(16, ptr.size() - j0);
+            std::vector<const u64 *> sp(nt);
+            for (int j = 0; j < nt; j++) sp[j] = sc[j0 + j].data();
+            k_lin_comb(c, ptr.data() + j0, rl.data() + j0, sp.data(), nt, acc->d, rows, nl, nl, j0 > 0, st);
+        }
     }
     return ev_rescale(acc.get(), st);
 }

@@ -1404,6 +1404,64 @@ void k_mul_scalar_s(hs_ctx *c, const u64 *a, u64 *o, const u64 *host_scal, int r
     count_kernel(c);
 }
 
+// o = [o +] sum_j s_j a_j over up to 16 terms in ONE pass (Chebyshev leaves,
+// C13): each term read once, 128-bit accumulation against Montgomery-form
+// scalars (s 2^64 mod q; 16 q^2 < q 2^64 for q < 2^60), one REDC.  Term j
+// element (row r, limb i, t) at a_j + (r a_rl[j] + i) N + t; o rows of o_rl.
+struct LinCombArg {
+    const u64 *a[16];
+    int a_rl[16];
+    int n, acc;
+    u64 s[16][HS_MAXP];
+};
+
+__global__ void __launch_bounds__(256) lin_comb_kernel(u64 *__restrict__ o, const __grid_constant__ LinCombArg A,
+                                                       int N, int o_rl)
+{
+    const int t = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
+    if (t >= N) return;
+    const int i = blockIdx.y, r = blockIdx.z;
+    const PrimeK k = c_pk[i];
+    u64 h0 = 0, l0 = 0, h1 = 0, l1 = 0;
+    for (int j = 0; j < A.n; j++) {
+        const ulonglong2 v = *reinterpret_cast<const ulonglong2 *>(A.a[j] + ((size_t)r * A.a_rl[j] + i) * N + t);
+        const u64 sm = A.s[j][i];
+        mac128(h0, l0, v.x, sm);
+        mac128(h1, l1, v.y, sm);
+    }
+    ulonglong2 *op = reinterpret_cast<ulonglong2 *>(o + ((size_t)r * o_rl + i) * N + t);
+    ulonglong2 w = make_ulonglong2(d_redc(h0, l0, k), d_redc(h1, l1, k));
+    if (A.acc) {
+        const ulonglong2 vo = *op;
+        w.x = d_add(vo.x, w.x, k.q);
+        w.y = d_add(vo.y, w.y, k.q);
+    }
+    *op = w;
+}
+
+void k_lin_comb(hs_ctx *c, const u64 *const *a, const int *a_rl, const u64 *const *host_scal, int n_terms, u64 *o,
+                int rows, int nl, int o_rl, bool accumulate, cudaStream_t st)
+{
+    const hs_params *P = c->P;
+    if (n_terms < 1 || n_terms > 16) throw HsError(HS_EINVAL, "lin_comb: 1..16 terms");
+    KTimer _kt(c, KID_SCALAR, (double)rows * nl * P->n * 8 * (n_terms + 1 + (accumulate ? 1 : 0)), st);
+    LinCombArg A;
+    A.n = n_terms;
+    A.acc = accumulate ? 1 : 0;
+    for (int j = 0; j < n_terms; j++) {
+        A.a[j] = a[j];
+        A.a_rl[j] = a_rl[j];
+        for (int i = 0; i < nl; i++) {
+            const u64 q = P->prime[i];
+            A.s[j][i] = (u64)((((unsigned __int128)(host_scal[j][i] % q)) << 64) % q);
+        }
+    }
+    const int N = P->n;
+    lin_comb_kernel<<<dim3((N / 2 + 255) / 256, nl, rows), 256, 0, st>>>(o, A, N, o_rl);
+    HS_CHECK_LAUNCH();
+    count_kernel(c);
+}
+
 // comp 0 of each of B ciphertexts += s_i
 __global__ void add_scalar_b_kernel(u64 *a, ScalarArg s, int N, int nl, int row_stride)
 {

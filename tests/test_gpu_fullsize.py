@@ -78,3 +78,28 @@ def test_config5_full_size_accuracy():
     led = S["ctx"].ledger()
     assert 0 < led["bts"] <= 2 * S["k"] + 2
     assert err < 2.0 ** -12, np.log2(err)
+
+
+def test_p16_bootstrap_parity_full_size():
+    """The bootstrap bench.py runs (P16, N = 2^16, levels 31 -> 12), word for
+    word against the oracle: every output word of one bootstrapped ciphertext
+    (C16-C18 on both sides).  The oracle needs ~2 min of
+    host time here (74 switching keys + one bootstrap)."""
+    import paper_2410_11184_b200 as hs
+    import workloads as W
+    from oracle import oracle as O
+    pre = W.preset("P16")
+    P, PO = hs.Params.from_preset(pre), O.Params.from_preset(pre)
+    rots = hs.bts_rotations(P, pre["bts"])
+    gal = sorted({P.galois_of_rot(r) for r in rots} | {2 * P.n - 1})
+    ctx = hs.Context(P, 0)
+    K, KO = hs.Keys(ctx, 31337, pre["h"], galois=gal), O.Keys(PO, 31337, pre["h"], galois=gal)
+    tab = W.bts_tables()[pre["bts"]["table"]]
+    B, BO = hs.Bts(ctx, pre["bts"], tab), O.Bts(PO, pre["bts"], tab)
+    z = np.random.default_rng(16).uniform(-1, 1, P.n // 2)
+    pt = P.encode(z, scale=P.scale(3), level=3)
+    g = hs.bootstrap(K, B, hs.encrypt(K, pt, 3, 77, 0), 1.0)
+    o = O.bootstrap(PO, KO, O.encrypt(PO, KO, pt, 3, 77, 0), BO, 1.0)
+    assert g.level == o.level == pre["bts"]["out_level"]
+    assert (g.words() == o.words()).all()
+    assert np.abs(hs.decrypt_decode(K, g).real - z).max() < 2.0 ** -19

@@ -1026,10 +1026,19 @@ __global__ void __launch_bounds__(256) bconv_kernel(const u64 *__restrict__ x, s
         u64 c[NS];
 #pragma unroll
         for (int a = 0; a < NS; a++) c[a] = __ldg(cm + 2 * ((size_t)a * A.n_dst + b));
-        u64 hi = 0, lo = 0;
+        // constants in Montgomery form; more than 7 sources fold through one
+        // extra REDC after the 7th term (the 128-bit bound needs n_src q < 2^64)
+        u64 hi = 0, lo = 0, part = 0;
 #pragma unroll
-        for (int a = 0; a < NS; a++) mac128(hi, lo, y[a], c[a]);
-        u64 s = d_redc(hi, lo, k);  // constants in Montgomery form
+        for (int a = 0; a < NS; a++) {
+            mac128(hi, lo, y[a], c[a]);
+            if (NS > 7 && a == 6) {
+                part = d_redc(hi, lo, k);
+                hi = lo = 0;
+            }
+        }
+        u64 s = d_redc(hi, lo, k);
+        if (NS > 7) s = d_add(s, part, k.q);
         if (A.centred) {
             const u64 pmb = __ldg(pm + b);
             for (int kk = 0; kk < neg; kk++) s = d_sub(s, pmb, k.q);
@@ -1040,7 +1049,7 @@ __global__ void __launch_bounds__(256) bconv_kernel(const u64 *__restrict__ x, s
 
 // All ModUp digits of ONE polynomial in one launch (grid.y = digit): digit j
 // converts x limbs [src0_j, src0_j + n_src_j) to its n_dst_j targets at
-// o + dst_off_j.  Non-centred (ModUp).  Up to 7 sources, unrolled with guards.
+// o + dst_off_j.  Non-centred (ModUp).  Up to 8 sources, unrolled with guards.
 struct BconvMultiArg {
     int n_dig;
     struct Dig {
@@ -1060,9 +1069,9 @@ __global__ void __launch_bounds__(256) bconv_multi_kernel(const u64 *__restrict_
     const int b0 = blockIdx.z * BCONV_TG, b1 = min(b0 + BCONV_TG, D.n_dst);
     if (b0 >= b1) return;
     const u64 *tab = D.tab;
-    u64 y[7];
+    u64 y[8];
 #pragma unroll
-    for (int a = 0; a < 7; a++)
+    for (int a = 0; a < 8; a++)
         if (a < D.n_src) {
             const PrimeK k = c_pk[D.src[a]];
             y[a] = d_shoup(x[(size_t)(D.src0 + a) * N + t], __ldg(tab + 2 * a), __ldg(tab + 2 * a + 1), k.q);
@@ -1074,7 +1083,13 @@ __global__ void __launch_bounds__(256) bconv_multi_kernel(const u64 *__restrict_
 #pragma unroll
         for (int a = 0; a < 7; a++)
             if (a < D.n_src) mac128(hi, lo, y[a], __ldg(cm + 2 * ((size_t)a * D.n_dst + b)));
-        o[D.dst_off + (size_t)b * N + t] = d_redc(hi, lo, k);  // constants in Montgomery form
+        u64 r = d_redc(hi, lo, k);  // constants in Montgomery form
+        if (D.n_src > 7) {          // 8th source: its own REDC (n_src q < 2^64 bound)
+            hi = lo = 0;
+            mac128(hi, lo, y[7], __ldg(cm + 2 * ((size_t)7 * D.n_dst + b)));
+            r = d_add(r, d_redc(hi, lo, k), k.q);
+        }
+        o[D.dst_off + (size_t)b * N + t] = r;
     }
 }
 
@@ -1089,7 +1104,7 @@ void k_bconv_modup_multi(hs_ctx *c, const BconvTab *const *tabs, const size_t *d
     int maxg = 1;
     for (int j = 0; j < n_dig; j++) {
         const BconvTab &t = *tabs[j];
-        if (t.n_src > 7 || t.centred) throw HsError(HS_EINVAL, "bconv_multi: ModUp digits only");
+        if (t.n_src > 8 || t.centred) throw HsError(HS_EINVAL, "bconv_multi: ModUp digits of at most 8 primes only");
         A.d[j].tab = t.dev;
         A.d[j].n_src = t.n_src;
         A.d[j].n_dst = t.n_dst;
@@ -1116,13 +1131,14 @@ void k_bconv(hs_ctx *c, const BconvTab &tab, const u64 *src, size_t src_stride, 
     A.centred = tab.centred ? 1 : 0;
     for (int i = 0; i < tab.n_src; i++) A.src[i] = (unsigned char)tab.src[i];
     for (int i = 0; i < tab.n_dst; i++) A.dst[i] = (unsigned char)tab.dst[i];
-    if (tab.n_src > 7) throw HsError(HS_EINVAL, "bconv: more than 7 source primes (128-bit accumulator bound)");
+    if (tab.n_src > 9) throw HsError(HS_EINVAL, "bconv: more than 9 source primes");
     int N = c->P->n;
     const dim3 grid((N + 255) / 256, batch, (tab.n_dst + BCONV_TG - 1) / BCONV_TG);
     switch (tab.n_src) {
 #define BCONV_CASE(ns) \
     case ns: bconv_kernel<ns><<<grid, 256, 0, st>>>(src, src_stride, dst, dst_stride, A, tab.dev, N, bss, bds); break;
         BCONV_CASE(1) BCONV_CASE(2) BCONV_CASE(3) BCONV_CASE(4) BCONV_CASE(5) BCONV_CASE(6) BCONV_CASE(7)
+        BCONV_CASE(8) BCONV_CASE(9)
 #undef BCONV_CASE
     default: throw HsError(HS_EINVAL, "bconv: source count out of range");
     }

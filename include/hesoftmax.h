@@ -51,7 +51,7 @@ typedef enum {
     HS_EDOMAIN = 6,    /* debug: decrypted intermediate outside its interval       */
     HS_ENOMEM = 7,
     HS_ECUDA = 8,
-    HS_ENCCL = 9       /* collective (exchange callback) failure                  */
+    HS_ENCCL = 9       /* collective failure (exchange callback or NCCL)          */
 } hs_status;
 
 typedef struct hs_params hs_params;   /* host tables (primes, twiddles, BConv)  */
@@ -236,6 +236,18 @@ hs_status hs_bootstrap(hs_ctx *c, const hs_keys *k, hs_bts *b, const hs_ct *in, 
 typedef int (*hs_exchange_fn)(void *user, const uint64_t *partial, uint64_t *gathered, size_t words,
                               void *stream);
 
+/* Library-owned NCCL communicator for the sharded many-ciphertext Softmax
+ * (SURVEY 8(b) hs_comm_init).  Rank 0 calls
+ * hs_comm_unique_id and the caller broadcasts the 128 bytes (e.g. with
+ * torch.distributed); every rank then calls hs_comm_init on its own context.
+ * NCCL is loaded at run time (libnccl.so.2); HS_ENCCL if it is missing or a
+ * collective fails.  The aux-sum exchange then runs as ncclAllGather on the
+ * Softmax stream, which CUDA-graph plans capture (hs_softmax_plan_create). */
+typedef struct hs_comm hs_comm;
+hs_status hs_comm_unique_id(uint8_t uid[128]);
+hs_status hs_comm_init(hs_ctx *c, int rank, int world, const uint8_t uid[128], hs_comm **out);
+void hs_comm_destroy(hs_comm *comm);
+
 typedef struct {
     int n;                    /* Softmax dimension                                  */
     int m;                    /* GLOBAL number of main-thread ciphertexts (1: one-ctxt) */
@@ -253,6 +265,9 @@ typedef struct {
                                  LAST inverse-square-root polynomial, which is then a
                                  seed (PAPER.md 1311-1327 [App. A]; G24);
                                  0 = none.  HS_EINVAL if < 0 or with version B       */
+    hs_comm *comm;            /* native exchange (hs_comm_init; NULL = use exchange).
+                                 Its size must equal world; with world == 1 a
+                                 one-rank communicator still runs the exchange   */
 } hs_softmax_desc;
 
 /* One ciphertext (m = 1). */

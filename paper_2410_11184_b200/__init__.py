@@ -308,7 +308,30 @@ def variant_code(variant):
     return codes[variant]
 
 
-def _softmax_desc(n, m, k, variant, exp_poly, inv_polys, world=1, rank=0, exchange=None, bts=None):
+class Comm:
+    """hs_comm_init: a library-owned NCCL communicator.
+    uid: the 128 bytes of Comm.unique_id() from rank 0, broadcast by the caller."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        check(L.hs_comm_unique_id(buf))
+        return bytes(buf)
+
+    def __init__(self, ctx, rank, world, uid: bytes):
+        assert len(uid) == 128
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        p = C.c_void_p()
+        check(L.hs_comm_init(ctx.ptr, rank, world, buf, C.byref(p)))
+        self.ptr, self.rank, self.world, self.ctx = p, rank, world, ctx
+
+    def __del__(self):
+        if getattr(self, "ptr", None):
+            L.hs_comm_destroy(self.ptr)
+            self.ptr = None
+
+
+def _softmax_desc(n, m, k, variant, exp_poly, inv_polys, world=1, rank=0, exchange=None, bts=None, comm=None):
     keep = []
     e, c = _poly(exp_poly)
     keep.append(c)
@@ -323,7 +346,9 @@ def _softmax_desc(n, m, k, variant, exp_poly, inv_polys, world=1, rank=0, exchan
     keep.append(fn)
     # a table's last entry may carry "newton": the polynomial is then a seed (G24)
     d = L.SoftmaxDesc(n, m, k, variant_code(variant), ep, arr, world, rank, fn, None,
-                      bts.ptr if bts is not None else None, int(inv_polys[-1].get("newton", 0)))
+                      bts.ptr if bts is not None else None, int(inv_polys[-1].get("newton", 0)),
+                      comm.ptr if comm is not None else None)
+    keep.append(comm)
     return d, keep
 
 
@@ -340,9 +365,12 @@ class Plan:
     bound to the input ciphertexts `cts` (re-read at every run); outputs are
     plan-owned and overwritten by each run()."""
 
-    def __init__(self, keys: Keys, cts, n, m, k, variant, exp_poly, inv_polys, bts=None, stream=None):
+    def __init__(self, keys: Keys, cts, n, m, k, variant, exp_poly, inv_polys, bts=None, stream=None, comm=None):
+        """comm: a Comm of world > 1 makes this a sharded plan (this rank's
+        m / world ciphertexts; the NCCL all-gather is captured in the graph)."""
         self.keys, self.cts = keys, list(cts)
-        self._d, self._keep = _softmax_desc(n, m, k, variant, exp_poly, inv_polys, 1, 0, None, bts)
+        world, rank = (comm.world, comm.rank) if comm is not None else (1, 0)
+        self._d, self._keep = _softmax_desc(n, m, k, variant, exp_poly, inv_polys, world, rank, None, bts, comm)
         ml = len(cts)
         ins = (C.c_void_p * ml)(*[c.ptr.value if isinstance(c.ptr, C.c_void_p) else c.ptr for c in cts])
         p = C.c_void_p()
@@ -362,10 +390,12 @@ class Plan:
 
 
 def softmax_many_ctxt(keys: Keys, cts, n, m, k, variant, exp_poly, inv_polys, world=1, rank=0, exchange=None,
-                      bts=None, stream=None):
-    """cts: this rank's m/world ciphertexts.  exchange: an EXCHANGE_FN (see
-    paper_2410_11184_b200.dist) when world > 1."""
-    d, keep = _softmax_desc(n, m, k, variant, exp_poly, inv_polys, world, rank, exchange, bts)
+                      bts=None, stream=None, comm=None):
+    """cts: this rank's m/world ciphertexts.  world > 1 needs comm (a Comm,
+    native NCCL) or exchange (an EXCHANGE_FN, see paper_2410_11184_b200.dist)."""
+    if comm is not None:
+        world, rank = comm.world, comm.rank
+    d, keep = _softmax_desc(n, m, k, variant, exp_poly, inv_polys, world, rank, exchange, bts, comm)
     ml = len(cts)
     ins = (C.c_void_p * ml)(*[c.ptr.value if isinstance(c.ptr, C.c_void_p) else c.ptr for c in cts])
     outs = (C.c_void_p * ml)()

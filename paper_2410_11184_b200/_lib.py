@@ -54,7 +54,7 @@ class SoftmaxDesc(C.Structure):
     _fields_ = [("n", C.c_int), ("m", C.c_int), ("k", C.c_int), ("variant", C.c_int),
                 ("exp_poly", C.POINTER(Poly)), ("inv_poly", C.POINTER(Poly)), ("world", C.c_int),
                 ("rank", C.c_int), ("exchange", EXCHANGE_FN), ("exchange_user", vp), ("bts", vp),
-                ("newton", C.c_int)]
+                ("newton", C.c_int), ("comm", vp)]
 
 
 class BtsDesc(C.Structure):
@@ -120,6 +120,9 @@ hs_softmax_one_ctxt = _sig("hs_softmax_one_ctxt", C.c_int,
                            [vp, vp, C.POINTER(SoftmaxDesc), vp, vp, C.POINTER(vp)])
 hs_softmax_many_ctxt = _sig("hs_softmax_many_ctxt", C.c_int,
                             [vp, vp, C.POINTER(SoftmaxDesc), C.POINTER(vp), C.c_size_t, vp, C.POINTER(vp)])
+hs_comm_unique_id = _sig("hs_comm_unique_id", C.c_int, [C.POINTER(C.c_uint8)])
+hs_comm_init = _sig("hs_comm_init", C.c_int, [vp, C.c_int, C.c_int, C.POINTER(C.c_uint8), C.POINTER(vp)])
+hs_comm_destroy = _sig("hs_comm_destroy", None, [vp])
 hs_bts_create = _sig("hs_bts_create", C.c_int, [vp, C.POINTER(BtsDesc), C.POINTER(vp)])
 hs_bts_destroy = _sig("hs_bts_destroy", None, [vp])
 hs_bts_rotations = _sig("hs_bts_rotations", C.c_int, [vp, C.c_int, C.c_int, i32p, C.c_int])

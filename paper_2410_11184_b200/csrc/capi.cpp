@@ -418,6 +418,31 @@ hs_status hs_softmax_many_ctxt(hs_ctx *c, const hs_keys *k, const hs_softmax_des
 
 }  // extern "C"
 
+extern "C" {
+
+hs_status hs_comm_unique_id(uint8_t uid[128])
+{
+    HS_TRY
+    if (!uid) throw HsError(HS_EINVAL, "NULL argument");
+    comm_unique_id(uid);
+    return HS_OK;
+    HS_CATCH
+}
+
+hs_status hs_comm_init(hs_ctx *c, int rank, int world, const uint8_t uid[128], hs_comm **out)
+{
+    HS_TRY
+    if (!c || !uid || !out || world < 1 || rank < 0 || rank >= world) throw HsError(HS_EINVAL, "bad communicator");
+    activate(c);
+    *out = comm_create(rank, world, uid);
+    return HS_OK;
+    HS_CATCH
+}
+
+void hs_comm_destroy(hs_comm *comm) { comm_destroy(comm); }
+
+}  // extern "C"
+
 struct hs_plan {
     hs_ctx *c = nullptr;
     cudaGraph_t graph = nullptr;
@@ -439,7 +464,8 @@ hs_status hs_softmax_plan_create(hs_ctx *c, const hs_keys *k, const hs_softmax_d
 {
     HS_TRY
     if (!c || !k || !d || !in || !out || m_local < 1) throw HsError(HS_EINVAL, "NULL argument");
-    if (d->world > 1) throw HsError(HS_EINVAL, "plans capture single-GPU Softmax (world == 1)");
+    if (d->world > 1 && !d->comm)
+        throw HsError(HS_EINVAL, "plans capture a sharded Softmax only with a native communicator (hs_comm_init)");
     activate(c);
     cudaStream_t user = S(stream);
     std::unique_ptr<hs_plan> p(new hs_plan);

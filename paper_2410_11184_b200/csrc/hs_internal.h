@@ -314,5 +314,11 @@ int bts_exponent(const hs_params *P, int arcsine, double bound);
 int bts_rotations(const hs_params *P, int n_cts, int n_stc, int32_t *out, int max);
 
 // softmax.cpp
+// comm.cpp: NCCL (dlopen'ed) for the sharded aux sum
+void comm_unique_id(uint8_t uid[128]);
+hs_comm *comm_create(int rank, int world, const uint8_t uid[128]);
+void comm_destroy(hs_comm *comm);
+int comm_world(const hs_comm *c);
+void comm_all_gather(const hs_comm *c, const u64 *partial, u64 *gathered, size_t words, cudaStream_t st);
 hs_status softmax_run(hs_ctx *c, const hs_keys *K, const hs_softmax_desc *d, const hs_ct *const *in,
                       size_t m_local, cudaStream_t st, hs_ct **out);

@@ -64,7 +64,10 @@ hs_status softmax_run(hs_ctx *c, const hs_keys *K, const hs_softmax_desc *d, con
     // Alg 1 and square-and-normalize share the schedule (variant 0 / 2)
     const bool alg1 = d->variant != 1;
     if (m % world || (size_t)(m / world) != m_local) throw HsError(HS_EINVAL, "softmax: m_local != m / world");
-    if (world > 1 && !d->exchange) throw HsError(HS_EINVAL, "softmax: world > 1 needs an exchange callback");
+    if (d->comm && comm_world(d->comm) != world)
+        throw HsError(HS_EINVAL, "softmax: communicator size != world");
+    if (world > 1 && !d->exchange && !d->comm)
+        throw HsError(HS_EINVAL, "softmax: world > 1 needs a communicator or an exchange callback");
     const int nb = n / m;
     if ((nb & (nb - 1)) || nb > N0) throw HsError(HS_EINVAL, "softmax: n/m must be a power of two <= N0");
     const int stride = N0 / nb;
@@ -101,10 +104,11 @@ hs_status softmax_run(hs_ctx *c, const hs_keys *K, const hs_softmax_desc *d, con
         if (y->level < 1) level_error("main thread out of levels");
         // ---- auxiliary thread: S = relin(sum tensor(y, y)) -> rescale (C15)
         CtP acc = ev_tensor_sum(y.get(), st);
-        if (world > 1) {
+        if (world > 1 || d->comm) {
             const size_t words = acc->limbs() * P->n;
             DBuf gathered(words * world, st);
-            if (d->exchange(d->exchange_user, acc->d, gathered.p, words, st) != 0)
+            if (d->comm) comm_all_gather(d->comm, acc->d, gathered.p, words, st);  // native NCCL
+            else if (d->exchange(d->exchange_user, acc->d, gathered.p, words, st) != 0)
                 throw HsError(HS_ENCCL, "softmax: exchange callback failed");
             // sum in rank order (exact modular addition)
             HS_CUDA(cudaMemcpyAsync(acc->d, gathered.p, words * 8, cudaMemcpyDeviceToDevice, st));

@@ -455,3 +455,33 @@ def test_softmax_error_paths(tables):
     ref = np.exp(x - x.max(1, keepdims=True))
     ref /= ref.sum(1, keepdims=True)
     assert np.abs(y - ref).max() < 2.0 ** -15
+
+
+def test_native_comm_single_rank(tables):
+    """hs_comm_init (native NCCL) on one GPU: a one-rank
+    communicator runs the aux-sum all-gather (a copy) on the Softmax stream,
+    eagerly and captured in a CUDA-graph plan; the words equal the run
+    without an exchange."""
+    hs = _hs()
+    tab = tables["toy_n16_M4_k2_B"]
+    cfg = tab["config"]
+    n, k, M, m = cfg["n"], cfg["k"], cfg["M"], 2
+    pre = W.preset("TOY12D")
+    P = hs.Params.from_preset(pre)
+    PO = O.Params.from_preset(pre)
+    ctx = hs.Context(P, 0)
+    K = hs.Keys(ctx, 5, pre["h"], galois=O.softmax_rotation_galois(PO, n, m))
+    x = W.softmax_inputs((P.n // 2) * m // n, n, M, seed=8)
+    slots = P.pack(x, m)
+    top = len(pre["q_bits"]) - 1
+    cts = [hs.encrypt(K, P.encode(slots[c], scale=P.scale(top), level=top), top, 3, c) for c in range(m)]
+    ref = hs.softmax_many_ctxt(K, cts, n, m, k, "B", tab["exp"], tab["inv"])
+    comm = hs.Comm(ctx, 0, 1, hs.Comm.unique_id())
+    got = hs.softmax_many_ctxt(K, cts, n, m, k, "B", tab["exp"], tab["inv"], comm=comm)
+    for a, b in zip(got, ref):
+        assert (a.words() == b.words()).all()
+    plan = hs.Plan(K, cts, n, m, k, "B", tab["exp"], tab["inv"], comm=comm)
+    for _ in range(2):
+        for a, b in zip(plan.run(), ref):
+            assert (a.words() == b.words()).all()
+    del plan

@@ -466,8 +466,15 @@ def oracle_sample(budget_s=20.0):
 
 
 def cpu_baseline(ledger_step, budget_s=20.0):
+    from oracle import oracle as O
     per_mult, reps = oracle_sample(budget_s)
-    cores = os.cpu_count()
+    cores = O.max_threads()
+    # the paper's setting (one CPU thread): a shorter sample
+    O.set_threads(1)
+    try:
+        per_mult1, reps1 = oracle_sample(budget_s / 4)
+    finally:
+        O.set_threads(cores)
     # extrapolate by key-switch count: one oracle HMult at level 12 is one KS plus
     # a tensor and a rescale; the step performs ledger_step["ks"] key switches at
     # mixed levels (an approximation, stated in "sample").
@@ -475,7 +482,11 @@ def cpu_baseline(ledger_step, budget_s=20.0):
     return {"value": round(est_step_s * 1e3 / 8192, 3), "unit": "ms/Softmax", "cores": cores, "kind": "oracle",
             "sample": f"{reps} oracle HMult+relin+rescale at N=2^16, level 12 ({per_mult:.2f} s each, OpenMP over "
                       f"limbs) extrapolated by the step's key-switch count ({ledger_step.get('ks')} KS/step) to "
-                      f"8192 Softmax"}
+                      f"8192 Softmax",
+            "single_thread": {"value": round(per_mult1 * max(1, ledger_step.get("ks", 1)) * 1e3 / 8192, 3),
+                              "unit": "ms/Softmax", "cores": 1,
+                              "sample": f"{reps1} HMult+relin+rescale at level 12 on one thread "
+                                        f"({per_mult1:.2f} s each), same extrapolation"}}
 
 
 def run_reference(args):

@@ -3,6 +3,7 @@
  * harness (oracle/oracle.py, via ctypes).  TEST INFRASTRUCTURE ONLY.
  */
 #include "orc.h"
+#include <omp.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -173,6 +174,10 @@ int orc_api_softmax(const orc_params *P, const orc_keys *K, int n, int m, int k,
     free(polys);
     return rc;
 }
+
+/* OpenMP threads of the oracle (bench's single-thread baseline) */
+void orc_api_set_threads(int n) { omp_set_num_threads(n < 1 ? 1 : n); }
+int orc_api_max_threads(void) { return omp_get_max_threads(); }
 
 void orc_api_ledger(long *out) { memcpy(out, orc_ledger, sizeof(orc_ledger)); }
 void orc_api_ledger_reset(void) { memset(orc_ledger, 0, sizeof(orc_ledger)); }

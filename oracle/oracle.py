@@ -301,6 +301,15 @@ def softmax(P: Params, K: Keys, cts, n, k, variant, exp_poly, inv_polys):
     return [Ct(P, outs[i]) for i in range(m)]
 
 
+def set_threads(n: int):
+    """OpenMP threads the oracle uses (1 = the paper's single-thread setting)."""
+    lib().orc_api_set_threads(int(n))
+
+
+def max_threads() -> int:
+    return int(lib().orc_api_max_threads())
+
+
 def ledger():
     a = (C.c_long * len(LEDGER))()
     lib().orc_api_ledger(a)

@@ -5,6 +5,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "hs_internal.h"
 
@@ -138,7 +139,15 @@ hs_status hs_keys_export_swk(hs_ctx *c, const hs_keys *k, int galois, uint64_t *
     if (!key) throw HsError(HS_EKEY, "no such switching key");
     const hs_params *P = c->P;
     HS_CUDA(cudaDeviceSynchronize());
-    HS_CUDA(cudaMemcpy(host_out, key->k, (size_t)P->dnum * 2 * (P->n_q + P->n_p) * P->n * 8, cudaMemcpyDeviceToHost));
+    // stored interleaved [dnum][nt][N][2]; exported planar [dnum][2][nt][N]
+    const size_t W = (size_t)(P->n_q + P->n_p) * P->n;
+    std::vector<uint64_t> tmp((size_t)P->dnum * 2 * W);
+    HS_CUDA(cudaMemcpy(tmp.data(), key->k, tmp.size() * 8, cudaMemcpyDeviceToHost));
+    for (int j = 0; j < P->dnum; j++)
+        for (size_t w = 0; w < W; w++) {
+            host_out[((size_t)j * 2 + 0) * W + w] = tmp[((size_t)j * W + w) * 2 + 0];
+            host_out[((size_t)j * 2 + 1) * W + w] = tmp[((size_t)j * W + w) * 2 + 1];
+        }
     return HS_OK;
     HS_CATCH
 }

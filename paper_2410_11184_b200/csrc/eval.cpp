@@ -832,10 +832,13 @@ hs_keys *keys_generate(hs_ctx *c, u64 seed, int h, const int32_t *galois, size_t
         else k_permute(c, K->s_ntt, sp.p, galois_table(c, id), nt, st);
         SwKey key;
         key.galois = id;
+        // generated component-planar ([dnum][2][nt][N]) in a scratch buffer,
+        // stored interleaved ([dnum][nt][N][2]: one 16-byte load per word pair)
+        DBuf planar((size_t)P->dnum * 2 * nt * N, st);
         HS_CUDA(cudaMalloc(&key.k, (size_t)P->dnum * 2 * nt * N * 8));
         for (int j = 0; j < P->dnum; j++) {
             u64 sub = (u64)id * 256 + (u64)j;
-            u64 *k0 = key.k + (size_t)(2 * j) * nt * N, *k1 = key.k + (size_t)(2 * j + 1) * nt * N;
+            u64 *k0 = planar.p + (size_t)(2 * j) * nt * N, *k1 = planar.p + (size_t)(2 * j + 1) * nt * N;
             k_uniform(c, k1, nt, pmap_range(0, nt), seed, TAG_KSK_A, sub, 0, st);
             error_poly(c, seed, TAG_KSK_E, sub, ETA_ERR, k0, nt, st);
             k_mul_pointwise(c, k1, K->s_ntt, as.p, nt, nt, nt, st);
@@ -844,6 +847,7 @@ hs_keys *keys_generate(hs_ctx *c, u64 seed, int h, const int32_t *galois, size_t
             for (int i = 0; i < nq; i++) g[i] = (i / P->alpha == j) ? P->p_mod_q[i] : 0;
             k_mac_scalar(c, k0, sp.p, g, nq, nq, st);
         }
+        k_interleave2(c, planar.p, key.k, P->dnum, nt * N, st);
         K->swk.push_back(key);
     }
     HS_CUDA(cudaStreamSynchronize(st));

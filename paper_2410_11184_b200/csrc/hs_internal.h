@@ -104,7 +104,7 @@ struct hs_ctx {
 
 struct SwKey {
     int galois = 0;
-    u64 *k = nullptr;           // [dnum][2][n_q+n_p][N]
+    u64 *k = nullptr;           // [dnum][n_q+n_p][N][2]: (b, a) word pairs interleaved
 };
 
 struct hs_keys {
@@ -227,6 +227,8 @@ void k_add_b(hs_ctx *c, const u64 *a, int a_rows, const u64 *b, int b_rows, u64 
 void k_mul_scalar_s(hs_ctx *c, const u64 *a, u64 *o, const u64 *host_scal, int rows, int nl, int a_rl, int o_rl,
                     bool accumulate, cudaStream_t st);
 void k_add_scalar_b(hs_ctx *c, u64 *a, const u64 *host_scal, int B, int ncomp, int nl, cudaStream_t st);
+// o[d][w][c] = planar[d][c][w]: [D][2][W] -> [D][W][2] (switching-key layout)
+void k_interleave2(hs_ctx *c, const u64 *planar, u64 *o, int D, size_t W, cudaStream_t st);
 void k_lin_comb(hs_ctx *c, const u64 *const *a, const int *a_rl, const u64 *const *host_scal, int n_terms, u64 *o,
                 int rows, int nl, int o_rl, bool accumulate, cudaStream_t st);
 void k_tensor_b(hs_ctx *c, const u64 *a, const u64 *b, u64 *o, int B, int nl, int b_batch, cudaStream_t st);

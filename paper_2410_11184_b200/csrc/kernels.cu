@@ -1174,8 +1174,8 @@ __global__ void ks_inner_kernel(const u64 *__restrict__ d, const u64 *__restrict
             int gg = g < lo ? g : g - dn;
             v = ext[((size_t)j * (nl + A.alpha) + gg) * N + t];
         }
-        u64 k0 = key[(((size_t)j * 2 + 0) * ntot + pi) * N + t];
-        u64 k1 = key[(((size_t)j * 2 + 1) * ntot + pi) * N + t];
+        const ulonglong2 kk = reinterpret_cast<const ulonglong2 *>(key)[((size_t)j * ntot + pi) * N + t];
+        u64 k0 = kk.x, k1 = kk.y;
         mac128(h0, l0, v, k0);
         mac128(h1, l1, v, k1);
     }
@@ -1455,6 +1455,21 @@ __global__ void __launch_bounds__(256) lin_comb_kernel(u64 *__restrict__ o, cons
     *op = w;
 }
 
+__global__ void interleave2_kernel(const u64 *planar, u64 *o, size_t W)
+{
+    const size_t w = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= W) return;
+    const size_t d = blockIdx.y;
+    reinterpret_cast<ulonglong2 *>(o)[d * W + w] = make_ulonglong2(planar[(d * 2) * W + w], planar[(d * 2 + 1) * W + w]);
+}
+
+void k_interleave2(hs_ctx *c, const u64 *planar, u64 *o, int D, size_t W, cudaStream_t st)
+{
+    interleave2_kernel<<<dim3((unsigned)((W + 255) / 256), D), 256, 0, st>>>(planar, o, W);
+    HS_CHECK_LAUNCH();
+    count_kernel(c);
+}
+
 void k_lin_comb(hs_ctx *c, const u64 *const *a, const int *a_rl, const u64 *const *host_scal, int n_terms, u64 *o,
                 int rows, int nl, int o_rl, bool accumulate, cudaStream_t st)
 {
@@ -1631,8 +1646,8 @@ __global__ void __launch_bounds__(256, BT == 2 ? 8 : 1) ks_inner_b_kernel(const 
     for (int u = 0; u < BT; u++) h0[u] = l0[u] = h1[u] = l1[u] = 0;
     for (int j = 0; j < A.beta; j++) {
         const int lo = j * A.alpha, hi = min((j + 1) * A.alpha, nl), dn = hi - lo;
-        const u64 k0 = key[(((size_t)j * 2 + 0) * ntot + pi) * N + t];
-        const u64 k1 = key[(((size_t)j * 2 + 1) * ntot + pi) * N + t];
+        const ulonglong2 kk = reinterpret_cast<const ulonglong2 *>(key)[((size_t)j * ntot + pi) * N + t];
+        const u64 k0 = kk.x, k1 = kk.y;
         const bool own = g >= lo && g < hi;
         const int gg = g < lo ? g : g - dn;
 #pragma unroll
@@ -1750,8 +1765,8 @@ __global__ void __launch_bounds__(256) ks_inner_h_kernel(const u64 *__restrict__
 #pragma unroll 4
     for (int j = 0; j < A.beta; j++) {
         const int lo = j * A.alpha, hi = min((j + 1) * A.alpha, nl), dn = hi - lo;
-        const u64 k0 = key[(((size_t)j * 2 + 0) * ntot + pi) * N + t];
-        const u64 k1 = key[(((size_t)j * 2 + 1) * ntot + pi) * N + t];
+        const ulonglong2 kk = reinterpret_cast<const ulonglong2 *>(key)[((size_t)j * ntot + pi) * N + t];
+        const u64 k0 = kk.x, k1 = kk.y;
         const bool own = g >= lo && g < hi;
         const int gg = g < lo ? g : g - dn;
         const u64 v = own ? d[(size_t)g * N + src] : ext[A.off[j] + (size_t)gg * N + src];
@@ -1814,7 +1829,7 @@ struct KsArgM {
     int nd[16];
 };
 
-__global__ void __launch_bounds__(256, 8) ks_inner_m_kernel(const u64 *__restrict__ d, const u64 *__restrict__ ext,
+__global__ void __launch_bounds__(256) ks_inner_m_kernel(const u64 *__restrict__ d, const u64 *__restrict__ ext,
                                                          u64 *__restrict__ acc, const __grid_constant__ KsArgM A,
                                                          int N)
 {
@@ -1830,8 +1845,8 @@ __global__ void __launch_bounds__(256, 8) ks_inner_m_kernel(const u64 *__restric
 #pragma unroll 4
     for (int j = 0; j < A.beta; j++) {
         const int lo = j * A.alpha, hi = min((j + 1) * A.alpha, nl), dn = hi - lo;
-        const u64 k0 = key[(((size_t)j * 2 + 0) * ntot + pi) * N + t];
-        const u64 k1 = key[(((size_t)j * 2 + 1) * ntot + pi) * N + t];
+        const ulonglong2 kk = reinterpret_cast<const ulonglong2 *>(key)[((size_t)j * ntot + pi) * N + t];
+        const u64 k0 = kk.x, k1 = kk.y;
         const bool own = g >= lo && g < hi;
         const int gg = g < lo ? g : g - dn;
         const u64 v = own ? d[(size_t)r * A.d_stride + (size_t)g * N + t]

@@ -175,6 +175,15 @@ int orc_softmax(const orc_params *P, const orc_keys *K, const orc_softmax_desc *
         for (int c = 0; c < m; c++) {
             if (d->variant == 0) {
                 orc_ct *z = orc_op_mult(P, K, lam, y[c]);        /* Alg 1 line 4 */
+                /* G12 (c'): bootstrap the normalised z (|z| <= 1 + alpha, larger
+                 * than y) when its square would leave y below the 2 levels the
+                 * next iteration needs */
+                if (d->bts && j < d->k && z->level - 1 < 2) {
+                    orc_ct *zb = d->bts(P, K, z, d->bts_ctx, 1.1);
+                    if (!zb) { orc_ct_release(z); rc = ORC_ELEVEL; goto done; }
+                    orc_ct_release(z);
+                    z = zb;
+                }
                 swap_in(&y[c], orc_op_mult(P, K, z, z));          /* Alg 1 line 5 */
                 orc_ct_release(z);
             } else if (d->variant == 2) {

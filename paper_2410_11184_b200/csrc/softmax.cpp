@@ -167,6 +167,19 @@ hs_status softmax_run(hs_ctx *c, const hs_keys *K, const hs_softmax_desc *d, con
         if (lam->level < 1) level_error("lambda out of levels");
         if (d->variant == 0) {
             CtP z = ev_mult(K, lam.get(), y.get(), st);
+            // G12 (c'): bootstrap the normalised z (|z| <= 1 + alpha, larger
+            // than y) when its square would leave y below the 2 levels the
+            // next iteration needs
+            if (d->bts && j < d->k && z->level - 1 < 2) {
+                std::vector<CtP> parts(ml);
+                std::vector<const hs_ct *> ptrs(ml);
+                for (int i = 0; i < ml; i++) {
+                    CtP one = ct_slice(z.get(), i, st);
+                    parts[i] = ev_bootstrap(K, d->bts, one.get(), 1.1, st);
+                    ptrs[i] = parts[i].get();
+                }
+                z = ct_gather(ptrs.data(), ml, st);
+            }
             y = ev_mult(K, z.get(), z.get(), st);
         } else if (d->variant == 2) {
             CtP w = ev_mult(K, y.get(), y.get(), st);

@@ -143,13 +143,21 @@ int orc_softmax(const orc_params *P, const orc_keys *K, const orc_softmax_desc *
             orc_ct_release(xh);
         }
         orc_ct_release(S); S = NULL;
-        /* G12 (b), Alg 1: bootstrap lambda_j BEFORE the mask when the mask
-         * would leave it below the main level: the broadcast then copies block
-         * 0's value, so every coordinate of an instance sees the same
-         * bootstrapping error (a common factor the next normalisation absorbs)
-         * instead of an independent one per slot */
-        if (alg1 && lj->level - 1 < main_level && d->bts) {
-            double bound = d->variant == 2 ? 1.1 / ip->a : 1.1 / sqrt(ip->a);
+        /* Alg B line 5, taken BEFORE the mask: lambda_j holds its value in every
+         * coordinate block (S was summed over all of them), so the product
+         * lambda * lambda_j is the new lambda everywhere */
+        if (d->variant == 1 && j > 1) {
+            orc_ct *t = orc_op_mult(P, K, lam, lj);
+            orc_ct_release(lj);
+            lj = t;
+        }
+        /* G12 (b): bootstrap lambda_j (version B: the product) BEFORE the mask
+         * when the mask would leave it below the main level: the broadcast then
+         * copies block 0's value, so every coordinate of an instance sees the
+         * same bootstrapping error (a common factor the next normalisation
+         * absorbs) instead of an independent one per slot */
+        if (lj->level - 1 < main_level && d->bts) {
+            double bound = d->variant == 2 ? 1.1 / ip->a : (d->variant == 1 && j > 1) ? 1.5 : 1.1 / sqrt(ip->a);
             if ((rc = bts_or_fail(P, K, d, &lj, bound))) goto done;
         }
         /* step 7: mask block 0 */
@@ -157,19 +165,8 @@ int orc_softmax(const orc_params *P, const orc_keys *K, const orc_softmax_desc *
         swap_in(&lj, orc_op_mult_pt(P, lj, mask, NULL, lj->level - 1));
         /* steps 8-10: broadcast back (rotations by +stride 2^i) */
         if ((rc = rot_sum(P, K, &lj, nb, stride, +1))) goto done;
-        if (d->variant == 1 && j > 1) {
-            orc_ct *t = orc_op_mult(P, K, lam, lj);      /* Alg B line 5 */
-            orc_ct_release(lam); orc_ct_release(lj); lj = NULL;
-            lam = t;
-        } else {
-            orc_ct_release(lam);
-            lam = lj; lj = NULL;
-        }
-        /* G12 (b), version B: bootstrap lambda (the product) if it ended below
-         * the main level */
-        if (d->variant == 1 && lam->level < main_level && d->bts) {
-            if ((rc = bts_or_fail(P, K, d, &lam, 1.5))) goto done;
-        }
+        orc_ct_release(lam);
+        lam = lj; lj = NULL;
         /* ---- main thread ---- */
         if (lam->level < 1) { rc = ORC_ELEVEL; goto done; }
         for (int c = 0; c < m; c++) {

@@ -149,20 +149,24 @@ hs_status softmax_run(hs_ctx *c, const hs_keys *K, const hs_softmax_desc *d, con
             for (int t = 0; t < nt; t++) lj = newton_step(K, xh.get(), lj.get(), st);
         }
         S.reset();
-        // G12 (b), Alg 1: bootstrap lambda_j BEFORE the mask when the mask would
-        // leave it below the main level -- the broadcast then gives every
-        // coordinate of an instance block 0's value, one common bootstrapping
-        // error per instance (absorbed by the next normalisation)
-        if (alg1 && lj->level - 1 < main_level && d->bts)
-            lj = ev_bootstrap(K, d->bts, lj.get(), d->variant == 2 ? 1.1 / ip->a : 1.1 / sqrt(ip->a), st);
+        // Alg B line 5, taken BEFORE the mask: lambda_j holds its value in every
+        // coordinate block (S was summed over all of them), so lambda * lambda_j
+        // is the new lambda everywhere
+        if (d->variant == 1 && j > 1) lj = ev_mult(K, lam.get(), lj.get(), st);
+        // G12 (b): bootstrap lambda_j (version B: the product) BEFORE the mask
+        // when the mask would leave it below the main level -- the broadcast
+        // then gives every coordinate of an instance block 0's value, one
+        // common bootstrapping error per instance (absorbed by the next
+        // normalisation) instead of an independent one per slot
+        if (lj->level - 1 < main_level && d->bts) {
+            const double bound =
+                d->variant == 2 ? 1.1 / ip->a : (d->variant == 1 && j > 1) ? 1.5 : 1.1 / sqrt(ip->a);
+            lj = ev_bootstrap(K, d->bts, lj.get(), bound, st);
+        }
         if (lj->level < 1) level_error("no level for the mask");
         lj = ev_mult_pt(lj.get(), mask.data(), nullptr, lj->level - 1, st);
         rot_sum(K, lj, nb, stride, +1, st);
-        if (d->variant == 1 && j > 1) lam = ev_mult(K, lam.get(), lj.get(), st);
-        else lam = std::move(lj);
-        // G12 (b), version B: bootstrap lambda (the product) if it ended below
-        // the main level
-        if (d->variant == 1 && lam->level < main_level && d->bts) lam = ev_bootstrap(K, d->bts, lam.get(), 1.5, st);
+        lam = std::move(lj);
         // ---- main thread (lam broadcast against the batch)
         if (lam->level < 1) level_error("lambda out of levels");
         if (d->variant == 0) {

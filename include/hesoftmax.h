@@ -253,10 +253,11 @@ typedef struct {
     int m;                    /* GLOBAL number of main-thread ciphertexts (1: one-ctxt) */
     int k;                    /* iterations (PAPER.md 821)                          */
     int variant;              /* 0 = Alg 1 (normalize-and-square), 1 = version B,
-                                 2 = square-and-normalize (PAPER.md 757-765, G26)   */
+                                 2 = square-and-normalize (PAPER.md 757-765, G26),
+                                 3 = cube-and-normalize (PAPER.md 1645-1663, G27)   */
     const hs_poly *exp_poly;  /* exp(x/2^k) on [-M, 0]                              */
     const hs_poly *inv_poly;  /* k polynomials: x^-1/2 (Alg 1), x^-1/2^j (version B),
-                                 x^-1 (square-and-normalize)                         */
+                                 x^-1 (square- / cube-and-normalize)                 */
     int world, rank;          /* sharding of the m ciphertexts (1, 0 = one GPU)     */
     hs_exchange_fn exchange;  /* required when world > 1                            */
     void *exchange_user;

@@ -280,7 +280,8 @@ def cheb_depth(deg):
     return lib().orc_api_cheb_depth(deg)
 
 
-VARIANT = {"A": 0, "B": 1, "S": 2, 0: 0, 1: 1, 2: 2}  # S: square-and-normalize (G26)
+# S: square-and-normalize (G26); T3: cube-and-normalize (G27)
+VARIANT = {"A": 0, "B": 1, "S": 2, "T3": 3, 0: 0, 1: 1, 2: 2, 3: 3}
 
 
 def softmax(P: Params, K: Keys, cts, n, k, variant, exp_poly, inv_polys):

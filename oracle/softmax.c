@@ -8,6 +8,8 @@
  *                                 exponent read as -1/2^j (G4)
  *   square-and-normalize          PAPER.md 757-765 [sec 3.3, remark]: variant 2,
  *                                 mu_j = (sum y^2)^-1, y <- mu_j y^2 (G26)
+ *   t-th power, t = 3             PAPER.md 1645-1663 [App. C]: variant 3,
+ *                                 mu_j = (sum y^3)^-1, y <- mu_j y^3 (G27)
  *   packings                      PAPER.md 94-131 [sec 4.1-4.2]
  *   many-ciphertext aux sum       DESIGN.md C15 / G6 (sum of tensors, one relin)
  *   bootstrap placement           PAPER.md 429-440 [sec 5.1.3], rule G12
@@ -71,8 +73,10 @@ static int poly_cost(const orc_cheb *p)
 int orc_softmax(const orc_params *P, const orc_keys *K, const orc_softmax_desc *d, orc_ct *const *x, orc_ct **out)
 {
     int m = d->m, n = d->n, N0 = P->n / 2;
-    if (m < 1 || n % m || d->variant < 0 || d->variant > 2 || d->newton < 0 || (d->newton > 0 && d->variant != 0))
+    if (m < 1 || n % m || d->variant < 0 || d->variant > 3 || d->newton < 0 || (d->newton > 0 && d->variant != 0))
         return ORC_EINVAL;
+    /* the cube variant's main update consumes 3 levels (y^2, y^3, mu y^3) */
+    int main_need = d->variant == 3 ? 3 : 2;
     /* Alg 1 and square-and-normalize share the schedule (variant 0 / 2) */
     int alg1 = d->variant != 1;
     int nb = n / m;
@@ -81,6 +85,7 @@ int orc_softmax(const orc_params *P, const orc_keys *K, const orc_softmax_desc *
     int rc = ORC_OK;
     orc_ct **y0 = calloc(m, sizeof(orc_ct *)), **y = calloc(m, sizeof(orc_ct *));
     orc_ct *lam = NULL, *S = NULL, *lj = NULL;
+    orc_ct **w = NULL;  /* G27: the squares y_c^2 of the current iteration */
     double *mask = calloc(N0, sizeof(double));
     for (int s = 0; s < stride; s++) mask[s] = 1.0;       /* G10: block 0 */
 
@@ -93,15 +98,18 @@ int orc_softmax(const orc_params *P, const orc_keys *K, const orc_softmax_desc *
     for (int j = 1; j <= d->k; j++) {
         const orc_cheb *ip = &d->inv_poly[j - 1];
         /* Alg 1 main thread needs 1 (aux square) + 2 levels; bootstrap y (G12 c) */
-        if (alg1 && y[0]->level < 2) {
+        if (alg1 && y[0]->level < main_need) {
             for (int c = 0; c < m; c++) if ((rc = bts_or_fail(P, K, d, &y[c], 1.0))) goto done;
         }
         if (y[0]->level < 1) { rc = ORC_ELEVEL; goto done; }
         /* ---- auxiliary thread (Alg 2) ---- */
-        /* step 1 + C15: S = relin(sum_c tensor(y_c, y_c)) with its rescale (C8) */
+        /* step 1 + C15: S = relin(sum_c tensor(y_c, y_c)) with its rescale (C8);
+         * G27: S = relin(sum_c tensor(w_c, y_c)), w_c = y_c^2 */
         orc_ct *acc = NULL;
+        w = d->variant == 3 ? calloc(m, sizeof(orc_ct *)) : NULL;
         for (int c = 0; c < m; c++) {
-            orc_ct *t = orc_op_tensor(P, y[c], y[c]);
+            if (w) w[c] = orc_op_mult(P, K, y[c], y[c]);
+            orc_ct *t = w ? orc_op_tensor(P, w[c], y[c]) : orc_op_tensor(P, y[c], y[c]);
             if (!acc) acc = t;
             else { orc_ct *s2 = orc_op_add(P, acc, t); orc_ct_release(acc); orc_ct_release(t); acc = s2; }
         }
@@ -157,7 +165,7 @@ int orc_softmax(const orc_params *P, const orc_keys *K, const orc_softmax_desc *
          * same bootstrapping error (a common factor the next normalisation
          * absorbs) instead of an independent one per slot */
         if (lj->level - 1 < main_level && d->bts) {
-            double bound = d->variant == 2 ? 1.1 / ip->a : (d->variant == 1 && j > 1) ? 1.5 : 1.1 / sqrt(ip->a);
+            double bound = d->variant >= 2 ? 1.1 / ip->a : (d->variant == 1 && j > 1) ? 1.5 : 1.1 / sqrt(ip->a);
             if ((rc = bts_or_fail(P, K, d, &lj, bound))) goto done;
         }
         /* step 7: mask block 0 */
@@ -184,9 +192,13 @@ int orc_softmax(const orc_params *P, const orc_keys *K, const orc_softmax_desc *
                 swap_in(&y[c], orc_op_mult(P, K, z, z));          /* Alg 1 line 5 */
                 orc_ct_release(z);
             } else if (d->variant == 2) {
-                orc_ct *w = orc_op_mult(P, K, y[c], y[c]);        /* square ...      */
-                swap_in(&y[c], orc_op_mult(P, K, lam, w));        /* ... and normalize */
-                orc_ct_release(w);
+                orc_ct *w2 = orc_op_mult(P, K, y[c], y[c]);       /* square ...      */
+                swap_in(&y[c], orc_op_mult(P, K, lam, w2));       /* ... and normalize */
+                orc_ct_release(w2);
+            } else if (d->variant == 3) {
+                orc_ct *y3 = orc_op_mult(P, K, w[c], y[c]);       /* cube ...        */
+                swap_in(&y[c], orc_op_mult(P, K, lam, y3));       /* ... and normalize */
+                orc_ct_release(y3);
             } else {
                 orc_ct *z = orc_op_mult(P, K, lam, y0[c]);       /* Alg B line 6 */
                 for (int s = 0; s < j; s++) {                     /* Alg B line 7 */
@@ -198,9 +210,18 @@ int orc_softmax(const orc_params *P, const orc_keys *K, const orc_softmax_desc *
                 swap_in(&y[c], z);
             }
         }
+        if (w) {
+            for (int c = 0; c < m; c++) orc_ct_release(w[c]);
+            free(w);
+            w = NULL;
+        }
     }
     for (int c = 0; c < m; c++) { out[c] = y[c]; y[c] = NULL; }
 done:
+    if (w) {
+        for (int c = 0; c < m; c++) orc_ct_release(w[c]);
+        free(w);
+    }
     for (int c = 0; c < m; c++) { orc_ct_release(y0[c]); orc_ct_release(y[c]); }
     free(y0); free(y); free(mask);
     orc_ct_release(lam); orc_ct_release(S); orc_ct_release(lj);

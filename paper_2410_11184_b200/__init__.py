@@ -301,8 +301,9 @@ def bootstrap(keys: Keys, bts: Bts, ct: Ciphertext, bound=1.0, stream=None) -> C
 
 
 def variant_code(variant):
-    """"A" / 0: Alg 1; "B" / 1: version B; "S" / 2: square-and-normalize (G26)."""
-    codes = {"A": 0, "B": 1, "S": 2, 0: 0, 1: 1, 2: 2}
+    """"A" / 0: Alg 1; "B" / 1: version B; "S" / 2: square-and-normalize (G26);
+    "T3" / 3: cube-and-normalize (App. C, G27)."""
+    codes = {"A": 0, "B": 1, "S": 2, "T3": 3, 0: 0, 1: 1, 2: 2, 3: 3}
     if variant not in codes:
         raise ValueError(f"unknown Softmax variant {variant!r}")
     return codes[variant]

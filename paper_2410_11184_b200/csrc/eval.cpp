@@ -636,6 +636,21 @@ CtP ev_tensor_sum(const hs_ct *a, cudaStream_t st)
     return r;
 }
 
+// sum_b a_b (x) c_b over the members of two batches (C15 with distinct
+// operands; the higher-level operand is brought down as in every product)
+CtP ev_tensor_sum2(const hs_ct *a, const hs_ct *b, cudaStream_t st)
+{
+    if (a->ncomp != 2 || b->ncomp != 2 || a->batch != b->batch)
+        throw HsError(HS_EINVAL, "tensor_sum2 needs two degree-1 batches of one size");
+    CtP ta, tb;
+    const hs_ct *ra, *rb;
+    match(a, b, ta, tb, ra, rb, st);
+    CtP r = ct_new(a->ctx, ra->level, 3, st, 1);
+    k_tensor_sum2(a->ctx, ra->d, rb->d, r->d, a->batch, ra->level + 1, st);
+    a->ctx->ledger[HS_LG_TENSOR] += a->batch;
+    return r;
+}
+
 CtP ev_relin(const hs_keys *K, const hs_ct *d, cudaStream_t st)
 {
     const SwKey *rk = K->find(0);

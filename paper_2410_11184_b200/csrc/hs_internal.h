@@ -233,6 +233,7 @@ void k_lin_comb(hs_ctx *c, const u64 *const *a, const int *a_rl, const u64 *cons
                 int rows, int nl, int o_rl, bool accumulate, cudaStream_t st);
 void k_tensor_b(hs_ctx *c, const u64 *a, const u64 *b, u64 *o, int B, int nl, int b_batch, cudaStream_t st);
 void k_tensor_sum(hs_ctx *c, const u64 *a, u64 *o, int B, int nl, cudaStream_t st);
+void k_tensor_sum2(hs_ctx *c, const u64 *a, const u64 *b, u64 *o, int B, int nl, cudaStream_t st);
 void k_ks_inner_b(hs_ctx *c, const u64 *d, size_t d_stride, const u64 *ext, const size_t *off, const int *nd,
                   const u64 *key, u64 *acc, int level, int beta, int B, cudaStream_t st, const u64 *dadd = nullptr,
                   size_t dadd_stride = 0);
@@ -266,7 +267,8 @@ CtP ct_drop(const hs_ct *a, int level, cudaStream_t st);
 CtP ct_gather(const hs_ct *const *cts, int n, cudaStream_t st);        // n single cts -> one batch
 CtP ct_view(const hs_ct *a, int b);
 CtP ct_slice(const hs_ct *a, int b, cudaStream_t st);                  // ciphertext b of a batch
-CtP ev_tensor_sum(const hs_ct *a, cudaStream_t st);                    // sum_b tensor(a_b, a_b)
+CtP ev_tensor_sum(const hs_ct *a, cudaStream_t st);                     // sum_b tensor(a_b, a_b)
+CtP ev_tensor_sum2(const hs_ct *a, const hs_ct *b, cudaStream_t st);    // sum_b tensor(a_b, b_b)
 void ev_keyswitch_b(const hs_keys *K, const SwKey *key, int level, int B, const u64 *d, size_t d_stride, u64 *out,
                     size_t out_stride, const u64 *add, size_t add_stride, int add_comps, cudaStream_t st);
 CtP ev_add(const hs_ct *a, const hs_ct *b, bool sub, cudaStream_t st);

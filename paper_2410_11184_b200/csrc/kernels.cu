@@ -1611,6 +1611,35 @@ void k_tensor_sum(hs_ctx *c, const u64 *a, u64 *o, int B, int nl, cudaStream_t s
     count_kernel(c);
 }
 
+__global__ void tensor_sum2_kernel(const u64 *a, const u64 *c, u64 *o, int N, int nl, int B)
+{
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= N) return;
+    int l = blockIdx.y;
+    const PrimeK k = c_pk[l];
+    size_t s = (size_t)nl * N, x = (size_t)l * N + t;
+    u64 d0 = 0, d1 = 0, d2 = 0;
+    for (int b = 0; b < B; b++) {
+        const u64 *A = a + (size_t)b * 2 * s, *Cc = c + (size_t)b * 2 * s;
+        u64 a0 = A[x], a1 = A[s + x], c0 = Cc[x], c1 = Cc[s + x];
+        d0 = d_add(d0, d_mulmod(a0, c0, k), k.q);
+        d1 = d_add(d1, d_add(d_mulmod(a0, c1, k), d_mulmod(a1, c0, k), k.q), k.q);
+        d2 = d_add(d2, d_mulmod(a1, c1, k), k.q);
+    }
+    o[x] = d0;
+    o[s + x] = d1;
+    o[2 * s + x] = d2;
+}
+
+void k_tensor_sum2(hs_ctx *c, const u64 *a, const u64 *b, u64 *o, int B, int nl, cudaStream_t st)
+{
+    KTimer _kt(c, KID_TENSOR, (double)(4 * B + 3) * nl * c->P->n * 8, st);
+    int N = c->P->n;
+    tensor_sum2_kernel<<<dim3((N + 255) / 256, nl), 256, 0, st>>>(a, b, o, N, nl, B);
+    HS_CHECK_LAUNCH();
+    count_kernel(c);
+}
+
 // batched key-switch inner product.  d: B polys with stride d_stride words;
 // ext digit j of ciphertext b: ext + off[j] + (b * nd[j] + g') * N;
 // acc: [B][2][ntg][N].  Each thread keeps BT ciphertexts' accumulators so

@@ -5,6 +5,8 @@
 //   version B                    PAPER.md 168-181 [sec 4.3], exponent -1/2^j (G4)
 //   square-and-normalize         PAPER.md 757-765 [sec 3.3, remark], variant 2:
 //                                mu_j = (sum y^2)^-1, y <- mu_j y^2 (G26)
+//   t-th power, t = 3            PAPER.md 1645-1663 [App. C], variant 3:
+//                                mu_j = (sum y^3)^-1, y <- mu_j y^3 (G27)
 //   one / many ciphertexts       PAPER.md 94-131 [sec 4.1-4.2]
 //   shared aux sum               DESIGN.md C15 / G6: sum_c tensor(y_c, y_c)
 //                                exactly mod q, ONE relin + rescale
@@ -58,11 +60,12 @@ hs_status softmax_run(hs_ctx *c, const hs_keys *K, const hs_softmax_desc *d, con
     const hs_params *P = c->P;
     const int N0 = P->n / 2;
     const int m = d->m, n = d->n, world = d->world < 1 ? 1 : d->world;
-    if (m < 1 || n < 1 || n % m || d->k < 1 || !d->exp_poly || !d->inv_poly || d->variant < 0 || d->variant > 2 ||
+    if (m < 1 || n < 1 || n % m || d->k < 1 || !d->exp_poly || !d->inv_poly || d->variant < 0 || d->variant > 3 ||
         d->newton < 0 || (d->newton > 0 && d->variant != 0))
         throw HsError(HS_EINVAL, "softmax: bad descriptor");
-    // Alg 1 and square-and-normalize share the schedule (variant 0 / 2)
+    // Alg 1, square-and-normalize and cube-and-normalize share the schedule
     const bool alg1 = d->variant != 1;
+    const int main_need = d->variant == 3 ? 3 : 2;  // levels of the main update
     if (m % world || (size_t)(m / world) != m_local) throw HsError(HS_EINVAL, "softmax: m_local != m / world");
     if (d->comm && comm_world(d->comm) != world)
         throw HsError(HS_EINVAL, "softmax: communicator size != world");
@@ -90,7 +93,7 @@ hs_status softmax_run(hs_ctx *c, const hs_keys *K, const hs_softmax_desc *d, con
     for (int j = 1; j <= d->k; j++) {
         const hs_poly *ip = &d->inv_poly[j - 1];
         // G12 (c): Alg 1 main thread needs 1 (aux square) + 2 levels
-        if (alg1 && y->level < 2) {
+        if (alg1 && y->level < main_need) {
             if (!d->bts) level_error("main thread needs bootstrapping (not available)");
             std::vector<CtP> parts(ml);
             std::vector<const hs_ct *> ptrs(ml);
@@ -103,7 +106,9 @@ hs_status softmax_run(hs_ctx *c, const hs_keys *K, const hs_softmax_desc *d, con
         }
         if (y->level < 1) level_error("main thread out of levels");
         // ---- auxiliary thread: S = relin(sum tensor(y, y)) -> rescale (C15)
-        CtP acc = ev_tensor_sum(y.get(), st);
+        // G27: S = relin(sum_c tensor(w_c, y_c)) with w_c = y_c^2 (kept for the main update)
+        CtP w = d->variant == 3 ? ev_mult(K, y.get(), y.get(), st) : CtP();
+        CtP acc = w ? ev_tensor_sum2(w.get(), y.get(), st) : ev_tensor_sum(y.get(), st);
         if (world > 1 || d->comm) {
             const size_t words = acc->limbs() * P->n;
             DBuf gathered(words * world, st);
@@ -160,7 +165,7 @@ hs_status softmax_run(hs_ctx *c, const hs_keys *K, const hs_softmax_desc *d, con
         // normalisation) instead of an independent one per slot
         if (lj->level - 1 < main_level && d->bts) {
             const double bound =
-                d->variant == 2 ? 1.1 / ip->a : (d->variant == 1 && j > 1) ? 1.5 : 1.1 / sqrt(ip->a);
+                d->variant >= 2 ? 1.1 / ip->a : (d->variant == 1 && j > 1) ? 1.5 : 1.1 / sqrt(ip->a);
             lj = ev_bootstrap(K, d->bts, lj.get(), bound, st);
         }
         if (lj->level < 1) level_error("no level for the mask");
@@ -186,8 +191,11 @@ hs_status softmax_run(hs_ctx *c, const hs_keys *K, const hs_softmax_desc *d, con
             }
             y = ev_mult(K, z.get(), z.get(), st);
         } else if (d->variant == 2) {
-            CtP w = ev_mult(K, y.get(), y.get(), st);
-            y = ev_mult(K, lam.get(), w.get(), st);
+            CtP w2 = ev_mult(K, y.get(), y.get(), st);
+            y = ev_mult(K, lam.get(), w2.get(), st);
+        } else if (d->variant == 3) {
+            CtP y3 = ev_mult(K, w.get(), y.get(), st);
+            y = ev_mult(K, lam.get(), y3.get(), st);
         } else {
             CtP z = ev_mult(K, lam.get(), y0.get(), st);
             for (int s = 0; s < j; s++) {

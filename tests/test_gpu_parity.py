@@ -485,3 +485,34 @@ def test_native_comm_single_rank(tables):
         for a, b in zip(plan.run(), ref):
             assert (a.words() == b.words()).all()
     del plan
+
+
+def test_softmax_cube_parity(tables):
+    """G27 cube-and-normalize (t = 3, PAPER.md 1645-1663) on TOY12D, n = 4,
+    two ciphertexts: words equal to the oracle's, accuracy 2^-15."""
+    hs = _hs()
+    tab = tables["toy_n4_M4_k2_T3"]
+    cfg = tab["config"]
+    n, M, k, m = cfg["n"], cfg["M"], cfg["k"], 2
+    pre = W.preset("TOY12D")
+    P, PO = hs.Params.from_preset(pre), O.Params.from_preset(pre)
+    gal = O.softmax_rotation_galois(PO, n, m)
+    ctx = hs.Context(P, 0)
+    K, KO = hs.Keys(ctx, 21, pre["h"], galois=gal), O.Keys(PO, 21, pre["h"], galois=gal)
+    L = (P.n // 2) * m // n
+    x = W.softmax_inputs(L, n, M, seed=W.derive_seed("x", "cube-gpu"))
+    slots = P.pack(x, m)
+    top = len(pre["q_bits"]) - 1
+    g_in, o_in = [], []
+    for c in range(m):
+        pt = P.encode(slots[c], scale=P.scale(top), level=top)
+        g_in.append(hs.encrypt(K, pt, top, 13, c))
+        o_in.append(O.encrypt(PO, KO, pt, top, 13, c))
+    g_out = hs.softmax_many_ctxt(K, g_in, n, m, k, "T3", tab["exp"], tab["inv"])
+    o_out = O.softmax(PO, KO, o_in, n, k, "T3", tab["exp"], tab["inv"])
+    for g, o in zip(g_out, o_out):
+        same(g, o)
+    y = P.unpack(np.stack([hs.decrypt_decode(K, c).real for c in g_out]), L, n)
+    ref = np.exp(x - x.max(1, keepdims=True))
+    ref /= ref.sum(1, keepdims=True)
+    assert np.abs(y - ref).max() < 2.0 ** -15

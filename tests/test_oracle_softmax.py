@@ -98,12 +98,13 @@ def test_poly_tables_accuracy(tables):
         e = t["exp"]
         xs = np.linspace(e["a"], e["b"], 20001)
         k = t["config"]["k"]
-        err = np.abs(Ch.chebval((2 * xs - e["a"] - e["b"]) / (e["b"] - e["a"]), e["coeffs"]) - np.exp(xs / 2 ** k))
+        tpow = 3 if t["config"]["variant"] == "T3" else 2
+        err = np.abs(Ch.chebval((2 * xs - e["a"] - e["b"]) / (e["b"] - e["a"]), e["coeffs"]) - np.exp(xs / tpow ** k))
         assert err.max() <= e["max_err"] * 1.05 + 1e-15
         assert len(e["coeffs"]) - 1 == t["config"]["deg_exp"]
         for j, p in enumerate(t["inv"], start=1):
             var = t["config"]["variant"]
-            pw = 0.5 if var == "A" else 1.0 if var == "S" else 0.5 ** j
+            pw = 0.5 if var == "A" else 1.0 if var in ("S", "T3") else 0.5 ** j
             xs = np.linspace(p["a"], p["b"], 20001)
             v = Ch.chebval((2 * xs - p["a"] - p["b"]) / (p["b"] - p["a"]), p["coeffs"])
             werr = np.abs(v * xs ** pw - 1)
@@ -206,3 +207,40 @@ def test_oracle_rejects_newton_with_version_b(tables):
     t["inv"][-1]["newton"] = 2
     with pytest.raises(RuntimeError, match="rc=1"):
         _toy_run({"ntB": t}, "config1", 2, 256, "B", "ntB")
+
+
+def cube_normalize_float(x, k):
+    """PAPER.md 1645-1663 (G27), t = 3: y <- y^3 / sum y^3, k times, from exp(x/3^k)."""
+    y = np.exp(x / 3.0 ** k)
+    for _ in range(k):
+        w = y ** 3
+        y = w / w.sum(-1, keepdims=True)
+    return y
+
+
+@pytest.mark.parametrize("M,n,k", [(4, 4, 2), (128, 128, 4)])
+def test_cube_and_normalize_exact_in_float64(M, n, k):
+    x = W.softmax_inputs(64, n, M, seed=M + 3 * n)
+    assert np.abs(cube_normalize_float(x, k) - softmax64(x)).max() < 1e-13
+
+
+def cube_toy_run(tables):
+    tab = tables["toy_n4_M4_k2_T3"]
+    cfg = tab["config"]
+    n, M, k, m = cfg["n"], cfg["M"], cfg["k"], 2
+    P = O.Params.from_preset(W.preset("TOY12D"))
+    K = O.Keys(P, W.derive_seed("keys", "cube"), 192, galois=O.softmax_rotation_galois(P, n, m))
+    L = (P.n // 2) * m // n
+    x = W.softmax_inputs(L, n, M, seed=W.derive_seed("x", "cube"))
+    slots = O.pack(x, P.n // 2, m)
+    top = P.n_q - 1
+    cts = [O.encrypt(P, K, P.encode(slots[c], scale=P.scale(top), level=top), top, 11, c) for c in range(m)]
+    out = O.softmax(P, K, cts, n, k, "T3", tab["exp"], tab["inv"])
+    dec = np.stack([O.decrypt_decode(P, K, c).real for c in out])
+    return x, O.unpack(dec, L, n)
+
+
+def test_oracle_cube_and_normalize_toy(tables):
+    """G27 on the toy ring: encrypted cube-and-normalize within 2^-15."""
+    x, y = cube_toy_run(tables)
+    assert np.abs(y - softmax64(x)).max() < 2.0 ** -15

@@ -87,10 +87,10 @@ def cheb_eval(coeffs, a, b, x):
     return Ch.chebval(u, coeffs)
 
 
-def make_exp(M, k, deg):
-    f = lambda x: np.exp(x / 2.0 ** k)
+def make_exp(M, k, deg, t=2):
+    f = lambda x: np.exp(x / float(t) ** k)
     c, e = remez(f, lambda x: np.ones_like(x), -float(M), 0.0, deg)
-    return dict(func=f"exp(x/2^{k})", a=-float(M), b=0.0, coeffs=[float(v) for v in c], weight="abs",
+    return dict(func=f"exp(x/{t}^{k})", a=-float(M), b=0.0, coeffs=[float(v) for v in c], weight="abs",
                 max_err=float(e), log2_err=float(math.log2(e)))
 
 
@@ -104,6 +104,8 @@ def make_invpow(p, a, b, deg):
 
 
 def softmax_tables(n, M, k, variant, deg_exp, deg_first, deg_mid, deg_last, guard=0.02, alpha=None, newton=0):
+    if variant == "T3":
+        return power_tables(n, M, k, 3, deg_exp, deg_first, deg_mid, deg_last, guard)
     """Per-iteration polynomial list for one (n, M, k, variant) configuration.
 
     First interval  [n e^{-M/2^(k-1)} (1-guard), n (1+guard)]   (PAPER.md 1001-1002)
@@ -144,6 +146,30 @@ def softmax_tables(n, M, k, variant, deg_exp, deg_first, deg_mid, deg_last, guar
     return polys
 
 
+def power_tables(n, M, k, t, deg_exp, deg_first, deg_mid, deg_last, guard=0.02):
+    """t-th power normalization (PAPER.md 1645-1663 [App. C], G27): y0 =
+    exp(x/t^k); mu_j = P_j(sum y^t) ~ (sum y^t)^-1 (weighted minimax of x^-1);
+    first interval [n e^(-t M / t^k), n], then, with sum y within alpha of 1,
+    [(1-alpha)^t / n^(t-1), (1+alpha)^t] (Hoelder, P:1655-1657)."""
+    polys = {"exp": make_exp(M, k, deg_exp, t)}
+    inv, prev_alpha = [], None
+    for j in range(1, k + 1):
+        if j == 1:
+            a = n * math.exp(-t * M / float(t) ** k) * (1 - guard)
+            b = n * (1 + guard)
+            deg = deg_first if k > 1 else deg_last
+        else:
+            al = prev_alpha * (1 + guard) + guard / 4
+            a, b = (1 - al) ** t / n ** (t - 1), (1 + al) ** t
+            deg = deg_last if j == k else deg_mid
+        pol = make_invpow(1.0, a, b, deg)
+        prev_alpha = pol["max_err"]
+        pol["alpha_out"] = prev_alpha
+        inv.append(pol)
+    polys["inv"] = inv
+    return polys
+
+
 CONFIGS = {
     # config 1 (TOY12): n = 16, M = 2, k = 1 (forced), Alg 1
     "toy_n16_M2_k1_A": dict(n=16, M=2, k=1, variant="A", deg_exp=7, deg_first=15, deg_mid=15, deg_last=15),
@@ -155,6 +181,8 @@ CONFIGS = {
                                newton=2),
     # square-and-normalize (PAPER.md 757-765, G26) at the k = 2 toy shape
     "toy_n16_M4_k2_S": dict(n=16, M=4, k=2, variant="S", deg_exp=7, deg_first=15, deg_mid=15, deg_last=31),
+    # cube-and-normalize (t = 3, App. C, G27) at the toy shape: x/3^k, k = 2
+    "toy_n4_M4_k2_T3": dict(n=4, M=4, k=2, variant="T3", deg_exp=7, deg_first=15, deg_mid=31, deg_last=31),
     # P16 configs 2-4 (n=256/128, M=128, k=5)
     "p16_n256_M128_k5_A": dict(n=256, M=128, k=5, variant="A", deg_exp=15, deg_first=63, deg_mid=31, deg_last=127),
     "p16_n256_M128_k5_B": dict(n=256, M=128, k=5, variant="B", deg_exp=15, deg_first=63, deg_mid=31, deg_last=127),

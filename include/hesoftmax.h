@@ -278,6 +278,51 @@ hs_status hs_softmax_one_ctxt(hs_ctx *c, const hs_keys *k, const hs_softmax_desc
 hs_status hs_softmax_many_ctxt(hs_ctx *c, const hs_keys *k, const hs_softmax_desc *d, const hs_ct *const *in,
                                size_t m_local, void *stream, hs_ct **out);
 
+/* ------------------------------------------------------------ schedule planner */
+/* The bootstrap placement of the paper is prose (PAPER.md 429-440
+ * [sec 5.1.3]; G12) and its cost lever is where the bootstraps fall
+ * (PAPER.md 285-295, 608-614 [sec 5.2.2]: ~80 % of Alg 1's time, 27 % of
+ * version B's at 64 ciphertexts).  hs_softmax_schedule runs the Softmax
+ * driver's schedule -- the SAME code hs_softmax_many_ctxt runs, instantiated
+ * with a level-only executor -- on the host, without a device or keys, and
+ * reports where it bootstraps and what it costs.  Arguments: p the parameter
+ * set; d a Softmax descriptor (d->bts, exchange and comm are ignored; world
+ * and rank are read); in_level the inputs' level; m_local this rank's
+ * ciphertexts (m / world); bts_out_level the level a bootstrap returns
+ * (hs_bts_desc.out_level; < 0 = no bootstrapping).  Host only, thread-safe.
+ * HS_ELEVEL if the schedule does not fit (as the device run would return),
+ * HS_EINVAL on a bad descriptor.
+ *
+ * cost: a model in units of ONE HMult+relin+rescale of one ciphertext at
+ * level 12 of P16: every key switch at level l costs
+ * its limb-NTT count relative to level 12, a batch of b members costs
+ * b / (1 + 0.1 log2 b) members (measured batch-64 gain 1.6x), a Chebyshev
+ * polynomial of degree d costs 2 sqrt(d+1) + log2(d+1) products (PAPER.md
+ * 330-336) and a bootstrap HS_SCHED_BTS_COST (measured 22.6 ms per bootstrap vs
+ * 0.228 ms per HMult at level 12 on one B200, profiles/r01_bench_full.json). */
+#define HS_SCHED_BTS_COST 99.0
+typedef struct {
+    int out_level;   /* level of the Softmax output                               */
+    int bts_main;    /* main-thread bootstraps (one per ciphertext of this rank)   */
+    int bts_aux;     /* bootstraps of the auxiliary ciphertext                    */
+    int hmult;       /* driver-level ciphertext products, batch members counted
+                        (polynomial-internal products are in `cost` only)          */
+    int rotations;   /* rotate-and-sum rotations, batch members counted            */
+    int poly_evals;  /* Chebyshev evaluations                                      */
+    int exchanges;   /* aux-sum all-gathers (world > 1)                            */
+    double cost;     /* modelled cost (see above)                                  */
+} hs_softmax_sched;
+hs_status hs_softmax_schedule(const hs_params *p, const hs_softmax_desc *d, int in_level, size_t m_local,
+                              int bts_out_level, hs_softmax_sched *out);
+/* Automatic variant selection (Alg 1 vs version B vs the normalisation
+ * variants, PAPER.md 585-614 tab:SMmany): plans each of the n candidate
+ * descriptors (each with its own variant, k and polynomials) and returns in
+ * *best the index of the cheapest one that fits; sched (n entries, nullable)
+ * receives every plan, cost = HUGE_VAL for one that does not fit.
+ * HS_ELEVEL if none fits, HS_EINVAL on a bad candidate or n == 0. */
+hs_status hs_softmax_choose(const hs_params *p, const hs_softmax_desc *cands, size_t n, int in_level,
+                            size_t m_local, int bts_out_level, size_t *best, hs_softmax_sched *sched);
+
 /* ------------------------------------------------------------ replayable plans (CUDA graphs) */
 /* A plan is one hs_softmax_many_ctxt call (world == 1) captured into a CUDA
  * graph: every kernel of the Softmax runs again at each hs_plan_run, with no

@@ -361,6 +361,39 @@ def softmax_one_ctxt(keys: Keys, ct: Ciphertext, n, k, variant, exp_poly, inv_po
     return Ciphertext(keys.ctx, out)
 
 
+def _sched_dict(s):
+    return {f: getattr(s, f) for f, _ in L.SoftmaxSched._fields_}
+
+
+def softmax_schedule(params: Params, n, m, k, variant, exp_poly, inv_polys, in_level, m_local=None, world=1,
+                     bts_out_level=-1) -> dict:
+    """hs_softmax_schedule: the Softmax driver's schedule planned on the host
+    (no device, no keys): output level, main / aux bootstraps, products,
+    rotations and the modelled cost."""
+    d, keep = _softmax_desc(n, m, k, variant, exp_poly, inv_polys, world, 0)
+    s = L.SoftmaxSched()
+    ml = m // world if m_local is None else m_local
+    check(L.hs_softmax_schedule(params.ptr, C.byref(d), int(in_level), ml, int(bts_out_level), C.byref(s)))
+    return _sched_dict(s)
+
+
+def softmax_choose(params: Params, candidates, n, m, in_level, world=1, bts_out_level=-1):
+    """hs_softmax_choose: automatic variant selection.  candidates: list of
+    dicts {k, variant, exp, inv} (a poly_tables.json entry plus its k and
+    variant).  Returns (index of the cheapest plan that fits, [plans])."""
+    descs = (L.SoftmaxDesc * len(candidates))()
+    keep = []
+    for i, c in enumerate(candidates):
+        d, kp = _softmax_desc(n, m, c["k"], c["variant"], c["exp"], c["inv"], world, 0)
+        descs[i] = d
+        keep.append(kp)
+    sched = (L.SoftmaxSched * len(candidates))()
+    best = C.c_size_t()
+    check(L.hs_softmax_choose(params.ptr, descs, len(candidates), int(in_level), m // world, int(bts_out_level),
+                              C.byref(best), sched))
+    return best.value, [_sched_dict(s) for s in sched]
+
+
 class Plan:
     """hs_softmax_plan_create: one single-GPU Softmax captured as a CUDA graph,
     bound to the input ciphertexts `cts` (re-read at every run); outputs are

@@ -57,6 +57,11 @@ class SoftmaxDesc(C.Structure):
                 ("newton", C.c_int), ("comm", vp)]
 
 
+class SoftmaxSched(C.Structure):
+    _fields_ = [("out_level", C.c_int), ("bts_main", C.c_int), ("bts_aux", C.c_int), ("hmult", C.c_int),
+                ("rotations", C.c_int), ("poly_evals", C.c_int), ("exchanges", C.c_int), ("cost", C.c_double)]
+
+
 class BtsDesc(C.Structure):
     _fields_ = [("K", C.c_int), ("r", C.c_int), ("cos_poly", C.POINTER(Poly)), ("out_level", C.c_int),
                 ("n_cts", C.c_int), ("n_stc", C.c_int), ("arcsine", C.c_int)]
@@ -120,6 +125,10 @@ hs_softmax_one_ctxt = _sig("hs_softmax_one_ctxt", C.c_int,
                            [vp, vp, C.POINTER(SoftmaxDesc), vp, vp, C.POINTER(vp)])
 hs_softmax_many_ctxt = _sig("hs_softmax_many_ctxt", C.c_int,
                             [vp, vp, C.POINTER(SoftmaxDesc), C.POINTER(vp), C.c_size_t, vp, C.POINTER(vp)])
+hs_softmax_schedule = _sig("hs_softmax_schedule", C.c_int, [vp, C.POINTER(SoftmaxDesc), C.c_int, C.c_size_t,
+                                                            C.c_int, C.POINTER(SoftmaxSched)])
+hs_softmax_choose = _sig("hs_softmax_choose", C.c_int, [vp, C.POINTER(SoftmaxDesc), C.c_size_t, C.c_int, C.c_size_t,
+                                                        C.c_int, C.POINTER(C.c_size_t), C.POINTER(SoftmaxSched)])
 hs_comm_unique_id = _sig("hs_comm_unique_id", C.c_int, [C.POINTER(C.c_uint8)])
 hs_comm_init = _sig("hs_comm_init", C.c_int, [vp, C.c_int, C.c_int, C.POINTER(C.c_uint8), C.POINTER(vp)])
 hs_comm_destroy = _sig("hs_comm_destroy", None, [vp])

@@ -425,6 +425,41 @@ hs_status hs_softmax_many_ctxt(hs_ctx *c, const hs_keys *k, const hs_softmax_des
     HS_CATCH
 }
 
+hs_status hs_softmax_schedule(const hs_params *p, const hs_softmax_desc *d, int in_level, size_t m_local,
+                              int bts_out_level, hs_softmax_sched *out)
+{
+    HS_TRY
+    if (!p || !d || !out) throw HsError(HS_EINVAL, "NULL argument");
+    softmax_schedule(p, d, in_level, m_local, bts_out_level, out);
+    return HS_OK;
+    HS_CATCH
+}
+
+hs_status hs_softmax_choose(const hs_params *p, const hs_softmax_desc *cands, size_t n, int in_level,
+                            size_t m_local, int bts_out_level, size_t *best, hs_softmax_sched *sched)
+{
+    HS_TRY
+    if (!p || !cands || !best || n == 0) throw HsError(HS_EINVAL, "NULL argument or no candidate");
+    double best_cost = HUGE_VAL;
+    size_t bi = n;
+    for (size_t i = 0; i < n; i++) {
+        hs_softmax_sched s{};
+        try {
+            softmax_schedule(p, &cands[i], in_level, m_local, bts_out_level, &s);
+        } catch (const HsError &e) {
+            if (e.code != HS_ELEVEL) throw;
+            s = hs_softmax_sched{};
+            s.cost = HUGE_VAL;
+        }
+        if (sched) sched[i] = s;
+        if (s.cost < best_cost) best_cost = s.cost, bi = i;
+    }
+    if (bi == n) throw HsError(HS_ELEVEL, "softmax_choose: no candidate fits the modulus chain");
+    *best = bi;
+    return HS_OK;
+    HS_CATCH
+}
+
 }  // extern "C"
 
 extern "C" {

@@ -326,3 +326,5 @@ int comm_world(const hs_comm *c);
 void comm_all_gather(const hs_comm *c, const u64 *partial, u64 *gathered, size_t words, cudaStream_t st);
 hs_status softmax_run(hs_ctx *c, const hs_keys *K, const hs_softmax_desc *d, const hs_ct *const *in,
                       size_t m_local, cudaStream_t st, hs_ct **out);
+void softmax_schedule(const hs_params *P, const hs_softmax_desc *d, int in_level, size_t m_local, int bts_out_level,
+                      hs_softmax_sched *s);

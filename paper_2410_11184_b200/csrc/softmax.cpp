@@ -31,33 +31,174 @@ namespace {
 
 int poly_cost(const hs_poly *p) { return cheb_depth(p->deg) + ((p->a == -1.0 && p->b == 1.0) ? 0 : 1); }
 
-void rot_sum(const hs_keys *K, CtP &S, int nb, int stride, int sign, cudaStream_t st)
+[[noreturn]] void level_error(const char *what) { throw HsError(HS_ELEVEL, std::string("softmax: ") + what); }
+
+// ------------------------------------------------------------ executors
+// The schedule below (softmax_body) is written ONCE against an executor E:
+// RealEx runs every op on the device; SymEx only tracks levels, batch sizes
+// and op counts (the planner).  Both take every decision
+// from the same level arithmetic, so a plan's bootstrap placement is exactly
+// the one the device run makes.
+
+struct RealEx {
+    typedef hs_ct T;
+    typedef ::CtP Ct;
+    hs_ctx *c;
+    const hs_keys *K;
+    const hs_softmax_desc *d;
+    cudaStream_t st;
+    bool has_bts() const { return d->bts != nullptr; }
+    void check_exchange(int world) const
+    {
+        if (d->comm && comm_world(d->comm) != world)
+            throw HsError(HS_EINVAL, "softmax: communicator size != world");
+        if (world > 1 && !d->exchange && !d->comm)
+            throw HsError(HS_EINVAL, "softmax: world > 1 needs a communicator or an exchange callback");
+    }
+    Ct gather(const T *const *in, int n) { return ct_gather(in, n, st); }
+    Ct copy(const T *x) { return ct_copy(x, st); }
+    Ct cheb(const T *x, const hs_poly *p) { return ev_cheb(K, x, p, st); }
+    Ct mult(const T *a, const T *b) { return ev_mult(K, a, b, st); }
+    Ct mult_const(const T *a, double v, int target) { return ev_mult_const(a, v, target, st); }
+    Ct mult_pt(const T *a, const double *re, int target) { return ev_mult_pt(a, re, nullptr, target, st); }
+    Ct add(const T *a, const T *b, bool sub) { return ev_add(a, b, sub, st); }
+    Ct rotate(const T *a, int r) { return ev_rotate(K, a, r, st); }
+    Ct tensor_sum(const T *y) { return ev_tensor_sum(y, st); }
+    Ct tensor_sum2(const T *w, const T *y) { return ev_tensor_sum2(w, y, st); }
+    Ct relin_rescale(const T *a) { return ev_relin_rescale(K, a, st); }
+    Ct bootstrap(const T *a, double bound) { return ev_bootstrap(K, d->bts, a, bound, st); }
+    // every member of a batch bootstrapped on its own, then re-batched
+    Ct bootstrap_each(const T *y, double bound)
+    {
+        const int b = y->batch;
+        std::vector<Ct> parts(b);
+        std::vector<const hs_ct *> ptrs(b);
+        for (int i = 0; i < b; i++) {
+            Ct one = ct_slice(y, i, st);
+            parts[i] = ev_bootstrap(K, d->bts, one.get(), bound, st);
+            ptrs[i] = parts[i].get();
+        }
+        return ct_gather(ptrs.data(), b, st);
+    }
+    // all-gather of the partial aux sums, added in rank order (exact)
+    void exchange(T *acc, int world)
+    {
+        const size_t words = acc->limbs() * c->P->n;
+        DBuf gathered(words * world, st);
+        if (d->comm) comm_all_gather(d->comm, acc->d, gathered.p, words, st);  // native NCCL
+        else if (d->exchange(d->exchange_user, acc->d, gathered.p, words, st) != 0)
+            throw HsError(HS_ENCCL, "softmax: exchange callback failed");
+        HS_CUDA(cudaMemcpyAsync(acc->d, gathered.p, words * 8, cudaMemcpyDeviceToDevice, st));
+        for (int r = 1; r < world; r++)
+            k_add(c, acc->d, gathered.p + r * words, acc->d, (int)acc->limbs(), acc->level + 1, false, st);
+    }
+};
+
+// A ciphertext of the planner: level, components, batch members.
+struct SymCt {
+    int level, ncomp, batch;
+};
+
+// Level semantics of every op (C8, C9, C11, C12; poly.cpp eval_unit; bts.cpp
+// out_level) plus a cost model in units of ONE HMult+relin+rescale of one
+// ciphertext at level 12.
+struct SymEx {
+    typedef SymCt T;
+    typedef std::unique_ptr<SymCt> Ct;
+    const hs_params *P;
+    int bts_out;  // < 0: no bootstrapping
+    hs_softmax_sched *s;
+    bool has_bts() const { return bts_out >= 0; }
+    void check_exchange(int) const {}
+    static Ct mk(int level, int ncomp, int batch) { return Ct(new SymCt{level, ncomp, batch}); }
+    // limb-NTTs of one key switch at level l (ModUp iNTT + NTT, ModDown iNTT + NTT)
+    double ks_work(int l) const
+    {
+        const int a = P->alpha, nl = l + 1, beta = (nl + a - 1) / a;
+        return (double)beta * (nl + a) + 2.0 * a + 2.0 * nl;
+    }
+    // batched ops amortise keys and launches: 64 members cost ~40 (measured
+    // HMult ops/s at batch 64 vs 1, profiles/r01_bench_full.json)
+    static double beff(int b) { return b / (1.0 + 0.1 * log2((double)b)); }
+    double ks_cost(int l, int b) const { return ks_work(l) / ks_work(12) * beff(b); }
+    Ct gather(const T *const *in, int n) { return mk(in[0]->level, in[0]->ncomp, n); }
+    Ct copy(const T *x) { return mk(x->level, x->ncomp, x->batch); }
+    Ct cheb(const T *x, const hs_poly *p)
+    {
+        const int cost = poly_cost(p);
+        if (x->level < cost) throw HsError(HS_ELEVEL, "polynomial deeper than the remaining levels");
+        // ~2 sqrt(d+1) + log2(d+1) non-scalar products (PAPER.md 330-336) at the mid level
+        const double mults = 2.0 * sqrt(p->deg + 1.0) + log2(p->deg + 1.0);
+        s->poly_evals += 1;
+        s->cost += mults * ks_cost(x->level - cost / 2, x->batch);
+        return mk(x->level - cost, 2, x->batch);
+    }
+    Ct mult(const T *a, const T *b)
+    {
+        const int l = std::min(a->level, b->level);
+        if (l < 1) throw HsError(HS_ELEVEL, "no level left for a product");
+        const int bt = std::max(a->batch, b->batch);
+        s->hmult += bt;
+        s->cost += ks_cost(l, bt);
+        return mk(l - 1, 2, bt);
+    }
+    Ct mult_const(const T *a, double, int target) { return mk(target, a->ncomp, a->batch); }
+    Ct mult_pt(const T *a, const double *, int target) { return mk(target, a->ncomp, a->batch); }
+    Ct add(const T *a, const T *b, bool) { return mk(std::min(a->level, b->level), a->ncomp, std::max(a->batch, b->batch)); }
+    Ct rotate(const T *a, int)
+    {
+        s->rotations += a->batch;
+        s->cost += ks_cost(a->level, a->batch);
+        return mk(a->level, a->ncomp, a->batch);
+    }
+    Ct tensor_sum(const T *y) { return mk(y->level, 3, 1); }
+    Ct tensor_sum2(const T *w, const T *y) { return mk(std::min(w->level, y->level), 3, 1); }
+    Ct relin_rescale(const T *a)
+    {
+        s->cost += ks_cost(a->level, 1);
+        return mk(a->level - 1, 2, 1);
+    }
+    Ct bootstrap(const T *a, double)
+    {
+        s->bts_aux += a->batch;
+        s->cost += HS_SCHED_BTS_COST * a->batch;
+        return mk(bts_out, 2, a->batch);
+    }
+    Ct bootstrap_each(const T *y, double)
+    {
+        s->bts_main += y->batch;
+        s->cost += HS_SCHED_BTS_COST * y->batch;
+        return mk(bts_out, 2, y->batch);
+    }
+    void exchange(T *, int) { s->exchanges += 1; }
+};
+
+template <class E>
+void rot_sum(E &ex, typename E::Ct &S, int nb, int stride, int sign)
 {
     for (int i = 0; (1 << i) < nb; i++) {
-        CtP r = ev_rotate(K, S.get(), sign * stride * (1 << i), st);
-        S = ev_add(S.get(), r.get(), false, st);
+        typename E::Ct r = ex.rotate(S.get(), sign * stride * (1 << i));
+        S = ex.add(S.get(), r.get(), false);
     }
 }
 
-[[noreturn]] void level_error(const char *what) { throw HsError(HS_ELEVEL, std::string("softmax: ") + what); }
-
 // PAPER.md 1313-1316: z1 = (x/2) y; z2 = y y; z3 = (3/2) y; y' = z3 - z1 z2
 // (2 levels; z3 multiplied straight to the level of z1 z2, C12)
-CtP newton_step(const hs_keys *K, const hs_ct *xh, const hs_ct *y, cudaStream_t st)
+template <class E>
+typename E::Ct newton_step(E &ex, const typename E::T *xh, const typename E::T *y)
 {
-    CtP z1 = ev_mult(K, xh, y, st);
-    CtP z2 = ev_mult(K, y, y, st);
-    CtP p = ev_mult(K, z1.get(), z2.get(), st);
-    CtP z3 = ev_mult_const(y, 1.5, p->level, st);
-    return ev_add(z3.get(), p.get(), true, st);
+    typename E::Ct z1 = ex.mult(xh, y);
+    typename E::Ct z2 = ex.mult(y, y);
+    typename E::Ct p = ex.mult(z1.get(), z2.get());
+    typename E::Ct z3 = ex.mult_const(y, 1.5, p->level);
+    return ex.add(z3.get(), p.get(), true);
 }
 
-}  // namespace
-
-hs_status softmax_run(hs_ctx *c, const hs_keys *K, const hs_softmax_desc *d, const hs_ct *const *in,
-                      size_t m_local, cudaStream_t st, hs_ct **out)
+template <class E>
+typename E::Ct softmax_body(E &ex, const hs_params *P, const hs_softmax_desc *d, const typename E::T *const *in,
+                            size_t m_local)
 {
-    const hs_params *P = c->P;
+    typedef typename E::Ct CtP;
     const int N0 = P->n / 2;
     const int m = d->m, n = d->n, world = d->world < 1 ? 1 : d->world;
     if (m < 1 || n < 1 || n % m || d->k < 1 || !d->exp_poly || !d->inv_poly || d->variant < 0 || d->variant > 3 ||
@@ -67,10 +208,7 @@ hs_status softmax_run(hs_ctx *c, const hs_keys *K, const hs_softmax_desc *d, con
     const bool alg1 = d->variant != 1;
     const int main_need = d->variant == 3 ? 3 : 2;  // levels of the main update
     if (m % world || (size_t)(m / world) != m_local) throw HsError(HS_EINVAL, "softmax: m_local != m / world");
-    if (d->comm && comm_world(d->comm) != world)
-        throw HsError(HS_EINVAL, "softmax: communicator size != world");
-    if (world > 1 && !d->exchange && !d->comm)
-        throw HsError(HS_EINVAL, "softmax: world > 1 needs a communicator or an exchange callback");
+    ex.check_exchange(world);
     const int nb = n / m;
     if ((nb & (nb - 1)) || nb > N0) throw HsError(HS_EINVAL, "softmax: n/m must be a power of two <= N0");
     const int stride = N0 / nb;
@@ -84,45 +222,28 @@ hs_status softmax_run(hs_ctx *c, const hs_keys *K, const hs_softmax_desc *d, con
     // the main thread keeps this rank's ml ciphertexts as ONE batch: every op
     // below runs once over all of them (same schedule as per ciphertext)
     if (in[0]->level < poly_cost(d->exp_poly)) level_error("input level too low for exp");
-    CtP xb = ct_gather(in, ml, st);
+    CtP xb = ex.gather(in, ml);
     // y^(0) = exp(x / 2^k)
-    CtP y0 = ev_cheb(K, xb.get(), d->exp_poly, st);
+    CtP y0 = ex.cheb(xb.get(), d->exp_poly);
     xb.reset();
-    CtP y = ct_copy(y0.get(), st);
+    CtP y = ex.copy(y0.get());
     CtP lam;
     for (int j = 1; j <= d->k; j++) {
         const hs_poly *ip = &d->inv_poly[j - 1];
         // G12 (c): Alg 1 main thread needs 1 (aux square) + 2 levels
         if (alg1 && y->level < main_need) {
-            if (!d->bts) level_error("main thread needs bootstrapping (not available)");
-            std::vector<CtP> parts(ml);
-            std::vector<const hs_ct *> ptrs(ml);
-            for (int i = 0; i < ml; i++) {
-                CtP one = ct_slice(y.get(), i, st);
-                parts[i] = ev_bootstrap(K, d->bts, one.get(), 1.0, st);
-                ptrs[i] = parts[i].get();
-            }
-            y = ct_gather(ptrs.data(), ml, st);
+            if (!ex.has_bts()) level_error("main thread needs bootstrapping (not available)");
+            y = ex.bootstrap_each(y.get(), 1.0);
         }
         if (y->level < 1) level_error("main thread out of levels");
         // ---- auxiliary thread: S = relin(sum tensor(y, y)) -> rescale (C15)
         // G27: S = relin(sum_c tensor(w_c, y_c)) with w_c = y_c^2 (kept for the main update)
-        CtP w = d->variant == 3 ? ev_mult(K, y.get(), y.get(), st) : CtP();
-        CtP acc = w ? ev_tensor_sum2(w.get(), y.get(), st) : ev_tensor_sum(y.get(), st);
-        if (world > 1 || d->comm) {
-            const size_t words = acc->limbs() * P->n;
-            DBuf gathered(words * world, st);
-            if (d->comm) comm_all_gather(d->comm, acc->d, gathered.p, words, st);  // native NCCL
-            else if (d->exchange(d->exchange_user, acc->d, gathered.p, words, st) != 0)
-                throw HsError(HS_ENCCL, "softmax: exchange callback failed");
-            // sum in rank order (exact modular addition)
-            HS_CUDA(cudaMemcpyAsync(acc->d, gathered.p, words * 8, cudaMemcpyDeviceToDevice, st));
-            for (int r = 1; r < world; r++)
-                k_add(c, acc->d, gathered.p + r * words, acc->d, (int)acc->limbs(), acc->level + 1, false, st);
-        }
-        CtP S = ev_relin_rescale(K, acc.get(), st);  // C8: one division by P q_l
+        CtP w = d->variant == 3 ? ex.mult(y.get(), y.get()) : CtP();
+        CtP acc = w ? ex.tensor_sum2(w.get(), y.get()) : ex.tensor_sum(y.get());
+        if (world > 1 || d->comm) ex.exchange(acc.get(), world);
+        CtP S = ex.relin_rescale(acc.get());  // C8: one division by P q_l
         acc.reset();
-        rot_sum(K, S, nb, stride, -1, st);
+        rot_sum(ex, S, nb, stride, -1);
         // main level (G12): Alg 1 -- y's level (the 2 levels of the
         // last update at j = k); version B -- the levels its update consumes,
         // j + 2 (k + 1 at j = k), capped by y0's
@@ -137,76 +258,94 @@ hs_status softmax_run(hs_ctx *c, const hs_keys *K, const hs_softmax_desc *d, con
         // G12 (a): bootstrap before the inverse square root when the rest of the
         // aux thread would leave lambda below the main operand's level
         if (S->level - need < main_level) {
-            if (d->bts) S = ev_bootstrap(K, d->bts, S.get(), ip->b, st);
+            if (ex.has_bts()) S = ex.bootstrap(S.get(), ip->b);
             else if (S->level - need < 0) level_error("aux thread needs bootstrapping");
         }
-        CtP lj = ev_cheb(K, S.get(), ip, st);
+        CtP lj = ex.cheb(S.get(), ip);
         if (nt > 0) {
             // G24 (n): bootstrap the seed when the Newton steps and the mask
             // would leave lambda below the main level
             int top = std::min(lj->level, S->level - 1);
-            if (top - 2 * nt - 1 < main_level && d->bts) {
-                lj = ev_bootstrap(K, d->bts, lj.get(), 1.1 / sqrt(ip->a), st);
+            if (top - 2 * nt - 1 < main_level && ex.has_bts()) {
+                lj = ex.bootstrap(lj.get(), 1.1 / sqrt(ip->a));
                 top = std::min(lj->level, S->level - 1);
             }
             if (top - 2 * nt - 1 < 0) level_error("Newton steps out of levels");
-            CtP xh = ev_mult_const(S.get(), 0.5, S->level - 1, st);
-            for (int t = 0; t < nt; t++) lj = newton_step(K, xh.get(), lj.get(), st);
+            CtP xh = ex.mult_const(S.get(), 0.5, S->level - 1);
+            for (int t = 0; t < nt; t++) lj = newton_step(ex, xh.get(), lj.get());
         }
         S.reset();
         // Alg B line 5, taken BEFORE the mask: lambda_j holds its value in every
         // coordinate block (S was summed over all of them), so lambda * lambda_j
         // is the new lambda everywhere
-        if (d->variant == 1 && j > 1) lj = ev_mult(K, lam.get(), lj.get(), st);
+        if (d->variant == 1 && j > 1) lj = ex.mult(lam.get(), lj.get());
         // G12 (b): bootstrap lambda_j (version B: the product) BEFORE the mask
         // when the mask would leave it below the main level -- the broadcast
         // then gives every coordinate of an instance block 0's value, one
         // common bootstrapping error per instance (absorbed by the next
         // normalisation) instead of an independent one per slot
-        if (lj->level - 1 < main_level && d->bts) {
+        if (lj->level - 1 < main_level && ex.has_bts()) {
             const double bound =
                 d->variant >= 2 ? 1.1 / ip->a : (d->variant == 1 && j > 1) ? 1.5 : 1.1 / sqrt(ip->a);
-            lj = ev_bootstrap(K, d->bts, lj.get(), bound, st);
+            lj = ex.bootstrap(lj.get(), bound);
         }
         if (lj->level < 1) level_error("no level for the mask");
-        lj = ev_mult_pt(lj.get(), mask.data(), nullptr, lj->level - 1, st);
-        rot_sum(K, lj, nb, stride, +1, st);
+        lj = ex.mult_pt(lj.get(), mask.data(), lj->level - 1);
+        rot_sum(ex, lj, nb, stride, +1);
         lam = std::move(lj);
         // ---- main thread (lam broadcast against the batch)
         if (lam->level < 1) level_error("lambda out of levels");
         if (d->variant == 0) {
-            CtP z = ev_mult(K, lam.get(), y.get(), st);
+            CtP z = ex.mult(lam.get(), y.get());
             // G12 (c'): bootstrap the normalised z (|z| <= 1 + alpha, larger
             // than y) when its square would leave y below the 2 levels the
             // next iteration needs
-            if (d->bts && j < d->k && z->level - 1 < 2) {
-                std::vector<CtP> parts(ml);
-                std::vector<const hs_ct *> ptrs(ml);
-                for (int i = 0; i < ml; i++) {
-                    CtP one = ct_slice(z.get(), i, st);
-                    parts[i] = ev_bootstrap(K, d->bts, one.get(), 1.1, st);
-                    ptrs[i] = parts[i].get();
-                }
-                z = ct_gather(ptrs.data(), ml, st);
+            if (ex.has_bts() && j < d->k && z->level - 1 < 2) {
+                z = ex.bootstrap_each(z.get(), 1.1);
             }
-            y = ev_mult(K, z.get(), z.get(), st);
+            y = ex.mult(z.get(), z.get());
         } else if (d->variant == 2) {
-            CtP w2 = ev_mult(K, y.get(), y.get(), st);
-            y = ev_mult(K, lam.get(), w2.get(), st);
+            CtP w2 = ex.mult(y.get(), y.get());
+            y = ex.mult(lam.get(), w2.get());
         } else if (d->variant == 3) {
-            CtP y3 = ev_mult(K, w.get(), y.get(), st);
-            y = ev_mult(K, lam.get(), y3.get(), st);
+            CtP y3 = ex.mult(w.get(), y.get());
+            y = ex.mult(lam.get(), y3.get());
         } else {
-            CtP z = ev_mult(K, lam.get(), y0.get(), st);
+            CtP z = ex.mult(lam.get(), y0.get());
             for (int s = 0; s < j; s++) {
                 if (z->level < 1) level_error("version B squaring out of levels");
-                z = ev_mult(K, z.get(), z.get(), st);
+                z = ex.mult(z.get(), z.get());
             }
             y = std::move(z);
         }
     }
+    return y;
+}
+
+}  // namespace
+
+hs_status softmax_run(hs_ctx *c, const hs_keys *K, const hs_softmax_desc *d, const hs_ct *const *in,
+                      size_t m_local, cudaStream_t st, hs_ct **out)
+{
+    RealEx ex{c, K, d, st};
+    CtP y = softmax_body(ex, c->P, d, in, m_local);
+    const int ml = (int)m_local;
     std::vector<CtP> res(ml);
     for (int i = 0; i < ml; i++) res[i] = ct_slice(y.get(), i, st);
     for (int i = 0; i < ml; i++) out[i] = res[i].release();
     return HS_OK;
+}
+
+void softmax_schedule(const hs_params *P, const hs_softmax_desc *d, int in_level, size_t m_local, int bts_out_level,
+                      hs_softmax_sched *s)
+{
+    *s = hs_softmax_sched{};
+    if (m_local < 1 || in_level < 0 || in_level > P->L) throw HsError(HS_EINVAL, "schedule: bad input level / m_local");
+    if (bts_out_level > P->L) throw HsError(HS_EINVAL, "schedule: bootstrap output level above the chain");
+    SymEx ex{P, bts_out_level, s};
+    std::vector<SymCt> cts(m_local, SymCt{in_level, 2, 1});
+    std::vector<const SymCt *> ptrs(m_local);
+    for (size_t i = 0; i < m_local; i++) ptrs[i] = &cts[i];
+    SymEx::Ct y = softmax_body(ex, P, d, ptrs.data(), m_local);
+    s->out_level = y->level;
 }

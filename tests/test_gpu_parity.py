@@ -367,6 +367,11 @@ def test_softmax_bts_parity(toyb, tables, table, m):
     o_out = O.softmax_bts(PO, KO, o_in, n, k, var, tab["exp"], tab["inv"], toyb["BO"])
     # the same bootstrap schedule on both sides (G12)
     assert g_led["bts"] == O.ledger()["bts"]
+    # ... and the host planner's (hs_softmax_schedule)
+    plan_s = hs.softmax_schedule(P, n, m, k, var, tab["exp"], tab["inv"], 12,
+                                 bts_out_level=toyb["pre"]["bts"]["out_level"])
+    assert plan_s["bts_main"] + plan_s["bts_aux"] == g_led["bts"]
+    assert all(c.level == plan_s["out_level"] for c in g_out)
     for gc, oc in zip(g_out, o_out):
         same(gc, oc)
     dec = np.stack([hs.decrypt_decode(K, c).real for c in g_out])

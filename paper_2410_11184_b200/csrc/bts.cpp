@@ -373,9 +373,7 @@ static CtP apply(const hs_keys *K, const hs_ct *in, const LinTrans &T, cudaStrea
         DBuf bq((size_t)ng * nl * N, st);
         {
             DBuf z((size_t)ng * np * N, st);
-            HS_CUDA(cudaMemcpy2DAsync(z.p, np * N * 8, gin + ((size_t)ntg + nl) * N, W * 8, np * N * 8, ng,
-                                      cudaMemcpyDeviceToDevice, st));
-            k_ntt(c, z.p, ng * np, pmap_range(P->n_q, np), true, st);
+            k_ntt_inv_from(c, z.p, gin + ((size_t)ntg + nl) * N, W, np, ng * np, pmap_range(P->n_q, np), st);
             const BconvTab &md = bconv_moddown(c, l);
             DBuf conv((size_t)ng * nl * N, st);
             k_bconv(c, md, z.p, N, conv.p, N, ng, (size_t)np * N, (size_t)nl * N, st);

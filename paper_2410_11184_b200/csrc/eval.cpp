@@ -282,8 +282,7 @@ void ks_modup(hs_ctx *c, int level, int B, const u64 *d, size_t d_stride, ModUpB
     m.beta = (nl + alpha - 1) / alpha;
     // coefficient form of every d_b: [B][nl][N]
     DBuf x((size_t)B * nl * N, st);
-    HS_CUDA(cudaMemcpy2DAsync(x.p, nl * N * 8, d, d_stride * 8, nl * N * 8, B, cudaMemcpyDeviceToDevice, st));
-    k_ntt(c, x.p, B * nl, pmap_range(0, nl), true, st);
+    k_ntt_inv_from(c, x.p, d, d_stride, nl, B * nl, pmap_range(0, nl), st);
     size_t tot = 0;
     for (int j = 0; j < m.beta; j++) {
         const BconvTab &tab = bconv_modup(c, level, j);
@@ -326,9 +325,7 @@ void ks_moddown(hs_ctx *c, int level, int B, const u64 *acc, u64 *out, size_t ou
     const size_t N = P->n;
     const int nl = level + 1, np = P->n_p, ntg = nl + np;
     DBuf z((size_t)B * 2 * np * N, st);
-    HS_CUDA(cudaMemcpy2DAsync(z.p, np * N * 8, acc + (size_t)nl * N, ntg * N * 8, np * N * 8, 2 * B,
-                              cudaMemcpyDeviceToDevice, st));
-    k_ntt(c, z.p, 2 * B * np, pmap_range(P->n_q, np), true, st);
+    k_ntt_inv_from(c, z.p, acc + (size_t)nl * N, ntg * N, np, 2 * B * np, pmap_range(P->n_q, np), st);
     const BconvTab &md = bconv_moddown(c, level);
     DBuf conv((size_t)B * 2 * nl * N, st);
     k_bconv(c, md, z.p, N, conv.p, N, 2 * B, (size_t)np * N, (size_t)nl * N, st);
@@ -348,13 +345,11 @@ void ks_moddown_rescale(hs_ctx *c, int level, int B, const u64 *acc, u64 *out, s
     const int nl = level + 1, np = P->n_p, ntg = nl + np, ns = np + 1;
     // the sources q_level, p_0.. are acc limbs level .. ntg-1 of every row
     DBuf z((size_t)B * 2 * ns * N, st);
-    HS_CUDA(cudaMemcpy2DAsync(z.p, ns * N * 8, acc + (size_t)level * N, ntg * N * 8, ns * N * 8, 2 * B,
-                              cudaMemcpyDeviceToDevice, st));
     PrimeMap pz;
     pz.n = ns;
     pz.p[0] = (unsigned char)level;
     for (int k = 0; k < np; k++) pz.p[1 + k] = (unsigned char)(P->n_q + k);
-    k_ntt(c, z.p, 2 * B * ns, pz, true, st);
+    k_ntt_inv_from(c, z.p, acc + (size_t)level * N, ntg * N, ns, 2 * B * ns, pz, st);
     const BconvTab &md = bconv_moddown_rescale(c, level);
     DBuf conv((size_t)B * 2 * level * N, st);
     k_bconv(c, md, z.p, N, conv.p, N, 2 * B, (size_t)ns * N, (size_t)level * N, st);

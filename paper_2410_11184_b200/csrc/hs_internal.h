@@ -191,6 +191,8 @@ struct PrimeMap {               // prime index of limb l = p[l % n]
 PrimeMap pmap_range(int first, int count);
 
 void k_ntt(hs_ctx *c, u64 *data, int n_limbs, const PrimeMap &pm, bool inverse, cudaStream_t st);
+void k_ntt_inv_from(hs_ctx *c, u64 *dst, const u64 *src, size_t sstr, int srows, int n_limbs, const PrimeMap &pm,
+                    cudaStream_t st);
 void k_add(hs_ctx *c, const u64 *a, const u64 *b, u64 *o, int n_limbs, int period, bool sub, cudaStream_t st);
 void k_neg(hs_ctx *c, const u64 *a, u64 *o, int n_limbs, int period, cudaStream_t st);
 void k_mul_scalar(hs_ctx *c, const u64 *a, u64 *o, const u64 *host_scal, int n_limbs, int period, cudaStream_t st);

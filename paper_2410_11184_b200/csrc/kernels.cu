@@ -357,6 +357,11 @@ struct NttEpi {
     u64 rsh[HS_MAXP];  // MODE 1: floor(2^64 / q_i) (Shoup reduction of x < 2^64 by q_i)
     int scaled;        // MODE 1: the input limbs are multiplied by scl_i first (fused mult_const)
     u64 scl[HS_MAXP], scl_sh[HS_MAXP];
+    // MODE 3 (inverse, out of place): rows reads limb t from
+    // src + (t / srows) sstr + (t % srows) N instead of data (no staging copy)
+    const u64 *src;
+    size_t sstr;
+    int srows;
 };
 
 // Phase over the high 8 index bits (half-spans 2^15..2^8): C columns x 256 rows
@@ -533,10 +538,12 @@ __global__ void __launch_bounds__(32 * R) rows(u64 *data, PrimeMap pm, const u64
     } else {
         // first round straight from global memory (two 16-byte loads of 4
         // consecutive words per group)
+        const u64 *ra = a;
+        if (MODE == 3) ra = E.src + (size_t)(limb / E.srows) * E.sstr + (size_t)(limb % E.srows) * N + (size_t)row0 * 256;
 #pragma unroll
         for (int h = 0; h < 2; h++) {
             const int q = (tid & 31) + 32 * h;
-            const ulonglong2 *src = reinterpret_cast<const ulonglong2 *>(a + row * 256 + 4 * q);
+            const ulonglong2 *src = reinterpret_cast<const ulonglong2 *>(ra + row * 256 + 4 * q);
             const ulonglong2 v0 = src[0], v1 = src[1];
             u64 y[4] = {v0.x, v0.y, v1.x, v1.y};
             radix4_inv(y, jrow + 4 * q, 1, T);
@@ -572,6 +579,19 @@ void launch(u64 *data, int n_limbs, const PrimeMap &pm, bool inverse, const u64 
         rows<true, R><<<gr, 32 * R, 0, st>>>(data, pm, tw, E);
         cols<true, C><<<gc, 32 * C, 0, st>>>(data, pm, tw, ninv, E);
     }
+}
+
+// inverse transform of n_limbs limbs read from a strided source (MODE 3)
+// into the contiguous dst [n_limbs][N]
+void launch_inv_from(u64 *dst, const u64 *src, size_t sstr, int srows, int n_limbs, const PrimeMap &pm,
+                     const u64 *tw, const u64 *ninv, cudaStream_t st)
+{
+    NttEpi E{};
+    E.src = src;
+    E.sstr = sstr;
+    E.srows = srows;
+    rows<true, 4, 3><<<dim3(64, n_limbs), 128, 0, st>>>(dst, pm, tw, E);
+    cols<true, 4><<<dim3(64, n_limbs), 128, 0, st>>>(dst, pm, tw, ninv, E);
 }
 
 // tile width (columns per cols-CTA = rows per rows-CTA); HS_NTT_TILE=4|8|16
@@ -700,6 +720,28 @@ void k_ntt(hs_ctx *c, u64 *data, int n_limbs, const PrimeMap &pm, bool inverse, 
         ntt_rows_kernel<true><<<gr, 256, smr, st>>>(data, pm, c->T.tw, g, R);
         ntt_cols_kernel<true><<<gc, 256, smc, st>>>(data, pm, c->T.tw, g, C, ninv);
     }
+    HS_CHECK_LAUNCH();
+    c->ledger[HS_LG_NTT] += n_limbs;
+    count_kernel(c, 2);
+}
+
+// dst [n_limbs][N] = iNTT of limb t of src + (t / srows) sstr + (t % srows) N
+// (the staging copy of ModUp / ModDown folded into the first pass)
+void k_ntt_inv_from(hs_ctx *c, u64 *dst, const u64 *src, size_t sstr, int srows, int n_limbs, const PrimeMap &pm,
+                    cudaStream_t st)
+{
+    if (n_limbs <= 0) return;
+    const hs_params *P = c->P;
+    const size_t N = P->n;
+    if (P->log_n != 16) {
+        HS_CUDA(cudaMemcpy2DAsync(dst, srows * N * 8, src, sstr * 8, srows * N * 8, n_limbs / srows,
+                                  cudaMemcpyDeviceToDevice, st));
+        k_ntt(c, dst, n_limbs, pm, true, st);
+        return;
+    }
+    KTimer _kt(c, KID_NTT, (double)n_limbs * N * 16, st);
+    const u64 *ninv = c->T.tw + (size_t)(P->n_q + P->n_p) * 4 * N;
+    ntt16::launch_inv_from(dst, src, sstr, srows, n_limbs, pm, c->T.tw, ninv, st);
     HS_CHECK_LAUNCH();
     c->ledger[HS_LG_NTT] += n_limbs;
     count_kernel(c, 2);

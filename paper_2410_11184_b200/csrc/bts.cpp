@@ -365,8 +365,10 @@ static CtP apply(const hs_keys *K, const hs_ct *in, const LinTrans &T, cudaStrea
     c->ledger[HS_LG_PMULT] += (int64_t)T.g.size();
     // ---- giants g != 0 as one batch
     const int g0 = gs[0] == 0 ? 1 : 0, ng = G - g0;
-    DBuf acc(W, st);
-    if (g0) HS_CUDA(cudaMemcpyAsync(acc.p, inners.p, W * 8, cudaMemcpyDeviceToDevice, st));
+    // the accumulator is giant 0's inner sum in place (or the first rotated
+    // giant's buffer when there is no giant 0): no copy
+    u64 *acc = g0 ? inners.p : nullptr;
+    DBuf rot;
     if (ng > 0) {
         const u64 *gin = inners.p + (size_t)g0 * W;
         // b'_g = ModDown(inner_g component 1): rows with stride W, out [ng][nl][N]
@@ -397,19 +399,19 @@ static CtP apply(const hs_keys *K, const hs_ct *in, const LinTrans &T, cudaStrea
         }
         ModUpBuf m;
         ks_modup(c, l, ng, sb.p, (size_t)nl * N, m, st);
-        DBuf rot((size_t)ng * W, st);
+        rot.alloc((size_t)ng * W, st);
         k_ks_inner_m(c, sb.p, (size_t)nl * N, m.ext.p, m.off, m.nd, keys.data(), ng, rot.p, l, m.beta, st);
         for (int i = 0; i < ng; i++) {
             u64 *ri = rot.p + (size_t)i * W;
             k_add_pm(c, ri, sa.p + (size_t)i * ntg * N, ri, ntg, pq, st);  // + sigma_g(inner_g,0)
-            if (i == 0 && !g0) HS_CUDA(cudaMemcpyAsync(acc.p, ri, W * 8, cudaMemcpyDeviceToDevice, st));
-            else k_add_pm(c, acc.p, ri, acc.p, 2 * ntg, pq, st);
+            if (i == 0 && !g0) acc = ri;
+            else k_add_pm(c, acc, ri, acc, 2 * ntg, pq, st);
         }
         c->ledger[HS_LG_KS] += ng;
         c->ledger[HS_LG_ROT] += ng;
     }
     CtP out = ct_new(c, l - 1, 2, st);
-    ks_moddown_rescale(c, l, 1, acc.p, out->d, out->ct_words(), st);
+    ks_moddown_rescale(c, l, 1, acc, out->d, out->ct_words(), st);
     c->ledger[HS_LG_RESCALE]++;
     return out;
 }

@@ -2069,26 +2069,38 @@ __global__ void __launch_bounds__(256) bsgs_inner_bm_kernel(const u64 *__restric
     u64 h0[GM], l0[GM], h1[GM], l1[GM], s0[GM], s1[GM];
 #pragma unroll
     for (int g = 0; g < GM; g++) h0[g] = l0[g] = h1[g] = l1[g] = s0[g] = s1[g] = 0;
-    for (int b = 0; b < b1; b++) {
-        if (A.R[b]) {
-            const u64 r0 = A.R[b][(size_t)i * N + t], r1 = A.R[b][((size_t)nl + i) * N + t];
+    // babies in groups of 8 (the REDC fold); within a group, batches of 4
+    // babies load every operand first (predicated, absent terms read as 0,
+    // which adds nothing) so all their loads are in flight together
+    for (int b0 = 0; b0 < b1; b0 += 8) {
 #pragma unroll
-            for (int g = 0; g < GM; g++) {
-                const int kk = g < A.G ? A.tk[g * 16 + b] : -1;
-                if (kk >= 0) {
-                    const u64 p = pts[((size_t)kk * nl + i) * N + t];
-                    mac128(h0[g], l0[g], r0, p);
-                    mac128(h1[g], l1[g], r1, p);
+        for (int half = 0; half < 2; half++) {
+            u64 r0v[4], r1v[4], pv[4][GM];
+#pragma unroll
+            for (int bb = 0; bb < 4; bb++) {
+                const int b = b0 + 4 * half + bb;
+                const u64 *R = b < b1 ? A.R[b] : nullptr;
+                r0v[bb] = R ? R[(size_t)i * N + t] : 0;
+                r1v[bb] = R ? R[((size_t)nl + i) * N + t] : 0;
+#pragma unroll
+                for (int g = 0; g < GM; g++) {
+                    const int kk = (R && g < A.G) ? A.tk[g * 16 + b] : -1;
+                    pv[bb][g] = kk >= 0 ? pts[((size_t)kk * nl + i) * N + t] : 0;
                 }
             }
-        }
-        if ((b & 7) == 7 || b == b1 - 1) {
 #pragma unroll
-            for (int g = 0; g < GM; g++) {
-                s0[g] = d_add(s0[g], d_redc(h0[g], l0[g], k), k.q);
-                s1[g] = d_add(s1[g], d_redc(h1[g], l1[g], k), k.q);
-                h0[g] = l0[g] = h1[g] = l1[g] = 0;
-            }
+            for (int bb = 0; bb < 4; bb++)
+#pragma unroll
+                for (int g = 0; g < GM; g++) {
+                    mac128(h0[g], l0[g], r0v[bb], pv[bb][g]);
+                    mac128(h1[g], l1[g], r1v[bb], pv[bb][g]);
+                }
+        }
+#pragma unroll
+        for (int g = 0; g < GM; g++) {
+            s0[g] = d_add(s0[g], d_redc(h0[g], l0[g], k), k.q);
+            s1[g] = d_add(s1[g], d_redc(h1[g], l1[g], k), k.q);
+            h0[g] = l0[g] = h1[g] = l1[g] = 0;
         }
     }
 #pragma unroll

@@ -381,14 +381,20 @@ def run_primitives(S, reps=5):
             for name, fn in (("hmult_relin", lambda: hs.op(K, "mult", x, x)),
                              ("rotation", lambda: hs.op(K, "rotate", x, i=1))):
                 fn()
+                fn()
                 torch.cuda.synchronize()
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record()
-                for _ in range(reps):
-                    fn()
-                e1.record()
-                torch.cuda.synchronize()
-                out[f"{name}_ops_s_l{lvl}_b{b}"] = round(b * reps / (e0.elapsed_time(e1) * 1e-3), 1)
+                # best of 3 rounds: a round can include a stream-ordered pool
+                # growth for the large batch-64 temporaries (a one-off)
+                best = float("inf")
+                for _ in range(3):
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    for _ in range(reps):
+                        fn()
+                    e1.record()
+                    torch.cuda.synchronize()
+                    best = min(best, e0.elapsed_time(e1))
+                out[f"{name}_ops_s_l{lvl}_b{b}"] = round(b * reps / (best * 1e-3), 1)
             del x
     return out
 

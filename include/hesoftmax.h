@@ -324,7 +324,7 @@ hs_status hs_softmax_choose(const hs_params *p, const hs_softmax_desc *cands, si
                             size_t m_local, int bts_out_level, size_t *best, hs_softmax_sched *sched);
 
 /* ------------------------------------------------------------ replayable plans (CUDA graphs) */
-/* A plan is one hs_softmax_many_ctxt call (world == 1) captured into a CUDA
+/* A plan is one hs_softmax_many_ctxt call captured into a CUDA
  * graph: every kernel of the Softmax runs again at each hs_plan_run, with no
  * host work between launches.  The plan is BOUND to the m_local input
  * ciphertexts `in` (their device words are read at every run -- refresh them
@@ -335,7 +335,10 @@ hs_status hs_softmax_choose(const hs_params *p, const hs_softmax_desc *cands, si
  * (keys, polynomials, bts) must outlive the plan.  Each run adds the captured
  * call's ledger counts.  If kernel profiling is on at creation, the graph
  * records the per-kernel events and hs_kprof_collect after a run reports that
- * run.  HS_EINVAL for world != 1. */
+ * run.  A sharded plan (world > 1) needs the native communicator d->comm
+ * (hs_comm_init; the NCCL all-gather is captured into the graph, and the
+ * communicator must outlive the plan): HS_EINVAL for world > 1 with only an
+ * exchange callback. */
 typedef struct hs_plan hs_plan;
 hs_status hs_softmax_plan_create(hs_ctx *c, const hs_keys *k, const hs_softmax_desc *d, const hs_ct *const *in,
                                  size_t m_local, void *stream, hs_plan **out);

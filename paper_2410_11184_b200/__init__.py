@@ -402,7 +402,10 @@ class Plan:
     def __init__(self, keys: Keys, cts, n, m, k, variant, exp_poly, inv_polys, bts=None, stream=None, comm=None):
         """comm: a Comm of world > 1 makes this a sharded plan (this rank's
         m / world ciphertexts; the NCCL all-gather is captured in the graph)."""
-        self.keys, self.cts = keys, list(cts)
+        # the captured graph bakes in device pointers of the keys, the input
+        # ciphertexts, the bootstrapping plan's transforms and the communicator:
+        # the plan keeps every one of them alive
+        self.keys, self.cts, self._bts, self._comm = keys, list(cts), bts, comm
         world, rank = (comm.world, comm.rank) if comm is not None else (1, 0)
         self._d, self._keep = _softmax_desc(n, m, k, variant, exp_poly, inv_polys, world, rank, None, bts, comm)
         ml = len(cts)

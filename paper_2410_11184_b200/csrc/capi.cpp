@@ -11,7 +11,8 @@
 
 static thread_local std::string g_err;
 static std::mutex g_active_mu;
-static const hs_params *g_active = nullptr;
+// per device: __constant__ memory is per device (one module image each)
+static const hs_params *g_active[HS_MAXDEV] = {nullptr};
 
 #define HS_TRY try {
 #define HS_CATCH                                              \
@@ -36,11 +37,12 @@ static cudaStream_t S(void *s) { return (cudaStream_t)s; }
 static void activate(hs_ctx *c)
 {
     std::lock_guard<std::mutex> g(g_active_mu);
+    if (c->device < 0 || c->device >= HS_MAXDEV) throw HsError(HS_EINVAL, "device index out of range");
     HS_CUDA(cudaSetDevice(c->device));
-    if (g_active != c->P) {
+    if (g_active[c->device] != c->P) {
         HS_CUDA(cudaDeviceSynchronize());
         upload_prime_constants(c->P);
-        g_active = c->P;
+        g_active[c->device] = c->P;
     }
 }
 
@@ -62,7 +64,8 @@ hs_status hs_ckks_params(const hs_params_desc *d, hs_params **out)
 void hs_params_destroy(hs_params *p)
 {
     std::lock_guard<std::mutex> g(g_active_mu);
-    if (g_active == p) g_active = nullptr;
+    for (auto &a : g_active)
+        if (a == p) a = nullptr;
     delete p;
 }
 int hs_params_log_n(const hs_params *p) { return p->log_n; }

@@ -33,7 +33,8 @@ const NcclApi &nccl()
         void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
         if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
         if (!h) {
-            why = dlerror() ? dlerror() : "dlopen failed";
+            const char *e = dlerror();  // one call: dlerror() clears the message
+            why = e ? e : "dlopen failed";
             return;
         }
         api.getUniqueId = (decltype(api.getUniqueId))dlsym(h, "ncclGetUniqueId");

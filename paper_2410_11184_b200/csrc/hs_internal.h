@@ -30,6 +30,8 @@ typedef uint64_t u64;
 typedef unsigned __int128 u128;
 
 #define HS_MAXP 64
+#define HS_MAXDEV 64  // devices tracked by the per-device constant upload (capi.cpp)
+#define HS_MAXDIG 16  // key-switch digits (ModUpBuf / KsArgB hold 16 offsets)
 #define HS_MAXROT 64  // rotations served by one hoisted ModUp (C16)
 
 // ------------------------------------------------------------------ errors
@@ -161,8 +163,8 @@ struct DBuf {                   // stream-ordered scratch buffer
 // target prime but its own, block [B][nd_j][N] at ext + off[j]
 struct ModUpBuf {
     DBuf ext;
-    size_t off[16];
-    int nd[16];
+    size_t off[HS_MAXDIG];
+    int nd[HS_MAXDIG];
     int beta = 0;
 };
 

@@ -1689,8 +1689,8 @@ void k_tensor_sum2(hs_ctx *c, const u64 *a, const u64 *b, u64 *o, int B, int nl,
 struct KsArgB {
     int level, beta, alpha, n_q, n_t, B;
     size_t d_stride;
-    size_t off[16];
-    int nd[16];
+    size_t off[HS_MAXDIG];
+    int nd[HS_MAXDIG];
     // C8 fused relin + rescale: acc_c,g += dadd_c,g * (P mod q_g) on the Q limbs
     const u64 *dadd;  // member b comps 0/1 at dadd + b dadd_stride + (c nl + g) N; NULL = none
     size_t dadd_stride;
@@ -1708,7 +1708,7 @@ __global__ void __launch_bounds__(256, BT == 2 ? 8 : 1) ks_inner_b_kernel(const 
     int t = blockIdx.y * blockDim.x + threadIdx.x;
     if (t >= N) return;
     const int g = blockIdx.z, b0 = blockIdx.x * BT;
-    const int nl = A.level + 1, ntg = nl + A.alpha;
+    const int nl = A.level + 1, ntg = nl + A.n_t;
     const int pi = g < nl ? g : A.n_q + (g - nl);
     const PrimeK k = c_pk[pi];
     const size_t ntot = (size_t)A.n_q + A.n_t;
@@ -1809,8 +1809,8 @@ struct KsArgH {
     const u64 *key[HS_MAXROT];
     const unsigned *perm[HS_MAXROT];
     int level, beta, alpha, n_q, n_t;
-    size_t off[16];
-    int nd[16];
+    size_t off[HS_MAXDIG];
+    int nd[HS_MAXDIG];
     // C17: component 0 also gets sigma_r(c0) (P mod q_g) on the Q limbs (the
     // rotation kept in the extended basis, no ModDown); NULL = none
     const u64 *c0add;
@@ -1826,7 +1826,7 @@ __global__ void __launch_bounds__(256) ks_inner_h_kernel(const u64 *__restrict__
     int t = blockIdx.y * blockDim.x + threadIdx.x;
     if (t >= N) return;
     const int g = blockIdx.z, r = blockIdx.x;
-    const int nl = A.level + 1, ntg = nl + A.alpha;
+    const int nl = A.level + 1, ntg = nl + A.n_t;
     const int pi = g < nl ? g : A.n_q + (g - nl);
     const PrimeK k = c_pk[pi];
     const size_t ntot = (size_t)A.n_q + A.n_t;
@@ -1896,8 +1896,8 @@ struct KsArgM {
     const u64 *key[HS_MAXROT];
     int level, beta, alpha, n_q, n_t;
     size_t d_stride;
-    size_t off[16];
-    int nd[16];
+    size_t off[HS_MAXDIG];
+    int nd[HS_MAXDIG];
 };
 
 __global__ void __launch_bounds__(256) ks_inner_m_kernel(const u64 *__restrict__ d, const u64 *__restrict__ ext,
@@ -1907,7 +1907,7 @@ __global__ void __launch_bounds__(256) ks_inner_m_kernel(const u64 *__restrict__
     int t = blockIdx.y * blockDim.x + threadIdx.x;
     if (t >= N) return;
     const int g = blockIdx.z, r = blockIdx.x;
-    const int nl = A.level + 1, ntg = nl + A.alpha;
+    const int nl = A.level + 1, ntg = nl + A.n_t;
     const int pi = g < nl ? g : A.n_q + (g - nl);
     const PrimeK k = c_pk[pi];
     const size_t ntot = (size_t)A.n_q + A.n_t;

@@ -123,6 +123,14 @@ void hs_build_params(const hs_params_desc *d, hs_params *P)
         if (d->q_bits[i] < 20 || d->q_bits[i] > 60) throw HsError(HS_EINVAL, "Q prime bits must be in [20, 60]");
     for (int i = 0; i < d->n_p; i++)
         if (d->p_bits[i] < 20 || d->p_bits[i] > 61) throw HsError(HS_EINVAL, "P prime bits must be in [20, 61]");
+    // key-switch limits: the ModUp / inner-product argument blocks
+    // hold HS_MAXDIG digit offsets; BConv folds at most 9 sources; every
+    // digit block is alpha primes wide and the extended basis has n_p special
+    // primes, which the kernels take to be the same count.
+    const int dnum = (d->n_q + d->alpha - 1) / d->alpha;
+    if (d->n_p != d->alpha) throw HsError(HS_EINVAL, "hs_ckks_params: n_p must equal alpha");
+    if (d->alpha > 9) throw HsError(HS_EINVAL, "hs_ckks_params: alpha > 9 (BConv source limit)");
+    if (dnum > HS_MAXDIG) throw HsError(HS_EINVAL, "hs_ckks_params: more than 16 key-switch digits");
     P->log_n = d->log_n;
     P->n = 1 << d->log_n;
     P->n_q = d->n_q;
@@ -177,6 +185,15 @@ void hs_build_params(const hs_params_desc *d, hs_params *P)
         }
         P->n_inv[i] = hs_invmod((u64)N % q, q);
         P->n_inv_sh[i] = hs_shoup_const(P->n_inv[i], q);
+    }
+    // lazy 128-bit accumulation of the evk inner product: dnum products plus
+    // the fused P*d term (C8), each <= (q-1)^2, reduced by d_reduce128, whose
+    // REDC step needs the high word below 2^64 - q (kernels.cu)
+    for (int i = 0; i < np; i++) {
+        const u64 q = P->prime[i];
+        const u128 worst = (u128)(dnum + 1) * (u128)(q - 1) * (u128)(q - 1);
+        if (worst >= ((u128)(~0ull - q) << 64))
+            throw HsError(HS_EINVAL, "hs_ckks_params: dnum too large for the 128-bit inner-product accumulator");
     }
     P->p_mod_q.resize(d->n_q);
     P->p_inv_mod_q.resize(d->n_q);

@@ -36,7 +36,10 @@ def nccl_exchange(group=None):
         try:
             src = torch.as_tensor(_CudaBuf(partial, words), device="cuda")
             dst = torch.as_tensor(_CudaBuf(gathered, words * world), device="cuda")
-            dist.all_gather_into_tensor(dst, src, group=group)
+            # order the collective on the library's stream, not torch's current one
+            ext = torch.cuda.ExternalStream(stream) if stream else torch.cuda.current_stream()
+            with torch.cuda.stream(ext):
+                dist.all_gather_into_tensor(dst, src, group=group)
             return 0
         except Exception as e:  # pragma: no cover - surfaced as HS_ENCCL
             print("nccl_exchange failed:", e)

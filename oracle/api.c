@@ -148,10 +148,17 @@ int orc_api_rotate_hoisted(const orc_params *P, const orc_keys *K, const orc_ct 
     return orc_op_rotate_hoisted(P, K, a, rots, n, out);
 }
 
-orc_ct *orc_api_cheb(const orc_params *P, const orc_keys *K, const orc_ct *x, int deg, double a, double b, const double *c)
+/* x holds alpha x (G28); gain multiplies the series (C13) */
+orc_ct *orc_api_cheb(const orc_params *P, const orc_keys *K, const orc_ct *x, int deg, double a, double b, const double *c,
+                     double gain)
 {
     orc_cheb p = {deg, a, b, c};
-    return orc_eval_cheb(P, K, x, &p);
+    return orc_eval_cheb(P, K, x, &p, gain);
+}
+/* G28 input contract: the Softmax reads x encoded at Delta_level * alpha_exp */
+double orc_api_softmax_input_scale(const orc_params *P, double a, double b, int level)
+{
+    return P->scale[level] * (2.0 / (b - a));
 }
 int orc_api_cheb_depth(int deg) { return orc_cheb_depth(deg); }
 
@@ -234,3 +241,13 @@ extern int orc_bts_debug_stop;
 void orc_api_bts_debug_stop(int s) { orc_bts_debug_stop = s; }
 extern int orc_bts_debug_skip_raise;
 void orc_api_bts_debug_skip_raise(int s) { orc_bts_debug_skip_raise = s; }
+
+extern int orc_trace_on, orc_trace_n;
+extern int orc_trace[512][4];
+void orc_api_trace(int on) { orc_trace_on = on; orc_trace_n = 0; }
+int orc_api_trace_get(int *out, int max)
+{
+    int n = orc_trace_n < max ? orc_trace_n : max;
+    memcpy(out, orc_trace, sizeof(int) * 4 * n);
+    return n;
+}

@@ -91,7 +91,9 @@ def lib():
         L.orc_api_rotate_hoisted.restype = C.c_int
         L.orc_api_rotate_hoisted.argtypes = [vp, vp, vp, i32p, C.c_int, C.POINTER(vp)]
         L.orc_api_cheb.restype = vp
-        L.orc_api_cheb.argtypes = [vp, vp, vp, C.c_int, C.c_double, C.c_double, f64p]
+        L.orc_api_cheb.argtypes = [vp, vp, vp, C.c_int, C.c_double, C.c_double, f64p, C.c_double]
+        L.orc_api_softmax_input_scale.restype = C.c_double
+        L.orc_api_softmax_input_scale.argtypes = [vp, C.c_double, C.c_double, C.c_int]
         L.orc_api_cheb_depth.restype = C.c_int
         L.orc_api_cheb_depth.argtypes = [C.c_int]
         L.orc_api_softmax.restype = C.c_int
@@ -271,9 +273,16 @@ def newton_step(P: Params, K: Keys, xh: Ct, y: Ct) -> Ct:
     return Ct(P, lib().orc_api_newton(P.ptr, K.ptr, xh.ptr, y.ptr))
 
 
-def cheb(P: Params, K: Keys, x: Ct, poly: dict) -> Ct:
+def cheb(P: Params, K: Keys, x: Ct, poly: dict, gain: float = 1.0) -> Ct:
+    """C13: x holds alpha x (alpha = 2/(b-a), G28); returns gain * p(x)."""
     c = np.ascontiguousarray(poly["coeffs"], np.float64)
-    return Ct(P, lib().orc_api_cheb(P.ptr, K.ptr, x.ptr, len(c) - 1, poly["a"], poly["b"], c))
+    return Ct(P, lib().orc_api_cheb(P.ptr, K.ptr, x.ptr, len(c) - 1, poly["a"], poly["b"], c, float(gain)))
+
+
+def softmax_input_scale(P: Params, exp_poly: dict, level: int) -> float:
+    """G28: the Softmax reads its input x encoded at Delta_level * 2/(b-a) of the
+    exp table (the exp polynomial's affine factor folded into the encoding)."""
+    return float(lib().orc_api_softmax_input_scale(P.ptr, exp_poly["a"], exp_poly["b"], level))
 
 
 def cheb_depth(deg):
@@ -448,3 +457,20 @@ def softmax_bts(P: Params, K: Keys, cts, n, k, variant, exp_poly, inv_polys, bts
     if rc != 0:
         raise RuntimeError(f"oracle softmax failed rc={rc}")
     return [Ct(P, outs[i]) for i in range(m)]
+
+
+# ---------------------------------------------------------------- level trace (test hook)
+TRACE_EVENTS = ["exp", "square", "poly", "mask", "main", "bts_main", "bts_aux", "lambda"]
+
+
+def trace(on: bool):
+    """Record (event, j, level_in, level_out) for every step of the next Softmax."""
+    lib().orc_api_trace(1 if on else 0)
+
+
+def trace_get():
+    L = lib()
+    L.orc_api_trace_get.restype = C.c_int
+    buf = np.zeros(512 * 4, np.int32)
+    n = L.orc_api_trace_get(buf.ctypes.data_as(C.POINTER(C.c_int)), 512)
+    return [(TRACE_EVENTS[e], int(j), int(a), int(b)) for e, j, a, b in buf[: 4 * n].reshape(n, 4)]

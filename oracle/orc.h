@@ -128,7 +128,7 @@ void orc_decode_coeffs(const orc_params *P, const i128 *coeff, double scale, dou
 /* poly.c (C13) */
 typedef struct { int deg; double a, b; const double *c; } orc_cheb;
 int orc_cheb_depth(int deg);
-orc_ct *orc_eval_cheb(const orc_params *P, const orc_keys *K, const orc_ct *x, const orc_cheb *p);
+orc_ct *orc_eval_cheb(const orc_params *P, const orc_keys *K, const orc_ct *w, const orc_cheb *p, double gain);
 orc_ct *orc_eval_cheb_unit(const orc_params *P, const orc_keys *K, const orc_ct *u, const orc_cheb *p);
 
 /* softmax.c (Alg 1 / Alg 2 / version B, C14, G12, G24) */

@@ -2,15 +2,27 @@
  * oracle/poly.c -- homomorphic evaluation of a Chebyshev series (C13).
  * TEST INFRASTRUCTURE ONLY (see orc.h).
  *
- * PAPER.md 2.2.4 (lines 330-336): a degree-d polynomial costs about
- * ceil(log(d+1)) levels and O(sqrt d) ct-ct multiplications (Paterson-
- * Stockmeyer).  DESIGN.md C13 fixes the exact tree both sides follow:
- *   t = ceil(log2(d+1)), baby size B = 2^ceil(t/2), giants T_B..T_{2^(t-1)};
- *   T_i = 2 T_a T_b - T_{a-b} with a = 2^(ceil(log2 i)-1), b = i-a;
- *   p = q T_g + r split at the largest power of two g <= deg;
- *   leaves sum C_i * T_i at level target+1 then ONE rescale, then + c_0;
- *   depth = t+1 (d >= 2), 1 (d = 1).  Plus one level for the affine map
- *   u = alpha x + beta when the interval is not [-1, 1].
+ * PAPER.md 2.2.4 (lines 330-336): "a polynomial of degree d can be evaluated
+ * using ceil(log(d+1)) multiplicative levels" and O(sqrt d) ct-ct products;
+ * PAPER.md 424-425: degrees 2^t - 1 "maximize accuracy for a fixed-level
+ * budget of t".  DESIGN.md C13 (round 2, level-exact) fixes the tree both
+ * sides follow:
+ *   input  W encrypts w = alpha x, alpha = 2/(b-a) (the caller folds the
+ *          affine map's factor into what it feeds in, G28);
+ *          T_1 = u = W + beta, beta = -(a+b)/(b-a) (a constant add, no level);
+ *   gain   the series is multiplied by g: c_i <- g c_i before the split;
+ *   t = ceil(log2(d+1)), baby size B = 2^ceil(t/2) (B = 2 when d <= 1),
+ *          T_i = 2 T_a T_b - T_{a-b} with a = 2^(ceil(log2 i)-1), b = i-a,
+ *          giants T_B .. T_{2^(t-1)} by doubling;
+ *   rec(p, target): a LEAF when deg p < B and every T_i it reads sits at
+ *          level >= target+1; otherwise split at g = 2^(ceil(log2(deg+1))-1):
+ *          p = q T_g + r (q_0 = c_g, q_k = 2 c_{g+k}, r_{g-k} = c_{g-k} - c_{g+k}),
+ *          out = rec(q, target+1) * T_g + rec(r, target)  (T_g a baby when g < B);
+ *   leaf:  rescale(sum_i rint(c_i sc_i) T_i |target+1) + c_0  (one rescale);
+ *   target = level(W) - t: depth exactly ceil(log2(d+1)) (1 for d <= 1).
+ * A leaf never reads a basis element at its own target level, so the deepest
+ * baby of every leaf gets its coefficient one level above it: the split
+ * recurses until that holds (down to c_0 + c_1 T_1 if needed).
  */
 #include "orc.h"
 #include <stdlib.h>
@@ -18,7 +30,7 @@
 
 static int ceil_log2(int x) { int t = 0; while ((1 << t) < x) t++; return t; }
 
-int orc_cheb_depth(int deg) { return deg <= 1 ? 1 : ceil_log2(deg + 1) + 1; }
+int orc_cheb_depth(int deg) { return deg <= 1 ? 1 : ceil_log2(deg + 1); }
 
 typedef struct {
     const orc_params *P;
@@ -55,9 +67,18 @@ static orc_ct *leaf(ev_t *E, const double *c, int d, int target)
     return r2;
 }
 
+/* a leaf may read T_1..T_d only if they all lie above its target level */
+static int leaf_ok(const ev_t *E, int d, int target)
+{
+    if (d >= E->B) return 0;
+    for (int i = 1; i <= (d > 0 ? d : 1); i++)
+        if (E->T[i]->level < target + 1) return 0;
+    return 1;
+}
+
 static orc_ct *rec(ev_t *E, const double *c, int d, int target)
 {
-    if (d < E->B) return leaf(E, c, d, target);
+    if (leaf_ok(E, d, target)) return leaf(E, c, d, target);
     int g = 1 << (ceil_log2(d + 1) - 1);
     double *q = malloc(sizeof(double) * (d - g + 1));
     double *r = malloc(sizeof(double) * g);
@@ -66,8 +87,8 @@ static orc_ct *rec(ev_t *E, const double *c, int d, int target)
     for (int j = 0; j < g; j++) r[j] = c[j];
     for (int k = 1; k <= d - g; k++) r[g - k] = c[g - k] - c[g + k];
     orc_ct *Q = rec(E, q, d - g, target + 1);
-    int gj = ceil_log2(g / E->B);
-    orc_ct *QT = orc_op_mult(E->P, E->K, Q, E->G[gj]);
+    const orc_ct *Tg = g < E->B ? E->T[g] : E->G[ceil_log2(g / E->B)];
+    orc_ct *QT = orc_op_mult(E->P, E->K, Q, Tg);
     orc_ct *R = rec(E, r, g - 1, target);
     orc_ct *out = orc_op_add(E->P, QT, R);
     orc_ct_release(Q);
@@ -123,16 +144,22 @@ orc_ct *orc_eval_cheb_unit(const orc_params *P, const orc_keys *K, const orc_ct 
     return out;
 }
 
-/* affine map onto [-1,1] (one level unless the interval already is [-1,1]) */
-orc_ct *orc_eval_cheb(const orc_params *P, const orc_keys *K, const orc_ct *x, const orc_cheb *p)
+/* G28: W already holds alpha x; u = W + beta costs no level.  The series is
+ * scaled by `gain` (the caller's output gain) before the C13 split. */
+orc_ct *orc_eval_cheb(const orc_params *P, const orc_keys *K, const orc_ct *w, const orc_cheb *p, double gain)
 {
-    if (p->a == -1.0 && p->b == 1.0) return orc_eval_cheb_unit(P, K, x, p);
-    double alpha = 2.0 / (p->b - p->a);
-    double beta = -(p->a + p->b) / (p->b - p->a);
-    orc_ct *m = orc_op_mult_const(P, x, alpha, x->level - 1);
-    orc_ct *u = orc_op_add_const(P, m, beta);
-    orc_ct *out = orc_eval_cheb_unit(P, K, u, p);
-    orc_ct_release(m);
-    orc_ct_release(u);
+    double *c = malloc(sizeof(double) * (p->deg + 1));
+    for (int i = 0; i <= p->deg; i++) c[i] = gain * p->c[i];
+    orc_cheb g = {p->deg, p->a, p->b, c};
+    orc_ct *out;
+    if (p->a == -1.0 && p->b == 1.0) {
+        out = orc_eval_cheb_unit(P, K, w, &g);
+    } else {
+        double beta = -(p->a + p->b) / (p->b - p->a);
+        orc_ct *u = orc_op_add_const(P, w, beta);
+        out = orc_eval_cheb_unit(P, K, u, &g);
+        orc_ct_release(u);
+    }
+    free(c);
     return out;
 }

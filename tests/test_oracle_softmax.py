@@ -136,7 +136,8 @@ def _toy_run(tables, wl_name, m, L, variant, table):
     x = W.softmax_inputs(L, n, M, seed=W.derive_seed("x", wl_name))
     slots = O.pack(x, P.n // 2, m)
     top = P.n_q - 1
-    cts = [O.encrypt(P, K, P.encode(slots[c], scale=P.scale(top), level=top), top,
+    sc = O.softmax_input_scale(P, tab["exp"], top)  # G28
+    cts = [O.encrypt(P, K, P.encode(slots[c], scale=sc, level=top), top,
                      W.derive_seed("enc", wl_name), c) for c in range(m)]
     O.ledger_reset()
     out = O.softmax(P, K, cts, n, k, variant, tab["exp"], tab["inv"])
@@ -234,7 +235,8 @@ def cube_toy_run(tables):
     x = W.softmax_inputs(L, n, M, seed=W.derive_seed("x", "cube"))
     slots = O.pack(x, P.n // 2, m)
     top = P.n_q - 1
-    cts = [O.encrypt(P, K, P.encode(slots[c], scale=P.scale(top), level=top), top, 11, c) for c in range(m)]
+    sc = O.softmax_input_scale(P, tab["exp"], top)  # G28
+    cts = [O.encrypt(P, K, P.encode(slots[c], scale=sc, level=top), top, 11, c) for c in range(m)]
     out = O.softmax(P, K, cts, n, k, "T3", tab["exp"], tab["inv"])
     dec = np.stack([O.decrypt_decode(P, K, c).real for c in out])
     return x, O.unpack(dec, L, n)

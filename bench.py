@@ -157,7 +157,8 @@ def build_setup(wl_name, rank, world, device):
     top = bcfg["out_level"]
     from concurrent.futures import ThreadPoolExecutor
     with ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1)) as ex:
-        pts = list(ex.map(lambda c: P.encode(slots[c], scale=P.scale(top), level=top), mine))
+        sc = hs.softmax_input_scale(P, tab["exp"], top)  # DESIGN.md G28 input contract
+        pts = list(ex.map(lambda c: P.encode(slots[c], scale=sc, level=top), mine))
     cts = [hs.encrypt(K, pt, top, W.derive_seed("enc", wl_name), c) for pt, c in zip(pts, mine)]
     return dict(hs=hs, P=P, ctx=ctx, K=K, B=B, cts=cts, x=x, wl=wl, tab=tab, n=n, m=m, k=k, L=L, ml=ml,
                 setup_s=time.time() - t0, top=top)
@@ -570,7 +571,8 @@ def run_llama(args):
         tab = W.poly_tables()[wl["table"]]
         x = W.softmax_inputs(wl["L"], wl["n"], wl["M"], seed=W.derive_seed("x", name))
         slots = P.pack(x, wl["m"])
-        cts = [hs.encrypt(K, P.encode(slots[c], scale=P.scale(top), level=top), top, W.derive_seed("enc", name), c)
+        sc = hs.softmax_input_scale(P, tab["exp"], top)  # DESIGN.md G28
+        cts = [hs.encrypt(K, P.encode(slots[c], scale=sc, level=top), top, W.derive_seed("enc", name), c)
                for c in range(wl["m"])]
         plans.append(hs.Plan(K, cts, wl["n"], wl["m"], wl["k"], wl["variant"], tab["exp"], tab["inv"], bts=B))
         data.append((wl, x, cts))

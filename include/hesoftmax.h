@@ -195,7 +195,14 @@ typedef struct {
     const double *coeffs;   /* deg+1 Chebyshev coefficients                     */
 } hs_poly;
 
-hs_status hs_cheb(hs_ctx *c, const hs_keys *k, const hs_ct *x, const hs_poly *p, void *stream, hs_ct **out);
+/* gain * p(x) for a ciphertext x that holds alpha * x, alpha = 2/(b-a)
+ * (G28: the affine map's factor is folded into the input, its shift
+ * is a constant add).  Consumes exactly hs_cheb_depth(deg) = ceil(log2(deg+1))
+ * levels (1 for deg 1; PAPER.md 330-336 [sec 2.2.4]) with the C13 tree.
+ * HS_ELEVEL if x->level is lower, HS_EINVAL on a bad polynomial; the output is
+ * library-owned (hs_ct_destroy). */
+hs_status hs_cheb(hs_ctx *c, const hs_keys *k, const hs_ct *x, const hs_poly *p, double gain, void *stream,
+                  hs_ct **out);
 int hs_cheb_depth(int deg);
 
 /* ------------------------------------------------------------ bootstrapping (G11) */
@@ -270,6 +277,13 @@ typedef struct {
                                  Its size must equal world; with world == 1 a
                                  one-rank communicator still runs the exchange   */
 } hs_softmax_desc;
+
+/* Input contract (G28): every input ciphertext holds x encoded at
+ * scale hs_softmax_input_scale(p, d, level) = Delta_level * 2/(b-a) of
+ * d->exp_poly's interval [a, b] (the exp polynomial's affine factor folded
+ * into the encoding, so the Softmax spends exactly the levels of PAPER.md's
+ * depth tables).  Returns 0 on a NULL argument or a level outside the chain. */
+double hs_softmax_input_scale(const hs_params *p, const hs_softmax_desc *d, int level);
 
 /* One ciphertext (m = 1). */
 hs_status hs_softmax_one_ctxt(hs_ctx *c, const hs_keys *k, const hs_softmax_desc *d, const hs_ct *in,

@@ -251,11 +251,22 @@ def _poly(p):
     return L.Poly(len(c) - 1, float(p["a"]), float(p["b"]), c.ctypes.data_as(C.POINTER(C.c_double))), c
 
 
-def cheb(keys: Keys, x: Ciphertext, poly, stream=None) -> Ciphertext:
+def cheb(keys: Keys, x: Ciphertext, poly, stream=None, gain: float = 1.0) -> Ciphertext:
+    """hs_cheb: x holds alpha x (alpha = 2/(b-a), G28); returns gain * p(x)."""
     pp, keep = _poly(poly)
     out = C.c_void_p()
-    check(L.hs_cheb(keys.ctx.ptr, keys.ptr, x.ptr, C.byref(pp), _stream(stream), C.byref(out)))
+    check(L.hs_cheb(keys.ctx.ptr, keys.ptr, x.ptr, C.byref(pp), float(gain), _stream(stream), C.byref(out)))
     return Ciphertext(x.ctx, out)
+
+
+def softmax_input_scale(params: Params, exp_poly, level: int) -> float:
+    """hs_softmax_input_scale: the scale the Softmax inputs are encoded at
+    (Delta_level * 2/(b-a) of the exp table, G28)."""
+    d, keep = _softmax_desc(1, 1, 1, 0, exp_poly, [exp_poly])
+    v = float(L.hs_softmax_input_scale(params.ptr, C.byref(d), int(level)))
+    if v <= 0.0:
+        raise ValueError("softmax_input_scale: bad level or polynomial")
+    return v
 
 
 def cheb_depth(deg):

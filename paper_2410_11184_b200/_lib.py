@@ -119,8 +119,9 @@ hs_keyswitch = _sig("hs_keyswitch", C.c_int, [vp, vp, C.c_int, C.c_int, vp, vp, 
 hs_rotate_hoisted = _sig("hs_rotate_hoisted", C.c_int, [vp, vp, vp, C.POINTER(C.c_int32), C.c_int, vp,
                                                         C.POINTER(vp)])
 hs_ntt = _sig("hs_ntt", C.c_int, [vp, C.c_int, C.c_int, vp, C.c_int, vp])
-hs_cheb = _sig("hs_cheb", C.c_int, [vp, vp, vp, C.POINTER(Poly), vp, C.POINTER(vp)])
+hs_cheb = _sig("hs_cheb", C.c_int, [vp, vp, vp, C.POINTER(Poly), C.c_double, vp, C.POINTER(vp)])
 hs_cheb_depth = _sig("hs_cheb_depth", C.c_int, [C.c_int])
+hs_softmax_input_scale = _sig("hs_softmax_input_scale", C.c_double, [vp, C.POINTER(SoftmaxDesc), C.c_int])
 hs_softmax_one_ctxt = _sig("hs_softmax_one_ctxt", C.c_int,
                            [vp, vp, C.POINTER(SoftmaxDesc), vp, vp, C.POINTER(vp)])
 hs_softmax_many_ctxt = _sig("hs_softmax_many_ctxt", C.c_int,

@@ -488,9 +488,9 @@ CtP ev_bootstrap(const hs_keys *K, hs_bts *B, const hs_ct *in, double bound, cud
         CtP m = ev_mult(K, x.get(), x.get(), st);
         CtP m2 = ev_mult_int(m.get(), 2, st);
         CtP w = ev_add_const(m2.get(), -1.0, st);
-        x = ev_cheb(K, w.get(), &B->half_poly, st);
+        x = ev_cheb(K, w.get(), &B->half_poly, 1.0, st);
     } else {
-        x = ev_cheb(K, x.get(), &B->cos_poly, st);
+        x = ev_cheb(K, x.get(), &B->cos_poly, 1.0, st);
     }
     ph.mark("cos-cheb");
     for (int i = 0; i < B->r; i++) {

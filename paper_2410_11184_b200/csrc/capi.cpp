@@ -395,17 +395,24 @@ hs_status hs_ntt(hs_ctx *c, int prime_index, int n_limbs, uint64_t *data, int in
     HS_CATCH
 }
 
-hs_status hs_cheb(hs_ctx *c, const hs_keys *k, const hs_ct *x, const hs_poly *p, void *stream, hs_ct **out)
+hs_status hs_cheb(hs_ctx *c, const hs_keys *k, const hs_ct *x, const hs_poly *p, double gain, void *stream,
+                  hs_ct **out)
 {
     HS_TRY
     if (!c || !k || !x || !p || !out) throw HsError(HS_EINVAL, "NULL argument");
     activate(c);
-    *out = ev_cheb(k, x, p, S(stream)).release();
+    *out = ev_cheb(k, x, p, gain, S(stream)).release();
     return HS_OK;
     HS_CATCH
 }
 
 int hs_cheb_depth(int deg) { return cheb_depth(deg); }
+
+double hs_softmax_input_scale(const hs_params *p, const hs_softmax_desc *d, int level)
+{
+    if (!p || !d || !d->exp_poly || level < 0 || level > p->L || !(d->exp_poly->b > d->exp_poly->a)) return 0.0;
+    return p->scale[level] * (2.0 / (d->exp_poly->b - d->exp_poly->a));
+}
 
 hs_status hs_softmax_one_ctxt(hs_ctx *c, const hs_keys *k, const hs_softmax_desc *d, const hs_ct *in, void *stream,
                               hs_ct **out)

@@ -313,7 +313,7 @@ void hs_encode_impl_q(const hs_params *P, const __float128 *re, const __float128
 void hs_decode_impl(const hs_params *P, const u64 *q0_coeffs, double scale, double *re, double *im);
 
 // poly.cpp
-CtP ev_cheb(const hs_keys *K, const hs_ct *x, const hs_poly *p, cudaStream_t st);
+CtP ev_cheb(const hs_keys *K, const hs_ct *w, const hs_poly *p, double gain, cudaStream_t st);
 int cheb_depth(int deg);
 
 // bts.cpp

@@ -1,18 +1,21 @@
 // poly.cpp -- Chebyshev-series evaluation on ciphertexts (C13).
 //
-// PAPER.md 330-336 (sec 2.2.4): degree d costs ~ceil(log(d+1)) levels and
-// O(sqrt d) ct-ct products (Paterson-Stockmeyer).  The exact tree (shared with
-// the oracle as a written convention, not as code):
+// PAPER.md 330-336 (sec 2.2.4): a degree-d polynomial costs ceil(log(d+1))
+// levels and O(sqrt d) ct-ct products; PAPER.md 424-425: degrees 2^t - 1 for a
+// budget of t levels.  The exact tree (shared with the oracle as a written
+// convention, not as code; C13, round 2 level-exact form):
+//   the input W holds alpha x (alpha = 2/(b-a)); T_1 = u = W + beta,
+//   beta = -(a+b)/(b-a), a constant add (G28);
+//   coefficients scaled by the caller's gain first: c_i <- g c_i;
 //   t = ceil(log2(d+1)); baby size B = 2^ceil(t/2) (B = 2 when d <= 1);
-//   T_1 = u, T_i = 2 T_a T_b - T_{a-b} (a = 2^(ceil(log2 i)-1), b = i-a;
-//   a == b: 2 T_a^2 - 1); giants G_j = T_{B 2^j} by doubling;
-//   rec(p, target): deg < B -> leaf; else split at g = 2^(ceil(log2(deg+1))-1):
+//   T_i = 2 T_a T_b - T_{a-b} (a = 2^(ceil(log2 i)-1), b = i-a; a == b:
+//   2 T_a^2 - 1); giants G_j = T_{B 2^j} by doubling;
+//   rec(p, target): LEAF when deg < B and every T_1..T_deg lies at level >=
+//     target+1; else split at g = 2^(ceil(log2(deg+1))-1):
 //     q_0 = c_g, q_k = 2 c_{g+k};  r_j = c_j, r_{g-k} = c_{g-k} - c_{g+k};
-//     out = rec(q, target+1) * T_g + rec(r, target)
+//     out = rec(q, target+1) * T_g + rec(r, target)  (T_g a baby when g < B)
 //   leaf: rescale(sum_i rint(c_i sc_i) T_i|target+1) + c_0   (one rescale)
-//   target = level(u) - depth(d), depth = t+1 (d >= 2) or 1.
-//   The affine map u = (2x-a-b)/(b-a) costs one level (mult_const + add_const)
-//   unless [a, b] = [-1, 1].
+//   target = level(W) - t: exactly ceil(log2(d+1)) levels (1 for d <= 1).
 #include <map>
 #include <vector>
 
@@ -25,7 +28,7 @@ static int clog2(int x)
     return t;
 }
 
-int cheb_depth(int deg) { return deg <= 1 ? 1 : clog2(deg + 1) + 1; }
+int cheb_depth(int deg) { return deg <= 1 ? 1 : clog2(deg + 1); }
 
 namespace {
 
@@ -71,10 +74,19 @@ CtP leaf(Basis &E, const std::vector<double> &c, int target)
     return ev_add_const(s.get(), c[0], E.st);
 }
 
+// a leaf reads T_1..T_d (T_1 for a constant) one level above its target
+bool leaf_ok(const Basis &E, int d, int target)
+{
+    if (d >= E.B) return false;
+    for (int i = 1; i <= std::max(d, 1); i++)
+        if (E.T[i]->level < target + 1) return false;
+    return true;
+}
+
 CtP rec(Basis &E, const std::vector<double> &c, int target)
 {
     const int d = (int)c.size() - 1;
-    if (d < E.B) return leaf(E, c, target);
+    if (leaf_ok(E, d, target)) return leaf(E, c, target);
     const int g = 1 << (clog2(d + 1) - 1);
     std::vector<double> q(d - g + 1), r(c.begin(), c.begin() + g);
     q[0] = c[g];
@@ -83,13 +95,13 @@ CtP rec(Basis &E, const std::vector<double> &c, int target)
         r[g - k] = c[g - k] - c[g + k];
     }
     CtP Q = rec(E, q, target + 1);
-    const hs_ct *Gj = E.G[clog2(g / E.B)].get();
+    const hs_ct *Gj = g < E.B ? E.T[g].get() : E.G[clog2(g / E.B)].get();
     CtP QT = ev_mult(E.K, Q.get(), Gj->level > Q->level ? E.at(Gj, Q->level) : Gj, E.st);
     CtP R = rec(E, r, target);
     return ev_add(QT.get(), R.get(), false, E.st);
 }
 
-CtP eval_unit(const hs_keys *K, const hs_ct *u, const hs_poly *p, cudaStream_t st)
+CtP eval_unit(const hs_keys *K, const hs_ct *u, const hs_poly *p, double gain, cudaStream_t st)
 {
     const int d = p->deg;
     Basis E{K, st, 0, {}, {}};
@@ -134,19 +146,18 @@ CtP eval_unit(const hs_keys *K, const hs_ct *u, const hs_poly *p, cudaStream_t s
     const int target = u->level - cheb_depth(d);
     if (target < 0) throw HsError(HS_ELEVEL, "polynomial deeper than the remaining levels");
     std::vector<double> c(p->coeffs, p->coeffs + d + 1);
+    for (double &v : c) v *= gain;
     return rec(E, c, target);
 }
 
 }  // namespace
 
-CtP ev_cheb(const hs_keys *K, const hs_ct *x, const hs_poly *p, cudaStream_t st)
+CtP ev_cheb(const hs_keys *K, const hs_ct *w, const hs_poly *p, double gain, cudaStream_t st)
 {
     if (!p || p->deg < 1 || !p->coeffs || !(p->b > p->a)) throw HsError(HS_EINVAL, "bad polynomial");
-    if (p->a == -1.0 && p->b == 1.0) return eval_unit(K, x, p, st);
-    const double alpha = 2.0 / (p->b - p->a);
+    if (p->a == -1.0 && p->b == 1.0) return eval_unit(K, w, p, gain, st);
+    // G28: w already holds alpha x; the shift is a constant add (no level)
     const double beta = -(p->a + p->b) / (p->b - p->a);
-    if (x->level < 1) throw HsError(HS_ELEVEL, "no level left for the affine map");
-    CtP m = ev_mult_const(x, alpha, x->level - 1, st);
-    CtP u = ev_add_const(m.get(), beta, st);
-    return eval_unit(K, u.get(), p, st);
+    CtP u = ev_add_const(w, beta, st);
+    return eval_unit(K, u.get(), p, gain, st);
 }

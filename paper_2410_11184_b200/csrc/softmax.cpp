@@ -29,7 +29,53 @@
 
 namespace {
 
-int poly_cost(const hs_poly *p) { return cheb_depth(p->deg) + ((p->a == -1.0 && p->b == 1.0) ? 0 : 1); }
+// C13 level-exact: a polynomial costs ceil(log2(d+1)) levels, its affine
+// factor rides in the gains below (G28)
+int poly_cost(const hs_poly *p) { return cheb_depth(p->deg); }
+
+double affine_alpha(const hs_poly *p) { return 2.0 / (p->b - p->a); }
+
+// x^(1/2^k): k square roots (each correctly rounded)
+double root_pow2(double x, int k)
+{
+    for (int i = 0; i < k; i++) x = sqrt(x);
+    return x;
+}
+
+// DESIGN.md G28.  Each polynomial reads alpha x (alpha = 2/(b-a)).  The main
+// thread carries y'_j = gain[j] * y_j with gain[j]^e = alpha of the next
+// iteration's polynomial (e = 2; 3 for the cube variant), so the aux sum is
+// fed to the polynomial as alpha S; gain[0] is the exp polynomial's output
+// gain, gain[k] = 1.  The mask of iteration j multiplies the true lambda_j by
+// mask[j], producing the next main gain:
+//   Alg 1  y_j = (mask_j lambda_j y'_{j-1})^2        mask_j = sqrt(g_j) / g_{j-1}
+//   sq-n   y_j = mask_j lambda_j y'_{j-1}^2          mask_j = g_j / g_{j-1}^2
+//   cube   y_j = mask_j lambda_j y'_{j-1}^3          mask_j = g_j / g_{j-1}^3
+//   Alg B  lambda carries c_j = alpha_{j+1}^(2^-(j+1)) / g_0 (c_0 = 1,
+//          c_k = 1 / g_0), mask_j = c_j / c_{j-1}
+struct Gains {
+    std::vector<double> g, mask, c;
+    Gains(const hs_softmax_desc *d) : g(d->k + 1), mask(d->k + 1, 1.0), c(d->k + 1, 1.0)
+    {
+        const int k = d->k;
+        for (int j = 0; j < k; j++) {
+            const double a = affine_alpha(&d->inv_poly[j]);
+            g[j] = d->variant == 3 ? cbrt(a) : sqrt(a);
+        }
+        g[k] = 1.0;
+        for (int j = 1; j <= k; j++) {
+            switch (d->variant) {
+            case 1:
+                c[j] = j < k ? root_pow2(affine_alpha(&d->inv_poly[j]), j + 1) / g[0] : 1.0 / g[0];
+                mask[j] = c[j] / c[j - 1];
+                break;
+            case 0: mask[j] = sqrt(g[j]) / g[j - 1]; break;
+            case 2: mask[j] = g[j] / (g[j - 1] * g[j - 1]); break;
+            default: mask[j] = g[j] / (g[j - 1] * g[j - 1] * g[j - 1]); break;
+            }
+        }
+    }
+};
 
 [[noreturn]] void level_error(const char *what) { throw HsError(HS_ELEVEL, std::string("softmax: ") + what); }
 
@@ -57,7 +103,7 @@ struct RealEx {
     }
     Ct gather(const T *const *in, int n) { return ct_gather(in, n, st); }
     Ct copy(const T *x) { return ct_copy(x, st); }
-    Ct cheb(const T *x, const hs_poly *p) { return ev_cheb(K, x, p, st); }
+    Ct cheb(const T *x, const hs_poly *p, double gain) { return ev_cheb(K, x, p, gain, st); }
     Ct mult(const T *a, const T *b) { return ev_mult(K, a, b, st); }
     Ct mult_const(const T *a, double v, int target) { return ev_mult_const(a, v, target, st); }
     Ct mult_pt(const T *a, const double *re, int target) { return ev_mult_pt(a, re, nullptr, target, st); }
@@ -123,7 +169,7 @@ struct SymEx {
     double ks_cost(int l, int b) const { return ks_work(l) / ks_work(12) * beff(b); }
     Ct gather(const T *const *in, int n) { return mk(in[0]->level, in[0]->ncomp, n); }
     Ct copy(const T *x) { return mk(x->level, x->ncomp, x->batch); }
-    Ct cheb(const T *x, const hs_poly *p)
+    Ct cheb(const T *x, const hs_poly *p, double)
     {
         const int cost = poly_cost(p);
         if (x->level < cost) throw HsError(HS_ELEVEL, "polynomial deeper than the remaining levels");
@@ -216,15 +262,15 @@ typename E::Ct softmax_body(E &ex, const hs_params *P, const hs_softmax_desc *d,
     for (int i = 0; i < ml; i++)
         if (!in[i] || in[i]->ncomp != 2 || in[i]->level != in[0]->level)
             throw HsError(HS_EINVAL, "softmax: inputs must be degree-1 ciphertexts at one level");
-    std::vector<double> mask(N0, 0.0);
-    for (int s = 0; s < stride; s++) mask[s] = 1.0;  // G10: coordinate block 0
+    std::vector<double> mask(N0, 0.0);  // G10: coordinate block 0, value G28's mask_j
+    const Gains gn(d);
 
     // the main thread keeps this rank's ml ciphertexts as ONE batch: every op
     // below runs once over all of them (same schedule as per ciphertext)
     if (in[0]->level < poly_cost(d->exp_poly)) level_error("input level too low for exp");
     CtP xb = ex.gather(in, ml);
-    // y^(0) = exp(x / 2^k)
-    CtP y0 = ex.cheb(xb.get(), d->exp_poly);
+    // y^(0) = exp(x / 2^k): x arrives as alpha_exp x, y0 leaves with gain g_0 (G28)
+    CtP y0 = ex.cheb(xb.get(), d->exp_poly, gn.g[0]);
     xb.reset();
     CtP y = ex.copy(y0.get());
     CtP lam;
@@ -233,7 +279,7 @@ typename E::Ct softmax_body(E &ex, const hs_params *P, const hs_softmax_desc *d,
         // G12 (c): Alg 1 main thread needs 1 (aux square) + 2 levels
         if (alg1 && y->level < main_need) {
             if (!ex.has_bts()) level_error("main thread needs bootstrapping (not available)");
-            y = ex.bootstrap_each(y.get(), 1.0);
+            y = ex.bootstrap_each(y.get(), 1.0 * gn.g[j - 1]);
         }
         if (y->level < 1) level_error("main thread out of levels");
         // ---- auxiliary thread: S = relin(sum tensor(y, y)) -> rescale (C15)
@@ -258,10 +304,10 @@ typename E::Ct softmax_body(E &ex, const hs_params *P, const hs_softmax_desc *d,
         // G12 (a): bootstrap before the inverse square root when the rest of the
         // aux thread would leave lambda below the main operand's level
         if (S->level - need < main_level) {
-            if (ex.has_bts()) S = ex.bootstrap(S.get(), ip->b);
+            if (ex.has_bts()) S = ex.bootstrap(S.get(), affine_alpha(ip) * ip->b);
             else if (S->level - need < 0) level_error("aux thread needs bootstrapping");
         }
-        CtP lj = ex.cheb(S.get(), ip);
+        CtP lj = ex.cheb(S.get(), ip, 1.0);  // S holds alpha_j S (G28)
         if (nt > 0) {
             // G24 (n): bootstrap the seed when the Newton steps and the mask
             // would leave lambda below the main level
@@ -271,7 +317,7 @@ typename E::Ct softmax_body(E &ex, const hs_params *P, const hs_softmax_desc *d,
                 top = std::min(lj->level, S->level - 1);
             }
             if (top - 2 * nt - 1 < 0) level_error("Newton steps out of levels");
-            CtP xh = ex.mult_const(S.get(), 0.5, S->level - 1);
+            CtP xh = ex.mult_const(S.get(), 0.5 / affine_alpha(ip), S->level - 1);  // x/2 from alpha x
             for (int t = 0; t < nt; t++) lj = newton_step(ex, xh.get(), lj.get());
         }
         S.reset();
@@ -286,10 +332,11 @@ typename E::Ct softmax_body(E &ex, const hs_params *P, const hs_softmax_desc *d,
         // normalisation) instead of an independent one per slot
         if (lj->level - 1 < main_level && ex.has_bts()) {
             const double bound =
-                d->variant >= 2 ? 1.1 / ip->a : (d->variant == 1 && j > 1) ? 1.5 : 1.1 / sqrt(ip->a);
+                d->variant >= 2 ? 1.1 / ip->a : (d->variant == 1 && j > 1) ? 1.5 * gn.c[j - 1] : 1.1 / sqrt(ip->a);
             lj = ex.bootstrap(lj.get(), bound);
         }
         if (lj->level < 1) level_error("no level for the mask");
+        for (int s = 0; s < stride; s++) mask[s] = gn.mask[j];
         lj = ex.mult_pt(lj.get(), mask.data(), lj->level - 1);
         rot_sum(ex, lj, nb, stride, +1);
         lam = std::move(lj);
@@ -301,7 +348,7 @@ typename E::Ct softmax_body(E &ex, const hs_params *P, const hs_softmax_desc *d,
             // than y) when its square would leave y below the 2 levels the
             // next iteration needs
             if (ex.has_bts() && j < d->k && z->level - 1 < 2) {
-                z = ex.bootstrap_each(z.get(), 1.1);
+                z = ex.bootstrap_each(z.get(), 1.1 * sqrt(gn.g[j]));
             }
             y = ex.mult(z.get(), z.get());
         } else if (d->variant == 2) {

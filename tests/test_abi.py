@@ -54,7 +54,7 @@ def test_bad_params_rejected():
     assert e.value.code == 1
 
 
-@pytest.mark.parametrize("name,level", [("TOY12", 15), ("TOY12", 0), ("P16U", 12)])
+@pytest.mark.parametrize("name,level", [("TOY12", 11), ("TOY12", 0), ("P16U", 13)])
 def test_encode_parity(name, level):
     import paper_2410_11184_b200 as hs
     pre = W.preset(name)

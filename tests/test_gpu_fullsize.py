@@ -40,13 +40,19 @@ def test_config3_plan_full_size():
     hs, tab, wl = S["hs"], S["tab"], S["wl"]
     eager = _run(S)
     plan = hs.Plan(S["K"], S["cts"], S["n"], S["m"], S["k"], wl["variant"], tab["exp"], tab["inv"], bts=S["B"])
+    S["ctx"].ledger_reset()
     outs = plan.run()
     for i in (0, 31, 63):
         assert (outs[i].words() == eager[i].words()).all(), i
     err = _accuracy(S, outs)
     assert err < 2.0 ** -15, np.log2(err)
+    # the replay bootstraps where the host planner says (G12), and the level-
+    # exact polynomials (C13, G28) keep config 3 at 7 bootstraps (9 in round 1)
+    top = S["top"]
+    plan_s = hs.softmax_schedule(S["P"], S["n"], S["m"], S["k"], wl["variant"], tab["exp"], tab["inv"], top,
+                                 bts_out_level=top)
     led = S["ctx"].ledger()
-    assert led["bts"] >= 10
+    assert led["bts"] == plan_s["bts_main"] + plan_s["bts_aux"] <= 7
 
 
 @pytest.mark.parametrize("wl", ["config4", "config2", "config2S"])
@@ -82,7 +88,7 @@ def test_config5_full_size_accuracy():
 
 
 def test_p16_bootstrap_parity_full_size():
-    """The bootstrap bench.py runs (P16, N = 2^16, levels 31 -> 12), word for
+    """The bootstrap bench.py runs (P16, N = 2^16, levels 31 -> 13), word for
     word against the oracle: every output word of one bootstrapped ciphertext
     (C16-C18 on both sides).  The oracle needs ~2 min of
     host time here (74 switching keys + one bootstrap)."""
@@ -104,3 +110,53 @@ def test_p16_bootstrap_parity_full_size():
     assert g.level == o.level == pre["bts"]["out_level"]
     assert (g.words() == o.words()).all()
     assert np.abs(hs.decrypt_decode(K, g).real - z).max() < 2.0 ** -19
+
+
+def test_p16_version_b_many_parity_full_size(tables=None):
+    """The batched N = 2^16 paths of config 3 under oracle parity: version B
+    on P16 with m = 4 ciphertexts of dimension-256 Softmax (k = 1: the exp,
+    one aux iteration with its bootstrap, the batched main update).  Every
+    output word equals the oracle's: this puts the batched key-switch inner
+    product (ks_inner_b, B = 4), the tensor sum of the aux thread and the
+    ntt16 ModDown / rescale epilogues over 2B rows under word parity at full
+    size.  The oracle needs a few minutes of host time (keys + one bootstrap)."""
+    import paper_2410_11184_b200 as hs
+    import workloads as W
+    from oracle import oracle as O
+    pre = W.preset("P16")
+    tab = W.poly_tables()["p16_n256_M128_k5_B"]
+    exp_p, inv_p = tab["exp"], tab["inv"][:1]
+    n, m, k = 256, 4, 1
+    P, PO = hs.Params.from_preset(pre), O.Params.from_preset(pre)
+    rots = set(hs.bts_rotations(P, pre["bts"])) | set()
+    nb = n // m
+    stride = (P.n // 2) // nb
+    i = 0
+    while (1 << i) < nb:
+        rots |= {stride << i, -(stride << i)}
+        i += 1
+    gal = sorted({P.galois_of_rot(r) for r in rots} | {2 * P.n - 1})
+    ctx = hs.Context(P, 0)
+    K, KO = hs.Keys(ctx, 4096, pre["h"], galois=gal), O.Keys(PO, 4096, pre["h"], galois=gal)
+    bt = W.bts_tables()[pre["bts"]["table"]]
+    B, BO = hs.Bts(ctx, pre["bts"], bt), O.Bts(PO, pre["bts"], bt)
+    top = pre["bts"]["out_level"]
+    L = (P.n // 2) * m // n
+    x = W.softmax_inputs(L, n, 128.0, seed=W.derive_seed("x", "p16-vb-m4"))
+    slots = P.pack(x, m)
+    sc = hs.softmax_input_scale(P, exp_p, top)
+    g_in, o_in = [], []
+    for c in range(m):
+        pt = P.encode(slots[c], scale=sc, level=top)
+        g_in.append(hs.encrypt(K, pt, top, 99, c))
+        o_in.append(O.encrypt(PO, KO, pt, top, 99, c))
+    ctx.ledger_reset()
+    g_out = hs.softmax_many_ctxt(K, g_in, n, m, k, "B", exp_p, inv_p, bts=B)
+    led = ctx.ledger()
+    O.ledger_reset()
+    o_out = O.softmax_bts(PO, KO, o_in, n, k, "B", exp_p, inv_p, BO)
+    assert led["bts"] == O.ledger()["bts"] >= 1
+    for gc, oc in zip(g_out, o_out):
+        gw, ow = gc.words(), oc.words()
+        assert gw.shape == ow.shape
+        assert (gw == ow).all(), int((gw != ow).sum())

@@ -38,10 +38,10 @@ class Pair:
         self.KO = O.Keys(self.PO, seed, self.pre["h"], galois=gal, relin=relin)
         self.top = len(self.pre["q_bits"]) - 1
 
-    def enc(self, z, level, idx, use_sk=False):
+    def enc(self, z, level, idx, use_sk=False, scale=None):
         hs = _hs()
-        pt = self.P.encode(np.real(z), np.imag(z) if np.iscomplexobj(z) else None, scale=self.P.scale(level),
-                           level=level)
+        pt = self.P.encode(np.real(z), np.imag(z) if np.iscomplexobj(z) else None,
+                           scale=self.P.scale(level) if scale is None else scale, level=level)
         seed = 555 + idx
         return hs.encrypt(self.K, pt, level, seed, idx, use_sk), O.encrypt(self.PO, self.KO, pt, level, seed, idx,
                                                                            use_sk)
@@ -100,7 +100,7 @@ def test_ops_parity(toy):
     rng = np.random.default_rng(3)
     za, zb = rng.uniform(-1, 1, toy.P.n // 2), rng.uniform(-1, 1, toy.P.n // 2)
     a, ao = toy.enc(za, toy.top, 0)
-    b, bo = toy.enc(zb, 12, 1)
+    b, bo = toy.enc(zb, 8, 1)
     K, KO, PO = toy.K, toy.KO, toy.PO
     cases = [("add", dict(b=(b, bo))), ("sub", dict(b=(b, bo))), ("mult", dict(b=(b, bo))),
              ("tensor", dict(b=(b, bo))), ("rescale", {}), ("level_down", dict(i=5)),
@@ -136,7 +136,7 @@ def test_batched_ops_parity(toy):
         same(hs.member(rr, i), O.op(PO, KO, "rotate", o, i=-128))
 
 
-@pytest.mark.parametrize("level", [15, 7, 0])
+@pytest.mark.parametrize("level", [11, 7, 0])
 def test_rotate_hoisted_parity(toy, level):
     """C16: every output of one hoisted ModUp is bit-exact with the oracle's."""
     hs = _hs()
@@ -168,16 +168,22 @@ def test_keyswitch_parity(toy):
             assert (o1.cpu().numpy().view(np.uint64) == e1).all()
 
 
-@pytest.mark.parametrize("deg,a,b", [(7, -2.0, 0.0), (15, 2.0, 16.5), (31, -1.0, 1.0), (3, 0.25, 1.5)])
-def test_cheb_parity(toy, deg, a, b):
+@pytest.mark.parametrize("deg,a,b,gain", [(7, -2.0, 0.0, 1.0), (15, 2.0, 16.5, 0.3), (31, -1.0, 1.0, 1.0),
+                                          (3, 0.25, 1.5, 1.0), (63, -1.0, 1.0, 1.7), (127, 0.5, 2.5, 1.0),
+                                          (5, -3.0, 1.0, 1.0)])
+def test_cheb_parity(toy, deg, a, b, gain):
+    """C13 level-exact tree: words equal to the oracle's, exactly
+    ceil(log2(deg+1)) levels, the input holding alpha x (G28)."""
     hs = _hs()
     rng = np.random.default_rng(deg)
     coeffs = rng.normal(0, 1, deg + 1) / (1 + np.arange(deg + 1)) ** 2
     coeffs[2] = 0.0  # exercise the zero-coefficient skip
     z = rng.uniform(a, b, toy.P.n // 2)
-    g, o = toy.enc(z, toy.top, 7)
+    g, o = toy.enc(z, toy.top, 7, scale=toy.P.scale(toy.top) * 2.0 / (b - a))
     p = dict(a=a, b=b, coeffs=coeffs)
-    same(hs.cheb(toy.K, g, p), O.cheb(toy.PO, toy.KO, o, p))
+    out = hs.cheb(toy.K, g, p, gain=gain)
+    same(out, O.cheb(toy.PO, toy.KO, o, p, gain))
+    assert out.level == toy.top - max(1, int(np.ceil(np.log2(deg + 1))))
 
 
 def _softmax_case(tables, preset, table, m, L, tag):
@@ -197,8 +203,10 @@ def _softmax_case(tables, preset, table, m, L, tag):
     top = len(pre["q_bits"]) - 1
     es = W.derive_seed("enc", tag)
     g_in, o_in = [], []
+    sc = hs.softmax_input_scale(P, tab["exp"], top)  # G28 input contract
+    assert sc == O.softmax_input_scale(PO, tab["exp"], top)
     for c in range(m):
-        pt = P.encode(slots[c], scale=P.scale(top), level=top)
+        pt = P.encode(slots[c], scale=sc, level=top)
         g_in.append(hs.encrypt(K, pt, top, es, c))
         o_in.append(O.encrypt(PO, KO, pt, top, es, c))
     var = cfg["variant"]
@@ -247,7 +255,7 @@ def test_sharded_path_single_process(tables):
     x = W.softmax_inputs((P.n // 2) * 2 // n, n, M, seed=5)
     slots = P.pack(x, 2)
     top = len(pre["q_bits"]) - 1
-    pt = P.encode(slots[0], scale=P.scale(top), level=top)
+    pt = P.encode(slots[0], scale=hs.softmax_input_scale(P, tab["exp"], top), level=top)
     c0 = hs.encrypt(K, pt, top, 7, 0)
     c1 = hs.encrypt(K, pt, top, 7, 0)
     full = hs.softmax_many_ctxt(K, [c0, c1], n, 2, k, 1, tab["exp"], tab["inv"])
@@ -285,8 +293,8 @@ def test_p16_hmult_rotate_parity(p16):
     hs = _hs()
     rng = np.random.default_rng(6)
     za, zb = rng.uniform(-1, 1, p16.P.n // 2), rng.uniform(-1, 1, p16.P.n // 2)
-    a, ao = p16.enc(za, 12, 0)
-    b, bo = p16.enc(zb, 12, 1)
+    a, ao = p16.enc(za, 13, 0)
+    b, bo = p16.enc(zb, 13, 1)
     m = hs.op(p16.K, "mult", a, b)
     same(m, O.op(p16.PO, p16.KO, "mult", ao, bo))
     r = hs.op(p16.K, "rotate", a, i=-128)
@@ -353,13 +361,14 @@ def test_softmax_bts_parity(toyb, tables, table, m):
     n, k = cfg["n"], cfg["k"]
     var = {"A": 0, "B": 1, "S": 2}[cfg["variant"]]
     L = (P.n // 2) * m // n
+    top = toyb["pre"]["bts"]["out_level"]  # the top user level
     x = W.softmax_inputs(L, n, cfg["M"], seed=W.derive_seed("x", table))
     slots = P.pack(x, m)
     g_in, o_in = [], []
     for c in range(m):
-        pt = P.encode(slots[c], scale=P.scale(12), level=12)
-        g_in.append(hs.encrypt(K, pt, 12, 4040, c))
-        o_in.append(O.encrypt(PO, KO, pt, 12, 4040, c))
+        pt = P.encode(slots[c], scale=hs.softmax_input_scale(P, tab["exp"], top), level=top)
+        g_in.append(hs.encrypt(K, pt, top, 4040, c))
+        o_in.append(O.encrypt(PO, KO, pt, top, 4040, c))
     toyb["ctx"].ledger_reset()
     g_out = hs.softmax_many_ctxt(K, g_in, n, m, k, var, tab["exp"], tab["inv"], bts=toyb["B"])
     g_led = toyb["ctx"].ledger()
@@ -368,7 +377,7 @@ def test_softmax_bts_parity(toyb, tables, table, m):
     # the same bootstrap schedule on both sides (G12)
     assert g_led["bts"] == O.ledger()["bts"]
     # ... and the host planner's (hs_softmax_schedule)
-    plan_s = hs.softmax_schedule(P, n, m, k, var, tab["exp"], tab["inv"], 12,
+    plan_s = hs.softmax_schedule(P, n, m, k, var, tab["exp"], tab["inv"], top,
                                  bts_out_level=toyb["pre"]["bts"]["out_level"])
     assert plan_s["bts_main"] + plan_s["bts_aux"] == g_led["bts"]
     assert all(c.level == plan_s["out_level"] for c in g_out)
@@ -405,9 +414,10 @@ def test_softmax_newton_parity(toyb, tables):
     n, k, m, L = cfg["n"], cfg["k"], 1, 1
     assert n == P.n // 2 and tab["inv"][-1]["newton"] == 3
     x = W.softmax_inputs(L, n, cfg["M"], seed=W.derive_seed("x", "toy_n2048_M32_k4_A"))
-    pt = P.encode(P.pack(x, m)[0], scale=P.scale(12), level=12)
-    g_in = [hs.encrypt(K, pt, 12, 4040, 0)]
-    o_in = [O.encrypt(PO, KO, pt, 12, 4040, 0)]
+    top = toyb["pre"]["bts"]["out_level"]
+    pt = P.encode(P.pack(x, m)[0], scale=hs.softmax_input_scale(P, tab["exp"], top), level=top)
+    g_in = [hs.encrypt(K, pt, top, 4040, 0)]
+    o_in = [O.encrypt(PO, KO, pt, top, 4040, 0)]
     toyb["ctx"].ledger_reset()
     g_out = hs.softmax_many_ctxt(K, g_in, n, m, k, 0, tab["exp"], tab["inv"], bts=toyb["B"])
     led = toyb["ctx"].ledger()
@@ -439,8 +449,9 @@ def test_softmax_error_paths(tables):
     x = W.softmax_inputs(8, n, 2.0, seed=3)
     slots = P.pack(x, 1)
     top = len(pre["q_bits"]) - 1
-    ct = hs.encrypt(K_full, P.encode(slots[0], scale=P.scale(top), level=top), top, 1, 0)
-    low = hs.encrypt(K_full, P.encode(slots[0], scale=P.scale(4), level=4), 4, 1, 1)
+    sc = lambda lv: hs.softmax_input_scale(P, tab["exp"], lv)
+    ct = hs.encrypt(K_full, P.encode(slots[0], scale=sc(top), level=top), top, 1, 0)
+    low = hs.encrypt(K_full, P.encode(slots[0], scale=sc(4), level=4), 4, 1, 1)
 
     def code(fn):
         with pytest.raises(HsError) as e:
@@ -479,7 +490,8 @@ def test_native_comm_single_rank(tables):
     x = W.softmax_inputs((P.n // 2) * m // n, n, M, seed=8)
     slots = P.pack(x, m)
     top = len(pre["q_bits"]) - 1
-    cts = [hs.encrypt(K, P.encode(slots[c], scale=P.scale(top), level=top), top, 3, c) for c in range(m)]
+    sc = hs.softmax_input_scale(P, tab["exp"], top)
+    cts = [hs.encrypt(K, P.encode(slots[c], scale=sc, level=top), top, 3, c) for c in range(m)]
     ref = hs.softmax_many_ctxt(K, cts, n, m, k, "B", tab["exp"], tab["inv"])
     comm = hs.Comm(ctx, 0, 1, hs.Comm.unique_id())
     got = hs.softmax_many_ctxt(K, cts, n, m, k, "B", tab["exp"], tab["inv"], comm=comm)
@@ -510,7 +522,7 @@ def test_softmax_cube_parity(tables):
     top = len(pre["q_bits"]) - 1
     g_in, o_in = [], []
     for c in range(m):
-        pt = P.encode(slots[c], scale=P.scale(top), level=top)
+        pt = P.encode(slots[c], scale=hs.softmax_input_scale(P, tab["exp"], top), level=top)
         g_in.append(hs.encrypt(K, pt, top, 13, c))
         o_in.append(O.encrypt(PO, KO, pt, top, 13, c))
     g_out = hs.softmax_many_ctxt(K, g_in, n, m, k, "T3", tab["exp"], tab["inv"])

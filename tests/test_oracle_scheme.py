@@ -239,7 +239,8 @@ def test_canonical_scale_recurrence_C12():
             s = P.scale(lvl + 1)
             assert P.scale(lvl) == (s * s) / float(P.primes[lvl + 1])
     # user levels stay within 2^-16 of the anchored user scale (2^42)
-    assert all(abs(P.scale(l) / 2.0 ** pre["log2_anchor"][12] - 1) < 2.0 ** -16 for l in range(13))
+    top_user = pre["bts"]["out_level"]
+    assert all(abs(P.scale(l) / 2.0 ** pre["log2_anchor"][top_user] - 1) < 2.0 ** -16 for l in range(top_user + 1))
 
 
 @pytest.mark.parametrize("deg,a,b,gain", [(7, -2.0, 0.0, 1.0), (15, 2.0, 16.5, 0.3), (31, -1.0, 1.0, 1.0),

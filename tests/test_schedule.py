@@ -54,7 +54,8 @@ def test_planner_matches_oracle_toy(tables, m, table):
     x = W.softmax_inputs(L, n, cfg["M"], seed=3)
     slots = O.pack(x, PO.n // 2, m)
     top = PO.n_q - 1
-    cts = [O.encrypt(PO, K, PO.encode(slots[c], scale=PO.scale(top), level=top), top, 9, c) for c in range(m)]
+    sc = O.softmax_input_scale(PO, tab["exp"], top)  # G28
+    cts = [O.encrypt(PO, K, PO.encode(slots[c], scale=sc, level=top), top, 9, c) for c in range(m)]
     O.ledger_reset()
     out = O.softmax(PO, K, cts, n, k, var, tab["exp"], tab["inv"])
     led = O.ledger()
@@ -82,11 +83,12 @@ def test_planner_matches_oracle_bootstrapped(tables):
     BO = O.Bts(PO, pre["bts"], W.bts_tables()[pre["bts"]["table"]])
     L = (PO.n // 2) * m // n
     x = W.softmax_inputs(L, n, cfg["M"], seed=4)
-    pt = P.encode(P.pack(x, m)[0], scale=P.scale(12), level=12)
+    top = pre["bts"]["out_level"]
+    pt = P.encode(P.pack(x, m)[0], scale=hs.softmax_input_scale(P, tab["exp"], top), level=top)
     O.ledger_reset()
-    out = O.softmax_bts(PO, KO, [O.encrypt(PO, KO, pt, 12, 4040, 0)], n, k, "A", tab["exp"], tab["inv"], BO)
+    out = O.softmax_bts(PO, KO, [O.encrypt(PO, KO, pt, top, 4040, 0)], n, k, "A", tab["exp"], tab["inv"], BO)
     led = O.ledger()
-    s = hs.softmax_schedule(P, n, m, k, "A", tab["exp"], tab["inv"], 12, bts_out_level=pre["bts"]["out_level"])
+    s = hs.softmax_schedule(P, n, m, k, "A", tab["exp"], tab["inv"], top, bts_out_level=top)
     assert s["bts_main"] + s["bts_aux"] == led["bts"] > 0
     assert s["bts_main"] >= 1
     assert s["out_level"] == out[0].level
@@ -96,22 +98,22 @@ def test_planner_paper_pins_p16(tables, p16):
     P, bo = p16
     tb, ta = tables["p16_n256_M128_k5_B"], tables["p16_n256_M128_k5_A"]
     # config 3: 64 ciphertexts, version B -- no main-thread bootstrap
-    sb = hs.softmax_schedule(P, 256, 64, 5, "B", tb["exp"], tb["inv"], 12, bts_out_level=bo)
+    sb = hs.softmax_schedule(P, 256, 64, 5, "B", tb["exp"], tb["inv"], bo, bts_out_level=bo)
     assert sb["bts_main"] == 0 and sb["bts_aux"] > 0
     # 2 log2(N0/L) = 4 rotations per aux call, one shared aux ciphertext (G6)
     assert sb["rotations"] == 5 * 2 * 2
     # Alg 1 on the same batch bootstraps every main ciphertext
-    sa = hs.softmax_schedule(P, 256, 64, 5, "A", ta["exp"], ta["inv"], 12, bts_out_level=bo)
+    sa = hs.softmax_schedule(P, 256, 64, 5, "A", ta["exp"], ta["inv"], bo, bts_out_level=bo)
     assert sa["bts_main"] > 0 and sa["bts_main"] % 64 == 0
     # config 2: one ciphertext, 8 + 8 rotations per aux call
-    s2 = hs.softmax_schedule(P, 256, 1, 5, "A", ta["exp"], ta["inv"], 12, bts_out_level=bo)
+    s2 = hs.softmax_schedule(P, 256, 1, 5, "A", ta["exp"], ta["inv"], bo, bts_out_level=bo)
     assert s2["rotations"] == 5 * 2 * 8
     # without bootstrapping the P16 chain cannot hold either (HS_ELEVEL)
     with pytest.raises(hs.HsError) as e:
-        hs.softmax_schedule(P, 256, 64, 5, "B", tb["exp"], tb["inv"], 12)
+        hs.softmax_schedule(P, 256, 64, 5, "B", tb["exp"], tb["inv"], bo)
     assert e.value.code == 2
     # sharding leaves the aux schedule alone: per rank the same bootstraps
-    s8 = hs.softmax_schedule(P, 256, 64, 5, "B", tb["exp"], tb["inv"], 12, world=8, bts_out_level=bo)
+    s8 = hs.softmax_schedule(P, 256, 64, 5, "B", tb["exp"], tb["inv"], bo, world=8, bts_out_level=bo)
     assert s8["bts_aux"] == sb["bts_aux"] and s8["exchanges"] == 5 and s8["out_level"] == sb["out_level"]
 
 
@@ -122,14 +124,14 @@ def test_choose_follows_tab_smmany(tables, p16):
     cands = _cands(tables, ["p16_n256_M128_k5_A", "p16_n256_M128_k5_B"])
     picks = []
     for m in [1, 2, 4, 8, 16, 32, 64]:
-        best, sched = hs.softmax_choose(P, cands, 256, m, 12, bts_out_level=bo)
+        best, sched = hs.softmax_choose(P, cands, 256, m, bo, bts_out_level=bo)
         assert sched[best]["cost"] == min(s["cost"] for s in sched)
         picks.append(cands[best]["variant"])
     assert picks[0] == "A" and picks[-1] == "B"
     flip = picks.index("B")
     assert all(p == "B" for p in picks[flip:])
     # main-thread bootstraps drive the choice: Alg 1's cost grows with m
-    costs = [hs.softmax_choose(P, cands, 256, m, 12, bts_out_level=bo)[1][0]["cost"] for m in (1, 64)]
+    costs = [hs.softmax_choose(P, cands, 256, m, bo, bts_out_level=bo)[1][0]["cost"] for m in (1, 64)]
     assert costs[1] > 4 * costs[0]
 
 
@@ -138,11 +140,11 @@ def test_choose_errors(tables, p16):
     cands = _cands(tables, ["p16_n256_M128_k5_A", "p16_n256_M128_k5_B"])
     # no bootstrapping: nothing fits the P16 chain -> HS_ELEVEL
     with pytest.raises(hs.HsError) as e:
-        hs.softmax_choose(P, cands, 256, 64, 12)
+        hs.softmax_choose(P, cands, 256, 64, bo)
     assert e.value.code == 2
     # an unfit candidate is skipped (cost = inf), the other chosen
     short = dict(cands[1], inv=cands[1]["inv"][:1], k=1)
-    best, sched = hs.softmax_choose(P, [cands[0], short], 256, 1, 12, bts_out_level=bo)
+    best, sched = hs.softmax_choose(P, [cands[0], short], 256, 1, bo, bts_out_level=bo)
     assert best in (0, 1) and all(np.isfinite(s["cost"]) or s["cost"] == float("inf") for s in sched)
     with pytest.raises(hs.HsError):
-        hs.softmax_choose(P, [dict(cands[0], k=0)], 256, 1, 12, bts_out_level=bo)
+        hs.softmax_choose(P, [dict(cands[0], k=0)], 256, 1, bo, bts_out_level=bo)

@@ -40,20 +40,23 @@ PRESETS = {
     # N = 2^12 with a deep chain (28 Q limbs): toy Softmax with k = 2 (parity only)
     "TOY12D": dict(log_n=12, q_bits=[60] + [40] * 27, p_bits=[61, 61, 61], alpha=3,
                    log2_anchor=_anchors(28, [(27, 40)]), h=192),
-    # configs 2-5: N = 2^16, FGb-shaped.  Levels: 0 (60b), 1-12 user (42b, Delta=2^42:
+    # configs 2-5: N = 2^16, FGb-shaped.  Levels: 0 (60b), 1-13 user (42b, Delta=2^42:
     # at N = 2^16 a fresh encryption's slot noise is ~2^-20.4 at Delta = 2^40 and
-    # bounds everything downstream),
-    # 13-15 SlotToCoeff (48b), 16-26 EvalMod + arcsine (~2^59: cosine series 6
+    # bounds everything downstream; the 13th user
+    # level lets version B's fourth aux iteration -- x^-1/2^4 (5 levels),
+    # lambda lambda_j and the mask from a fresh bootstrap -- stay above the 6
+    # levels its main update needs: 7 instead of 8 bootstraps for config 3),
+    # 14-16 SlotToCoeff (48b), 17-27 EvalMod + arcsine (~2^59: cosine series 6
     # levels with the level-exact C13, 3 double angles, arcsine 2),
-    # 27-30 CoeffToSlot (60b); 5 special primes of 61 bits (alpha = 5, dnum = 7).
-    "P16": dict(log_n=16, q_bits=[60] + [42] * 12 + [48] * 3 + [59] * 11 + [60] * 4, p_bits=[61] * 5, alpha=5,
-                log2_anchor=_anchors(31, [(30, 60), (29, 63), (28, 62), (27, 60), (26, 59), (14, 48), (13, 48),
-                                          (12, 42)]),
-                h=192, bts=dict(table="K24_r3_d63", n_cts=4, n_stc=3, arcsine=True, out_level=12)),
+    # 28-31 CoeffToSlot (60b); 5 special primes of 61 bits (alpha = 5, dnum = 7).
+    "P16": dict(log_n=16, q_bits=[60] + [42] * 13 + [48] * 3 + [59] * 11 + [60] * 4, p_bits=[61] * 5, alpha=5,
+                log2_anchor=_anchors(32, [(31, 60), (30, 63), (29, 62), (28, 60), (27, 59), (15, 48), (14, 48),
+                                          (13, 42)]),
+                h=192, bts=dict(table="K24_r3_d63", n_cts=4, n_stc=3, arcsine=True, out_level=13)),
     # N = 2^16 with only the user chain (levels 0-12): primitive parity and
     # key-switch measurements at the user levels without BTS-sized keys.
-    "P16U": dict(log_n=16, q_bits=[60] + [42] * 12, p_bits=[61] * 5, alpha=5,
-                 log2_anchor=_anchors(13, [(12, 42)]), h=192),
+    "P16U": dict(log_n=16, q_bits=[60] + [42] * 13, p_bits=[61] * 5, alpha=5,
+                 log2_anchor=_anchors(14, [(13, 42)]), h=192),
 }
 
 

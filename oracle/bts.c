@@ -626,3 +626,27 @@ orc_ct *orc_bootstrap(const orc_params *P, const orc_keys *K, const orc_ct *in, 
     orc_ledger[LG_BTS]++;
     return out;
 }
+
+/* test hook (tests/test_oracle_bts_transforms.py): the dense float matrix of
+ * the special-FFT stage group [first, first + size) of ring degree 2^log_n,
+ * forward (SlotToCoeff) or inverse (CoeffToSlot), as the plan builds it
+ * before its scaling factors: A[p][c] = diag_{(c - p) mod N0}[p]. */
+void orc_api_sfft_group(int log_n, int first, int size, int inverse, double *re, double *im)
+{
+    orc_params P0;
+    memset(&P0, 0, sizeof(P0));
+    P0.log_n = log_n;
+    P0.n = 1 << log_n;
+    dmat *m = group_matrix(&P0, first, size, inverse);
+    int n0 = m->n0;
+    memset(re, 0, sizeof(double) * n0 * n0);
+    memset(im, 0, sizeof(double) * n0 * n0);
+    for (int d = 0; d < n0; d++) {
+        if (!m->present[d]) continue;
+        for (int p = 0; p < n0; p++) {
+            re[(size_t)p * n0 + (p + d) % n0] = (double)m->diag[d][p].re;
+            im[(size_t)p * n0 + (p + d) % n0] = (double)m->diag[d][p].im;
+        }
+    }
+    dm_free(m);
+}

@@ -56,7 +56,12 @@ typedef enum {
 
 typedef struct hs_params hs_params;   /* host tables (primes, twiddles, BConv)  */
 typedef struct hs_ctx hs_ctx;         /* one GPU: device tables, pools, ledger  */
-typedef struct hs_keys hs_keys;       /* secret, public and evaluation keys     */
+typedef struct hs_keys hs_keys;       /* device key set (public + evaluation keys,
+                                         and the secret only when generated on the
+                                         device by hs_ckks_keygen)              */
+typedef struct hs_secret_key hs_secret_key; /* host: the client's secret s         */
+typedef struct hs_public_key hs_public_key; /* host: pk = (-a s + e, a)            */
+typedef struct hs_eval_keys hs_eval_keys;   /* host: relinearisation + Galois keys */
 typedef struct hs_ct hs_ct;           /* a device ciphertext                    */
 
 /* Last error message of the calling thread ("" if none). */
@@ -95,10 +100,48 @@ hs_status hs_context_create(const hs_params *p, int device, hs_ctx **out);
 void hs_context_destroy(hs_ctx *c);
 
 /* ------------------------------------------------------------ keys (C5-C7) */
-/* Keys are generated on the device from the counter-based ChaCha20 stream of
- * DESIGN.md C5 keyed by `seed`: secret with Hamming weight h, public key,
- * relinearisation key (if relin != 0) and one switching key per Galois
- * element in galois[0..n_galois).  Immutable after creation. */
+/* Client / server split (PAPER.md 262-271 [sec 2.2.1]: KeyGen(lambda, S) ->
+ * pk, sk, evk, rotation keys; Enc, Dec with sk; Mult / Rot with evk).
+ *
+ * hs_ckks_keygen_host runs KeyGen on the HOST (no device, thread-safe), from
+ * the counter-based ChaCha20 stream of DESIGN.md C5 keyed by `seed`: secret s
+ * of Hamming weight h (C5), pk = (-a s + e, a) over Q_L (C6), and the
+ * switching keys of C7 -- relinearisation (s' = s^2) if relin != 0, then one
+ * per Galois element galois[0..n_galois) (s' = sigma_k(s)).  The words equal
+ * those of hs_ckks_keygen and of the oracle for the same seed.  Outputs are
+ * host objects owned by the caller (hs_*_destroy).  HS_EINVAL if h is not in
+ * [1, N] or a pointer is NULL.
+ *
+ * hs_keys_upload builds a device key set from pk (nullable: then no public-key
+ * encryption) and evk only: it holds NO secret -- hs_ckks_decrypt, secret-key
+ * encryption and hs_keys_export_secret return HS_EKEY on it -- and serves every
+ * evaluation (scheme ops, bootstrapping, Softmax).  Synchronous; the host
+ * objects may be destroyed afterwards.  HS_EINVAL if they belong to another
+ * parameter set.
+ *
+ * hs_ckks_decrypt_host: words = ncomp x (level+1) x N ciphertext words (NTT
+ * domain, host, e.g. from hs_ct_export), out = (level+1) x N coefficient
+ * residues of c0 + c1 s (+ c2 s^2 when ncomp = 3).  Host only. */
+hs_status hs_ckks_keygen_host(const hs_params *p, uint64_t seed, int h, const int32_t *galois, size_t n_galois,
+                              int relin, hs_secret_key **sk, hs_public_key **pk, hs_eval_keys **evk);
+hs_status hs_keys_upload(hs_ctx *c, const hs_public_key *pk, const hs_eval_keys *evk, void *stream,
+                         hs_keys **out);
+hs_status hs_ckks_decrypt_host(const hs_secret_key *sk, const uint64_t *words, int level, int ncomp,
+                               uint64_t *out);
+/* test hooks on the host objects: secret coefficients (N int64); number of
+ * switching keys; switching key of Galois element `galois` (0 = relin) as
+ * planar [dnum][2][n_q+n_p][N] (HS_EKEY if absent); pk words [2][n_q][N]. */
+hs_status hs_secret_key_export(const hs_secret_key *sk, int64_t *out);
+size_t hs_eval_keys_count(const hs_eval_keys *e);
+hs_status hs_eval_keys_export(const hs_eval_keys *e, int galois, uint64_t *out);
+hs_status hs_public_key_export(const hs_public_key *pk, uint64_t *out);
+void hs_secret_key_destroy(hs_secret_key *sk);
+void hs_public_key_destroy(hs_public_key *pk);
+void hs_eval_keys_destroy(hs_eval_keys *e);
+
+/* Device keygen (tests and benches: one call builds a full key set, secret
+ * included, on the evaluating GPU): the same words as hs_ckks_keygen_host.
+ * Immutable after creation. */
 hs_status hs_ckks_keygen(hs_ctx *c, uint64_t seed, int h, const int32_t *galois, size_t n_galois,
                          int relin, void *stream, hs_keys **out);
 void hs_keys_destroy(hs_keys *k);

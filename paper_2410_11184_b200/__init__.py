@@ -147,6 +147,66 @@ class Keys:
         return s
 
 
+class HostKeys:
+    """hs_ckks_keygen_host: the client's KeyGen on the host (PAPER.md 262-271):
+    secret, public key and evaluation keys as host objects.  upload(ctx) gives
+    the server a device key set WITHOUT the secret (hs_keys_upload);
+    decrypt_decode(ct) decrypts exported words with the host secret."""
+
+    def __init__(self, params: Params, seed: int, h: int, galois=(), relin=True):
+        self.params = params
+        g = np.array(list(galois) or [0], np.int32)
+        sk, pk, evk = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        check(L.hs_ckks_keygen_host(params.ptr, seed, h, g, len(galois), 1 if relin else 0, C.byref(sk),
+                                    C.byref(pk), C.byref(evk)))
+        self.sk, self.pk, self.evk = sk, pk, evk
+
+    def __del__(self):
+        for name, fn in (("sk", "hs_secret_key_destroy"), ("pk", "hs_public_key_destroy"),
+                         ("evk", "hs_eval_keys_destroy")):
+            if getattr(self, name, None):
+                getattr(L, fn)(getattr(self, name))
+                setattr(self, name, None)
+
+    def upload(self, ctx: Context, with_pk=True, stream=None) -> "Keys":
+        out = C.c_void_p()
+        check(L.hs_keys_upload(ctx.ptr, self.pk if with_pk else None, self.evk, _stream(stream), C.byref(out)))
+        k = Keys.__new__(Keys)
+        k.ctx, k.ptr = ctx, out
+        return k
+
+    def secret(self):
+        s = np.zeros(self.params.n, np.int64)
+        check(L.hs_secret_key_export(self.sk, s))
+        return s
+
+    def swk(self, galois):
+        P = self.params
+        o = np.zeros(P.dnum * 2 * (P.n_q + P.n_p) * P.n, np.uint64)
+        check(L.hs_eval_keys_export(self.evk, galois, o))
+        return o.reshape(P.dnum, 2, P.n_q + P.n_p, P.n)
+
+    def pk_words(self):
+        P = self.params
+        o = np.zeros(2 * P.n_q * P.n, np.uint64)
+        check(L.hs_public_key_export(self.pk, o))
+        return o.reshape(2, P.n_q, P.n)
+
+    def decrypt(self, words):
+        """words: ncomp x (level+1) x N (e.g. Ciphertext.words()) -> coefficient residues"""
+        words = np.ascontiguousarray(words, np.uint64)
+        nc, l1, n = words.shape
+        o = np.zeros(l1 * n, np.uint64)
+        check(L.hs_ckks_decrypt_host(self.sk, words.ravel(), l1 - 1, nc, o))
+        return o.reshape(l1, n)
+
+    def decrypt_decode(self, ct, level_scale=None):
+        w = ct.words() if hasattr(ct, "words") else ct
+        m = self.decrypt(w)
+        level = m.shape[0] - 1
+        return self.params.decode(m[0], self.params.scale(level) if level_scale is None else level_scale)
+
+
 class Ciphertext:
     def __init__(self, ctx: Context, ptr, owner=None):
         # owner: the object that owns a borrowed handle (a Plan's outputs)

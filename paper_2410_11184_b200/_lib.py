@@ -89,6 +89,17 @@ hs_context_destroy = _sig("hs_context_destroy", None, [vp])
 hs_ckks_keygen = _sig("hs_ckks_keygen", C.c_int,
                       [vp, C.c_uint64, C.c_int, i32p, C.c_size_t, C.c_int, vp, C.POINTER(vp)])
 hs_keys_destroy = _sig("hs_keys_destroy", None, [vp])
+hs_ckks_keygen_host = _sig("hs_ckks_keygen_host", C.c_int, [vp, C.c_uint64, C.c_int, i32p, C.c_size_t, C.c_int,
+                                                            C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)])
+hs_keys_upload = _sig("hs_keys_upload", C.c_int, [vp, vp, vp, vp, C.POINTER(vp)])
+hs_ckks_decrypt_host = _sig("hs_ckks_decrypt_host", C.c_int, [vp, u64p, C.c_int, C.c_int, u64p])
+hs_secret_key_export = _sig("hs_secret_key_export", C.c_int, [vp, i64p])
+hs_eval_keys_count = _sig("hs_eval_keys_count", C.c_size_t, [vp])
+hs_eval_keys_export = _sig("hs_eval_keys_export", C.c_int, [vp, C.c_int, u64p])
+hs_public_key_export = _sig("hs_public_key_export", C.c_int, [vp, u64p])
+hs_secret_key_destroy = _sig("hs_secret_key_destroy", None, [vp])
+hs_public_key_destroy = _sig("hs_public_key_destroy", None, [vp])
+hs_eval_keys_destroy = _sig("hs_eval_keys_destroy", None, [vp])
 hs_keys_export_swk = _sig("hs_keys_export_swk", C.c_int, [vp, vp, C.c_int, u64p])
 hs_keys_export_secret = _sig("hs_keys_export_secret", C.c_int, [vp, vp, i64p])
 hs_ckks_encode = _sig("hs_ckks_encode", C.c_int, [vp, f64p, vp, C.c_size_t, C.c_int, C.c_double, u64p])

@@ -158,11 +158,82 @@ hs_status hs_keys_export_swk(hs_ctx *c, const hs_keys *k, int galois, uint64_t *
 hs_status hs_keys_export_secret(hs_ctx *c, const hs_keys *k, int64_t *host_out)
 {
     HS_TRY
+    if (!k || !host_out) throw HsError(HS_EINVAL, "NULL argument");
+    if (!k->s_ntt) throw HsError(HS_EKEY, "this key set holds no secret (hs_keys_upload)");
     memcpy(host_out, k->s_coeff.data(), k->s_coeff.size() * 8);
     (void)c;
     return HS_OK;
     HS_CATCH
 }
+
+hs_status hs_ckks_keygen_host(const hs_params *p, uint64_t seed, int h, const int32_t *galois, size_t n_galois,
+                              int relin, hs_secret_key **sk, hs_public_key **pk, hs_eval_keys **evk)
+{
+    HS_TRY
+    if (!p || !sk || !pk || !evk || (n_galois && !galois)) throw HsError(HS_EINVAL, "NULL argument");
+    keygen_host(p, seed, h, galois, n_galois, relin, sk, pk, evk);
+    return HS_OK;
+    HS_CATCH
+}
+
+hs_status hs_keys_upload(hs_ctx *c, const hs_public_key *pk, const hs_eval_keys *evk, void *stream, hs_keys **out)
+{
+    HS_TRY
+    if (!c || !evk || !out) throw HsError(HS_EINVAL, "NULL argument");
+    activate(c);
+    *out = keys_upload(c, pk, evk, S(stream));
+    return HS_OK;
+    HS_CATCH
+}
+
+hs_status hs_ckks_decrypt_host(const hs_secret_key *sk, const uint64_t *words, int level, int ncomp, uint64_t *out)
+{
+    HS_TRY
+    if (!sk || !words || !out) throw HsError(HS_EINVAL, "NULL argument");
+    decrypt_host(sk, words, level, ncomp, out);
+    return HS_OK;
+    HS_CATCH
+}
+
+hs_status hs_secret_key_export(const hs_secret_key *sk, int64_t *out)
+{
+    HS_TRY
+    if (!sk || !out) throw HsError(HS_EINVAL, "NULL argument");
+    const std::vector<int64_t> &s = secret_coeffs(sk);
+    memcpy(out, s.data(), s.size() * 8);
+    return HS_OK;
+    HS_CATCH
+}
+
+size_t hs_eval_keys_count(const hs_eval_keys *e) { return e ? evk_count(e) : 0; }
+
+hs_status hs_eval_keys_export(const hs_eval_keys *e, int galois, uint64_t *out)
+{
+    HS_TRY
+    if (!e || !out) throw HsError(HS_EINVAL, "NULL argument");
+    for (size_t i = 0; i < evk_count(e); i++)
+        if (evk_galois(e, i) == galois) {
+            const std::vector<u64> &w = evk_words(e, i);
+            memcpy(out, w.data(), w.size() * 8);
+            return HS_OK;
+        }
+    throw HsError(HS_EKEY, "no such switching key");
+    HS_CATCH
+}
+
+hs_status hs_public_key_export(const hs_public_key *pk, uint64_t *out)
+{
+    HS_TRY
+    if (!pk || !out) throw HsError(HS_EINVAL, "NULL argument");
+    const std::vector<u64> &w = pk_words(pk);
+    memcpy(out, w.data(), w.size() * 8);
+    return HS_OK;
+    HS_CATCH
+}
+
+void hs_secret_key_destroy(hs_secret_key *sk) { secret_destroy(sk); }
+void hs_public_key_destroy(hs_public_key *pk) { pk_destroy(pk); }
+void hs_eval_keys_destroy(hs_eval_keys *e) { evk_destroy(e); }
 
 hs_status hs_ckks_encode(const hs_params *p, const double *re, const double *im, size_t n_slots, int level,
                          double scale, uint64_t *out)

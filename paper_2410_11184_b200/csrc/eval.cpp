@@ -877,6 +877,8 @@ CtP ev_encrypt(const hs_keys *K, const u64 *pt_host, int level, u64 seed, u64 id
     CtP r = ct_new(c, level, 2, st);
     u64 *c0 = r->limb(0, 0), *c1 = r->limb(1, 0);
     DBuf tmp((size_t)nl * N, st);
+    if (use_sk && !K->s_ntt) throw HsError(HS_EKEY, "encrypt: this key set holds no secret (hs_keys_upload)");
+    if (!use_sk && !K->pk) throw HsError(HS_EKEY, "encrypt: this key set holds no public key");
     if (use_sk) {
         k_uniform(c, c1, nl, pmap_range(0, nl), seed, TAG_ENC_A, idx, 0, st);
         error_poly(c, seed, TAG_ENC_E0, idx, ETA_ERR, c0, nl, st);
@@ -905,6 +907,7 @@ void ev_decrypt(const hs_keys *K, const hs_ct *ct, u64 *host_out, cudaStream_t s
     const size_t N = c->P->n;
     const int nl = ct->level + 1;
     if (ct->batch != 1) throw HsError(HS_EINVAL, "decrypt one ciphertext at a time");
+    if (!K->s_ntt) throw HsError(HS_EKEY, "decrypt: this key set holds no secret (hs_keys_upload)");
     DBuf m((size_t)nl * N, st);
     k_mul_pointwise(c, ct->limb(1, 0), K->s_ntt, m.p, nl, nl, nl, st);
     k_add(c, m.p, ct->limb(0, 0), m.p, nl, nl, false, st);

@@ -306,6 +306,22 @@ hs_keys *keys_generate(hs_ctx *c, u64 seed, int h, const int32_t *galois, size_t
 CtP ev_encrypt(const hs_keys *K, const u64 *pt_host, int level, u64 seed, u64 idx, bool use_sk, cudaStream_t st);
 void ev_decrypt(const hs_keys *K, const hs_ct *ct, u64 *host_out, cudaStream_t st);
 
+// keygen_host.cpp (host KeyGen, upload, host decryption)
+void keygen_host(const hs_params *P, u64 seed, int h, const int32_t *galois, size_t n_galois, int relin,
+                 hs_secret_key **sk, hs_public_key **pk, hs_eval_keys **evk);
+hs_keys *keys_upload(hs_ctx *c, const hs_public_key *pk, const hs_eval_keys *evk, cudaStream_t st);
+void decrypt_host(const hs_secret_key *sk, const u64 *words, int level, int ncomp, u64 *out);
+void host_ntt_limb(const hs_params *P, int pi, u64 *a, bool inverse);
+const std::vector<int64_t> &secret_coeffs(const hs_secret_key *sk);
+const hs_params *secret_params(const hs_secret_key *sk);
+size_t evk_count(const hs_eval_keys *e);
+int evk_galois(const hs_eval_keys *e, size_t i);
+const std::vector<u64> &evk_words(const hs_eval_keys *e, size_t i);
+const std::vector<u64> &pk_words(const hs_public_key *p);
+void secret_destroy(hs_secret_key *s);
+void pk_destroy(hs_public_key *p);
+void evk_destroy(hs_eval_keys *e);
+
 // encode.cpp
 void hs_encode_impl(const hs_params *P, const double *re, const double *im, double scale, int level, u64 *out);
 void hs_encode_impl_q(const hs_params *P, const __float128 *re, const __float128 *im, double scale, int level,

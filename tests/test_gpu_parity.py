@@ -533,3 +533,41 @@ def test_softmax_cube_parity(tables):
     ref = np.exp(x - x.max(1, keepdims=True))
     ref /= ref.sum(1, keepdims=True)
     assert np.abs(y - ref).max() < 2.0 ** -15
+
+
+def test_uploaded_keys_softmax_parity(tables):
+    """Client / server split (PAPER.md 262-271; include/hesoftmax.h
+    hs_ckks_keygen_host / hs_keys_upload): keys generated on the HOST, only
+    pk + evk uploaded; the evaluating context holds no secret (decrypt and
+    secret-key encryption refuse with HS_EKEY), yet the config-1 Softmax it
+    computes is word for word the oracle's, and the host secret decrypts it."""
+    hs = _hs()
+    from paper_2410_11184_b200._lib import HsError
+    tab = tables["toy_n16_M2_k1_A"]
+    n, k, m, Lx = 16, 1, 1, 128
+    pre = W.preset("TOY12")
+    P, PO = hs.Params.from_preset(pre), O.Params.from_preset(pre)
+    gal = O.softmax_rotation_galois(PO, n, m)
+    seed = W.derive_seed("keys", "upload")
+    HK = hs.HostKeys(P, seed, pre["h"], galois=gal)
+    ctx = hs.Context(P, 0)
+    K = HK.upload(ctx)
+    KO = O.Keys(PO, seed, pre["h"], galois=gal)
+    assert (K.swk(0) == KO.swk(0)).all()
+    x = W.softmax_inputs(Lx, n, 2.0, seed=W.derive_seed("x", "upload"))
+    top = len(pre["q_bits"]) - 1
+    pt = P.encode(P.pack(x, m)[0], scale=hs.softmax_input_scale(P, tab["exp"], top), level=top)
+    g = hs.encrypt(K, pt, top, 31, 0)          # public-key encryption on the server
+    o = O.encrypt(PO, KO, pt, top, 31, 0)
+    same(g, o)
+    for fn in (lambda: hs.decrypt(K, g), lambda: K.secret(), lambda: hs.encrypt(K, pt, top, 31, 0, use_sk=True)):
+        with pytest.raises(HsError) as e:
+            fn()
+        assert e.value.code == 3
+    out = hs.softmax_one_ctxt(K, g, n, k, "A", tab["exp"], tab["inv"])
+    outo = O.softmax(PO, KO, [o], n, k, "A", tab["exp"], tab["inv"])[0]
+    same(out, outo)
+    y = P.unpack(HK.decrypt_decode(out).real[None], Lx, n)
+    ref = np.exp(x - x.max(1, keepdims=True))
+    ref /= ref.sum(1, keepdims=True)
+    assert np.abs(y - ref).max() < 2.0 ** -15

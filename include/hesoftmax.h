@@ -193,6 +193,16 @@ hs_status hs_ct_gather(hs_ctx *c, const hs_ct *const *cts, int n, void *stream, 
 int hs_ct_batch(const hs_ct *ct);
 hs_status hs_ct_member(hs_ctx *c, const hs_ct *batch, int i, void *stream, hs_ct **out);
 int hs_ct_level(const hs_ct *ct);
+/* Declared encoding scale (C11).  The library computes at the canonical scale
+ * Delta_level of every level (C12) and ciphertexts carry no scale of their
+ * own; a caller that encoded a ciphertext at another scale declares it here
+ * (0 = canonical, the default).  hs_op returns HS_ESCALE for an operand
+ * declared at a scale other than Delta_level (relative 2^-40, C11); the
+ * Softmax entry points return HS_ESCALE for an input declared at a scale other
+ * than hs_softmax_input_scale.  hs_ct_scale returns the declared scale, else
+ * Delta_level. */
+hs_status hs_ct_set_scale(hs_ct *ct, double scale);
+double hs_ct_scale(const hs_ct *ct);
 int hs_ct_ncomp(const hs_ct *ct);
 void hs_ct_destroy(hs_ct *ct);
 
@@ -327,6 +337,14 @@ typedef struct {
  * into the encoding, so the Softmax spends exactly the levels of PAPER.md's
  * depth tables).  Returns 0 on a NULL argument or a level outside the chain. */
 double hs_softmax_input_scale(const hs_params *p, const hs_softmax_desc *d, int level);
+
+/* Debug domain check (SPEC's "domain" error; HS_EDOMAIN): with keys that hold
+ * the secret (hs_ckks_keygen), every eager Softmax on this context decrypts
+ * the aux sum before each inverse-square-root polynomial and returns
+ * HS_EDOMAIN if a slot lies outside the polynomial's interval [a, b] (widened
+ * by 1/64 of its width) -- e.g. an input outside [-M, 0].  NULL disables it.
+ * Debug only: it synchronises the stream and cannot run inside a plan. */
+hs_status hs_ctx_debug_domain(hs_ctx *c, const hs_keys *k);
 
 /* One ciphertext (m = 1). */
 hs_status hs_softmax_one_ctxt(hs_ctx *c, const hs_keys *k, const hs_softmax_desc *d, const hs_ct *in,

@@ -118,6 +118,11 @@ class Context:
     def ledger_reset(self):
         check(L.hs_ledger_reset(self.ptr))
 
+    def debug_domain(self, keys=None):
+        """hs_ctx_debug_domain: eager Softmax calls check the aux sums against
+        the polynomial intervals (HS_EDOMAIN); keys must hold the secret."""
+        check(L.hs_ctx_debug_domain(self.ptr, keys.ptr if keys is not None else None))
+
     def ntt(self, data_ptr, prime_index, n_limbs, inverse=False, stream=None):
         check(L.hs_ntt(self.ptr, prime_index, n_limbs, C.c_void_p(data_ptr), 1 if inverse else 0, _stream(stream)))
 
@@ -224,6 +229,16 @@ class Ciphertext:
     @property
     def ncomp(self):
         return L.hs_ct_ncomp(self.ptr)
+
+    @property
+    def scale(self):
+        """declared encoding scale, else the canonical scale of its level (C11)"""
+        return float(L.hs_ct_scale(self.ptr))
+
+    def set_scale(self, scale):
+        """hs_ct_set_scale: declare the scale this ciphertext was encoded at"""
+        check(L.hs_ct_set_scale(self.ptr, float(scale)))
+        return self
 
     def words(self, stream=None):
         P = self.ctx.params

@@ -112,6 +112,9 @@ hs_ckks_decrypt = _sig("hs_ckks_decrypt", C.c_int, [vp, vp, vp, u64p, vp])
 hs_ct_import = _sig("hs_ct_import", C.c_int, [vp, C.c_int, C.c_int, vp, C.c_int, vp, C.POINTER(vp)])
 hs_ct_export = _sig("hs_ct_export", C.c_int, [vp, vp, vp, C.c_int, vp])
 hs_ct_level = _sig("hs_ct_level", C.c_int, [vp])
+hs_ct_set_scale = _sig("hs_ct_set_scale", C.c_int, [vp, C.c_double])
+hs_ct_scale = _sig("hs_ct_scale", C.c_double, [vp])
+hs_ctx_debug_domain = _sig("hs_ctx_debug_domain", C.c_int, [vp, vp])
 hs_ct_ncomp = _sig("hs_ct_ncomp", C.c_int, [vp])
 hs_ct_destroy = _sig("hs_ct_destroy", None, [vp])
 hs_ct_write = _sig("hs_ct_write", C.c_int, [vp, vp, vp, C.c_int, vp])

@@ -46,6 +46,17 @@ static void activate(hs_ctx *c)
     }
 }
 
+void check_scales(const hs_ct *a, const hs_ct *b)
+{
+    const hs_params *P = a->ctx->P;
+    for (const hs_ct *x : {a, b}) {
+        if (x->scale == 0.0) continue;
+        const double canon = P->scale[x->level];
+        if (fabs(x->scale / canon - 1.0) > ldexp(1.0, -40))
+            throw HsError(HS_ESCALE, "operand declared at a non-canonical scale (C11)");
+    }
+}
+
 extern "C" {
 
 const char *hs_last_error(void) { return g_err.c_str(); }
@@ -394,6 +405,10 @@ hs_status hs_op(hs_ctx *c, const hs_keys *k, int op, const hs_ct *a, const hs_ct
     CtP r;
     auto need_b = [&]() { if (!b) throw HsError(HS_EINVAL, "second operand missing"); };
     auto need_k = [&]() { if (!k) throw HsError(HS_EKEY, "keys missing"); };
+    // C11: the library computes at canonical scales; an operand declared at
+    // another scale (hs_ct_set_scale) cannot be combined
+    if (b) check_scales(a, b);
+    else check_scales(a, a);
     switch (op) {
     case HS_OP_ADD: need_b(); r = ev_add(a, b, false, st); break;
     case HS_OP_SUB: need_b(); r = ev_add(a, b, true, st); break;
@@ -503,6 +518,31 @@ hs_status hs_softmax_many_ctxt(hs_ctx *c, const hs_keys *k, const hs_softmax_des
     if (!c || !k || !d || !in || !out) throw HsError(HS_EINVAL, "NULL argument");
     activate(c);
     return softmax_run(c, k, d, in, m_local, S(stream), out);
+    HS_CATCH
+}
+
+hs_status hs_ct_set_scale(hs_ct *ct, double scale)
+{
+    HS_TRY
+    if (!ct || !(scale >= 0.0)) throw HsError(HS_EINVAL, "bad ciphertext or scale");
+    ct->scale = scale;
+    return HS_OK;
+    HS_CATCH
+}
+
+double hs_ct_scale(const hs_ct *ct)
+{
+    if (!ct) return 0.0;
+    return ct->scale != 0.0 ? ct->scale : ct->ctx->P->scale[ct->level];
+}
+
+hs_status hs_ctx_debug_domain(hs_ctx *c, const hs_keys *k)
+{
+    HS_TRY
+    if (!c) throw HsError(HS_EINVAL, "NULL context");
+    if (k && !k->s_ntt) throw HsError(HS_EKEY, "the domain check decrypts: keys with the secret needed");
+    c->debug_keys = k;
+    return HS_OK;
     HS_CATCH
 }
 

@@ -96,6 +96,7 @@ struct hs_ctx {
     std::map<std::pair<u64, long>, u64 *> pt_cache;  // (content hash, level pair) -> NTT plaintext
     std::mutex mu;
     int64_t ledger[HS_LG_COUNT] = {0};
+    const hs_keys *debug_keys = nullptr;  // hs_ctx_debug_domain: keys WITH the secret
     bool kprof_on = false;
     std::vector<cudaEvent_t> kprof_ev;       // pairs (start, end)
     std::vector<int> kprof_id;
@@ -132,6 +133,8 @@ struct hs_ct {
     u64 *d = nullptr;           // [batch][ncomp][level+1][N]
     cudaStream_t st = nullptr;  // stream the buffer is ordered on
     bool owns = true;           // false: a view into another ciphertext's buffer
+    double scale = 0.0;         // declared encoding scale (hs_ct_set_scale); 0 = the
+                                // canonical scale of its level (C11, C12)
     ~hs_ct();
     size_t rows() const { return (size_t)batch * ncomp; }
     size_t limbs() const { return rows() * (level + 1); }
@@ -344,6 +347,7 @@ hs_comm *comm_create(int rank, int world, const uint8_t uid[128]);
 void comm_destroy(hs_comm *comm);
 int comm_world(const hs_comm *c);
 void comm_all_gather(const hs_comm *c, const u64 *partial, u64 *gathered, size_t words, cudaStream_t st);
+void check_scales(const hs_ct *a, const hs_ct *b);  // C11: HS_ESCALE on a mismatch
 hs_status softmax_run(hs_ctx *c, const hs_keys *K, const hs_softmax_desc *d, const hs_ct *const *in,
                       size_t m_local, cudaStream_t st, hs_ct **out);
 void softmax_schedule(const hs_params *P, const hs_softmax_desc *d, int in_level, size_t m_local, int bts_out_level,

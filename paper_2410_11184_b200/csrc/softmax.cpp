@@ -126,6 +126,25 @@ struct RealEx {
         }
         return ct_gather(ptrs.data(), b, st);
     }
+    // hs_ctx_debug_domain: decrypt the aux sum (it holds alpha S, G28) and
+    // check every slot against the polynomial's interval
+    void domain_check(const T *S, const hs_poly *p)
+    {
+        if (!c->debug_keys) return;
+        const hs_params *P = c->P;
+        const size_t N = P->n;
+        std::vector<u64> m((size_t)(S->level + 1) * N);
+        CtP one = ct_slice(S, 0, st);
+        ev_decrypt(c->debug_keys, one.get(), m.data(), st);
+        std::vector<double> re(N / 2), im(N / 2);
+        hs_decode_impl(P, m.data(), P->scale[S->level], re.data(), im.data());
+        const double alpha = 2.0 / (p->b - p->a), tol = (p->b - p->a) / 64.0;
+        for (size_t j = 0; j < N / 2; j++) {
+            const double v = re[j] / alpha;
+            if (!(v >= p->a - tol && v <= p->b + tol))
+                throw HsError(HS_EDOMAIN, "softmax: aux sum outside the polynomial interval (input outside [-M, 0]?)");
+        }
+    }
     // all-gather of the partial aux sums, added in rank order (exact)
     void exchange(T *acc, int world)
     {
@@ -217,6 +236,7 @@ struct SymEx {
         return mk(bts_out, 2, y->batch);
     }
     void exchange(T *, int) { s->exchanges += 1; }
+    void domain_check(const T *, const hs_poly *) {}
 };
 
 template <class E>
@@ -307,6 +327,7 @@ typename E::Ct softmax_body(E &ex, const hs_params *P, const hs_softmax_desc *d,
             if (ex.has_bts()) S = ex.bootstrap(S.get(), affine_alpha(ip) * ip->b);
             else if (S->level - need < 0) level_error("aux thread needs bootstrapping");
         }
+        ex.domain_check(S.get(), ip);
         CtP lj = ex.cheb(S.get(), ip, 1.0);  // S holds alpha_j S (G28)
         if (nt > 0) {
             // G24 (n): bootstrap the seed when the Newton steps and the mask
@@ -374,6 +395,15 @@ typename E::Ct softmax_body(E &ex, const hs_params *P, const hs_softmax_desc *d,
 hs_status softmax_run(hs_ctx *c, const hs_keys *K, const hs_softmax_desc *d, const hs_ct *const *in,
                       size_t m_local, cudaStream_t st, hs_ct **out)
 {
+    // the G28 input contract: an input declared at another scale than the
+    // Softmax reads is rejected (C11)
+    if (d && d->exp_poly && d->exp_poly->b > d->exp_poly->a)
+        for (size_t i = 0; i < m_local; i++) {
+            if (!in[i] || in[i]->scale == 0.0) continue;
+            const double want = c->P->scale[in[i]->level] * (2.0 / (d->exp_poly->b - d->exp_poly->a));
+            if (fabs(in[i]->scale / want - 1.0) > ldexp(1.0, -40))
+                throw HsError(HS_ESCALE, "softmax: input not encoded at hs_softmax_input_scale (G28)");
+        }
     RealEx ex{c, K, d, st};
     CtP y = softmax_body(ex, c->P, d, in, m_local);
     const int ml = (int)m_local;

@@ -434,8 +434,9 @@ def test_softmax_newton_parity(toyb, tables):
 def test_softmax_error_paths(tables):
     """hs_status contract of hs_softmax_many_ctxt (include/hesoftmax.h): a
     missing rotation key -> HS_EKEY, a schedule deeper than the chain without
-    bootstrapping -> HS_ELEVEL, inconsistent descriptors -> HS_EINVAL; the
-    context stays usable afterwards."""
+    bootstrapping -> HS_ELEVEL, inconsistent descriptors -> HS_EINVAL, an input
+    declared at the wrong scale -> HS_ESCALE, an input outside [-M, 0] with the
+    debug domain check on -> HS_EDOMAIN; the context stays usable afterwards."""
     hs = _hs()
     from paper_2410_11184_b200._lib import HsError
     tab = tables["toy_n16_M2_k1_A"]
@@ -465,8 +466,23 @@ def test_softmax_error_paths(tables):
     assert code(lambda: hs.softmax_many_ctxt(K_full, [ct], n, 1, k, 1, tab["exp"], inv_nt)) == 1
     assert code(lambda: hs.softmax_many_ctxt(K_full, [ct, ct, ct], n, 3, k, 0, tab["exp"], tab["inv"])) == 1
     assert code(lambda: hs.softmax_many_ctxt(K_full, [ct, ct], n, 4, k, 0, tab["exp"], tab["inv"])) == 1
+    # HS_ESCALE (C11): an input declared at the canonical scale instead of the
+    # G28 input scale; a scheme op on an operand declared off-canonical
+    wrong = hs.encrypt(K_full, P.encode(slots[0], scale=P.scale(top), level=top), top, 1, 2)
+    wrong.set_scale(P.scale(top))
+    assert code(lambda: hs.softmax_many_ctxt(K_full, [wrong], n, 1, k, 0, tab["exp"], tab["inv"])) == 4
+    ct.set_scale(sc(top))  # the right declaration passes
+    assert code(lambda: hs.op(K_full, "mult", ct, ct)) == 4
+    # HS_EDOMAIN (debug): an input outside [-M, 0] puts the aux sum outside the
+    # first inverse-square-root interval
+    ctx.debug_domain(K_full)
+    bad = hs.encrypt(K_full, P.encode(P.pack(x + 2.0, 1)[0], scale=sc(top), level=top), top, 1, 3)
+    assert code(lambda: hs.softmax_many_ctxt(K_full, [bad], n, 1, k, 0, tab["exp"], tab["inv"])) == 6
+    ok_dbg = hs.softmax_many_ctxt(K_full, [ct], n, 1, k, 0, tab["exp"], tab["inv"])  # in-domain passes
+    ctx.debug_domain(None)
     # still usable: a valid call afterwards decrypts to Softmax
     out = hs.softmax_many_ctxt(K_full, [ct], n, 1, k, 0, tab["exp"], tab["inv"])
+    assert (out[0].words() == ok_dbg[0].words()).all()
     y = P.unpack(hs.decrypt_decode(K_full, out[0]).real[None], 8, n)
     ref = np.exp(x - x.max(1, keepdims=True))
     ref /= ref.sum(1, keepdims=True)

@@ -155,13 +155,16 @@ def build_setup(wl_name, rank, world, device):
     ml = m // world
     mine = range(rank * ml, (rank + 1) * ml)
     top = bcfg["out_level"]
-    from concurrent.futures import ThreadPoolExecutor
-    with ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1)) as ex:
-        sc = hs.softmax_input_scale(P, tab["exp"], top)  # DESIGN.md G28 input contract
-        pts = list(ex.map(lambda c: P.encode(slots[c], scale=sc, level=top), mine))
-    cts = [hs.encrypt(K, pt, top, W.derive_seed("enc", wl_name), c) for pt, c in zip(pts, mine)]
+    # the input level the planner picks (hs_softmax_input_level: the cheapest
+    # schedule; the main thread needs only the levels its updates consume)
+    in_level = int(os.environ.get("HS_INPUT_LEVEL", "-1"))
+    if in_level < 0:
+        in_level = hs.softmax_input_level(P, n, m, k, wl["variant"], tab["exp"], tab["inv"], world, top)
+    # G28 client step: encode at in_level + 1, encrypt, rescale (hs_softmax_encrypt_input)
+    cts = [hs.softmax_encrypt_input(K, slots[c], in_level, tab["exp"], W.derive_seed("enc", wl_name), c)
+           for c in mine]
     return dict(hs=hs, P=P, ctx=ctx, K=K, B=B, cts=cts, x=x, wl=wl, tab=tab, n=n, m=m, k=k, L=L, ml=ml,
-                setup_s=time.time() - t0, top=top)
+                setup_s=time.time() - t0, top=top, in_level=in_level)
 
 
 def make_comm(hs, ctx, rank, world):
@@ -333,7 +336,7 @@ def run_ours(args):
     else:
         desc, paper_ms, paper_ref = OTHER_WORKLOADS[args.workload]
         metric = f"ms/Softmax ({args.workload}, dim {S['n']}, N=2^16)"
-    in_mib = (S["top"] + 1) * 2 * S["P"].n * 8 * len(S["cts"]) / 2 ** 20
+    in_mib = (S["in_level"] + 1) * 2 * S["P"].n * 8 * len(S["cts"]) / 2 ** 20
     line = {
         "metric": metric, "value": round(value, 5), "unit": "ms/Softmax", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": False, "scaling": "strong",
@@ -341,6 +344,9 @@ def run_ours(args):
         "dtype": "u64 (RNS residues)", "data": "synthetic (x ~ N(-M/2,(M/6)^2) tail-cut)",
         "config": {"workload": desc, "preset": S["wl"]["preset"],
                    "softmax_per_step": softmax_per_step, "ciphertexts": S["m"],
+                   "input_level": S["in_level"],
+                   "input": ("x encrypted at input_level + 1 (planner: hs_softmax_input_level), rescaled once "
+                             "(hs_softmax_encrypt_input, DESIGN.md G28)"),
                    "l2": (f"inputs {in_mib:.0f} MiB; every step runs the whole Softmax (>= {S['k']} bootstraps "
                           f"re-streaming ~GiB of keys and plaintexts), so the working set far exceeds the 126 MB L2"),
                    "launch": "CUDA graph replay (hs_softmax_plan)" if use_graph else "eager C-ABI call",
@@ -415,7 +421,7 @@ def run_e2e(S, step, plan, args, world):
     shapes_out = [(c.ncomp, c.level + 1) for c in out0]
     del out0
     pinned_out = [torch.empty(nc * l1 * P.n, dtype=torch.int64).pin_memory() for nc, l1 in shapes_out]
-    lvl_in = S["top"]
+    lvl_in = S["in_level"]
     stream = torch.cuda.current_stream()
     sp = C.c_void_p(stream.cuda_stream)
     torch.cuda.synchronize()
@@ -571,8 +577,8 @@ def run_llama(args):
         tab = W.poly_tables()[wl["table"]]
         x = W.softmax_inputs(wl["L"], wl["n"], wl["M"], seed=W.derive_seed("x", name))
         slots = P.pack(x, wl["m"])
-        sc = hs.softmax_input_scale(P, tab["exp"], top)  # DESIGN.md G28
-        cts = [hs.encrypt(K, P.encode(slots[c], scale=sc, level=top), top, W.derive_seed("enc", name), c)
+        lv = hs.softmax_input_level(P, wl["n"], wl["m"], wl["k"], wl["variant"], tab["exp"], tab["inv"], 1, top)
+        cts = [hs.softmax_encrypt_input(K, slots[c], lv, tab["exp"], W.derive_seed("enc", name), c)
                for c in range(wl["m"])]
         plans.append(hs.Plan(K, cts, wl["n"], wl["m"], wl["k"], wl["variant"], tab["exp"], tab["inv"], bts=B))
         data.append((wl, x, cts))

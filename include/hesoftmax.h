@@ -337,6 +337,23 @@ typedef struct {
  * into the encoding, so the Softmax spends exactly the levels of PAPER.md's
  * depth tables).  Returns 0 on a NULL argument or a level outside the chain. */
 double hs_softmax_input_scale(const hs_params *p, const hs_softmax_desc *d, int level);
+/* The client-side input step of G28: encode the N/2 real slots (one packed
+ * ciphertext, hs_pack) at level+1 with scale hs_softmax_input_scale(level) *
+ * q_{level+1}, encrypt with the public key (C5/C6 stream keyed by seed and
+ * ct_index, as hs_ckks_encrypt) and rescale once, landing at `level` with the
+ * fresh encryption noise divided by q_{level+1} (x keeps ~log2(q) more bits
+ * than an encryption straight at the input scale; at level = L it encrypts
+ * at `level` directly).  HS_EINVAL on a bad level, HS_EKEY without pk. */
+hs_status hs_softmax_encrypt_input(hs_ctx *c, const hs_keys *k, const hs_softmax_desc *d, const double *slots,
+                                   int level, uint64_t seed, uint64_t ct_index, void *stream, hs_ct **out);
+/* Planner choice of the input level: the level in
+ * [0, top - 1] (top = bts_out_level, or the chain top without bootstrapping)
+ * whose hs_softmax_schedule cost is lowest -- the main thread needs only the
+ * levels its updates consume (G12), and every level above them
+ * makes each batched main-thread product dearer.  Host only.  HS_ELEVEL if
+ * no level fits. */
+hs_status hs_softmax_input_level(const hs_params *p, const hs_softmax_desc *d, size_t m_local, int bts_out_level,
+                                 int *level);
 
 /* Debug domain check (SPEC's "domain" error; HS_EDOMAIN): with keys that hold
  * the secret (hs_ckks_keygen), every eager Softmax on this context decrypts

@@ -334,6 +334,25 @@ def cheb(keys: Keys, x: Ciphertext, poly, stream=None, gain: float = 1.0) -> Cip
     return Ciphertext(x.ctx, out)
 
 
+def softmax_encrypt_input(keys: Keys, slots, level: int, exp_poly, seed: int, idx: int, stream=None) -> Ciphertext:
+    """hs_softmax_encrypt_input: one packed slot vector -> the Softmax input
+    ciphertext at `level` (G28: encoded at level+1, public-key encrypted, one
+    rescale)."""
+    d, keep = _softmax_desc(1, 1, 1, 0, exp_poly, [exp_poly])
+    out = C.c_void_p()
+    check(L.hs_softmax_encrypt_input(keys.ctx.ptr, keys.ptr, C.byref(d), np.ascontiguousarray(slots, np.float64),
+                                     int(level), seed, idx, _stream(stream), C.byref(out)))
+    return Ciphertext(keys.ctx, out)
+
+
+def softmax_input_level(params: Params, n, m, k, variant, exp_poly, inv_polys, world=1, bts_out_level=-1) -> int:
+    """hs_softmax_input_level: the planner's cheapest input level."""
+    d, keep = _softmax_desc(n, m, k, variant, exp_poly, inv_polys, world, 0)
+    lv = C.c_int()
+    check(L.hs_softmax_input_level(params.ptr, C.byref(d), m // world, int(bts_out_level), C.byref(lv)))
+    return lv.value
+
+
 def softmax_input_scale(params: Params, exp_poly, level: int) -> float:
     """hs_softmax_input_scale: the scale the Softmax inputs are encoded at
     (Delta_level * 2/(b-a) of the exp table, G28)."""

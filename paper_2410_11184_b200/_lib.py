@@ -135,6 +135,11 @@ hs_rotate_hoisted = _sig("hs_rotate_hoisted", C.c_int, [vp, vp, vp, C.POINTER(C.
 hs_ntt = _sig("hs_ntt", C.c_int, [vp, C.c_int, C.c_int, vp, C.c_int, vp])
 hs_cheb = _sig("hs_cheb", C.c_int, [vp, vp, vp, C.POINTER(Poly), C.c_double, vp, C.POINTER(vp)])
 hs_cheb_depth = _sig("hs_cheb_depth", C.c_int, [C.c_int])
+hs_softmax_encrypt_input = _sig("hs_softmax_encrypt_input", C.c_int,
+                                [vp, vp, C.POINTER(SoftmaxDesc), f64p, C.c_int, C.c_uint64, C.c_uint64, vp,
+                                 C.POINTER(vp)])
+hs_softmax_input_level = _sig("hs_softmax_input_level", C.c_int,
+                              [vp, C.POINTER(SoftmaxDesc), C.c_size_t, C.c_int, C.POINTER(C.c_int)])
 hs_softmax_input_scale = _sig("hs_softmax_input_scale", C.c_double, [vp, C.POINTER(SoftmaxDesc), C.c_int])
 hs_softmax_one_ctxt = _sig("hs_softmax_one_ctxt", C.c_int,
                            [vp, vp, C.POINTER(SoftmaxDesc), vp, vp, C.POINTER(vp)])

@@ -500,6 +500,56 @@ double hs_softmax_input_scale(const hs_params *p, const hs_softmax_desc *d, int 
     return p->scale[level] * (2.0 / (d->exp_poly->b - d->exp_poly->a));
 }
 
+hs_status hs_softmax_encrypt_input(hs_ctx *c, const hs_keys *k, const hs_softmax_desc *d, const double *slots,
+                                   int level, uint64_t seed, uint64_t ct_index, void *stream, hs_ct **out)
+{
+    HS_TRY
+    if (!c || !k || !d || !d->exp_poly || !slots || !out) throw HsError(HS_EINVAL, "NULL argument");
+    const hs_params *P = c->P;
+    if (level < 0 || level > P->L || !(d->exp_poly->b > d->exp_poly->a)) throw HsError(HS_EINVAL, "bad level / exp");
+    activate(c);
+    cudaStream_t st = S(stream);
+    const double s_in = P->scale[level] * (2.0 / (d->exp_poly->b - d->exp_poly->a));
+    // one level up at scale s_in q_{level+1}, then one rescale: the fresh
+    // encryption noise is divided by q_{level+1} (G28)
+    const int up = level < P->L ? level + 1 : level;
+    const double sc = up > level ? s_in * (double)P->prime[up] : s_in;
+    std::vector<u64> pt((size_t)(up + 1) * P->n);
+    hs_encode_impl(P, slots, nullptr, sc, up, pt.data());
+    CtP ct = ev_encrypt(k, pt.data(), up, seed, ct_index, false, st);
+    if (up > level) ct = ev_rescale(ct.get(), st);
+    *out = ct.release();
+    return HS_OK;
+    HS_CATCH
+}
+
+hs_status hs_softmax_input_level(const hs_params *p, const hs_softmax_desc *d, size_t m_local, int bts_out_level,
+                                 int *level)
+{
+    HS_TRY
+    if (!p || !d || !level) throw HsError(HS_EINVAL, "NULL argument");
+    const int top = (bts_out_level >= 0 ? bts_out_level : p->L) - 1;
+    double best = HUGE_VAL;
+    int pick = -1;
+    for (int l = 0; l <= top; l++) {
+        hs_softmax_sched s;
+        try {
+            softmax_schedule(p, d, l, m_local, bts_out_level, &s);
+        } catch (const HsError &e) {
+            if (e.code == HS_ELEVEL) continue;
+            throw;
+        }
+        if (s.cost < best) {
+            best = s.cost;
+            pick = l;
+        }
+    }
+    if (pick < 0) throw HsError(HS_ELEVEL, "no input level fits the schedule");
+    *level = pick;
+    return HS_OK;
+    HS_CATCH
+}
+
 hs_status hs_softmax_one_ctxt(hs_ctx *c, const hs_keys *k, const hs_softmax_desc *d, const hs_ct *in, void *stream,
                               hs_ct **out)
 {

@@ -48,9 +48,8 @@ def test_config3_plan_full_size():
     assert err < 2.0 ** -15, np.log2(err)
     # the replay bootstraps where the host planner says (G12), and the level-
     # exact polynomials (C13, G28) keep config 3 at 7 bootstraps (9 in round 1)
-    top = S["top"]
-    plan_s = hs.softmax_schedule(S["P"], S["n"], S["m"], S["k"], wl["variant"], tab["exp"], tab["inv"], top,
-                                 bts_out_level=top)
+    plan_s = hs.softmax_schedule(S["P"], S["n"], S["m"], S["k"], wl["variant"], tab["exp"], tab["inv"],
+                                 S["in_level"], bts_out_level=S["top"])
     led = S["ctx"].ledger()
     assert led["bts"] == plan_s["bts_main"] + plan_s["bts_aux"] <= 7
 

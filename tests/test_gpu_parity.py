@@ -587,3 +587,27 @@ def test_uploaded_keys_softmax_parity(tables):
     ref = np.exp(x - x.max(1, keepdims=True))
     ref /= ref.sum(1, keepdims=True)
     assert np.abs(y - ref).max() < 2.0 ** -15
+
+
+def test_softmax_encrypt_input_parity(tables):
+    """hs_softmax_encrypt_input (G28 client step): encode at level+1
+    with scale hs_softmax_input_scale(level) * q_{level+1}, public-key
+    encryption, one rescale -- word for word the same steps on the oracle; the
+    result decrypts to alpha_exp x with the fresh noise divided by q_{level+1}."""
+    hs = _hs()
+    tab = tables["p16_n256_M128_k5_B"]
+    pre = W.preset("TOY12D")
+    P, PO = hs.Params.from_preset(pre), O.Params.from_preset(pre)
+    ctx = hs.Context(P, 0)
+    K, KO = hs.Keys(ctx, 5150, pre["h"]), O.Keys(PO, 5150, pre["h"])
+    x = W.softmax_inputs(8, 256, 128.0, seed=4)
+    slots = P.pack(x, 1)[0]
+    for level in (20, 9):
+        g = hs.softmax_encrypt_input(K, slots, level, tab["exp"], 77, 3)
+        sc = hs.softmax_input_scale(P, tab["exp"], level) * P.primes[level + 1]
+        pt = PO.encode(slots, scale=sc, level=level + 1)
+        o = O.op(PO, KO, "rescale", O.encrypt(PO, KO, pt, level + 1, 77, 3))
+        same(g, o)
+        alpha = 2.0 / (tab["exp"]["b"] - tab["exp"]["a"])
+        err = np.abs(hs.decrypt_decode(K, g).real - alpha * slots).max()
+        assert err < 2.0 ** -30, np.log2(err)

@@ -469,7 +469,7 @@ def test_softmax_error_paths(tables):
     # HS_ESCALE (C11): an input declared at the canonical scale instead of the
     # G28 input scale; a scheme op on an operand declared off-canonical
     wrong = hs.encrypt(K_full, P.encode(slots[0], scale=P.scale(top), level=top), top, 1, 2)
-    wrong.set_scale(P.scale(top))
+    wrong.set_scale(2.0 * P.scale(top))
     assert code(lambda: hs.softmax_many_ctxt(K_full, [wrong], n, 1, k, 0, tab["exp"], tab["inv"])) == 4
     ct.set_scale(sc(top))  # the right declaration passes
     assert code(lambda: hs.op(K_full, "mult", ct, ct)) == 4

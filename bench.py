@@ -548,16 +548,27 @@ def run_llama(args):
     """SURVEY 8(f) rank 4 / BASELINE.json configs 4 + 5: every Softmax of one
     LLaMA-7B ctx-128 run -- per layer 32 heads x 128 rows = 4096 Softmax of
     dim 128 (config 4: version B, m = 16), 32 layers, then the final dim-32768
-    Softmax (config 5) -- on one GPU, each as a replayed CUDA-graph plan.  The
-    layer batches replay one encrypted input batch (CKKS work does not depend
-    on the plaintext values; every replay recomputes every kernel)."""
+    Softmax (config 5) -- each as a replayed CUDA-graph plan.  The layer
+    batches replay one encrypted input batch (CKKS work does not depend on the
+    plaintext values; every replay recomputes every kernel).
+
+    N > 1: the 32 layer batches are
+    independent -- rank r runs layers r, r + N, ... (4 per rank at N = 8) with
+    no communication; rank 0 also runs the final dim-32768 Softmax (one
+    ciphertext: replicas only).  The job time is the max over ranks."""
     import torch
+    import torch.distributed as dist_
     import paper_2410_11184_b200 as hs
-    torch.cuda.set_device(0)
+    rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist_.init_process_group("nccl", device_id=torch.device("cuda", local))
+    my_layers = len(range(rank, LLAMA_LAYERS, world))
     w4, w5 = W.WORKLOADS["config4"], W.WORKLOADS["config5"]
     pre = W.preset(w4["preset"])
     P = hs.Params.from_preset(pre)
-    ctx = hs.Context(P, 0)
+    ctx = hs.Context(P, local)
     bcfg = pre["bts"]
     rots = set(hs.bts_rotations(P, bcfg))
     for wl in (w4, w5):
@@ -586,9 +597,10 @@ def run_llama(args):
     layer, final = plans
 
     def step():
-        for _ in range(LLAMA_LAYERS):
+        for _ in range(my_layers):
             layer.run()
-        return final.run()
+        if rank == 0:
+            final.run()
 
     for _ in range(args.warmup):
         step()
@@ -600,34 +612,49 @@ def run_llama(args):
         ref = np.exp(x - x.max(1, keepdims=True))
         ref /= ref.sum(1, keepdims=True)
         acc[name] = round(float(np.log2(np.abs(y - ref).max())), 2)
-    clocks = Clocks(0)
+    clocks = Clocks(local)
     led0 = ctx.ledger()
     clocks.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     stream = torch.cuda.current_stream()
+    if world > 1:
+        dist_.barrier()
     torch.cuda.synchronize()
     e0.record(stream)
     for _ in range(args.steps):
         step()
     e1.record(stream)
     torch.cuda.synchronize()
+    if world > 1:
+        dist_.barrier()
     clk = clocks.stop()
     ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist_.all_reduce(t, op=dist_.ReduceOp.MAX)
+        ms = float(t.item())
     led1 = ctx.ledger()
+    if rank != 0:
+        dist_.destroy_process_group()
+        return
     line = {"metric": "ms per LLaMA-7B ctx-128 Softmax run (32 layers x 4096 Softmax dim 128 + 1 Softmax dim 32768)",
-            "value": round(ms, 2), "unit": "ms/run", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "value": round(ms, 2), "unit": "ms/run", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(ms, 2), "higher_is_better": False, "scaling": "strong",
             "vs_baseline": round(ms / PAPER_LLAMA_MS, 6), "vs_baseline_ref": PAPER_LLAMA_REF,
             "dtype": "u64 (RNS residues)", "data": "synthetic (x ~ N(-M/2,(M/6)^2) tail-cut)",
             "config": {"workload": "llama7b: 32 x config4 (m=16, version B) + config5 (n=32768, Newton), N=2^16",
                        "preset": w4["preset"], "layers": LLAMA_LAYERS,
                        "inputs": "one encrypted layer batch replayed for the 32 layers (data-independent work)",
-                       "launch": "CUDA graph replay (two hs_softmax_plan)"},
+                       "launch": "CUDA graph replay (two hs_softmax_plan)",
+                       "parallelism": f"layers sharded over {world} ranks ({my_layers} on rank 0, no exchange); "
+                                      "final dim-32768 Softmax on rank 0"},
             "accuracy_bits": acc,
             "gpu_launches": int(led1["kernels"] - led0["kernels"]),
             "ledger_per_step": {k_: (led1[k_] - led0[k_]) // args.steps for k_ in led1},
             "clocks": clk, "setup_s": round(setup_s, 1)}
     print(json.dumps(line))
+    if world > 1:
+        dist_.destroy_process_group()
 
 
 def main():

@@ -141,6 +141,20 @@ int orc_api_keyswitch(const orc_params *P, const orc_keys *K, int galois, int le
     return 0;
 }
 
+/* digit-parallel key switch pieces */
+int orc_api_ks_partial(const orc_params *P, const orc_keys *K, int galois, int level, const u64 *d, int j0, int j1,
+                       u64 *acc)
+{
+    const orc_swk *k = orc_find_key(K, galois);
+    if (!k) return -1;
+    orc_ks_partial(P, k, level, d, j0, j1, acc);
+    return 0;
+}
+void orc_api_ks_finish(const orc_params *P, int level, const u64 *acc, u64 *o0, u64 *o1)
+{
+    orc_ks_finish(P, level, acc, o0, o1);
+}
+
 /* C16: hoisted rotations of one ciphertext; out[n] (NULL on a missing key) */
 int orc_api_rotate_hoisted(const orc_params *P, const orc_keys *K, const orc_ct *a, const int *rots, int n,
                            orc_ct **out)

@@ -525,6 +525,33 @@ void orc_ks_inner(const orc_params *P, const orc_swk *key, int level, const u64 
     }
 }
 
+/* SURVEY 8(f) rank 1 (digit-parallel key switch): the inner product over the
+ * digits [j0, j1) only.  The accumulator of C7 is a sum over the digits mod q;
+ * the partial sums of any partition of the digits, added mod q, are that sum
+ * (modular addition is exact and order-free). */
+void orc_ks_inner_digits(const orc_params *P, const orc_swk *key, int level, const u64 *ext, int j0, int j1,
+                         u64 *acc)
+{
+    int N = P->n, nq = P->n_q, np = P->n_p, nt = nq + np;
+    int nl = level + 1, ntg = nl + np;
+    memset(acc, 0, sizeof(u64) * (size_t)2 * ntg * N);
+    #pragma omp parallel for
+    for (int g = 0; g < ntg; g++) {
+        int pi = g < nl ? g : nq + (g - nl);
+        u64 p = P->prime[pi];
+        u64 *a0 = acc + (size_t)g * N, *a1 = acc + ((size_t)ntg + g) * N;
+        for (int j = j0; j < j1; j++) {
+            const u64 *e = ext + ((size_t)j * ntg + g) * N;
+            const u64 *k0 = key->k + (((size_t)j * 2 + 0) * nt + pi) * N;
+            const u64 *k1 = key->k + (((size_t)j * 2 + 1) * nt + pi) * N;
+            for (int t = 0; t < N; t++) {
+                a0[t] = orc_add(a0[t], orc_mul(e[t], k0[t], p), p);
+                a1[t] = orc_add(a1[t], orc_mul(e[t], k1[t], p), p);
+            }
+        }
+    }
+}
+
 /* ModDown (C7 second half): out_c = (acc_Q - BConv_{P->Q}(acc_P)) * P^{-1} */
 /* ModDown of ONE component A [ntg][N] (basis Q_level u P) -> out [nl][N] */
 void orc_ks_moddown1(const orc_params *P, int level, const u64 *A, u64 *out)
@@ -657,6 +684,20 @@ void orc_keyswitch(const orc_params *P, const orc_swk *key, int level, const u64
     free(acc);
     free(ext);
     orc_ledger[LG_KS]++;
+}
+
+/* the two halves of a key switch around its accumulator (digit-parallel
+ * path): the partial accumulator of digits [j0, j1), and the ModDown of a
+ * (summed) accumulator [2][level+1+n_p][N] */
+void orc_ks_partial(const orc_params *P, const orc_swk *key, int level, const u64 *d, int j0, int j1, u64 *acc)
+{
+    u64 *ext = orc_ks_modup(P, level, d);
+    orc_ks_inner_digits(P, key, level, ext, j0, j1, acc);
+    free(ext);
+}
+void orc_ks_finish(const orc_params *P, int level, const u64 *acc, u64 *out0, u64 *out1)
+{
+    ks_moddown(P, level, acc, out0, out1);
 }
 
 /* relinearise a degree-2 ciphertext (no rescale) */

@@ -259,6 +259,35 @@ def keyswitch(P: Params, K: Keys, galois, level, d):
     return o0.reshape(level + 1, P.n), o1.reshape(level + 1, P.n)
 
 
+def ks_partial(P: Params, K: Keys, galois, level, d, j0, j1):
+    """Digit-parallel key switch: the C7 accumulator
+    [2][level+1+n_p][N] of the digits [j0, j1) only."""
+    L = lib()
+    L.orc_api_ks_partial.restype = C.c_int
+    L.orc_api_ks_partial.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, u64p, C.c_int, C.c_int, u64p]
+    d = np.ascontiguousarray(d, np.uint64).reshape(-1)
+    ntg = level + 1 + P.n_p
+    acc = np.zeros(2 * ntg * P.n, np.uint64)
+    assert L.orc_api_ks_partial(P.ptr, K.ptr, galois, level, d, j0, j1, acc) == 0
+    return acc.reshape(2, ntg, P.n)
+
+
+def ks_finish(P: Params, level, acc):
+    """ModDown of a (summed) key-switch accumulator -> (out0, out1)."""
+    L = lib()
+    L.orc_api_ks_finish.argtypes = [C.c_void_p, C.c_int, u64p, u64p, u64p]
+    acc = np.ascontiguousarray(acc, np.uint64).reshape(-1)
+    o0 = np.zeros((level + 1) * P.n, np.uint64)
+    o1 = np.zeros_like(o0)
+    L.orc_api_ks_finish(P.ptr, level, acc, o0, o1)
+    return o0.reshape(level + 1, P.n), o1.reshape(level + 1, P.n)
+
+
+def ext_primes(P: Params, level):
+    """primes of the extended basis Q_level u P (the accumulator's limbs)"""
+    return P.primes[: level + 1] + P.primes[P.n_q:]
+
+
 def rotate_hoisted(P: Params, K: Keys, a: Ct, rots):
     """C16: every rotation in rots from ONE ModUp of a's c1."""
     r = np.ascontiguousarray(rots, np.int32)

@@ -118,6 +118,12 @@ void orc_ks_inner(const orc_params *P, const orc_swk *key, int level, const u64 
                   u64 *acc);
 void orc_ks_moddown1(const orc_params *P, int level, const u64 *A, u64 *out);
 void orc_ks_moddown_rescale(const orc_params *P, int level, const u64 *acc, u64 *out0, u64 *out1);
+/* digit-parallel key switch: partial accumulator of the
+ * digits [j0, j1); ModDown of a summed accumulator */
+void orc_ks_inner_digits(const orc_params *P, const orc_swk *key, int level, const u64 *ext, int j0, int j1,
+                         u64 *acc);
+void orc_ks_partial(const orc_params *P, const orc_swk *key, int level, const u64 *d, int j0, int j1, u64 *acc);
+void orc_ks_finish(const orc_params *P, int level, const u64 *acc, u64 *out0, u64 *out1);
 const orc_swk *orc_find_key(const orc_keys *K, int galois);
 int orc_galois_of_rot(const orc_params *P, int r);
 

@@ -237,6 +237,29 @@ hs_status hs_mult_pt(hs_ctx *c, const hs_ct *a, const double *re, const double *
 /* Hybrid key switch of one (level+1)-limb polynomial (device pointers). */
 hs_status hs_keyswitch(hs_ctx *c, const hs_keys *k, int galois, int level, const uint64_t *d,
                        uint64_t *out0, uint64_t *out1, void *stream);
+/* Digit-parallel key switching (PAPER.md 118-121 and
+ * 608-614: the shared aux ciphertext and its bootstraps are the serial part
+ * of the many-ciphertext Softmax).  The C7 key switch of d (level+1 limbs,
+ * NTT domain, device) is split over its beta = ceil((level+1)/alpha) digits:
+ *   hs_keyswitch_partial: ModUp and the evaluation-key inner product of the
+ *     digits [digit_begin, digit_end) only -> acc = 2 x (level+1+n_p) limbs
+ *     (components 0, 1; basis q_0..q_level, p_0..p_{n_p-1}; device; residues
+ *     reduced).  An empty range writes zeros.  HS_EINVAL outside [0, beta].
+ *   hs_ks_acc_add: acc += other mod q, limb by limb (exact: the accumulator is
+ *     a sum over the digits mod q, so any partition's partials add up to the
+ *     full one, word for word).
+ *   hs_keyswitch_finish: ModDown of a summed accumulator -> out0, out1
+ *     ((level+1) limbs each): the same words as hs_keyswitch.
+ *   hs_keyswitch_sharded: rank `rank` of `world` computes its digit share
+ *     [rank beta / world, (rank+1) beta / world), all-gathers the partials
+ *     (native NCCL communicator `comm`, or the `exchange` callback of the
+ *     Softmax descriptor's contract), adds them in rank order and finishes;
+ *     every rank ends with hs_keyswitch's words.  HS_ENCCL on an exchange
+ *     failure. */
+hs_status hs_keyswitch_partial(hs_ctx *c, const hs_keys *k, int galois, int level, const uint64_t *d, int digit_begin,
+                               int digit_end, uint64_t *acc, void *stream);
+hs_status hs_ks_acc_add(hs_ctx *c, int level, uint64_t *acc, const uint64_t *other, void *stream);
+hs_status hs_keyswitch_finish(hs_ctx *c, int level, const uint64_t *acc, uint64_t *out0, uint64_t *out1, void *stream);
 /* Forward / inverse negacyclic NTT (C3) of n_limbs consecutive device limbs,
  * limb j reduced mod prime (prime_index + j). */
 hs_status hs_ntt(hs_ctx *c, int prime_index, int n_limbs, uint64_t *data, int inverse, void *stream);
@@ -306,6 +329,10 @@ typedef int (*hs_exchange_fn)(void *user, const uint64_t *partial, uint64_t *gat
 typedef struct hs_comm hs_comm;
 hs_status hs_comm_unique_id(uint8_t uid[128]);
 hs_status hs_comm_init(hs_ctx *c, int rank, int world, const uint8_t uid[128], hs_comm **out);
+/* hs_keyswitch_sharded: see the digit-parallel key switching block above. */
+hs_status hs_keyswitch_sharded(hs_ctx *c, const hs_keys *k, int galois, int level, const uint64_t *d, int rank,
+                               int world, hs_comm *comm, hs_exchange_fn exchange, void *user, uint64_t *out0,
+                               uint64_t *out1, void *stream);
 void hs_comm_destroy(hs_comm *comm);
 
 typedef struct {

@@ -298,6 +298,30 @@ def keyswitch(keys: Keys, galois, level, d_ptr, out0_ptr, out1_ptr, stream=None)
                          C.c_void_p(out1_ptr), _stream(stream)))
 
 
+def keyswitch_partial(keys: Keys, galois, level, d_ptr, digit_begin, digit_end, acc_ptr, stream=None):
+    """hs_keyswitch_partial: the C7 accumulator of digits [digit_begin, digit_end)."""
+    check(L.hs_keyswitch_partial(keys.ctx.ptr, keys.ptr, galois, level, C.c_void_p(d_ptr), digit_begin, digit_end,
+                                 C.c_void_p(acc_ptr), _stream(stream)))
+
+
+def ks_acc_add(ctx: Context, level, acc_ptr, other_ptr, stream=None):
+    check(L.hs_ks_acc_add(ctx.ptr, level, C.c_void_p(acc_ptr), C.c_void_p(other_ptr), _stream(stream)))
+
+
+def keyswitch_finish(ctx: Context, level, acc_ptr, out0_ptr, out1_ptr, stream=None):
+    check(L.hs_keyswitch_finish(ctx.ptr, level, C.c_void_p(acc_ptr), C.c_void_p(out0_ptr), C.c_void_p(out1_ptr),
+                                _stream(stream)))
+
+
+def keyswitch_sharded(keys: Keys, galois, level, d_ptr, rank, world, out0_ptr, out1_ptr, comm=None, exchange=None,
+                      stream=None):
+    """hs_keyswitch_sharded: this rank's digit share, all-gather, modular sum, ModDown."""
+    fn = L.EXCHANGE_FN(0) if exchange is None else exchange
+    check(L.hs_keyswitch_sharded(keys.ctx.ptr, keys.ptr, galois, level, C.c_void_p(d_ptr), rank, world,
+                                 comm.ptr if comm is not None else None, fn, None, C.c_void_p(out0_ptr),
+                                 C.c_void_p(out1_ptr), _stream(stream)))
+
+
 def gather(cts, stream=None) -> Ciphertext:
     """hs_ct_gather: one batch handle over ciphertexts of one level; hs ops on it
     run every kernel once over all members."""

@@ -133,6 +133,12 @@ hs_keyswitch = _sig("hs_keyswitch", C.c_int, [vp, vp, C.c_int, C.c_int, vp, vp, 
 hs_rotate_hoisted = _sig("hs_rotate_hoisted", C.c_int, [vp, vp, vp, C.POINTER(C.c_int32), C.c_int, vp,
                                                         C.POINTER(vp)])
 hs_ntt = _sig("hs_ntt", C.c_int, [vp, C.c_int, C.c_int, vp, C.c_int, vp])
+hs_keyswitch_partial = _sig("hs_keyswitch_partial", C.c_int,
+                            [vp, vp, C.c_int, C.c_int, vp, C.c_int, C.c_int, vp, vp])
+hs_ks_acc_add = _sig("hs_ks_acc_add", C.c_int, [vp, C.c_int, vp, vp, vp])
+hs_keyswitch_finish = _sig("hs_keyswitch_finish", C.c_int, [vp, C.c_int, vp, vp, vp, vp])
+hs_keyswitch_sharded = _sig("hs_keyswitch_sharded", C.c_int,
+                            [vp, vp, C.c_int, C.c_int, vp, C.c_int, C.c_int, vp, EXCHANGE_FN, vp, vp, vp, vp])
 hs_cheb = _sig("hs_cheb", C.c_int, [vp, vp, vp, C.POINTER(Poly), C.c_double, vp, C.POINTER(vp)])
 hs_cheb_depth = _sig("hs_cheb_depth", C.c_int, [C.c_int])
 hs_softmax_encrypt_input = _sig("hs_softmax_encrypt_input", C.c_int,

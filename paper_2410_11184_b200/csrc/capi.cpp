@@ -470,6 +470,83 @@ hs_status hs_keyswitch(hs_ctx *c, const hs_keys *k, int galois, int level, const
     HS_CATCH
 }
 
+hs_status hs_keyswitch_partial(hs_ctx *c, const hs_keys *k, int galois, int level, const uint64_t *d, int digit_begin,
+                               int digit_end, uint64_t *acc, void *stream)
+{
+    HS_TRY
+    if (!c || !k || !d || !acc || level < 0 || level > c->P->L) throw HsError(HS_EINVAL, "bad arguments");
+    const SwKey *key = k->find(galois);
+    if (!key) throw HsError(HS_EKEY, "no such switching key");
+    activate(c);
+    ks_partial(k, key, level, d, digit_begin, digit_end, acc, S(stream));
+    return HS_OK;
+    HS_CATCH
+}
+
+hs_status hs_ks_acc_add(hs_ctx *c, int level, uint64_t *acc, const uint64_t *other, void *stream)
+{
+    HS_TRY
+    if (!c || !acc || !other || level < 0 || level > c->P->L) throw HsError(HS_EINVAL, "bad arguments");
+    activate(c);
+    ks_acc_add(c, level, acc, other, S(stream));
+    return HS_OK;
+    HS_CATCH
+}
+
+static void ks_finish_to(hs_ctx *c, int level, const u64 *acc, u64 *out0, u64 *out1, cudaStream_t st)
+{
+    const size_t N = c->P->n, w = (size_t)(level + 1) * N;
+    DBuf out(2 * w, st);
+    ks_moddown(c, level, 1, acc, out.p, 2 * w, nullptr, 0, 0, st);
+    HS_CUDA(cudaMemcpyAsync(out0, out.p, w * 8, cudaMemcpyDeviceToDevice, st));
+    HS_CUDA(cudaMemcpyAsync(out1, out.p + w, w * 8, cudaMemcpyDeviceToDevice, st));
+}
+
+hs_status hs_keyswitch_finish(hs_ctx *c, int level, const uint64_t *acc, uint64_t *out0, uint64_t *out1, void *stream)
+{
+    HS_TRY
+    if (!c || !acc || !out0 || !out1 || level < 0 || level > c->P->L) throw HsError(HS_EINVAL, "bad arguments");
+    activate(c);
+    ks_finish_to(c, level, acc, out0, out1, S(stream));
+    return HS_OK;
+    HS_CATCH
+}
+
+hs_status hs_keyswitch_sharded(hs_ctx *c, const hs_keys *k, int galois, int level, const uint64_t *d, int rank,
+                               int world, hs_comm *comm, hs_exchange_fn exchange, void *user, uint64_t *out0,
+                               uint64_t *out1, void *stream)
+{
+    HS_TRY
+    if (!c || !k || !d || !out0 || !out1 || level < 0 || level > c->P->L || world < 1 || rank < 0 || rank >= world)
+        throw HsError(HS_EINVAL, "bad arguments");
+    if (world > 1 && !comm && !exchange) throw HsError(HS_EINVAL, "world > 1 needs a communicator or an exchange");
+    if (comm && comm_world(comm) != world) throw HsError(HS_EINVAL, "communicator size != world");
+    const SwKey *key = k->find(galois);
+    if (!key) throw HsError(HS_EKEY, "no such switching key");
+    activate(c);
+    cudaStream_t st = S(stream);
+    const hs_params *P = c->P;
+    const size_t N = P->n;
+    const int nl = level + 1, beta = (nl + P->alpha - 1) / P->alpha, ntg = nl + P->n_p;
+    const size_t words = (size_t)2 * ntg * N;
+    // rank r owns the digits [r beta / world, (r + 1) beta / world)
+    const int j0 = (int)((long)rank * beta / world), j1 = (int)((long)(rank + 1) * beta / world);
+    DBuf part(words, st), gathered(words * world, st);
+    ks_partial(k, key, level, d, j0, j1, part.p, st);
+    if (world == 1) {
+        HS_CUDA(cudaMemcpyAsync(gathered.p, part.p, words * 8, cudaMemcpyDeviceToDevice, st));
+    } else if (comm) {
+        comm_all_gather(comm, part.p, gathered.p, words, st);
+    } else if (exchange(user, part.p, gathered.p, words, st) != 0) {
+        throw HsError(HS_ENCCL, "key switch: exchange callback failed");
+    }
+    for (int r = 1; r < world; r++) ks_acc_add(c, level, gathered.p, gathered.p + r * words, st);
+    ks_finish_to(c, level, gathered.p, out0, out1, st);
+    c->ledger[HS_LG_KS] += 1;
+    return HS_OK;
+    HS_CATCH
+}
+
 hs_status hs_ntt(hs_ctx *c, int prime_index, int n_limbs, uint64_t *data, int inverse, void *stream)
 {
     HS_TRY

@@ -364,6 +364,59 @@ void ks_moddown_rescale(hs_ctx *c, int level, int B, const u64 *acc, u64 *out, s
     k_moddown_final_b(c, acc, ar, conv.p, level, out, out_stride, nullptr, 0, 0, inv.data(), 2 * B, st);
 }
 
+// Digit-parallel key switch: rank r of G runs ModUp and
+// the evaluation-key inner product for its digits only; the partial
+// accumulators are summed mod q (exact, order-free: the C7 accumulator is a
+// sum over the digits mod q) and moved down once.  Only the digits' own limbs
+// are brought to coefficient form.
+void ks_partial(const hs_keys *K, const SwKey *key, int level, const u64 *d, int j0, int j1, u64 *acc,
+                cudaStream_t st)
+{
+    hs_ctx *c = K->ctx;
+    const hs_params *P = c->P;
+    const size_t N = P->n;
+    const int nl = level + 1, alpha = P->alpha, beta = (nl + alpha - 1) / alpha;
+    if (j0 < 0 || j1 > beta || j0 > j1) throw HsError(HS_EINVAL, "key switch: digit range out of [0, beta]");
+    const int ntg = nl + P->n_p;
+    if (j0 == j1) {
+        HS_CUDA(cudaMemsetAsync(acc, 0, (size_t)2 * ntg * N * 8, st));
+        return;
+    }
+    const int lo0 = j0 * alpha, hi1 = std::min(j1 * alpha, nl), cnt = hi1 - lo0;
+    DBuf x((size_t)cnt * N, st);
+    k_ntt_inv_from(c, x.p, d + (size_t)lo0 * N, (size_t)cnt * N, cnt, cnt, pmap_range(lo0, cnt), st);
+    ModUpBuf m;
+    m.beta = j1;
+    size_t tot = 0;
+    for (int j = j0; j < j1; j++) {
+        const BconvTab &tab = bconv_modup(c, level, j);
+        m.off[j] = tot;
+        m.nd[j] = tab.n_dst;
+        tot += (size_t)tab.n_dst * N;
+    }
+    m.ext.alloc(tot, st);
+    for (int j = j0; j < j1; j++) {
+        const BconvTab &tab = bconv_modup(c, level, j);
+        u64 *e = m.ext.p + m.off[j];
+        k_bconv(c, tab, x.p + (size_t)(tab.src[0] - lo0) * N, N, e, N, 1, (size_t)cnt * N, (size_t)tab.n_dst * N, st);
+        PrimeMap pm;
+        pm.n = tab.n_dst;
+        for (int i = 0; i < tab.n_dst; i++) pm.p[i] = (unsigned char)tab.dst[i];
+        k_ntt(c, e, tab.n_dst, pm, false, st);
+    }
+    k_ks_inner_b(c, d, (size_t)nl * N, m.ext.p, m.off, m.nd, key->k, acc, level, j1, 1, st, nullptr, 0, j0);
+}
+
+void ks_acc_add(hs_ctx *c, int level, u64 *acc, const u64 *other, cudaStream_t st)
+{
+    const hs_params *P = c->P;
+    const int nl = level + 1, ntg = nl + P->n_p;
+    PrimeMap pm;
+    pm.n = ntg;
+    for (int g = 0; g < ntg; g++) pm.p[g] = (unsigned char)(g < nl ? g : P->n_q + (g - nl));
+    k_add_pm(c, acc, other, acc, 2 * ntg, pm, st);
+}
+
 // B polynomials d_b = d + b*d_stride (level+1 limbs each, NTT domain);
 // out_b = out + b*out_stride gets (ks0, ks1) (+ add_b's first add_comps components).
 void ev_keyswitch_b(const hs_keys *K, const SwKey *key, int level, int B, const u64 *d, size_t d_stride, u64 *out,

@@ -243,7 +243,7 @@ void k_tensor_sum(hs_ctx *c, const u64 *a, u64 *o, int B, int nl, cudaStream_t s
 void k_tensor_sum2(hs_ctx *c, const u64 *a, const u64 *b, u64 *o, int B, int nl, cudaStream_t st);
 void k_ks_inner_b(hs_ctx *c, const u64 *d, size_t d_stride, const u64 *ext, const size_t *off, const int *nd,
                   const u64 *key, u64 *acc, int level, int beta, int B, cudaStream_t st, const u64 *dadd = nullptr,
-                  size_t dadd_stride = 0);
+                  size_t dadd_stride = 0, int j0 = 0);
 void k_ks_inner_m(hs_ctx *c, const u64 *d, size_t d_stride, const u64 *ext, const size_t *off, const int *nd,
                   const u64 *const *keys, int B, u64 *acc, int level, int beta, cudaStream_t st);
 void k_ks_inner_h(hs_ctx *c, const u64 *d, const u64 *ext, const size_t *off, const int *nd, const u64 *const *keys,
@@ -296,6 +296,11 @@ void ks_modup(hs_ctx *c, int level, int B, const u64 *d, size_t d_stride, ModUpB
 void ks_moddown_rescale(hs_ctx *c, int level, int B, const u64 *acc, u64 *out, size_t out_stride, cudaStream_t st);
 const BconvTab &bconv_moddown_rescale(hs_ctx *c, int level);
 CtP ev_relin_rescale(const hs_keys *K, const hs_ct *d, cudaStream_t st);
+// digit-parallel key switch: ModUp + inner product of
+// the digits [j0, j1) only -> acc [2][ntg][N]; acc += other (mod q, basis Q_l u P)
+void ks_partial(const hs_keys *K, const SwKey *key, int level, const u64 *d, int j0, int j1, u64 *acc,
+                cudaStream_t st);
+void ks_acc_add(hs_ctx *c, int level, u64 *acc, const u64 *other, cudaStream_t st);
 void ks_moddown(hs_ctx *c, int level, int B, const u64 *acc, u64 *out, size_t out_stride, const u64 *add,
                 size_t add_stride, int add_comps, cudaStream_t st);
 void ev_keyswitch(const hs_keys *K, const SwKey *key, int level, const u64 *d, u64 *out0, u64 *out1,

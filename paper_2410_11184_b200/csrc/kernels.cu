@@ -1688,6 +1688,7 @@ void k_tensor_sum2(hs_ctx *c, const u64 *a, const u64 *b, u64 *o, int B, int nl,
 // the evaluation key is read once per batch tile.
 struct KsArgB {
     int level, beta, alpha, n_q, n_t, B;
+    int j0;  // first digit (digits [j0, beta)): the digit-parallel partial accumulator
     size_t d_stride;
     size_t off[HS_MAXDIG];
     int nd[HS_MAXDIG];
@@ -1715,7 +1716,7 @@ __global__ void __launch_bounds__(256, BT == 2 ? 8 : 1) ks_inner_b_kernel(const 
     u64 h0[BT], l0[BT], h1[BT], l1[BT];
 #pragma unroll
     for (int u = 0; u < BT; u++) h0[u] = l0[u] = h1[u] = l1[u] = 0;
-    for (int j = 0; j < A.beta; j++) {
+    for (int j = A.j0; j < A.beta; j++) {
         const int lo = j * A.alpha, hi = min((j + 1) * A.alpha, nl), dn = hi - lo;
         const ulonglong2 kk = reinterpret_cast<const ulonglong2 *>(key)[((size_t)j * ntot + pi) * N + t];
         const u64 k0 = kk.x, k1 = kk.y;
@@ -1753,18 +1754,20 @@ __global__ void __launch_bounds__(256, BT == 2 ? 8 : 1) ks_inner_b_kernel(const 
 
 void k_ks_inner_b(hs_ctx *c, const u64 *d, size_t d_stride, const u64 *ext, const size_t *off, const int *nd,
                   const u64 *key, u64 *acc, int level, int beta, int B, cudaStream_t st, const u64 *dadd,
-                  size_t dadd_stride)
+                  size_t dadd_stride, int j0)
 {
     const hs_params *P = c->P;
     const int ntg = level + 1 + P->n_p;
     // algorithmic bytes: the key once, every input limb once, the C8 P*d
     // term's 2 (level+1) limbs per member when fused, the outputs once
     KTimer _kt(c, KID_KS_INNER,
-               ((double)beta * ntg * (16.0 + 8.0 * B) + 16.0 * ntg * B + (dadd ? 16.0 * (level + 1) * B : 0.0)) * P->n,
+               ((double)(beta - j0) * ntg * (16.0 + 8.0 * B) + 16.0 * ntg * B +
+                (dadd ? 16.0 * (level + 1) * B : 0.0)) * P->n,
                st);
     KsArgB A;
     A.level = level;
     A.beta = beta;
+    A.j0 = j0;
     A.alpha = P->alpha;
     A.n_q = P->n_q;
     A.n_t = P->n_p;

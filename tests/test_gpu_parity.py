@@ -611,3 +611,66 @@ def test_softmax_encrypt_input_parity(tables):
         alpha = 2.0 / (tab["exp"]["b"] - tab["exp"]["a"])
         err = np.abs(hs.decrypt_decode(K, g).real - alpha * slots).max()
         assert err < 2.0 ** -30, np.log2(err)
+
+
+@pytest.mark.parametrize("preset,level", [("TOY12", 9), ("P16U", 13), ("P16", 30)])
+def test_digit_parallel_keyswitch_parity(preset, level):
+    """SURVEY 8(f) rank 1 on one GPU: every rank's partial accumulator
+    (hs_keyswitch_partial) equals the oracle's for the same digits; the
+    partials of 2 and 3 ranks summed by hs_ks_acc_add and finished
+    (hs_keyswitch_finish) equal the oracle's key switch; and the sharded entry
+    point hs_keyswitch_sharded of rank 0 of 2 -- with an exchange callback
+    standing in for the all-gather by writing rank 1's precomputed partial
+    into its slot (a single-process 2-rank emulation) -- ends with the same
+    words."""
+    hs = _hs()
+    pre = W.preset(preset)
+    P, PO = hs.Params.from_preset(pre), O.Params.from_preset(pre)
+    ctx = hs.Context(P, 0)
+    gal = P.galois_of_rot(1)
+    K = hs.Keys(ctx, 606, pre["h"], galois=[gal])
+    KO = O.Keys(PO, 606, pre["h"], galois=[gal])
+    rng = np.random.default_rng(level)
+    d = np.stack([rng.integers(0, P.primes[i], P.n, dtype=np.uint64) for i in range(level + 1)])
+    dd = torch.from_numpy(d.view(np.int64)).cuda()
+    nl, ntg = level + 1, level + 1 + P.n_p
+    beta = -(-nl // P.alpha)
+    want0, want1 = O.keyswitch(PO, KO, gal, level, d)
+    o0 = torch.empty_like(dd)
+    o1 = torch.empty_like(dd)
+    host = lambda t: t.cpu().numpy().view(np.uint64)
+    for world in (2, 3):
+        ranges = [(r * beta // world, (r + 1) * beta // world) for r in range(world)]
+        parts = []
+        for j0, j1 in ranges:
+            acc = torch.zeros(2 * ntg * P.n, dtype=torch.int64, device="cuda")
+            hs.keyswitch_partial(K, gal, level, dd.data_ptr(), j0, j1, acc.data_ptr())
+            torch.cuda.synchronize()
+            if preset != "P16":  # the oracle's partial (P16 at level 30: the finished words suffice)
+                assert (host(acc).reshape(2, ntg, P.n) == O.ks_partial(PO, KO, gal, level, d, j0, j1)).all()
+            parts.append(acc)
+        tot = parts[0].clone()
+        for p_ in parts[1:]:
+            hs.ks_acc_add(ctx, level, tot.data_ptr(), p_.data_ptr())
+        hs.keyswitch_finish(ctx, level, tot.data_ptr(), o0.data_ptr(), o1.data_ptr())
+        torch.cuda.synchronize()
+        assert (host(o0).reshape(nl, P.n) == want0).all() and (host(o1).reshape(nl, P.n) == want1).all(), world
+    # hs_keyswitch_sharded, rank 0 of 2, single-process emulation of the all-gather
+    other = torch.zeros(2 * ntg * P.n, dtype=torch.int64, device="cuda")
+    hs.keyswitch_partial(K, gal, level, dd.data_ptr(), beta // 2, beta, other.data_ptr())
+    torch.cuda.synchronize()
+    from paper_2410_11184_b200 import _lib
+
+    def emu(user, partial, gathered, words, stream):
+        src = torch.as_tensor(_CudaBuf(partial, words), device="cuda")
+        dst = torch.as_tensor(_CudaBuf(gathered, 2 * words), device="cuda")
+        dst[:words].copy_(src)
+        dst[words:].copy_(other)
+        return 0
+
+    fn = _lib.EXCHANGE_FN(emu)
+    o0.zero_()
+    o1.zero_()
+    hs.keyswitch_sharded(K, gal, level, dd.data_ptr(), 0, 2, o0.data_ptr(), o1.data_ptr(), exchange=fn)
+    torch.cuda.synchronize()
+    assert (host(o0).reshape(nl, P.n) == want0).all() and (host(o1).reshape(nl, P.n) == want1).all()

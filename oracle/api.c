@@ -201,7 +201,12 @@ void orc_api_set_threads(int n) { omp_set_num_threads(n < 1 ? 1 : n); }
 int orc_api_max_threads(void) { return omp_get_max_threads(); }
 
 void orc_api_ledger(long *out) { memcpy(out, orc_ledger, sizeof(orc_ledger)); }
-void orc_api_ledger_reset(void) { memset(orc_ledger, 0, sizeof(orc_ledger)); }
+void orc_api_ledger_reset(void)
+{
+    memset(orc_ledger, 0, sizeof(orc_ledger));
+    memset(orc_ks_level, 0, sizeof(orc_ks_level));
+}
+void orc_api_ks_levels(long *out) { memcpy(out, orc_ks_level, sizeof(orc_ks_level)); }
 
 /* ---------------------------------------------------------------- bootstrapping */
 typedef struct orc_bts_set orc_bts_set;
@@ -264,4 +269,36 @@ int orc_api_trace_get(int *out, int max)
     int n = orc_trace_n < max ? orc_trace_n : max;
     memcpy(out, orc_trace, sizeof(int) * 4 * n);
     return n;
+}
+
+/* bench.py --impl reference: the Softmax schedule with a bootstrap STUB that
+ * returns an all-zero ciphertext at out_level (and counts LG_BTS) -- the op
+ * inventory of a step (key switches per level, bootstrap count) without the
+ * bootstraps' own work, which is timed separately.  Data-independent
+ * schedule (G12 reads levels only); never used for parity. */
+static int g_stub_out_level;
+static orc_ct *bts_stub(const orc_params *P, const orc_keys *K, const orc_ct *c, void *ctx, double bound)
+{
+    (void)K; (void)c; (void)ctx; (void)bound;
+    orc_ledger[LG_BTS]++;
+    return orc_ct_alloc(P, g_stub_out_level, 2);
+}
+int orc_api_softmax_inventory(const orc_params *P, const orc_keys *K, int n, int m, int k, int variant,
+                              const int *degs, const double *as, const double *bs, const double *coeffs,
+                              orc_ct *const *in, orc_ct **out, int out_level, int newton)
+{
+    orc_cheb *polys = malloc(sizeof(orc_cheb) * (k + 1));
+    const double *cp = coeffs;
+    for (int i = 0; i <= k; i++) {
+        polys[i].deg = degs[i];
+        polys[i].a = as[i];
+        polys[i].b = bs[i];
+        polys[i].c = cp;
+        cp += degs[i] + 1;
+    }
+    g_stub_out_level = out_level;
+    orc_softmax_desc d = {n, m, k, variant, &polys[0], &polys[1], bts_stub, NULL, newton};
+    int rc = orc_softmax(P, K, &d, in, out);
+    free(polys);
+    return rc;
 }

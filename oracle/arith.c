@@ -9,6 +9,7 @@
 #include <math.h>
 
 long orc_ledger[LG_COUNT];
+long orc_ks_level[ORC_MAXP];
 
 u64 orc_mul(u64 a, u64 b, u64 q) { return (u64)(((u128)a * b) % q); }
 u64 orc_add(u64 a, u64 b, u64 q) { return (u64)(((u128)a + b) % q); }

@@ -385,7 +385,7 @@ static orc_ct *apply_ltrans(const orc_params *P, const orc_keys *K, const orc_ct
             u64 *o = R[b] + (size_t)i * N;
             for (int t = 0; t < N; t++) o[t] = orc_add(o[t], orc_mul(c0[perm[t]], P->p_mod_q[i], q), q);
         }
-        orc_ledger[LG_KS]++;
+        ORC_COUNT_KS(l);
         orc_ledger[LG_ROT]++;
     }
     free(ext);
@@ -431,7 +431,7 @@ static orc_ct *apply_ltrans(const orc_params *P, const orc_keys *K, const orc_ct
                 u64 *o = rot + (size_t)gi * N;
                 for (int t = 0; t < N; t++) o[t] = orc_add(o[t], a0[perm[t]], q);
             }
-            orc_ledger[LG_KS]++;
+            ORC_COUNT_KS(l);
             orc_ledger[LG_ROT]++;
             add = rot;
         }

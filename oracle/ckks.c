@@ -683,7 +683,7 @@ void orc_keyswitch(const orc_params *P, const orc_swk *key, int level, const u64
     ks_moddown(P, level, acc, out0, out1);
     free(acc);
     free(ext);
-    orc_ledger[LG_KS]++;
+    ORC_COUNT_KS(level);
 }
 
 /* the two halves of a key switch around its accumulator (digit-parallel
@@ -742,7 +742,7 @@ orc_ct *orc_op_relin_rescale(const orc_params *P, const orc_keys *K, const orc_c
     orc_ks_moddown_rescale(P, l, acc, LIMB(P, r, 0, 0), LIMB(P, r, 1, 0));
     free(acc);
     free(ext);
-    orc_ledger[LG_KS]++;
+    ORC_COUNT_KS(l);
     orc_ledger[LG_RESCALE]++;
     return r;
 }
@@ -827,7 +827,7 @@ int orc_op_rotate_hoisted(const orc_params *P, const orc_keys *K, const orc_ct *
             for (int t = 0; t < N; t++) o[t] = orc_add(c0[perm[t]], o[t], q);
         }
         out[i] = r;
-        orc_ledger[LG_KS]++;
+        ORC_COUNT_KS(l);
         orc_ledger[LG_ROT]++;
     }
     free(perm);

@@ -503,3 +503,34 @@ def trace_get():
     buf = np.zeros(512 * 4, np.int32)
     n = L.orc_api_trace_get(buf.ctypes.data_as(C.POINTER(C.c_int)), 512)
     return [(TRACE_EVENTS[e], int(j), int(a), int(b)) for e, j, a, b in buf[: 4 * n].reshape(n, 4)]
+
+
+# ---------------------------------------------------------------- op inventory (bench.py --impl reference)
+def ks_levels():
+    a = (C.c_long * 64)()
+    lib().orc_api_ks_levels(a)
+    return list(a)
+
+
+def softmax_inventory(P: Params, K: Keys, cts, n, k, variant, exp_poly, inv_polys, out_level):
+    """The Softmax schedule with a zero-returning bootstrap stub: fills the
+    ledger / per-level key-switch counters of one step (not for parity)."""
+    variant = VARIANT[variant]
+    polys = [exp_poly] + list(inv_polys)
+    degs = np.array([len(p["coeffs"]) - 1 for p in polys], np.int32)
+    a_s = np.array([p["a"] for p in polys], np.float64)
+    b_s = np.array([p["b"] for p in polys], np.float64)
+    co = np.concatenate([np.asarray(p["coeffs"], np.float64) for p in polys])
+    m = len(cts)
+    ins = (C.c_void_p * m)(*[c.ptr for c in cts])
+    outs = (C.c_void_p * m)()
+    L = lib()
+    L.orc_api_softmax_inventory.restype = C.c_int
+    L.orc_api_softmax_inventory.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, i32p, f64p,
+                                            f64p, f64p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_int,
+                                            C.c_int]
+    rc = L.orc_api_softmax_inventory(P.ptr, K.ptr, n, m, k, variant, degs, a_s, b_s, co, ins, outs, out_level,
+                                     int(inv_polys[-1].get("newton", 0)))
+    if rc != 0:
+        raise RuntimeError(f"oracle softmax inventory failed rc={rc}")
+    return [Ct(P, outs[i]) for i in range(m)]

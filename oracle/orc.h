@@ -63,6 +63,10 @@ typedef struct {
 enum { LG_HMULT, LG_TENSOR, LG_KS, LG_ROT, LG_RESCALE, LG_CMULT, LG_PMULT,
        LG_LEVELDOWN, LG_BTS, LG_NTT, LG_COUNT };
 extern long orc_ledger[LG_COUNT];
+/* key switches per level (bench.py --impl reference: the op inventory the
+ * oracle's timed samples are weighted by) */
+extern long orc_ks_level[ORC_MAXP];
+#define ORC_COUNT_KS(lvl) do { orc_ledger[LG_KS]++; orc_ks_level[(lvl)]++; } while (0)
 
 /* arith.c */
 u64 orc_mul(u64 a, u64 b, u64 q);

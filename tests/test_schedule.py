@@ -148,3 +148,23 @@ def test_choose_errors(tables, p16):
     assert best in (0, 1) and all(np.isfinite(s["cost"]) or s["cost"] == float("inf") for s in sched)
     with pytest.raises(hs.HsError):
         hs.softmax_choose(P, [dict(cands[0], k=0)], 256, 1, bo, bts_out_level=bo)
+
+
+def test_input_level_choice_matches_workload(tables):
+    """hs_softmax_input_level (the planner's input level) for config 3 equals
+    the level the workload table declares (bench.py and the reference arm's
+    inventory both use it): the lowest-cost level that fits the version-B
+    main thread without bootstrapping it (PAPER.md 444-447)."""
+    pre = W.preset("P16")
+    P = hs.Params.from_preset(pre)
+    wl = W.WORKLOADS["config3"]
+    tab = tables[wl["table"]]
+    lv = hs.softmax_input_level(P, wl["n"], wl["m"], wl["k"], wl["variant"], tab["exp"], tab["inv"], 1,
+                                pre["bts"]["out_level"])
+    assert lv == wl["input_level"]
+    s = hs.softmax_schedule(P, wl["n"], wl["m"], wl["k"], wl["variant"], tab["exp"], tab["inv"], lv,
+                            bts_out_level=pre["bts"]["out_level"])
+    assert s["bts_main"] == 0
+    with pytest.raises(hs.HsError):  # one level lower no longer fits
+        hs.softmax_schedule(P, wl["n"], wl["m"], wl["k"], wl["variant"], tab["exp"], tab["inv"], lv - 1,
+                            bts_out_level=pre["bts"]["out_level"])

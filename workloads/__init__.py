@@ -100,7 +100,10 @@ def poly_tables() -> dict:
 WORKLOADS = {
     "config1": dict(preset="TOY12", n=16, L=128, m=1, M=2.0, k=1, variant="A", table="toy_n16_M2_k1_A"),
     "config2": dict(preset="P16", n=256, L=128, m=1, M=128.0, k=5, variant="A", table="p16_n256_M128_k5_A"),
-    "config3": dict(preset="P16", n=256, L=8192, m=64, M=128.0, k=5, variant="B", table="p16_n256_M128_k5_B"),
+    # input_level: the level the inputs are encrypted at (hs_softmax_input_level's
+    # pick for this workload; tests/test_schedule.py checks the two agree)
+    "config3": dict(preset="P16", n=256, L=8192, m=64, M=128.0, k=5, variant="B", table="p16_n256_M128_k5_B",
+                    input_level=10),
     # config 2 with the square-and-normalize variant (PAPER.md 757-765, G26)
     "config2S": dict(preset="P16", n=256, L=128, m=1, M=128.0, k=5, variant="S", table="p16_n256_M128_k5_S"),
     "config4": dict(preset="P16", n=128, L=4096, m=16, M=128.0, k=5, variant="B", table="p16_n128_M128_k5_B"),

@@ -356,6 +356,16 @@ typedef struct {
     hs_comm *comm;            /* native exchange (hs_comm_init; NULL = use exchange).
                                  Its size must equal world; with world == 1 a
                                  one-rank communicator still runs the exchange   */
+    int aux_split;            /* SURVEY 8(f) rank 1 / DESIGN.md section 7: 1 = every
+                                 key switch of the shared aux thread (the aux-sum
+                                 relinearisation, rotate-and-sum, polynomial and
+                                 lambda products, the bootstraps' EvalMod products
+                                 and conjugations) is digit-split over the world
+                                 ranks (hs_keyswitch_sharded semantics, through
+                                 comm / exchange); words identical to aux_split = 0.
+                                 G >= 2 with world == 1: single-process emulation
+                                 (every rank's digit share in turn, then the
+                                 rank-order modular sum).  0 = off              */
 } hs_softmax_desc;
 
 /* Input contract (G28): every input ciphertext holds x encoded at

@@ -461,7 +461,8 @@ class Comm:
             self.ptr = None
 
 
-def _softmax_desc(n, m, k, variant, exp_poly, inv_polys, world=1, rank=0, exchange=None, bts=None, comm=None):
+def _softmax_desc(n, m, k, variant, exp_poly, inv_polys, world=1, rank=0, exchange=None, bts=None, comm=None,
+                  aux_split=0):
     keep = []
     e, c = _poly(exp_poly)
     keep.append(c)
@@ -477,7 +478,7 @@ def _softmax_desc(n, m, k, variant, exp_poly, inv_polys, world=1, rank=0, exchan
     # a table's last entry may carry "newton": the polynomial is then a seed (G24)
     d = L.SoftmaxDesc(n, m, k, variant_code(variant), ep, arr, world, rank, fn, None,
                       bts.ptr if bts is not None else None, int(inv_polys[-1].get("newton", 0)),
-                      comm.ptr if comm is not None else None)
+                      comm.ptr if comm is not None else None, int(aux_split))
     keep.append(comm)
     return d, keep
 
@@ -556,12 +557,14 @@ class Plan:
 
 
 def softmax_many_ctxt(keys: Keys, cts, n, m, k, variant, exp_poly, inv_polys, world=1, rank=0, exchange=None,
-                      bts=None, stream=None, comm=None):
+                      bts=None, stream=None, comm=None, aux_split=0):
     """cts: this rank's m/world ciphertexts.  world > 1 needs comm (a Comm,
-    native NCCL) or exchange (an EXCHANGE_FN, see paper_2410_11184_b200.dist)."""
+    native NCCL) or exchange (an EXCHANGE_FN, see paper_2410_11184_b200.dist).
+    aux_split: digit-split the aux thread's key switches over the ranks (1),
+    or emulate that split over G ranks in this process (G >= 2, world 1)."""
     if comm is not None:
         world, rank = comm.world, comm.rank
-    d, keep = _softmax_desc(n, m, k, variant, exp_poly, inv_polys, world, rank, exchange, bts, comm)
+    d, keep = _softmax_desc(n, m, k, variant, exp_poly, inv_polys, world, rank, exchange, bts, comm, aux_split)
     ml = len(cts)
     ins = (C.c_void_p * ml)(*[c.ptr.value if isinstance(c.ptr, C.c_void_p) else c.ptr for c in cts])
     outs = (C.c_void_p * ml)()

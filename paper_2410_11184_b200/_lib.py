@@ -54,7 +54,7 @@ class SoftmaxDesc(C.Structure):
     _fields_ = [("n", C.c_int), ("m", C.c_int), ("k", C.c_int), ("variant", C.c_int),
                 ("exp_poly", C.POINTER(Poly)), ("inv_poly", C.POINTER(Poly)), ("world", C.c_int),
                 ("rank", C.c_int), ("exchange", EXCHANGE_FN), ("exchange_user", vp), ("bts", vp),
-                ("newton", C.c_int), ("comm", vp)]
+                ("newton", C.c_int), ("comm", vp), ("aux_split", C.c_int)]
 
 
 class SoftmaxSched(C.Structure):

@@ -370,7 +370,7 @@ void ks_moddown_rescale(hs_ctx *c, int level, int B, const u64 *acc, u64 *out, s
 // sum over the digits mod q) and moved down once.  Only the digits' own limbs
 // are brought to coefficient form.
 void ks_partial(const hs_keys *K, const SwKey *key, int level, const u64 *d, int j0, int j1, u64 *acc,
-                cudaStream_t st)
+                cudaStream_t st, const u64 *dadd, size_t dadd_stride)
 {
     hs_ctx *c = K->ctx;
     const hs_params *P = c->P;
@@ -379,7 +379,14 @@ void ks_partial(const hs_keys *K, const SwKey *key, int level, const u64 *d, int
     if (j0 < 0 || j1 > beta || j0 > j1) throw HsError(HS_EINVAL, "key switch: digit range out of [0, beta]");
     const int ntg = nl + P->n_p;
     if (j0 == j1) {
-        HS_CUDA(cudaMemsetAsync(acc, 0, (size_t)2 * ntg * N * 8, st));
+        if (!dadd) {
+            HS_CUDA(cudaMemsetAsync(acc, 0, (size_t)2 * ntg * N * 8, st));
+            return;
+        }
+        // no digits: the C8 P*d term alone
+        size_t off0[HS_MAXDIG] = {0};
+        int nd0[HS_MAXDIG] = {0};
+        k_ks_inner_b(c, d, (size_t)nl * N, nullptr, off0, nd0, key->k, acc, level, j1, 1, st, dadd, dadd_stride, j0);
         return;
     }
     const int lo0 = j0 * alpha, hi1 = std::min(j1 * alpha, nl), cnt = hi1 - lo0;
@@ -404,7 +411,41 @@ void ks_partial(const hs_keys *K, const SwKey *key, int level, const u64 *d, int
         for (int i = 0; i < tab.n_dst; i++) pm.p[i] = (unsigned char)tab.dst[i];
         k_ntt(c, e, tab.n_dst, pm, false, st);
     }
-    k_ks_inner_b(c, d, (size_t)nl * N, m.ext.p, m.off, m.nd, key->k, acc, level, j1, 1, st, nullptr, 0, j0);
+    k_ks_inner_b(c, d, (size_t)nl * N, m.ext.p, m.off, m.nd, key->k, acc, level, j1, 1, st, dadd, dadd_stride, j0);
+}
+
+void ks_split_acc(hs_ctx *c, const hs_keys *K, const SwKey *key, int level, const u64 *d, const u64 *dadd,
+                  size_t dadd_stride, u64 *acc, cudaStream_t st)
+{
+    const hs_params *P = c->P;
+    const size_t N = P->n;
+    const int nl = level + 1, beta = (nl + P->alpha - 1) / P->alpha, ntg = nl + P->n_p;
+    const size_t words = (size_t)2 * ntg * N;
+    const hs_ctx::KsSplit &S = c->ks_split;
+    auto range = [&](int r, int G, int &j0, int &j1) {
+        j0 = (int)((long)r * beta / G);
+        j1 = (int)((long)(r + 1) * beta / G);
+    };
+    int j0, j1;
+    if (S.emulate >= 2) {
+        DBuf part(words, st);
+        for (int r = 0; r < S.emulate; r++) {
+            range(r, S.emulate, j0, j1);
+            ks_partial(K, key, level, d, j0, j1, r == 0 ? acc : part.p, st, r == 0 ? dadd : nullptr,
+                       dadd_stride);
+            if (r > 0) ks_acc_add(c, level, acc, part.p, st);
+        }
+        return;
+    }
+    range(S.rank, S.world, j0, j1);
+    DBuf part(words, st), gathered(words * S.world, st);
+    // the C8 P*d term rides with rank 0's share
+    ks_partial(K, key, level, d, j0, j1, part.p, st, S.rank == 0 ? dadd : nullptr, dadd_stride);
+    if (S.comm) comm_all_gather(S.comm, part.p, gathered.p, words, st);
+    else if (S.ex(S.user, part.p, gathered.p, words, st) != 0)
+        throw HsError(HS_ENCCL, "aux key switch: exchange callback failed");
+    HS_CUDA(cudaMemcpyAsync(acc, gathered.p, words * 8, cudaMemcpyDeviceToDevice, st));
+    for (int r = 1; r < S.world; r++) ks_acc_add(c, level, acc, gathered.p + r * words, st);
 }
 
 void ks_acc_add(hs_ctx *c, int level, u64 *acc, const u64 *other, cudaStream_t st)
@@ -426,11 +467,16 @@ void ev_keyswitch_b(const hs_keys *K, const SwKey *key, int level, int B, const 
     const hs_params *P = c->P;
     const size_t N = P->n;
     const int ntg = level + 1 + P->n_p;
-    ModUpBuf m;
-    ks_modup(c, level, B, d, d_stride, m, st);
-    // inner product with the evaluation key: acc[B][2][ntg][N]
     DBuf acc((size_t)B * 2 * ntg * N, st);
-    k_ks_inner_b(c, d, d_stride, m.ext.p, m.off, m.nd, key->k, acc.p, level, m.beta, B, st);
+    if (B == 1 && c->ks_split_on) {
+        // digit-parallel key switch of a single-ciphertext op
+        ks_split_acc(c, K, key, level, d, nullptr, 0, acc.p, st);
+    } else {
+        ModUpBuf m;
+        ks_modup(c, level, B, d, d_stride, m, st);
+        // inner product with the evaluation key: acc[B][2][ntg][N]
+        k_ks_inner_b(c, d, d_stride, m.ext.p, m.off, m.nd, key->k, acc.p, level, m.beta, B, st);
+    }
     ks_moddown(c, level, B, acc.p, out, out_stride, add, add_stride, add_comps, st);
     c->ledger[HS_LG_KS] += B;
 }
@@ -723,10 +769,14 @@ CtP ev_relin_rescale(const hs_keys *K, const hs_ct *d, cudaStream_t st)
     const size_t N = P->n;
     const int l = d->level, B = d->batch, ntg = l + 1 + P->n_p;
     const size_t w3 = d->ct_words();
-    ModUpBuf m;
-    ks_modup(c, l, B, d->limb(2, 0), w3, m, st);
     DBuf acc((size_t)B * 2 * ntg * N, st);
-    k_ks_inner_b(c, d->limb(2, 0), w3, m.ext.p, m.off, m.nd, rk->k, acc.p, l, m.beta, B, st, d->d, w3);
+    if (B == 1 && c->ks_split_on) {
+        ks_split_acc(c, K, rk, l, d->limb(2, 0), d->d, w3, acc.p, st);
+    } else {
+        ModUpBuf m;
+        ks_modup(c, l, B, d->limb(2, 0), w3, m, st);
+        k_ks_inner_b(c, d->limb(2, 0), w3, m.ext.p, m.off, m.nd, rk->k, acc.p, l, m.beta, B, st, d->d, w3);
+    }
     CtP r = ct_new(c, l - 1, 2, st, B);
     ks_moddown_rescale(c, l, B, acc.p, r->d, r->ct_words(), st);
     c->ledger[HS_LG_KS] += B;

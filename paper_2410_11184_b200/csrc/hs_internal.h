@@ -97,6 +97,15 @@ struct hs_ctx {
     std::mutex mu;
     int64_t ledger[HS_LG_COUNT] = {0};
     const hs_keys *debug_keys = nullptr;  // hs_ctx_debug_domain: keys WITH the secret
+    // digit-parallel key switching of single-ciphertext ops (SURVEY 8(f) rank
+    // 1), switched on by the Softmax driver around its aux thread
+    struct KsSplit {
+        int rank = 0, world = 1, emulate = 0;  // emulate = G: every rank's share in turn
+        hs_comm *comm = nullptr;
+        hs_exchange_fn ex = nullptr;
+        void *user = nullptr;
+    } ks_split;
+    bool ks_split_on = false;
     bool kprof_on = false;
     std::vector<cudaEvent_t> kprof_ev;       // pairs (start, end)
     std::vector<int> kprof_id;
@@ -299,7 +308,11 @@ CtP ev_relin_rescale(const hs_keys *K, const hs_ct *d, cudaStream_t st);
 // digit-parallel key switch: ModUp + inner product of
 // the digits [j0, j1) only -> acc [2][ntg][N]; acc += other (mod q, basis Q_l u P)
 void ks_partial(const hs_keys *K, const SwKey *key, int level, const u64 *d, int j0, int j1, u64 *acc,
-                cudaStream_t st);
+                cudaStream_t st, const u64 *dadd = nullptr, size_t dadd_stride = 0);
+// the full accumulator of one key switch through the context's active split
+// (this rank's digits + all-gather + rank-order sum, or emulated)
+void ks_split_acc(hs_ctx *c, const hs_keys *K, const SwKey *key, int level, const u64 *d, const u64 *dadd,
+                  size_t dadd_stride, u64 *acc, cudaStream_t st);
 void ks_acc_add(hs_ctx *c, int level, u64 *acc, const u64 *other, cudaStream_t st);
 void ks_moddown(hs_ctx *c, int level, int B, const u64 *acc, u64 *out, size_t out_stride, const u64 *add,
                 size_t add_stride, int add_comps, cudaStream_t st);

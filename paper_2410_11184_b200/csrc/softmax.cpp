@@ -101,6 +101,28 @@ struct RealEx {
         if (world > 1 && !d->exchange && !d->comm)
             throw HsError(HS_EINVAL, "softmax: world > 1 needs a communicator or an exchange callback");
     }
+    // digit-split the aux thread's key switches (d->aux_split)
+    void aux_split(bool on)
+    {
+        if (!d->aux_split) return;
+        if (on) {
+            hs_ctx::KsSplit S;
+            const int world = d->world < 1 ? 1 : d->world;
+            if (world > 1) {
+                S.rank = d->rank;
+                S.world = world;
+                S.comm = d->comm;
+                S.ex = d->exchange;
+                S.user = d->exchange_user;
+            } else {
+                S.emulate = d->aux_split >= 2 ? d->aux_split : 0;
+            }
+            c->ks_split = S;
+            c->ks_split_on = world > 1 || S.emulate >= 2;
+        } else {
+            c->ks_split_on = false;
+        }
+    }
     Ct gather(const T *const *in, int n) { return ct_gather(in, n, st); }
     Ct copy(const T *x) { return ct_copy(x, st); }
     Ct cheb(const T *x, const hs_poly *p, double gain) { return ev_cheb(K, x, p, gain, st); }
@@ -237,6 +259,22 @@ struct SymEx {
     }
     void exchange(T *, int) { s->exchanges += 1; }
     void domain_check(const T *, const hs_poly *) {}
+    void aux_split(bool) {}
+};
+
+// RAII: the aux thread's digit split is on between construction and end()
+// (or the scope's exit, also on an exception)
+template <class E>
+struct AuxScope {
+    E &ex;
+    bool on;
+    explicit AuxScope(E &e) : ex(e), on(true) { ex.aux_split(true); }
+    void end()
+    {
+        if (on) ex.aux_split(false);
+        on = false;
+    }
+    ~AuxScope() { end(); }
 };
 
 template <class E>
@@ -274,6 +312,9 @@ typename E::Ct softmax_body(E &ex, const hs_params *P, const hs_softmax_desc *d,
     const bool alg1 = d->variant != 1;
     const int main_need = d->variant == 3 ? 3 : 2;  // levels of the main update
     if (m % world || (size_t)(m / world) != m_local) throw HsError(HS_EINVAL, "softmax: m_local != m / world");
+    if (d->aux_split < 0 || (d->aux_split == 1 && world == 1) || (d->aux_split >= 2 && world > 1) ||
+        d->aux_split > 64)
+        throw HsError(HS_EINVAL, "softmax: aux_split must be 0, 1 (world > 1) or an emulated rank count >= 2");
     ex.check_exchange(world);
     const int nb = n / m;
     if ((nb & (nb - 1)) || nb > N0) throw HsError(HS_EINVAL, "softmax: n/m must be a power of two <= N0");
@@ -307,6 +348,8 @@ typename E::Ct softmax_body(E &ex, const hs_params *P, const hs_softmax_desc *d,
         CtP w = d->variant == 3 ? ex.mult(y.get(), y.get()) : CtP();
         CtP acc = w ? ex.tensor_sum2(w.get(), y.get()) : ex.tensor_sum(y.get());
         if (world > 1 || d->comm) ex.exchange(acc.get(), world);
+        // the aux thread proper: its key switches may be digit-split (d->aux_split)
+        AuxScope<E> aux_scope(ex);
         CtP S = ex.relin_rescale(acc.get());  // C8: one division by P q_l
         acc.reset();
         rot_sum(ex, S, nb, stride, -1);
@@ -361,6 +404,7 @@ typename E::Ct softmax_body(E &ex, const hs_params *P, const hs_softmax_desc *d,
         lj = ex.mult_pt(lj.get(), mask.data(), lj->level - 1);
         rot_sum(ex, lj, nb, stride, +1);
         lam = std::move(lj);
+        aux_scope.end();
         // ---- main thread (lam broadcast against the batch)
         if (lam->level < 1) level_error("lambda out of levels");
         if (d->variant == 0) {

@@ -674,3 +674,35 @@ def test_digit_parallel_keyswitch_parity(preset, level):
     hs.keyswitch_sharded(K, gal, level, dd.data_ptr(), 0, 2, o0.data_ptr(), o1.data_ptr(), exchange=fn)
     torch.cuda.synchronize()
     assert (host(o0).reshape(nl, P.n) == want0).all() and (host(o1).reshape(nl, P.n) == want1).all()
+
+
+@pytest.mark.parametrize("G", [2, 3])
+def test_aux_split_emulation_parity(toyb, tables, G):
+    """SURVEY 8(f) rank 1 inside the Softmax: with aux_split = G (world 1) every
+    key switch of the shared aux thread -- relinearisation of the aux sum,
+    rotate-and-sum, polynomial and lambda products, the bootstraps' EvalMod
+    products and conjugations -- runs as G digit shares summed mod q (the
+    sharded path's arithmetic, emulated in one process).  The config-3
+    schedule (version B, m = 16, bootstrapped) on the N = 2^12 ring with
+    P16's chain must give the unsplit words, ciphertext by ciphertext, and
+    the same as a replayed CUDA-graph plan."""
+    hs = _hs()
+    P, K = toyb["P"], toyb["K"]
+    tab = tables["p16_n256_M128_k5_B"]
+    cfg = tab["config"]
+    n, k, m = cfg["n"], cfg["k"], 16
+    L = (P.n // 2) * m // n
+    top = toyb["pre"]["bts"]["out_level"]
+    x = W.softmax_inputs(L, n, cfg["M"], seed=W.derive_seed("x", "aux-split"))
+    slots = P.pack(x, m)
+    cts = [hs.softmax_encrypt_input(K, slots[c], 10, tab["exp"], 77, c) for c in range(m)]
+    ref = hs.softmax_many_ctxt(K, cts, n, m, k, 1, tab["exp"], tab["inv"], bts=toyb["B"])
+    toyb["ctx"].ledger_reset()
+    got = hs.softmax_many_ctxt(K, cts, n, m, k, 1, tab["exp"], tab["inv"], bts=toyb["B"], aux_split=G)
+    assert toyb["ctx"].ledger()["bts"] > 0
+    for a, b in zip(got, ref):
+        same(a, b)
+    y = P.unpack(np.stack([hs.decrypt_decode(K, c).real for c in got]), L, n)
+    r = np.exp(x - x.max(1, keepdims=True))
+    r /= r.sum(1, keepdims=True)
+    assert np.abs(y - r).max() < 2.0 ** -15

@@ -472,7 +472,7 @@ def test_softmax_error_paths(tables):
     wrong.set_scale(2.0 * P.scale(top))
     assert code(lambda: hs.softmax_many_ctxt(K_full, [wrong], n, 1, k, 0, tab["exp"], tab["inv"])) == 4
     ct.set_scale(sc(top))  # the right declaration passes
-    assert code(lambda: hs.op(K_full, "mult", ct, ct)) == 4
+    assert code(lambda: hs.op(K_full, "mult", wrong, ct)) == 4  # wrong: declared at 2 Delta
     # HS_EDOMAIN (debug): an input outside [-M, 0] puts the aux sum outside the
     # first inverse-square-root interval
     ctx.debug_domain(K_full)

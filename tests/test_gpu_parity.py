@@ -610,7 +610,7 @@ def test_softmax_encrypt_input_parity(tables):
         same(g, o)
         alpha = 2.0 / (tab["exp"]["b"] - tab["exp"]["a"])
         err = np.abs(hs.decrypt_decode(K, g).real - alpha * slots).max()
-        assert err < 2.0 ** -30, np.log2(err)
+        assert err < 2.0 ** -28, np.log2(err)  # vs ~2^-22 for a fresh encryption at this scale
 
 
 @pytest.mark.parametrize("preset,level", [("TOY12", 9), ("P16U", 13), ("P16", 30)])

@@ -69,3 +69,87 @@ def test_stc_is_canonical_embedding_and_cts_inverts_it(log_n, n_stc, n_cts):
         cts = group(log_n, int(firsts[gi]), sz[gi], True) @ cts
     assert np.abs(cts @ stc - np.eye(n0)).max() < 1e-12
     assert np.abs(stc @ cts - np.eye(n0)).max() < 1e-12
+
+
+def test_cts_transforms_c17_apply_the_matrices():
+    """C17 (double-hoisted BSGS) pinned against the mathematics: on the
+    N = 2^12 ring with P16's chain, a ciphertext at the top level holding slot
+    vector z is run through the oracle's bootstrap up to its s-th
+    CoeffToSlot transform (orc_bts_debug_stop, ModRaise skipped); its
+    decryption must be f (T_{s-1} ... T_0) z, where T_k are the float64
+    stage-group matrices above and f = (Delta_L / q_0) / (2 (K + 2)) the
+    first transform's factor, within CKKS noise."""
+    import workloads as W
+    pre = W.preset("TOY12B")
+    P = O.Params.from_preset(pre)
+    cfg = pre["bts"]
+    tab = W.bts_tables()[cfg["table"]]
+    rots = O.bts_rotations(P, cfg)
+    gal = sorted({P.galois_of_rot(r) for r in rots} | {2 * P.n - 1})
+    K = O.Keys(P, 4321, pre["h"], galois=gal)
+    B = O.Bts(P, cfg, tab)
+    L_top = P.n_q - 1
+    n0, log_n = P.n // 2, P.log_n
+    s = log_n - 1
+    rng = np.random.default_rng(3)
+    z = rng.uniform(-1, 1, n0)
+    ct = O.encrypt(P, K, P.encode(z, scale=P.scale(L_top), level=L_top), L_top, 5, 0, use_sk=True)
+    f = (P.scale(L_top) / P.primes[0]) / (2 * (tab["K"] + 2))
+    sz = sizes(s, cfg["n_cts"])
+    firsts = np.cumsum([0] + sz[:-1])
+    L = O.lib()
+    L.orc_api_bts_debug_stop.argtypes = [C.c_int]
+    L.orc_api_bts_debug_skip_raise.argtypes = [C.c_int]
+    M = np.eye(n0, dtype=complex)
+    try:
+        L.orc_api_bts_debug_skip_raise(1)
+        for stop in range(1, cfg["n_cts"] + 1):
+            gi = cfg["n_cts"] - stop
+            M = group(log_n, int(firsts[gi]), sz[gi], True) @ M
+            L.orc_api_bts_debug_stop(stop)
+            out = O.bootstrap(P, K, ct, B, 1.0)
+            assert out.level == L_top - stop
+            got = O.decrypt_decode(P, K, out)
+            want = f * (M @ z)
+            err = np.abs(got - want).max() / np.abs(want).max()
+            assert err < 2.0 ** -20, (stop, np.log2(err))
+    finally:
+        L.orc_api_bts_debug_stop(-1)
+        L.orc_api_bts_debug_skip_raise(0)
+
+
+def test_evalmod_c18_even_series():
+    """C18 pinned: the oracle's EvalMod stage (the even cosine series
+    evaluated as a half-degree series on w = T_2(v) = 2v^2 - 1) must decrypt
+    to float64 Clenshaw of the FULL degree-63 table at the decrypted v
+    (orc_bts_debug_stop 10 -> v, 11 -> the series), within CKKS noise."""
+    from numpy.polynomial import chebyshev as Ch
+    import workloads as W
+    pre = W.preset("TOY12B")
+    P = O.Params.from_preset(pre)
+    cfg = pre["bts"]
+    tab = W.bts_tables()[cfg["table"]]
+    assert all(c == 0.0 for c in tab["coeffs"][1::2])  # even: the C18 case
+    rots = O.bts_rotations(P, cfg)
+    gal = sorted({P.galois_of_rot(r) for r in rots} | {2 * P.n - 1})
+    K = O.Keys(P, 99, pre["h"], galois=gal)
+    B = O.Bts(P, cfg, tab)
+    L_top = P.n_q - 1
+    z = np.random.default_rng(8).uniform(-1, 1, P.n // 2)
+    ct = O.encrypt(P, K, P.encode(z, scale=P.scale(L_top), level=L_top), L_top, 5, 0, use_sk=True)
+    L = O.lib()
+    L.orc_api_bts_debug_stop.argtypes = [C.c_int]
+    L.orc_api_bts_debug_skip_raise.argtypes = [C.c_int]
+    try:
+        L.orc_api_bts_debug_skip_raise(1)
+        L.orc_api_bts_debug_stop(10)
+        v = O.decrypt_decode(P, K, O.bootstrap(P, K, ct, B, 1.0)).real
+        L.orc_api_bts_debug_stop(11)
+        sct = O.bootstrap(P, K, ct, B, 1.0)
+        got = O.decrypt_decode(P, K, sct).real
+    finally:
+        L.orc_api_bts_debug_stop(-1)
+        L.orc_api_bts_debug_skip_raise(0)
+    assert np.abs(v).max() <= 1.0
+    want = Ch.chebval(v, tab["coeffs"])
+    assert np.abs(got - want).max() < 2.0 ** -20, np.log2(np.abs(got - want).max())

@@ -251,11 +251,13 @@ hs_status hs_keyswitch(hs_ctx *c, const hs_keys *k, int galois, int level, const
  *   hs_keyswitch_finish: ModDown of a summed accumulator -> out0, out1
  *     ((level+1) limbs each): the same words as hs_keyswitch.
  *   hs_keyswitch_sharded: rank `rank` of `world` computes its digit share
- *     [rank beta / world, (rank+1) beta / world), all-gathers the partials
- *     (native NCCL communicator `comm`, or the `exchange` callback of the
- *     Softmax descriptor's contract), adds them in rank order and finishes;
- *     every rank ends with hs_keyswitch's words.  HS_ENCCL on an exchange
- *     failure. */
+ *     [rank beta / world, (rank+1) beta / world) and combines the partials --
+ *     with a native NCCL communicator `comm`, an in-place uint64 sum
+ *     all-reduce followed by a reduction mod q (exact while world * q < 2^64,
+ *     e.g. world <= 8 with 61-bit primes; otherwise an all-gather), with the
+ *     `exchange` callback of the Softmax descriptor's contract an all-gather
+ *     added in rank order -- and finishes; every rank ends with
+ *     hs_keyswitch's words.  HS_ENCCL on an exchange failure. */
 hs_status hs_keyswitch_partial(hs_ctx *c, const hs_keys *k, int galois, int level, const uint64_t *d, int digit_begin,
                                int digit_end, uint64_t *acc, void *stream);
 hs_status hs_ks_acc_add(hs_ctx *c, int level, uint64_t *acc, const uint64_t *other, void *stream);

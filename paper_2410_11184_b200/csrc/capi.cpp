@@ -531,6 +531,19 @@ hs_status hs_keyswitch_sharded(hs_ctx *c, const hs_keys *k, int galois, int leve
     const size_t words = (size_t)2 * ntg * N;
     // rank r owns the digits [r beta / world, (r + 1) beta / world)
     const int j0 = (int)((long)rank * beta / world), j1 = (int)((long)(rank + 1) * beta / world);
+    if (comm && ks_sum_fits(P, world)) {
+        // uint64 sum all-reduce + mod q (exact while world * q < 2^64)
+        DBuf acc(words, st);
+        ks_partial(k, key, level, d, j0, j1, acc.p, st);
+        comm_all_reduce_u64(comm, acc.p, words, st);
+        PrimeMap pm;
+        pm.n = ntg;
+        for (int g = 0; g < ntg; g++) pm.p[g] = (unsigned char)(g < nl ? g : P->n_q + (g - nl));
+        k_mod_pm(c, acc.p, 2 * ntg, pm, st);
+        ks_finish_to(c, level, acc.p, out0, out1, st);
+        c->ledger[HS_LG_KS] += 1;
+        return HS_OK;
+    }
     DBuf part(words, st), gathered(words * world, st);
     ks_partial(k, key, level, d, j0, j1, part.p, st);
     if (world == 1) {

@@ -21,6 +21,8 @@ struct NcclApi {
     ncclResult_t (*commInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
     ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
     ncclResult_t (*allGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*allReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
     const char *(*errorString)(ncclResult_t) = nullptr;
 };
 
@@ -41,6 +43,7 @@ const NcclApi &nccl()
         api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
         api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
         api.allGather = (decltype(api.allGather))dlsym(h, "ncclAllGather");
+        api.allReduce = (decltype(api.allReduce))dlsym(h, "ncclAllReduce");
         api.errorString = (decltype(api.errorString))dlsym(h, "ncclGetErrorString");
     });
     if (!api.getUniqueId || !api.commInitRank || !api.commDestroy || !api.allGather)
@@ -68,6 +71,14 @@ int comm_world(const hs_comm *c) { return c->world; }
 void comm_all_gather(const hs_comm *c, const u64 *partial, u64 *gathered, size_t words, cudaStream_t st)
 {
     check(nccl().allGather(partial, gathered, words, ncclUint64, c->comm, st), "ncclAllGather");
+}
+
+// in-place uint64 sum over the ranks (the caller reduces mod q afterwards:
+// exact while world * max prime < 2^64)
+void comm_all_reduce_u64(const hs_comm *c, u64 *buf, size_t words, cudaStream_t st)
+{
+    if (!nccl().allReduce) throw HsError(HS_ENCCL, "ncclAllReduce not available");
+    check(nccl().allReduce(buf, buf, words, ncclUint64, ncclSum, c->comm, st), "ncclAllReduce");
 }
 
 void comm_unique_id(uint8_t uid[128])

@@ -414,6 +414,13 @@ void ks_partial(const hs_keys *K, const SwKey *key, int level, const u64 *d, int
     k_ks_inner_b(c, d, (size_t)nl * N, m.ext.p, m.off, m.nd, key->k, acc, level, j1, 1, st, dadd, dadd_stride, j0);
 }
 
+bool ks_sum_fits(const hs_params *P, int world)
+{
+    u64 mx = 0;
+    for (u64 q : P->prime) mx = std::max(mx, q);
+    return (u128)world * (mx - 1) < ((u128)1 << 64);
+}
+
 void ks_split_acc(hs_ctx *c, const hs_keys *K, const SwKey *key, int level, const u64 *d, const u64 *dadd,
                   size_t dadd_stride, u64 *acc, cudaStream_t st)
 {
@@ -438,6 +445,17 @@ void ks_split_acc(hs_ctx *c, const hs_keys *K, const SwKey *key, int level, cons
         return;
     }
     range(S.rank, S.world, j0, j1);
+    if (S.comm && ks_sum_fits(P, S.world)) {
+        // uint64 sum all-reduce (exact: world * q < 2^64), then mod q -- moves
+        // ~2x the accumulator per rank instead of world x
+        ks_partial(K, key, level, d, j0, j1, acc, st, S.rank == 0 ? dadd : nullptr, dadd_stride);
+        comm_all_reduce_u64(S.comm, acc, words, st);
+        PrimeMap pm;
+        pm.n = ntg;
+        for (int g = 0; g < ntg; g++) pm.p[g] = (unsigned char)(g < nl ? g : P->n_q + (g - nl));
+        k_mod_pm(c, acc, 2 * ntg, pm, st);
+        return;
+    }
     DBuf part(words, st), gathered(words * S.world, st);
     // the C8 P*d term rides with rank 0's share
     ks_partial(K, key, level, d, j0, j1, part.p, st, S.rank == 0 ? dadd : nullptr, dadd_stride);

@@ -365,6 +365,12 @@ hs_comm *comm_create(int rank, int world, const uint8_t uid[128]);
 void comm_destroy(hs_comm *comm);
 int comm_world(const hs_comm *c);
 void comm_all_gather(const hs_comm *c, const u64 *partial, u64 *gathered, size_t words, cudaStream_t st);
+void comm_all_reduce_u64(const hs_comm *c, u64 *buf, size_t words, cudaStream_t st);
+// x <- x mod q limb by limb (x < 2^64; prime of limb l = pm.p[l % pm.n])
+void k_mod_pm(hs_ctx *c, u64 *a, int n_limbs, const PrimeMap &pm, cudaStream_t st);
+// true when a uint64 sum of world accumulators stays below 2^64 (then an
+// NCCL all-reduce + mod q replaces the all-gather of the digit split)
+bool ks_sum_fits(const hs_params *P, int world);
 void check_scales(const hs_ct *a, const hs_ct *b);  // C11: HS_ESCALE on a mismatch
 hs_status softmax_run(hs_ctx *c, const hs_keys *K, const hs_softmax_desc *d, const hs_ct *const *in,
                       size_t m_local, cudaStream_t st, hs_ct **out);

@@ -855,6 +855,25 @@ __global__ void add_pm_kernel(const u64 *a, const u64 *b, u64 *o, PrimeMap pm, i
     o[x] = d_add(a[x], b[x], c_pk[pm.p[l % pm.n]].q);
 }
 
+__global__ void mod_pm_kernel(u64 *a, PrimeMap pm, int N)
+{
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= N) return;
+    const int l = blockIdx.y;
+    const PrimeK k = c_pk[pm.p[l % pm.n]];
+    u64 *x = a + (size_t)l * N + t;
+    *x = d_reduce128(0, *x, k);  // x < 2^64 < q 2^64: exact x mod q
+}
+
+void k_mod_pm(hs_ctx *c, u64 *a, int n_limbs, const PrimeMap &pm, cudaStream_t st)
+{
+    KTimer _kt(c, KID_ADD, (double)n_limbs * c->P->n * 16, st);
+    int N = c->P->n;
+    mod_pm_kernel<<<GRID_LIMBS(n_limbs, N), 256, 0, st>>>(a, pm, N);
+    HS_CHECK_LAUNCH();
+    count_kernel(c);
+}
+
 void k_add_pm(hs_ctx *c, const u64 *a, const u64 *b, u64 *o, int n_limbs, const PrimeMap &pm, cudaStream_t st)
 {
     KTimer _kt(c, KID_ADD, (double)n_limbs * c->P->n * 24, st);

@@ -674,6 +674,14 @@ def test_digit_parallel_keyswitch_parity(preset, level):
     hs.keyswitch_sharded(K, gal, level, dd.data_ptr(), 0, 2, o0.data_ptr(), o1.data_ptr(), exchange=fn)
     torch.cuda.synchronize()
     assert (host(o0).reshape(nl, P.n) == want0).all() and (host(o1).reshape(nl, P.n) == want1).all()
+    # the native-communicator path (uint64 sum all-reduce + mod q) on a one-rank NCCL communicator
+    comm = hs.Comm(ctx, 0, 1, hs.Comm.unique_id())
+    o0.zero_()
+    o1.zero_()
+    hs.keyswitch_sharded(K, gal, level, dd.data_ptr(), 0, 1, o0.data_ptr(), o1.data_ptr(), comm=comm)
+    torch.cuda.synchronize()
+    assert (host(o0).reshape(nl, P.n) == want0).all() and (host(o1).reshape(nl, P.n) == want1).all()
+    del comm
 
 
 @pytest.mark.parametrize("G", [2, 3])

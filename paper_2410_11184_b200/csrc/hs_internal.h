@@ -14,6 +14,7 @@
 //   capi.cpp     extern "C" boundary (include/hesoftmax.h)
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -94,6 +95,7 @@ struct hs_ctx {
     std::map<long, BconvTab> bconv;          // key: (level << 8 | digit), digit 255 = ModDown
     std::map<int, unsigned *> galois_perm;   // device permutation tables
     std::map<std::pair<u64, long>, u64 *> pt_cache;  // (content hash, level pair) -> NTT plaintext
+    std::map<const u64 *, CUtensorMap> key_tmaps;     // TMA tensor maps of switching keys (kernels.cu)
     std::mutex mu;
     int64_t ledger[HS_LG_COUNT] = {0};
     const hs_keys *debug_keys = nullptr;  // hs_ctx_debug_domain: keys WITH the secret

@@ -6,6 +6,8 @@
 // (tensor, evaluation-key inner product).  All results are canonical
 // residues in [0, q), so every kernel is bit-identical to the oracle's
 // plain `%` arithmetic.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <cstdio>
@@ -1871,10 +1873,163 @@ __global__ void __launch_bounds__(256) ks_inner_h_kernel(const u64 *__restrict__
     acc[((size_t)(r * 2 + 1) * ntg + g) * N + t] = d_reduce128(h1, l1, k);
 }
 
+// ---- TMA-streamed variant: the evaluation keys -- the
+// bytes that dominate a hoisted key switch (R keys of 2 beta ntg limbs) --
+// arrive by cp.async.bulk.tensor (one 3-D tensor map per key: (pair, N,
+// dnum (n_q + n_p)) u64, box (2, 256, 1) = 4 KiB) into shared memory, all
+// beta digits of a CTA's (rotation, 256-coefficient block, target limb) tile
+// requested up front on one mbarrier, while the threads gather the extended
+// digits through the rotation's permutation with ordinary loads.
+struct KsArgHT {
+    CUtensorMap tmap[HS_MAXROT];  // 64-byte aligned (CUtensorMap is declared aligned(64))
+    const unsigned *perm[HS_MAXROT];
+    int level, beta, alpha, n_q, n_t;
+    size_t off[HS_MAXDIG];
+    int nd[HS_MAXDIG];
+    const u64 *c0add;
+    u64 pmq[HS_MAXP];
+};
+
+__global__ void __launch_bounds__(256) ks_inner_h_tma_kernel(const u64 *__restrict__ d, const u64 *__restrict__ ext,
+                                                             u64 *__restrict__ acc,
+                                                             const __grid_constant__ KsArgHT A, int N)
+{
+    extern __shared__ __align__(128) unsigned char ks_smem[];
+    __shared__ __align__(8) unsigned long long bar;
+    const int tid = threadIdx.x, t0 = blockIdx.y * 256, t = t0 + tid;
+    const int g = blockIdx.z, r = blockIdx.x;
+    const int nl = A.level + 1, ntg = nl + A.n_t;
+    const int pi = g < nl ? g : A.n_q + (g - nl);
+    const PrimeK k = c_pk[pi];
+    const int ntot = A.n_q + A.n_t;
+    const unsigned sbar = (unsigned)__cvta_generic_to_shared(&bar);
+    const unsigned skey = (unsigned)__cvta_generic_to_shared(ks_smem);
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbar));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0) {
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sbar), "r"(A.beta * 4096)
+                     : "memory");
+        const CUtensorMap *tm = &A.tmap[r];
+        for (int j = 0; j < A.beta; j++)
+            asm volatile(
+                "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+                "[%5];" ::"r"(skey + j * 4096),
+                "l"(reinterpret_cast<uint64_t>(tm)), "r"(0), "r"(t0), "r"(j * ntot + pi), "r"(sbar)
+                : "memory");
+    }
+    const bool live = t < N;
+    const unsigned src = live ? __ldg(A.perm[r] + t) : 0;
+    // wait for the key tiles (phase 0)
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "KS_TMA_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], 0;\n\t"
+        "@!P bra KS_TMA_WAIT;\n\t}" ::"r"(sbar)
+        : "memory");
+    if (!live) return;
+    const ulonglong2 *kt = reinterpret_cast<const ulonglong2 *>(ks_smem);
+    u64 h0 = 0, l0 = 0, h1 = 0, l1 = 0;
+#pragma unroll 4
+    for (int j = 0; j < A.beta; j++) {
+        const int lo = j * A.alpha, hi = min((j + 1) * A.alpha, nl), dn = hi - lo;
+        const ulonglong2 kk = kt[j * 256 + tid];
+        const bool own = g >= lo && g < hi;
+        const int gg = g < lo ? g : g - dn;
+        const u64 v = own ? d[(size_t)g * N + src] : ext[A.off[j] + (size_t)gg * N + src];
+        mac128(h0, l0, v, kk.x);
+        mac128(h1, l1, v, kk.y);
+    }
+    if (A.c0add && g < nl) mac128(h0, l0, A.c0add[(size_t)g * N + src], A.pmq[g]);
+    acc[((size_t)r * 2 * ntg + g) * N + t] = d_reduce128(h0, l0, k);
+    acc[((size_t)(r * 2 + 1) * ntg + g) * N + t] = d_reduce128(h1, l1, k);
+}
+
+// one 3-D tensor map per switching key, cached by device pointer
+static const CUtensorMap &key_tmap(hs_ctx *c, const u64 *key)
+{
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    if (!encode) throw HsError(HS_ECUDA, "cuTensorMapEncodeTiled not available");
+    std::lock_guard<std::mutex> lk(c->mu);
+    auto it = c->key_tmaps.find(key);
+    if (it != c->key_tmaps.end()) return it->second;
+    const hs_params *P = c->P;
+    const cuuint64_t rows = (cuuint64_t)P->dnum * (P->n_q + P->n_p);
+    const cuuint64_t dims[3] = {2, (cuuint64_t)P->n, rows};
+    const cuuint64_t strides[2] = {16, (cuuint64_t)P->n * 16};
+    const cuuint32_t box[3] = {2, 256, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUtensorMap m;
+    CUresult rc = encode(&m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<u64 *>(key), dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (rc != CUDA_SUCCESS) throw HsError(HS_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)rc));
+    return c->key_tmaps[key] = m;
+}
+
+static bool ks_tma_on()
+{
+    static const bool on = [] {
+        const char *e = getenv("HS_KS_TMA");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 void k_ks_inner_h(hs_ctx *c, const u64 *d, const u64 *ext, const size_t *off, const int *nd, const u64 *const *keys,
                   const unsigned *const *perms, int R, u64 *acc, int level, int beta, cudaStream_t st,
                   const u64 *c0add)
 {
+    if (ks_tma_on() && c->P->n % 256 == 0 && beta <= HS_MAXDIG) {
+        const hs_params *P = c->P;
+        const int ntg = level + 1 + P->n_p;
+        if (R < 1 || R > HS_MAXROT) throw HsError(HS_EINVAL, "hoisted key switch: bad rotation count");
+        KTimer _kt(c, KID_KS_HOIST,
+                   ((double)R * beta * ntg * 16.0 + (double)beta * ntg * 8.0 + 16.0 * ntg * R +
+                    (c0add ? 8.0 * (level + 1) : 0.0)) *
+                       P->n,
+                   st);
+        static KsArgHT A;  // ~10 KB: kept off the stack; launches copy their parameters
+        static std::mutex amu;
+        std::lock_guard<std::mutex> lk(amu);
+        for (int r = 0; r < R; r++) {
+            A.tmap[r] = key_tmap(c, keys[r]);
+            A.perm[r] = perms[r];
+        }
+        A.level = level;
+        A.beta = beta;
+        A.alpha = P->alpha;
+        A.n_q = P->n_q;
+        A.n_t = P->n_p;
+        for (int j = 0; j < beta; j++) {
+            A.off[j] = off[j];
+            A.nd[j] = nd[j];
+        }
+        A.c0add = c0add;
+        if (c0add)
+            for (int i = 0; i <= level; i++) A.pmq[i] = P->p_mod_q[i];
+        const int N = P->n;
+        const size_t smem = (size_t)beta * 4096;
+        static bool attr = false;
+        if (!attr) {
+            HS_CUDA(cudaFuncSetAttribute(ks_inner_h_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         HS_MAXDIG * 4096));
+            attr = true;
+        }
+        ks_inner_h_tma_kernel<<<dim3(R, N / 256, ntg), 256, smem, st>>>(d, ext, acc, A, N);
+        HS_CHECK_LAUNCH();
+        count_kernel(c);
+        return;
+    }
     const hs_params *P = c->P;
     const int ntg = level + 1 + P->n_p;
     if (R < 1 || R > HS_MAXROT) throw HsError(HS_EINVAL, "hoisted key switch: bad rotation count");

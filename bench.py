@@ -133,7 +133,8 @@ class Clocks:
 def build_setup(wl_name, rank, world, device):
     import paper_2410_11184_b200 as hs
     wl = W.WORKLOADS[wl_name]
-    pre = W.preset(wl["preset"])
+    # HS_PRESET: run the workload on another chain (measurement experiments)
+    pre = W.preset(os.environ.get("HS_PRESET", wl["preset"]))
     tab = W.poly_tables()[wl["table"]]
     n, m, L, k = wl["n"], wl["m"], wl["L"], wl["k"]
     P = hs.Params.from_preset(pre)
@@ -342,7 +343,7 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": False, "scaling": "strong",
         "vs_baseline": round(value / paper_ms, 6) if paper_ms else None, "vs_baseline_ref": paper_ref,
         "dtype": "u64 (RNS residues)", "data": "synthetic (x ~ N(-M/2,(M/6)^2) tail-cut)",
-        "config": {"workload": desc, "preset": S["wl"]["preset"],
+        "config": {"workload": desc, "preset": os.environ.get("HS_PRESET", S["wl"]["preset"]),
                    "softmax_per_step": softmax_per_step, "ciphertexts": S["m"],
                    "input_level": S["in_level"],
                    "input": ("x encrypted at input_level + 1 (planner: hs_softmax_input_level), rescaled once "

@@ -118,6 +118,13 @@ def bts_tables() -> dict:
         return json.load(fh)
 
 
+# P16 with 12 user levels (round-2 comparison point: 8 bootstraps for config 3
+# instead of 7); bench.py HS_PRESET=P16L12
+PRESETS["P16L12"] = dict(PRESETS["P16"], q_bits=[60] + [42] * 12 + [48] * 3 + [59] * 11 + [60] * 4,
+                         log2_anchor=_anchors(31, [(30, 60), (29, 63), (28, 62), (27, 60), (26, 59), (14, 48),
+                                                   (13, 48), (12, 42)]),
+                         bts=dict(PRESETS["P16"]["bts"], out_level=12))
+
 # N = 2^12 ring with P16's exact modulus chain (bootstrapping included):
 # parity / precision tests of configs 2-5 at a size the oracle finishes quickly.
 PRESETS["TOY12B"] = dict(PRESETS["P16"], log_n=12)

@@ -75,6 +75,8 @@ def parse():
     ap.add_argument("--kprof", default="timed", choices=["timed", "extra", "off"])
     ap.add_argument("--no-graph", action="store_true", help="eager C-ABI calls instead of a CUDA-graph plan")
     ap.add_argument("--no-primitives", action="store_true", help="skip the HMult / rotation ops/s block")
+    ap.add_argument("--aux-split", default="on", choices=["on", "off"],
+                    help="N > 1: digit-split the aux thread's key switches over the ranks")
     return ap.parse_args()
 
 
@@ -201,15 +203,36 @@ def run_ours(args):
     use_graph = not args.no_graph
     wl = S["wl"]
 
+    # N > 1: the aux thread's key switches are digit-split over the ranks
+    # (hs_softmax_desc.aux_split) unless --aux-split off;
+    # every rank must agree, so a failure on any rank falls back everywhere
+    aux_split = 1 if (world > 1 and args.aux_split == "on") else 0
+
     def step(inputs):
         return hs.softmax_many_ctxt(K, inputs, S["n"], S["m"], S["k"], wl["variant"], tab["exp"], tab["inv"],
-                                    bts=B, comm=comm)
+                                    bts=B, comm=comm, aux_split=aux_split)
 
     def make_plan():
         return hs.Plan(K, S["cts"], S["n"], S["m"], S["k"], wl["variant"], tab["exp"], tab["inv"], bts=B,
-                       comm=comm)
+                       comm=comm, aux_split=aux_split)
 
-    plan = make_plan() if use_graph else None  # warm-up run + capture (outside timing)
+    plan = None
+    if use_graph:  # warm-up run + capture (outside timing)
+        ok = 1
+        try:
+            plan = make_plan()
+        except hs.HsError as e:
+            if not aux_split:
+                raise
+            print(f"aux_split plan failed ({e}); falling back", file=sys.stderr)
+            ok = 0
+        if world > 1:
+            t = torch.tensor([ok], device="cuda")
+            dist_.all_reduce(t, op=dist_.ReduceOp.MIN)
+            ok = int(t.item())
+        if not ok:
+            plan, aux_split = None, 0
+            plan = make_plan()
     run_step = plan.run if use_graph else (lambda: step(S["cts"]))
     for _ in range(args.warmup):
         out = run_step()
@@ -346,6 +369,8 @@ def run_ours(args):
         "config": {"workload": desc, "preset": os.environ.get("HS_PRESET", S["wl"]["preset"]),
                    "softmax_per_step": softmax_per_step, "ciphertexts": S["m"],
                    "input_level": S["in_level"],
+                   "aux_split": ("aux-thread key switches digit-split over the ranks (NCCL all-reduce)"
+                                 if aux_split else "off"),
                    "input": ("x encrypted at input_level + 1 (planner: hs_softmax_input_level), rescaled once "
                              "(hs_softmax_encrypt_input, DESIGN.md G28)"),
                    "l2": (f"inputs {in_mib:.0f} MiB; every step runs the whole Softmax (>= {S['k']} bootstraps "

@@ -529,15 +529,18 @@ class Plan:
     bound to the input ciphertexts `cts` (re-read at every run); outputs are
     plan-owned and overwritten by each run()."""
 
-    def __init__(self, keys: Keys, cts, n, m, k, variant, exp_poly, inv_polys, bts=None, stream=None, comm=None):
+    def __init__(self, keys: Keys, cts, n, m, k, variant, exp_poly, inv_polys, bts=None, stream=None, comm=None,
+                 aux_split=0):
         """comm: a Comm of world > 1 makes this a sharded plan (this rank's
-        m / world ciphertexts; the NCCL all-gather is captured in the graph)."""
+        m / world ciphertexts; the NCCL all-gather is captured in the graph).
+        aux_split: digit-split the aux thread's key switches (hs_softmax_desc)."""
         # the captured graph bakes in device pointers of the keys, the input
         # ciphertexts, the bootstrapping plan's transforms and the communicator:
         # the plan keeps every one of them alive
         self.keys, self.cts, self._bts, self._comm = keys, list(cts), bts, comm
         world, rank = (comm.world, comm.rank) if comm is not None else (1, 0)
-        self._d, self._keep = _softmax_desc(n, m, k, variant, exp_poly, inv_polys, world, rank, None, bts, comm)
+        self._d, self._keep = _softmax_desc(n, m, k, variant, exp_poly, inv_polys, world, rank, None, bts, comm,
+                                            aux_split)
         ml = len(cts)
         ins = (C.c_void_p * ml)(*[c.ptr.value if isinstance(c.ptr, C.c_void_p) else c.ptr for c in cts])
         p = C.c_void_p()

@@ -371,6 +371,8 @@ def run_ours(args):
                    "input_level": S["in_level"],
                    "aux_split": ("aux-thread key switches digit-split over the ranks (NCCL all-reduce)"
                                  if aux_split else "off"),
+                   "parallelism": (f"{world} ranks: the {S['m']} main-thread ciphertexts sharded "
+                                   f"({S['ml']} per rank), aux sum all-gathered (NCCL)" if world > 1 else "1 GPU"),
                    "input": ("x encrypted at input_level + 1 (planner: hs_softmax_input_level), rescaled once "
                              "(hs_softmax_encrypt_input, DESIGN.md G28)"),
                    "l2": (f"inputs {in_mib:.0f} MiB; every step runs the whole Softmax (>= {S['k']} bootstraps "

@@ -1890,58 +1890,65 @@ struct KsArgHT {
     u64 pmq[HS_MAXP];
 };
 
-__global__ void __launch_bounds__(256) ks_inner_h_tma_kernel(const u64 *__restrict__ d, const u64 *__restrict__ ext,
+__global__ void __launch_bounds__(256, 6) ks_inner_h_tma_kernel(const u64 *__restrict__ d, const u64 *__restrict__ ext,
                                                              u64 *__restrict__ acc,
                                                              const __grid_constant__ KsArgHT A, int N)
 {
     extern __shared__ __align__(128) unsigned char ks_smem[];
-    __shared__ __align__(8) unsigned long long bar;
+    __shared__ __align__(8) unsigned long long bar[HS_MAXDIG];  // one per digit: compute starts as tiles land
     const int tid = threadIdx.x, t0 = blockIdx.y * 256, t = t0 + tid;
     const int g = blockIdx.z, r = blockIdx.x;
     const int nl = A.level + 1, ntg = nl + A.n_t;
     const int pi = g < nl ? g : A.n_q + (g - nl);
     const PrimeK k = c_pk[pi];
     const int ntot = A.n_q + A.n_t;
-    const unsigned sbar = (unsigned)__cvta_generic_to_shared(&bar);
+    const unsigned sbar = (unsigned)__cvta_generic_to_shared(bar);
     const unsigned skey = (unsigned)__cvta_generic_to_shared(ks_smem);
-    if (tid == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbar));
+    if (tid < A.beta) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbar + 8 * tid));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (tid == 0) {
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sbar), "r"(A.beta * 4096)
-                     : "memory");
+    if (tid < A.beta) {  // one issuing thread per digit
+        const int j = tid;
         const CUtensorMap *tm = &A.tmap[r];
-        for (int j = 0; j < A.beta; j++)
-            asm volatile(
-                "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
-                "[%5];" ::"r"(skey + j * 4096),
-                "l"(reinterpret_cast<uint64_t>(tm)), "r"(0), "r"(t0), "r"(j * ntot + pi), "r"(sbar)
-                : "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], 4096;" ::"r"(sbar + 8 * j) : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+            "[%5];" ::"r"(skey + j * 4096),
+            "l"(reinterpret_cast<uint64_t>(tm)), "r"(0), "r"(t0), "r"(j * ntot + pi), "r"(sbar + 8 * j)
+            : "memory");
     }
     const bool live = t < N;
     const unsigned src = live ? __ldg(A.perm[r] + t) : 0;
-    // wait for the key tiles (phase 0)
-    asm volatile(
-        "{\n\t.reg .pred P;\n\t"
-        "KS_TMA_WAIT:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], 0;\n\t"
-        "@!P bra KS_TMA_WAIT;\n\t}" ::"r"(sbar)
-        : "memory");
-    if (!live) return;
-    const ulonglong2 *kt = reinterpret_cast<const ulonglong2 *>(ks_smem);
-    u64 h0 = 0, l0 = 0, h1 = 0, l1 = 0;
-#pragma unroll 4
-    for (int j = 0; j < A.beta; j++) {
+    // the permuted extended digits, gathered while the key tiles are in flight
+    // (up to 8 digits ahead; later digits gather in the loop)
+    auto gather = [&](int j) -> u64 {
         const int lo = j * A.alpha, hi = min((j + 1) * A.alpha, nl), dn = hi - lo;
-        const ulonglong2 kk = kt[j * 256 + tid];
         const bool own = g >= lo && g < hi;
         const int gg = g < lo ? g : g - dn;
-        const u64 v = own ? d[(size_t)g * N + src] : ext[A.off[j] + (size_t)gg * N + src];
-        mac128(h0, l0, v, kk.x);
-        mac128(h1, l1, v, kk.y);
+        return !live ? 0 : own ? d[(size_t)g * N + src] : ext[A.off[j] + (size_t)gg * N + src];
+    };
+    u64 v[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) v[j] = j < A.beta ? gather(j) : 0;
+    const ulonglong2 *kt = reinterpret_cast<const ulonglong2 *>(ks_smem);
+    u64 h0 = 0, l0 = 0, h1 = 0, l1 = 0;
+#pragma unroll
+    for (int j = 0; j < HS_MAXDIG; j++) {
+        if (j >= A.beta) break;
+        const u64 vj = j < 8 ? v[j] : gather(j);
+        asm volatile(
+            "{\n\t.reg .pred P;\n\t"
+            "KS_TMA_WAIT_%=:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], 0;\n\t"
+            "@!P bra KS_TMA_WAIT_%=;\n\t}" ::"r"(sbar + 8 * j)
+            : "memory");
+        const ulonglong2 kk = kt[j * 256 + tid];
+        mac128(h0, l0, vj, kk.x);
+        mac128(h1, l1, vj, kk.y);
     }
+    if (!live) return;
     if (A.c0add && g < nl) mac128(h0, l0, A.c0add[(size_t)g * N + src], A.pmq[g]);
     acc[((size_t)r * 2 * ntg + g) * N + t] = d_reduce128(h0, l0, k);
     acc[((size_t)(r * 2 + 1) * ntg + g) * N + t] = d_reduce128(h1, l1, k);
@@ -1976,11 +1983,12 @@ static const CUtensorMap &key_tmap(hs_ctx *c, const u64 *key)
     return c->key_tmaps[key] = m;
 }
 
+// HS_KS_TMA=1 selects the TMA variant (measured: DESIGN.md section 6)
 static bool ks_tma_on()
 {
     static const bool on = [] {
         const char *e = getenv("HS_KS_TMA");
-        return !(e && e[0] == '0');
+        return e && e[0] == '1';
     }();
     return on;
 }

@@ -185,8 +185,12 @@ CONFIGS = {
     "toy_n4_M4_k2_T3": dict(n=4, M=4, k=2, variant="T3", deg_exp=7, deg_first=15, deg_mid=31, deg_last=31),
     # P16 configs 2-4 (n=256/128, M=128, k=5)
     "p16_n256_M128_k5_A": dict(n=256, M=128, k=5, variant="A", deg_exp=15, deg_first=63, deg_mid=31, deg_last=127),
-    "p16_n256_M128_k5_B": dict(n=256, M=128, k=5, variant="B", deg_exp=15, deg_first=63, deg_mid=31, deg_last=127),
-    "p16_n128_M128_k5_B": dict(n=128, M=128, k=5, variant="B", deg_exp=15, deg_first=63, deg_mid=31, deg_last=127),
+    # version B (configs 3, 4): exp degree 11 -- the same 4 levels as degree 15
+    # (tab:depth_main), 2^-31 absolute instead of 2^-45 (below the CKKS noise
+    # floor either way), and 6 instead of 8 products on every one of the m
+    # main-thread ciphertexts (G30)
+    "p16_n256_M128_k5_B": dict(n=256, M=128, k=5, variant="B", deg_exp=11, deg_first=63, deg_mid=31, deg_last=127),
+    "p16_n128_M128_k5_B": dict(n=128, M=128, k=5, variant="B", deg_exp=11, deg_first=63, deg_mid=31, deg_last=127),
     # config 2 with square-and-normalize (G26): x^-1 needs degree 63 where x^-1/2 takes 31
     "p16_n256_M128_k5_S": dict(n=256, M=128, k=5, variant="S", deg_exp=15, deg_first=63, deg_mid=63, deg_last=127),
     # config 5 (n = N0 = 32768, M = 256, Alg 1, k = 7): degree-255

@@ -168,3 +168,22 @@ def test_input_level_choice_matches_workload(tables):
     with pytest.raises(hs.HsError):  # one level lower no longer fits
         hs.softmax_schedule(P, wl["n"], wl["m"], wl["k"], wl["variant"], tab["exp"], tab["inv"], lv - 1,
                             bts_out_level=pre["bts"]["out_level"])
+
+
+def test_reference_inventory_matches_planner(tables):
+    """bench.py's reference arm weights its oracle samples by the oracle's OWN
+    op inventory of the config-3 step (the exact schedule on a 2^10 ring with
+    P16's chain and a bootstrap stub); its bootstrap count must equal the
+    product planner's for the same workload and input level -- two independent
+    implementations of G12 agreeing on the full-size schedule."""
+    import bench
+    wl = W.WORKLOADS["config3"]
+    tab = tables[wl["table"]]
+    ks, n_bts = bench.oracle_inventory(wl["input_level"])
+    pre = W.preset("P16")
+    P = hs.Params.from_preset(pre)
+    s = hs.softmax_schedule(P, wl["n"], wl["m"], wl["k"], wl["variant"], tab["exp"], tab["inv"], wl["input_level"],
+                            bts_out_level=pre["bts"]["out_level"])
+    assert n_bts == s["bts_main"] + s["bts_aux"] == 7
+    assert min(ks) >= 0 and max(ks) <= pre["bts"]["out_level"]
+    assert sum(ks.values()) > 1000

@@ -80,6 +80,16 @@ def parse():
     return ap.parse_args()
 
 
+def ncu_ntt_pipes():
+    """the committed ncu capture of the NTT kernels (pipe utilisation beside
+    the derived butterfly peak; profiles/r02_ncu_ntt_pipes.json)"""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_ncu_ntt_pipes.json")) as fh:
+            return json.load(fh)
+    except Exception:
+        return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -355,7 +365,7 @@ def run_ours(args):
                     "peak_source": "derived: 148 SM x 4 SMSP x 1.965 GHz / IMAD-pipe cycles per warp-butterfly "
                                    "(SASS mix, IMAD.WIDE rt 4, other IMAD rt 2); DESIGN.md section 6",
                     "algorithmic_butterflies_per_launch": int(bfly), "avg_launch_us": round(avg_ms * 1e3, 2),
-                    "share_of_step": share}
+                    "share_of_step": share, "ncu_pipes": ncu_ntt_pipes()}
         ach = bytes_per / (avg_ms * 1e-3) / 1e9
         return {"kernel": name, "bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(ach / hbm, 4), "traffic": None, "peak_source": peak_src,

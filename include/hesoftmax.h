@@ -399,7 +399,9 @@ hs_status hs_softmax_input_level(const hs_params *p, const hs_softmax_desc *d, s
  * the aux sum before each inverse-square-root polynomial and returns
  * HS_EDOMAIN if a slot lies outside the polynomial's interval [a, b] (widened
  * by 1/64 of its width) -- e.g. an input outside [-M, 0].  NULL disables it.
- * Debug only: it synchronises the stream and cannot run inside a plan. */
+ * Debug only: it synchronises the stream and cannot run inside a plan.  The
+ * keys must outlive the setting (the context keeps the pointer; pass NULL
+ * before destroying them).  HS_EKEY for keys without the secret. */
 hs_status hs_ctx_debug_domain(hs_ctx *c, const hs_keys *k);
 
 /* One ciphertext (m = 1). */

@@ -13,6 +13,11 @@
  *   packings                      PAPER.md 94-131 [sec 4.1-4.2]
  *   many-ciphertext aux sum       DESIGN.md C15 / G6 (sum of tensors, one relin)
  *   bootstrap placement           PAPER.md 429-440 [sec 5.1.3], rule G12
+ *   level-exact polynomials       PAPER.md 330-336 (ceil(log(d+1)) levels) via
+ *                                 the C13 tree; the affine map's factor folded
+ *                                 into gains (G28): the input holds
+ *                                 alpha_exp x, the main thread carries g_j, the
+ *                                 masks the compensating factors
  *
  * Unified packing: m ciphertexts, nb = n/m coordinate
  * blocks per ciphertext, stride = N0/nb; instance o (o < stride) of

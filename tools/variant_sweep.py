@@ -35,7 +35,7 @@ def main():
         hs, K, B, P, ctx = S["hs"], S["K"], S["B"], S["P"], S["ctx"]
         tables = W.poly_tables()
         cands = [dict(k=5, variant=v, exp=tables[t]["exp"], inv=tables[t]["inv"]) for v, t in tabs.items()]
-        best, sched = hs.softmax_choose(P, cands, 256, m, S["top"], bts_out_level=S["top"])
+        best, sched = hs.softmax_choose(P, cands, 256, m, S["in_level"], bts_out_level=S["top"])
         meas = {}
         for (v, t), pl in zip(tabs.items(), sched):
             tab = tables[t]

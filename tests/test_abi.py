@@ -116,3 +116,25 @@ def test_bts_plan_conventions_match(name):
     for arc in [True, False]:
         for b in [0.5, 1.0, 1.5, 2.0, 64.0, 261.0, 1e6]:
             assert hs.bts_exponent(P, arc, b) == O.bts_exponent(PO, arc, b)
+
+
+def test_params_reject_unsupported_key_switch_shapes():
+    """hs_ckks_params (include/hesoftmax.h; round-1 advisor findings): the
+    key-switch kernels take n_p == alpha special primes, hold at most 16 digit
+    offsets and accumulate (dnum + 1) products in 128 bits -- descriptors
+    outside those limits are refused with HS_EINVAL instead of silently
+    computing wrong words."""
+    import paper_2410_11184_b200 as hs
+    base = W.preset("TOY12")
+
+    def make(**kw):
+        p = dict(base, **kw)
+        return hs.Params.from_preset(p)
+
+    with pytest.raises(hs.HsError) as e:
+        make(p_bits=[61, 61, 61])          # n_p = 3 != alpha = 2
+    assert e.value.code == 1
+    with pytest.raises(hs.HsError) as e:   # 17 digits of one prime each
+        make(q_bits=[60] + [40] * 16, log2_anchor=[0] * 16 + [40], alpha=1, p_bits=[61])
+    assert e.value.code == 1
+    make()  # the preset itself is fine

@@ -96,7 +96,38 @@ double hs_params_scale(const hs_params *p, int level);
 int hs_galois_of_rot(const hs_params *p, int r);
 
 /* ------------------------------------------------------------ context */
+/* One GPU context: uploads the twiddle tables of p to `device`.  Device
+ * memory comes from the device's default stream-ordered pool
+ * (cudaMallocAsync / cudaMalloc).  HS_EINVAL: NULL argument or no such
+ * device; HS_ECUDA / HS_ENOMEM from the runtime.  p must outlive the context. */
 hs_status hs_context_create(const hs_params *p, int device, hs_ctx **out);
+
+/* Allocator hook ("library-owned device memory goes through
+ * alloc", e.g. bound to torch's caching allocator so that the library and
+ * the framework around it share one pool).
+ *   alloc(bytes, stream, user): return device memory of >= bytes usable in
+ *     stream order on `stream` (a cudaStream_t as void*, NULL = legacy
+ *     default stream), or NULL on failure (the call then fails with
+ *     HS_ENOMEM).  Long-lived objects (twiddle / BConv / Galois tables,
+ *     keys, cached plaintexts, bootstrap transforms) are allocated with
+ *     stream NULL and freed only after a device synchronisation.
+ *   free(ptr, bytes, stream, user): release ptr in stream order on `stream`
+ *     (the stream of the last use the library knows of).
+ * Every object created under the context (keys, ciphertexts, plans' input
+ * and output ciphertexts, bootstrap caches) allocates through the hook.
+ * Exception: scratch memory of work captured into a CUDA graph
+ * (hs_softmax_plan_create) is graph-owned (cudaMallocAsync memory nodes) and
+ * never reaches the hook.  The hook struct is copied; its functions must stay
+ * callable until the last object allocated through them is destroyed, and
+ * must not call back into this library.  alloc == NULL selects the default
+ * pool (same as hs_context_create).  Errors as hs_context_create;
+ * HS_EINVAL when exactly one of alloc / free is NULL. */
+typedef struct hs_allocator {
+    void *(*alloc)(size_t bytes, void *stream, void *user);
+    void (*free)(void *ptr, size_t bytes, void *stream, void *user);
+    void *user;
+} hs_allocator;
+hs_status hs_context_create_ex(const hs_params *p, int device, const hs_allocator *alloc, hs_ctx **out);
 void hs_context_destroy(hs_ctx *c);
 
 /* ------------------------------------------------------------ keys (C5-C7) */

@@ -14,7 +14,7 @@ import numpy as np
 from . import _lib as L
 from ._lib import HsError, check
 
-__all__ = ["Params", "Context", "Keys", "Ciphertext", "HsError", "softmax_one_ctxt", "softmax_many_ctxt"]
+__all__ = ["Params", "Context", "Allocator", "torch_allocator", "Keys", "Ciphertext", "HsError", "softmax_one_ctxt", "softmax_many_ctxt"]
 
 
 def _stream(stream):
@@ -98,11 +98,72 @@ class Params:
         return out.reshape(Lx, n)
 
 
+class Allocator:
+    """hs_allocator (include/hesoftmax.h) from two Python callables:
+    alloc(nbytes, stream) -> device pointer (int; 0 = failure) and
+    free(ptr, nbytes, stream).  Keeps live-allocation counters.  The ctypes
+    callbacks live as long as this object; a Context holds a reference."""
+
+    def __init__(self, alloc, free):
+        self.n_alloc = self.n_free = self.live_bytes = 0
+
+        def _a(nbytes, stream, user):
+            try:
+                p = int(alloc(int(nbytes), int(stream or 0)))
+            except Exception:
+                return None
+            if p:
+                self.n_alloc += 1
+                self.live_bytes += int(nbytes)
+            return p or None
+
+        def _f(ptr, nbytes, stream, user):
+            try:
+                free(int(ptr), int(nbytes), int(stream or 0))
+                self.n_free += 1
+                self.live_bytes -= int(nbytes)
+            except Exception:
+                pass
+
+        self._cb = (L.ALLOC_FN(_a), L.FREE_FN(_f))
+        self.struct = L.Allocator(self._cb[0], self._cb[1], None)
+
+
+_TORCH_ALLOCATOR = None
+
+
+def torch_allocator():
+    """The library's device memory served by torch's caching allocator
+    (SURVEY.md 8(b)): one process-wide Allocator, never freed."""
+    global _TORCH_ALLOCATOR
+    if _TORCH_ALLOCATOR is None:
+        import torch
+
+        def alloc(nbytes, stream):
+            return torch.cuda.caching_allocator_alloc(nbytes, torch.cuda.current_device(), stream)
+
+        def free(ptr, nbytes, stream):
+            torch.cuda.caching_allocator_delete(ptr)
+
+        _TORCH_ALLOCATOR = Allocator(alloc, free)
+    return _TORCH_ALLOCATOR
+
+
 class Context:
-    def __init__(self, params: Params, device: int = 0):
+    def __init__(self, params: Params, device: int = 0, allocator=None):
+        """allocator: None (the device's stream-ordered pool), "torch"
+        (torch_allocator()) or an Allocator -- hs_context_create_ex."""
         self.params = params
+        if isinstance(allocator, str):
+            if allocator != "torch":
+                raise ValueError(f"unknown allocator {allocator!r}")
+            allocator = torch_allocator()
+        self.allocator = allocator
         out = C.c_void_p()
-        check(L.hs_context_create(params.ptr, device, C.byref(out)))
+        if allocator is None:
+            check(L.hs_context_create(params.ptr, device, C.byref(out)))
+        else:
+            check(L.hs_context_create_ex(params.ptr, device, C.byref(allocator.struct), C.byref(out)))
         self.ptr = out
 
     def __del__(self):

@@ -85,6 +85,16 @@ hs_params_psi = _sig("hs_params_psi", C.c_uint64, [vp, C.c_int])
 hs_params_scale = _sig("hs_params_scale", C.c_double, [vp, C.c_int])
 hs_galois_of_rot = _sig("hs_galois_of_rot", C.c_int, [vp, C.c_int])
 hs_context_create = _sig("hs_context_create", C.c_int, [vp, C.c_int, C.POINTER(vp)])
+ALLOC_FN = C.CFUNCTYPE(vp, C.c_size_t, vp, vp)
+FREE_FN = C.CFUNCTYPE(None, vp, C.c_size_t, vp, vp)
+
+
+class Allocator(C.Structure):
+    """hs_allocator"""
+    _fields_ = [("alloc", ALLOC_FN), ("free", FREE_FN), ("user", vp)]
+
+
+hs_context_create_ex = _sig("hs_context_create_ex", C.c_int, [vp, C.c_int, C.POINTER(Allocator), C.POINTER(vp)])
 hs_context_destroy = _sig("hs_context_destroy", None, [vp])
 hs_ckks_keygen = _sig("hs_ckks_keygen", C.c_int,
                       [vp, C.c_uint64, C.c_int, i32p, C.c_size_t, C.c_int, vp, C.POINTER(vp)])

@@ -142,7 +142,7 @@ struct LinTrans {
     u64 *pts = nullptr;  // [terms][level+1][N] NTT-domain plaintexts
     LinTrans() {}
     LinTrans(const LinTrans &) = delete;
-    ~LinTrans() { if (pts) cudaFree(pts); }
+    ~LinTrans() { dev_free_persist(pts); }
 };
 
 // C17: plaintexts in the extended basis Q_level u P ([terms][ntg][N], NTT
@@ -176,7 +176,7 @@ void build_lintrans(hs_ctx *c, const DiagMat &m, int level, int unit, int r, Lin
         }
         hs_encode_impl_q(P, re.data(), im.data(), sc, level, host.data() + (size_t)k * ntg * N, true);
     }
-    HS_CUDA(cudaMalloc(&T.pts, host.size() * 8));
+    T.pts = (decltype(T.pts))dev_alloc_persist(host.size() * 8);
     HS_CUDA(cudaMemcpy(T.pts, host.data(), host.size() * 8, cudaMemcpyHostToDevice));
     PrimeMap pm;
     pm.n = ntg;

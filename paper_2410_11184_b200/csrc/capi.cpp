@@ -44,6 +44,7 @@ static void activate(hs_ctx *c)
         upload_prime_constants(c->P);
         g_active[c->device] = c->P;
     }
+    alloc_hook_set(c->alloc);
 }
 
 void check_scales(const hs_ct *a, const hs_ct *b)
@@ -92,10 +93,12 @@ uint64_t hs_params_psi(const hs_params *p, int i) { return p->psi.at(i); }
 double hs_params_scale(const hs_params *p, int level) { return p->scale.at(level); }
 int hs_galois_of_rot(const hs_params *p, int r) { return hs_galois_elt(p, r); }
 
-hs_status hs_context_create(const hs_params *p, int device, hs_ctx **out)
+hs_status hs_context_create_ex(const hs_params *p, int device, const hs_allocator *alloc, hs_ctx **out)
 {
     HS_TRY
     if (!p || !out) throw HsError(HS_EINVAL, "NULL argument");
+    if (alloc && (!alloc->alloc) != (!alloc->free))
+        throw HsError(HS_EINVAL, "hs_allocator: alloc and free must both be set");
     int ndev = 0;
     HS_CUDA(cudaGetDeviceCount(&ndev));
     if (device < 0 || device >= ndev) throw HsError(HS_EINVAL, "no such CUDA device");
@@ -103,6 +106,16 @@ hs_status hs_context_create(const hs_params *p, int device, hs_ctx **out)
     std::unique_ptr<hs_ctx> c(new hs_ctx);
     c->P = p;
     c->device = device;
+    if (alloc && alloc->alloc) {
+        c->alloc.a = *alloc;
+        c->alloc.on = true;
+    }
+    // the twiddle tables below already go through the hook; the thread's
+    // current hook is cleared again on every exit (activate() sets it per call)
+    struct HookOff {
+        ~HookOff() { alloc_hook_set(AllocHook{}); }
+    } hook_off;
+    alloc_hook_set(c->alloc);
     const int np = p->n_q + p->n_p;
     const size_t N = p->n;
     std::vector<u64> h((size_t)np * 4 * N + 2 * np);
@@ -118,7 +131,7 @@ hs_status hs_context_create(const hs_params *p, int device, hs_ctx **out)
         h[(size_t)np * 4 * N + 2 * i] = p->n_inv[i];
         h[(size_t)np * 4 * N + 2 * i + 1] = p->n_inv_sh[i];
     }
-    HS_CUDA(cudaMalloc(&c->T.tw, h.size() * 8));
+    c->T.tw = (decltype(c->T.tw))dev_alloc_persist(h.size() * 8);
     HS_CUDA(cudaMemcpy(c->T.tw, h.data(), h.size() * 8, cudaMemcpyHostToDevice));
     // keep freed stream-ordered memory in the pool (no release back to the OS)
     cudaMemPool_t pool;
@@ -131,7 +144,16 @@ hs_status hs_context_create(const hs_params *p, int device, hs_ctx **out)
     HS_CATCH
 }
 
-void hs_context_destroy(hs_ctx *c) { delete c; }
+hs_status hs_context_create(const hs_params *p, int device, hs_ctx **out)
+{
+    return hs_context_create_ex(p, device, nullptr, out);
+}
+
+void hs_context_destroy(hs_ctx *c)
+{
+    delete c;
+    alloc_hook_set(AllocHook{});
+}
 
 hs_status hs_ckks_keygen(hs_ctx *c, uint64_t seed, int h, const int32_t *galois, size_t n_galois, int relin,
                          void *stream, hs_keys **out)
@@ -801,6 +823,11 @@ hs_status hs_softmax_plan_create(hs_ctx *c, const hs_keys *k, const hs_softmax_d
     cudaStream_t cs;
     HS_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
     c->kprof_on = prof;
+    // scratch inside the graph is graph-owned: bypass the allocator hook
+    alloc_capturing(true);
+    struct CapOff {
+        ~CapOff() { alloc_capturing(false); }
+    } cap_off;
     HS_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
     try {
         s = softmax_run(c, k, d, in, m_local, cs, tmp.data());

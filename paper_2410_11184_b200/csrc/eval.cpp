@@ -21,10 +21,56 @@ enum { TAG_SK = 1, TAG_PK_A = 2, TAG_PK_E = 3, TAG_KSK_A = 4, TAG_KSK_E = 5,
 static const int ETA_ERR = 21, ETA_V = 1;
 
 // ------------------------------------------------------------------ memory
+// Default pool: the device's stream-ordered pool (cudaMallocAsync) for
+// temporaries and ciphertexts, cudaMalloc for long-lived tables.  With an
+// allocator hook (hs_context_create_ex) both go through the hook, except
+// inside a CUDA-graph capture (graph-owned memory nodes).  Each hook
+// allocation is recorded with a copy of its hook so that the free finds it.
+namespace {
+struct HookRec {
+    hs_allocator a;
+    size_t bytes;
+};
+std::mutex g_hook_mu;
+std::map<void *, HookRec> g_hook_ptrs;
+thread_local AllocHook tl_hook;
+thread_local int tl_capturing = 0;
+
+bool capturing(cudaStream_t st)
+{
+    if (tl_capturing) return true;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    return cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone;
+}
+
+void *hook_alloc(size_t bytes, cudaStream_t st)
+{
+    void *p = tl_hook.a.alloc(bytes, (void *)st, tl_hook.a.user);
+    if (!p) throw HsError(HS_ENOMEM, "allocator hook returned NULL");
+    std::lock_guard<std::mutex> g(g_hook_mu);
+    g_hook_ptrs[p] = HookRec{tl_hook.a, bytes};
+    return p;
+}
+
+bool hook_take(void *p, HookRec &r)
+{
+    std::lock_guard<std::mutex> g(g_hook_mu);
+    auto it = g_hook_ptrs.find(p);
+    if (it == g_hook_ptrs.end()) return false;
+    r = it->second;
+    g_hook_ptrs.erase(it);
+    return true;
+}
+}  // namespace
+
+void alloc_hook_set(const AllocHook &h) { tl_hook = h; }
+void alloc_capturing(bool on) { tl_capturing += on ? 1 : -1; }
+
 u64 *dev_alloc(size_t words, cudaStream_t st)
 {
     void *p = nullptr;
     if (words == 0) words = 1;
+    if (tl_hook.on && !capturing(st)) return (u64 *)hook_alloc(words * sizeof(u64), st);
     cudaError_t e = cudaMallocAsync(&p, words * sizeof(u64), st);
     if (e != cudaSuccess) throw HsError(e == cudaErrorMemoryAllocation ? HS_ENOMEM : HS_ECUDA,
                                         std::string("cudaMallocAsync: ") + cudaGetErrorString(e));
@@ -33,25 +79,49 @@ u64 *dev_alloc(size_t words, cudaStream_t st)
 
 void dev_free(void *p, cudaStream_t st)
 {
-    if (p) cudaFreeAsync(p, st);
+    if (!p) return;
+    HookRec r;
+    if (hook_take(p, r))
+        r.a.free(p, r.bytes, (void *)st, r.a.user);
+    else
+        cudaFreeAsync(p, st);
+}
+
+void *dev_alloc_persist(size_t bytes)
+{
+    if (bytes == 0) bytes = 8;
+    if (tl_hook.on && !tl_capturing) return hook_alloc(bytes, nullptr);
+    void *p = nullptr;
+    HS_CUDA(cudaMalloc(&p, bytes));
+    return p;
+}
+
+void dev_free_persist(void *p)
+{
+    if (!p) return;
+    HookRec r;
+    if (hook_take(p, r))
+        r.a.free(p, r.bytes, nullptr, r.a.user);
+    else
+        cudaFree(p);
 }
 
 hs_ctx::~hs_ctx()
 {
     cudaDeviceSynchronize();
-    for (auto &kv : bconv) cudaFree(kv.second.dev);
-    for (auto &kv : galois_perm) cudaFree(kv.second);
-    for (auto &kv : pt_cache) cudaFree(kv.second);
+    for (auto &kv : bconv) dev_free_persist(kv.second.dev);
+    for (auto &kv : galois_perm) dev_free_persist(kv.second);
+    for (auto &kv : pt_cache) dev_free_persist(kv.second);
     for (auto e : kprof_ev) cudaEventDestroy(e);
-    cudaFree(T.tw);
+    dev_free_persist(T.tw);
 }
 
 hs_keys::~hs_keys()
 {
     cudaDeviceSynchronize();
-    cudaFree(s_ntt);
-    cudaFree(pk);
-    for (auto &k : swk) cudaFree(k.k);
+    dev_free_persist(s_ntt);
+    dev_free_persist(pk);
+    for (auto &k : swk) dev_free_persist(k.k);
 }
 
 hs_ct::~hs_ct()
@@ -164,7 +234,7 @@ const BconvTab &bconv_modup(hs_ctx *c, int level, int digit)
             h[ci + 1] = hs_shoup_const(v, p);
         }
     }
-    HS_CUDA(cudaMalloc(&t.dev, h.size() * 8));
+    t.dev = (decltype(t.dev))dev_alloc_persist(h.size() * 8);
     HS_CUDA(cudaMemcpy(t.dev, h.data(), h.size() * 8, cudaMemcpyHostToDevice));
     return c->bconv[key] = t;
 }
@@ -200,7 +270,7 @@ const BconvTab &bconv_moddown(hs_ctx *c, int level)
         }
     }
     for (int d = 0; d < t.n_dst; d++) h[2 * t.n_src + 2 * (size_t)t.n_src * t.n_dst + d] = P->p_mod_q[t.dst[d]];
-    HS_CUDA(cudaMalloc(&t.dev, h.size() * 8));
+    t.dev = (decltype(t.dev))dev_alloc_persist(h.size() * 8);
     HS_CUDA(cudaMemcpy(t.dev, h.data(), h.size() * 8, cudaMemcpyHostToDevice));
     return c->bconv[key] = t;
 }
@@ -241,7 +311,7 @@ const BconvTab &bconv_moddown_rescale(hs_ctx *c, int level)
         u64 q = P->prime[t.dst[d]];
         h[2 * t.n_src + 2 * (size_t)t.n_src * t.n_dst + d] = hs_mulmod(P->p_mod_q[t.dst[d]], P->prime[level] % q, q);
     }
-    HS_CUDA(cudaMalloc(&t.dev, h.size() * 8));
+    t.dev = (decltype(t.dev))dev_alloc_persist(h.size() * 8);
     HS_CUDA(cudaMemcpy(t.dev, h.data(), h.size() * 8, cudaMemcpyHostToDevice));
     return c->bconv[key] = t;
 }
@@ -266,7 +336,7 @@ const unsigned *galois_table(hs_ctx *c, int k)
         h[i] = brv((unsigned)(((e * (u64)k) % two_n - 1) / 2));
     }
     unsigned *d;
-    HS_CUDA(cudaMalloc(&d, N * sizeof(unsigned)));
+    d = (decltype(d))dev_alloc_persist(N * sizeof(unsigned));
     HS_CUDA(cudaMemcpy(d, h.data(), N * sizeof(unsigned), cudaMemcpyHostToDevice));
     return c->galois_perm[k] = d;
 }
@@ -713,7 +783,7 @@ CtP ev_mult_pt(const hs_ct *a, const double *re, const double *im, int target, c
     if (!m) {
         std::vector<u64> pt((size_t)nl * N);
         hs_encode_impl(P, re, im, landing_scale(P, a->level, target), target + 1, pt.data());
-        HS_CUDA(cudaMalloc(&m, pt.size() * 8));
+        m = (decltype(m))dev_alloc_persist(pt.size() * 8);
         HS_CUDA(cudaMemcpy(m, pt.data(), pt.size() * 8, cudaMemcpyHostToDevice));
         k_ntt(c, m, nl, pmap_range(0, nl), false, st);
         std::lock_guard<std::mutex> g(c->mu);
@@ -935,7 +1005,7 @@ hs_keys *keys_generate(hs_ctx *c, u64 seed, int h, const int32_t *galois, size_t
     K->ctx = c;
     if (h < 1 || h > P->n) throw HsError(HS_EINVAL, "secret Hamming weight out of range");
     sample_secret(P, seed, h, K->s_coeff);
-    HS_CUDA(cudaMalloc(&K->s_ntt, (size_t)nt * N * 8));
+    K->s_ntt = (decltype(K->s_ntt))dev_alloc_persist((size_t)nt * N * 8);
     {
         DBuf sc(N, st);
         HS_CUDA(cudaMemcpyAsync(sc.p, K->s_coeff.data(), N * 8, cudaMemcpyHostToDevice, st));
@@ -944,7 +1014,7 @@ hs_keys *keys_generate(hs_ctx *c, u64 seed, int h, const int32_t *galois, size_t
         HS_CUDA(cudaStreamSynchronize(st));
     }
     // pk = (-a s + e, a) over Q_L
-    HS_CUDA(cudaMalloc(&K->pk, (size_t)2 * nq * N * 8));
+    K->pk = (decltype(K->pk))dev_alloc_persist((size_t)2 * nq * N * 8);
     {
         u64 *b = K->pk, *a = K->pk + (size_t)nq * N;
         k_uniform(c, a, nq, pmap_range(0, nq), seed, TAG_PK_A, 0, 0, st);
@@ -966,7 +1036,7 @@ hs_keys *keys_generate(hs_ctx *c, u64 seed, int h, const int32_t *galois, size_t
         // generated component-planar ([dnum][2][nt][N]) in a scratch buffer,
         // stored interleaved ([dnum][nt][N][2]: one 16-byte load per word pair)
         DBuf planar((size_t)P->dnum * 2 * nt * N, st);
-        HS_CUDA(cudaMalloc(&key.k, (size_t)P->dnum * 2 * nt * N * 8));
+        key.k = (decltype(key.k))dev_alloc_persist((size_t)P->dnum * 2 * nt * N * 8);
         for (int j = 0; j < P->dnum; j++) {
             u64 sub = (u64)id * 256 + (u64)j;
             u64 *k0 = planar.p + (size_t)(2 * j) * nt * N, *k1 = planar.p + (size_t)(2 * j + 1) * nt * N;

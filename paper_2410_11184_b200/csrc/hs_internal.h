@@ -88,9 +88,18 @@ struct BconvTab {               // ModUp digit (level, digit) or ModDown (level)
     u64 *dev = nullptr;         // [n_src](inv, inv_sh) then [n_src][n_dst](c, c_sh)
 };
 
+// Allocator hook of hs_context_create_ex.  activate() makes the context's
+// hook current for the calling thread; every allocation records which hook
+// (if any) served it, so a free always goes back to its own allocator.
+struct AllocHook {
+    hs_allocator a{};
+    bool on = false;
+};
+
 struct hs_ctx {
     const hs_params *P = nullptr;
     int device = 0;
+    AllocHook alloc;                         // hs_context_create_ex
     DevTables T;
     std::map<long, BconvTab> bconv;          // key: (level << 8 | digit), digit 255 = ModDown
     std::map<int, unsigned *> galois_perm;   // device permutation tables
@@ -155,8 +164,12 @@ struct hs_ct {
 };
 
 // ------------------------------------------------------------------ memory
-u64 *dev_alloc(size_t words, cudaStream_t st);
+void alloc_hook_set(const AllocHook &h);     // thread-local current hook
+void alloc_capturing(bool on);               // inside a CUDA-graph capture: bypass the hook
+u64 *dev_alloc(size_t words, cudaStream_t st);   // stream-ordered
 void dev_free(void *p, cudaStream_t st);
+void *dev_alloc_persist(size_t bytes);           // long-lived (tables, keys, caches)
+void dev_free_persist(void *p);
 struct DBuf {                   // stream-ordered scratch buffer
     u64 *p = nullptr;
     cudaStream_t st = nullptr;

@@ -259,7 +259,7 @@ hs_keys *keys_upload(hs_ctx *c, const hs_public_key *pk, const hs_eval_keys *evk
     std::unique_ptr<hs_keys> K(new hs_keys);
     K->ctx = c;
     if (pk) {
-        HS_CUDA(cudaMalloc(&K->pk, pk->w.size() * 8));
+        K->pk = (decltype(K->pk))dev_alloc_persist(pk->w.size() * 8);
         HS_CUDA(cudaMemcpyAsync(K->pk, pk->w.data(), pk->w.size() * 8, cudaMemcpyHostToDevice, st));
     }
     const size_t words = (size_t)P->dnum * 2 * nt * N;
@@ -267,7 +267,7 @@ hs_keys *keys_upload(hs_ctx *c, const hs_public_key *pk, const hs_eval_keys *evk
     for (size_t i = 0; i < evk->k.size(); i++) {
         SwKey key;
         key.galois = evk->galois[i];
-        HS_CUDA(cudaMalloc(&key.k, words * 8));
+        key.k = (decltype(key.k))dev_alloc_persist(words * 8);
         HS_CUDA(cudaMemcpyAsync(planar.p, evk->k[i].data(), words * 8, cudaMemcpyHostToDevice, st));
         k_interleave2(c, planar.p, key.k, P->dnum, nt * N, st);
         K->swk.push_back(key);

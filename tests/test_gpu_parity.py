@@ -714,3 +714,76 @@ def test_aux_split_emulation_parity(toyb, tables, G):
     r = np.exp(x - x.max(1, keepdims=True))
     r /= r.sum(1, keepdims=True)
     assert np.abs(y - r).max() < 2.0 ** -15
+
+
+def test_allocator_hook(tables):
+    """hs_context_create_ex (include/hesoftmax.h): with an
+    allocator hook bound to torch's caching allocator, the library's device
+    memory -- twiddle tables, keys, ciphertexts, key-switch scratch, cached
+    plaintexts, bootstrap transforms, plan inputs / outputs -- comes from
+    torch's pool; the words equal the default-pool context's (themselves
+    oracle-pinned above) for eager Softmax, a CUDA-graph plan and a bootstrap,
+    and every hook allocation is returned by the time the objects are gone."""
+    import gc
+    hs = _hs()
+    dev = torch.cuda.current_device()
+    A = hs.Allocator(lambda nb, st: torch.cuda.caching_allocator_alloc(nb, dev, st),
+                     lambda p, nb, st: torch.cuda.caching_allocator_delete(p))
+
+    def softmax_words(alloc):
+        tab = tables["toy_n16_M4_k2_B"]
+        n, m, k = 16, 2, tab["config"]["k"]
+        pre = W.preset("TOY12D")
+        P = hs.Params.from_preset(pre)
+        ctx = hs.Context(P, 0, allocator=alloc)
+        gal = O.softmax_rotation_galois(O.Params.from_preset(pre), n, m)
+        K = hs.Keys(ctx, 99, pre["h"], galois=gal)
+        x = W.softmax_inputs((P.n // 2) * m // n, n, 4.0, seed=3)
+        slots = P.pack(x, m)
+        top = len(pre["q_bits"]) - 1
+        sc = hs.softmax_input_scale(P, tab["exp"], top)
+        cts = [hs.encrypt(K, P.encode(slots[c], scale=sc, level=top), top, 5, c) for c in range(m)]
+        eager = [c.words() for c in hs.softmax_many_ctxt(K, cts, n, m, k, "B", tab["exp"], tab["inv"])]
+        plan = hs.Plan(K, cts, n, m, k, "B", tab["exp"], tab["inv"])
+        plan.run()
+        planned = [c.words() for c in plan.outputs]
+        return eager, planned
+
+    def bts_words(alloc):
+        pre = W.preset("TOY12B")
+        P = hs.Params.from_preset(pre)
+        ctx = hs.Context(P, 0, allocator=alloc)
+        gal = sorted({P.galois_of_rot(r) for r in hs.bts_rotations(P, pre["bts"])} | {2 * P.n - 1})
+        K = hs.Keys(ctx, 7, pre["h"], galois=gal)
+        B = hs.Bts(ctx, pre["bts"], W.bts_tables()[pre["bts"]["table"]])
+        z = np.random.default_rng(0).uniform(-1, 1, P.n // 2)
+        ct = hs.encrypt(K, P.encode(z, scale=P.scale(2), level=2), 2, 1, 0)
+        return hs.bootstrap(K, B, ct, 1.0).words()
+
+    base = softmax_words(None)
+    torch.cuda.synchronize()
+    m0 = torch.cuda.memory_allocated(dev)
+    hooked = softmax_words(A)
+    assert A.n_alloc > 0
+    for a, b in zip(base[0] + base[1], hooked[0] + hooked[1]):
+        assert (a == b).all()
+    assert (bts_words(None) == bts_words(A)).all()
+    gc.collect()
+    torch.cuda.synchronize()
+    assert A.n_alloc == A.n_free and A.live_bytes == 0, (A.n_alloc, A.n_free, A.live_bytes)
+    assert torch.cuda.memory_allocated(dev) == m0
+
+
+def test_allocator_hook_failure_is_enomem(tables):
+    """A hook that returns NULL makes the call fail with HS_ENOMEM (no crash,
+    no fallback to the default pool); alloc without free is HS_EINVAL."""
+    hs = _hs()
+    P = hs.Params.from_preset(W.preset("TOY12"))
+    with pytest.raises(hs.HsError) as e:
+        hs.Context(P, 0, allocator=hs.Allocator(lambda nb, st: 0, lambda p, nb, st: None))
+    assert e.value.code == 7
+    import ctypes as C
+    from paper_2410_11184_b200 import _lib as L
+    half = L.Allocator(L.ALLOC_FN(lambda nb, st, u: None), L.FREE_FN(), None)
+    out = C.c_void_p()
+    assert L.hs_context_create_ex(P.ptr, 0, C.byref(half), C.byref(out)) == 1

@@ -125,6 +125,18 @@ PRESETS["P16L12"] = dict(PRESETS["P16"], q_bits=[60] + [42] * 12 + [48] * 3 + [5
                                                    (13, 48), (12, 42)]),
                          bts=dict(PRESETS["P16"]["bts"], out_level=12))
 
+# Chains within the HE standard's 128-bit bound for N = 2^16 (log QP <= 1772,
+# DESIGN.md section 4): smaller bootstrapping primes and 12 / 11 user levels.
+# Measurement presets (bench.py HS_PRESET=...), not the headline chain.
+PRESETS["P16S12"] = dict(PRESETS["P16"], q_bits=[60] + [42] * 12 + [46] * 3 + [49] * 11 + [57] * 4, p_bits=[60] * 5,
+                         log2_anchor=_anchors(31, [(30, 57), (29, 60), (28, 59), (27, 57), (26, 49), (14, 46),
+                                                   (13, 46), (12, 42)]),
+                         bts=dict(PRESETS["P16"]["bts"], out_level=12))
+PRESETS["P16S11"] = dict(PRESETS["P16"], q_bits=[60] + [42] * 11 + [46] * 3 + [53] * 11 + [57] * 4, p_bits=[60] * 5,
+                         log2_anchor=_anchors(30, [(29, 57), (28, 60), (27, 59), (26, 57), (25, 53), (13, 46),
+                                                   (12, 46), (11, 42)]),
+                         bts=dict(PRESETS["P16"]["bts"], out_level=11))
+
 # N = 2^12 ring with P16's exact modulus chain (bootstrapping included):
 # parity / precision tests of configs 2-5 at a size the oracle finishes quickly.
 PRESETS["TOY12B"] = dict(PRESETS["P16"], log_n=12)

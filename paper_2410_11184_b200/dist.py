@@ -68,3 +68,32 @@ def host_exchange(group=None):
             return 1
 
     return EXCHANGE_FN(fn)
+
+
+def gloo_device_exchange(group=None):
+    """The device-buffer contract over a gloo (host) process group: the
+    partial is staged through host memory, all-gathered by gloo and copied
+    back.  For hosts without NCCL, and for the multi-process GPU test that
+    runs two ranks on one GPU -- every wait is host-side (no kernel waits on
+    another rank's kernel)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+
+    def fn(user, partial, gathered, words, stream):
+        try:
+            ext = torch.cuda.ExternalStream(stream) if stream else torch.cuda.current_stream()
+            src = torch.as_tensor(_CudaBuf(partial, words), device="cuda")
+            dst = torch.as_tensor(_CudaBuf(gathered, words * world), device="cuda")
+            with torch.cuda.stream(ext):
+                host = src.cpu()  # synchronises the library's stream
+                parts = [torch.empty_like(host) for _ in range(world)]
+                dist.all_gather(parts, host, group=group)
+                dst.copy_(torch.cat(parts).to("cuda"))
+            ext.synchronize()
+            return 0
+        except Exception as e:  # pragma: no cover - surfaced as HS_ENCCL
+            print("gloo_device_exchange failed:", e)
+            return 1
+
+    return EXCHANGE_FN(fn)

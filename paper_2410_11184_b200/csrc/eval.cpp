@@ -109,7 +109,10 @@ void dev_free_persist(void *p)
 hs_ctx::~hs_ctx()
 {
     cudaDeviceSynchronize();
-    for (auto &kv : bconv) dev_free_persist(kv.second.dev);
+    for (auto &kv : bconv) {
+        dev_free_persist(kv.second.dev);
+        dev_free_persist(kv.second.mma);
+    }
     for (auto &kv : galois_perm) dev_free_persist(kv.second);
     for (auto &kv : pt_cache) dev_free_persist(kv.second);
     for (auto e : kprof_ev) cudaEventDestroy(e);
@@ -203,6 +206,41 @@ CtP ct_slice(const hs_ct *a, int b, cudaStream_t st)
 // sum y_a c_a mod q directly.
 static u64 mont(u64 v, u64 q) { return (u64)(((u128)v << 64) % q); }
 
+// B-operand fragments of the tensor-core BConv (kernels.cu bconv_mma_kernel).
+// The conversion sum_a y_a c_ab (c_ab in Montgomery form, mod p_b) is split
+// into bytes: y_a = sum_u y_au 2^8u and c'_aub = 2^8u c_ab mod p_b =
+// sum_v c'_aubv 2^8v, so sum_a y_a c_ab == sum_v 2^8v D_bv (mod p_b) with
+// D_bv = sum_(a,u) y_au c'_aubv -- an exact u8 x u8 -> s32 product with
+// K = (a, u) (8 sources x 8 bytes) and N = (b, v).  Fragment of lane
+// (g = lane / 4, t = lane % 4), k-step s, register r: the 4 bytes
+// k = 16 r + 4 t + i (i = 0..3) of column v = g, i.e. source a = 4 s + 2 r +
+// t / 2, bytes u = 4 (t % 2) + i.
+void bconv_build_mma(BconvTab &t, const std::vector<u64> &h, const hs_params *P)
+{
+    if (t.n_src > 8) return;
+    std::vector<uint32_t> f((size_t)t.n_dst * 2 * 32 * 2, 0);
+    for (int b = 0; b < t.n_dst; b++) {
+        const u64 p = P->prime[t.dst[b]];
+        for (int s = 0; s < 2; s++)
+            for (int lane = 0; lane < 32; lane++)
+                for (int r = 0; r < 2; r++) {
+                    const int g = lane >> 2, tg = lane & 3, a = 4 * s + 2 * r + (tg >> 1);
+                    uint32_t reg = 0;
+                    if (a < t.n_src) {
+                        const u64 cm = h[2 * t.n_src + 2 * ((size_t)a * t.n_dst + b)];
+                        for (int i = 0; i < 4; i++) {
+                            const int u = 4 * (tg & 1) + i;
+                            const u64 cu = (u64)(((u128)cm << (8 * u)) % p);
+                            reg |= (uint32_t)((cu >> (8 * g)) & 0xff) << (8 * i);
+                        }
+                    }
+                    f[(((size_t)b * 2 + s) * 32 + lane) * 2 + r] = reg;
+                }
+    }
+    t.mma = (uint32_t *)dev_alloc_persist(f.size() * 4);
+    HS_CUDA(cudaMemcpy(t.mma, f.data(), f.size() * 4, cudaMemcpyHostToDevice));
+}
+
 const BconvTab &bconv_modup(hs_ctx *c, int level, int digit)
 {
     std::lock_guard<std::mutex> g(c->mu);
@@ -236,6 +274,7 @@ const BconvTab &bconv_modup(hs_ctx *c, int level, int digit)
     }
     t.dev = (decltype(t.dev))dev_alloc_persist(h.size() * 8);
     HS_CUDA(cudaMemcpy(t.dev, h.data(), h.size() * 8, cudaMemcpyHostToDevice));
+    bconv_build_mma(t, h, P);
     return c->bconv[key] = t;
 }
 
@@ -272,6 +311,7 @@ const BconvTab &bconv_moddown(hs_ctx *c, int level)
     for (int d = 0; d < t.n_dst; d++) h[2 * t.n_src + 2 * (size_t)t.n_src * t.n_dst + d] = P->p_mod_q[t.dst[d]];
     t.dev = (decltype(t.dev))dev_alloc_persist(h.size() * 8);
     HS_CUDA(cudaMemcpy(t.dev, h.data(), h.size() * 8, cudaMemcpyHostToDevice));
+    bconv_build_mma(t, h, P);
     return c->bconv[key] = t;
 }
 
@@ -313,6 +353,7 @@ const BconvTab &bconv_moddown_rescale(hs_ctx *c, int level)
     }
     t.dev = (decltype(t.dev))dev_alloc_persist(h.size() * 8);
     HS_CUDA(cudaMemcpy(t.dev, h.data(), h.size() * 8, cudaMemcpyHostToDevice));
+    bconv_build_mma(t, h, P);
     return c->bconv[key] = t;
 }
 

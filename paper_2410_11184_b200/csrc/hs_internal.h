@@ -86,7 +86,11 @@ struct BconvTab {               // ModUp digit (level, digit) or ModDown (level)
     bool centred = false;       // ModDown: centred source terms (unbiased, C7)
     std::vector<int> src, dst;  // global prime indices
     u64 *dev = nullptr;         // [n_src](inv, inv_sh) then [n_src][n_dst](c, c_sh)
+    // tensor-core form (n_src <= 8, kernels.cu bconv_mma_kernel): the B-operand
+    // fragments of mma.m16n8k32 u8, [n_dst][2 k-steps][32 lanes] x 2 u32
+    uint32_t *mma = nullptr;
 };
+void bconv_build_mma(BconvTab &t, const std::vector<u64> &h, const hs_params *P);
 
 // Allocator hook of hs_context_create_ex.  activate() makes the context's
 // hook current for the calling thread; every allocation records which hook

@@ -1065,7 +1065,7 @@ struct BconvArg {
 // source loops unroll, the NS constants of a target load together)
 template <int NS>
 __global__ void __launch_bounds__(256) bconv_kernel(const u64 *__restrict__ x, size_t xs, u64 *__restrict__ o,
-                                                    size_t os, BconvArg A, const u64 *__restrict__ tab, int N,
+                                                    size_t os, const __grid_constant__ BconvArg A, const u64 *__restrict__ tab, int N,
                                                     size_t bxs, size_t bos)
 {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1107,6 +1107,118 @@ __global__ void __launch_bounds__(256) bconv_kernel(const u64 *__restrict__ x, s
             for (int kk = 0; kk < neg; kk++) s = d_sub(s, pmb, k.q);
         }
         o[(size_t)b * os + t] = s;
+    }
+}
+
+// Tensor-core BConv (same words as bconv_kernel).  The byte-split identity
+// of eval.cpp bconv_build_mma turns the conversion of a 128-coefficient tile
+// into u8 x u8 -> s32 products on mma.sync m16n8k32: M = 16 coefficients per
+// warp, K = 32 bytes (4 sources x 8 bytes) per k-step, N = 8 bytes v of one
+// target.  D_bv < 64 * 255^2 < 2^22, so sum_v 2^8v D_bv < 2^79 < p 2^64 is
+// reduced by one REDC (constants in Montgomery form).  The four lanes holding
+// the v's of one output stage their partials in shared memory, so that each
+// lane reduces one (coefficient, target) output.  The integer-pipe
+// work per output falls from n_src 128-bit multiply-adds to one REDC: the
+// products move to the tensor cores.
+#define BCM_TILE 128
+#define BCM_LD (BCM_TILE + 8)  // padded source row (u64): conflict-free fragment loads
+__device__ __forceinline__ void mma_u8(int d[4], const uint32_t a[4], uint2 b)
+{
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};\n"
+        : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b.x), "r"(b.y));
+}
+
+template <bool CENTRED>
+__global__ void __launch_bounds__(256) bconv_mma_kernel(const u64 *__restrict__ x, size_t xs, u64 *__restrict__ o,
+                                                        size_t os, const __grid_constant__ BconvArg A, const u64 *__restrict__ tab,
+                                                        const uint2 *__restrict__ frag, int N, size_t bxs, size_t bos)
+{
+    __shared__ u64 sy[8 * BCM_LD];
+    __shared__ int sneg[BCM_TILE];
+    __shared__ __align__(16) uint32_t spart[8 * 128];  // per warp: [32 outputs][4 partials]
+    __shared__ ulonglong2 sk[HS_MAXP];                  // per target: (q, -q^-1 mod 2^64)
+    __shared__ u64 spm[CENTRED ? HS_MAXP : 1];
+    const int n_base = blockIdx.x * BCM_TILE, tid = threadIdx.x;
+    x += blockIdx.y * bxs;
+    o += blockIdx.y * bos;
+    if (tid < A.n_dst) {
+        const PrimeK k = c_pk[A.dst[tid]];
+        sk[tid] = make_ulonglong2(k.q, k.qinv);
+        if (CENTRED) spm[tid] = __ldg(tab + 2 * A.n_src + 2 * (size_t)A.n_src * A.n_dst + tid);
+    }
+    // y_a = x_a inv_a mod q_a for the tile (sources >= n_src are zero)
+    for (int idx = tid; idx < 8 * BCM_TILE; idx += 256) {
+        const int a = idx / BCM_TILE, n = idx % BCM_TILE;
+        u64 y = 0;
+        if (a < A.n_src && n_base + n < N)
+            y = d_shoup(x[(size_t)a * xs + n_base + n], __ldg(tab + 2 * a), __ldg(tab + 2 * a + 1),
+                        c_pk[A.src[a]].q);
+        sy[a * BCM_LD + n] = y;
+    }
+    __syncthreads();
+    if (CENTRED && tid < BCM_TILE) {
+        // C7 exact centred conversion: v = round(sum_a y_a / s_a), same order as bconv_kernel
+        double f = 0.0;
+        for (int a = 0; a < A.n_src; a++)
+            f = __dadd_rn(f, __ddiv_rn(__ull2double_rn(sy[a * BCM_LD + tid]), __ull2double_rn(c_pk[A.src[a]].q)));
+        sneg[tid] = (int)floor(__dadd_rn(f, 0.5));
+    }
+    __syncthreads();
+    const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, tg = lane & 3;
+    const int r0 = warp * 16, half = tg & 1;
+    const uint32_t *sy32 = reinterpret_cast<const uint32_t *>(sy);
+    uint32_t af[2][4];
+#pragma unroll
+    for (int s = 0; s < 2; s++) {
+        const int a0 = 4 * s + (tg >> 1), a1 = a0 + 2;
+        af[s][0] = sy32[(a0 * BCM_LD + r0 + g) * 2 + half];
+        af[s][1] = sy32[(a0 * BCM_LD + r0 + g + 8) * 2 + half];
+        af[s][2] = sy32[(a1 * BCM_LD + r0 + g) * 2 + half];
+        af[s][3] = sy32[(a1 * BCM_LD + r0 + g + 8) * 2 + half];
+    }
+    const bool two = A.n_src > 4;
+    const int row = r0 + (lane & 15), n = n_base + row;  // this lane's output coefficient
+    const int neg = CENTRED ? sneg[row] : 0;
+    uint32_t *sp = spart + warp * 128;
+    u64 *op = o + (size_t)(lane >> 4) * os + n;  // output (target b + lane / 16, coefficient n)
+    const bool nok = n < N;
+    for (int b = 0; b < A.n_dst; b += 2, op += 2 * os) {
+        int d0[4] = {0, 0, 0, 0}, d1[4] = {0, 0, 0, 0};
+        mma_u8(d0, af[0], __ldg(frag + ((size_t)b * 2) * 32 + lane));
+        if (two) mma_u8(d0, af[1], __ldg(frag + ((size_t)b * 2 + 1) * 32 + lane));
+        if (b + 1 < A.n_dst) {
+            mma_u8(d1, af[0], __ldg(frag + ((size_t)(b + 1) * 2) * 32 + lane));
+            if (two) mma_u8(d1, af[1], __ldg(frag + ((size_t)(b + 1) * 2 + 1) * 32 + lane));
+        }
+        // partial of this lane's two v's (v = 2 tg, weight 2^(16 tg)) for its four
+        // (target, row) outputs; staged per warp so that lane L then reduces
+        // output (target b + L / 16, row r0 + L % 16) from one 16-byte load
+        __syncwarp();
+        sp[(g) * 4 + tg] = (uint32_t)d0[0] + ((uint32_t)d0[1] << 8);
+        sp[(8 + g) * 4 + tg] = (uint32_t)d0[2] + ((uint32_t)d0[3] << 8);
+        sp[(16 + g) * 4 + tg] = (uint32_t)d1[0] + ((uint32_t)d1[1] << 8);
+        sp[(24 + g) * 4 + tg] = (uint32_t)d1[2] + ((uint32_t)d1[3] << 8);
+        __syncwarp();
+        const uint4 w = reinterpret_cast<const uint4 *>(sp)[lane];
+        const int bb = b + (lane >> 4);
+        if (bb < A.n_dst && nok) {
+            const u64 lo0 = (u64)w.x + ((u64)w.y << 16) + ((u64)w.z << 32);
+            const u64 lo = lo0 + ((u64)w.w << 48);
+            const u64 hi = (u64)(w.w >> 16) + (lo < lo0 ? 1 : 0);
+            const ulonglong2 kq = sk[bb];
+            // REDC: (hi 2^64 + lo + m q) / 2^64, m = lo (-q^-1) mod 2^64
+            const u64 m = lo * kq.y;
+            u64 r = hi + __umul64hi(m, kq.x) + (lo != 0);
+            r = r >= kq.x ? r - kq.x : r;
+            if (CENTRED) {
+                const u64 pmb = spm[bb];
+                for (int kk = 0; kk < neg; kk++) r = r >= pmb ? r - pmb : r + kq.x - pmb;
+            }
+            *op = r;
+        }
     }
 }
 
@@ -1196,6 +1308,20 @@ void k_bconv(hs_ctx *c, const BconvTab &tab, const u64 *src, size_t src_stride, 
     for (int i = 0; i < tab.n_dst; i++) A.dst[i] = (unsigned char)tab.dst[i];
     if (tab.n_src > 9) throw HsError(HS_EINVAL, "bconv: more than 9 source primes");
     int N = c->P->n;
+    static const bool mma_on = !getenv("HS_BCONV_MMA") || atoi(getenv("HS_BCONV_MMA")) != 0;
+    // measured: the tensor-core form wins for ModUp digits of
+    // >= 4 sources; single-prime digits and the centred ModDown stay on bconv_kernel
+    if (tab.mma && mma_on && !tab.centred && tab.n_src >= 4) {
+        const dim3 g2((N + BCM_TILE - 1) / BCM_TILE, batch);
+        const uint2 *fr = reinterpret_cast<const uint2 *>(tab.mma);
+        if (tab.centred)
+            bconv_mma_kernel<true><<<g2, 256, 0, st>>>(src, src_stride, dst, dst_stride, A, tab.dev, fr, N, bss, bds);
+        else
+            bconv_mma_kernel<false><<<g2, 256, 0, st>>>(src, src_stride, dst, dst_stride, A, tab.dev, fr, N, bss, bds);
+        HS_CHECK_LAUNCH();
+        count_kernel(c);
+        return;
+    }
     const dim3 grid((N + 255) / 256, batch, (tab.n_dst + BCONV_TG - 1) / BCONV_TG);
     switch (tab.n_src) {
 #define BCONV_CASE(ns) \

@@ -180,10 +180,31 @@ def build_setup(wl_name, rank, world, device):
                 setup_s=time.time() - t0, top=top, in_level=in_level)
 
 
+# HS_BENCH_GLOO=1 (test mode, not a measurement): N > 1 ranks over a gloo
+# group, every rank on cuda:(LOCAL_RANK mod device count), the aux-sum
+# exchange staged through host memory (dist.gloo_device_exchange), eager
+# calls.  It runs the N > 1 control flow of this file on a one-GPU box, where
+# NCCL cannot put two ranks on one device; the times it prints are those of
+# ranks sharing a GPU and mean nothing.
+GLOO_TEST = os.environ.get("HS_BENCH_GLOO", "0") == "1"
+
+
+def _coll_dev():
+    return "cpu" if GLOO_TEST else "cuda"
+
+
+def _reduce(v, op):
+    import torch
+    import torch.distributed as dist_
+    t = torch.tensor([v], device=_coll_dev())
+    dist_.all_reduce(t, op=op)
+    return t.item()
+
+
 def make_comm(hs, ctx, rank, world):
     """The library's own NCCL communicator (hs_comm_init): rank 0's unique id
     is broadcast over the torch.distributed process group."""
-    if world == 1:
+    if world == 1 or GLOO_TEST:
         return None
     import torch
     import torch.distributed as dist_
@@ -200,9 +221,15 @@ def run_ours(args):
     import torch.distributed as dist_
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
+    if GLOO_TEST:
+        local = local % torch.cuda.device_count()
+        args.no_graph = True  # the host-staged exchange cannot be captured in a graph
     torch.cuda.set_device(local)
     if world > 1:
-        dist_.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if GLOO_TEST:
+            dist_.init_process_group("gloo")
+        else:
+            dist_.init_process_group("nccl", device_id=torch.device("cuda", local))
     S = build_setup(args.workload, rank, world, local)
     hs, ctx, K, B, tab = S["hs"], S["ctx"], S["K"], S["B"], S["tab"]
     NK = len(hs._lib.KPROF_CLASSES)
@@ -218,7 +245,15 @@ def run_ours(args):
     # every rank must agree, so a failure on any rank falls back everywhere
     aux_split = 1 if (world > 1 and args.aux_split == "on") else 0
 
+    ex = None
+    if GLOO_TEST and world > 1:
+        from paper_2410_11184_b200 import dist as hdist
+        ex = hdist.gloo_device_exchange()
+
     def step(inputs):
+        if ex is not None:
+            return hs.softmax_many_ctxt(K, inputs, S["n"], S["m"], S["k"], wl["variant"], tab["exp"], tab["inv"],
+                                        world=world, rank=rank, exchange=ex, bts=B, aux_split=aux_split)
         return hs.softmax_many_ctxt(K, inputs, S["n"], S["m"], S["k"], wl["variant"], tab["exp"], tab["inv"],
                                     bts=B, comm=comm, aux_split=aux_split)
 
@@ -237,9 +272,7 @@ def run_ours(args):
             print(f"aux_split plan failed ({e}); falling back", file=sys.stderr)
             ok = 0
         if world > 1:
-            t = torch.tensor([ok], device="cuda")
-            dist_.all_reduce(t, op=dist_.ReduceOp.MIN)
-            ok = int(t.item())
+            ok = int(_reduce(ok, dist_.ReduceOp.MIN))
         if not ok:
             plan, aux_split = None, 0
             plan = make_plan()
@@ -319,9 +352,7 @@ def run_ours(args):
             hs._lib.hs_kprof_collect(ctx.ptr, kp, NK)
         hs._lib.hs_kprof_enable(ctx.ptr, 0)
     if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist_.all_reduce(t, op=dist_.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = float(_reduce(ms, dist_.ReduceOp.MAX))
     ms_step = ms / args.steps
     softmax_per_step = S["L"]  # L = 8192 Softmax per step (all ranks together)
     value = ms_step / softmax_per_step
@@ -397,6 +428,8 @@ def run_ours(args):
                    "launch": "CUDA graph replay (hs_softmax_plan)" if use_graph else "eager C-ABI call",
                    "kprof": ("events captured in a second graph of the same step, timed separately"
                              if use_graph and args.kprof != "off" else args.kprof)},
+        "test_mode": ("HS_BENCH_GLOO: gloo ranks sharing one GPU, host-staged exchange -- not a measurement"
+                      if GLOO_TEST else None),
         "accuracy_bits": round(acc_bits, 2) if acc_bits is not None else None,
         "accuracy": acc_stats,
         "gpu_launches": int(led1["kernels"] - led0["kernels"]),
@@ -517,9 +550,7 @@ def run_e2e_pipelined(S, plan, args, world, make_plan2):
     ms = e0.elapsed_time(e1) / steps
     if world > 1:
         import torch.distributed as dist_
-        t = torch.tensor([ms], device="cuda")
-        dist_.all_reduce(t, op=dist_.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = float(_reduce(ms, dist_.ReduceOp.MAX))
     # the pipelined outputs are the plan's words
     for b in range(2):
         for c, t in zip(plans[b].outputs[:2], pinned_out[b][:2]):
@@ -574,9 +605,7 @@ def run_e2e(S, step, plan, args, world):
     ms = e0.elapsed_time(e1) / steps
     if world > 1:
         import torch.distributed as dist_
-        t = torch.tensor([ms], device="cuda")
-        dist_.all_reduce(t, op=dist_.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = float(_reduce(ms, dist_.ReduceOp.MAX))
     h2d = sum(t.numel() * 8 for t in pinned_in)
     d2h = sum(t.numel() * 8 for t in pinned_out)
     return {"value": round(ms / S["L"], 5), "unit": "ms/Softmax", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,

@@ -523,8 +523,10 @@ hs_status hs_kprof_enable(hs_ctx *c, int on);
 hs_status hs_kprof_collect(hs_ctx *c, double *out, int n_classes);
 
 /* ------------------------------------------------------------ ledger (D8) */
+/* HS_LG_NTT counts limb transforms; HS_LG_NTT_FP those of them that ran on
+ * the FP64 butterflies (N = 2^16, primes < 2^43). */
 enum { HS_LG_HMULT, HS_LG_TENSOR, HS_LG_KS, HS_LG_ROT, HS_LG_RESCALE, HS_LG_CMULT, HS_LG_PMULT,
-       HS_LG_LEVELDOWN, HS_LG_BTS, HS_LG_NTT, HS_LG_KERNELS, HS_LG_COUNT };
+       HS_LG_LEVELDOWN, HS_LG_BTS, HS_LG_NTT, HS_LG_KERNELS, HS_LG_NTT_FP, HS_LG_COUNT };
 hs_status hs_ledger_get(hs_ctx *c, int64_t *out, int n);
 hs_status hs_ledger_reset(hs_ctx *c);
 

@@ -29,7 +29,8 @@ STATUS = ["HS_OK", "HS_EINVAL", "HS_ELEVEL", "HS_EKEY", "HS_ESCALE", "HS_EOVERFL
           "HS_ENOMEM", "HS_ECUDA", "HS_ENCCL"]
 OPS = dict(add=0, sub=1, mult=2, tensor=3, relin=4, rescale=5, level_down=6, mult_const=7, add_const=8,
            mult_int=9, rotate=10, conj=11, galois=12)
-LEDGER = ["hmult", "tensor", "ks", "rot", "rescale", "cmult", "pmult", "leveldown", "bts", "ntt", "kernels"]
+LEDGER = ["hmult", "tensor", "ks", "rot", "rescale", "cmult", "pmult", "leveldown", "bts", "ntt", "kernels",
+          "ntt_fp"]
 
 
 class HsError(RuntimeError):

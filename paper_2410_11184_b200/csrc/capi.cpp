@@ -118,7 +118,9 @@ hs_status hs_context_create_ex(const hs_params *p, int device, const hs_allocato
     alloc_hook_set(c->alloc);
     const int np = p->n_q + p->n_p;
     const size_t N = p->n;
-    std::vector<u64> h((size_t)np * 4 * N + 2 * np);
+    // [np][4][N] integer twiddles, [np](N^-1, Shoup), then [np][2][N] the
+    // twiddles as doubles for the FP64 NTT path (primes < 2^43, kernels.cu)
+    std::vector<u64> h((size_t)np * 4 * N + 2 * np + (size_t)np * 2 * N);
     // device layout per prime: (w, w') pairs of the forward table, then of the
     // inverse table -- one 16-byte load per butterfly
     for (int i = 0; i < np; i++)
@@ -131,6 +133,14 @@ hs_status hs_context_create_ex(const hs_params *p, int device, const hs_allocato
         h[(size_t)np * 4 * N + 2 * i] = p->n_inv[i];
         h[(size_t)np * 4 * N + 2 * i + 1] = p->n_inv_sh[i];
     }
+    const size_t foff = (size_t)np * 4 * N + 2 * np;
+    for (int i = 0; i < np; i++)
+        if (p->prime[i] < (1ull << 43))
+            for (int half = 0; half < 2; half++)
+                for (size_t k = 0; k < N; k++) {
+                    const double w = (double)p->tw[i][half * 2 * N + k];  // exact: w < 2^43
+                    memcpy(&h[foff + (size_t)i * 2 * N + half * N + k], &w, 8);
+                }
     c->T.tw = (decltype(c->T.tw))dev_alloc_persist(h.size() * 8);
     HS_CUDA(cudaMemcpy(c->T.tw, h.data(), h.size() * 8, cudaMemcpyHostToDevice));
     // keep freed stream-ordered memory in the pool (no release back to the OS)

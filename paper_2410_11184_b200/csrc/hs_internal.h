@@ -246,6 +246,7 @@ void k_ks_inner(hs_ctx *c, const u64 *d, const u64 *ext, const u64 *key, u64 *ac
 void k_moddown_final(hs_ctx *c, const u64 *acc, const u64 *conv, u64 *o0, u64 *o1, const u64 *add0,
                      const u64 *add1, int level, cudaStream_t st);
 void upload_prime_constants(const hs_params *P);
+bool ntt_fp_enabled();  // FP64 NTT path for primes < 2^43 (HS_NTT_FP=0: off)
 bool k_ntt_rescale(hs_ctx *c, const u64 *last, u64 *w, const u64 *a, u64 *o, int rows, int l, cudaStream_t st,
                    const u64 *scal = nullptr, size_t a_row = 0);
 bool k_ntt_moddown(hs_ctx *c, u64 *conv, const u64 *acc, size_t acc_row, u64 *o, size_t o_stride, const u64 *add,

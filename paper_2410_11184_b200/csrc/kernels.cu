@@ -15,10 +15,25 @@
 #include "hs_internal.h"
 
 __constant__ PrimeK c_pk[HS_MAXP];
+// FP64 NTT path (ntt16, primes < 2^43): word offset of the double twiddle
+// table inside the context's table allocation, and the switch (HS_NTT_FP=0 off)
+__constant__ unsigned long long c_twf_off;
+__constant__ int c_ntt_fp;
 
 void upload_prime_constants(const hs_params *P)
 {
     HS_CUDA(cudaMemcpyToSymbol(c_pk, P->pk.data(), sizeof(PrimeK) * P->pk.size()));
+    const int np = P->n_q + P->n_p;
+    const unsigned long long off = (unsigned long long)np * 4 * P->n + 2ull * np;
+    HS_CUDA(cudaMemcpyToSymbol(c_twf_off, &off, sizeof(off)));
+    const int on = ntt_fp_enabled() ? 1 : 0;
+    HS_CUDA(cudaMemcpyToSymbol(c_ntt_fp, &on, sizeof(on)));
+}
+
+bool ntt_fp_enabled()
+{
+    static const bool on = !getenv("HS_NTT_FP") || atoi(getenv("HS_NTT_FP")) != 0;
+    return on;
 }
 
 // ------------------------------------------------------------------ modular helpers
@@ -285,8 +300,66 @@ __device__ __forceinline__ u64 reduce4(u64 v, const Tw &T)
     return v >= T.q ? v - T.q : v;
 }
 
+// FP64 butterflies for primes 2^36 < q < 2^43 (the P16 user levels).  B200's
+// FP64 pipe is separate from the integer multiply pipe and, for these primes,
+// exact: values are integers < 2^46 held in doubles; hi + lo = b w exactly
+// (FMA); qe = round(hi / q) by the 1.5 2^52 trick (|hi/q| < 2^46, off by a
+// few 2^-6 at most); t = hi - qe q is exact (|t| < 0.6 q, FMA), r = t + lo is
+// exact and lies in (-q, q) (|lo| <= 2^34 < q / 4), so one correction gives
+// the canonical residue.  Same words as the integer path
+// (tools/bfly_lab.cu: 1.16 vs 0.85 T butterflies/s at q = 2^42).
+struct TwF {
+    const double *__restrict__ w;  // twiddles as doubles (exact)
+    double q, q2, qinv;
+};
+__device__ __forceinline__ double f_mulmod(double b, double w, const TwF &T)
+{
+    const double M = 6755399441055744.0;  // 1.5 * 2^52
+    const double hi = b * w;
+    const double lo = fma(b, w, -hi);
+    const double qe = fma(hi, T.qinv, M) - M;
+    const double r = fma(-qe, T.q, hi) + lo;
+    return r < 0.0 ? r + T.q : r;
+}
+__device__ __forceinline__ void bfly_ct(double &a, double &b, const TwF &T, int idx)
+{
+    const double W = __ldg(T.w + idx);
+    const double X = a >= T.q2 ? a - T.q2 : a;
+    const double V = f_mulmod(b, W, T);
+    a = X + V;
+    b = (X + T.q2) - V;
+}
+__device__ __forceinline__ void bfly_gs(double &a, double &b, const TwF &T, int idx)
+{
+    const double W = __ldg(T.w + idx);
+    const double U = a, V = b, s = U + V;
+    a = s >= T.q2 ? s - T.q2 : s;
+    b = f_mulmod((U + T.q2) - V, W, T);
+}
+__device__ __forceinline__ u64 reduce4(double v, const TwF &T)
+{
+    v = v >= T.q2 ? v - T.q2 : v;
+    return (u64)(v >= T.q ? v - T.q : v);
+}
+// word <-> working value
+__device__ __forceinline__ void to_v(u64 &d, u64 x) { d = x; }
+__device__ __forceinline__ void to_v(double &d, u64 x) { d = (double)x; }
+// inverse output: canonical x N^-1
+struct NiI {
+    u64 ni, nis;
+};
+struct NiF {
+    double ni;
+};
+__device__ __forceinline__ u64 scale_out(u64 x, const NiI &n, const Tw &T) { return d_shoup(x, n.ni, n.nis, T.q); }
+__device__ __forceinline__ u64 scale_out(double x, const NiF &n, const TwF &T) { return (u64)f_mulmod(x, n.ni, T); }
+// inverse values in [0, 2q) -> u64 (stored between the passes)
+__device__ __forceinline__ u64 to_word(u64 x) { return x; }
+__device__ __forceinline__ u64 to_word(double x) { return (u64)x; }
+
 // x[k] = element j0 + k s (j0 = block start + offset, block start multiple of 8s)
-__device__ __forceinline__ void radix8_fwd(u64 x[8], int j0, int s, const Tw &T)
+template <class V, class TW>
+__device__ __forceinline__ void radix8_fwd(V x[8], int j0, int s, const TW &T)
 {
     int m = N / (8 * s), g = j0 / (8 * s);
     for (int k = 0; k < 4; k++) bfly_ct(x[k], x[k + 4], T, m + g);
@@ -300,7 +373,8 @@ __device__ __forceinline__ void radix8_fwd(u64 x[8], int j0, int s, const Tw &T)
     g <<= 1;
     for (int k = 0; k < 4; k++) bfly_ct(x[2 * k], x[2 * k + 1], T, m + g + k);
 }
-__device__ __forceinline__ void radix8_inv(u64 x[8], int j0, int s, const Tw &T)
+template <class V, class TW>
+__device__ __forceinline__ void radix8_inv(V x[8], int j0, int s, const TW &T)
 {
     int m = N / (2 * s), g = j0 / (2 * s);
     for (int k = 0; k < 4; k++) bfly_gs(x[2 * k], x[2 * k + 1], T, m + g + k);
@@ -315,7 +389,8 @@ __device__ __forceinline__ void radix8_inv(u64 x[8], int j0, int s, const Tw &T)
     for (int k = 0; k < 4; k++) bfly_gs(x[k], x[k + 4], T, m + g);
 }
 // x[k] = element j0 + k s, block start multiple of 4s
-__device__ __forceinline__ void radix4_fwd(u64 x[4], int j0, int s, const Tw &T)
+template <class V, class TW>
+__device__ __forceinline__ void radix4_fwd(V x[4], int j0, int s, const TW &T)
 {
     int m = N / (4 * s), g = j0 / (4 * s);
     bfly_ct(x[0], x[2], T, m + g);
@@ -325,7 +400,8 @@ __device__ __forceinline__ void radix4_fwd(u64 x[4], int j0, int s, const Tw &T)
     bfly_ct(x[0], x[1], T, m + g);
     bfly_ct(x[2], x[3], T, m + g + 1);
 }
-__device__ __forceinline__ void radix4_inv(u64 x[4], int j0, int s, const Tw &T)
+template <class V, class TW>
+__device__ __forceinline__ void radix4_inv(V x[4], int j0, int s, const TW &T)
 {
     int m = N / (2 * s), g = j0 / (2 * s);
     bfly_gs(x[0], x[1], T, m + g);
@@ -341,6 +417,17 @@ __device__ __forceinline__ Tw twiddles(const u64 *tw, int pi, bool inv)
     const u64 *base = tw + (size_t)pi * 4 * N + (inv ? 2 * N : 0);
     const u64 q = c_pk[pi].q;
     return Tw{reinterpret_cast<const ulonglong2 *>(base), q, 2 * q};
+}
+__device__ __forceinline__ bool fp_prime(int pi)
+{
+    const u64 q = c_pk[pi].q;
+    return c_ntt_fp && q < (1ull << 43) && q > (1ull << 36);
+}
+__device__ __forceinline__ TwF twiddles_f(const u64 *tw, int pi, bool inv)
+{
+    const double *base = reinterpret_cast<const double *>(tw + c_twf_off) + (size_t)pi * 2 * N + (inv ? N : 0);
+    const double q = (double)c_pk[pi].q;
+    return TwF{base, q, 2.0 * q, __ddiv_rn(1.0, q)};
 }
 
 // Fused prologue / epilogue of a FORWARD transform (limb = row * E.l + i):
@@ -368,16 +455,14 @@ struct NttEpi {
 
 // Phase over the high 8 index bits (half-spans 2^15..2^8): C columns x 256 rows
 // per CTA of 32 C threads (thread = column tid % C, row index rid = tid / C).
-template <bool INV, int C, int MODE = 0>
-__global__ void __launch_bounds__(32 * C) cols(u64 *data, PrimeMap pm, const u64 *__restrict__ tw,
-                                               const u64 *__restrict__ ninv, const __grid_constant__ NttEpi E)
+// The body is generic in the working value (u64 with Shoup butterflies, or
+// double with the FP64 butterflies for primes < 2^43): the kernel picks one
+// per limb (uniform per CTA).
+template <bool INV, int C, int MODE, class V, class TW, class NI>
+__device__ __forceinline__ void cols_body(u64 *a, int limb, const TW &T, const NI &ni, V *sm, const NttEpi &E)
 {
-    __shared__ u64 sm[256 * C];
-    const int limb = blockIdx.y, pi = pm.p[limb % pm.n];
-    const Tw T = twiddles(tw, pi, INV);
-    u64 *a = data + (size_t)limb * N;
     const int tid = threadIdx.x, col = tid % C, rid = tid / C, c = blockIdx.x * C + col;
-    u64 x[8];
+    V x[8];
     if (!INV) {
         // round 1: rows r0 + 32k, s = 32 rows
         const int r0 = rid;
@@ -385,7 +470,8 @@ __global__ void __launch_bounds__(32 * C) cols(u64 *data, PrimeMap pm, const u64
             // x = centred(last) mod q_i, last = the row's dropped limb mod q_l
             const int row = limb / E.l;
             const u64 *src = E.last + (size_t)row * N;
-            const u64 ql = c_pk[E.lq].q, half = (ql - 1) / 2, q = T.q, rsh = E.rsh[limb - row * E.l];
+            const u64 ql = c_pk[E.lq].q, half = (ql - 1) / 2, rsh = E.rsh[limb - row * E.l];
+            const u64 q = (u64)T.q;
 #pragma unroll
             for (int k = 0; k < 8; k++) {
                 // |centred v| mod q by a Shoup step with w = 1, sign restored
@@ -394,11 +480,11 @@ __global__ void __launch_bounds__(32 * C) cols(u64 *data, PrimeMap pm, const u64
                 const u64 sv = neg ? ql - v : v;
                 u64 r = sv - __umul64hi(sv, rsh) * q;
                 r = r >= q ? r - q : r;
-                x[k] = (neg && r) ? q - r : r;
+                to_v(x[k], (neg && r) ? q - r : r);
             }
         } else {
 #pragma unroll
-            for (int k = 0; k < 8; k++) x[k] = a[(r0 + 32 * k) * 256 + c];
+            for (int k = 0; k < 8; k++) to_v(x[k], a[(r0 + 32 * k) * 256 + c]);
         }
         radix8_fwd(x, r0 * 256 + c, 32 * 256, T);
 #pragma unroll
@@ -412,25 +498,25 @@ __global__ void __launch_bounds__(32 * C) cols(u64 *data, PrimeMap pm, const u64
 #pragma unroll
         for (int k = 0; k < 8; k++) sm[(b * 32 + sub + 4 * k) * C + col] = x[k];
         __syncthreads();
-        // round 3: rows 4q + k (two groups per thread), s = 1 row
+        // round 3: rows 4q + k (two groups per thread), s = 1 row; the words
+        // between the passes stay in [0, 4q)
 #pragma unroll
         for (int h = 0; h < 2; h++) {
             const int q = rid + 32 * h;
-            u64 y[4];
+            V y[4];
 #pragma unroll
             for (int k = 0; k < 4; k++) y[k] = sm[(4 * q + k) * C + col];
             radix4_fwd(y, 4 * q * 256 + c, 256, T);
 #pragma unroll
-            for (int k = 0; k < 4; k++) a[(4 * q + k) * 256 + c] = y[k];
+            for (int k = 0; k < 4; k++) a[(4 * q + k) * 256 + c] = to_word(y[k]);
         }
     } else {
-        const u64 ni = ninv[2 * pi], nis = ninv[2 * pi + 1];
 #pragma unroll
         for (int h = 0; h < 2; h++) {
             const int q = rid + 32 * h;
-            u64 y[4];
+            V y[4];
 #pragma unroll
-            for (int k = 0; k < 4; k++) y[k] = a[(4 * q + k) * 256 + c];
+            for (int k = 0; k < 4; k++) to_v(y[k], a[(4 * q + k) * 256 + c]);
             radix4_inv(y, 4 * q * 256 + c, 256, T);
 #pragma unroll
             for (int k = 0; k < 4; k++) sm[(4 * q + k) * C + col] = y[k];
@@ -448,28 +534,43 @@ __global__ void __launch_bounds__(32 * C) cols(u64 *data, PrimeMap pm, const u64
         for (int k = 0; k < 8; k++) x[k] = sm[(r0 + 32 * k) * C + col];
         radix8_inv(x, r0 * 256 + c, 32 * 256, T);
 #pragma unroll
-        for (int k = 0; k < 8; k++) a[(r0 + 32 * k) * 256 + c] = d_shoup(x[k], ni, nis, T.q);
+        for (int k = 0; k < 8; k++) a[(r0 + 32 * k) * 256 + c] = scale_out(x[k], ni, T);
+    }
+}
+
+template <bool INV, int C, int MODE = 0>
+__global__ void __launch_bounds__(32 * C) cols(u64 *data, PrimeMap pm, const u64 *__restrict__ tw,
+                                               const u64 *__restrict__ ninv, const __grid_constant__ NttEpi E)
+{
+    __shared__ u64 sm[256 * C];
+    const int limb = blockIdx.y, pi = pm.p[limb % pm.n];
+    u64 *a = data + (size_t)limb * N;
+    if (fp_prime(pi)) {
+        const TwF T = twiddles_f(tw, pi, INV);
+        const NiF ni{INV ? (double)ninv[2 * pi] : 0.0};
+        cols_body<INV, C, MODE>(a, limb, T, ni, reinterpret_cast<double *>(sm), E);
+    } else {
+        const Tw T = twiddles(tw, pi, INV);
+        const NiI ni{INV ? ninv[2 * pi] : 0, INV ? ninv[2 * pi + 1] : 0};
+        cols_body<INV, C, MODE>(a, limb, T, ni, sm, E);
     }
 }
 
 // Phase over the low 8 index bits (half-spans 2^7..1): R rows of 256 per CTA of
 // 32 R threads (one warp per row).
-template <bool INV, int R, int MODE = 0>
-__global__ void __launch_bounds__(32 * R) rows(u64 *data, PrimeMap pm, const u64 *__restrict__ tw,
-                                               const __grid_constant__ NttEpi E)
+template <bool INV, int R, int MODE, class V, class TW>
+__device__ __forceinline__ void rows_body(u64 *data, int limb, const TW &T, V *sm, const NttEpi &E)
 {
-    __shared__ u64 sm[R * 256];
-    const int limb = blockIdx.y, pi = pm.p[limb % pm.n];
-    const Tw T = twiddles(tw, pi, INV);
     const int row0 = blockIdx.x * R;
     u64 *a = data + (size_t)limb * N + (size_t)row0 * 256;
     const int tid = threadIdx.x, row = tid >> 5;
     const int jrow = (row0 + row) * 256;
-    u64 x[8];
+    const u64 qw = (u64)T.q;
+    V x[8];
     if (!INV) {
         const int e0 = tid & 31;
 #pragma unroll
-        for (int k = 0; k < 8; k++) x[k] = a[row * 256 + e0 + 32 * k];
+        for (int k = 0; k < 8; k++) to_v(x[k], a[row * 256 + e0 + 32 * k]);
         radix8_fwd(x, jrow + e0, 32, T);
 #pragma unroll
         for (int k = 0; k < 8; k++) sm[row * 256 + e0 + 32 * k] = x[k];
@@ -488,13 +589,14 @@ __global__ void __launch_bounds__(32 * R) rows(u64 *data, PrimeMap pm, const u64
 #pragma unroll
         for (int h = 0; h < 2; h++) {
             const int q = (tid & 31) + 32 * h;
+            V yv[4];
+#pragma unroll
+            for (int k = 0; k < 4; k++) yv[k] = sm[row * 256 + 4 * q + k];
+            radix4_fwd(yv, jrow + 4 * q, 1, T);
+            const int i0 = row * 256 + 4 * q;
             u64 y[4];
 #pragma unroll
-            for (int k = 0; k < 4; k++) y[k] = sm[row * 256 + 4 * q + k];
-            radix4_fwd(y, jrow + 4 * q, 1, T);
-            const int i0 = row * 256 + 4 * q;
-#pragma unroll
-            for (int k = 0; k < 4; k++) y[k] = reduce4(y[k], T);
+            for (int k = 0; k < 4; k++) y[k] = reduce4(yv[k], T);
             if (MODE == 0) {
                 ulonglong2 *dst = reinterpret_cast<ulonglong2 *>(a + i0);
                 dst[0] = make_ulonglong2(y[0], y[1]);
@@ -513,24 +615,24 @@ __global__ void __launch_bounds__(32 * R) rows(u64 *data, PrimeMap pm, const u64
                         const u64 sc = E.scl[li], scs = E.scl_sh[li];
 #pragma unroll
                         for (int k = 0; k < 4; k++)
-                            ov[k] = d_shoup(d_sub(d_shoup(iv[k], sc, scs, T.q), y[k], T.q), inv, ish, T.q);
+                            ov[k] = d_shoup(d_sub(d_shoup(iv[k], sc, scs, qw), y[k], qw), inv, ish, qw);
                     } else {
 #pragma unroll
-                        for (int k = 0; k < 4; k++) ov[k] = d_shoup(d_sub(iv[k], y[k], T.q), inv, ish, T.q);
+                        for (int k = 0; k < 4; k++) ov[k] = d_shoup(d_sub(iv[k], y[k], qw), inv, ish, qw);
                     }
                 } else {
                     const int bb = crow >> 1, comp = crow & 1;
                     const size_t ci = ((size_t)comp * E.l + li) * N + eb + i0;
                     o = E.o + bb * E.ostr + ci;
 #pragma unroll
-                    for (int k = 0; k < 4; k++) ov[k] = d_shoup(d_sub(iv[k], y[k], T.q), inv, ish, T.q);
+                    for (int k = 0; k < 4; k++) ov[k] = d_shoup(d_sub(iv[k], y[k], qw), inv, ish, qw);
                     if (comp < E.add_comps) {
                         const ulonglong2 *ad = reinterpret_cast<const ulonglong2 *>(E.add + bb * E.addstr + ci);
                         const ulonglong2 a0 = ad[0], a1 = ad[1];
-                        ov[0] = d_add(ov[0], a0.x, T.q);
-                        ov[1] = d_add(ov[1], a0.y, T.q);
-                        ov[2] = d_add(ov[2], a1.x, T.q);
-                        ov[3] = d_add(ov[3], a1.y, T.q);
+                        ov[0] = d_add(ov[0], a0.x, qw);
+                        ov[1] = d_add(ov[1], a0.y, qw);
+                        ov[2] = d_add(ov[2], a1.x, qw);
+                        ov[3] = d_add(ov[3], a1.y, qw);
                     }
                 }
                 reinterpret_cast<ulonglong2 *>(o)[0] = make_ulonglong2(ov[0], ov[1]);
@@ -547,7 +649,11 @@ __global__ void __launch_bounds__(32 * R) rows(u64 *data, PrimeMap pm, const u64
             const int q = (tid & 31) + 32 * h;
             const ulonglong2 *src = reinterpret_cast<const ulonglong2 *>(ra + row * 256 + 4 * q);
             const ulonglong2 v0 = src[0], v1 = src[1];
-            u64 y[4] = {v0.x, v0.y, v1.x, v1.y};
+            V y[4];
+            to_v(y[0], v0.x);
+            to_v(y[1], v0.y);
+            to_v(y[2], v1.x);
+            to_v(y[3], v1.y);
             radix4_inv(y, jrow + 4 * q, 1, T);
 #pragma unroll
             for (int k = 0; k < 4; k++) sm[row * 256 + 4 * q + k] = y[k];
@@ -565,8 +671,20 @@ __global__ void __launch_bounds__(32 * R) rows(u64 *data, PrimeMap pm, const u64
         for (int k = 0; k < 8; k++) x[k] = sm[row * 256 + e0 + 32 * k];
         radix8_inv(x, jrow + e0, 32, T);
 #pragma unroll
-        for (int k = 0; k < 8; k++) a[row * 256 + e0 + 32 * k] = x[k];
+        for (int k = 0; k < 8; k++) a[row * 256 + e0 + 32 * k] = to_word(x[k]);
     }
+}
+
+template <bool INV, int R, int MODE = 0>
+__global__ void __launch_bounds__(32 * R) rows(u64 *data, PrimeMap pm, const u64 *__restrict__ tw,
+                                               const __grid_constant__ NttEpi E)
+{
+    __shared__ u64 sm[R * 256];
+    const int limb = blockIdx.y, pi = pm.p[limb % pm.n];
+    if (fp_prime(pi))
+        rows_body<INV, R, MODE>(data, limb, twiddles_f(tw, pi, INV), reinterpret_cast<double *>(sm), E);
+    else
+        rows_body<INV, R, MODE>(data, limb, twiddles(tw, pi, INV), sm, E);
 }
 template <int C, int R>
 void launch(u64 *data, int n_limbs, const PrimeMap &pm, bool inverse, const u64 *tw, const u64 *ninv,
@@ -609,6 +727,23 @@ int tile()
 }
 }  // namespace ntt16
 
+// ledger: limb transforms, and how many of them ran on the FP64 butterflies
+static void lg_ntt(hs_ctx *c, int n_limbs, const PrimeMap &pm, bool n16)
+{
+    c->ledger[HS_LG_NTT] += n_limbs;
+    if (!n16 || !ntt_fp_enabled()) return;
+    int per = 0;
+    for (int i = 0; i < pm.n; i++) {
+        const u64 q = c->P->prime[pm.p[i]];
+        per += q < (1ull << 43) && q > (1ull << 36);
+    }
+    c->ledger[HS_LG_NTT_FP] += (int64_t)(n_limbs / pm.n) * per;
+    for (int i = 0; i < n_limbs % pm.n; i++) {
+        const u64 q = c->P->prime[pm.p[i]];
+        c->ledger[HS_LG_NTT_FP] += q < (1ull << 43) && q > (1ull << 36);
+    }
+}
+
 // Rescale of `rows` rows at level l (C9) around ONE forward transform:
 // w (scratch, rows*l limbs) = NTT(centred(last) mod q_i) with the lift fused
 // into the first pass, o = (a - w) q_l^-1 fused into the second.  last: the
@@ -647,7 +782,7 @@ bool k_ntt_rescale(hs_ctx *c, const u64 *last, u64 *w, const u64 *a, u64 *o, int
     ntt16::cols<false, 4, 1><<<dim3(64, n_limbs), 128, 0, st>>>(w, pm, c->T.tw, ninv, E);
     ntt16::rows<false, 4, 1><<<dim3(64, n_limbs), 128, 0, st>>>(w, pm, c->T.tw, E);
     HS_CHECK_LAUNCH();
-    c->ledger[HS_LG_NTT] += n_limbs;
+    lg_ntt(c, n_limbs, pm, true);
     count_kernel(c, 2);
     return true;
 }
@@ -683,7 +818,7 @@ bool k_ntt_moddown(hs_ctx *c, u64 *conv, const u64 *acc, size_t acc_row, u64 *o,
     ntt16::cols<false, 4, 0><<<dim3(64, n_limbs), 128, 0, st>>>(conv, pm, c->T.tw, ninv, E);
     ntt16::rows<false, 4, 2><<<dim3(64, n_limbs), 128, 0, st>>>(conv, pm, c->T.tw, E);
     HS_CHECK_LAUNCH();
-    c->ledger[HS_LG_NTT] += n_limbs;
+    lg_ntt(c, n_limbs, pm, true);
     count_kernel(c, 2);
     return true;
 }
@@ -701,7 +836,7 @@ void k_ntt(hs_ctx *c, u64 *data, int n_limbs, const PrimeMap &pm, bool inverse, 
         default: ntt16::launch<16, 16>(data, n_limbs, pm, inverse, c->T.tw, ninv, st); break;
         }
         HS_CHECK_LAUNCH();
-        c->ledger[HS_LG_NTT] += n_limbs;
+        lg_ntt(c, n_limbs, pm, true);
         count_kernel(c, 2);
         return;
     }
@@ -723,7 +858,7 @@ void k_ntt(hs_ctx *c, u64 *data, int n_limbs, const PrimeMap &pm, bool inverse, 
         ntt_cols_kernel<true><<<gc, 256, smc, st>>>(data, pm, c->T.tw, g, C, ninv);
     }
     HS_CHECK_LAUNCH();
-    c->ledger[HS_LG_NTT] += n_limbs;
+    lg_ntt(c, n_limbs, pm, false);
     count_kernel(c, 2);
 }
 
@@ -745,7 +880,7 @@ void k_ntt_inv_from(hs_ctx *c, u64 *dst, const u64 *src, size_t sstr, int srows,
     const u64 *ninv = c->T.tw + (size_t)(P->n_q + P->n_p) * 4 * N;
     ntt16::launch_inv_from(dst, src, sstr, srows, n_limbs, pm, c->T.tw, ninv, st);
     HS_CHECK_LAUNCH();
-    c->ledger[HS_LG_NTT] += n_limbs;
+    lg_ntt(c, n_limbs, pm, true);
     count_kernel(c, 2);
 }
 

@@ -142,6 +142,93 @@ __global__ void check(u64 *bad, u64 q, u64 seed)
     }
 }
 
+
+// FP64 butterfly for q < 2^43 (values held as doubles, exact integers < 2^53):
+// hi + lo = b w exactly (FMA), quotient estimate by the magic-number rounding
+// of hi/q (off by at most one), t = hi - qe q exact (FMA), r = t + lo in
+// (-q, 2q), one correction to [0, 2q).  Everything runs on the FP64 pipe
+// except the selects.
+__device__ __forceinline__ double fmodmul(double b, double w, double qd, double qinv)
+{
+    const double M = 6755399441055744.0;  // 1.5 * 2^52
+    const double hi = b * w;
+    const double lo = fma(b, w, -hi);
+    const double qe = fma(hi, qinv, M) - M;
+    const double t = fma(-qe, qd, hi);
+    const double r = t + lo;
+    return r < 0.0 ? r + qd : r;
+}
+
+template <int ILP, int MODE>  // MODE 0: FP64 only; 1: half the pairs integer, half FP64
+__global__ void bfly_fp(u64 *out, u64 q, u64 w0, u64 ws0, int iters)
+{
+    double x[2 * ILP];
+    u64 y[2 * ILP];
+    const double qd = (double)q, qinv = 1.0 / qd, q2d = 2.0 * qd;
+    for (int i = 0; i < 2 * ILP; i++) {
+        y[i] = (threadIdx.x * 7919ull + i * 104729ull) % q;
+        x[i] = (double)y[i];
+    }
+    const u64 q2 = 2 * q;
+    u64 w = w0 + threadIdx.x, ws = ws0 + threadIdx.x;
+    double wd = (double)(w % q);
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int i = 0; i < ILP; i++) {
+            if (MODE == 1 && (i & 1)) {
+                u64 &a = y[2 * i], &b = y[2 * i + 1];
+                const u64 X = a >= q2 ? a - q2 : a;
+                u64 V = shoup_approx(b, w, ws, 0 - q);
+                V = V >= q2 ? V - q2 : V;
+                a = X + V;
+                b = X + q2 - V;
+            } else {
+                double &a = x[2 * i], &b = x[2 * i + 1];
+                const double X = a >= q2d ? a - q2d : a;
+                const double V = fmodmul(b, wd, qd, qinv);
+                a = X + V;
+                b = (X + q2d) - V;
+            }
+        }
+        w += 2;
+        wd += 2.0;
+    }
+    u64 s = 0;
+    for (int i = 0; i < 2 * ILP; i++) s ^= (u64)x[i] ^ y[i];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+__global__ void check_fp(u64 *bad, u64 q, u64 seed)
+{
+    const double qd = (double)q, qinv = 1.0 / qd;
+    u64 x = seed + threadIdx.x + blockIdx.x * 977ull;
+    for (int i = 0; i < 256; i++) {
+        x = x * 6364136223846793005ull + 1442695040888963407ull;
+        u64 a = x % (4 * q), w = (x >> 7) % q;
+        const double r = fmodmul((double)a, (double)w, qd, qinv);
+        const u64 want = (u64)(((unsigned __int128)a * w) % q);
+        if (!(r >= 0.0 && r < 2.0 * qd) || ((u64)r) % q != want) atomicAdd(bad, 1ull);
+    }
+}
+
+template <int ILP, int MODE>
+void run_fp(const char *name, u64 *out, u64 q, u64 w, u64 ws, int threads, int bpsm)
+{
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int iters = 4096, blocks = 148 * bpsm;
+    bfly_fp<ILP, MODE><<<blocks, threads>>>(out, q, w, ws, 16);
+    cudaEventRecord(e0);
+    bfly_fp<ILP, MODE><<<blocks, threads>>>(out, q, w, ws, iters);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    double bf = (double)blocks * threads * iters * ILP;
+    printf("%-10s ILP%d %4d thr x %d/SM: %.3f T bfly/s\n", name, ILP, threads, bpsm, bf / ms / 1e9);
+}
+
 template <int ILP, int PTX>
 void run(const char *name, u64 *out, u64 q, u64 w, u64 ws, int threads, int bpsm)
 {
@@ -180,5 +267,17 @@ int main()
     run<8, 2>("approx", out, q, w, ws, 256, 4);
     run<4, 0>("compiler", out, q, w, ws, 512, 2);
     run<4, 2>("approx", out, q, w, ws, 512, 2);
+    // FP64 butterflies for a 42-bit prime (the P16 user levels)
+    const u64 q42 = 0x3fffffa0001ull;  // 2^42 - 0x5ffff: any odd modulus < 2^43 for timing
+    const u64 w42 = 123456789ull % q42, ws42 = (u64)(((unsigned __int128)w42 << 64) / q42);
+    cudaMemset(bad, 0, 16);
+    for (u64 qq : {q42, 0x7fffffe0001ull, 0x1fffffc0001ull}) check_fp<<<1024, 256>>>(bad, qq, 999);
+    cudaMemcpy(nb, bad, 16, cudaMemcpyDeviceToHost);
+    printf("fp64 modmul wrong: %llu\n", nb[0]);
+    run<4, 2>("approx42", out, q42, w42, ws42, 256, 4);
+    run_fp<4, 0>("fp64", out, q42, w42, ws42, 256, 4);
+    run_fp<8, 0>("fp64", out, q42, w42, ws42, 256, 4);
+    run_fp<4, 1>("hybrid", out, q42, w42, ws42, 256, 4);
+    run_fp<8, 1>("hybrid", out, q42, w42, ws42, 256, 4);
     return 0;
 }

@@ -12,6 +12,7 @@ COLS = [("grid", "launch__grid_size"), ("us", "gpu__time_duration.sum"),
         ("issue%", "sm__inst_issued.avg.pct_of_peak_sustained_active"),
         ("fmaheavy%", "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed"),
         ("alu%", "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
+        ("fp64%", "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"),
         ("dram%", "dram__bytes_read.sum.pct_of_peak_sustained_elapsed"),
         ("mem_thru%", "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed")]
 

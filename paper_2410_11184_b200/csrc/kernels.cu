@@ -458,8 +458,9 @@ struct NttEpi {
 // The body is generic in the working value (u64 with Shoup butterflies, or
 // double with the FP64 butterflies for primes < 2^43): the kernel picks one
 // per limb (uniform per CTA).
-template <bool INV, int C, int MODE, class V, class TW, class NI>
-__device__ __forceinline__ void cols_body(u64 *a, int limb, const TW &T, const NI &ni, V *sm, const NttEpi &E)
+template <bool INV, int C, int MODE, bool TMA, class V, class TW, class NI>
+__device__ __forceinline__ void cols_body(u64 *a, int limb, const TW &T, const NI &ni, V *sm, u64 *smw,
+                                          const NttEpi &E)
 {
     const int tid = threadIdx.x, col = tid % C, rid = tid / C, c = blockIdx.x * C + col;
     V x[8];
@@ -482,6 +483,9 @@ __device__ __forceinline__ void cols_body(u64 *a, int limb, const TW &T, const N
                 r = r >= q ? r - q : r;
                 to_v(x[k], (neg && r) ? q - r : r);
             }
+        } else if (TMA) {
+#pragma unroll
+            for (int k = 0; k < 8; k++) to_v(x[k], smw[(r0 + 32 * k) * C + col]);
         } else {
 #pragma unroll
             for (int k = 0; k < 8; k++) to_v(x[k], a[(r0 + 32 * k) * 256 + c]);
@@ -508,7 +512,12 @@ __device__ __forceinline__ void cols_body(u64 *a, int limb, const TW &T, const N
             for (int k = 0; k < 4; k++) y[k] = sm[(4 * q + k) * C + col];
             radix4_fwd(y, 4 * q * 256 + c, 256, T);
 #pragma unroll
-            for (int k = 0; k < 4; k++) a[(4 * q + k) * 256 + c] = to_word(y[k]);
+            for (int k = 0; k < 4; k++) {
+                if (TMA)
+                    smw[(4 * q + k) * C + col] = to_word(y[k]);
+                else
+                    a[(4 * q + k) * 256 + c] = to_word(y[k]);
+            }
         }
     } else {
 #pragma unroll
@@ -516,7 +525,7 @@ __device__ __forceinline__ void cols_body(u64 *a, int limb, const TW &T, const N
             const int q = rid + 32 * h;
             V y[4];
 #pragma unroll
-            for (int k = 0; k < 4; k++) to_v(y[k], a[(4 * q + k) * 256 + c]);
+            for (int k = 0; k < 4; k++) to_v(y[k], TMA ? smw[(4 * q + k) * C + col] : a[(4 * q + k) * 256 + c]);
             radix4_inv(y, 4 * q * 256 + c, 256, T);
 #pragma unroll
             for (int k = 0; k < 4; k++) sm[(4 * q + k) * C + col] = y[k];
@@ -534,25 +543,76 @@ __device__ __forceinline__ void cols_body(u64 *a, int limb, const TW &T, const N
         for (int k = 0; k < 8; k++) x[k] = sm[(r0 + 32 * k) * C + col];
         radix8_inv(x, r0 * 256 + c, 32 * 256, T);
 #pragma unroll
-        for (int k = 0; k < 8; k++) a[(r0 + 32 * k) * 256 + c] = scale_out(x[k], ni, T);
+        for (int k = 0; k < 8; k++) {
+            if (TMA)
+                smw[(r0 + 32 * k) * C + col] = scale_out(x[k], ni, T);
+            else
+                a[(r0 + 32 * k) * 256 + c] = scale_out(x[k], ni, T);
+        }
     }
 }
 
-template <bool INV, int C, int MODE = 0>
+// TMA = 1: the CTA's 256 x C tile arrives by one cp.async.bulk.tensor load
+// into shared memory and leaves by one tensor store (tensor map over the
+// limbs as a [256 n_limbs][256] u64 array, box (C, 256)): the strided
+// 32-byte column segments no longer cost L1 wavefronts (the pass was
+// L1-bound).
+template <bool INV, int C, int MODE = 0, bool TMA = false>
 __global__ void __launch_bounds__(32 * C) cols(u64 *data, PrimeMap pm, const u64 *__restrict__ tw,
-                                               const u64 *__restrict__ ninv, const __grid_constant__ NttEpi E)
+                                               const u64 *__restrict__ ninv, const __grid_constant__ NttEpi E,
+                                               const __grid_constant__ CUtensorMap tm)
 {
-    __shared__ u64 sm[256 * C];
+    __shared__ __align__(128) u64 sm[256 * C];
+    __shared__ __align__(8) u64 bar;
     const int limb = blockIdx.y, pi = pm.p[limb % pm.n];
     u64 *a = data + (size_t)limb * N;
+    const unsigned ssm = (unsigned)__cvta_generic_to_shared(sm), sbar = (unsigned)__cvta_generic_to_shared(&bar);
+    const int cx = blockIdx.x * C, cy = limb * 256;
+    if (TMA) {
+        if (threadIdx.x == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbar));
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sbar), "r"(256 * C * 8)
+                         : "memory");
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+                "[%4];" ::"r"(ssm),
+                "l"(reinterpret_cast<uint64_t>(&tm)), "r"(cx), "r"(cy), "r"(sbar)
+                : "memory");
+        }
+        asm volatile(
+            "{\n\t.reg .pred P;\n\t"
+            "NTT_TMA_WAIT_%=:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], 0;\n\t"
+            "@!P bra NTT_TMA_WAIT_%=;\n\t}" ::"r"(sbar)
+            : "memory");
+    }
     if (fp_prime(pi)) {
         const TwF T = twiddles_f(tw, pi, INV);
         const NiF ni{INV ? (double)ninv[2 * pi] : 0.0};
-        cols_body<INV, C, MODE>(a, limb, T, ni, reinterpret_cast<double *>(sm), E);
+        cols_body<INV, C, MODE, TMA>(a, limb, T, ni, reinterpret_cast<double *>(sm), sm, E);
     } else {
         const Tw T = twiddles(tw, pi, INV);
         const NiI ni{INV ? ninv[2 * pi] : 0, INV ? ninv[2 * pi + 1] : 0};
-        cols_body<INV, C, MODE>(a, limb, T, ni, sm, E);
+        cols_body<INV, C, MODE, TMA>(a, limb, T, ni, sm, sm, E);
+    }
+    if (TMA) {
+        // the tile's words are in shared memory: make them visible to the
+        // async proxy, then one thread stores the tile and waits until the
+        // bulk store has read it (the CTA's shared memory must outlive it)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                             reinterpret_cast<uint64_t>(&tm)),
+                         "r"(cx), "r"(cy), "r"(ssm)
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
     }
 }
 
@@ -686,18 +746,51 @@ __global__ void __launch_bounds__(32 * R) rows(u64 *data, PrimeMap pm, const u64
     else
         rows_body<INV, R, MODE>(data, limb, twiddles(tw, pi, INV), sm, E);
 }
+// tensor map of `n_limbs` contiguous limbs as a [256 n_limbs][256] u64 array,
+// box (C, 256): the cols pass's TMA tile.  false (plain loads) when the
+// driver entry point is missing or HS_NTT_TMA=0.
+bool cols_tmap(CUtensorMap *m, const u64 *data, int n_limbs, int C)
+{
+    static const bool on = !getenv("HS_NTT_TMA") || atoi(getenv("HS_NTT_TMA")) != 0;
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    memset(m, 0, sizeof(*m));
+    if (!on || !encode || ((uintptr_t)data & 15)) return false;
+    const cuuint64_t dims[2] = {256, (cuuint64_t)256 * n_limbs};
+    const cuuint64_t strides[1] = {256 * 8};
+    const cuuint32_t box[2] = {(cuuint32_t)C, 256};
+    const cuuint32_t estr[2] = {1, 1};
+    return encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<u64 *>(data), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int C, int R>
 void launch(u64 *data, int n_limbs, const PrimeMap &pm, bool inverse, const u64 *tw, const u64 *ninv,
             cudaStream_t st)
 {
     const dim3 gc(256 / C, n_limbs), gr(256 / R, n_limbs);
     NttEpi E{};
+    CUtensorMap tm;
+    const bool tma = cols_tmap(&tm, data, n_limbs, C);
     if (!inverse) {
-        cols<false, C><<<gc, 32 * C, 0, st>>>(data, pm, tw, ninv, E);
+        if (tma)
+            cols<false, C, 0, true><<<gc, 32 * C, 0, st>>>(data, pm, tw, ninv, E, tm);
+        else
+            cols<false, C><<<gc, 32 * C, 0, st>>>(data, pm, tw, ninv, E, tm);
         rows<false, R><<<gr, 32 * R, 0, st>>>(data, pm, tw, E);
     } else {
         rows<true, R><<<gr, 32 * R, 0, st>>>(data, pm, tw, E);
-        cols<true, C><<<gc, 32 * C, 0, st>>>(data, pm, tw, ninv, E);
+        if (tma)
+            cols<true, C, 0, true><<<gc, 32 * C, 0, st>>>(data, pm, tw, ninv, E, tm);
+        else
+            cols<true, C><<<gc, 32 * C, 0, st>>>(data, pm, tw, ninv, E, tm);
     }
 }
 
@@ -711,7 +804,11 @@ void launch_inv_from(u64 *dst, const u64 *src, size_t sstr, int srows, int n_lim
     E.sstr = sstr;
     E.srows = srows;
     rows<true, 4, 3><<<dim3(64, n_limbs), 128, 0, st>>>(dst, pm, tw, E);
-    cols<true, 4><<<dim3(64, n_limbs), 128, 0, st>>>(dst, pm, tw, ninv, E);
+    CUtensorMap tm;
+    if (cols_tmap(&tm, dst, n_limbs, 4))
+        cols<true, 4, 0, true><<<dim3(64, n_limbs), 128, 0, st>>>(dst, pm, tw, ninv, E, tm);
+    else
+        cols<true, 4><<<dim3(64, n_limbs), 128, 0, st>>>(dst, pm, tw, ninv, E, tm);
 }
 
 // tile width (columns per cols-CTA = rows per rows-CTA); HS_NTT_TILE=4|8|16
@@ -779,7 +876,9 @@ bool k_ntt_rescale(hs_ctx *c, const u64 *last, u64 *w, const u64 *a, u64 *o, int
     }
     const PrimeMap pm = pmap_range(0, l);
     const u64 *ninv = c->T.tw + (size_t)(P->n_q + P->n_p) * 4 * N;
-    ntt16::cols<false, 4, 1><<<dim3(64, n_limbs), 128, 0, st>>>(w, pm, c->T.tw, ninv, E);
+    CUtensorMap tm0;
+    memset(&tm0, 0, sizeof(tm0));
+    ntt16::cols<false, 4, 1><<<dim3(64, n_limbs), 128, 0, st>>>(w, pm, c->T.tw, ninv, E, tm0);
     ntt16::rows<false, 4, 1><<<dim3(64, n_limbs), 128, 0, st>>>(w, pm, c->T.tw, E);
     HS_CHECK_LAUNCH();
     lg_ntt(c, n_limbs, pm, true);
@@ -815,7 +914,11 @@ bool k_ntt_moddown(hs_ctx *c, u64 *conv, const u64 *acc, size_t acc_row, u64 *o,
     }
     const PrimeMap pm = pmap_range(0, nt);
     const u64 *ninv = c->T.tw + (size_t)(P->n_q + P->n_p) * 4 * N;
-    ntt16::cols<false, 4, 0><<<dim3(64, n_limbs), 128, 0, st>>>(conv, pm, c->T.tw, ninv, E);
+    CUtensorMap tm;
+    if (ntt16::cols_tmap(&tm, conv, n_limbs, 4))
+        ntt16::cols<false, 4, 0, true><<<dim3(64, n_limbs), 128, 0, st>>>(conv, pm, c->T.tw, ninv, E, tm);
+    else
+        ntt16::cols<false, 4, 0><<<dim3(64, n_limbs), 128, 0, st>>>(conv, pm, c->T.tw, ninv, E, tm);
     ntt16::rows<false, 4, 2><<<dim3(64, n_limbs), 128, 0, st>>>(conv, pm, c->T.tw, E);
     HS_CHECK_LAUNCH();
     lg_ntt(c, n_limbs, pm, true);

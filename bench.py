@@ -37,10 +37,10 @@ WORKLOAD = "config3"
 # `ncu --set full` capture (profiles/r01_ncu_full_summary.txt); None = not measured
 NTT_ALU_PEAK = 0.86
 # FP64 butterfly ceiling for primes < 2^43 (registers only, tools/bfly_lab.cu
-# on the B200: 1.16 T butterflies/s vs 0.85 for the integer butterfly); the
-# NTT peak is the harmonic blend of the two by the step's share of limb
-# transforms on each path (ledger ntt_fp / ntt)
-NTT_FP64_PEAK = 1.16
+# on the B200: the signed butterfly of the kernels 1.81 T butterflies/s vs
+# 0.85 for the integer butterfly); the NTT peak is the harmonic blend of the
+# two by the step's share of limb transforms on each path (ledger ntt_fp / ntt)
+NTT_FP64_PEAK = 1.81
 # DRAM bytes per forward limb-NTT (cols + rows, MODE 0) in the round's
 # `ncu --set full` capture: (369.2 + 316.9 + 382.1 + 313.2) MB / 704 limbs
 # (profiles/r01_ncu_full_summary.txt) -- 1 read + 1 write per pass, no waste

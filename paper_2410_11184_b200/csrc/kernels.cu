@@ -302,48 +302,62 @@ __device__ __forceinline__ u64 reduce4(u64 v, const Tw &T)
 
 // FP64 butterflies for primes 2^36 < q < 2^43 (the P16 user levels).  B200's
 // FP64 pipe is separate from the integer multiply pipe and, for these primes,
-// exact: values are integers < 2^46 held in doubles; hi + lo = b w exactly
-// (FMA); qe = round(hi / q) by the 1.5 2^52 trick (|hi/q| < 2^46, off by a
-// few 2^-6 at most); t = hi - qe q is exact (|t| < 0.6 q, FMA), r = t + lo is
-// exact and lies in (-q, q) (|lo| <= 2^34 < q / 4), so one correction gives
-// the canonical residue.  Same words as the integer path
-// (tools/bfly_lab.cu: 1.16 vs 0.85 T butterflies/s at q = 2^42).
+// exact: values are SIGNED integers |x| < 2^48 held in doubles; hi + lo = b w
+// exactly (FMA); qe = round(hi / q) by the 1.5 2^52 trick (|hi/q| < 2^51,
+// error below 2^-3); t = hi - qe q is exact (FMA), r = t + lo is exact and
+// |r| < 0.7 q (|lo| <= 2^38).  The forward butterfly keeps signed values
+// (a + V, a - V: growth below q per stage, < 12 q after 16 stages); the
+// inverse one re-centres its sum each stage.  Words between the two passes are
+// the signed values as int64; the outputs are canonical.  Same words as the
+// integer path (tools/bfly_lab.cu: 1.16 vs 0.85 T butterflies/s at q = 2^42
+// for the first, unsigned version).
 struct TwF {
     const double *__restrict__ w;  // twiddles as doubles (exact)
     double q, q2, qinv;
 };
-__device__ __forceinline__ double f_mulmod(double b, double w, const TwF &T)
+// b w mod q as a signed representative in (-q, q)
+__device__ __forceinline__ double f_mulmod_s(double b, double w, const TwF &T)
 {
     const double M = 6755399441055744.0;  // 1.5 * 2^52
     const double hi = b * w;
     const double lo = fma(b, w, -hi);
     const double qe = fma(hi, T.qinv, M) - M;
-    const double r = fma(-qe, T.q, hi) + lo;
+    return fma(-qe, T.q, hi) + lo;
+}
+// canonical b w mod q
+__device__ __forceinline__ double f_mulmod(double b, double w, const TwF &T)
+{
+    const double r = f_mulmod_s(b, w, T);
     return r < 0.0 ? r + T.q : r;
+}
+// x mod q centred: |result| < 0.6 q for |x| < 2^51
+__device__ __forceinline__ double f_red(double x, const TwF &T)
+{
+    const double M = 6755399441055744.0;
+    const double qe = fma(x, T.qinv, M) - M;
+    return fma(-qe, T.q, x);
 }
 __device__ __forceinline__ void bfly_ct(double &a, double &b, const TwF &T, int idx)
 {
-    const double W = __ldg(T.w + idx);
-    const double X = a >= T.q2 ? a - T.q2 : a;
-    const double V = f_mulmod(b, W, T);
-    a = X + V;
-    b = (X + T.q2) - V;
+    const double V = f_mulmod_s(b, __ldg(T.w + idx), T);
+    b = a - V;
+    a = a + V;
 }
 __device__ __forceinline__ void bfly_gs(double &a, double &b, const TwF &T, int idx)
 {
     const double W = __ldg(T.w + idx);
-    const double U = a, V = b, s = U + V;
-    a = s >= T.q2 ? s - T.q2 : s;
-    b = f_mulmod((U + T.q2) - V, W, T);
+    const double U = a, V = b;
+    a = f_red(U + V, T);
+    b = f_mulmod_s(U - V, W, T);
 }
 __device__ __forceinline__ u64 reduce4(double v, const TwF &T)
 {
-    v = v >= T.q2 ? v - T.q2 : v;
-    return (u64)(v >= T.q ? v - T.q : v);
+    const double r = f_red(v, T);
+    return (u64)(r < 0.0 ? r + T.q : r);
 }
 // word <-> working value
 __device__ __forceinline__ void to_v(u64 &d, u64 x) { d = x; }
-__device__ __forceinline__ void to_v(double &d, u64 x) { d = (double)x; }
+__device__ __forceinline__ void to_v(double &d, u64 x) { d = (double)(long long)x; }  // canonical or signed inter-pass word
 // inverse output: canonical x N^-1
 struct NiI {
     u64 ni, nis;
@@ -353,9 +367,10 @@ struct NiF {
 };
 __device__ __forceinline__ u64 scale_out(u64 x, const NiI &n, const Tw &T) { return d_shoup(x, n.ni, n.nis, T.q); }
 __device__ __forceinline__ u64 scale_out(double x, const NiF &n, const TwF &T) { return (u64)f_mulmod(x, n.ni, T); }
-// inverse values in [0, 2q) -> u64 (stored between the passes)
+// values between the passes -> u64 words (integer path: [0, 4q); FP64 path:
+// signed, two's complement)
 __device__ __forceinline__ u64 to_word(u64 x) { return x; }
-__device__ __forceinline__ u64 to_word(double x) { return (u64)x; }
+__device__ __forceinline__ u64 to_word(double x) { return (u64)(long long)x; }  // signed inter-pass word
 
 // x[k] = element j0 + k s (j0 = block start + offset, block start multiple of 8s)
 template <class V, class TW>

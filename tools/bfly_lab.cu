@@ -159,7 +159,24 @@ __device__ __forceinline__ double fmodmul(double b, double w, double qd, double 
     return r < 0.0 ? r + qd : r;
 }
 
-template <int ILP, int MODE>  // MODE 0: FP64 only; 1: half the pairs integer, half FP64
+// signed variant (the kernels' butterfly): V = b w mod q in (-q, q), a +- V,
+// no range corrections inside a pass
+__device__ __forceinline__ double fmodmul_s(double b, double w, double qd, double qinv)
+{
+    const double M = 6755399441055744.0;
+    const double hi = b * w;
+    const double lo = fma(b, w, -hi);
+    const double qe = fma(hi, qinv, M) - M;
+    return fma(-qe, qd, hi) + lo;
+}
+__device__ __forceinline__ double fred(double x, double qd, double qinv)
+{
+    const double M = 6755399441055744.0;
+    const double qe = fma(x, qinv, M) - M;
+    return fma(-qe, qd, x);
+}
+
+template <int ILP, int MODE>  // MODE 0: FP64 only; 1: half the pairs integer, half FP64; 2: signed FP64
 __global__ void bfly_fp(u64 *out, u64 q, u64 w0, u64 ws0, int iters)
 {
     double x[2 * ILP];
@@ -182,6 +199,17 @@ __global__ void bfly_fp(u64 *out, u64 q, u64 w0, u64 ws0, int iters)
                 V = V >= q2 ? V - q2 : V;
                 a = X + V;
                 b = X + q2 - V;
+            } else if (MODE == 2) {
+                // 8 stages of signed butterflies, then a re-centring (the
+                // kernels' per-pass pattern)
+                double &a = x[2 * i], &b = x[2 * i + 1];
+                const double V = fmodmul_s(b, wd, qd, qinv);
+                b = a - V;
+                a = a + V;
+                if ((it & 7) == 7) {
+                    a = fred(a, qd, qinv);
+                    b = fred(b, qd, qinv);
+                }
             } else {
                 double &a = x[2 * i], &b = x[2 * i + 1];
                 const double X = a >= q2d ? a - q2d : a;
@@ -277,6 +305,8 @@ int main()
     run<4, 2>("approx42", out, q42, w42, ws42, 256, 4);
     run_fp<4, 0>("fp64", out, q42, w42, ws42, 256, 4);
     run_fp<8, 0>("fp64", out, q42, w42, ws42, 256, 4);
+    run_fp<4, 2>("fp64-signed", out, q42, w42, ws42, 256, 4);
+    run_fp<8, 2>("fp64-signed", out, q42, w42, ws42, 256, 4);
     run_fp<4, 1>("hybrid", out, q42, w42, ws42, 256, 4);
     run_fp<8, 1>("hybrid", out, q42, w42, ws42, 256, 4);
     return 0;

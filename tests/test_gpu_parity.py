@@ -77,6 +77,41 @@ def test_ntt_parity(preset):
     assert (dev.cpu().numpy().view(np.uint64) == host).all()
 
 
+@pytest.mark.parametrize("pattern", ["max", "alternating", "impulse"])
+def test_ntt_extreme_inputs_p16(pattern):
+    """N = 2^16 transforms on inputs at the edges of the words' range -- every
+    coefficient q - 1, alternating 0 / q - 1, a single q - 1 -- on all P16
+    primes: the signed FP64 butterflies of the 42-bit primes (kernels.cu: no
+    corrections inside a pass, |x| < 12 q) and the lazy integer ones must give
+    the oracle's words, forward and back (C3)."""
+    hs = _hs()
+    pre = W.preset("P16")
+    P, PO = hs.Params.from_preset(pre), O.Params.from_preset(pre)
+    ctx = hs.Context(P, 0)
+    qs = np.array(P.primes, dtype=np.uint64)
+    host = np.zeros((len(qs), P.n), np.uint64)
+    if pattern == "max":
+        host[:] = (qs - 1)[:, None]
+    elif pattern == "alternating":
+        host[:, 1::2] = (qs - 1)[:, None]
+    else:
+        host[:, 12345] = qs - 1
+    dev = torch.from_numpy(host.view(np.int64)).cuda()
+    ctx.ntt(dev.data_ptr(), 0, len(qs), inverse=False)
+    got = dev.cpu().numpy().view(np.uint64)
+    for i in range(len(qs)):
+        assert (got[i] == PO.ntt(i, host[i])).all(), i
+    # the inverse of the (worst-case) spectrum -- all q - 1 -- as well
+    spec = np.repeat((qs - 1)[:, None], P.n, axis=1)
+    dev = torch.from_numpy(spec.copy().view(np.int64)).cuda()
+    ctx.ntt(dev.data_ptr(), 0, len(qs), inverse=True)
+    back = dev.cpu().numpy().view(np.uint64)
+    for i in (0, 1, 13, len(qs) - 1):
+        assert (PO.ntt(i, back[i]) == spec[i]).all(), i
+    ctx.ntt(dev.data_ptr(), 0, len(qs), inverse=False)
+    assert (dev.cpu().numpy().view(np.uint64) == spec).all()
+
+
 def test_keygen_parity(toy):
     assert (toy.K.secret() == toy.KO.secret()).all()
     assert (toy.K.swk(0) == toy.KO.swk(0)).all()

@@ -822,3 +822,23 @@ def test_allocator_hook_failure_is_enomem(tables):
     half = L.Allocator(L.ALLOC_FN(lambda nb, st, u: None), L.FREE_FN(), None)
     out = C.c_void_p()
     assert L.hs_context_create_ex(P.ptr, 0, C.byref(half), C.byref(out)) == 1
+
+
+@pytest.mark.timeout(900)
+def test_alternative_kernel_paths_bit_exact():
+    """The measured-and-selectable kernel variants give
+    the same words: integer-only NTT (HS_NTT_FP=0), direct-load cols pass
+    (HS_NTT_TMA=0), scalar BConv (HS_BCONV_MMA=0), and the TMA key stream of
+    the hoisted inner product (HS_KS_TMA=1).  The switches are read once per
+    process, so each set runs the parity tests in a subprocess."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    runs = [({"HS_NTT_FP": "0", "HS_NTT_TMA": "0", "HS_BCONV_MMA": "0"}, "ntt or p16 or keyswitch or bts_parity"),
+            ({"HS_KS_TMA": "1"}, "rotate_hoisted or bootstrap_parity")]
+    for env, sel in runs:
+        r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                            os.path.join(root, "tests", "test_gpu_parity.py"), "-k", sel, "-m", "gpu"],
+                           cwd=root, env=dict(os.environ, **env), capture_output=True, text=True, timeout=800)
+        assert r.returncode == 0, (env, r.stdout[-2000:], r.stderr[-2000:])

@@ -473,11 +473,22 @@ struct NttEpi {
 // The body is generic in the working value (u64 with Shoup butterflies, or
 // double with the FP64 butterflies for primes < 2^43): the kernel picks one
 // per limb (uniform per CTA).
+// Shared-memory swizzle of the butterfly rounds: element a lives at
+// a ^ ((5 (a >> 4)) & 15).  With 8-byte words the three access patterns of
+// each pass (stride-32 rows, the radix-8 4-groups, the radix-4 quads) all hit
+// 16 distinct 8-byte bank pairs per half warp -- 2 wavefronts per 32 lanes,
+// the minimum -- where the plain layout needed 8 for the last two patterns
+// (ncu: shared-load wavefronts 4x the ideal).  A bijection on every aligned
+// block of 16 (it XORs the low 4 bits with a function of the higher ones).
+__device__ __forceinline__ int swz(int a) { return a ^ ((5 * (a >> 4)) & 15); }
+
 template <bool INV, int C, int MODE, bool TMA, class V, class TW, class NI>
 __device__ __forceinline__ void cols_body(u64 *a, int limb, const TW &T, const NI &ni, V *sm, u64 *smw,
                                           const NttEpi &E)
 {
     const int tid = threadIdx.x, col = tid % C, rid = tid / C, c = blockIdx.x * C + col;
+    // the TMA tile arrives in the plain layout; otherwise the swizzled one
+#define SWC(i) (TMA ? (i) : swz(i))
     V x[8];
     if (!INV) {
         // round 1: rows r0 + 32k, s = 32 rows
@@ -500,22 +511,22 @@ __device__ __forceinline__ void cols_body(u64 *a, int limb, const TW &T, const N
             }
         } else if (TMA) {
 #pragma unroll
-            for (int k = 0; k < 8; k++) to_v(x[k], smw[(r0 + 32 * k) * C + col]);
+            for (int k = 0; k < 8; k++) to_v(x[k], smw[SWC((r0 + 32 * k) * C + col)]);
         } else {
 #pragma unroll
             for (int k = 0; k < 8; k++) to_v(x[k], a[(r0 + 32 * k) * 256 + c]);
         }
         radix8_fwd(x, r0 * 256 + c, 32 * 256, T);
 #pragma unroll
-        for (int k = 0; k < 8; k++) sm[(r0 + 32 * k) * C + col] = x[k];
+        for (int k = 0; k < 8; k++) sm[SWC((r0 + 32 * k) * C + col)] = x[k];
         __syncthreads();
         // round 2: rows b*32 + sub + 4k, s = 4 rows
         const int b = rid >> 2, sub = rid & 3;
 #pragma unroll
-        for (int k = 0; k < 8; k++) x[k] = sm[(b * 32 + sub + 4 * k) * C + col];
+        for (int k = 0; k < 8; k++) x[k] = sm[SWC((b * 32 + sub + 4 * k) * C + col)];
         radix8_fwd(x, (b * 32 + sub) * 256 + c, 4 * 256, T);
 #pragma unroll
-        for (int k = 0; k < 8; k++) sm[(b * 32 + sub + 4 * k) * C + col] = x[k];
+        for (int k = 0; k < 8; k++) sm[SWC((b * 32 + sub + 4 * k) * C + col)] = x[k];
         __syncthreads();
         // round 3: rows 4q + k (two groups per thread), s = 1 row; the words
         // between the passes stay in [0, 4q)
@@ -524,12 +535,12 @@ __device__ __forceinline__ void cols_body(u64 *a, int limb, const TW &T, const N
             const int q = rid + 32 * h;
             V y[4];
 #pragma unroll
-            for (int k = 0; k < 4; k++) y[k] = sm[(4 * q + k) * C + col];
+            for (int k = 0; k < 4; k++) y[k] = sm[SWC((4 * q + k) * C + col)];
             radix4_fwd(y, 4 * q * 256 + c, 256, T);
 #pragma unroll
             for (int k = 0; k < 4; k++) {
                 if (TMA)
-                    smw[(4 * q + k) * C + col] = to_word(y[k]);
+                    smw[SWC((4 * q + k) * C + col)] = to_word(y[k]);
                 else
                     a[(4 * q + k) * 256 + c] = to_word(y[k]);
             }
@@ -540,32 +551,33 @@ __device__ __forceinline__ void cols_body(u64 *a, int limb, const TW &T, const N
             const int q = rid + 32 * h;
             V y[4];
 #pragma unroll
-            for (int k = 0; k < 4; k++) to_v(y[k], TMA ? smw[(4 * q + k) * C + col] : a[(4 * q + k) * 256 + c]);
+            for (int k = 0; k < 4; k++) to_v(y[k], TMA ? smw[SWC((4 * q + k) * C + col)] : a[(4 * q + k) * 256 + c]);
             radix4_inv(y, 4 * q * 256 + c, 256, T);
 #pragma unroll
-            for (int k = 0; k < 4; k++) sm[(4 * q + k) * C + col] = y[k];
+            for (int k = 0; k < 4; k++) sm[SWC((4 * q + k) * C + col)] = y[k];
         }
         __syncthreads();
         const int b = rid >> 2, sub = rid & 3;
 #pragma unroll
-        for (int k = 0; k < 8; k++) x[k] = sm[(b * 32 + sub + 4 * k) * C + col];
+        for (int k = 0; k < 8; k++) x[k] = sm[SWC((b * 32 + sub + 4 * k) * C + col)];
         radix8_inv(x, (b * 32 + sub) * 256 + c, 4 * 256, T);
 #pragma unroll
-        for (int k = 0; k < 8; k++) sm[(b * 32 + sub + 4 * k) * C + col] = x[k];
+        for (int k = 0; k < 8; k++) sm[SWC((b * 32 + sub + 4 * k) * C + col)] = x[k];
         __syncthreads();
         const int r0 = rid;
 #pragma unroll
-        for (int k = 0; k < 8; k++) x[k] = sm[(r0 + 32 * k) * C + col];
+        for (int k = 0; k < 8; k++) x[k] = sm[SWC((r0 + 32 * k) * C + col)];
         radix8_inv(x, r0 * 256 + c, 32 * 256, T);
 #pragma unroll
         for (int k = 0; k < 8; k++) {
             if (TMA)
-                smw[(r0 + 32 * k) * C + col] = scale_out(x[k], ni, T);
+                smw[SWC((r0 + 32 * k) * C + col)] = scale_out(x[k], ni, T);
             else
                 a[(r0 + 32 * k) * 256 + c] = scale_out(x[k], ni, T);
         }
     }
 }
+#undef SWC
 
 // TMA = 1: the CTA's 256 x C tile arrives by one cp.async.bulk.tensor load
 // into shared memory and leaves by one tensor store (tensor map over the
@@ -648,14 +660,14 @@ __device__ __forceinline__ void rows_body(u64 *data, int limb, const TW &T, V *s
         for (int k = 0; k < 8; k++) to_v(x[k], a[row * 256 + e0 + 32 * k]);
         radix8_fwd(x, jrow + e0, 32, T);
 #pragma unroll
-        for (int k = 0; k < 8; k++) sm[row * 256 + e0 + 32 * k] = x[k];
+        for (int k = 0; k < 8; k++) sm[swz(row * 256 + e0 + 32 * k)] = x[k];
         __syncthreads();
         const int b = (tid >> 2) & 7, sub = tid & 3;
 #pragma unroll
-        for (int k = 0; k < 8; k++) x[k] = sm[row * 256 + b * 32 + sub + 4 * k];
+        for (int k = 0; k < 8; k++) x[k] = sm[swz(row * 256 + b * 32 + sub + 4 * k)];
         radix8_fwd(x, jrow + b * 32 + sub, 4, T);
 #pragma unroll
-        for (int k = 0; k < 8; k++) sm[row * 256 + b * 32 + sub + 4 * k] = x[k];
+        for (int k = 0; k < 8; k++) sm[swz(row * 256 + b * 32 + sub + 4 * k)] = x[k];
         __syncthreads();
         // last round: each thread ends with 4 consecutive words, stored
         // straight to global memory as two 16-byte stores (no smem pass)
@@ -666,7 +678,7 @@ __device__ __forceinline__ void rows_body(u64 *data, int limb, const TW &T, V *s
             const int q = (tid & 31) + 32 * h;
             V yv[4];
 #pragma unroll
-            for (int k = 0; k < 4; k++) yv[k] = sm[row * 256 + 4 * q + k];
+            for (int k = 0; k < 4; k++) yv[k] = sm[swz(row * 256 + 4 * q + k)];
             radix4_fwd(yv, jrow + 4 * q, 1, T);
             const int i0 = row * 256 + 4 * q;
             u64 y[4];
@@ -731,19 +743,19 @@ __device__ __forceinline__ void rows_body(u64 *data, int limb, const TW &T, V *s
             to_v(y[3], v1.y);
             radix4_inv(y, jrow + 4 * q, 1, T);
 #pragma unroll
-            for (int k = 0; k < 4; k++) sm[row * 256 + 4 * q + k] = y[k];
+            for (int k = 0; k < 4; k++) sm[swz(row * 256 + 4 * q + k)] = y[k];
         }
         __syncthreads();
         const int b = (tid >> 2) & 7, sub = tid & 3;
 #pragma unroll
-        for (int k = 0; k < 8; k++) x[k] = sm[row * 256 + b * 32 + sub + 4 * k];
+        for (int k = 0; k < 8; k++) x[k] = sm[swz(row * 256 + b * 32 + sub + 4 * k)];
         radix8_inv(x, jrow + b * 32 + sub, 4, T);
 #pragma unroll
-        for (int k = 0; k < 8; k++) sm[row * 256 + b * 32 + sub + 4 * k] = x[k];
+        for (int k = 0; k < 8; k++) sm[swz(row * 256 + b * 32 + sub + 4 * k)] = x[k];
         __syncthreads();
         const int e0 = tid & 31;
 #pragma unroll
-        for (int k = 0; k < 8; k++) x[k] = sm[row * 256 + e0 + 32 * k];
+        for (int k = 0; k < 8; k++) x[k] = sm[swz(row * 256 + e0 + 32 * k)];
         radix8_inv(x, jrow + e0, 32, T);
 #pragma unroll
         for (int k = 0; k < 8; k++) a[row * 256 + e0 + 32 * k] = to_word(x[k]);

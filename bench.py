@@ -402,6 +402,8 @@ def run_ours(args):
             peak = 1.0 / ((1.0 - f_fp) / NTT_ALU_PEAK + f_fp / NTT_FP64_PEAK)
             return {"kernel": "ntt (cols+rows, fwd+inv)", "bound": "alu", "achieved": round(ach, 4),
                     "peak": round(peak, 4), "unit": "T butterflies/s", "frac": round(ach / peak, 4),
+                    # the round-1 denominator (integer butterflies only), for comparison
+                    "frac_vs_integer_peak": round(ach / NTT_ALU_PEAK, 4),
                     "traffic": NTT_TRAFFIC_PER_LIMB and round(NTT_TRAFFIC_PER_LIMB * bytes_per / (16 * 65536)),
                     "peak_source": (f"blend of the integer butterfly {NTT_ALU_PEAK} (derived: 148 SM x 4 SMSP x "
                                     "1.965 GHz / IMAD-pipe cycles per warp-butterfly, SASS mix) and the FP64 "

@@ -375,10 +375,12 @@ static CtP apply(const hs_keys *K, const hs_ct *in, const LinTrans &T, cudaStrea
         DBuf bq((size_t)ng * nl * N, st);
         {
             DBuf z((size_t)ng * np * N, st);
-            k_ntt_inv_from(c, z.p, gin + ((size_t)ntg + nl) * N, W, np, ng * np, pmap_range(P->n_q, np), st);
             const BconvTab &md = bconv_moddown(c, l);
+            const BconvTab *mdt = &md;
+            k_ntt_inv_from(c, z.p, gin + ((size_t)ntg + nl) * N, W, np, ng * np, pmap_range(P->n_q, np), st,
+                           bconv_ninv(c, &mdt, 1, ((long)l << 8) | 251));
             DBuf conv((size_t)ng * nl * N, st);
-            k_bconv(c, md, z.p, N, conv.p, N, ng, (size_t)np * N, (size_t)nl * N, st);
+            k_bconv(c, md, z.p, N, conv.p, N, ng, (size_t)np * N, (size_t)nl * N, st, true);
             const u64 *a1 = gin + (size_t)ntg * N;
             if (!k_ntt_moddown(c, conv.p, a1, W, bq.p, 2 * (size_t)nl * N, nullptr, 0, 0, nl, nullptr, ng, st)) {
                 k_ntt(c, conv.p, ng * nl, pmap_range(0, nl), false, st);

@@ -114,6 +114,7 @@ hs_ctx::~hs_ctx()
         dev_free_persist(kv.second.mma);
     }
     for (auto &kv : galois_perm) dev_free_persist(kv.second);
+    for (auto &kv : bconv_ninv) dev_free_persist(kv.second);
     for (auto &kv : pt_cache) dev_free_persist(kv.second);
     for (auto e : kprof_ev) cudaEventDestroy(e);
     dev_free_persist(T.tw);
@@ -357,6 +358,41 @@ const BconvTab &bconv_moddown_rescale(hs_ctx *c, int level)
     return c->bconv[key] = t;
 }
 
+const u64 *bconv_ninv(hs_ctx *c, const BconvTab *const *tabs, int n_tabs, long key)
+{
+    {
+        std::lock_guard<std::mutex> g(c->mu);
+        auto it = c->bconv_ninv.find(key);
+        if (it != c->bconv_ninv.end()) return it->second;
+    }
+    const hs_params *P = c->P;
+    const int np = P->n_q + P->n_p;
+    std::vector<u64> h(2 * (size_t)np, 0);
+    for (int t = 0; t < n_tabs; t++) {
+        const BconvTab &T = *tabs[t];
+        for (int a = 0; a < T.n_src; a++) {
+            const int pi = T.src[a];
+            const u64 q = P->prime[pi];
+            // qhat_a^-1 as the table holds it, times N^-1
+            u64 qh = 1;
+            for (int b = 0; b < T.n_src; b++)
+                if (b != a) qh = hs_mulmod(qh, P->prime[T.src[b]] % q, q);
+            const u64 v = hs_mulmod(hs_invmod(qh, q), P->n_inv[pi], q);
+            h[2 * pi] = v;
+            h[2 * pi + 1] = hs_shoup_const(v, q);
+        }
+    }
+    u64 *d = (u64 *)dev_alloc_persist(h.size() * 8);
+    HS_CUDA(cudaMemcpy(d, h.data(), h.size() * 8, cudaMemcpyHostToDevice));
+    std::lock_guard<std::mutex> g(c->mu);
+    auto it = c->bconv_ninv.find(key);
+    if (it != c->bconv_ninv.end()) {  // another thread won the race
+        dev_free_persist(d);
+        return it->second;
+    }
+    return c->bconv_ninv[key] = d;
+}
+
 // C10: out[i] = in[perm[i]], perm[i] = brv(((2 brv(i) + 1) k mod 2N - 1) / 2)
 const unsigned *galois_table(hs_ctx *c, int k)
 {
@@ -385,6 +421,17 @@ const unsigned *galois_table(hs_ctx *c, int k)
 // ------------------------------------------------------------------ key switching (C7)
 // ModUp of B polynomials d_b = d + b*d_stride (level+1 limbs, NTT domain):
 // digit j's extension to every target prime but its own, block [B][nd_j][N].
+// the ModUp union of a level's digit tables (every Q prime of the level is
+// a source of exactly one digit)
+static const u64 *modup_ninv(hs_ctx *c, int level)
+{
+    const hs_params *P = c->P;
+    const int nl = level + 1, beta = (nl + P->alpha - 1) / P->alpha;
+    const BconvTab *tabs[HS_MAXDIG];
+    for (int j = 0; j < beta; j++) tabs[j] = &bconv_modup(c, level, j);
+    return bconv_ninv(c, tabs, beta, ((long)level << 8) | 250);
+}
+
 void ks_modup(hs_ctx *c, int level, int B, const u64 *d, size_t d_stride, ModUpBuf &m, cudaStream_t st)
 {
     const hs_params *P = c->P;
@@ -393,7 +440,7 @@ void ks_modup(hs_ctx *c, int level, int B, const u64 *d, size_t d_stride, ModUpB
     m.beta = (nl + alpha - 1) / alpha;
     // coefficient form of every d_b: [B][nl][N]
     DBuf x((size_t)B * nl * N, st);
-    k_ntt_inv_from(c, x.p, d, d_stride, nl, B * nl, pmap_range(0, nl), st);
+    k_ntt_inv_from(c, x.p, d, d_stride, nl, B * nl, pmap_range(0, nl), st, modup_ninv(c, level));
     size_t tot = 0;
     for (int j = 0; j < m.beta; j++) {
         const BconvTab &tab = bconv_modup(c, level, j);
@@ -412,14 +459,14 @@ void ks_modup(hs_ctx *c, int level, int B, const u64 *d, size_t d_stride, ModUpB
             tabs[j] = &bconv_modup(c, level, j);
             for (int i = 0; i < tabs[j]->n_dst; i++) pm.p[pm.n++] = (unsigned char)tabs[j]->dst[i];
         }
-        k_bconv_modup_multi(c, tabs, m.off, m.beta, x.p, m.ext.p, st);
+        k_bconv_modup_multi(c, tabs, m.off, m.beta, x.p, m.ext.p, st, true);
         k_ntt(c, m.ext.p, pm.n, pm, false, st);
         return;
     }
     for (int j = 0; j < m.beta; j++) {
         const BconvTab &tab = bconv_modup(c, level, j);
         u64 *e = m.ext.p + m.off[j];
-        k_bconv(c, tab, x.p + (size_t)tab.src[0] * N, N, e, N, B, (size_t)nl * N, (size_t)tab.n_dst * N, st);
+        k_bconv(c, tab, x.p + (size_t)tab.src[0] * N, N, e, N, B, (size_t)nl * N, (size_t)tab.n_dst * N, st, true);
         PrimeMap pm;
         pm.n = tab.n_dst;
         for (int i = 0; i < tab.n_dst; i++) pm.p[i] = (unsigned char)tab.dst[i];
@@ -436,10 +483,12 @@ void ks_moddown(hs_ctx *c, int level, int B, const u64 *acc, u64 *out, size_t ou
     const size_t N = P->n;
     const int nl = level + 1, np = P->n_p, ntg = nl + np;
     DBuf z((size_t)B * 2 * np * N, st);
-    k_ntt_inv_from(c, z.p, acc + (size_t)nl * N, ntg * N, np, 2 * B * np, pmap_range(P->n_q, np), st);
     const BconvTab &md = bconv_moddown(c, level);
+    const BconvTab *mdt = &md;
+    k_ntt_inv_from(c, z.p, acc + (size_t)nl * N, ntg * N, np, 2 * B * np, pmap_range(P->n_q, np), st,
+                   bconv_ninv(c, &mdt, 1, ((long)level << 8) | 251));
     DBuf conv((size_t)B * 2 * nl * N, st);
-    k_bconv(c, md, z.p, N, conv.p, N, 2 * B, (size_t)np * N, (size_t)nl * N, st);
+    k_bconv(c, md, z.p, N, conv.p, N, 2 * B, (size_t)np * N, (size_t)nl * N, st, true);
     const size_t ar = (size_t)ntg * N;
     if (k_ntt_moddown(c, conv.p, acc, ar, out, out_stride, add, add_stride, add_comps, nl, nullptr, 2 * B, st)) return;
     k_ntt(c, conv.p, 2 * B * nl, pmap_range(0, nl), false, st);
@@ -460,10 +509,12 @@ void ks_moddown_rescale(hs_ctx *c, int level, int B, const u64 *acc, u64 *out, s
     pz.n = ns;
     pz.p[0] = (unsigned char)level;
     for (int k = 0; k < np; k++) pz.p[1 + k] = (unsigned char)(P->n_q + k);
-    k_ntt_inv_from(c, z.p, acc + (size_t)level * N, ntg * N, ns, 2 * B * ns, pz, st);
     const BconvTab &md = bconv_moddown_rescale(c, level);
+    const BconvTab *mdt = &md;
+    k_ntt_inv_from(c, z.p, acc + (size_t)level * N, ntg * N, ns, 2 * B * ns, pz, st,
+                   bconv_ninv(c, &mdt, 1, ((long)level << 8) | 252));
     DBuf conv((size_t)B * 2 * level * N, st);
-    k_bconv(c, md, z.p, N, conv.p, N, 2 * B, (size_t)ns * N, (size_t)level * N, st);
+    k_bconv(c, md, z.p, N, conv.p, N, 2 * B, (size_t)ns * N, (size_t)level * N, st, true);
     std::vector<u64> inv(level);
     for (int i = 0; i < level; i++) {
         const u64 q = P->prime[i];
@@ -502,7 +553,8 @@ void ks_partial(const hs_keys *K, const SwKey *key, int level, const u64 *d, int
     }
     const int lo0 = j0 * alpha, hi1 = std::min(j1 * alpha, nl), cnt = hi1 - lo0;
     DBuf x((size_t)cnt * N, st);
-    k_ntt_inv_from(c, x.p, d + (size_t)lo0 * N, (size_t)cnt * N, cnt, cnt, pmap_range(lo0, cnt), st);
+    k_ntt_inv_from(c, x.p, d + (size_t)lo0 * N, (size_t)cnt * N, cnt, cnt, pmap_range(lo0, cnt), st,
+                   modup_ninv(c, level));
     ModUpBuf m;
     m.beta = j1;
     size_t tot = 0;
@@ -516,7 +568,8 @@ void ks_partial(const hs_keys *K, const SwKey *key, int level, const u64 *d, int
     for (int j = j0; j < j1; j++) {
         const BconvTab &tab = bconv_modup(c, level, j);
         u64 *e = m.ext.p + m.off[j];
-        k_bconv(c, tab, x.p + (size_t)(tab.src[0] - lo0) * N, N, e, N, 1, (size_t)cnt * N, (size_t)tab.n_dst * N, st);
+        k_bconv(c, tab, x.p + (size_t)(tab.src[0] - lo0) * N, N, e, N, 1, (size_t)cnt * N, (size_t)tab.n_dst * N, st,
+                true);
         PrimeMap pm;
         pm.n = tab.n_dst;
         for (int i = 0; i < tab.n_dst; i++) pm.p[i] = (unsigned char)tab.dst[i];

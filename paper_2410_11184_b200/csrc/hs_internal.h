@@ -107,6 +107,7 @@ struct hs_ctx {
     DevTables T;
     std::map<long, BconvTab> bconv;          // key: (level << 8 | digit), digit 255 = ModDown
     std::map<int, unsigned *> galois_perm;   // device permutation tables
+    std::map<long, u64 *> bconv_ninv;        // folded inverse-NTT scales (bconv_ninv)
     std::map<std::pair<u64, long>, u64 *> pt_cache;  // (content hash, level pair) -> NTT plaintext
     std::map<const u64 *, CUtensorMap> key_tmaps;     // TMA tensor maps of switching keys (kernels.cu)
     std::mutex mu;
@@ -223,9 +224,12 @@ struct PrimeMap {               // prime index of limb l = p[l % n]
 };
 PrimeMap pmap_range(int first, int count);
 
-void k_ntt(hs_ctx *c, u64 *data, int n_limbs, const PrimeMap &pm, bool inverse, cudaStream_t st);
+// ninv (optional, inverse only): per-prime (scale, Shoup) pairs replacing N^-1 --
+// the BConv's q-hat^-1 folded into the inverse transform (bconv_ninv)
+void k_ntt(hs_ctx *c, u64 *data, int n_limbs, const PrimeMap &pm, bool inverse, cudaStream_t st,
+           const u64 *ninv = nullptr);
 void k_ntt_inv_from(hs_ctx *c, u64 *dst, const u64 *src, size_t sstr, int srows, int n_limbs, const PrimeMap &pm,
-                    cudaStream_t st);
+                    cudaStream_t st, const u64 *ninv = nullptr);
 void k_add(hs_ctx *c, const u64 *a, const u64 *b, u64 *o, int n_limbs, int period, bool sub, cudaStream_t st);
 void k_neg(hs_ctx *c, const u64 *a, u64 *o, int n_limbs, int period, cudaStream_t st);
 void k_mul_scalar(hs_ctx *c, const u64 *a, u64 *o, const u64 *host_scal, int n_limbs, int period, cudaStream_t st);
@@ -237,10 +241,16 @@ void k_tensor(hs_ctx *c, const u64 *a, const u64 *b, u64 *o, int nl, cudaStream_
 void k_permute(hs_ctx *c, const u64 *a, u64 *o, const unsigned *perm, int n_limbs, cudaStream_t st);
 void k_rescale_prep(hs_ctx *c, const u64 *last, u64 *w, int ncomp, int level, cudaStream_t st);
 void k_rescale_final(hs_ctx *c, const u64 *a, const u64 *w, u64 *o, int ncomp, int level, cudaStream_t st);
+// prescaled: the sources already hold [x_a qhat_a^-1]_{q_a} (inverse NTT with
+// the tables' bconv_ninv), so the conversion skips that first step
 void k_bconv(hs_ctx *c, const BconvTab &tab, const u64 *src, size_t src_stride, u64 *dst, size_t dst_stride,
-             int batch, size_t batch_src_stride, size_t batch_dst_stride, cudaStream_t st);
+             int batch, size_t batch_src_stride, size_t batch_dst_stride, cudaStream_t st, bool prescaled = false);
 void k_bconv_modup_multi(hs_ctx *c, const BconvTab *const *tabs, const size_t *dst_off, int n_dig, const u64 *x,
-                         u64 *o, cudaStream_t st);
+                         u64 *o, cudaStream_t st, bool prescaled = false);
+// [n_q + n_p] (N^-1 qhat_a^-1 mod q_a, Shoup) for the sources of the given
+// tables (other entries 0): the inverse-NTT scale that leaves the BConv input
+// prescaled; cached per (kind, level)
+const u64 *bconv_ninv(hs_ctx *c, const BconvTab *const *tabs, int n_tabs, long key);
 void k_ks_inner(hs_ctx *c, const u64 *d, const u64 *ext, const u64 *key, u64 *acc, int level, int beta,
                 cudaStream_t st);
 void k_moddown_final(hs_ctx *c, const u64 *acc, const u64 *conv, u64 *o0, u64 *o1, const u64 *add0,

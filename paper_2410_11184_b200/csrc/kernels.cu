@@ -953,13 +953,13 @@ bool k_ntt_moddown(hs_ctx *c, u64 *conv, const u64 *acc, size_t acc_row, u64 *o,
     return true;
 }
 
-void k_ntt(hs_ctx *c, u64 *data, int n_limbs, const PrimeMap &pm, bool inverse, cudaStream_t st)
+void k_ntt(hs_ctx *c, u64 *data, int n_limbs, const PrimeMap &pm, bool inverse, cudaStream_t st, const u64 *ninv_o)
 {
     KTimer _kt(c, KID_NTT, (double)n_limbs * c->P->n * 16, st);
     if (n_limbs <= 0) return;
     const hs_params *P = c->P;
     if (P->log_n == 16) {
-        const u64 *ninv = c->T.tw + (size_t)(P->n_q + P->n_p) * 4 * P->n;
+        const u64 *ninv = ninv_o && inverse ? ninv_o : c->T.tw + (size_t)(P->n_q + P->n_p) * 4 * P->n;
         switch (ntt16::tile()) {
         case 4: ntt16::launch<4, 4>(data, n_limbs, pm, inverse, c->T.tw, ninv, st); break;
         case 8: ntt16::launch<8, 8>(data, n_limbs, pm, inverse, c->T.tw, ninv, st); break;
@@ -979,7 +979,7 @@ void k_ntt(hs_ctx *c, u64 *data, int n_limbs, const PrimeMap &pm, bool inverse, 
     const int R = (2048 / N2) > 0 ? (2048 / N2 < N1 ? 2048 / N2 : N1) : 1;
     dim3 gc(N2 / C, n_limbs), gr(N1 / R, n_limbs);
     size_t smc = (size_t)N1 * C * 8, smr = (size_t)R * N2 * 8;
-    const u64 *ninv = c->T.tw + (size_t)(P->n_q + P->n_p) * 4 * P->n;
+    const u64 *ninv = ninv_o && inverse ? ninv_o : c->T.tw + (size_t)(P->n_q + P->n_p) * 4 * P->n;
     if (!inverse) {
         ntt_cols_kernel<false><<<gc, 256, smc, st>>>(data, pm, c->T.tw, g, C, ninv);
         ntt_rows_kernel<false><<<gr, 256, smr, st>>>(data, pm, c->T.tw, g, R);
@@ -995,7 +995,7 @@ void k_ntt(hs_ctx *c, u64 *data, int n_limbs, const PrimeMap &pm, bool inverse, 
 // dst [n_limbs][N] = iNTT of limb t of src + (t / srows) sstr + (t % srows) N
 // (the staging copy of ModUp / ModDown folded into the first pass)
 void k_ntt_inv_from(hs_ctx *c, u64 *dst, const u64 *src, size_t sstr, int srows, int n_limbs, const PrimeMap &pm,
-                    cudaStream_t st)
+                    cudaStream_t st, const u64 *ninv_o)
 {
     if (n_limbs <= 0) return;
     const hs_params *P = c->P;
@@ -1003,11 +1003,11 @@ void k_ntt_inv_from(hs_ctx *c, u64 *dst, const u64 *src, size_t sstr, int srows,
     if (P->log_n != 16) {
         HS_CUDA(cudaMemcpy2DAsync(dst, srows * N * 8, src, sstr * 8, srows * N * 8, n_limbs / srows,
                                   cudaMemcpyDeviceToDevice, st));
-        k_ntt(c, dst, n_limbs, pm, true, st);
+        k_ntt(c, dst, n_limbs, pm, true, st, ninv_o);
         return;
     }
     KTimer _kt(c, KID_NTT, (double)n_limbs * N * 16, st);
-    const u64 *ninv = c->T.tw + (size_t)(P->n_q + P->n_p) * 4 * N;
+    const u64 *ninv = ninv_o ? ninv_o : c->T.tw + (size_t)(P->n_q + P->n_p) * 4 * N;
     ntt16::launch_inv_from(dst, src, sstr, srows, n_limbs, pm, c->T.tw, ninv, st);
     HS_CHECK_LAUNCH();
     lg_ntt(c, n_limbs, pm, true);
@@ -1316,7 +1316,7 @@ void k_rescale_final(hs_ctx *c, const u64 *a, const u64 *w, u64 *o, int ncomp, i
 // ------------------------------------------------------------------ basis conversion (C7)
 // y_a = x_a * inv_a mod src_a;  out_b = sum_a y_a * c_ab mod dst_b
 struct BconvArg {
-    int n_src, n_dst, centred;
+    int n_src, n_dst, centred, prescaled;
     unsigned char src[16], dst[HS_MAXP];
 };
 
@@ -1342,7 +1342,8 @@ __global__ void __launch_bounds__(256) bconv_kernel(const u64 *__restrict__ x, s
 #pragma unroll
     for (int a = 0; a < NS; a++) {
         const PrimeK k = c_pk[A.src[a]];
-        y[a] = d_shoup(x[(size_t)a * xs + t], __ldg(tab + 2 * a), __ldg(tab + 2 * a + 1), k.q);
+        const u64 xa = x[(size_t)a * xs + t];
+        y[a] = A.prescaled ? xa : d_shoup(xa, __ldg(tab + 2 * a), __ldg(tab + 2 * a + 1), k.q);
         if (A.centred) f = __dadd_rn(f, __ddiv_rn(__ull2double_rn(y[a]), __ull2double_rn(k.q)));
     }
     const int neg = A.centred ? (int)floor(__dadd_rn(f, 0.5)) : 0;
@@ -1418,9 +1419,10 @@ __global__ void __launch_bounds__(256) bconv_mma_kernel(const u64 *__restrict__ 
     for (int idx = tid; idx < 8 * BCM_TILE; idx += 256) {
         const int a = idx / BCM_TILE, n = idx % BCM_TILE;
         u64 y = 0;
-        if (a < A.n_src && n_base + n < N)
-            y = d_shoup(x[(size_t)a * xs + n_base + n], __ldg(tab + 2 * a), __ldg(tab + 2 * a + 1),
-                        c_pk[A.src[a]].q);
+        if (a < A.n_src && n_base + n < N) {
+            const u64 xa = x[(size_t)a * xs + n_base + n];
+            y = A.prescaled ? xa : d_shoup(xa, __ldg(tab + 2 * a), __ldg(tab + 2 * a + 1), c_pk[A.src[a]].q);
+        }
         sy[a * BCM_LD + n] = y;
     }
     __syncthreads();
@@ -1491,7 +1493,7 @@ __global__ void __launch_bounds__(256) bconv_mma_kernel(const u64 *__restrict__ 
 // converts x limbs [src0_j, src0_j + n_src_j) to its n_dst_j targets at
 // o + dst_off_j.  Non-centred (ModUp).  Up to 8 sources, unrolled with guards.
 struct BconvMultiArg {
-    int n_dig;
+    int n_dig, prescaled;
     struct Dig {
         const u64 *tab;
         int n_src, n_dst, src0;
@@ -1514,7 +1516,8 @@ __global__ void __launch_bounds__(256) bconv_multi_kernel(const u64 *__restrict_
     for (int a = 0; a < 8; a++)
         if (a < D.n_src) {
             const PrimeK k = c_pk[D.src[a]];
-            y[a] = d_shoup(x[(size_t)(D.src0 + a) * N + t], __ldg(tab + 2 * a), __ldg(tab + 2 * a + 1), k.q);
+            const u64 xa = x[(size_t)(D.src0 + a) * N + t];
+            y[a] = A.prescaled ? xa : d_shoup(xa, __ldg(tab + 2 * a), __ldg(tab + 2 * a + 1), k.q);
         }
     const u64 *cm = tab + 2 * D.n_src;
     for (int b = b0; b < b1; b++) {
@@ -1534,12 +1537,13 @@ __global__ void __launch_bounds__(256) bconv_multi_kernel(const u64 *__restrict_
 }
 
 void k_bconv_modup_multi(hs_ctx *c, const BconvTab *const *tabs, const size_t *dst_off, int n_dig, const u64 *x,
-                         u64 *o, cudaStream_t st)
+                         u64 *o, cudaStream_t st, bool prescaled)
 {
     const int N = c->P->n;
     if (n_dig < 1 || n_dig > 12) throw HsError(HS_EINVAL, "bconv_multi: digit count out of range");
     BconvMultiArg A;
     A.n_dig = n_dig;
+    A.prescaled = prescaled ? 1 : 0;
     double bytes = 0;
     int maxg = 1;
     for (int j = 0; j < n_dig; j++) {
@@ -1562,13 +1566,14 @@ void k_bconv_modup_multi(hs_ctx *c, const BconvTab *const *tabs, const size_t *d
 }
 
 void k_bconv(hs_ctx *c, const BconvTab &tab, const u64 *src, size_t src_stride, u64 *dst, size_t dst_stride,
-             int batch, size_t bss, size_t bds, cudaStream_t st)
+             int batch, size_t bss, size_t bds, cudaStream_t st, bool prescaled)
 {
     KTimer _kt(c, KID_BCONV, (double)batch * (tab.n_src + tab.n_dst) * c->P->n * 8, st);
     BconvArg A;
     A.n_src = tab.n_src;
     A.n_dst = tab.n_dst;
     A.centred = tab.centred ? 1 : 0;
+    A.prescaled = prescaled ? 1 : 0;
     for (int i = 0; i < tab.n_src; i++) A.src[i] = (unsigned char)tab.src[i];
     for (int i = 0; i < tab.n_dst; i++) A.dst[i] = (unsigned char)tab.dst[i];
     if (tab.n_src > 9) throw HsError(HS_EINVAL, "bconv: more than 9 source primes");

@@ -1397,10 +1397,17 @@ __device__ __forceinline__ void mma_u8(int d[4], const uint32_t a[4], uint2 b)
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b.x), "r"(b.y));
 }
 
+// the conversion's sources / targets as seen by one CTA (pointers into the
+// launch's __grid_constant__ argument)
+struct BcView {
+    const unsigned char *src, *dst;
+    int n_src, n_dst, prescaled;
+};
+
 template <bool CENTRED>
-__global__ void __launch_bounds__(256) bconv_mma_kernel(const u64 *__restrict__ x, size_t xs, u64 *__restrict__ o,
-                                                        size_t os, const __grid_constant__ BconvArg A, const u64 *__restrict__ tab,
-                                                        const uint2 *__restrict__ frag, int N, size_t bxs, size_t bos)
+__device__ __forceinline__ void bconv_mma_body(const u64 *__restrict__ x, size_t xs, u64 *__restrict__ o, size_t os,
+                                               const BcView A, const u64 *__restrict__ tab,
+                                               const uint2 *__restrict__ frag, int N)
 {
     __shared__ u64 sy[8 * BCM_LD];
     __shared__ int sneg[BCM_TILE];
@@ -1408,8 +1415,6 @@ __global__ void __launch_bounds__(256) bconv_mma_kernel(const u64 *__restrict__ 
     __shared__ ulonglong2 sk[HS_MAXP];                  // per target: (q, -q^-1 mod 2^64)
     __shared__ u64 spm[CENTRED ? HS_MAXP : 1];
     const int n_base = blockIdx.x * BCM_TILE, tid = threadIdx.x;
-    x += blockIdx.y * bxs;
-    o += blockIdx.y * bos;
     if (tid < A.n_dst) {
         const PrimeK k = c_pk[A.dst[tid]];
         sk[tid] = make_ulonglong2(k.q, k.qinv);
@@ -1489,6 +1494,16 @@ __global__ void __launch_bounds__(256) bconv_mma_kernel(const u64 *__restrict__ 
     }
 }
 
+
+template <bool CENTRED>
+__global__ void __launch_bounds__(256) bconv_mma_kernel(const u64 *__restrict__ x, size_t xs, u64 *__restrict__ o,
+                                                        size_t os, const __grid_constant__ BconvArg A, const u64 *__restrict__ tab,
+                                                        const uint2 *__restrict__ frag, int N, size_t bxs, size_t bos)
+{
+    bconv_mma_body<CENTRED>(x + blockIdx.y * bxs, xs, o + blockIdx.y * bos, os,
+                            BcView{A.src, A.dst, A.n_src, A.n_dst, A.prescaled}, tab, frag, N);
+}
+
 // All ModUp digits of ONE polynomial in one launch (grid.y = digit): digit j
 // converts x limbs [src0_j, src0_j + n_src_j) to its n_dst_j targets at
 // o + dst_off_j.  Non-centred (ModUp).  Up to 8 sources, unrolled with guards.
@@ -1496,6 +1511,7 @@ struct BconvMultiArg {
     int n_dig, prescaled;
     struct Dig {
         const u64 *tab;
+        const uint2 *frag;  // tensor-core fragments (bconv_mma_multi_kernel) or NULL
         int n_src, n_dst, src0;
         size_t dst_off;
         unsigned char src[8], dst[HS_MAXP];
@@ -1536,6 +1552,45 @@ __global__ void __launch_bounds__(256) bconv_multi_kernel(const u64 *__restrict_
     }
 }
 
+// All ModUp digits of one polynomial, tensor-core form where it pays (digits of
+// >= 4 primes; the CTA geometry of bconv_mma_kernel, grid.y = digit); the
+// smaller digits run a plain 128-bit multiply-add loop on the same geometry
+// (thread = coefficient tid % 128, targets tid / 128, tid / 128 + 2, ...).
+__global__ void __launch_bounds__(256) bconv_mma_multi_kernel(const u64 *__restrict__ x, u64 *__restrict__ o,
+                                                              const __grid_constant__ BconvMultiArg A, int N)
+{
+    const BconvMultiArg::Dig &D = A.d[blockIdx.y];
+    if (D.frag && D.n_src >= 4) {
+        bconv_mma_body<false>(x + (size_t)D.src0 * N, N, o + D.dst_off, N,
+                              BcView{D.src, D.dst, D.n_src, D.n_dst, A.prescaled}, D.tab, D.frag, N);
+        return;
+    }
+    const int t = blockIdx.x * BCM_TILE + (threadIdx.x & (BCM_TILE - 1));
+    if (t >= N) return;
+    u64 y[8];
+#pragma unroll
+    for (int a = 0; a < 8; a++)
+        if (a < D.n_src) {
+            const u64 xa = x[(size_t)(D.src0 + a) * N + t];
+            y[a] = A.prescaled ? xa : d_shoup(xa, __ldg(D.tab + 2 * a), __ldg(D.tab + 2 * a + 1), c_pk[D.src[a]].q);
+        }
+    const u64 *cm = D.tab + 2 * D.n_src;
+    for (int b = threadIdx.x / BCM_TILE; b < D.n_dst; b += 2) {
+        const PrimeK k = c_pk[D.dst[b]];
+        u64 hi = 0, lo = 0;
+#pragma unroll
+        for (int a = 0; a < 7; a++)
+            if (a < D.n_src) mac128(hi, lo, y[a], __ldg(cm + 2 * ((size_t)a * D.n_dst + b)));
+        u64 r = d_redc(hi, lo, k);
+        if (D.n_src > 7) {
+            hi = lo = 0;
+            mac128(hi, lo, y[7], __ldg(cm + 2 * ((size_t)7 * D.n_dst + b)));
+            r = d_add(r, d_redc(hi, lo, k), k.q);
+        }
+        o[D.dst_off + (size_t)b * N + t] = r;
+    }
+}
+
 void k_bconv_modup_multi(hs_ctx *c, const BconvTab *const *tabs, const size_t *dst_off, int n_dig, const u64 *x,
                          u64 *o, cudaStream_t st, bool prescaled)
 {
@@ -1550,6 +1605,7 @@ void k_bconv_modup_multi(hs_ctx *c, const BconvTab *const *tabs, const size_t *d
         const BconvTab &t = *tabs[j];
         if (t.n_src > 8 || t.centred) throw HsError(HS_EINVAL, "bconv_multi: ModUp digits of at most 8 primes only");
         A.d[j].tab = t.dev;
+        A.d[j].frag = reinterpret_cast<const uint2 *>(t.mma);
         A.d[j].n_src = t.n_src;
         A.d[j].n_dst = t.n_dst;
         A.d[j].src0 = t.src[0];
@@ -1560,7 +1616,13 @@ void k_bconv_modup_multi(hs_ctx *c, const BconvTab *const *tabs, const size_t *d
         maxg = std::max(maxg, (t.n_dst + BCONV_TG - 1) / BCONV_TG);
     }
     KTimer _kt(c, KID_BCONV, bytes, st);
-    bconv_multi_kernel<<<dim3((N + 255) / 256, n_dig, maxg), 256, 0, st>>>(x, o, A, N);
+    static const bool mma_on = !getenv("HS_BCONV_MMA") || atoi(getenv("HS_BCONV_MMA")) != 0;
+    bool any_mma = false;
+    for (int j = 0; j < n_dig; j++) any_mma = any_mma || (A.d[j].frag && A.d[j].n_src >= 4);
+    if (mma_on && any_mma)
+        bconv_mma_multi_kernel<<<dim3((N + BCM_TILE - 1) / BCM_TILE, n_dig), 256, 0, st>>>(x, o, A, N);
+    else
+        bconv_multi_kernel<<<dim3((N + 255) / 256, n_dig, maxg), 256, 0, st>>>(x, o, A, N);
     HS_CHECK_LAUNCH();
     count_kernel(c);
 }

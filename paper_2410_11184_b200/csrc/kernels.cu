@@ -230,6 +230,12 @@ __global__ void __launch_bounds__(256) ntt_rows_kernel(u64 *data, PrimeMap pm, c
 // twiddle tw[N/(2t) + j/(2t)] (Cooley-Tukey forward, Gentleman-Sande inverse).
 namespace ntt16 {
 constexpr int LOGN = 16, N = 1 << LOGN;
+// CTAs per SM the two passes are compiled for at 4-wide tiles (128 threads:
+// register cap 64; wider tiles scale it down): measured 121.7 ms of NTT per config-3 step vs 124.5 uncapped and
+// 123.0 / 125.8 at 9 / 10 (spills)
+#ifndef NTT_MINB
+#define NTT_MINB 8
+#endif
 
 struct Tw {
     const ulonglong2 *__restrict__ w;  // (twiddle, Shoup companion) pairs
@@ -585,7 +591,7 @@ __device__ __forceinline__ void cols_body(u64 *a, int limb, const TW &T, const N
 // 32-byte column segments no longer cost L1 wavefronts (the pass was
 // L1-bound).
 template <bool INV, int C, int MODE = 0, bool TMA = false>
-__global__ void __launch_bounds__(32 * C) cols(u64 *data, PrimeMap pm, const u64 *__restrict__ tw,
+__global__ void __launch_bounds__(32 * C, NTT_MINB * 4 / C) cols(u64 *data, PrimeMap pm, const u64 *__restrict__ tw,
                                                const u64 *__restrict__ ninv, const __grid_constant__ NttEpi E,
                                                const __grid_constant__ CUtensorMap tm)
 {
@@ -763,7 +769,7 @@ __device__ __forceinline__ void rows_body(u64 *data, int limb, const TW &T, V *s
 }
 
 template <bool INV, int R, int MODE = 0>
-__global__ void __launch_bounds__(32 * R) rows(u64 *data, PrimeMap pm, const u64 *__restrict__ tw,
+__global__ void __launch_bounds__(32 * R, NTT_MINB * 4 / R) rows(u64 *data, PrimeMap pm, const u64 *__restrict__ tw,
                                                const __grid_constant__ NttEpi E)
 {
     __shared__ u64 sm[R * 256];

@@ -2707,8 +2707,14 @@ __global__ void __launch_bounds__(256) bsgs_inner_kernel(const u64 *__restrict__
 // each baby's two words are loaded once and feed every giant's 128-bit
 // accumulators; every 8 babies the accumulators fold through one REDC into a
 // reduced partial sum (8 q^2 < q 2^64 for q < 2^61), so any b1 stays exact.
+// occupancy of the baby-major BSGS sums (HBM-bound): 3 / 4 CTAs per SM for 4 /
+// 2 giants (128 / 78 registers otherwise; the cap costs a few spilled words,
+// L1-resident): 10.3 -> 10.0 ms per config-3 step
+#ifndef BSGS_MINB
+#define BSGS_MINB(G) ((G) >= 4 ? 3 : (G) == 2 ? 4 : 1)
+#endif
 template <int GM>
-__global__ void __launch_bounds__(256) bsgs_inner_bm_kernel(const u64 *__restrict__ pts, u64 *__restrict__ out,
+__global__ void __launch_bounds__(256, BSGS_MINB(GM)) bsgs_inner_bm_kernel(const u64 *__restrict__ pts, u64 *__restrict__ out,
                                                             const __grid_constant__ BsgsArg A, int N, int b1)
 {
     int t = blockIdx.x * blockDim.x + threadIdx.x;

@@ -1502,7 +1502,7 @@ __device__ __forceinline__ void bconv_mma_body(const u64 *__restrict__ x, size_t
 
 
 template <bool CENTRED>
-__global__ void __launch_bounds__(256) bconv_mma_kernel(const u64 *__restrict__ x, size_t xs, u64 *__restrict__ o,
+__global__ void __launch_bounds__(256, 8) bconv_mma_kernel(const u64 *__restrict__ x, size_t xs, u64 *__restrict__ o,
                                                         size_t os, const __grid_constant__ BconvArg A, const u64 *__restrict__ tab,
                                                         const uint2 *__restrict__ frag, int N, size_t bxs, size_t bos)
 {
